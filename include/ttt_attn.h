@@ -1,0 +1,139 @@
+/*
+ * ttt_attn.h — C-ABI of libtttattn.so, the B200 (sm_100a) Training-Time-Test
+ * (TTT) attention library for EAGLE-3 draft training (SpecForge,
+ * arXiv 2603.18567).
+ *
+ * What it computes (the operation the paper defines):
+ *
+ *   TTT step j (0 <= j < TTT_MAX_STEPS) of the unrolled draft layer attends,
+ *   for every query row r of every sequence b and query head h, over the
+ *   concatenated keys/values  K = [K_0; K_1; ...; K_j]  (each L rows):
+ *
+ *     o_r = softmax( q_r K^T * c ) V          restricted to the allowed set
+ *
+ *   - Alg. 1 "TTT Attention"            PAPER.md:139-162 (§2.4)
+ *   - §2.4 equations, c = 1/sqrt(d_k)
+ *   - Alg. 2 "BlockMask Construction"   PAPER.md:289-317 (§4.2.1):
+ *       M_causal = (r >= k) && (k < T_b)                       (k < L)
+ *       M_suffix = (k >= L) && (k mod L < T_b) && ((k - r) mod L == 0)
+ *     i.e. row r sees base keys k <= r with k < T_b, plus — only if r < T_b —
+ *     exactly one "diagonal" key from each step list: K_i[r], i = 1..j.
+ *   - streaming (never materialising the L x (j+1)L logits) and block
+ *     skipping are PAPER.md:323-331 (§4.2.1 "Sparse Tree Attention").
+ *
+ *   Rows r >= T_b (padding) follow Alg. 2 verbatim: they attend to all base
+ *   keys k < T_b and to no step key (reading R4).
+ *
+ * Layouts (all row-major, "BSHD"):
+ *   q, out, dq           [batch][seq_len][num_q_heads][head_dim]
+ *   k_base, v_base,
+ *   k_steps[i], v_steps[i],
+ *   dk_*, dv_*           [batch][seq_len][num_kv_heads][head_dim]
+ *   lse                  [batch][num_q_heads][seq_len]  fp32, natural log,
+ *                        over the full allowed set (diagonal terms included)
+ *   GQA: query head h reads kv head  h / (num_q_heads / num_kv_heads).
+ *
+ * Element types:
+ *   TTT_BF16       q,k,v,out,dq: bf16; lse: fp32; dk/dv outputs: fp32
+ *                  (they are accumulators across the S reverse-order calls).
+ *                  Tensor-core path (tcgen05 + TMEM + TMA).
+ *   TTT_FP32_CHECK every tensor fp32; CUDA-core fp32 path used to check
+ *                  semantics at 1e-5 (SURVEY.md §8b "check mode").
+ *
+ * Ownership / lifetime: every data pointer is caller-owned DEVICE memory;
+ * the pointer arrays k_steps/v_steps/dk_steps/dv_steps and the desc (with
+ * its seq_lens) are HOST memory read during the call only. The library
+ * allocates nothing and keeps no per-call state; all work is enqueued on
+ * `stream` (cudaStream_t passed as void*; NULL = legacy default stream).
+ * Inputs must stay alive until the stream reaches the kernels.
+ *
+ * Errors: return codes only, nothing is thrown or aborted across the ABI.
+ * All argument validation runs before the first launch, so a non-zero
+ * return other than TTT_ERR_CUDA means nothing was enqueued or written.
+ * Asynchronous device faults surface at the caller's next synchronisation.
+ */
+#ifndef TTT_ATTN_H_
+#define TTT_ATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TTT_MAX_STEPS 32    /* step j in [0, TTT_MAX_STEPS); paper max TTT length 17 */
+#define TTT_MAX_BATCH 512   /* seq_lens are passed to the kernels by value */
+
+typedef enum { TTT_BF16 = 0, TTT_FP32_CHECK = 1 } ttt_dtype;
+
+typedef enum {
+  TTT_OK = 0,
+  TTT_ERR_INVALID_ARG = 1,  /* null pointer, non-positive size, Hq % Hkv != 0, bad flags */
+  TTT_ERR_UNSUPPORTED = 2,  /* head_dim not in {64,128}; BF16 mode needs seq_len % 128 == 0 */
+  TTT_ERR_STEP_RANGE = 3,   /* step < 0 or step >= TTT_MAX_STEPS */
+  TTT_ERR_ALIGNMENT = 4,    /* a device pointer not 16-byte aligned */
+  TTT_ERR_DEGENERATE = 5,   /* some seq_lens[b] < 1 (a row with no allowed key) or > seq_len */
+  TTT_ERR_WORKSPACE = 6,    /* workspace too small (see ttt_attn_workspace_size) */
+  TTT_ERR_CUDA = 7          /* a CUDA launch / driver call failed */
+} ttt_status;
+
+typedef struct {
+  int32_t batch;          /* B >= 1, <= TTT_MAX_BATCH */
+  int32_t seq_len;        /* L = padded per-step length (Alg. 2 Q_LEN) */
+  int32_t num_q_heads;    /* Hq */
+  int32_t num_kv_heads;   /* Hkv, Hq % Hkv == 0 */
+  int32_t head_dim;       /* D in {64, 128} */
+  int32_t dtype;          /* ttt_dtype */
+  float softmax_scale;    /* c; 0 => 1/sqrt(head_dim) */
+  const int32_t* seq_lens;/* HOST int32[batch]: T_b, 1 <= T_b <= L (Alg. 2 T); NULL => all T_b = L */
+} ttt_attn_desc;
+
+/* flags for ttt_attn_bwd */
+#define TTT_ACCUMULATE_DKV 1u /* += into dk_base/dv_base/dk_steps/dv_steps instead of overwrite.
+                                 Step j's backward adds its contribution; the S calls of one
+                                 unroll run in reverse order j = S-1..0. */
+
+/* Bytes of device workspace ttt_attn_fwd (is_bwd=0) / ttt_attn_bwd (is_bwd=1)
+ * need for this desc and step. 0 for fwd. Returns 0 on invalid desc. */
+size_t ttt_attn_workspace_size(const ttt_attn_desc* desc, int step, int is_bwd);
+
+/* Forward of TTT step `step` (= j, the number of step-list entries used).
+ *   q        [B][L][Hq][D]                 in
+ *   k_base   [B][L][Hkv][D], v_base        in   (K_0, V_0: "K^train")
+ *   k_steps  HOST array of `step` device ptrs, each [B][L][Hkv][D]  (K_1..K_j, "K^pred")
+ *   v_steps  likewise
+ *   out      [B][L][Hq][D]                 out
+ *   lse      [B][Hq][L] fp32               out  (natural-log logsumexp of c*q.k over the allowed set)
+ * step == 0 is ordinary causal attention with key padding (Alg. 2, suffix term vacuous). */
+int ttt_attn_fwd(const ttt_attn_desc* desc, int step,
+                 const void* q, const void* k_base, const void* v_base,
+                 const void* const* k_steps, const void* const* v_steps,
+                 void* out, float* lse,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Backward of TTT step `step`, recompute-based (no saved probabilities).
+ *   out, lse  from ttt_attn_fwd of the same step; dout = dL/d out (layout of out).
+ *   dq        [B][L][Hq][D]   (bf16 / fp32)  overwritten with this step's dq
+ *   dk_base, dv_base          fp32 [B][L][Hkv][D]  dL/dK_0, dL/dV_0
+ *   dk_steps, dv_steps        HOST arrays of `step` device ptrs, fp32 [B][L][Hkv][D]
+ *   flags     TTT_ACCUMULATE_DKV or 0
+ *   workspace >= ttt_attn_workspace_size(desc, step, 1) bytes of device memory. */
+int ttt_attn_bwd(const ttt_attn_desc* desc, int step,
+                 const void* q, const void* k_base, const void* v_base,
+                 const void* const* k_steps, const void* const* v_steps,
+                 const void* out, const float* lse, const void* dout,
+                 void* dq, float* dk_base, float* dv_base,
+                 float* const* dk_steps, float* const* dv_steps,
+                 unsigned flags, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Static string for a ttt_status code. */
+const char* ttt_attn_strerror(int code);
+
+/* Library version / build info string (arch it was compiled for). */
+const char* ttt_attn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TTT_ATTN_H_ */

@@ -1,0 +1,121 @@
+"""Seeded synthetic inputs shared by tests/, bench.py and the oracle checks.
+
+This module holds NO arithmetic of the method: it only draws random numbers
+and rounds them to the storage dtype, so the oracle and the CUDA path see the
+identical bits. Recipe (SURVEY.md §8d "Value distributions"):
+
+  * q, k, v, dO ~ N(0, 1) drawn in fp32 by ``numpy.random.default_rng(seed)``
+    then rounded to bf16 (round-to-nearest-even) for the BF16 path, kept fp32
+    for the FP32_CHECK path. With c = 1/sqrt(D) the logits are ~N(0, 1).
+  * "peaked" variant: q scaled by 4 before rounding (stresses max-subtraction).
+  * sequence lengths T_b ~ U[L/4, L] (padded conversations),
+    or T_b = L ("full") for throughput runs.
+  * seeds: inputs ``seed``, dO ``seed + 1``, lengths ``seed + 2``.
+  * one unroll of S TTT steps has S-1 step lists K_1..K_{S-1}, V_1..V_{S-1}
+    (step j uses the first j, reading R1) and one q / dO per step
+    (q_j depends on step j-1's output in EAGLE-3).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+
+@dataclass(frozen=True)
+class Shape:
+    batch: int
+    seq_len: int
+    num_q_heads: int
+    num_kv_heads: int
+    head_dim: int
+    ttt_steps: int
+
+    @property
+    def q_shape(self):
+        return (self.batch, self.seq_len, self.num_q_heads, self.head_dim)
+
+    @property
+    def kv_shape(self):
+        return (self.batch, self.seq_len, self.num_kv_heads, self.head_dim)
+
+
+# BASELINE.json "configs" (index order kept).
+CONFIGS = {
+    "tiny": Shape(1, 128, 4, 2, 64, 3),
+    "llama8b": Shape(8, 2048, 32, 8, 128, 7),
+    "qwen235b": Shape(1, 4096, 64, 4, 128, 7),
+    "longctx": Shape(1, 16384, 32, 8, 128, 7),
+    "dp": Shape(8, 4096, 32, 8, 128, 7),  # one micro-batch of the global-batch-64 DP sweep
+}
+
+
+def _normal(rng: np.random.Generator, shape, scale=1.0) -> np.ndarray:
+    x = rng.standard_normal(size=shape, dtype=np.float32)
+    if scale != 1.0:
+        x *= np.float32(scale)
+    return x
+
+
+def to_storage(x: np.ndarray, dtype: torch.dtype) -> torch.Tensor:
+    """fp32 numpy -> torch CPU tensor of the storage dtype (bf16 rounding is RNE)."""
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dtype)
+
+
+def seq_lens(shape: Shape, seed: int, mode: str = "ragged") -> np.ndarray:
+    """T_b per sequence: 'full' -> L; 'ragged' -> U[L/4, L] (seed + 2)."""
+    if mode == "full":
+        return np.full(shape.batch, shape.seq_len, dtype=np.int32)
+    rng = np.random.default_rng(seed + 2)
+    lo = max(1, shape.seq_len // 4)
+    return rng.integers(lo, shape.seq_len + 1, size=shape.batch, dtype=np.int32)
+
+
+@dataclass
+class Case:
+    """Host-side (CPU torch) tensors of one TTT unroll."""
+    shape: Shape
+    dtype: torch.dtype
+    q: list = field(default_factory=list)        # per step j: [B,L,Hq,D]
+    dout: list = field(default_factory=list)     # per step j: [B,L,Hq,D]
+    k_base: torch.Tensor = None                  # [B,L,Hkv,D]
+    v_base: torch.Tensor = None
+    k_steps: list = field(default_factory=list)  # S-1 of [B,L,Hkv,D]
+    v_steps: list = field(default_factory=list)
+    seq_lens: np.ndarray = None                  # int32[B]
+
+
+def make_case(shape: Shape, dtype: torch.dtype = torch.bfloat16, seed: int = 0,
+              lens: str = "ragged", peaked: bool = False, steps=None) -> Case:
+    """Draw one unroll's inputs. ``steps`` limits how many per-step q/dO are drawn."""
+    S = shape.ttt_steps if steps is None else steps
+    rng = np.random.default_rng(seed)
+    c = Case(shape=shape, dtype=dtype)
+    c.k_base = to_storage(_normal(rng, shape.kv_shape), dtype)
+    c.v_base = to_storage(_normal(rng, shape.kv_shape), dtype)
+    for _ in range(max(shape.ttt_steps - 1, 0)):
+        c.k_steps.append(to_storage(_normal(rng, shape.kv_shape), dtype))
+        c.v_steps.append(to_storage(_normal(rng, shape.kv_shape), dtype))
+    qscale = 4.0 if peaked else 1.0
+    for _ in range(S):
+        c.q.append(to_storage(_normal(rng, shape.q_shape, qscale), dtype))
+    rng_do = np.random.default_rng(seed + 1)
+    for _ in range(S):
+        c.dout.append(to_storage(_normal(rng_do, shape.q_shape), dtype))
+    c.seq_lens = seq_lens(shape, seed, lens)
+    return c
+
+
+def sample_rows(shape: Shape, n_per_head: int, seed: int) -> np.ndarray:
+    """Boolean row selector [B, Hq, L] with n_per_head random rows per (b, h),
+    always including rows 0 and L-1 (the ends of the causal range)."""
+    rng = np.random.default_rng(seed + 3)
+    sel = np.zeros((shape.batch, shape.num_q_heads, shape.seq_len), dtype=bool)
+    for b in range(shape.batch):
+        for h in range(shape.num_q_heads):
+            idx = rng.choice(shape.seq_len, size=min(n_per_head, shape.seq_len), replace=False)
+            sel[b, h, idx] = True
+            sel[b, h, 0] = True
+            sel[b, h, shape.seq_len - 1] = True
+    return sel
