@@ -1,0 +1,13 @@
+"""paper_2603_18567_b200 — B200-native (sm_100a) TTT attention for EAGLE-3 draft
+training (SpecForge, arXiv 2603.18567).
+
+The compute lives in libtttattn.so (tcgen05/TMEM/TMA kernels + an fp32 CUDA-core
+check mode) behind the C-ABI of include/ttt_attn.h; this package is its thin
+Python binding (same names) plus the seeded input generator and the
+data-parallel harness. Importing it without the built library raises.
+"""
+from ._lib import (  # noqa: F401
+    TTT_ACCUMULATE_DKV, TTT_BF16, TTT_FP32_CHECK, TTT_MAX_BATCH, TTT_MAX_STEPS, Desc, TTTError,
+    desc_for, make_desc, ttt_attn_bwd, ttt_attn_fwd, ttt_attn_strerror, ttt_attn_version,
+    ttt_attn_workspace_size,
+)

@@ -1,0 +1,144 @@
+"""ctypes binding of libtttattn.so — argument marshalling only.
+
+Every step of the TTT attention runs in the library's CUDA kernels; this file
+turns torch tensors into (device pointer, size) arguments of the C-ABI in
+include/ttt_attn.h and raises on a non-zero status. There is no CPU fallback:
+if the shared library is missing or was not built, import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtttattn.so")
+
+TTT_BF16 = 0
+TTT_FP32_CHECK = 1
+TTT_ACCUMULATE_DKV = 1
+TTT_MAX_STEPS = 32
+TTT_MAX_BATCH = 512
+
+STATUS = {
+    0: "TTT_OK", 1: "TTT_ERR_INVALID_ARG", 2: "TTT_ERR_UNSUPPORTED", 3: "TTT_ERR_STEP_RANGE",
+    4: "TTT_ERR_ALIGNMENT", 5: "TTT_ERR_DEGENERATE", 6: "TTT_ERR_WORKSPACE", 7: "TTT_ERR_CUDA",
+}
+
+
+class TTTError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Desc(ctypes.Structure):
+    _fields_ = [
+        ("batch", ctypes.c_int32), ("seq_len", ctypes.c_int32), ("num_q_heads", ctypes.c_int32),
+        ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("dtype", ctypes.c_int32),
+        ("softmax_scale", ctypes.c_float), ("seq_lens", ctypes.POINTER(ctypes.c_int32)),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} not found: build the CUDA library first (`make` or __graft_entry__.build()); "
+            "there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, sz, i, u = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint
+    pd = ctypes.POINTER(Desc)
+    lib.ttt_attn_workspace_size.argtypes = [pd, i, i]
+    lib.ttt_attn_workspace_size.restype = sz
+    lib.ttt_attn_fwd.argtypes = [pd, i, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.ttt_attn_fwd.restype = i
+    lib.ttt_attn_bwd.argtypes = [pd, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, u, vp, sz, vp]
+    lib.ttt_attn_bwd.restype = i
+    lib.ttt_attn_strerror.argtypes = [i]
+    lib.ttt_attn_strerror.restype = ctypes.c_char_p
+    lib.ttt_attn_version.argtypes = []
+    lib.ttt_attn_version.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = _load()
+
+
+def ttt_attn_strerror(code: int) -> str:
+    return _lib.ttt_attn_strerror(int(code)).decode()
+
+
+def ttt_attn_version() -> str:
+    return _lib.ttt_attn_version().decode()
+
+
+def make_desc(batch: int, seq_len: int, num_q_heads: int, num_kv_heads: int, head_dim: int,
+              dtype: int = TTT_BF16, softmax_scale: float = 0.0,
+              seq_lens: Optional[Sequence[int]] = None) -> Desc:
+    d = Desc()
+    d.batch, d.seq_len, d.num_q_heads, d.num_kv_heads, d.head_dim = (
+        int(batch), int(seq_len), int(num_q_heads), int(num_kv_heads), int(head_dim))
+    d.dtype, d.softmax_scale = int(dtype), float(softmax_scale)
+    if seq_lens is not None:
+        arr = (ctypes.c_int32 * int(batch))(*[int(x) for x in seq_lens])
+        d._seq_lens_keepalive = arr  # keep the host array alive with the desc
+        d.seq_lens = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32))
+    return d
+
+
+def desc_for(q: torch.Tensor, k_base: torch.Tensor, seq_lens=None, softmax_scale: float = 0.0) -> Desc:
+    """Desc from BSHD tensors: q [B,L,Hq,D], k_base [B,L,Hkv,D]."""
+    B, L, Hq, D = q.shape
+    dt = TTT_FP32_CHECK if q.dtype == torch.float32 else TTT_BF16
+    return make_desc(B, L, Hq, k_base.shape[2], D, dt, softmax_scale, seq_lens)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _ptr_list(ts: Sequence[torch.Tensor]):
+    arr = (ctypes.c_void_p * max(len(ts), 1))()
+    for n, t in enumerate(ts):
+        arr[n] = t.data_ptr()
+    return arr
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        if not torch.cuda.is_available():  # validation-only calls on a CPU host
+            return ctypes.c_void_p(0)
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check(code: int):
+    if code != 0:
+        raise TTTError(code, ttt_attn_strerror(code))
+
+
+def ttt_attn_workspace_size(desc: Desc, step: int, is_bwd: bool) -> int:
+    return int(_lib.ttt_attn_workspace_size(ctypes.byref(desc), int(step), int(bool(is_bwd))))
+
+
+def ttt_attn_fwd(desc: Desc, step: int, q, k_base, v_base, k_steps, v_steps, out, lse,
+                 workspace=None, stream=None) -> None:
+    """Enqueue ttt_attn_fwd (include/ttt_attn.h) on `stream` (default: current)."""
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(_lib.ttt_attn_fwd(ctypes.byref(desc), int(step), _ptr(q), _ptr(k_base), _ptr(v_base),
+                             _ptr_list(k_steps[:step]), _ptr_list(v_steps[:step]), _ptr(out), _ptr(lse),
+                             _ptr(workspace), ws_bytes, _stream(stream)))
+
+
+def ttt_attn_bwd(desc: Desc, step: int, q, k_base, v_base, k_steps, v_steps, out, lse, dout,
+                 dq, dk_base, dv_base, dk_steps, dv_steps, flags: int = 0, workspace=None,
+                 stream=None) -> None:
+    """Enqueue ttt_attn_bwd (include/ttt_attn.h) on `stream` (default: current)."""
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(_lib.ttt_attn_bwd(ctypes.byref(desc), int(step), _ptr(q), _ptr(k_base), _ptr(v_base),
+                             _ptr_list(k_steps[:step]), _ptr_list(v_steps[:step]), _ptr(out), _ptr(lse),
+                             _ptr(dout), _ptr(dq), _ptr(dk_base), _ptr(dv_base),
+                             _ptr_list(dk_steps[:step]), _ptr_list(dv_steps[:step]), int(flags),
+                             _ptr(workspace), ws_bytes, _stream(stream)))

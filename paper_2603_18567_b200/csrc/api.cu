@@ -1,0 +1,232 @@
+// api.cu — the C-ABI of libtttattn.so (include/ttt_attn.h): validation, TMA
+// tensor-map encoding, kernel launches. No allocation, no per-call state.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/ttt_attn.h"
+#include "ttt_params.cuh"
+
+namespace tttk {
+cudaError_t launch_zero_f32(float* x, size_t n, cudaStream_t st);
+cudaError_t launch_fwd_check(const Params& p, cudaStream_t st);
+cudaError_t launch_bwd_check(const Params& p, cudaStream_t st);
+cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, cudaStream_t st);
+cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, cudaStream_t st);
+}  // namespace tttk
+
+using namespace tttk;
+
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// BSHD bf16 tensor [B][L][H][D] -> 4-D map (D, H, L, B), box (64, 1, 128, 1), 128B swizzle.
+bool encode_bshd(CUtensorMap* m, const void* ptr, int B, int L, int H, int D) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)L, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)H * D * 2, (cuuint64_t)L * H * D * 2};
+  cuuint32_t box[4] = {64, 1, 128, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int validate_desc(const ttt_attn_desc* d, int step) {
+  if (!d) return TTT_ERR_INVALID_ARG;
+  if (d->batch < 1 || d->batch > TTT_MAX_BATCH || d->seq_len < 1 || d->num_q_heads < 1 || d->num_kv_heads < 1)
+    return TTT_ERR_INVALID_ARG;
+  if (d->num_q_heads % d->num_kv_heads) return TTT_ERR_INVALID_ARG;
+  if (d->dtype != TTT_BF16 && d->dtype != TTT_FP32_CHECK) return TTT_ERR_INVALID_ARG;
+  if (d->head_dim != 64 && d->head_dim != 128) return TTT_ERR_UNSUPPORTED;
+  if (!(d->softmax_scale >= 0.f) || std::isinf(d->softmax_scale)) return TTT_ERR_INVALID_ARG;
+  if (step < 0 || step >= TTT_MAX_STEPS) return TTT_ERR_STEP_RANGE;
+  if (d->dtype == TTT_BF16 && (d->seq_len % kTile)) return TTT_ERR_UNSUPPORTED;
+  if (d->seq_lens) {
+    for (int b = 0; b < d->batch; ++b)
+      if (d->seq_lens[b] < 1 || d->seq_lens[b] > d->seq_len) return TTT_ERR_DEGENERATE;
+  }
+  return TTT_OK;
+}
+
+void fill_common(Params& p, const ttt_attn_desc* d, int step) {
+  std::memset(&p, 0, sizeof(p));
+  p.B = d->batch;
+  p.L = d->seq_len;
+  p.Hq = d->num_q_heads;
+  p.Hkv = d->num_kv_heads;
+  p.D = d->head_dim;
+  p.G = p.Hq / p.Hkv;
+  p.step = step;
+  p.nqt = p.L / kTile;
+  p.scale = d->softmax_scale > 0.f ? d->softmax_scale : 1.0f / std::sqrt((float)p.D);
+  p.scale_log2 = p.scale * 1.4426950408889634f;
+  for (int b = 0; b < p.B; ++b) p.seq_lens[b] = d->seq_lens ? d->seq_lens[b] : p.L;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct BwdWs {
+  size_t delta, lse2, dq_acc, total;
+};
+BwdWs bwd_ws_layout(const ttt_attn_desc* d) {
+  BwdWs w{};
+  const size_t rows = (size_t)d->batch * d->num_q_heads * d->seq_len;
+  w.delta = 0;
+  w.lse2 = align256(rows * 4);
+  w.dq_acc = w.lse2 + align256(rows * 4);
+  w.total = w.dq_acc + align256(rows * (size_t)d->head_dim * 4);
+  return w;
+}
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? TTT_OK : TTT_ERR_CUDA; }
+
+}  // namespace
+
+extern "C" {
+
+const char* ttt_attn_strerror(int code) {
+  switch (code) {
+    case TTT_OK: return "ok";
+    case TTT_ERR_INVALID_ARG: return "invalid argument";
+    case TTT_ERR_UNSUPPORTED: return "unsupported configuration (head_dim must be 64/128; bf16 needs seq_len % 128 == 0)";
+    case TTT_ERR_STEP_RANGE: return "step out of range [0, TTT_MAX_STEPS)";
+    case TTT_ERR_ALIGNMENT: return "device pointer not 16-byte aligned";
+    case TTT_ERR_DEGENERATE: return "degenerate sequence length (need 1 <= seq_lens[b] <= seq_len)";
+    case TTT_ERR_WORKSPACE: return "workspace too small";
+    case TTT_ERR_CUDA: return "CUDA error";
+    default: return "unknown error";
+  }
+}
+
+const char* ttt_attn_version(void) { return "libtttattn 0.1 sm_100a (tcgen05/TMEM/TMA + fp32 check path)"; }
+
+size_t ttt_attn_workspace_size(const ttt_attn_desc* d, int step, int is_bwd) {
+  if (validate_desc(d, step) != TTT_OK) return 0;
+  if (!is_bwd || d->dtype == TTT_FP32_CHECK) return 0;
+  return bwd_ws_layout(d).total;
+}
+
+int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_base, const void* v_base,
+                 const void* const* k_steps, const void* const* v_steps, void* out, float* lse, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  int st = validate_desc(d, step);
+  if (st) return st;
+  if (!q || !k_base || !v_base || !out || !lse) return TTT_ERR_INVALID_ARG;
+  if (step > 0 && (!k_steps || !v_steps)) return TTT_ERR_INVALID_ARG;
+  for (int i = 0; i < step; ++i)
+    if (!k_steps[i] || !v_steps[i]) return TTT_ERR_INVALID_ARG;
+  if (!aligned16(q) || !aligned16(k_base) || !aligned16(v_base) || !aligned16(out) || !aligned16(lse))
+    return TTT_ERR_ALIGNMENT;
+  for (int i = 0; i < step; ++i)
+    if (!aligned16(k_steps[i]) || !aligned16(v_steps[i])) return TTT_ERR_ALIGNMENT;
+  Params p;
+  fill_common(p, d, step);
+  p.q = q;
+  p.k = k_base;
+  p.v = v_base;
+  for (int i = 0; i < step; ++i) {
+    p.ks[i] = k_steps[i];
+    p.vs[i] = v_steps[i];
+  }
+  p.out = out;
+  p.lse = lse;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (d->dtype == TTT_FP32_CHECK) return cuda_status(launch_fwd_check(p, s));
+  FwdMaps maps;
+  if (!encode_bshd(&maps.q, q, p.B, p.L, p.Hq, p.D) || !encode_bshd(&maps.k, k_base, p.B, p.L, p.Hkv, p.D) ||
+      !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D))
+    return TTT_ERR_CUDA;
+  return cuda_status(launch_fwd_sm100(p, maps, s));
+}
+
+int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_base, const void* v_base,
+                 const void* const* k_steps, const void* const* v_steps, const void* out, const float* lse,
+                 const void* dout, void* dq, float* dk_base, float* dv_base, float* const* dk_steps,
+                 float* const* dv_steps, unsigned flags, void* workspace, size_t workspace_bytes, void* stream) {
+  int st = validate_desc(d, step);
+  if (st) return st;
+  if (flags & ~TTT_ACCUMULATE_DKV) return TTT_ERR_INVALID_ARG;
+  if (!q || !k_base || !v_base || !out || !lse || !dout || !dq || !dk_base || !dv_base)
+    return TTT_ERR_INVALID_ARG;
+  if (step > 0 && (!k_steps || !v_steps || !dk_steps || !dv_steps)) return TTT_ERR_INVALID_ARG;
+  for (int i = 0; i < step; ++i)
+    if (!k_steps[i] || !v_steps[i] || !dk_steps[i] || !dv_steps[i]) return TTT_ERR_INVALID_ARG;
+  const void* ptrs[] = {q, k_base, v_base, out, lse, dout, dq, dk_base, dv_base};
+  for (const void* ptr : ptrs)
+    if (!aligned16(ptr)) return TTT_ERR_ALIGNMENT;
+  for (int i = 0; i < step; ++i)
+    if (!aligned16(k_steps[i]) || !aligned16(v_steps[i]) || !aligned16(dk_steps[i]) || !aligned16(dv_steps[i]))
+      return TTT_ERR_ALIGNMENT;
+  Params p;
+  fill_common(p, d, step);
+  p.accumulate = (flags & TTT_ACCUMULATE_DKV) ? 1 : 0;
+  p.q = q;
+  p.k = k_base;
+  p.v = v_base;
+  p.o = out;
+  p.lse_in = lse;
+  p.dout = dout;
+  p.dq = dq;
+  p.dk = dk_base;
+  p.dv = dv_base;
+  for (int i = 0; i < step; ++i) {
+    p.ks[i] = k_steps[i];
+    p.vs[i] = v_steps[i];
+    p.dks[i] = dk_steps[i];
+    p.dvs[i] = dv_steps[i];
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t kv_elems = (size_t)p.B * p.L * p.Hkv * p.D;
+  if (d->dtype == TTT_FP32_CHECK) {
+    if (!p.accumulate) {
+      cudaError_t e = launch_zero_f32(p.dk, kv_elems, s);
+      if (e == cudaSuccess) e = launch_zero_f32(p.dv, kv_elems, s);
+      for (int i = 0; i < step && e == cudaSuccess; ++i) {
+        e = launch_zero_f32(p.dks[i], kv_elems, s);
+        if (e == cudaSuccess) e = launch_zero_f32(p.dvs[i], kv_elems, s);
+      }
+      if (e != cudaSuccess) return TTT_ERR_CUDA;
+    }
+    return cuda_status(launch_bwd_check(p, s));
+  }
+  const BwdWs w = bwd_ws_layout(d);
+  if (!workspace || workspace_bytes < w.total) return TTT_ERR_WORKSPACE;
+  if (!aligned16(workspace)) return TTT_ERR_ALIGNMENT;
+  char* ws = static_cast<char*>(workspace);
+  p.delta = reinterpret_cast<float*>(ws + w.delta);
+  p.lse2 = reinterpret_cast<float*>(ws + w.lse2);
+  p.dq_acc = reinterpret_cast<float*>(ws + w.dq_acc);
+  BwdMaps maps;
+  if (!encode_bshd(&maps.q, q, p.B, p.L, p.Hq, p.D) || !encode_bshd(&maps.k, k_base, p.B, p.L, p.Hkv, p.D) ||
+      !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D) || !encode_bshd(&maps.dout, dout, p.B, p.L, p.Hq, p.D))
+    return TTT_ERR_CUDA;
+  return cuda_status(launch_bwd_sm100(p, maps, s));
+}
+
+}  // extern "C"

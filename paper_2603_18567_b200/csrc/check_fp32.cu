@@ -1,0 +1,164 @@
+// check_fp32.cu — TTT_FP32_CHECK mode: the same semantics as the tensor-core
+// path on CUDA cores in fp32, used to check mask / GQA / diagonal-fold / lse /
+// accumulate semantics at 1e-5 against the fp64 oracle.
+// tcgen05 .kind::tf32 has a 10-bit mantissa and cannot meet 1e-5, hence SIMT.
+//
+// One warp per query row (b, h, r); lanes split head_dim. Streaming (online)
+// softmax over the allowed set of Alg. 2 enumerated
+// directly: base keys k <= r with k < T_b, then — for r < T_b — the j
+// diagonal keys K_i[r] (Alg. 1 "concat s_i").
+#include <cuda_runtime.h>
+
+#include "ttt_params.cuh"
+
+namespace tttk {
+
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) fwd_check_kernel(const Params p) {
+  constexpr int E = D / 32;
+  const int lane = threadIdx.x & 31;
+  const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long rows = (long)p.B * p.Hq * p.L;
+  if (warp >= rows) return;
+  const int r = (int)(warp % p.L);
+  const int h = (int)((warp / p.L) % p.Hq);
+  const int b = (int)(warp / ((long)p.L * p.Hq));
+  const int g = h / p.G;
+  const int T = p.seq_lens[b];
+  const float* qrow = (const float*)p.q + (((size_t)b * p.L + r) * p.Hq + h) * D;
+  float qv[E], acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    qv[e] = qrow[lane + 32 * e];
+    acc[e] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  auto visit = [&](const float* krow, const float* vrow) {
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) s = fmaf(qv[e], krow[lane + 32 * e], s);
+    s = warp_sum(s) * p.scale;
+    const float mn = fmaxf(m, s);
+    const float a = expf(m - mn), w = expf(s - mn);
+    l = l * a + w;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = fmaf(w, vrow[lane + 32 * e], acc[e] * a);
+    m = mn;
+  };
+  const size_t kv_stride = (size_t)p.Hkv * D;
+  const float* K0 = (const float*)p.k + ((size_t)b * p.L * p.Hkv + g) * D;
+  const float* V0 = (const float*)p.v + ((size_t)b * p.L * p.Hkv + g) * D;
+  const int nbase = r < T ? r + 1 : T;
+  for (int k = 0; k < nbase; ++k) visit(K0 + k * kv_stride, V0 + k * kv_stride);
+  if (r < T) {
+    for (int i = 0; i < p.step; ++i) {
+      const size_t off = (((size_t)b * p.L + r) * p.Hkv + g) * D;
+      visit((const float*)p.ks[i] + off, (const float*)p.vs[i] + off);
+    }
+  }
+  float* orow = (float*)p.out + (((size_t)b * p.L + r) * p.Hq + h) * D;
+  const float inv = 1.f / l;
+#pragma unroll
+  for (int e = 0; e < E; ++e) orow[lane + 32 * e] = acc[e] * inv;
+  if (lane == 0) p.lse[((size_t)b * p.Hq + h) * p.L + r] = m + logf(l);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) bwd_check_kernel(const Params p) {
+  constexpr int E = D / 32;
+  const int lane = threadIdx.x & 31;
+  const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long rows = (long)p.B * p.Hq * p.L;
+  if (warp >= rows) return;
+  const int r = (int)(warp % p.L);
+  const int h = (int)((warp / p.L) % p.Hq);
+  const int b = (int)(warp / ((long)p.L * p.Hq));
+  const int g = h / p.G;
+  const int T = p.seq_lens[b];
+  const size_t qoff = (((size_t)b * p.L + r) * p.Hq + h) * D;
+  const float* qrow = (const float*)p.q + qoff;
+  const float* orow = (const float*)p.o + qoff;
+  const float* dorow = (const float*)p.dout + qoff;
+  float qv[E], dov[E], dq[E];
+  float delta = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    qv[e] = qrow[lane + 32 * e];
+    dov[e] = dorow[lane + 32 * e];
+    delta = fmaf(dov[e], orow[lane + 32 * e], delta);
+    dq[e] = 0.f;
+  }
+  delta = warp_sum(delta);  // Delta_r = dO_r . O_r
+  const float lse = p.lse_in[((size_t)b * p.Hq + h) * p.L + r];
+  auto visit = [&](const float* krow, const float* vrow, float* dkrow, float* dvrow) {
+    float s = 0.f, dp = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      s = fmaf(qv[e], krow[lane + 32 * e], s);
+      dp = fmaf(dov[e], vrow[lane + 32 * e], dp);
+    }
+    s = warp_sum(s) * p.scale;
+    dp = warp_sum(dp);
+    const float pr = expf(s - lse);         // P = exp(S - lse)
+    const float ds = pr * (dp - delta);     // dS = P o (dP - Delta)
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      dq[e] = fmaf(p.scale * ds, krow[lane + 32 * e], dq[e]);   // dQ += c dS K
+      atomicAdd(dkrow + lane + 32 * e, p.scale * ds * qv[e]);    // dK += c dS^T Q
+      atomicAdd(dvrow + lane + 32 * e, pr * dov[e]);             // dV += P^T dO
+    }
+  };
+  const size_t kv_stride = (size_t)p.Hkv * D;
+  const size_t base = ((size_t)b * p.L * p.Hkv + g) * D;
+  const float* K0 = (const float*)p.k + base;
+  const float* V0 = (const float*)p.v + base;
+  const int nbase = r < T ? r + 1 : T;
+  for (int k = 0; k < nbase; ++k)
+    visit(K0 + k * kv_stride, V0 + k * kv_stride, p.dk + base + k * kv_stride, p.dv + base + k * kv_stride);
+  if (r < T) {
+    const size_t off = (((size_t)b * p.L + r) * p.Hkv + g) * D;
+    for (int i = 0; i < p.step; ++i)
+      visit((const float*)p.ks[i] + off, (const float*)p.vs[i] + off, p.dks[i] + off, p.dvs[i] + off);
+  }
+  float* dqrow = (float*)p.dq + qoff;
+#pragma unroll
+  for (int e = 0; e < E; ++e) dqrow[lane + 32 * e] = dq[e];
+}
+
+__global__ void zero_f32_kernel(float* __restrict__ x, size_t n) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) x[i] = 0.f;
+}
+
+cudaError_t launch_zero_f32(float* x, size_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  zero_f32_kernel<<<blocks, 256, 0, st>>>(x, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwd_check(const Params& p, cudaStream_t st) {
+  const long rows = (long)p.B * p.Hq * p.L;
+  const int blocks = (int)((rows + 7) / 8);
+  if (p.D == 64) fwd_check_kernel<64><<<blocks, 256, 0, st>>>(p);
+  else fwd_check_kernel<128><<<blocks, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_check(const Params& p, cudaStream_t st) {
+  const long rows = (long)p.B * p.Hq * p.L;
+  const int blocks = (int)((rows + 7) / 8);
+  if (p.D == 64) bwd_check_kernel<64><<<blocks, 256, 0, st>>>(p);
+  else bwd_check_kernel<128><<<blocks, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace tttk

@@ -1,0 +1,53 @@
+// ttt_params.cuh — kernel parameter block shared by the launchers (api.cu) and
+// the kernels. Passed BY VALUE (kernel params live in constant bank), so a call
+// keeps no state in the library.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+
+#include "../../include/ttt_attn.h"
+
+namespace tttk {
+
+constexpr int kTile = 128;  // q-tile rows = kv-tile rows (UMMA M = N = 128)
+
+struct Params {
+  int B, L, Hq, Hkv, D, G;  // G = Hq / Hkv (GQA group size, kv head = h / G)
+  int step;                 // j: number of step-list entries (diagonal keys) used
+  int accumulate;           // bwd: += into dk/dv
+  int nqt;                  // L / 128 (tensor-core path)
+  int head_split;           // bwd: CTAs per (b, kv head, kv tile) sharing the G q-heads
+  float scale;              // c
+  float scale_log2;         // c * log2(e)
+  // forward / shared inputs
+  const void* q;
+  const void* k;  // K_0
+  const void* v;  // V_0
+  const void* ks[TTT_MAX_STEPS];
+  const void* vs[TTT_MAX_STEPS];
+  void* out;
+  float* lse;
+  // backward
+  const void* o;
+  const void* dout;
+  const float* lse_in;
+  void* dq;
+  float* dk;
+  float* dv;
+  float* dks[TTT_MAX_STEPS];
+  float* dvs[TTT_MAX_STEPS];
+  float* delta;   // workspace [B][Hq][L]: Delta = rowsum(dO o O)
+  float* lse2;    // workspace [B][Hq][L]: lse * log2(e)
+  float* dq_acc;  // workspace [B][L][Hq][D] fp32
+  int seq_lens[TTT_MAX_BATCH];
+};
+
+// Tensor maps for the tcgen05 paths (4-D: D, H, L, B; box 64 x 1 x 128 x 1, SW128)
+struct FwdMaps {
+  CUtensorMap q, k, v;
+};
+struct BwdMaps {
+  CUtensorMap q, k, v, dout;
+};
+
+}  // namespace tttk

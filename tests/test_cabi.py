@@ -1,0 +1,89 @@
+"""CPU-side checks of the C-ABI boundary (no GPU compute): the shared library
+loads, exports every function include/ttt_attn.h declares, and rejects bad
+arguments with the documented status codes before touching the device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2603_18567_b200 as ttt
+from paper_2603_18567_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    names = []
+    for fn in os.listdir(os.path.join(ROOT, "include")):
+        if fn.endswith(".h"):
+            src = open(os.path.join(ROOT, "include", fn)).read()
+            names += re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(ttt_attn_\w+)\s*\(", src, re.M)
+    return sorted(set(names))
+
+
+def test_header_symbols_exported():
+    names = _declared_functions()
+    assert {"ttt_attn_fwd", "ttt_attn_bwd", "ttt_attn_workspace_size", "ttt_attn_strerror"} <= set(names)
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_version_and_strerror():
+    assert "sm_100a" in ttt.ttt_attn_version()
+    for code in range(8):
+        assert ttt.ttt_attn_strerror(code)
+
+
+class FakeT:
+    """Stand-in exposing data_ptr() only: validation fails before any CUDA call."""
+    def __init__(self, ptr):
+        self.p = ptr
+
+    def data_ptr(self):
+        return self.p
+
+
+def _fwd(desc, step, align=16, null=False):
+    P = lambda i: FakeT(0 if null and i == 0 else 0x10000000 + 4096 * i + (align % 16))
+    ks = [P(10 + i) for i in range(max(step, 0))]
+    vs = [P(50 + i) for i in range(max(step, 0))]
+    ttt.ttt_attn_fwd(desc, step, P(0), P(1), P(2), ks, vs, P(3), P(4))
+
+
+@pytest.mark.parametrize("kw,step,code", [
+    (dict(head_dim=96), 0, 2),                 # unsupported head_dim
+    (dict(seq_len=100), 0, 2),                 # bf16 needs L % 128 == 0
+    (dict(num_kv_heads=3), 0, 1),              # Hq % Hkv != 0
+    (dict(), -1, 3), (dict(), 32, 3),          # step range
+    (dict(seq_lens=[0, 128]), 0, 5),           # degenerate T_b
+    (dict(seq_lens=[129, 128]), 0, 5),
+    (dict(batch=0), 0, 1),
+])
+def test_validation_codes(kw, step, code):
+    base = dict(batch=2, seq_len=128, num_q_heads=4, num_kv_heads=2, head_dim=64)
+    base.update(kw)
+    d = ttt.make_desc(**base)
+    with pytest.raises(ttt.TTTError) as ei:
+        _fwd(d, step)
+    assert ei.value.code == code
+
+
+def test_alignment_and_null():
+    d = ttt.make_desc(1, 128, 2, 1, 64)
+    with pytest.raises(ttt.TTTError) as ei:
+        _fwd(d, 1, align=8)
+    assert ei.value.code == 4
+    with pytest.raises(ttt.TTTError) as ei:
+        _fwd(d, 1, null=True)
+    assert ei.value.code == 1
+
+
+def test_workspace_size():
+    d = ttt.make_desc(8, 2048, 32, 8, 128)
+    ws = ttt.ttt_attn_workspace_size(d, 6, True)
+    rows = 8 * 32 * 2048
+    assert ws >= rows * 4 * 2 + rows * 128 * 4
+    assert ttt.ttt_attn_workspace_size(d, 6, False) == 0
+    assert ttt.ttt_attn_workspace_size(ttt.make_desc(8, 2048, 32, 8, 96), 0, True) == 0
