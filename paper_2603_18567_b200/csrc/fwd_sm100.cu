@@ -1,6 +1,352 @@
-// placeholder until the tcgen05 forward lands
+// fwd_sm100.cu — TTT attention forward on sm_100a tensor cores.
+//
+// What it computes: SURVEY.md §8(a) rows 1-6 — for each query row r the
+// softmax over the allowed set of Alg. 2: base keys
+// k <= r with k < T_b, streamed in 128-key tiles with online softmax
+// ("FlashAttention-style streaming"; BlockMask skipping,
+// PAPER.md:331), then — in the epilogue — the j per-step diagonal keys
+// K_i[r] (Alg. 1 "concat s_i ... o_t += alpha_i v_i") folded
+// into the same running max / sum, so the L x (j+1)L mask is never built.
+//
+// CTA work item: one 128-row q tile of TWO query heads of the same GQA group
+// (same K/V stream, identical causal length), so every K/V tile TMA'd into
+// shared memory feeds two S = Q K^T MMAs. Warp roles (320 threads):
+//   warps 0-3  softmax + epilogue, head slot 0 (TMEM lanes 0-127)
+//   warps 4-7  softmax + epilogue, head slot 1
+//   warp  8    TMA producer (Q once, then K/V tiles through a 2-stage ring)
+//   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512);
+// P (bf16, packed 2/column) is written over S and consumed by the PV MMA
+// straight from TMEM (A operand in TMEM, "ts" form).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include "ptx_sm100.cuh"
 #include "ttt_params.cuh"
+
 namespace tttk {
-cudaError_t launch_fwd_sm100(const Params&, const FwdMaps&, cudaStream_t) { return cudaErrorNotSupported; }
+namespace {
+
+constexpr int kFwdThreads = 320;
+constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only when the max grows by > 2^8
+
+struct FwdBars {
+  uint64_t q;
+  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+  uint64_t s_full[2], p_full[2], o_full[2];
+  uint32_t tmem_base;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    ttt_fwd_sm100_kernel(const __grid_constant__ Params p, const __grid_constant__ FwdMaps maps) {
+  constexpr int TB = kTile * D * 2;  // bytes of one 128 x D bf16 tile
+  constexpr int NBOX = D / 64;       // 64-column (128 B) swizzle boxes per tile
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;           // 2 tiles (head slots)
+  uint8_t* sK = smem + 2 * TB;  // 2 stages
+  uint8_t* sV = smem + 4 * TB;  // 2 stages
+  __shared__ FwdBars bars;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- work decode: longest (highest q tile) first -----------------------
+  const int npairs = (p.G + 1) >> 1;
+  const int per_qt = p.B * p.Hkv * npairs;
+  const int qt = p.nqt - 1 - (int)blockIdx.x / per_qt;
+  int rem = (int)blockIdx.x % per_qt;
+  const int b = rem / (p.Hkv * npairs);
+  rem %= p.Hkv * npairs;
+  const int g = rem / npairs;
+  const int hp = rem % npairs;
+  const int h0 = g * p.G + 2 * hp;
+  const bool has1 = (2 * hp + 1) < p.G;
+  const int T = p.seq_lens[b];
+  const int nkv = min(qt + 1, (T + kTile - 1) / kTile);  // BlockMask: skip k0 > q0+127 and k0 >= T
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars.q, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars.k_full[i], 1);
+      mbar_init(&bars.k_empty[i], 1);
+      mbar_init(&bars.v_full[i], 1);
+      mbar_init(&bars.v_empty[i], 1);
+      mbar_init(&bars.s_full[i], 1);
+      mbar_init(&bars.p_full[i], 128);
+      mbar_init(&bars.o_full[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 9) {
+    tmem_alloc(&bars.tmem_base, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = bars.tmem_base;
+
+  if (warp == 8) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      tma_prefetch_desc(&maps.q);
+      tma_prefetch_desc(&maps.k);
+      tma_prefetch_desc(&maps.v);
+      mbar_expect_tx(&bars.q, (has1 ? 2 : 1) * TB);
+#pragma unroll
+      for (int bx = 0; bx < NBOX; ++bx) {
+        tma_load_4d(sQ + bx * 16384, &maps.q, &bars.q, bx * 64, h0, qt * kTile, b);
+        if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.q, &bars.q, bx * 64, h0 + 1, qt * kTile, b);
+      }
+      for (int n = 0; n < nkv; ++n) {
+        const int st = n & 1, ph = (n >> 1) & 1;
+        mbar_wait(&bars.k_empty[st], ph ^ 1);
+        mbar_expect_tx(&bars.k_full[st], TB);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, g, n * kTile, b);
+        mbar_wait(&bars.v_empty[st], ph ^ 1);
+        mbar_expect_tx(&bars.v_full[st], TB);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, n * kTile, b);
+      }
+    }
+  } else if (warp == 9) {
+    // ================= MMA issuer (one thread) =================
+    if (lane == 0) {
+      constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);  // S = Q K^T, both K-major
+      constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);     // O += P V, V MN-major
+      const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+      auto issue_S = [&](int slot, int kst) {
+        const uint32_t qa = q_addr + slot * TB, ka = k_addr + kst * TB;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+          umma_ss(tbase + slot * 128, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), idS,
+                  ks > 0);
+        }
+      };
+      auto issue_PV = [&](int slot, int vst, bool acc) {
+        const uint32_t va = v_addr + vst * TB;
+#pragma unroll
+        for (int ks = 0; ks < kTile / 16; ++ks)
+          umma_ts(tbase + 256 + slot * 128, tbase + slot * 128 + ks * 8, sdesc_sw128(va + ks * 2048, 16384, 1024),
+                  idO, (acc || ks > 0) ? 1u : 0u);
+      };
+      mbar_wait(&bars.q, 0);
+      mbar_wait(&bars.k_full[0], 0);
+      tc_fence_after();
+      issue_S(0, 0);
+      umma_commit(&bars.s_full[0]);
+      if (has1) {
+        issue_S(1, 0);
+        umma_commit(&bars.s_full[1]);
+      }
+      umma_commit(&bars.k_empty[0]);
+      for (int n = 0; n < nkv; ++n) {
+        const int vst = n & 1, vph = (n >> 1) & 1;
+        const bool more = n + 1 < nkv;
+        const int kst = (n + 1) & 1, kph = ((n + 1) >> 1) & 1;
+        mbar_wait(&bars.v_full[vst], vph);
+        mbar_wait(&bars.p_full[0], n & 1);
+        tc_fence_after();
+        issue_PV(0, vst, n > 0);
+        if (more) {
+          mbar_wait(&bars.k_full[kst], kph);
+          tc_fence_after();
+          issue_S(0, kst);
+          umma_commit(&bars.s_full[0]);  // also covers PV0_n (commit tracks all prior MMAs)
+        } else {
+          umma_commit(&bars.o_full[0]);
+        }
+        if (has1) {
+          mbar_wait(&bars.p_full[1], n & 1);
+          tc_fence_after();
+          issue_PV(1, vst, n > 0);
+          umma_commit(&bars.v_empty[vst]);
+          if (more) {
+            issue_S(1, kst);
+            umma_commit(&bars.s_full[1]);
+            umma_commit(&bars.k_empty[kst]);
+          } else {
+            umma_commit(&bars.o_full[1]);
+          }
+        } else {
+          umma_commit(&bars.v_empty[vst]);
+          if (more) umma_commit(&bars.k_empty[kst]);
+        }
+      }
+    }
+  } else {
+    // ================= softmax + epilogue (warps 0-7) =================
+    const int slot = warp >> 2;
+    const int wq = warp & 3;
+    if (slot == 0 || has1) {
+      const int row = wq * 32 + lane;
+      const int r = qt * kTile + row;
+      const int h = h0 + slot;
+      const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+      const uint32_t tS = tbase + lane_off + slot * 128;
+      const uint32_t tO = tbase + lane_off + 256 + slot * 128;
+      const float sl2 = p.scale_log2;
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int n = 0; n < nkv; ++n) {
+        mbar_wait(&bars.s_full[slot], n & 1);
+        tc_fence_after();
+        float s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t raw[32];
+          tmem_ld32(tS + c * 32, raw);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(raw[i]);
+        }
+        const int kv0 = n * kTile;
+        const bool partial = (n == qt) || (kv0 + kTile > T);
+        float mx = -INFINITY;
+        if (partial) {
+          const int lim = min(r + 1, T) - kv0;  // allowed columns c < lim  (k <= r and k < T)
+#pragma unroll
+          for (int c = 0; c < 128; ++c) {
+            const float x = c < lim ? s[c] * sl2 : -INFINITY;
+            s[c] = x;
+            mx = fmaxf(mx, x);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) {
+            s[c] *= sl2;
+            mx = fmaxf(mx, s[c]);
+          }
+        }
+        const float m_new = fmaxf(m_run, mx);
+        const bool need = m_new > m_run + kRescaleThreshold;
+        if (__any_sync(0xffffffffu, need)) {
+          const float alpha = ex2(m_run - m_new);
+          if (n > 0) {  // PV_{n-1} is complete: s_full's commit covers it
+#pragma unroll
+            for (int c = 0; c < D; c += 32) {
+              uint32_t o[32];
+              tmem_ld32(tO + c, o);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st32(tO + c, o);
+            }
+          }
+          l_run *= alpha;
+          m_run = m_new;
+        }
+        float rs = 0.f;
+        uint32_t pk[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const float e0 = ex2(s[2 * c] - m_run), e1 = ex2(s[2 * c + 1] - m_run);
+          rs += e0 + e1;
+          pk[c] = pack_bf16(e0, e1);
+        }
+        l_run += rs;
+        tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars.p_full[slot]);
+      }
+      // ---- epilogue: diagonal fold (TTT step keys), normalise, store ----
+      mbar_wait(&bars.o_full[slot], 0);
+      tc_fence_after();
+      float w[TTT_MAX_STEPS];
+      float m_f = m_run;
+      const int nd = (r < T) ? p.step : 0;
+      const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D;
+      const size_t kv_off = (((size_t)b * p.L + r) * p.Hkv + g) * D;
+      const __nv_bfloat16* qrow = reinterpret_cast<const __nv_bfloat16*>(p.q) + q_off;
+      for (int i = 0; i < nd; ++i) {
+        const __nv_bfloat16* krow = reinterpret_cast<const __nv_bfloat16*>(p.ks[i]) + kv_off;
+        float acc = 0.f;
+#pragma unroll 4
+        for (int d = 0; d < D; d += 8) {
+          const uint4 qa = *reinterpret_cast<const uint4*>(qrow + d);
+          const uint4 ka = *reinterpret_cast<const uint4*>(krow + d);
+          const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&qa);
+          const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&ka);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 qf = __bfloat1622float2(q2[e]), kf = __bfloat1622float2(k2[e]);
+            acc = fmaf(qf.x, kf.x, acc);
+            acc = fmaf(qf.y, kf.y, acc);
+          }
+        }
+        w[i] = acc * sl2;  // s_i = c q_r . k_i (log2 units)
+        m_f = fmaxf(m_f, w[i]);
+      }
+      const float alpha = ex2(m_run - m_f);
+      float l_f = l_run * alpha;
+      for (int i = 0; i < nd; ++i) {
+        w[i] = ex2(w[i] - m_f);
+        l_f += w[i];
+      }
+      const float inv_l = 1.f / l_f;
+      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t o[32];
+        tmem_ld32(tO + c0, o);
+        float acc[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = __uint_as_float(o[i]) * alpha;
+        for (int i = 0; i < nd; ++i) {
+          const __nv_bfloat16* vrow = reinterpret_cast<const __nv_bfloat16*>(p.vs[i]) + kv_off + c0;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const uint4 va = *reinterpret_cast<const uint4*>(vrow + q4 * 8);
+            const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&va);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 vf = __bfloat1622float2(v2[e]);
+              acc[q4 * 8 + 2 * e] = fmaf(w[i], vf.x, acc[q4 * 8 + 2 * e]);
+              acc[q4 * 8 + 2 * e + 1] = fmaf(w[i], vf.y, acc[q4 * 8 + 2 * e + 1]);
+            }
+          }
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          uint4 v;
+          v.x = pack_bf16(acc[q4 * 8 + 0] * inv_l, acc[q4 * 8 + 1] * inv_l);
+          v.y = pack_bf16(acc[q4 * 8 + 2] * inv_l, acc[q4 * 8 + 3] * inv_l);
+          v.z = pack_bf16(acc[q4 * 8 + 4] * inv_l, acc[q4 * 8 + 5] * inv_l);
+          v.w = pack_bf16(acc[q4 * 8 + 6] * inv_l, acc[q4 * 8 + 7] * inv_l);
+          *reinterpret_cast<uint4*>(orow + c0 + q4 * 8) = v;
+        }
+      }
+      p.lse[((size_t)b * p.Hq + h) * p.L + r] = (m_f + log2f(l_f)) * 0.69314718055994531f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc(tbase, 512);
 }
+
+template <int D>
+cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, cudaStream_t st) {
+  const int smem = 6 * kTile * D * 2 + 1024;
+  static bool attr_set = false;  // benign race: idempotent attribute set
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(ttt_fwd_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int npairs = (p.G + 1) / 2;
+  const int grid = p.nqt * p.B * p.Hkv * npairs;
+  ttt_fwd_sm100_kernel<D><<<grid, kFwdThreads, smem, st>>>(p, maps);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, cudaStream_t st) {
+  return p.D == 64 ? launch_fwd_d<64>(p, maps, st) : launch_fwd_d<128>(p, maps, st);
+}
+
+}  // namespace tttk
