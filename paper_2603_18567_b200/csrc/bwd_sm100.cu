@@ -1,6 +1,531 @@
-// placeholder until the tcgen05 backward lands
+// bwd_sm100.cu — TTT attention backward on sm_100a.
+//
+// Recompute-based (no saved probabilities): P = exp(S - lse) is
+// rebuilt from the forward's lse. Three kernels per call, all on `stream`:
+//
+//  1. ttt_bwd_pre_kernel (HBM-streaming, CUDA cores), one warp per (b, r, kv head g):
+//       Delta_{h,r} = dO_{h,r} . O_{h,r};  lse2 = lse * log2(e)
+//       TTT diagonal keys (the j step entries of row r < T_b, Alg. 2 M_suffix,
+//       PAPER.md:305-309): p_i = exp(c q.K_i[r] - lse), dp_i = dO.V_i[r],
+//       ds_i = p_i (dp_i - Delta), dq_acc[r] = c sum_i ds_i K_i[r] (initialises the
+//       fp32 dq accumulator), dK_i[r] (+)= c sum_h ds_i q_h, dV_i[r] (+)= sum_h p_i dO_h.
+//       Zeroes dK_0/dV_0 rows when not accumulating (the main kernel adds into them).
+//  2. ttt_bwd_sm100_kernel (tcgen05), KV-outer: one CTA per (b, g, 128-key tile kt,
+//     head subset); loops over its query heads x causal q tiles qt >= kt:
+//       S^T = K Q^T, dP^T = V dO^T                         (SS MMAs, TMEM)
+//       P^T = exp2(S^T c log2e - lse2), dS^T = P^T o (dP^T - Delta)   (compute warps)
+//       dV += P^T dO, dK += dS^T Q                         (A operand from TMEM)
+//       dQ  = dS K  -> red.global.add into dq_acc           (A = dS from smem)
+//  3. ttt_bwd_dq_convert_kernel: dq = bf16(dq_acc).
+//
+// Warp roles of the main kernel (320 threads):
+//   warps 0-3 compute (thread = key row, TMEM lanes 0-127), warps 4-7 dQ drain
+//   (thread = query row), warp 8 TMA producer, warp 9 TMEM owner + MMA issuer.
+// TMEM columns: S^T/P^T [0,128) dP^T/dS^T/dQ [128,256) dV [256,256+D) dK [384,384+D).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include "ptx_sm100.cuh"
 #include "ttt_params.cuh"
+
 namespace tttk {
-cudaError_t launch_bwd_sm100(const Params&, const BwdMaps&, cudaStream_t) { return cudaErrorNotSupported; }
+namespace {
+
+constexpr int kBwdThreads = 320;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float warp_allsum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
 }
+
+template <int E>
+__device__ __forceinline__ void load_bf16(const void* base, size_t off, float (&x)[E]) {
+  const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(base) + off;
+  if constexpr (E == 4) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    x[0] = a.x; x[1] = a.y; x[2] = c.x; x[3] = c.y;
+  } else {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+    x[0] = a.x; x[1] = a.y;
+  }
+}
+
+// ------------------------------------------------------------------ kernel 1
+template <int D>
+__global__ void __launch_bounds__(128) ttt_bwd_pre_kernel(const __grid_constant__ Params p) {
+  constexpr int E = D / 32;
+  extern __shared__ float pre_smem[];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const long wid = (long)blockIdx.x * 4 + wl;
+  if (wid >= (long)p.B * p.L * p.Hkv) return;
+  const int G = p.G;
+  const int g = (int)(wid % p.Hkv);
+  const int r = (int)((wid / p.Hkv) % p.L);
+  const int b = (int)(wid / ((long)p.Hkv * p.L));
+  const int T = p.seq_lens[b];
+  float* sdq = pre_smem + (size_t)wl * (G * D + 2 * G);  // [G][D]
+  float* sdel = sdq + G * D;                              // [G]
+  float* sl2 = sdel + G;                                  // [G]
+  const size_t kv_off = (((size_t)b * p.L + r) * p.Hkv + g) * D + lane * E;
+
+  for (int hh = 0; hh < G; ++hh) {
+    const int h = g * G + hh;
+    const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + lane * E;
+    float o[E], d[E];
+    load_bf16<E>(p.o, q_off, o);
+    load_bf16<E>(p.dout, q_off, d);
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc = fmaf(o[e], d[e], acc);
+    const float delta = warp_allsum(acc);  // Delta_r = dO_r . O_r
+    const size_t li = ((size_t)b * p.Hq + h) * p.L + r;
+    const float l2 = p.lse_in[li] * kLog2e;
+    if (lane == 0) {
+      p.delta[li] = delta;
+      p.lse2[li] = l2;
+      sdel[hh] = delta;
+      sl2[hh] = l2;
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) sdq[hh * D + lane * E + e] = 0.f;
+  }
+  __syncwarp();
+  if (!p.accumulate) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      p.dk[kv_off + e] = 0.f;
+      p.dv[kv_off + e] = 0.f;
+    }
+  }
+  const int nd = r < T ? p.step : 0;
+  for (int i = 0; i < p.step; ++i) {
+    float dk[E], dv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) dk[e] = dv[e] = 0.f;
+    if (i < nd) {
+      float kk[E], vv[E];
+      load_bf16<E>(p.ks[i], kv_off, kk);
+      load_bf16<E>(p.vs[i], kv_off, vv);
+      for (int hh = 0; hh < G; ++hh) {
+        const int h = g * G + hh;
+        const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + lane * E;
+        float qq[E], dd[E];
+        load_bf16<E>(p.q, q_off, qq);
+        load_bf16<E>(p.dout, q_off, dd);
+        float s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          s = fmaf(qq[e], kk[e], s);
+          dp = fmaf(dd[e], vv[e], dp);
+        }
+        s = warp_allsum(s);
+        dp = warp_allsum(dp);
+        const float pr = ex2(s * p.scale_log2 - sl2[hh]);  // p_i = exp(c q.k_i - lse)
+        const float ds = pr * (dp - sdel[hh]);             // ds_i = p_i (dp_i - Delta)
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          dk[e] = fmaf(p.scale * ds, qq[e], dk[e]);
+          dv[e] = fmaf(pr, dd[e], dv[e]);
+          sdq[hh * D + lane * E + e] = fmaf(p.scale * ds, kk[e], sdq[hh * D + lane * E + e]);
+        }
+      }
+    }
+    float* dkp = p.dks[i] + kv_off;
+    float* dvp = p.dvs[i] + kv_off;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      dkp[e] = p.accumulate ? dkp[e] + dk[e] : dk[e];
+      dvp[e] = p.accumulate ? dvp[e] + dv[e] : dv[e];
+    }
+  }
+  __syncwarp();
+  for (int hh = 0; hh < G; ++hh) {
+    const int h = g * G + hh;
+    float* dst = p.dq_acc + (((size_t)b * p.L + r) * p.Hq + h) * D + lane * E;
+#pragma unroll
+    for (int e = 0; e < E; ++e) dst[e] = sdq[hh * D + lane * E + e];
+  }
+}
+
+// ------------------------------------------------------------------ kernel 2
+struct BwdBars {
+  uint64_t kv_full;
+  uint64_t q_full[2], q_empty[2];
+  uint64_t do_full, do_empty;
+  uint64_t s_full, dp_full, p_full, ds_full, ds_empty, dq_full, dq_empty, acc_full;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    ttt_bwd_sm100_kernel(const __grid_constant__ Params p, const __grid_constant__ BwdMaps maps) {
+  constexpr int TB = kTile * D * 2;
+  constexpr int NBOX = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + TB;
+  uint8_t* sQ = smem + 2 * TB;   // 2 stages
+  uint8_t* sDO = smem + 4 * TB;  // 1 stage
+  uint8_t* sDS = smem + 5 * TB;  // 128 x 128 bf16, [kv][q] in two 64-column SW128 boxes
+  float* sL = reinterpret_cast<float*>(smem + 5 * TB + 32768);  // [2][128] lse2
+  float* sDel = sL + 256;                                      // [2][128] Delta
+  __shared__ BwdBars bars;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hsplit = p.head_split;
+  const int nh = p.G / hsplit;
+  const int per_kt = p.B * p.Hkv * hsplit;
+  const int kt = (int)blockIdx.x / per_kt;  // ascending kt = descending work (causal)
+  int rem = (int)blockIdx.x % per_kt;
+  const int b = rem / (p.Hkv * hsplit);
+  rem %= p.Hkv * hsplit;
+  const int g = rem / hsplit;
+  const int hs = rem % hsplit;
+  const int T = p.seq_lens[b];
+  if (kt * kTile >= T) return;  // every key of the tile is padding: no gradient flows
+  const int nq = p.nqt - kt;
+  const int n_items = nh * nq;
+  const int h_first = g * p.G + hs * nh;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars.kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars.q_full[i], 1);
+      mbar_init(&bars.q_empty[i], 1);
+    }
+    mbar_init(&bars.do_full, 1);
+    mbar_init(&bars.do_empty, 1);
+    mbar_init(&bars.s_full, 1);
+    mbar_init(&bars.dp_full, 1);
+    mbar_init(&bars.p_full, 128);
+    mbar_init(&bars.ds_full, 128);
+    mbar_init(&bars.ds_empty, 1);
+    mbar_init(&bars.dq_full, 1);
+    mbar_init(&bars.dq_empty, 128);
+    mbar_init(&bars.acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 9) {
+    tmem_alloc(&bars.tmem_base, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = bars.tmem_base;
+
+  if (warp == 8) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      tma_prefetch_desc(&maps.q);
+      tma_prefetch_desc(&maps.k);
+      tma_prefetch_desc(&maps.v);
+      tma_prefetch_desc(&maps.dout);
+      mbar_expect_tx(&bars.kv_full, 2 * TB);
+#pragma unroll
+      for (int bx = 0; bx < NBOX; ++bx) {
+        tma_load_4d(sK + bx * 16384, &maps.k, &bars.kv_full, bx * 64, g, kt * kTile, b);
+        tma_load_4d(sV + bx * 16384, &maps.v, &bars.kv_full, bx * 64, g, kt * kTile, b);
+      }
+      for (int i = 0; i < n_items; ++i) {
+        const int h = h_first + i / nq, qt = kt + i % nq;
+        const int qs = i & 1, qph = (i >> 1) & 1;
+        mbar_wait(&bars.q_empty[qs], qph ^ 1);
+        mbar_expect_tx(&bars.q_full[qs], TB + 1024);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          tma_load_4d(sQ + qs * TB + bx * 16384, &maps.q, &bars.q_full[qs], bx * 64, h, qt * kTile, b);
+        const size_t li = ((size_t)b * p.Hq + h) * p.L + (size_t)qt * kTile;
+        bulk_load_1d(sL + qs * 128, p.lse2 + li, 512, &bars.q_full[qs]);
+        bulk_load_1d(sDel + qs * 128, p.delta + li, 512, &bars.q_full[qs]);
+        mbar_wait(&bars.do_empty, (i & 1) ^ 1);
+        mbar_expect_tx(&bars.do_full, TB);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          tma_load_4d(sDO + bx * 16384, &maps.dout, &bars.do_full, bx * 64, h, qt * kTile, b);
+      }
+    }
+  } else if (warp == 9) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      constexpr uint32_t idSP = idesc_bf16_f32(128, 128, false, false);  // S^T = K Q^T, dP^T = V dO^T
+      constexpr uint32_t idKV = idesc_bf16_f32(128, D, false, true);     // dV += P^T dO, dK += dS^T Q
+      constexpr uint32_t idDQ = idesc_bf16_f32(128, D, true, true);      // dQ = dS K
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aDO = smem_u32(sDO),
+                     aDS = smem_u32(sDS);
+      auto kmaj = [](uint32_t base, int ks) {
+        return sdesc_sw128(base + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
+      };
+      auto mnmaj = [](uint32_t base, int ks) { return sdesc_sw128(base + ks * 2048, 16384, 1024); };
+      auto issue_S = [&](int qs) {
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) umma_ss(tbase, kmaj(aK, ks), kmaj(aQ + qs * TB, ks), idSP, ks > 0);
+      };
+      auto issue_dP = [&]() {
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) umma_ss(tbase + 128, kmaj(aV, ks), kmaj(aDO, ks), idSP, ks > 0);
+      };
+      mbar_wait(&bars.kv_full, 0);
+      mbar_wait(&bars.q_full[0], 0);
+      tc_fence_after();
+      issue_S(0);
+      umma_commit(&bars.s_full);
+      mbar_wait(&bars.do_full, 0);
+      tc_fence_after();
+      issue_dP();
+      umma_commit(&bars.dp_full);
+      for (int i = 0; i < n_items; ++i) {
+        const int qs = i & 1;
+        const bool more = i + 1 < n_items;
+        // dV += P^T dO   (A = P^T in TMEM cols [0,64))
+        mbar_wait(&bars.p_full, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          umma_ts(tbase + 256, tbase + ks * 8, mnmaj(aDO, ks), idKV, (i > 0 || ks > 0) ? 1u : 0u);
+        umma_commit(&bars.do_empty);
+        // dK += dS^T Q   (A = dS^T in TMEM cols [128,192))
+        mbar_wait(&bars.ds_full, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          umma_ts(tbase + 384, tbase + 128 + ks * 8, mnmaj(aQ + qs * TB, ks), idKV, (i > 0 || ks > 0) ? 1u : 0u);
+        umma_commit(&bars.q_empty[qs]);
+        // next S^T while this item's dQ is drained
+        if (more) {
+          mbar_wait(&bars.q_full[(i + 1) & 1], ((i + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_S((i + 1) & 1);
+          umma_commit(&bars.s_full);
+        }
+        // dQ = dS K -> TMEM cols [128, 128+D)  (A = dS from smem, MN-major)
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) umma_ss(tbase + 128, mnmaj(aDS, ks), mnmaj(aK, ks), idDQ, ks > 0);
+        umma_commit(&bars.dq_full);
+        umma_commit(&bars.ds_empty);
+        if (more) {
+          mbar_wait(&bars.dq_empty, i & 1);
+          mbar_wait(&bars.do_full, (i + 1) & 1);
+          tc_fence_after();
+          issue_dP();
+          umma_commit(&bars.dp_full);
+        }
+      }
+      umma_commit(&bars.acc_full);
+    }
+  } else if (warp < 4) {
+    // ================= compute: P^T, dS^T (thread = key row) =================
+    const int row = warp * 32 + lane;
+    const int k = kt * kTile + row;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t tS = tbase + lane_off, tdP = tbase + lane_off + 128;
+    const float sl2 = p.scale_log2;
+    for (int i = 0; i < n_items; ++i) {
+      const int qs = i & 1;
+      const int qt = kt + i % nq;
+      mbar_wait(&bars.q_full[qs], (i >> 1) & 1);
+      mbar_wait(&bars.s_full, i & 1);
+      tc_fence_after();
+      const float* Lq = sL + qs * 128;
+      const float* Dq = sDel + qs * 128;
+      // allowed (k, q): k <= q and k < T  ->  column c allowed iff c >= k - qt*128 (and k < T)
+      const int cmin = (k < T) ? k - qt * kTile : kTile;  // columns [cmin, 128) allowed
+      float pr[128];
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        uint32_t raw[32];
+        tmem_ld32(tS + c4 * 32, raw);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int c = c4 * 32 + e;
+          const float x = __uint_as_float(raw[e]) * sl2 - Lq[c];
+          pr[c] = c >= cmin ? ex2(x) : 0.f;
+        }
+      }
+      {
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(pr[2 * c], pr[2 * c + 1]);
+        tmem_st32(tS, pk);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(pr[64 + 2 * c], pr[64 + 2 * c + 1]);
+        tmem_st32(tS + 32, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars.p_full);
+      mbar_wait(&bars.dp_full, i & 1);
+      mbar_wait(&bars.ds_empty, (i & 1) ^ 1);
+      tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t raw[32];
+        tmem_ld32(tdP + cc * 32, raw);
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int c = cc * 32 + 2 * e;
+          const float d0 = pr[c] * (__uint_as_float(raw[2 * e]) - Dq[c]);
+          const float d1 = pr[c + 1] * (__uint_as_float(raw[2 * e + 1]) - Dq[c + 1]);
+          pk[e] = pack_bf16(d0, d1);
+        }
+        tmem_st16(tdP + cc * 16, pk);  // dS^T (bf16) over the already-read dP^T columns
+        // smem dS: row = key row, q columns [cc*32, cc*32+32): box cc/2, 8-col chunks
+        uint8_t* boxp = sDS + (cc >> 1) * 16384 + row * 128;
+#pragma unroll
+        for (int e8 = 0; e8 < 4; ++e8) {
+          const int chunk = (cc & 1) * 4 + e8;
+          uint4 v;
+          v.x = pk[e8 * 4 + 0];
+          v.y = pk[e8 * 4 + 1];
+          v.z = pk[e8 * 4 + 2];
+          v.w = pk[e8 * 4 + 3];
+          *reinterpret_cast<uint4*>(boxp + ((chunk ^ (row & 7)) << 4)) = v;
+        }
+      }
+      fence_async_smem();
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars.ds_full);
+    }
+    // ---- dK, dV accumulators -> global (fp32 atomics: head splits and steps add up) ----
+    mbar_wait(&bars.acc_full, 0);
+    tc_fence_after();
+    if (k < T) {
+      const size_t off = (((size_t)b * p.L + k) * p.Hkv + g) * D;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t raw[32];
+        tmem_ld32(tbase + lane_off + 256 + c0, raw);
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          red_add_v4(p.dv + off + c0 + e, __uint_as_float(raw[e]), __uint_as_float(raw[e + 1]),
+                     __uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3]));
+        tmem_ld32(tbase + lane_off + 384 + c0, raw);
+        const float c = p.scale;
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          red_add_v4(p.dk + off + c0 + e, c * __uint_as_float(raw[e]), c * __uint_as_float(raw[e + 1]),
+                     c * __uint_as_float(raw[e + 2]), c * __uint_as_float(raw[e + 3]));
+      }
+    }
+  } else {
+    // ================= dQ drain (warps 4-7, thread = query row) =================
+    const int wq = warp - 4;
+    const int row = wq * 32 + lane;
+    const uint32_t tQ = tbase + ((uint32_t)(wq * 32) << 16) + 128;
+    for (int i = 0; i < n_items; ++i) {
+      const int h = h_first + i / nq, qt = kt + i % nq;
+      mbar_wait(&bars.dq_full, i & 1);
+      tc_fence_after();
+      float v[D];
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t raw[32];
+        tmem_ld32(tQ + c0, raw);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[c0 + e] = __uint_as_float(raw[e]) * p.scale;
+      }
+      tc_fence_before();
+      mbar_arrive(&bars.dq_empty);
+      float* dst = p.dq_acc + (((size_t)b * p.L + (size_t)qt * kTile + row) * p.Hq + h) * D;
+#pragma unroll
+      for (int e = 0; e < D; e += 4) red_add_v4(dst + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc(tbase, 512);
+}
+
+// ------------------------------------------------------------------ kernel 3
+__global__ void __launch_bounds__(256) ttt_bwd_dq_convert_kernel(const float* __restrict__ acc,
+                                                                 __nv_bfloat16* __restrict__ dq, size_t n8) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (; i < n8; i += stride) {
+    const float4 a = reinterpret_cast<const float4*>(acc)[2 * i];
+    const float4 c = reinterpret_cast<const float4*>(acc)[2 * i + 1];
+    uint4 o;
+    o.x = pack_bf16(a.x, a.y);
+    o.y = pack_bf16(a.z, a.w);
+    o.z = pack_bf16(c.x, c.y);
+    o.w = pack_bf16(c.z, c.w);
+    reinterpret_cast<uint4*>(dq)[i] = o;
+  }
+}
+
+int pick_head_split(const Params& p) {
+  const int base = p.nqt * p.B * p.Hkv;
+  int hs = 1;
+  while (hs < p.G && base * hs < 2 * 148) {
+    int nx = hs + 1;
+    while (nx < p.G && p.G % nx) ++nx;
+    hs = nx;
+  }
+  return hs;
+}
+
+template <int D>
+cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t st) {
+  Params p = p_in;
+  p.head_split = pick_head_split(p);
+  // 1. pre-pass
+  {
+    const long warps = (long)p.B * p.L * p.Hkv;
+    const size_t smem = 4 * (size_t)(p.G * D + 2 * p.G) * sizeof(float);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    ttt_bwd_pre_kernel<D><<<(unsigned)((warps + 3) / 4), 128, smem, st>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  // 2. main tensor-core kernel
+  {
+    const int smem = 5 * kTile * D * 2 + 32768 + 2048 + 1024;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaError_t e =
+          cudaFuncSetAttribute(ttt_bwd_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      attr_set = true;
+    }
+    const int grid = p.nqt * p.B * p.Hkv * p.head_split;
+    ttt_bwd_sm100_kernel<D><<<grid, kBwdThreads, smem, st>>>(p, maps);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  // 3. dq = bf16(dq_acc)
+  {
+    const size_t n8 = (size_t)p.B * p.L * p.Hq * D / 8;
+    unsigned blocks = (unsigned)((n8 + 255) / 256);
+    if (blocks > 148u * 8u) blocks = 148u * 8u;
+    ttt_bwd_dq_convert_kernel<<<blocks, 256, 0, st>>>(p.dq_acc, reinterpret_cast<__nv_bfloat16*>(p.dq), n8);
+    return cudaGetLastError();
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, cudaStream_t st) {
+  return p.D == 64 ? launch_bwd_d<64>(p, maps, st) : launch_bwd_d<128>(p, maps, st);
+}
+
+}  // namespace tttk

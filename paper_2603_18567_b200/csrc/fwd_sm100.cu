@@ -253,79 +253,117 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc_fence_before();
         mbar_arrive(&bars.p_full[slot]);
       }
-      // ---- epilogue: diagonal fold (TTT step keys), normalise, store ----
+      // ---- epilogue: merge the diagonal partial (fwd_diag_kernel), normalise, store ----
+      // The j diagonal keys of row r (Alg. 1 "concat s_i") were reduced
+      // by ttt_fwd_diag_kernel into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum); the
+      // merge is the same online-softmax update as one more "tile".
+      const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D;
+      const size_t lse_idx = ((size_t)b * p.Hq + h) * p.L + r;
+      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
+      const bool has_diag = (r < T) && (p.step > 0);
+      uint4 od[D / 8];
+      float A_d = -INFINITY;
+      if (has_diag) {
+        A_d = p.lse[lse_idx];
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) od[c] = *reinterpret_cast<const uint4*>(orow + c * 8);
+      }
       mbar_wait(&bars.o_full[slot], 0);
       tc_fence_after();
-      float w[TTT_MAX_STEPS];
-      float m_f = m_run;
-      const int nd = (r < T) ? p.step : 0;
-      const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D;
-      const size_t kv_off = (((size_t)b * p.L + r) * p.Hkv + g) * D;
-      const __nv_bfloat16* qrow = reinterpret_cast<const __nv_bfloat16*>(p.q) + q_off;
-      for (int i = 0; i < nd; ++i) {
-        const __nv_bfloat16* krow = reinterpret_cast<const __nv_bfloat16*>(p.ks[i]) + kv_off;
-        float acc = 0.f;
-#pragma unroll 4
-        for (int d = 0; d < D; d += 8) {
-          const uint4 qa = *reinterpret_cast<const uint4*>(qrow + d);
-          const uint4 ka = *reinterpret_cast<const uint4*>(krow + d);
-          const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&qa);
-          const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&ka);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 qf = __bfloat1622float2(q2[e]), kf = __bfloat1622float2(k2[e]);
-            acc = fmaf(qf.x, kf.x, acc);
-            acc = fmaf(qf.y, kf.y, acc);
-          }
-        }
-        w[i] = acc * sl2;  // s_i = c q_r . k_i (log2 units)
-        m_f = fmaxf(m_f, w[i]);
-      }
+      const float m_f = fmaxf(m_run, A_d);
       const float alpha = ex2(m_run - m_f);
-      float l_f = l_run * alpha;
-      for (int i = 0; i < nd; ++i) {
-        w[i] = ex2(w[i] - m_f);
-        l_f += w[i];
-      }
+      const float beta = has_diag ? ex2(A_d - m_f) : 0.f;
+      const float l_f = l_run * alpha + beta;
       const float inv_l = 1.f / l_f;
-      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
-#pragma unroll 1
+      const float a_n = alpha * inv_l, b_n = beta * inv_l;
+#pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t o[32];
         tmem_ld32(tO + c0, o);
-        float acc[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] = __uint_as_float(o[i]) * alpha;
-        for (int i = 0; i < nd; ++i) {
-          const __nv_bfloat16* vrow = reinterpret_cast<const __nv_bfloat16*>(p.vs[i]) + kv_off + c0;
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const uint4 va = *reinterpret_cast<const uint4*>(vrow + q4 * 8);
-            const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&va);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 vf = __bfloat1622float2(v2[e]);
-              acc[q4 * 8 + 2 * e] = fmaf(w[i], vf.x, acc[q4 * 8 + 2 * e]);
-              acc[q4 * 8 + 2 * e + 1] = fmaf(w[i], vf.y, acc[q4 * 8 + 2 * e + 1]);
-            }
-          }
-        }
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          uint4 v;
-          v.x = pack_bf16(acc[q4 * 8 + 0] * inv_l, acc[q4 * 8 + 1] * inv_l);
-          v.y = pack_bf16(acc[q4 * 8 + 2] * inv_l, acc[q4 * 8 + 3] * inv_l);
-          v.z = pack_bf16(acc[q4 * 8 + 4] * inv_l, acc[q4 * 8 + 5] * inv_l);
-          v.w = pack_bf16(acc[q4 * 8 + 6] * inv_l, acc[q4 * 8 + 7] * inv_l);
-          *reinterpret_cast<uint4*>(orow + c0 + q4 * 8) = v;
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(o[q4 * 8 + e]) * a_n;
+          if (has_diag) {
+            const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&od[c0 / 8 + q4]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 df = __bfloat1622float2(d2[e]);
+              v[2 * e] = fmaf(b_n, df.x, v[2 * e]);
+              v[2 * e + 1] = fmaf(b_n, df.y, v[2 * e + 1]);
+            }
+          }
+          uint4 w;
+          w.x = pack_bf16(v[0], v[1]);
+          w.y = pack_bf16(v[2], v[3]);
+          w.z = pack_bf16(v[4], v[5]);
+          w.w = pack_bf16(v[6], v[7]);
+          *reinterpret_cast<uint4*>(orow + c0 + q4 * 8) = w;
         }
       }
-      p.lse[((size_t)b * p.Hq + h) * p.L + r] = (m_f + log2f(l_f)) * 0.69314718055994531f;
+      p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc(tbase, 512);
+}
+
+// Diagonal pre-pass (TTT-specific): for every row r < T_b
+// and query head h, t_i = c log2(e) q_r . K_i[r] (i = 1..j),
+//   A_d = log2 sum_i 2^{t_i},  O_d = sum_i 2^{t_i - A_d} V_i[r]
+// written into lse (log2 units) and out (bf16); the main kernel merges them.
+// HBM-streaming: one warp per (b, r, kv head g), lanes split head_dim, rows
+// read once and shared by the G query heads of the group.
+template <int D>
+__global__ void __launch_bounds__(256) ttt_fwd_diag_kernel(const __grid_constant__ Params p) {
+  constexpr int E = D / 32;
+  const int lane = threadIdx.x & 31;
+  const long wid = (long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (wid >= (long)p.B * p.L * p.Hkv) return;
+  const int g = (int)(wid % p.Hkv);
+  const int r = (int)((wid / p.Hkv) % p.L);
+  const int b = (int)(wid / ((long)p.Hkv * p.L));
+  if (r >= p.seq_lens[b]) return;
+  const size_t kv_off = (((size_t)b * p.L + r) * p.Hkv + g) * D + lane * E;
+  float t[TTT_MAX_STEPS];
+  for (int hh = 0; hh < p.G; ++hh) {
+    const int h = g * p.G + hh;
+    const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + lane * E;
+    float qf[E];
+    {
+      const __nv_bfloat16* qp = reinterpret_cast<const __nv_bfloat16*>(p.q) + q_off;
+#pragma unroll
+      for (int e = 0; e < E; ++e) qf[e] = __bfloat162float(qp[e]);
+    }
+    float m = -INFINITY;
+    for (int i = 0; i < p.step; ++i) {
+      const __nv_bfloat16* kp = reinterpret_cast<const __nv_bfloat16*>(p.ks[i]) + kv_off;
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc = fmaf(qf[e], __bfloat162float(kp[e]), acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      t[i] = acc * p.scale_log2;
+      m = fmaxf(m, t[i]);
+    }
+    float l = 0.f, o[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] = 0.f;
+    for (int i = 0; i < p.step; ++i) {
+      const float w = ex2(t[i] - m);
+      l += w;
+      const __nv_bfloat16* vp = reinterpret_cast<const __nv_bfloat16*>(p.vs[i]) + kv_off;
+#pragma unroll
+      for (int e = 0; e < E; ++e) o[e] = fmaf(w, __bfloat162float(vp[e]), o[e]);
+    }
+    const float inv = 1.f / l;
+    __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
+#pragma unroll
+    for (int e = 0; e < E; ++e) op[e] = __float2bfloat16_rn(o[e] * inv);
+    if (lane == 0) p.lse[((size_t)b * p.Hq + h) * p.L + r] = m + log2f(l);
+  }
 }
 
 template <int D>
@@ -336,6 +374,10 @@ cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, cudaStream_t st) 
     cudaError_t e = cudaFuncSetAttribute(ttt_fwd_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
+  }
+  if (p.step > 0) {
+    const long warps = (long)p.B * p.L * p.Hkv;
+    ttt_fwd_diag_kernel<D><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(p);
   }
   const int npairs = (p.G + 1) / 2;
   const int grid = p.nqt * p.B * p.Hkv * npairs;
