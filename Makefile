@@ -2,7 +2,7 @@
 # tests/cuda/libumma_probe.so (test-only PTX probe).
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr $(EXTRA)
 PKG := paper_2603_18567_b200
 SRCS := $(wildcard $(PKG)/csrc/*.cu)
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/ttt_attn.h

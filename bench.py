@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""bench.py — TTT unrolled attention fwd+bwd on B200 (the driver's bench contract).
+
+One bench "step" = one TTT unroll of the EAGLE-3 draft layer attention at the
+Llama-3.1-8B draft shape (BASELINE.json configs[1]: B=8, L=2048, 32 q / 8 kv
+heads, head_dim 128, ttt_steps 7, bf16): 7 forward calls (j = 0..6) then 7
+backward calls (j = 6..0, the first overwriting, the rest accumulating
+dK/dV), all through the C-ABI (libtttattn.so). At N > 1 GPUs each rank runs
+the same per-GPU unroll on its own sequences (data parallel by sequence, weak
+scaling) and the draft-layer gradient bucket is all-reduced over NCCL,
+bucket i released after backward call i (DDP-style overlap).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0. See DESIGN.md §6 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2603_18567_b200.inputs import CONFIGS, Shape  # noqa: E402
+
+METRIC = "TTT attn fwd+bwd tokens/sec (Llama-3.1-8B EAGLE-3 draft shape, ttt_steps=7)"
+UNIT = "tokens/s"
+# EAGLE-3 draft layer of Llama-3.1-8B: fc 3d->d, q/k/v/o, MLP 14336, norms, 32000 head
+DRAFT_PARAMS = 424_700_000
+
+
+def alg_pairs(s: Shape, seq_lens=None):
+    """Allowed (q, k) pairs of one unroll, all b and q-heads:
+    per (b, h, step j): T(T+1)/2 + (L-T)T + j*T."""
+    L = s.seq_len
+    lens = [L] * s.batch if seq_lens is None else list(seq_lens)
+    base = sum(T * (T + 1) // 2 + (L - T) * T for T in lens)
+    diag = sum(lens)
+    per_step = [s.num_q_heads * (base + j * diag) for j in range(s.ttt_steps)]
+    base_only = s.num_q_heads * base
+    return per_step, base_only
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- oracle legs
+def oracle_sample(shape: Shape, target_s: float, seed: int = 0):
+    """Time the fp64 CPU oracle (oracle/, test infrastructure) on a bounded
+    sample of the workload: sequence 0, all query heads, `n` evenly spaced
+    query rows per head, all ttt_steps forward + backward. The oracle's cost
+    per row is uniform (it is dense over all (j+1)L keys), so the sample
+    scales: tokens-equivalent = n rows of one sequence with all heads."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    L, Hq, Hkv, D, S = shape.seq_len, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, shape.ttt_steps
+    bf = lambda a: torch.from_numpy(a).to(torch.bfloat16).float().numpy()
+    q = [bf(rng.standard_normal((1, L, Hq, D), dtype=np.float32)) for _ in range(S)]
+    do = [bf(rng.standard_normal((1, L, Hq, D), dtype=np.float32)) for _ in range(S)]
+    kb = bf(rng.standard_normal((1, L, Hkv, D), dtype=np.float32))
+    vb = bf(rng.standard_normal((1, L, Hkv, D), dtype=np.float32))
+    ks = [bf(rng.standard_normal((1, L, Hkv, D), dtype=np.float32)) for _ in range(S - 1)]
+    vs = [bf(rng.standard_normal((1, L, Hkv, D), dtype=np.float32)) for _ in range(S - 1)]
+    threads = oracle.default_threads()
+
+    def run(n_rows):
+        sel = np.zeros((1, Hq, L), dtype=bool)
+        sel[:, :, np.linspace(0, L - 1, n_rows).astype(int)] = True
+        t0 = time.perf_counter()
+        for j in range(S):
+            oracle.fwd(q[j], kb, vb, ks[:j], vs[:j], row_sel=sel, nthreads=threads)
+        for j in reversed(range(S)):
+            oracle.bwd(q[j], kb, vb, ks[:j], vs[:j], do[j], row_sel=sel, nthreads=threads)
+        return time.perf_counter() - t0
+
+    t1 = run(1)  # calibration: one row per head
+    n = int(max(1, min(L, target_s / max(t1, 1e-6))))
+    return n, threads, run
+
+
+def run_reference(args, shape: Shape, rank: int, world: int):
+    """--impl reference: the oracle as it stands, timed on this box's host cores."""
+    if rank != 0:
+        return
+    n, threads, run = oracle_sample(shape, target_s=2.0)
+    for _ in range(args.warmup):
+        run(n)
+    times = [run(n) for _ in range(args.steps)]
+    sec = sum(times) / len(times)
+    value = n / sec
+    sample = (f"sequence 0 of {shape.batch}, all {shape.num_q_heads} q heads, {n} of {shape.seq_len} rows, "
+              f"all {shape.ttt_steps} TTT steps fwd+bwd (dense fp64 oracle); tokens-equivalent = {n} per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(shape, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(shape: Shape, world: int):
+    return {"workload": "llama3.1-8b-eagle3-draft TTT attention unroll (fwd j=0..6 + bwd j=6..0)",
+            "batch_per_gpu": shape.batch, "global_batch": shape.batch * world, "seq_len": shape.seq_len,
+            "num_q_heads": shape.num_q_heads, "num_kv_heads": shape.num_kv_heads, "head_dim": shape.head_dim,
+            "ttt_steps": shape.ttt_steps, "seq_lens": "full (T_b = L)", "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2 (~5 GB touched per step vs 126 MB L2); no flush"}
+
+
+# --------------------------------------------------------------------------- our arm
+class Unroll:
+    """Device buffers of one per-GPU unroll + the C-ABI calls of one step."""
+
+    def __init__(self, shape: Shape, seed: int, dev):
+        import paper_2603_18567_b200 as ttt
+        self.ttt = ttt
+        self.s = s = shape
+        S = s.ttt_steps
+        g = torch.Generator(device=dev).manual_seed(seed)
+        mk = lambda shp: torch.randn(shp, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
+        self.q = [mk(s.q_shape) for _ in range(S)]
+        self.do = [mk(s.q_shape) for _ in range(S)]
+        self.k, self.v = mk(s.kv_shape), mk(s.kv_shape)
+        self.ks = [mk(s.kv_shape) for _ in range(S - 1)]
+        self.vs = [mk(s.kv_shape) for _ in range(S - 1)]
+        self.out = [torch.empty(s.q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
+        self.lse = [torch.empty(s.batch, s.num_q_heads, s.seq_len, device=dev) for _ in range(S)]
+        self.dq = [torch.empty(s.q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
+        z = lambda: torch.zeros(s.kv_shape, dtype=torch.float32, device=dev)
+        self.dk, self.dv = z(), z()
+        self.dks = [z() for _ in range(S - 1)]
+        self.dvs = [z() for _ in range(S - 1)]
+        self.desc = ttt.make_desc(s.batch, s.seq_len, s.num_q_heads, s.num_kv_heads, s.head_dim)
+        self.ws = torch.empty(ttt.ttt_attn_workspace_size(self.desc, S - 1, True), dtype=torch.uint8, device=dev)
+        self.inputs = self.q + self.do + [self.k, self.v] + self.ks + self.vs
+
+    def step(self, stream, on_bwd=None):
+        t, s = self.ttt, self.s
+        S = s.ttt_steps
+        for j in range(S):
+            t.ttt_attn_fwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, self.out[j], self.lse[j],
+                           stream=stream)
+        for j in reversed(range(S)):
+            t.ttt_attn_bwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, self.out[j], self.lse[j],
+                           self.do[j], self.dq[j], self.dk, self.dv, self.dks, self.dvs,
+                           flags=0 if j == S - 1 else t.TTT_ACCUMULATE_DKV, workspace=self.ws, stream=stream)
+            if on_bwd is not None:
+                on_bwd(S - 1 - j)
+
+
+def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
+    import paper_2603_18567_b200 as ttt
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    u = Unroll(shape, seed=1234 + rank, dev=dev)
+    stream = torch.cuda.current_stream(dev)
+    S = shape.ttt_steps
+
+    # draft-layer gradient bucket (synthetic stand-in), bf16, split per bwd call
+    buckets, works = [], []
+    if world > 1:
+        grad = torch.randn(DRAFT_PARAMS, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        buckets = list(torch.chunk(grad, S))
+
+    def on_bwd(i):
+        if world > 1:
+            works.append(dist.all_reduce(buckets[i], op=dist.ReduceOp.AVG, async_op=True))
+
+    def one_step():
+        u.step(stream, on_bwd)
+        while works:
+            works.pop().wait()
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region ----------------
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        wall = time.perf_counter() - w0
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    ms_per_step = ms / args.steps
+    tokens_per_step = shape.batch * shape.seq_len * world
+    value = tokens_per_step / (ms_per_step / 1e3)
+
+    # ---------------- per-kernel attribution (separate pass, CUDA events on the launch stream) ----------
+    prof_steps = 2
+    ttt.ttt_attn_profile_begin()
+    for _ in range(prof_steps):
+        one_step()
+    torch.cuda.synchronize()
+    kern = ttt.ttt_attn_profile_end()
+    launches_per_step = sum(n for _, n in kern.values()) // prof_steps
+
+    peaks = load_peaks()
+    per_step_pairs, base_pairs = alg_pairs(shape)
+    D = shape.head_dim
+    flops_step = 12 * D * sum(per_step_pairs)  # algorithmic: fwd 4D + bwd 8D per allowed pair
+    tflops = flops_step * world / (ms_per_step / 1e3) / 1e12 / world  # per GPU
+    # dominant kernel -> roofline
+    dom = max(kern.items(), key=lambda kv: kv[1][0])
+    dom_name, (dom_ms, dom_n) = dom
+    per_launch_flops = {
+        "ttt_bwd_sm100_kernel": 8 * D * base_pairs,   # dV, dP, dK, dQ over the base (causal) pairs
+        "ttt_fwd_sm100_kernel": 4 * D * base_pairs,   # QK^T, PV over the base pairs
+    }
+    roof = None
+    if dom_name in per_launch_flops:
+        avg_ms = dom_ms / dom_n
+        achieved = per_launch_flops[dom_name] / (avg_ms / 1e3) / 1e12
+        peak = peaks["bf16_tflops_sustained"]
+        roof = {"kernel": dom_name, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "peak_kind": f"bf16 sustained ({peaks['source']}, MEASURED_PEAKS.json)",
+                "frac_of_burst": achieved / peaks["bf16_tflops"], "avg_launch_ms": avg_ms,
+                "share_of_step": dom_ms / prof_steps / ms_per_step if world == 1 else None,
+                "traffic": ncu_traffic(dom_name), "algorithmic_flops_per_launch": per_launch_flops[dom_name]}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch Philox N(0,1) -> bf16, random per rank)",
+        "config": workload_config(shape, world),
+        "tflops_per_gpu": tflops, "frac_of_bf16_peak": tflops / peaks["bf16_tflops_sustained"],
+        "frac_of_bf16_burst_peak": tflops / peaks["bf16_tflops"],
+        "flops_convention": "algorithmic 12*D per allowed (q,k) pair (fwd 4D + bwd 8D; recompute excluded)",
+        "roofline": roof,
+        "kernels_ms_per_step": {k: v[0] / prof_steps for k, v in kern.items()},
+        "gpu_launches": launches_per_step * args.steps,
+        "wall_s_timed_region": wall,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_e2e:
+        line["e2e"] = run_e2e(u, stream, args, shape)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n, threads, run = oracle_sample(shape, target_s=12.0)
+        sec = run(n)
+        line["cpu_baseline"] = {
+            "value": n / sec, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": (f"sequence 0 of {shape.batch}, all {shape.num_q_heads} q heads, {n} of {shape.seq_len} rows, "
+                       f"all {shape.ttt_steps} TTT steps fwd+bwd (dense fp64 oracle, {sec:.1f} s); "
+                       f"tokens-equivalent = {n}")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(u: Unroll, stream, args, shape: Shape):
+    """Same metric through the public API with host buffers: every step copies
+    the unroll's inputs H2D from pinned memory and reads the accumulated base
+    gradients dK_0, dV_0 back D2H (the unroll's result), copies included."""
+    host_in = [t.cpu().pin_memory() for t in u.inputs]
+    host_out = [torch.empty(u.dk.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+    h2d = sum(t.numel() * t.element_size() for t in host_in)
+    d2h = sum(t.numel() * t.element_size() for t in host_out)
+    n = max(2, min(args.steps, 5))
+
+    def step():
+        for d, h in zip(u.inputs, host_in):
+            d.copy_(h, non_blocking=True)
+        u.step(stream)
+        host_out[0].copy_(u.dk, non_blocking=True)
+        host_out[1].copy_(u.dv, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    return {"value": shape.batch * shape.seq_len / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n}
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="llama8b", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # contract: W >= 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    shape = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, shape, rank, world)
+        return
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, shape, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

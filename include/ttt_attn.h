@@ -127,6 +127,20 @@ int ttt_attn_bwd(const ttt_attn_desc* desc, int step,
                  float* const* dk_steps, float* const* dv_steps,
                  unsigned flags, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Optional instrumentation (off by default; used by bench.py) ----------
+ * ttt_attn_profile_begin() arms per-kernel timing for the CALLING HOST THREAD:
+ * each kernel the library launches afterwards is bracketed by cudaEventRecord
+ * on its launch stream (events come from a library-owned pool of up to 4096
+ * pairs). ttt_attn_profile_end() synchronises on those events, writes the
+ * summed device milliseconds and launch counts per kernel kind into the
+ * caller's arrays (n_kinds entries, kinds listed by ttt_attn_kernel_name),
+ * and disarms. Returns the number of kinds filled, or < 0 on error.
+ * This is the only library state; computations never depend on it. */
+#define TTT_KERNEL_KINDS 8
+int ttt_attn_profile_begin(void);
+int ttt_attn_profile_end(double* ms_by_kind, int* launches_by_kind, int n_kinds);
+const char* ttt_attn_kernel_name(int kind);
+
 /* Static string for a ttt_status code. */
 const char* ttt_attn_strerror(int code);
 

@@ -9,5 +9,5 @@ data-parallel harness. Importing it without the built library raises.
 from ._lib import (  # noqa: F401
     TTT_ACCUMULATE_DKV, TTT_BF16, TTT_FP32_CHECK, TTT_MAX_BATCH, TTT_MAX_STEPS, Desc, TTTError,
     desc_for, make_desc, ttt_attn_bwd, ttt_attn_fwd, ttt_attn_strerror, ttt_attn_version,
-    ttt_attn_workspace_size,
+    ttt_attn_workspace_size, ttt_attn_profile_begin, ttt_attn_profile_end, ttt_attn_kernel_name,
 )

@@ -60,6 +60,12 @@ def _load():
     lib.ttt_attn_strerror.restype = ctypes.c_char_p
     lib.ttt_attn_version.argtypes = []
     lib.ttt_attn_version.restype = ctypes.c_char_p
+    lib.ttt_attn_profile_begin.argtypes = []
+    lib.ttt_attn_profile_begin.restype = i
+    lib.ttt_attn_profile_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), i]
+    lib.ttt_attn_profile_end.restype = i
+    lib.ttt_attn_kernel_name.argtypes = [i]
+    lib.ttt_attn_kernel_name.restype = ctypes.c_char_p
     return lib
 
 
@@ -117,6 +123,30 @@ def _stream(stream) -> ctypes.c_void_p:
 def _check(code: int):
     if code != 0:
         raise TTTError(code, ttt_attn_strerror(code))
+
+
+TTT_KERNEL_KINDS = 8
+
+
+def ttt_attn_kernel_name(kind: int) -> str:
+    return _lib.ttt_attn_kernel_name(int(kind)).decode()
+
+
+def ttt_attn_profile_begin() -> None:
+    """Arm per-kernel CUDA-event timing for this host thread (include/ttt_attn.h)."""
+    rc = _lib.ttt_attn_profile_begin()
+    if rc < 0:
+        _check(-rc)
+
+
+def ttt_attn_profile_end() -> dict:
+    """Disarm; return {kernel_name: (total_ms, launches)} for kinds that ran."""
+    ms = (ctypes.c_double * TTT_KERNEL_KINDS)()
+    n = (ctypes.c_int * TTT_KERNEL_KINDS)()
+    rc = _lib.ttt_attn_profile_end(ms, n, TTT_KERNEL_KINDS)
+    if rc < 0:
+        _check(-rc)
+    return {ttt_attn_kernel_name(k): (ms[k], n[k]) for k in range(rc) if n[k] > 0}
 
 
 def ttt_attn_workspace_size(desc: Desc, step: int, is_bwd: bool) -> int:

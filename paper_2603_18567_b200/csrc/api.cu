@@ -104,7 +104,40 @@ BwdWs bwd_ws_layout(const ttt_attn_desc* d) {
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? TTT_OK : TTT_ERR_CUDA; }
 
+// ---- instrumentation: library-owned event pool, armed per host thread ----
+constexpr int kProfPairs = 4096;
+struct ProfRec {
+  int kind;
+  int slot;
+};
+struct ProfState {
+  bool armed = false;
+  int used = 0;
+  int pending_kind = -1;
+  cudaEvent_t ev[2 * kProfPairs];
+  bool created = false;
+  ProfRec rec[kProfPairs];
+};
+thread_local ProfState g_prof;
+
 }  // namespace
+
+namespace tttk {
+void prof_mark(int kind, bool start, cudaStream_t st) {
+  ProfState& P = g_prof;
+  if (!P.armed) return;
+  if (start) {
+    if (P.used >= kProfPairs) return;
+    P.pending_kind = kind;
+    cudaEventRecord(P.ev[2 * P.used], st);
+  } else if (P.pending_kind == kind && P.used < kProfPairs) {
+    cudaEventRecord(P.ev[2 * P.used + 1], st);
+    P.rec[P.used] = {kind, P.used};
+    ++P.used;
+    P.pending_kind = -1;
+  }
+}
+}  // namespace tttk
 
 extern "C" {
 
@@ -120,6 +153,48 @@ const char* ttt_attn_strerror(int code) {
     case TTT_ERR_CUDA: return "CUDA error";
     default: return "unknown error";
   }
+}
+
+int ttt_attn_profile_begin(void) {
+  ProfState& P = g_prof;
+  if (!P.created) {
+    for (int i = 0; i < 2 * kProfPairs; ++i)
+      if (cudaEventCreate(&P.ev[i]) != cudaSuccess) return -TTT_ERR_CUDA;
+    P.created = true;
+  }
+  P.used = 0;
+  P.pending_kind = -1;
+  P.armed = true;
+  return 0;
+}
+
+int ttt_attn_profile_end(double* ms_by_kind, int* launches_by_kind, int n_kinds) {
+  ProfState& P = g_prof;
+  if (!P.armed) return -TTT_ERR_INVALID_ARG;
+  P.armed = false;
+  const int nk = n_kinds < TTT_KERNEL_KINDS ? n_kinds : TTT_KERNEL_KINDS;
+  for (int k = 0; k < nk; ++k) {
+    if (ms_by_kind) ms_by_kind[k] = 0.0;
+    if (launches_by_kind) launches_by_kind[k] = 0;
+  }
+  for (int i = 0; i < P.used; ++i) {
+    if (cudaEventSynchronize(P.ev[2 * i + 1]) != cudaSuccess) return -TTT_ERR_CUDA;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, P.ev[2 * i], P.ev[2 * i + 1]) != cudaSuccess) return -TTT_ERR_CUDA;
+    const int k = P.rec[i].kind;
+    if (k < nk) {
+      if (ms_by_kind) ms_by_kind[k] += ms;
+      if (launches_by_kind) launches_by_kind[k] += 1;
+    }
+  }
+  return nk;
+}
+
+const char* ttt_attn_kernel_name(int kind) {
+  static const char* names[TTT_KERNEL_KINDS] = {
+      "ttt_fwd_diag_kernel", "ttt_fwd_sm100_kernel", "ttt_bwd_pre_kernel", "ttt_bwd_sm100_kernel",
+      "ttt_bwd_dq_convert_kernel", "fwd_check_kernel", "bwd_check_kernel", "zero_f32_kernel"};
+  return (kind >= 0 && kind < TTT_KERNEL_KINDS) ? names[kind] : "unknown";
 }
 
 const char* ttt_attn_version(void) { return "libtttattn 0.1 sm_100a (tcgen05/TMEM/TMA + fp32 check path)"; }

@@ -405,17 +405,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ---- dK, dV accumulators -> global (fp32 atomics: head splits and steps add up) ----
     mbar_wait(&bars.acc_full, 0);
     tc_fence_after();
-    if (k < T) {
-      const size_t off = (((size_t)b * p.L + k) * p.Hkv + g) * D;
+    // tcgen05.ld is warp-collective (.sync.aligned): every lane loads, only rows k < T store
+    const bool store = k < T;
+    const size_t off = (((size_t)b * p.L + (store ? k : 0)) * p.Hkv + g) * D;
 #pragma unroll 1
-      for (int c0 = 0; c0 < D; c0 += 32) {
-        uint32_t raw[32];
-        tmem_ld32(tbase + lane_off + 256 + c0, raw);
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t raw[32];
+      tmem_ld32(tbase + lane_off + 256 + c0, raw);
+      if (store) {
 #pragma unroll
         for (int e = 0; e < 32; e += 4)
           red_add_v4(p.dv + off + c0 + e, __uint_as_float(raw[e]), __uint_as_float(raw[e + 1]),
                      __uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3]));
-        tmem_ld32(tbase + lane_off + 384 + c0, raw);
+      }
+      tmem_ld32(tbase + lane_off + 384 + c0, raw);
+      if (store) {
         const float c = p.scale;
 #pragma unroll
         for (int e = 0; e < 32; e += 4)
@@ -493,7 +497,9 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
                                            (int)smem);
       if (e != cudaSuccess) return e;
     }
+    prof_mark(kKindBwdPre, true, st);
     ttt_bwd_pre_kernel<D><<<(unsigned)((warps + 3) / 4), 128, smem, st>>>(p);
+    prof_mark(kKindBwdPre, false, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -508,7 +514,9 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
       attr_set = true;
     }
     const int grid = p.nqt * p.B * p.Hkv * p.head_split;
+    prof_mark(kKindBwdMain, true, st);
     ttt_bwd_sm100_kernel<D><<<grid, kBwdThreads, smem, st>>>(p, maps);
+    prof_mark(kKindBwdMain, false, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -517,7 +525,9 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
     const size_t n8 = (size_t)p.B * p.L * p.Hq * D / 8;
     unsigned blocks = (unsigned)((n8 + 255) / 256);
     if (blocks > 148u * 8u) blocks = 148u * 8u;
+    prof_mark(kKindBwdConvert, true, st);
     ttt_bwd_dq_convert_kernel<<<blocks, 256, 0, st>>>(p.dq_acc, reinterpret_cast<__nv_bfloat16*>(p.dq), n8);
+    prof_mark(kKindBwdConvert, false, st);
     return cudaGetLastError();
   }
 }

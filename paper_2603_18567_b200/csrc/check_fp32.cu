@@ -141,23 +141,29 @@ cudaError_t launch_zero_f32(float* x, size_t n, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
+  prof_mark(kKindZero, true, st);
   zero_f32_kernel<<<blocks, 256, 0, st>>>(x, n);
+  prof_mark(kKindZero, false, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fwd_check(const Params& p, cudaStream_t st) {
   const long rows = (long)p.B * p.Hq * p.L;
   const int blocks = (int)((rows + 7) / 8);
+  prof_mark(kKindCheckFwd, true, st);
   if (p.D == 64) fwd_check_kernel<64><<<blocks, 256, 0, st>>>(p);
   else fwd_check_kernel<128><<<blocks, 256, 0, st>>>(p);
+  prof_mark(kKindCheckFwd, false, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd_check(const Params& p, cudaStream_t st) {
   const long rows = (long)p.B * p.Hq * p.L;
   const int blocks = (int)((rows + 7) / 8);
+  prof_mark(kKindCheckBwd, true, st);
   if (p.D == 64) bwd_check_kernel<64><<<blocks, 256, 0, st>>>(p);
   else bwd_check_kernel<128><<<blocks, 256, 0, st>>>(p);
+  prof_mark(kKindCheckBwd, false, st);
   return cudaGetLastError();
 }
 

@@ -377,11 +377,15 @@ cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, cudaStream_t st) 
   }
   if (p.step > 0) {
     const long warps = (long)p.B * p.L * p.Hkv;
+    prof_mark(kKindFwdDiag, true, st);
     ttt_fwd_diag_kernel<D><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(p);
+    prof_mark(kKindFwdDiag, false, st);
   }
   const int npairs = (p.G + 1) / 2;
   const int grid = p.nqt * p.B * p.Hkv * npairs;
+  prof_mark(kKindFwdMain, true, st);
   ttt_fwd_sm100_kernel<D><<<grid, kFwdThreads, smem, st>>>(p, maps);
+  prof_mark(kKindFwdMain, false, st);
   return cudaGetLastError();
 }
 

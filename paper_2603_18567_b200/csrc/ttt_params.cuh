@@ -4,6 +4,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
+#include <cuda_runtime.h>
 
 #include "../../include/ttt_attn.h"
 
@@ -49,5 +50,13 @@ struct FwdMaps {
 struct BwdMaps {
   CUtensorMap q, k, v, dout;
 };
+
+// Instrumentation hook (api.cu): brackets one kernel launch with events when
+// ttt_attn_profile_begin() armed the calling thread; no-op otherwise.
+enum KernelKind {
+  kKindFwdDiag = 0, kKindFwdMain = 1, kKindBwdPre = 2, kKindBwdMain = 3,
+  kKindBwdConvert = 4, kKindCheckFwd = 5, kKindCheckBwd = 6, kKindZero = 7
+};
+void prof_mark(int kind, bool start, cudaStream_t st);
 
 }  // namespace tttk
