@@ -1,5 +1,6 @@
-"""Quick per-step kernel timing (dev tool, not the bench contract)."""
-import sys, os, time
+"""Per-step, per-kernel timing of one unroll (dev tool, not the bench contract).
+usage: python bench_tools/time_kernels.py [config] [bwd]"""
+import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2603_18567_b200 as ttt
@@ -21,31 +22,39 @@ z = lambda: torch.zeros(s.kv_shape, device=dev)
 dk, dv = z(), z(); dks = [z() for _ in range(S - 1)]; dvs = [z() for _ in range(S - 1)]
 ws = torch.empty(ttt.ttt_attn_workspace_size(desc, S - 1, True), dtype=torch.uint8, device=dev)
 tot_f = tot_b = 0.0
-for j in range(S):
-    pairs = B * Hq * (L * (L + 1) / 2 + j * L)
+fwd = lambda j: ttt.ttt_attn_fwd(desc, j, q, k, v, ks, vs, out, lse)
+bwd = lambda j: ttt.ttt_attn_bwd(desc, j, q, k, v, ks, vs, out, lse, do, dq, dk, dv, dks, dvs, flags=1, workspace=ws)
+
+
+def timeit(fn, n=10):
     for _ in range(3):
-        ttt.ttt_attn_fwd(desc, j, q, k, v, ks, vs, out, lse)
+        fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    n = 10
     e0.record()
     for _ in range(n):
-        ttt.ttt_attn_fwd(desc, j, q, k, v, ks, vs, out, lse)
+        fn()
     e1.record(); torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / n
+    ttt.ttt_attn_profile_begin()
+    fn()
+    torch.cuda.synchronize()
+    kern = ttt.ttt_attn_profile_end()
+    return e0.elapsed_time(e1) / n, kern
+
+
+for j in range(S):
+    pairs = B * Hq * (L * (L + 1) / 2 + j * L)
+    base = B * Hq * L * (L + 1) / 2
+    ms, kern = timeit(lambda: fwd(j))
     tot_f += ms
-    msg = f"{cfg} j={j} fwd {ms:.3f} ms {4*D*pairs/ms/1e9:.1f} TFLOP/s"
+    km = " ".join(f"{n.replace('ttt_','').replace('_kernel','')}={v[0]:.3f}" for n, v in kern.items())
+    msg = f"{cfg} j={j} fwd {ms:.3f} ms {4*D*pairs/ms/1e9:.1f} TFLOP/s [{km}]"
     if do_bwd:
-        for _ in range(2):
-            ttt.ttt_attn_bwd(desc, j, q, k, v, ks, vs, out, lse, do, dq, dk, dv, dks, dvs, flags=1, workspace=ws)
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(n):
-            ttt.ttt_attn_bwd(desc, j, q, k, v, ks, vs, out, lse, do, dq, dk, dv, dks, dvs, flags=1, workspace=ws)
-        e1.record(); torch.cuda.synchronize()
-        msb = e0.elapsed_time(e1) / n
+        msb, kern = timeit(lambda: bwd(j))
         tot_b += msb
-        msg += f" | bwd {msb:.3f} ms {8*D*pairs/msb/1e9:.1f} TFLOP/s"
+        mm = kern.get("ttt_bwd_sm100_kernel", (0, 1))[0]
+        km = " ".join(f"{n.replace('ttt_','').replace('_kernel','')}={v[0]:.3f}" for n, v in kern.items())
+        msg += f" | bwd {msb:.3f} ms {8*D*pairs/msb/1e9:.1f} TFLOP/s [{km}] main {8*D*base/mm/1e9:.0f} TF/s"
     print(msg, flush=True)
 P = B * Hq * (S * L * (L + 1) / 2 + L * S * (S - 1) / 2)
 print(f"unroll fwd {tot_f:.3f} ms ({4*D*P/tot_f/1e9:.1f} TFLOP/s)" + (f" bwd {tot_b:.3f} ms ({8*D*P/tot_b/1e9:.1f}) total {12*D*P/(tot_f+tot_b)/1e9:.1f} TFLOP/s" if do_bwd else ""))

@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtttattn.so")
+LIB_PATH = os.environ.get("TTT_ATTN_LIB") or os.path.join(_HERE, "libtttattn.so")  # env: dev A/B builds only
 
 TTT_BF16 = 0
 TTT_FP32_CHECK = 1

@@ -53,6 +53,19 @@ bool encode_bshd(CUtensorMap* m, const void* ptr, int B, int L, int H, int D) {
   return r == CUDA_SUCCESS;
 }
 
+// tiled fp32 dq accumulator as a 2-D tensor {32, rows}: box {32, 32} (4 KB), 128B swizzle.
+bool encode_dqacc(CUtensorMap* m, void* ptr, size_t rows) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {32, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {32 * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int validate_desc(const ttt_attn_desc* d, int step) {
@@ -299,7 +312,8 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
   p.dq_acc = reinterpret_cast<float*>(ws + w.dq_acc);
   BwdMaps maps;
   if (!encode_bshd(&maps.q, q, p.B, p.L, p.Hq, p.D) || !encode_bshd(&maps.k, k_base, p.B, p.L, p.Hkv, p.D) ||
-      !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D) || !encode_bshd(&maps.dout, dout, p.B, p.L, p.Hq, p.D))
+      !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D) || !encode_bshd(&maps.dout, dout, p.B, p.L, p.Hq, p.D) ||
+      !encode_dqacc(&maps.dqacc, p.dq_acc, (size_t)p.B * p.L * p.Hq * p.D / 32))
     return TTT_ERR_CUDA;
   return cuda_status(launch_bwd_sm100(p, maps, s));
 }

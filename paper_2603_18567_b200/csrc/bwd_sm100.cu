@@ -15,8 +15,9 @@
 //       S^T = K Q^T, dP^T = V dO^T                         (SS MMAs, TMEM)
 //       P^T = exp2(S^T c log2e - lse2), dS^T = P^T o (dP^T - Delta)   (compute warps)
 //       dV += P^T dO, dK += dS^T Q                         (A operand from TMEM)
-//       dQ  = dS K  -> red.global.add into dq_acc           (A = dS from smem)
+//       dQ  = dS K  -> TMA reduce-add into dq_acc           (A = dS from smem)
 //  3. ttt_bwd_dq_convert_kernel: dq = bf16(dq_acc).
+// dq_acc is a tile-contiguous fp32 workspace (see dqacc_index) reduced into by TMA.
 //
 // Warp roles of the main kernel (320 threads):
 //   warps 0-3 compute (thread = key row, TMEM lanes 0-127), warps 4-7 dQ drain
@@ -24,6 +25,8 @@
 // TMEM columns: S^T/P^T [0,128) dP^T/dS^T/dQ [128,256) dV [256,256+D) dK [384,384+D).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "ptx_sm100.cuh"
 #include "ttt_params.cuh"
@@ -55,100 +58,132 @@ __device__ __forceinline__ void load_bf16(const void* base, size_t off, float (&
   }
 }
 
+// dq_acc workspace layout (tile-contiguous so a warp's 32 rows x 32 columns of a
+// dQ tile are one 4 KB block the TMA reduce-add writes in full 128 B lines):
+//   [B][Hq][L/128][D/32][128 rows][32 cols] fp32
+__device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int r, int d) {
+  const int nc = p.D / 32;
+  return ((((size_t)(b * p.Hq + h) * p.nqt + (r >> 7)) * nc + (d >> 5)) * 128 + (r & 127)) * 32 + (d & 31);
+}
+
 // ------------------------------------------------------------------ kernel 1
+// One HALF-warp per (b, r, kv head g): 16 lanes x (D/16) contiguous elements,
+// 16-byte loads, 4-level shuffle reductions. Rows per block = 2 * warps.
+// One HALF-warp per (b, r, kv head g): 16 lanes x (D/16) contiguous elements,
+// 16-byte loads, 4-level shuffle reductions. Rows per block = 2 * warps.
 template <int D>
-__global__ void __launch_bounds__(128) ttt_bwd_pre_kernel(const __grid_constant__ Params p) {
-  constexpr int E = D / 32;
+__global__ void __launch_bounds__(256) ttt_bwd_pre_kernel(const __grid_constant__ Params p, int rows_per_block) {
+  constexpr int E = D / 16;
   extern __shared__ float pre_smem[];
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const long wid = (long)blockIdx.x * 4 + wl;
-  if (wid >= (long)p.B * p.L * p.Hkv) return;
+  const int lane = threadIdx.x & 31, hl = lane & 15;
+  const int lrow = threadIdx.x >> 4;  // row slot within the block
+  const long wid = (long)blockIdx.x * rows_per_block + lrow;
+  const long nrows = (long)p.B * p.L * p.Hkv;
+  const bool valid = wid < nrows;
+  const long w = valid ? wid : nrows - 1;  // clamp: shuffles stay warp-uniform
   const int G = p.G;
-  const int g = (int)(wid % p.Hkv);
-  const int r = (int)((wid / p.Hkv) % p.L);
-  const int b = (int)(wid / ((long)p.Hkv * p.L));
+  const int g = (int)(w % p.Hkv);
+  const int r = (int)((w / p.Hkv) % p.L);
+  const int b = (int)(w / ((long)p.Hkv * p.L));
   const int T = p.seq_lens[b];
-  float* sdq = pre_smem + (size_t)wl * (G * D + 2 * G);  // [G][D]
-  float* sdel = sdq + G * D;                              // [G]
-  float* sl2 = sdel + G;                                  // [G]
-  const size_t kv_off = (((size_t)b * p.L + r) * p.Hkv + g) * D + lane * E;
+  float* sdq = pre_smem + (size_t)lrow * (G * D + 2 * G);  // [G][D] dq accumulators
+  float* sdel = sdq + G * D;
+  float* sl2 = sdel + G;
+  const size_t kv_off = (((size_t)b * p.L + r) * p.Hkv + g) * D + hl * E;
 
   for (int hh = 0; hh < G; ++hh) {
     const int h = g * G + hh;
-    const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + lane * E;
+    const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + hl * E;
     float o[E], d[E];
-    load_bf16<E>(p.o, q_off, o);
-    load_bf16<E>(p.dout, q_off, d);
+    ld_row<D>(p.o, q_off, o);
+    ld_row<D>(p.dout, q_off, d);
     float acc = 0.f;
 #pragma unroll
     for (int e = 0; e < E; ++e) acc = fmaf(o[e], d[e], acc);
-    const float delta = warp_allsum(acc);  // Delta_r = dO_r . O_r
+    const float delta = half_allsum(acc);  // Delta_r = dO_r . O_r
     const size_t li = ((size_t)b * p.Hq + h) * p.L + r;
     const float l2 = p.lse_in[li] * kLog2e;
-    if (lane == 0) {
-      p.delta[li] = delta;
-      p.lse2[li] = l2;
+    if (hl == 0) {
+      if (valid) {
+        p.delta[li] = delta;
+        p.lse2[li] = l2;
+      }
       sdel[hh] = delta;
       sl2[hh] = l2;
     }
 #pragma unroll
-    for (int e = 0; e < E; ++e) sdq[hh * D + lane * E + e] = 0.f;
+    for (int e = 0; e < E; ++e) sdq[hh * D + hl * E + e] = 0.f;
   }
   __syncwarp();
-  if (!p.accumulate) {
+  if (valid && !p.accumulate) {
+    float4* dk4 = reinterpret_cast<float4*>(p.dk + kv_off);
+    float4* dv4 = reinterpret_cast<float4*>(p.dv + kv_off);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      p.dk[kv_off + e] = 0.f;
-      p.dv[kv_off + e] = 0.f;
+    for (int e = 0; e < E / 4; ++e) {
+      dk4[e] = z;
+      dv4[e] = z;
     }
   }
-  const int nd = r < T ? p.step : 0;
+  const bool act = valid && (r < T);  // diagonal keys exist only for rows r < T_b (Alg. 2 m_pad)
   for (int i = 0; i < p.step; ++i) {
-    float dk[E], dv[E];
+    float dk[E], dv[E], kk[E], vv[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) dk[e] = dv[e] = 0.f;
-    if (i < nd) {
-      float kk[E], vv[E];
-      load_bf16<E>(p.ks[i], kv_off, kk);
-      load_bf16<E>(p.vs[i], kv_off, vv);
-      for (int hh = 0; hh < G; ++hh) {
-        const int h = g * G + hh;
-        const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + lane * E;
-        float qq[E], dd[E];
-        load_bf16<E>(p.q, q_off, qq);
-        load_bf16<E>(p.dout, q_off, dd);
-        float s = 0.f, dp = 0.f;
+    ld_row<D>(p.ks[i], kv_off, kk);
+    ld_row<D>(p.vs[i], kv_off, vv);
+    for (int hh = 0; hh < G; ++hh) {
+      const int h = g * G + hh;
+      const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + hl * E;
+      float qq[E], dd[E];
+      ld_row<D>(p.q, q_off, qq);
+      ld_row<D>(p.dout, q_off, dd);
+      float s = 0.f, dp = 0.f;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          s = fmaf(qq[e], kk[e], s);
-          dp = fmaf(dd[e], vv[e], dp);
-        }
-        s = warp_allsum(s);
-        dp = warp_allsum(dp);
-        const float pr = ex2(s * p.scale_log2 - sl2[hh]);  // p_i = exp(c q.k_i - lse)
-        const float ds = pr * (dp - sdel[hh]);             // ds_i = p_i (dp_i - Delta)
+      for (int e = 0; e < E; ++e) {
+        s = fmaf(qq[e], kk[e], s);
+        dp = fmaf(dd[e], vv[e], dp);
+      }
+      s = half_allsum(s);
+      dp = half_allsum(dp);
+      const float pr = act ? ex2(s * p.scale_log2 - sl2[hh]) : 0.f;  // p_i = exp(c q.k_i - lse)
+      const float ds = pr * (dp - sdel[hh]);                          // ds_i = p_i (dp_i - Delta)
+      const float cds = p.scale * ds;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          dk[e] = fmaf(p.scale * ds, qq[e], dk[e]);
-          dv[e] = fmaf(pr, dd[e], dv[e]);
-          sdq[hh * D + lane * E + e] = fmaf(p.scale * ds, kk[e], sdq[hh * D + lane * E + e]);
-        }
+      for (int e = 0; e < E; ++e) {
+        dk[e] = fmaf(cds, qq[e], dk[e]);
+        dv[e] = fmaf(pr, dd[e], dv[e]);
+        sdq[hh * D + hl * E + e] = fmaf(cds, kk[e], sdq[hh * D + hl * E + e]);
       }
     }
-    float* dkp = p.dks[i] + kv_off;
-    float* dvp = p.dvs[i] + kv_off;
+    if (valid) {
+      float4* dk4 = reinterpret_cast<float4*>(p.dks[i] + kv_off);
+      float4* dv4 = reinterpret_cast<float4*>(p.dvs[i] + kv_off);
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      dkp[e] = p.accumulate ? dkp[e] + dk[e] : dk[e];
-      dvp[e] = p.accumulate ? dvp[e] + dv[e] : dv[e];
+      for (int e = 0; e < E / 4; ++e) {
+        float4 a = make_float4(dk[4 * e], dk[4 * e + 1], dk[4 * e + 2], dk[4 * e + 3]);
+        float4 c = make_float4(dv[4 * e], dv[4 * e + 1], dv[4 * e + 2], dv[4 * e + 3]);
+        if (p.accumulate) {
+          const float4 a0 = dk4[e], c0 = dv4[e];
+          a.x += a0.x; a.y += a0.y; a.z += a0.z; a.w += a0.w;
+          c.x += c0.x; c.y += c0.y; c.z += c0.z; c.w += c0.w;
+        }
+        dk4[e] = a;
+        dv4[e] = c;
+      }
     }
   }
   __syncwarp();
-  for (int hh = 0; hh < G; ++hh) {
-    const int h = g * G + hh;
-    float* dst = p.dq_acc + (((size_t)b * p.L + r) * p.Hq + h) * D + lane * E;
+  if (valid) {
+    for (int hh = 0; hh < G; ++hh) {
+      const int h = g * G + hh;
+      float* dst = p.dq_acc + dqacc_index(p, b, h, r, hl * E);
 #pragma unroll
-    for (int e = 0; e < E; ++e) dst[e] = sdq[hh * D + lane * E + e];
+      for (int e = 0; e < E / 4; ++e)
+        reinterpret_cast<float4*>(dst)[e] =
+            make_float4(sdq[hh * D + hl * E + 4 * e], sdq[hh * D + hl * E + 4 * e + 1],
+                        sdq[hh * D + hl * E + 4 * e + 2], sdq[hh * D + hl * E + 4 * e + 3]);
+    }
   }
 }
 
@@ -183,18 +218,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* sDS = smem + 5 * TB;  // 128 x 128 bf16, [kv][q] in two 64-column SW128 boxes
   float* sL = reinterpret_cast<float*>(smem + 5 * TB + 32768);  // [2][128] lse2
   float* sDel = sL + 256;                                      // [2][128] Delta
+  uint8_t* sDQ = smem + 5 * TB + 32768 + 2048;                 // 4 warps x 4 KB dQ staging (SW128)
   __shared__ BwdBars bars;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hsplit = p.head_split;
   const int nh = p.G / hsplit;
-  const int per_kt = p.B * p.Hkv * hsplit;
-  const int kt = (int)blockIdx.x / per_kt;  // ascending kt = descending work (causal)
-  int rem = (int)blockIdx.x % per_kt;
-  const int b = rem / (p.Hkv * hsplit);
-  rem %= p.Hkv * hsplit;
-  const int g = rem / hsplit;
-  const int hs = rem % hsplit;
+  // (b, g, head subset)-major, kv tile fastest (ascending = longest first): the CTAs of one
+  // kv head run together, so its Q / dO tiles and dq_acc rows stay hot in L2.
+  const int kt = (int)blockIdx.x % p.nqt;
+  const int grp = (int)blockIdx.x / p.nqt;
+  const int hs = grp % hsplit;
+  const int g = (grp / hsplit) % p.Hkv;
+  const int b = grp / (hsplit * p.Hkv);
   const int T = p.seq_lens[b];
   if (kt * kTile >= T) return;  // every key of the tile is padding: no gradient flows
   const int nq = p.nqt - kt;
@@ -429,9 +465,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else {
     // ================= dQ drain (warps 4-7, thread = query row) =================
+    // TMEM -> registers (scaled by c) -> warp-private 4 KB SW128 staging -> TMA reduce-add
+    // into the tile-contiguous fp32 dq_acc (one 32 x 32 box per warp per column chunk).
     const int wq = warp - 4;
-    const int row = wq * 32 + lane;
     const uint32_t tQ = tbase + ((uint32_t)(wq * 32) << 16) + 128;
+    uint8_t* stage = sDQ + wq * 4096;
+    if (lane == 0) tma_prefetch_desc(&maps.dqacc);
     for (int i = 0; i < n_items; ++i) {
       const int h = h_first + i / nq, qt = kt + i % nq;
       mbar_wait(&bars.dq_full, i & 1);
@@ -446,10 +485,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bars.dq_empty);
-      float* dst = p.dq_acc + (((size_t)b * p.L + (size_t)qt * kTile + row) * p.Hq + h) * D;
+      const int row_base = (((b * p.Hq + h) * p.nqt + qt) * (D / 32)) * 128 + wq * 32;
 #pragma unroll
-      for (int e = 0; e < D; e += 4) red_add_v4(dst + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+      for (int cc = 0; cc < D / 32; ++cc) {
+        if (lane == 0) bulk_wait_read0();  // previous reduce finished reading the staging buffer
+        __syncwarp();
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4) {
+          float4 val = make_float4(v[cc * 32 + 4 * k4], v[cc * 32 + 4 * k4 + 1], v[cc * 32 + 4 * k4 + 2],
+                                   v[cc * 32 + 4 * k4 + 3]);
+          *reinterpret_cast<float4*>(stage + lane * 128 + ((k4 ^ (lane & 7)) << 4)) = val;
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_2d(&maps.dqacc, stage, 0, row_base + cc * 128);
+          bulk_commit();
+        }
+      }
     }
+    if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -457,19 +512,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 // ------------------------------------------------------------------ kernel 3
-__global__ void __launch_bounds__(256) ttt_bwd_dq_convert_kernel(const float* __restrict__ acc,
-                                                                 __nv_bfloat16* __restrict__ dq, size_t n8) {
+// dq[b][r][h][:] = bf16(dq_acc tiled). One thread per 8 consecutive d of one row.
+__global__ void __launch_bounds__(256) ttt_bwd_dq_convert_kernel(const __grid_constant__ Params p) {
+  const size_t n8 = (size_t)p.B * p.L * p.Hq * p.D / 8;
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const int d8 = p.D / 8;
   for (; i < n8; i += stride) {
-    const float4 a = reinterpret_cast<const float4*>(acc)[2 * i];
-    const float4 c = reinterpret_cast<const float4*>(acc)[2 * i + 1];
+    const int d = (int)(i % d8) * 8;
+    const size_t row = i / d8;  // (b*L + r)*Hq + h
+    const int h = (int)(row % p.Hq);
+    const int r = (int)((row / p.Hq) % p.L);
+    const int b = (int)(row / ((size_t)p.Hq * p.L));
+    const float4* src = reinterpret_cast<const float4*>(p.dq_acc + dqacc_index(p, b, h, r, d));
+    const float4 a = src[0], c = src[1];
     uint4 o;
     o.x = pack_bf16(a.x, a.y);
     o.y = pack_bf16(a.z, a.w);
     o.z = pack_bf16(c.x, c.y);
     o.w = pack_bf16(c.z, c.w);
-    reinterpret_cast<uint4*>(dq)[i] = o;
+    reinterpret_cast<uint4*>(p.dq)[i] = o;
   }
 }
 
@@ -490,22 +552,24 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
   p.head_split = pick_head_split(p);
   // 1. pre-pass
   {
-    const long warps = (long)p.B * p.L * p.Hkv;
-    const size_t smem = 4 * (size_t)(p.G * D + 2 * p.G) * sizeof(float);
+    const int rows_per_block = 2 * std::max(1, std::min(8, 32 / std::max(1, p.G)));
+    const size_t smem = (size_t)rows_per_block * (p.G * D + 2 * p.G) * sizeof(float);
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
       if (e != cudaSuccess) return e;
     }
+    const long rows = (long)p.B * p.L * p.Hkv;
     prof_mark(kKindBwdPre, true, st);
-    ttt_bwd_pre_kernel<D><<<(unsigned)((warps + 3) / 4), 128, smem, st>>>(p);
+    ttt_bwd_pre_kernel<D><<<(unsigned)((rows + rows_per_block - 1) / rows_per_block), rows_per_block * 16, smem, st>>>(
+        p, rows_per_block);
     prof_mark(kKindBwdPre, false, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   // 2. main tensor-core kernel
   {
-    const int smem = 5 * kTile * D * 2 + 32768 + 2048 + 1024;
+    const int smem = 5 * kTile * D * 2 + 32768 + 2048 + 16384 + 1024;
     static bool attr_set = false;
     if (!attr_set) {
       cudaError_t e =
@@ -526,7 +590,7 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
     unsigned blocks = (unsigned)((n8 + 255) / 256);
     if (blocks > 148u * 8u) blocks = 148u * 8u;
     prof_mark(kKindBwdConvert, true, st);
-    ttt_bwd_dq_convert_kernel<<<blocks, 256, 0, st>>>(p.dq_acc, reinterpret_cast<__nv_bfloat16*>(p.dq), n8);
+    ttt_bwd_dq_convert_kernel<<<blocks, 256, 0, st>>>(p);
     prof_mark(kKindBwdConvert, false, st);
     return cudaGetLastError();
   }

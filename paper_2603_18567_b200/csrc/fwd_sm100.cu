@@ -51,15 +51,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- work decode: longest (highest q tile) first -----------------------
+  // ---- work decode: (b, g)-major so one kv head's K/V stay hot in L2; within
+  // it the longest (highest) q tiles first; head pairs of a tile adjacent ----
   const int npairs = (p.G + 1) >> 1;
-  const int per_qt = p.B * p.Hkv * npairs;
-  const int qt = p.nqt - 1 - (int)blockIdx.x / per_qt;
-  int rem = (int)blockIdx.x % per_qt;
-  const int b = rem / (p.Hkv * npairs);
-  rem %= p.Hkv * npairs;
-  const int g = rem / npairs;
-  const int hp = rem % npairs;
+  const int hp = (int)blockIdx.x % npairs;
+  const int t_ = (int)blockIdx.x / npairs;
+  const int qt = p.nqt - 1 - t_ % p.nqt;
+  const int g = (t_ / p.nqt) % p.Hkv;
+  const int b = t_ / (p.nqt * p.Hkv);
   const int h0 = g * p.G + 2 * hp;
   const bool has1 = (2 * hp + 1) < p.G;
   const int T = p.seq_lens[b];
@@ -311,58 +310,66 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 }
 
 // Diagonal pre-pass (TTT-specific): for every row r < T_b
-// and query head h, t_i = c log2(e) q_r . K_i[r] (i = 1..j),
+// and query head h, t_i = c log2(e) q_r . K_i[r] (i = 1..j) reduced with an online
+// softmax over i (Alg. 1 "concat s_i"):
 //   A_d = log2 sum_i 2^{t_i},  O_d = sum_i 2^{t_i - A_d} V_i[r]
 // written into lse (log2 units) and out (bf16); the main kernel merges them.
-// HBM-streaming: one warp per (b, r, kv head g), lanes split head_dim, rows
-// read once and shared by the G query heads of the group.
+// HBM-streaming: one half-warp per (b, r, kv head g), 16-byte loads; the
+// K_i / V_i rows are read once per group and shared by its G query heads.
 template <int D>
 __global__ void __launch_bounds__(256) ttt_fwd_diag_kernel(const __grid_constant__ Params p) {
-  constexpr int E = D / 32;
-  const int lane = threadIdx.x & 31;
-  const long wid = (long)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (wid >= (long)p.B * p.L * p.Hkv) return;
-  const int g = (int)(wid % p.Hkv);
-  const int r = (int)((wid / p.Hkv) % p.L);
-  const int b = (int)(wid / ((long)p.Hkv * p.L));
-  if (r >= p.seq_lens[b]) return;
-  const size_t kv_off = (((size_t)b * p.L + r) * p.Hkv + g) * D + lane * E;
-  float t[TTT_MAX_STEPS];
+  constexpr int E = D / 16;
+  const int hl = threadIdx.x & 15;
+  const long wid = (long)blockIdx.x * 16 + (threadIdx.x >> 4);
+  const long nrows = (long)p.B * p.L * p.Hkv;
+  const bool valid = wid < nrows;
+  const long w = valid ? wid : nrows - 1;  // clamp: shuffles stay warp-uniform
+  const int g = (int)(w % p.Hkv);
+  const int r = (int)((w / p.Hkv) % p.L);
+  const int b = (int)(w / ((long)p.Hkv * p.L));
+  const bool act = valid && r < p.seq_lens[b];
+  const size_t kv_off = (((size_t)b * p.L + r) * p.Hkv + g) * D + hl * E;
   for (int hh = 0; hh < p.G; ++hh) {
     const int h = g * p.G + hh;
-    const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + lane * E;
-    float qf[E];
-    {
-      const __nv_bfloat16* qp = reinterpret_cast<const __nv_bfloat16*>(p.q) + q_off;
-#pragma unroll
-      for (int e = 0; e < E; ++e) qf[e] = __bfloat162float(qp[e]);
-    }
-    float m = -INFINITY;
-    for (int i = 0; i < p.step; ++i) {
-      const __nv_bfloat16* kp = reinterpret_cast<const __nv_bfloat16*>(p.ks[i]) + kv_off;
-      float acc = 0.f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc = fmaf(qf[e], __bfloat162float(kp[e]), acc);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      t[i] = acc * p.scale_log2;
-      m = fmaxf(m, t[i]);
-    }
-    float l = 0.f, o[E];
+    const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + hl * E;
+    float qf[E], o[E];
+    ld_row<D>(p.q, q_off, qf);
 #pragma unroll
     for (int e = 0; e < E; ++e) o[e] = 0.f;
+    float m = -INFINITY, l = 0.f;
     for (int i = 0; i < p.step; ++i) {
-      const float w = ex2(t[i] - m);
-      l += w;
-      const __nv_bfloat16* vp = reinterpret_cast<const __nv_bfloat16*>(p.vs[i]) + kv_off;
+      float kk[E], vv[E];
+      ld_row<D>(p.ks[i], kv_off, kk);
+      ld_row<D>(p.vs[i], kv_off, vv);
+      float acc = 0.f;
 #pragma unroll
-      for (int e = 0; e < E; ++e) o[e] = fmaf(w, __bfloat162float(vp[e]), o[e]);
+      for (int e = 0; e < E; ++e) acc = fmaf(qf[e], kk[e], acc);
+      const float t = half_allsum(acc) * p.scale_log2;  // s_i = c q_r . k_i (log2 units)
+      const float mn = fmaxf(m, t);
+      const float a = ex2(m - mn), wgt = ex2(t - mn);
+      l = l * a + wgt;
+#pragma unroll
+      for (int e = 0; e < E; ++e) o[e] = fmaf(wgt, vv[e], o[e] * a);
+      m = mn;
     }
-    const float inv = 1.f / l;
-    __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
-#pragma unroll
-    for (int e = 0; e < E; ++e) op[e] = __float2bfloat16_rn(o[e] * inv);
-    if (lane == 0) p.lse[((size_t)b * p.Hq + h) * p.L + r] = m + log2f(l);
+    if (act) {
+      const float inv = 1.f / l;
+      __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
+      if constexpr (E == 8) {
+        uint4 u;
+        u.x = pack_bf16(o[0] * inv, o[1] * inv);
+        u.y = pack_bf16(o[2] * inv, o[3] * inv);
+        u.z = pack_bf16(o[4] * inv, o[5] * inv);
+        u.w = pack_bf16(o[6] * inv, o[7] * inv);
+        *reinterpret_cast<uint4*>(op) = u;
+      } else {
+        uint2 u;
+        u.x = pack_bf16(o[0] * inv, o[1] * inv);
+        u.y = pack_bf16(o[2] * inv, o[3] * inv);
+        *reinterpret_cast<uint2*>(op) = u;
+      }
+      if (hl == 0) p.lse[((size_t)b * p.Hq + h) * p.L + r] = m + log2f(l);
+    }
   }
 }
 
@@ -376,9 +383,9 @@ cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, cudaStream_t st) 
     attr_set = true;
   }
   if (p.step > 0) {
-    const long warps = (long)p.B * p.L * p.Hkv;
+    const long rows = (long)p.B * p.L * p.Hkv;
     prof_mark(kKindFwdDiag, true, st);
-    ttt_fwd_diag_kernel<D><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(p);
+    ttt_fwd_diag_kernel<D><<<(unsigned)((rows + 15) / 16), 256, 0, st>>>(p);
     prof_mark(kKindFwdDiag, false, st);
   }
   const int npairs = (p.G + 1) / 2;

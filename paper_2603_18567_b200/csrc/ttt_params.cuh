@@ -39,7 +39,7 @@ struct Params {
   float* dvs[TTT_MAX_STEPS];
   float* delta;   // workspace [B][Hq][L]: Delta = rowsum(dO o O)
   float* lse2;    // workspace [B][Hq][L]: lse * log2(e)
-  float* dq_acc;  // workspace [B][L][Hq][D] fp32
+  float* dq_acc;  // workspace fp32, tile-contiguous [B][Hq][L/128][D/32][128][32]
   int seq_lens[TTT_MAX_BATCH];
 };
 
@@ -49,6 +49,7 @@ struct FwdMaps {
 };
 struct BwdMaps {
   CUtensorMap q, k, v, dout;
+  CUtensorMap dqacc;  // 2-D fp32 view of the tiled dq_acc: {32 cols, rows}, box 32 x 32, SW128
 };
 
 // Instrumentation hook (api.cu): brackets one kernel launch with events when
