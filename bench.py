@@ -196,6 +196,7 @@ class Unroll:
         self.ks = [mk(s.kv_shape) for _ in range(S - 1)]
         self.vs = [mk(s.kv_shape) for _ in range(S - 1)]
         self.out = [torch.empty(s.q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
+        self.out_lo = [torch.empty(s.q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
         self.lse = [torch.empty(s.batch, s.num_q_heads, s.seq_len, device=dev) for _ in range(S)]
         self.dq = [torch.empty(s.q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
         z = lambda: torch.zeros(s.kv_shape, dtype=torch.float32, device=dev)
@@ -211,11 +212,12 @@ class Unroll:
         S = s.ttt_steps
         for j in range(S):
             t.ttt_attn_fwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, self.out[j], self.lse[j],
-                           stream=stream)
+                           out_lo=self.out_lo[j], stream=stream)
         for j in reversed(range(S)):
             t.ttt_attn_bwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, self.out[j], self.lse[j],
                            self.do[j], self.dq[j], self.dk, self.dv, self.dks, self.dvs,
-                           flags=0 if j == S - 1 else t.TTT_ACCUMULATE_DKV, workspace=self.ws, stream=stream)
+                           flags=0 if j == S - 1 else t.TTT_ACCUMULATE_DKV, workspace=self.ws, stream=stream,
+                           out_lo=self.out_lo[j])
             if on_bwd is not None:
                 on_bwd(S - 1 - j)
 

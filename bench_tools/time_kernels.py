@@ -15,15 +15,15 @@ g = torch.Generator(device=dev).manual_seed(0)
 mk = lambda shp: torch.randn(shp, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
 q = mk(s.q_shape); k = mk(s.kv_shape); v = mk(s.kv_shape)
 ks = [mk(s.kv_shape) for _ in range(S - 1)]; vs = [mk(s.kv_shape) for _ in range(S - 1)]
-out = torch.empty_like(q); lse = torch.empty(B, Hq, L, device=dev)
+out = torch.empty_like(q); olo = torch.empty_like(q); lse = torch.empty(B, Hq, L, device=dev)
 desc = ttt.make_desc(B, L, Hq, Hkv, D)
 do = mk(s.q_shape); dq = torch.empty_like(q)
 z = lambda: torch.zeros(s.kv_shape, device=dev)
 dk, dv = z(), z(); dks = [z() for _ in range(S - 1)]; dvs = [z() for _ in range(S - 1)]
 ws = torch.empty(ttt.ttt_attn_workspace_size(desc, S - 1, True), dtype=torch.uint8, device=dev)
 tot_f = tot_b = 0.0
-fwd = lambda j: ttt.ttt_attn_fwd(desc, j, q, k, v, ks, vs, out, lse)
-bwd = lambda j: ttt.ttt_attn_bwd(desc, j, q, k, v, ks, vs, out, lse, do, dq, dk, dv, dks, dvs, flags=1, workspace=ws)
+fwd = lambda j: ttt.ttt_attn_fwd(desc, j, q, k, v, ks, vs, out, lse, out_lo=olo)
+bwd = lambda j: ttt.ttt_attn_bwd(desc, j, q, k, v, ks, vs, out, lse, do, dq, dk, dv, dks, dvs, flags=1, workspace=ws, out_lo=olo)
 
 
 def timeit(fn, n=10):

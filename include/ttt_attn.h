@@ -104,16 +104,20 @@ size_t ttt_attn_workspace_size(const ttt_attn_desc* desc, int step, int is_bwd);
  *   k_steps  HOST array of `step` device ptrs, each [B][L][Hkv][D]  (K_1..K_j, "K^pred")
  *   v_steps  likewise
  *   out      [B][L][Hq][D]                 out
+ *   out_lo   [B][L][Hq][D] bf16 or NULL    out  (BF16 mode only: the rounding residual O - bf16(O)
+ *            of the fp32 output; lets ttt_attn_bwd form Delta = dO.O from ~16-bit-accurate O.
+ *            Ignored in FP32_CHECK mode.)
  *   lse      [B][Hq][L] fp32               out  (natural-log logsumexp of c*q.k over the allowed set)
  * step == 0 is ordinary causal attention with key padding (Alg. 2, suffix term vacuous). */
 int ttt_attn_fwd(const ttt_attn_desc* desc, int step,
                  const void* q, const void* k_base, const void* v_base,
                  const void* const* k_steps, const void* const* v_steps,
-                 void* out, float* lse,
+                 void* out, void* out_lo, float* lse,
                  void* workspace, size_t workspace_bytes, void* stream);
 
 /* Backward of TTT step `step`, recompute-based (no saved probabilities).
- *   out, lse  from ttt_attn_fwd of the same step; dout = dL/d out (layout of out).
+ *   out, out_lo, lse  from ttt_attn_fwd of the same step (out_lo may be NULL: Delta then
+ *             uses the bf16 out); dout = dL/d out (layout of out).
  *   dq        [B][L][Hq][D]   (bf16 / fp32)  overwritten with this step's dq
  *   dk_base, dv_base          fp32 [B][L][Hkv][D]  dL/dK_0, dL/dV_0
  *   dk_steps, dv_steps        HOST arrays of `step` device ptrs, fp32 [B][L][Hkv][D]
@@ -122,7 +126,7 @@ int ttt_attn_fwd(const ttt_attn_desc* desc, int step,
 int ttt_attn_bwd(const ttt_attn_desc* desc, int step,
                  const void* q, const void* k_base, const void* v_base,
                  const void* const* k_steps, const void* const* v_steps,
-                 const void* out, const float* lse, const void* dout,
+                 const void* out, const void* out_lo, const float* lse, const void* dout,
                  void* dq, float* dk_base, float* dv_base,
                  float* const* dk_steps, float* const* dv_steps,
                  unsigned flags, void* workspace, size_t workspace_bytes, void* stream);

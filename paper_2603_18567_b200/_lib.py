@@ -52,9 +52,9 @@ def _load():
     pd = ctypes.POINTER(Desc)
     lib.ttt_attn_workspace_size.argtypes = [pd, i, i]
     lib.ttt_attn_workspace_size.restype = sz
-    lib.ttt_attn_fwd.argtypes = [pd, i, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.ttt_attn_fwd.argtypes = [pd, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.ttt_attn_fwd.restype = i
-    lib.ttt_attn_bwd.argtypes = [pd, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, u, vp, sz, vp]
+    lib.ttt_attn_bwd.argtypes = [pd, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, u, vp, sz, vp]
     lib.ttt_attn_bwd.restype = i
     lib.ttt_attn_strerror.argtypes = [i]
     lib.ttt_attn_strerror.restype = ctypes.c_char_p
@@ -154,21 +154,21 @@ def ttt_attn_workspace_size(desc: Desc, step: int, is_bwd: bool) -> int:
 
 
 def ttt_attn_fwd(desc: Desc, step: int, q, k_base, v_base, k_steps, v_steps, out, lse,
-                 workspace=None, stream=None) -> None:
+                 out_lo=None, workspace=None, stream=None) -> None:
     """Enqueue ttt_attn_fwd (include/ttt_attn.h) on `stream` (default: current)."""
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(_lib.ttt_attn_fwd(ctypes.byref(desc), int(step), _ptr(q), _ptr(k_base), _ptr(v_base),
-                             _ptr_list(k_steps[:step]), _ptr_list(v_steps[:step]), _ptr(out), _ptr(lse),
-                             _ptr(workspace), ws_bytes, _stream(stream)))
+                             _ptr_list(k_steps[:step]), _ptr_list(v_steps[:step]), _ptr(out), _ptr(out_lo),
+                             _ptr(lse), _ptr(workspace), ws_bytes, _stream(stream)))
 
 
 def ttt_attn_bwd(desc: Desc, step: int, q, k_base, v_base, k_steps, v_steps, out, lse, dout,
                  dq, dk_base, dv_base, dk_steps, dv_steps, flags: int = 0, workspace=None,
-                 stream=None) -> None:
+                 stream=None, out_lo=None) -> None:
     """Enqueue ttt_attn_bwd (include/ttt_attn.h) on `stream` (default: current)."""
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(_lib.ttt_attn_bwd(ctypes.byref(desc), int(step), _ptr(q), _ptr(k_base), _ptr(v_base),
-                             _ptr_list(k_steps[:step]), _ptr_list(v_steps[:step]), _ptr(out), _ptr(lse),
-                             _ptr(dout), _ptr(dq), _ptr(dk_base), _ptr(dv_base),
+                             _ptr_list(k_steps[:step]), _ptr_list(v_steps[:step]), _ptr(out), _ptr(out_lo),
+                             _ptr(lse), _ptr(dout), _ptr(dq), _ptr(dk_base), _ptr(dv_base),
                              _ptr_list(dk_steps[:step]), _ptr_list(dv_steps[:step]), int(flags),
                              _ptr(workspace), ws_bytes, _stream(stream)))

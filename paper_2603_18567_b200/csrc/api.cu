@@ -219,8 +219,8 @@ size_t ttt_attn_workspace_size(const ttt_attn_desc* d, int step, int is_bwd) {
 }
 
 int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_base, const void* v_base,
-                 const void* const* k_steps, const void* const* v_steps, void* out, float* lse, void* workspace,
-                 size_t workspace_bytes, void* stream) {
+                 const void* const* k_steps, const void* const* v_steps, void* out, void* out_lo, float* lse,
+                 void* workspace, size_t workspace_bytes, void* stream) {
   (void)workspace;
   (void)workspace_bytes;
   int st = validate_desc(d, step);
@@ -229,7 +229,8 @@ int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
   if (step > 0 && (!k_steps || !v_steps)) return TTT_ERR_INVALID_ARG;
   for (int i = 0; i < step; ++i)
     if (!k_steps[i] || !v_steps[i]) return TTT_ERR_INVALID_ARG;
-  if (!aligned16(q) || !aligned16(k_base) || !aligned16(v_base) || !aligned16(out) || !aligned16(lse))
+  if (!aligned16(q) || !aligned16(k_base) || !aligned16(v_base) || !aligned16(out) || !aligned16(lse) ||
+      !aligned16(out_lo))
     return TTT_ERR_ALIGNMENT;
   for (int i = 0; i < step; ++i)
     if (!aligned16(k_steps[i]) || !aligned16(v_steps[i])) return TTT_ERR_ALIGNMENT;
@@ -243,6 +244,7 @@ int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
     p.vs[i] = v_steps[i];
   }
   p.out = out;
+  p.out_lo = d->dtype == TTT_BF16 ? out_lo : nullptr;
   p.lse = lse;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (d->dtype == TTT_FP32_CHECK) return cuda_status(launch_fwd_check(p, s));
@@ -254,8 +256,8 @@ int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
 }
 
 int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_base, const void* v_base,
-                 const void* const* k_steps, const void* const* v_steps, const void* out, const float* lse,
-                 const void* dout, void* dq, float* dk_base, float* dv_base, float* const* dk_steps,
+                 const void* const* k_steps, const void* const* v_steps, const void* out, const void* out_lo,
+                 const float* lse, const void* dout, void* dq, float* dk_base, float* dv_base, float* const* dk_steps,
                  float* const* dv_steps, unsigned flags, void* workspace, size_t workspace_bytes, void* stream) {
   int st = validate_desc(d, step);
   if (st) return st;
@@ -265,7 +267,7 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
   if (step > 0 && (!k_steps || !v_steps || !dk_steps || !dv_steps)) return TTT_ERR_INVALID_ARG;
   for (int i = 0; i < step; ++i)
     if (!k_steps[i] || !v_steps[i] || !dk_steps[i] || !dv_steps[i]) return TTT_ERR_INVALID_ARG;
-  const void* ptrs[] = {q, k_base, v_base, out, lse, dout, dq, dk_base, dv_base};
+  const void* ptrs[] = {q, k_base, v_base, out, lse, dout, dq, dk_base, dv_base, out_lo};
   for (const void* ptr : ptrs)
     if (!aligned16(ptr)) return TTT_ERR_ALIGNMENT;
   for (int i = 0; i < step; ++i)
@@ -278,6 +280,7 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
   p.k = k_base;
   p.v = v_base;
   p.o = out;
+  p.o_lo = d->dtype == TTT_BF16 ? out_lo : nullptr;
   p.lse_in = lse;
   p.dout = dout;
   p.dq = dq;

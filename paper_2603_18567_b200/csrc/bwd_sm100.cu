@@ -72,7 +72,7 @@ __device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int
 // One HALF-warp per (b, r, kv head g): 16 lanes x (D/16) contiguous elements,
 // 16-byte loads, 4-level shuffle reductions. Rows per block = 2 * warps.
 template <int D>
-__global__ void __launch_bounds__(256) ttt_bwd_pre_kernel(const __grid_constant__ Params p, int rows_per_block) {
+__global__ void __launch_bounds__(128) ttt_bwd_pre_kernel(const __grid_constant__ Params p, int rows_per_block) {
   constexpr int E = D / 16;
   extern __shared__ float pre_smem[];
   const int lane = threadIdx.x & 31, hl = lane & 15;
@@ -97,6 +97,12 @@ __global__ void __launch_bounds__(256) ttt_bwd_pre_kernel(const __grid_constant_
     float o[E], d[E];
     ld_row<D>(p.o, q_off, o);
     ld_row<D>(p.dout, q_off, d);
+    if (p.o_lo) {  // O = bf16 out + bf16 residual: Delta from ~16-bit-accurate O
+      float lo[E];
+      ld_row<D>(p.o_lo, q_off, lo);
+#pragma unroll
+      for (int e = 0; e < E; ++e) o[e] += lo[e];
+    }
     float acc = 0.f;
 #pragma unroll
     for (int e = 0; e < E; ++e) acc = fmaf(o[e], d[e], acc);
@@ -126,50 +132,85 @@ __global__ void __launch_bounds__(256) ttt_bwd_pre_kernel(const __grid_constant_
     }
   }
   const bool act = valid && (r < T);  // diagonal keys exist only for rows r < T_b (Alg. 2 m_pad)
-  for (int i = 0; i < p.step; ++i) {
-    float dk[E], dv[E], kk[E], vv[E];
+  // steps in chunks of 4: all K_i / V_i rows (and dK_i / dV_i for the RMW) of a chunk are
+  // loaded together and the 8 dot products of a head are reduced with interleaved shuffles.
+  constexpr int CH = 4;
+  for (int i0 = 0; i0 < p.step; i0 += CH) {
+    const int ni = min(CH, p.step - i0);
+    float kk[CH][E], vv[CH][E], dk[CH][E], dv[CH][E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) dk[e] = dv[e] = 0.f;
-    ld_row<D>(p.ks[i], kv_off, kk);
-    ld_row<D>(p.vs[i], kv_off, vv);
+    for (int u = 0; u < CH; ++u) {
+      if (u < ni) {
+        ld_row<D>(p.ks[i0 + u], kv_off, kk[u]);
+        ld_row<D>(p.vs[i0 + u], kv_off, vv[u]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) kk[u][e] = vv[u][e] = 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) dk[u][e] = dv[u][e] = 0.f;
+    }
     for (int hh = 0; hh < G; ++hh) {
       const int h = g * G + hh;
       const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + hl * E;
       float qq[E], dd[E];
       ld_row<D>(p.q, q_off, qq);
       ld_row<D>(p.dout, q_off, dd);
-      float s = 0.f, dp = 0.f;
+      float s[CH], dp[CH];
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        s = fmaf(qq[e], kk[e], s);
-        dp = fmaf(dd[e], vv[e], dp);
-      }
-      s = half_allsum(s);
-      dp = half_allsum(dp);
-      const float pr = act ? ex2(s * p.scale_log2 - sl2[hh]) : 0.f;  // p_i = exp(c q.k_i - lse)
-      const float ds = pr * (dp - sdel[hh]);                          // ds_i = p_i (dp_i - Delta)
-      const float cds = p.scale * ds;
+      for (int u = 0; u < CH; ++u) {
+        s[u] = 0.f;
+        dp[u] = 0.f;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        dk[e] = fmaf(cds, qq[e], dk[e]);
-        dv[e] = fmaf(pr, dd[e], dv[e]);
-        sdq[hh * D + hl * E + e] = fmaf(cds, kk[e], sdq[hh * D + hl * E + e]);
+        for (int e = 0; e < E; ++e) {
+          s[u] = fmaf(qq[e], kk[u][e], s[u]);
+          dp[u] = fmaf(dd[e], vv[u][e], dp[u]);
+        }
       }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {
+          s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+          dp[u] += __shfl_xor_sync(0xffffffffu, dp[u], o);
+        }
+      }
+      const float l2 = sl2[hh], del = sdel[hh];
+      float dqa[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) dqa[e] = 0.f;
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const float pr = (act && u < ni) ? ex2(s[u] * p.scale_log2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
+        const float cds = p.scale * pr * (dp[u] - del);                           // c ds_i, ds_i = p_i (dp_i - Delta)
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          dk[u][e] = fmaf(cds, qq[e], dk[u][e]);
+          dv[u][e] = fmaf(pr, dd[e], dv[u][e]);
+          dqa[e] = fmaf(cds, kk[u][e], dqa[e]);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) sdq[hh * D + hl * E + e] += dqa[e];
     }
     if (valid) {
-      float4* dk4 = reinterpret_cast<float4*>(p.dks[i] + kv_off);
-      float4* dv4 = reinterpret_cast<float4*>(p.dvs[i] + kv_off);
 #pragma unroll
-      for (int e = 0; e < E / 4; ++e) {
-        float4 a = make_float4(dk[4 * e], dk[4 * e + 1], dk[4 * e + 2], dk[4 * e + 3]);
-        float4 c = make_float4(dv[4 * e], dv[4 * e + 1], dv[4 * e + 2], dv[4 * e + 3]);
-        if (p.accumulate) {
-          const float4 a0 = dk4[e], c0 = dv4[e];
-          a.x += a0.x; a.y += a0.y; a.z += a0.z; a.w += a0.w;
-          c.x += c0.x; c.y += c0.y; c.z += c0.z; c.w += c0.w;
+      for (int u = 0; u < CH; ++u) {
+        if (u >= ni) break;
+        float4* dk4 = reinterpret_cast<float4*>(p.dks[i0 + u] + kv_off);
+        float4* dv4 = reinterpret_cast<float4*>(p.dvs[i0 + u] + kv_off);
+#pragma unroll
+        for (int e = 0; e < E / 4; ++e) {
+          float4 a = make_float4(dk[u][4 * e], dk[u][4 * e + 1], dk[u][4 * e + 2], dk[u][4 * e + 3]);
+          float4 c = make_float4(dv[u][4 * e], dv[u][4 * e + 1], dv[u][4 * e + 2], dv[u][4 * e + 3]);
+          if (p.accumulate) {
+            const float4 a0 = dk4[e], c0 = dv4[e];
+            a.x += a0.x; a.y += a0.y; a.z += a0.z; a.w += a0.w;
+            c.x += c0.x; c.y += c0.y; c.z += c0.z; c.w += c0.w;
+          }
+          dk4[e] = a;
+          dv4[e] = c;
         }
-        dk4[e] = a;
-        dv4[e] = c;
       }
     }
   }
@@ -210,7 +251,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   constexpr int TB = kTile * D * 2;
   constexpr int NBOX = D / 64;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment for SW128 tiles, keeping the pointer in the shared window (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sK = smem;
   uint8_t* sV = smem + TB;
   uint8_t* sQ = smem + 2 * TB;   // 2 stages
@@ -552,7 +594,7 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
   p.head_split = pick_head_split(p);
   // 1. pre-pass
   {
-    const int rows_per_block = 2 * std::max(1, std::min(8, 32 / std::max(1, p.G)));
+    const int rows_per_block = 2 * std::max(1, std::min(4, 32 / std::max(1, p.G)));
     const size_t smem = (size_t)rows_per_block * (p.G * D + 2 * p.G) * sizeof(float);
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,

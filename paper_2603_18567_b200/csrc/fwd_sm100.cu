@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   constexpr int TB = kTile * D * 2;  // bytes of one 128 x D bf16 tile
   constexpr int NBOX = D / 64;       // 64-column (128 B) swizzle boxes per tile
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment for SW128 tiles, keeping the pointer in the shared window (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;           // 2 tiles (head slots)
   uint8_t* sK = smem + 2 * TB;  // 2 stages
   uint8_t* sV = smem + 4 * TB;  // 2 stages
@@ -299,6 +300,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           w.z = pack_bf16(v[4], v[5]);
           w.w = pack_bf16(v[6], v[7]);
           *reinterpret_cast<uint4*>(orow + c0 + q4 * 8) = w;
+          if (p.out_lo) {  // residual O - bf16(O), so the backward's Delta sees ~16-bit O
+            const uint32_t hi[4] = {w.x, w.y, w.z, w.w};
+            uint32_t lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hi[e]));
+              lo[e] = pack_bf16(v[2 * e] - hf.x, v[2 * e + 1] - hf.y);
+            }
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out_lo) + q_off + c0 + q4 * 8) =
+                make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          }
         }
       }
       p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
@@ -337,19 +349,45 @@ __global__ void __launch_bounds__(256) ttt_fwd_diag_kernel(const __grid_constant
 #pragma unroll
     for (int e = 0; e < E; ++e) o[e] = 0.f;
     float m = -INFINITY, l = 0.f;
-    for (int i = 0; i < p.step; ++i) {
-      float kk[E], vv[E];
-      ld_row<D>(p.ks[i], kv_off, kk);
-      ld_row<D>(p.vs[i], kv_off, vv);
-      float acc = 0.f;
+    constexpr int CH = 4;  // steps per chunk: loads and shuffle chains of a chunk overlap
+    for (int i0 = 0; i0 < p.step; i0 += CH) {
+      const int ni = min(CH, p.step - i0);
+      float kk[CH][E], vv[CH][E], t[CH];
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc = fmaf(qf[e], kk[e], acc);
-      const float t = half_allsum(acc) * p.scale_log2;  // s_i = c q_r . k_i (log2 units)
-      const float mn = fmaxf(m, t);
-      const float a = ex2(m - mn), wgt = ex2(t - mn);
-      l = l * a + wgt;
+      for (int u = 0; u < CH; ++u) {
+        if (u < ni) {
+          ld_row<D>(p.ks[i0 + u], kv_off, kk[u]);
+          ld_row<D>(p.vs[i0 + u], kv_off, vv[u]);
+        } else {
 #pragma unroll
-      for (int e = 0; e < E; ++e) o[e] = fmaf(wgt, vv[e], o[e] * a);
+          for (int e = 0; e < E; ++e) kk[u][e] = vv[u][e] = 0.f;
+        }
+        t[u] = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) t[u] = fmaf(qf[e], kk[u][e], t[u]);
+      }
+#pragma unroll
+      for (int o2 = 8; o2 > 0; o2 >>= 1) {
+#pragma unroll
+        for (int u = 0; u < CH; ++u) t[u] += __shfl_xor_sync(0xffffffffu, t[u], o2);
+      }
+      float mn = m;
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        t[u] = u < ni ? t[u] * p.scale_log2 : -INFINITY;  // s_i = c q_r . k_i (log2 units)
+        mn = fmaxf(mn, t[u]);
+      }
+      const float a = ex2(m - mn);
+      l *= a;
+#pragma unroll
+      for (int e = 0; e < E; ++e) o[e] *= a;
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const float wgt = ex2(t[u] - mn);
+        l += wgt;
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[e] = fmaf(wgt, vv[u][e], o[e]);
+      }
       m = mn;
     }
     if (act) {

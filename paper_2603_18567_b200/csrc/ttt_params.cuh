@@ -27,9 +27,11 @@ struct Params {
   const void* ks[TTT_MAX_STEPS];
   const void* vs[TTT_MAX_STEPS];
   void* out;
+  void* out_lo;  // optional bf16 residual O - bf16(O)
   float* lse;
   // backward
   const void* o;
+  const void* o_lo;  // optional residual of o
   const void* dout;
   const float* lse_in;
   void* dq;

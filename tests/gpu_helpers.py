@@ -61,7 +61,9 @@ class DeviceCase:
         s = self.case.shape
         out = torch.empty(s.q_shape, dtype=self.dt, device=self.dev)
         lse = torch.empty((s.batch, s.num_q_heads, s.seq_len), dtype=torch.float32, device=self.dev)
-        ttt.ttt_attn_fwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, out, lse, stream=stream)
+        self.out_lo = torch.empty_like(out) if self.dt == torch.bfloat16 else None
+        ttt.ttt_attn_fwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, out, lse,
+                         out_lo=self.out_lo, stream=stream)
         return out, lse
 
     def alloc_grads(self, nsteps):
@@ -78,7 +80,8 @@ class DeviceCase:
         ttt.ttt_attn_bwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, out, lse,
                          self.dout[j] if dout is None else dout, dq, grads["dk_base"], grads["dv_base"],
                          grads["dk_steps"], grads["dv_steps"],
-                         flags=ttt.TTT_ACCUMULATE_DKV if accumulate else 0, workspace=ws)
+                         flags=ttt.TTT_ACCUMULATE_DKV if accumulate else 0, workspace=ws,
+                         out_lo=getattr(self, "out_lo", None))
         return dq
 
 
