@@ -1,0 +1,57 @@
+"""Timeline of one bwd CTA from a -DTTT_TRACE build (dev tool).
+usage: TTT_ATTN_LIB=build/libtttattn_variant.so python bench_tools/trace_bwd.py [cta]"""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2603_18567_b200 as ttt
+from paper_2603_18567_b200 import _lib
+from paper_2603_18567_b200.inputs import CONFIGS
+cta = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+lib = ctypes.CDLL(_lib.LIB_PATH)
+buf = np.zeros((4, 1 << 16), dtype=np.uint64)
+s = CONFIGS["llama8b"]; dev = "cuda"; j = 0
+g = torch.Generator(device=dev).manual_seed(0)
+mk = lambda shp: torch.randn(shp, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
+q = mk(s.q_shape); k = mk(s.kv_shape); v = mk(s.kv_shape); do = mk(s.q_shape)
+out = torch.empty_like(q); olo = torch.empty_like(q); lse = torch.empty(s.batch, s.num_q_heads, s.seq_len, device=dev)
+desc = ttt.make_desc(s.batch, s.seq_len, s.num_q_heads, s.num_kv_heads, s.head_dim)
+dq = torch.empty_like(q); z = lambda: torch.zeros(s.kv_shape, device=dev); dk, dv = z(), z()
+ws = torch.empty(ttt.ttt_attn_workspace_size(desc, 0, True), dtype=torch.uint8, device=dev)
+ttt.ttt_attn_fwd(desc, j, q, k, v, [], [], out, lse, out_lo=olo)
+lib.ttt_debug_trace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
+for _ in range(2):
+    ttt.ttt_attn_bwd(desc, j, q, k, v, [], [], out, lse, do, dq, dk, dv, [], [], flags=0, workspace=ws, out_lo=olo)
+lib.ttt_debug_trace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
+names = {0: {1: "mma:wait_p", 2: "mma:got_p", 3: "mma:got_ds", 4: "mma:got_q", 5: "mma:got_dqempty", 6: "mma:got_do"},
+         1: {1: "cmp:got_s", 2: "cmp:p_done", 3: "cmp:got_dp", 4: "cmp:ds_done"},
+         2: {1: "dq:got_dq", 2: "dq:drained"}}
+ev = []
+for role in range(3):
+    for x in buf[role]:
+        x = int(x)
+        if x == 0: continue
+        ev.append((x >> 20, names[role].get((x >> 12) & 0xFF, str((x >> 12) & 0xFF)), x & 0xFFF))
+ev.sort()
+t0 = ev[0][0]
+items = {}
+for t, n, i in ev:
+    items.setdefault(i, []).append((t - t0, n))
+for i in sorted(items)[:3] + sorted(items)[20:24]:
+    base = items[i][0][0]
+    print(f"item {i}: " + "  ".join(f"{n}@{t-base}" for t, n in items[i]))
+# per-item period
+starts = sorted((v[0][0], i) for i, v in items.items() if any(n == "cmp:got_s" for _, n in v))
+ts = [t for t, n, i in ev if n == "cmp:got_s"]
+d = np.diff(ts)
+print("items", len(ts), "period clk median", np.median(d), "mean", d.mean())
+for nm in ["mma:got_p", "mma:got_ds", "mma:got_q", "mma:got_dqempty", "mma:got_do", "cmp:p_done", "cmp:got_dp", "cmp:ds_done", "dq:got_dq", "dq:drained"]:
+    pass
+# average offsets relative to cmp:got_s of the same item
+acc = {}
+for i, v in items.items():
+    s0 = [t for t, n in v if n == "cmp:got_s"]
+    if not s0: continue
+    for t, n in v:
+        acc.setdefault(n, []).append(t - s0[0])
+for n, xs in sorted(acc.items(), key=lambda kv: np.median(kv[1])):
+    print(f"{n:18s} median offset {np.median(xs):8.0f}")

@@ -32,6 +32,10 @@
 #include "ttt_params.cuh"
 
 namespace tttk {
+#ifdef TTT_TRACE
+__device__ unsigned long long g_ttt_trace[4][kTraceCap];
+__device__ unsigned int g_ttt_trace_cta;
+#endif
 namespace {
 
 constexpr int kBwdThreads = 320;
@@ -357,6 +361,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) umma_ss(tbase + 128, kmaj(aV, ks), kmaj(aDO, ks), idSP, ks > 0);
       };
+      TTT_TRACE_DECL(0);
       mbar_wait(&bars.kv_full, 0);
       mbar_wait(&bars.q_full[0], 0);
       tc_fence_after();
@@ -370,7 +375,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int qs = i & 1;
         const bool more = i + 1 < n_items;
         // dV += P^T dO   (A = P^T in TMEM cols [0,64))
+        TTT_TRACE_EV(0, 1, i);
         mbar_wait(&bars.p_full, i & 1);
+        TTT_TRACE_EV(0, 2, i);
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
@@ -378,6 +385,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         umma_commit(&bars.do_empty);
         // dK += dS^T Q   (A = dS^T in TMEM cols [128,192))
         mbar_wait(&bars.ds_full, i & 1);
+        TTT_TRACE_EV(0, 3, i);
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
@@ -386,6 +394,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // next S^T while this item's dQ is drained
         if (more) {
           mbar_wait(&bars.q_full[(i + 1) & 1], ((i + 1) >> 1) & 1);
+          TTT_TRACE_EV(0, 4, i);
           tc_fence_after();
           issue_S((i + 1) & 1);
           umma_commit(&bars.s_full);
@@ -397,7 +406,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         umma_commit(&bars.ds_empty);
         if (more) {
           mbar_wait(&bars.dq_empty, i & 1);
+          TTT_TRACE_EV(0, 5, i);
           mbar_wait(&bars.do_full, (i + 1) & 1);
+          TTT_TRACE_EV(0, 6, i);
           tc_fence_after();
           issue_dP();
           umma_commit(&bars.dp_full);
@@ -412,11 +423,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     const uint32_t tS = tbase + lane_off, tdP = tbase + lane_off + 128;
     const float sl2 = p.scale_log2;
+    TTT_TRACE_DECL(1);
     for (int i = 0; i < n_items; ++i) {
       const int qs = i & 1;
       const int qt = kt + i % nq;
       mbar_wait(&bars.q_full[qs], (i >> 1) & 1);
       mbar_wait(&bars.s_full, i & 1);
+      if (threadIdx.x == 0) TTT_TRACE_EV(1, 1, i);
       tc_fence_after();
       const float* Lq = sL + qs * 128;
       const float* Dq = sDel + qs * 128;
@@ -446,7 +459,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars.p_full);
+      if (threadIdx.x == 0) TTT_TRACE_EV(1, 2, i);
       mbar_wait(&bars.dp_full, i & 1);
+      if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, i);
       mbar_wait(&bars.ds_empty, (i & 1) ^ 1);
       tc_fence_after();
 #pragma unroll
@@ -479,6 +494,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars.ds_full);
+      if (threadIdx.x == 0) TTT_TRACE_EV(1, 4, i);
     }
     // ---- dK, dV accumulators -> global (fp32 atomics: head splits and steps add up) ----
     mbar_wait(&bars.acc_full, 0);
@@ -513,9 +529,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t tQ = tbase + ((uint32_t)(wq * 32) << 16) + 128;
     uint8_t* stage = sDQ + wq * 4096;
     if (lane == 0) tma_prefetch_desc(&maps.dqacc);
+    TTT_TRACE_DECL(2);
     for (int i = 0; i < n_items; ++i) {
       const int h = h_first + i / nq, qt = kt + i % nq;
       mbar_wait(&bars.dq_full, i & 1);
+      if (threadIdx.x == 128) TTT_TRACE_EV(2, 1, i);
       tc_fence_after();
       float v[D];
 #pragma unroll
@@ -527,6 +545,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bars.dq_empty);
+      if (threadIdx.x == 128) TTT_TRACE_EV(2, 2, i);
       const int row_base = (((b * p.Hq + h) * p.nqt + qt) * (D / 32)) * 128 + wq * 32;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
@@ -639,6 +658,16 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
 }
 
 }  // namespace
+
+#ifdef TTT_TRACE
+extern "C" int ttt_debug_trace_read(void* host, unsigned int cta) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(host, g_ttt_trace, sizeof(g_ttt_trace)) != cudaSuccess) return 1;
+  unsigned long long z[4 * 1024] = {};
+  for (int r = 0; r < 4; ++r) cudaMemcpyToSymbol(g_ttt_trace, z, sizeof(z), (size_t)r * kTraceCap * 8);
+  return cudaMemcpyToSymbol(g_ttt_trace_cta, &cta, sizeof(cta)) != cudaSuccess;
+}
+#endif
 
 cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, cudaStream_t st) {
   return p.D == 64 ? launch_bwd_d<64>(p, maps, st) : launch_bwd_d<128>(p, maps, st);

@@ -27,6 +27,19 @@ def report(name, got, want, atol, rtol):
     return bad.any(), msg
 
 
+def assert_close_sum(name, got, parts, atol, rtol):
+    """Accumulated result vs a sum of per-call oracle contributions: each call is
+    allowed atol + rtol*|part|, so the sum is held to the sum of those bounds
+    (triangle inequality; reading R16)."""
+    got = np.asarray(got, np.float64)
+    want = np.sum(parts, axis=0)
+    bound = sum(atol + rtol * np.abs(np.asarray(x, np.float64)) for x in parts)
+    assert not np.isnan(got).any(), f"{name}: NaN in GPU result"
+    err = np.abs(got - want)
+    bad = err > bound
+    assert not bad.any(), f"{name}: max_abs={err.max():.3e} violations={int(bad.sum())}/{bad.size} (n={len(parts)})"
+
+
 def assert_close(name, got, want, atol, rtol, mask=None):
     got = np.asarray(got, np.float64)
     want = np.asarray(want, np.float64)

@@ -11,7 +11,7 @@ import torch
 
 import oracle
 from paper_2603_18567_b200.inputs import CONFIGS, Shape, make_case, sample_rows
-from tests.gpu_helpers import TOL_BF16, DeviceCase, assert_close, np32, oracle_inputs
+from tests.gpu_helpers import TOL_BF16, DeviceCase, assert_close, assert_close_sum, np32, oracle_inputs
 
 pytestmark = pytest.mark.gpu
 
@@ -44,7 +44,8 @@ def test_bwd_bf16_small(cuda_ok, name, shape, lens):
     dc = DeviceCase(case)
     S = shape.ttt_steps
     acc = dc.alloc_grads(S - 1)
-    want = None
+    parts = {"dk_base": [], "dv_base": [], "dk_steps": [[] for _ in range(S - 1)],
+             "dv_steps": [[] for _ in range(S - 1)]}
     for j in reversed(range(S)):
         out, lse = dc.fwd(j)
         g = dc.alloc_grads(S - 1)
@@ -55,20 +56,16 @@ def test_bwd_bf16_small(cuda_ok, name, shape, lens):
         torch.cuda.synchronize()
         og = oracle.bwd(*oracle_inputs(case, j), np32(case.dout[j]), seq_lens=case.seq_lens)
         _check_grads(name, dq, g, og, j)
-        if want is None:
-            want = {k: (v.copy() if not isinstance(v, list) else [np.zeros_like(og["dk_base"]) for _ in range(S - 1)])
-                    for k, v in og.items() if k != "dq"}
-        else:
-            want["dk_base"] += og["dk_base"]
-            want["dv_base"] += og["dv_base"]
+        parts["dk_base"].append(og["dk_base"])
+        parts["dv_base"].append(og["dv_base"])
         for i in range(j):
-            want["dk_steps"][i] += og["dk_steps"][i]
-            want["dv_steps"][i] += og["dv_steps"][i]
-    assert_close(f"{name} acc dk_base", np32(acc["dk_base"]), want["dk_base"], **TOL_BF16)
-    assert_close(f"{name} acc dv_base", np32(acc["dv_base"]), want["dv_base"], **TOL_BF16)
+            parts["dk_steps"][i].append(og["dk_steps"][i])
+            parts["dv_steps"][i].append(og["dv_steps"][i])
+    assert_close_sum(f"{name} acc dk_base", np32(acc["dk_base"]), parts["dk_base"], **TOL_BF16)
+    assert_close_sum(f"{name} acc dv_base", np32(acc["dv_base"]), parts["dv_base"], **TOL_BF16)
     for i in range(S - 1):
-        assert_close(f"{name} acc dk_{i+1}", np32(acc["dk_steps"][i]), want["dk_steps"][i], **TOL_BF16)
-        assert_close(f"{name} acc dv_{i+1}", np32(acc["dv_steps"][i]), want["dv_steps"][i], **TOL_BF16)
+        assert_close_sum(f"{name} acc dk_{i+1}", np32(acc["dk_steps"][i]), parts["dk_steps"][i], **TOL_BF16)
+        assert_close_sum(f"{name} acc dv_{i+1}", np32(acc["dv_steps"][i]), parts["dv_steps"][i], **TOL_BF16)
 
 
 def test_bwd_bf16_gradient_identities(cuda_ok):

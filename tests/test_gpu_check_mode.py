@@ -6,7 +6,7 @@ import torch
 
 import oracle
 from paper_2603_18567_b200.inputs import CONFIGS, Shape, make_case
-from tests.gpu_helpers import TOL_FP32, DeviceCase, assert_close, np32, oracle_inputs
+from tests.gpu_helpers import TOL_FP32, DeviceCase, assert_close, assert_close_sum, np32, oracle_inputs
 
 pytestmark = pytest.mark.gpu
 
