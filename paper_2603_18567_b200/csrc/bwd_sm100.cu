@@ -38,7 +38,6 @@ __device__ unsigned int g_ttt_trace_cta;
 #endif
 namespace {
 
-constexpr int kBwdThreads = 320;
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ float warp_allsum(float x) {
@@ -248,15 +247,52 @@ __device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+template <uint32_t N>
+__device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+// two back-to-back 32-column TMEM loads, one wait (64 regs)
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%64];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+      "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%65];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr), "r"(taddr + 32)
+      : "memory");
+}
+
+// Warp roles (16 warps, FA4-style split; setmaxnreg rebalances the register file):
+//   warps 0-3   dQ drain          (thread = query row of TMEM lane quadrant w)
+//   warps 4-11  compute P^T, dS^T (quadrant w & 3, query-column half (w - 4) >> 2)
+//   warp  12    TMEM owner + MMA issuer, warp 13 TMA producer, warps 14-15 idle
+// Per SMSP: {dQ 152, compute 136, compute 136, role 88 / idle 24} <= 512 registers.
+constexpr int kBwdThreads = 512;
+constexpr int kBwdSmem = 5 * 32768 + 32768 + 2048 + 32768 + 256;  // D = 128 layout (D = 64 uses less)
 
 template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     ttt_bwd_sm100_kernel(const __grid_constant__ Params p, const __grid_constant__ BwdMaps maps) {
   constexpr int TB = kTile * D * 2;
   constexpr int NBOX = D / 64;
-  extern __shared__ uint8_t smem_raw[];
-  // 1024-B alignment for SW128 tiles, keeping the pointer in the shared window (LDS/STS, not generic LD/ST)
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // dynamic smem only (no static __shared__): the window base is 1024-B aligned, checked below
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sK = smem;
   uint8_t* sV = smem + TB;
   uint8_t* sQ = smem + 2 * TB;   // 2 stages
@@ -264,8 +300,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* sDS = smem + 5 * TB;  // 128 x 128 bf16, [kv][q] in two 64-column SW128 boxes
   float* sL = reinterpret_cast<float*>(smem + 5 * TB + 32768);  // [2][128] lse2
   float* sDel = sL + 256;                                      // [2][128] Delta
-  uint8_t* sDQ = smem + 5 * TB + 32768 + 2048;                 // 4 warps x 4 KB dQ staging (SW128)
-  __shared__ BwdBars bars;
+  uint8_t* sDQ = smem + 5 * TB + 32768 + 2048;                 // 4 warps x 2 x 4 KB dQ staging (SW128)
+  BwdBars& bars = *reinterpret_cast<BwdBars*>(smem + 5 * TB + 32768 + 2048 + 32768);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hsplit = p.head_split;
@@ -282,6 +318,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int nq = p.nqt - kt;
   const int n_items = nh * nq;
   const int h_first = g * p.G + hs * nh;
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1 KB alignment
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.kv_full, 1);
@@ -293,15 +330,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(&bars.do_empty, 1);
     mbar_init(&bars.s_full, 1);
     mbar_init(&bars.dp_full, 1);
-    mbar_init(&bars.p_full, 128);
-    mbar_init(&bars.ds_full, 128);
+    mbar_init(&bars.p_full, 256);
+    mbar_init(&bars.ds_full, 256);
     mbar_init(&bars.ds_empty, 1);
     mbar_init(&bars.dq_full, 1);
     mbar_init(&bars.dq_empty, 128);
     mbar_init(&bars.acc_full, 1);
     fence_mbar_init();
   }
-  if (warp == 9) {
+  if (warp == 12) {
     tmem_alloc(&bars.tmem_base, 512);
     tmem_relinquish();
   }
@@ -310,8 +347,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   tc_fence_after();
   const uint32_t tbase = bars.tmem_base;
 
-  if (warp == 8) {
+  if (warp == 13) {
     // ================= TMA producer =================
+    reg_dealloc<88>();
     if (lane == 0) {
       tma_prefetch_desc(&maps.q);
       tma_prefetch_desc(&maps.k);
@@ -341,9 +379,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tma_load_4d(sDO + bx * 16384, &maps.dout, &bars.do_full, bx * 64, h, qt * kTile, b);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 12) {
     // ================= MMA issuer =================
+    reg_dealloc<88>();
     if (lane == 0) {
+      TTT_TRACE_DECL(0);
       constexpr uint32_t idSP = idesc_bf16_f32(128, 128, false, false);  // S^T = K Q^T, dP^T = V dO^T
       constexpr uint32_t idKV = idesc_bf16_f32(128, D, false, true);     // dV += P^T dO, dK += dS^T Q
       constexpr uint32_t idDQ = idesc_bf16_f32(128, D, true, true);      // dQ = dS K
@@ -353,6 +393,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         return sdesc_sw128(base + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
       };
       auto mnmaj = [](uint32_t base, int ks) { return sdesc_sw128(base + ks * 2048, 16384, 1024); };
+      // P^T / dS^T (bf16, packed 2 per column) of query-column half hf sit at TMEM
+      // columns [64 hf, 64 hf + 32) of the S / dP regions (each half writes over its own S columns)
+      auto pcol = [](int ks) { return (uint32_t)(64 * (ks >> 2) + 8 * (ks & 3)); };
       auto issue_S = [&](int qs) {
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) umma_ss(tbase, kmaj(aK, ks), kmaj(aQ + qs * TB, ks), idSP, ks > 0);
@@ -361,7 +404,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) umma_ss(tbase + 128, kmaj(aV, ks), kmaj(aDO, ks), idSP, ks > 0);
       };
-      TTT_TRACE_DECL(0);
       mbar_wait(&bars.kv_full, 0);
       mbar_wait(&bars.q_full[0], 0);
       tc_fence_after();
@@ -374,22 +416,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int i = 0; i < n_items; ++i) {
         const int qs = i & 1;
         const bool more = i + 1 < n_items;
-        // dV += P^T dO   (A = P^T in TMEM cols [0,64))
+        // dV += P^T dO   (A = P^T in TMEM)
         TTT_TRACE_EV(0, 1, i);
         mbar_wait(&bars.p_full, i & 1);
         TTT_TRACE_EV(0, 2, i);
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          umma_ts(tbase + 256, tbase + ks * 8, mnmaj(aDO, ks), idKV, (i > 0 || ks > 0) ? 1u : 0u);
+          umma_ts(tbase + 256, tbase + pcol(ks), mnmaj(aDO, ks), idKV, (i > 0 || ks > 0) ? 1u : 0u);
         umma_commit(&bars.do_empty);
-        // dK += dS^T Q   (A = dS^T in TMEM cols [128,192))
+        // dK += dS^T Q   (A = dS^T in TMEM)
         mbar_wait(&bars.ds_full, i & 1);
         TTT_TRACE_EV(0, 3, i);
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          umma_ts(tbase + 384, tbase + 128 + ks * 8, mnmaj(aQ + qs * TB, ks), idKV, (i > 0 || ks > 0) ? 1u : 0u);
+          umma_ts(tbase + 384, tbase + 128 + pcol(ks), mnmaj(aQ + qs * TB, ks), idKV,
+                  (i > 0 || ks > 0) ? 1u : 0u);
         umma_commit(&bars.q_empty[qs]);
         // next S^T while this item's dQ is drained
         if (more) {
@@ -416,12 +459,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       umma_commit(&bars.acc_full);
     }
-  } else if (warp < 4) {
-    // ================= compute: P^T, dS^T (thread = key row) =================
-    const int row = warp * 32 + lane;
+  } else if (warp >= 4 && warp < 12) {
+    // ================= compute: P^T, dS^T (thread = key row, 64 query columns) =================
+    reg_alloc<136>();
+    const int quad = warp & 3, hf = (warp - 4) >> 2;
+    const int row = quad * 32 + lane;
     const int k = kt * kTile + row;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    const uint32_t tS = tbase + lane_off, tdP = tbase + lane_off + 128;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const uint32_t tS = tbase + lane_off + 64 * hf, tdP = tbase + lane_off + 128 + 64 * hf;
     const float sl2 = p.scale_log2;
     TTT_TRACE_DECL(1);
     for (int i = 0; i < n_items; ++i) {
@@ -429,72 +474,72 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int qt = kt + i % nq;
       mbar_wait(&bars.q_full[qs], (i >> 1) & 1);
       mbar_wait(&bars.s_full, i & 1);
-      if (threadIdx.x == 0) TTT_TRACE_EV(1, 1, i);
+      if (threadIdx.x == 128) TTT_TRACE_EV(1, 1, i);
       tc_fence_after();
-      const float* Lq = sL + qs * 128;
-      const float* Dq = sDel + qs * 128;
-      // allowed (k, q): k <= q and k < T  ->  column c allowed iff c >= k - qt*128 (and k < T)
-      const int cmin = (k < T) ? k - qt * kTile : kTile;  // columns [cmin, 128) allowed
-      float pr[128];
+      const float4* Lq = reinterpret_cast<const float4*>(sL + qs * 128 + 64 * hf);
+      const float4* Dq = reinterpret_cast<const float4*>(sDel + qs * 128 + 64 * hf);
+      float pr[64];
+      {
+        uint32_t raw[64];
+        tmem_ld64(tS, raw);
+        // allowed (k, q): k <= q and k < T; full tiles (qt > kt, whole key tile < T) skip the test
+        const bool full = (qt > kt) && (kt * kTile + kTile <= T);
+        const int cmin = (k < T) ? k - qt * kTile - 64 * hf : kTile;  // local columns [cmin, 64) allowed
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        uint32_t raw[32];
-        tmem_ld32(tS + c4 * 32, raw);
+        for (int c4 = 0; c4 < 16; ++c4) {
+          const float4 l4 = Lq[c4];
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int c = c4 * 32 + e;
-          const float x = __uint_as_float(raw[e]) * sl2 - Lq[c];
-          pr[c] = c >= cmin ? ex2(x) : 0.f;
+          for (int e = 0; e < 4; ++e) {
+            const int c = 4 * c4 + e;
+            const float x = ex2(fmaf(__uint_as_float(raw[c]), sl2, -lv[e]));
+            pr[c] = (full || c >= cmin) ? x : 0.f;
+          }
         }
       }
       {
         uint32_t pk[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(pr[2 * c], pr[2 * c + 1]);
-        tmem_st32(tS, pk);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(pr[64 + 2 * c], pr[64 + 2 * c + 1]);
-        tmem_st32(tS + 32, pk);
+        tmem_st32(tS, pk);  // P^T over this half's own (already read) S columns
       }
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars.p_full);
-      if (threadIdx.x == 0) TTT_TRACE_EV(1, 2, i);
+      if (threadIdx.x == 128) TTT_TRACE_EV(1, 2, i);
       mbar_wait(&bars.dp_full, i & 1);
-      if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, i);
+      if (threadIdx.x == 128) TTT_TRACE_EV(1, 3, i);
       mbar_wait(&bars.ds_empty, (i & 1) ^ 1);
       tc_fence_after();
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
+      for (int cc = 0; cc < 2; ++cc) {
         uint32_t raw[32];
         tmem_ld32(tdP + cc * 32, raw);
         uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int c = cc * 32 + 2 * e;
-          const float d0 = pr[c] * (__uint_as_float(raw[2 * e]) - Dq[c]);
-          const float d1 = pr[c + 1] * (__uint_as_float(raw[2 * e + 1]) - Dq[c + 1]);
-          pk[e] = pack_bf16(d0, d1);
+        for (int e4 = 0; e4 < 8; ++e4) {
+          const float4 d4 = Dq[cc * 8 + e4];
+          const int c = cc * 32 + 4 * e4;
+          pk[2 * e4] = pack_bf16(pr[c] * (__uint_as_float(raw[4 * e4]) - d4.x),
+                                 pr[c + 1] * (__uint_as_float(raw[4 * e4 + 1]) - d4.y));
+          pk[2 * e4 + 1] = pack_bf16(pr[c + 2] * (__uint_as_float(raw[4 * e4 + 2]) - d4.z),
+                                     pr[c + 3] * (__uint_as_float(raw[4 * e4 + 3]) - d4.w));
         }
-        tmem_st16(tdP + cc * 16, pk);  // dS^T (bf16) over the already-read dP^T columns
-        // smem dS: row = key row, q columns [cc*32, cc*32+32): box cc/2, 8-col chunks
-        uint8_t* boxp = sDS + (cc >> 1) * 16384 + row * 128;
+        tmem_st16(tdP + cc * 16, pk);  // dS^T (bf16) over this half's already-read dP^T columns
+        // smem dS: row = key row, q columns [64 hf + 32 cc, +32): box hf, 8-column chunks 4 cc + e8
+        uint8_t* boxp = sDS + hf * 16384 + row * 128;
 #pragma unroll
         for (int e8 = 0; e8 < 4; ++e8) {
-          const int chunk = (cc & 1) * 4 + e8;
-          uint4 v;
-          v.x = pk[e8 * 4 + 0];
-          v.y = pk[e8 * 4 + 1];
-          v.z = pk[e8 * 4 + 2];
-          v.w = pk[e8 * 4 + 3];
-          *reinterpret_cast<uint4*>(boxp + ((chunk ^ (row & 7)) << 4)) = v;
+          const int chunk = cc * 4 + e8;
+          *reinterpret_cast<uint4*>(boxp + ((chunk ^ (row & 7)) << 4)) =
+              make_uint4(pk[e8 * 4 + 0], pk[e8 * 4 + 1], pk[e8 * 4 + 2], pk[e8 * 4 + 3]);
         }
       }
       fence_async_smem();
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars.ds_full);
-      if (threadIdx.x == 0) TTT_TRACE_EV(1, 4, i);
+      if (threadIdx.x == 128) TTT_TRACE_EV(1, 4, i);
     }
     // ---- dK, dV accumulators -> global (fp32 atomics: head splits and steps add up) ----
     mbar_wait(&bars.acc_full, 0);
@@ -502,8 +547,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // tcgen05.ld is warp-collective (.sync.aligned): every lane loads, only rows k < T store
     const bool store = k < T;
     const size_t off = (((size_t)b * p.L + (store ? k : 0)) * p.Hkv + g) * D;
+    const int cbeg = hf * (D / 2);
 #pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 32) {
+    for (int c0 = cbeg; c0 < cbeg + D / 2; c0 += 32) {
       uint32_t raw[32];
       tmem_ld32(tbase + lane_off + 256 + c0, raw);
       if (store) {
@@ -521,55 +567,56 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                      c * __uint_as_float(raw[e + 2]), c * __uint_as_float(raw[e + 3]));
       }
     }
-  } else {
-    // ================= dQ drain (warps 4-7, thread = query row) =================
-    // TMEM -> registers (scaled by c) -> warp-private 4 KB SW128 staging -> TMA reduce-add
-    // into the tile-contiguous fp32 dq_acc (one 32 x 32 box per warp per column chunk).
-    const int wq = warp - 4;
+  } else if (warp < 4) {
+    // ================= dQ drain (warps 0-3, thread = query row) =================
+    // TMEM -> registers (scaled by c) -> warp-private SW128 staging (double buffered) ->
+    // TMA reduce-add into the tile-contiguous fp32 dq_acc (one 32 x 32 box per chunk).
+    reg_alloc<152>();
+    const int wq = warp;
     const uint32_t tQ = tbase + ((uint32_t)(wq * 32) << 16) + 128;
-    uint8_t* stage = sDQ + wq * 4096;
+    uint8_t* stage = sDQ + wq * 8192;
     if (lane == 0) tma_prefetch_desc(&maps.dqacc);
     TTT_TRACE_DECL(2);
     for (int i = 0; i < n_items; ++i) {
       const int h = h_first + i / nq, qt = kt + i % nq;
       mbar_wait(&bars.dq_full, i & 1);
-      if (threadIdx.x == 128) TTT_TRACE_EV(2, 1, i);
+      if (threadIdx.x == 0) TTT_TRACE_EV(2, 1, i);
       tc_fence_after();
-      float v[D];
+      uint32_t v[D];
 #pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 32) {
-        uint32_t raw[32];
-        tmem_ld32(tQ + c0, raw);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) v[c0 + e] = __uint_as_float(raw[e]) * p.scale;
-      }
+      for (int c0 = 0; c0 < D; c0 += 64) tmem_ld64(tQ + c0, *reinterpret_cast<uint32_t(*)[64]>(&v[c0]));
       tc_fence_before();
       mbar_arrive(&bars.dq_empty);
-      if (threadIdx.x == 128) TTT_TRACE_EV(2, 2, i);
+      if (threadIdx.x == 0) TTT_TRACE_EV(2, 2, i);
       const int row_base = (((b * p.Hq + h) * p.nqt + qt) * (D / 32)) * 128 + wq * 32;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
-        if (lane == 0) bulk_wait_read0();  // previous reduce finished reading the staging buffer
+        uint8_t* buf = stage + (cc & 1) * 4096;
+        if (lane == 0) bulk_wait_read1();  // the reduce that last used this buffer has read it
         __syncwarp();
 #pragma unroll
         for (int k4 = 0; k4 < 8; ++k4) {
-          float4 val = make_float4(v[cc * 32 + 4 * k4], v[cc * 32 + 4 * k4 + 1], v[cc * 32 + 4 * k4 + 2],
-                                   v[cc * 32 + 4 * k4 + 3]);
-          *reinterpret_cast<float4*>(stage + lane * 128 + ((k4 ^ (lane & 7)) << 4)) = val;
+          const float c = p.scale;
+          float4 val = make_float4(c * __uint_as_float(v[cc * 32 + 4 * k4]), c * __uint_as_float(v[cc * 32 + 4 * k4 + 1]),
+                                   c * __uint_as_float(v[cc * 32 + 4 * k4 + 2]),
+                                   c * __uint_as_float(v[cc * 32 + 4 * k4 + 3]));
+          *reinterpret_cast<float4*>(buf + lane * 128 + ((k4 ^ (lane & 7)) << 4)) = val;
         }
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_reduce_add_2d(&maps.dqacc, stage, 0, row_base + cc * 128);
+          tma_reduce_add_2d(&maps.dqacc, buf, 0, row_base + cc * 128);
           bulk_commit();
         }
       }
     }
     if (lane == 0) bulk_wait0();
+  } else {
+    reg_dealloc<24>();  // warps 14-15: idle
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc(tbase, 512);
+  if (warp == 12) tmem_dealloc(tbase, 512);
 }
 
 // ------------------------------------------------------------------ kernel 3
@@ -630,7 +677,7 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
   }
   // 2. main tensor-core kernel
   {
-    const int smem = 5 * kTile * D * 2 + 32768 + 2048 + 16384 + 1024;
+    const int smem = 5 * kTile * D * 2 + 32768 + 2048 + 32768 + 256;
     static bool attr_set = false;
     if (!attr_set) {
       cudaError_t e =
