@@ -70,165 +70,228 @@ __device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int
 }
 
 // ------------------------------------------------------------------ kernel 1
-// One HALF-warp per (b, r, kv head g): 16 lanes x (D/16) contiguous elements,
-// 16-byte loads, 4-level shuffle reductions. Rows per block = 2 * warps.
-// One HALF-warp per (b, r, kv head g): 16 lanes x (D/16) contiguous elements,
-// 16-byte loads, 4-level shuffle reductions. Rows per block = 2 * warps.
-template <int D>
-__global__ void __launch_bounds__(128) ttt_bwd_pre_kernel(const __grid_constant__ Params p, int rows_per_block) {
-  constexpr int E = D / 16;
-  extern __shared__ float pre_smem[];
-  const int lane = threadIdx.x & 31, hl = lane & 15;
-  const int lrow = threadIdx.x >> 4;  // row slot within the block
-  const long wid = (long)blockIdx.x * rows_per_block + lrow;
-  const long nrows = (long)p.B * p.L * p.Hkv;
-  const bool valid = wid < nrows;
-  const long w = valid ? wid : nrows - 1;  // clamp: shuffles stay warp-uniform
-  const int G = p.G;
-  const int g = (int)(w % p.Hkv);
-  const int r = (int)((w / p.Hkv) % p.L);
-  const int b = (int)(w / ((long)p.Hkv * p.L));
-  const int T = p.seq_lens[b];
-  float* sdq = pre_smem + (size_t)lrow * (G * D + 2 * G);  // [G][D] dq accumulators
-  float* sdel = sdq + G * D;
-  float* sl2 = sdel + G;
-  const size_t kv_off = (((size_t)b * p.L + r) * p.Hkv + g) * D + hl * E;
+// HBM-streaming, TMA-staged: a persistent block walks groups of NR consecutive
+// (b, r, g) rows. For such a group every operand is ONE contiguous block in HBM
+// (q / dO / O / O_lo: NR*G*D bf16; K_i, V_i: NR*D bf16; dK_i, dV_i: NR*D fp32), so
+// thread 0 moves each with a single 1-D cp.async.bulk into a double-buffered
+// stage; dK_i / dV_i are accumulated in place in shared memory and written back
+// with bulk stores. 16 lanes per row, D/16 contiguous elements per lane.
+struct PreLayout {
+  int NR, G, D, step, acc, has_lo;
+  uint32_t off_q, off_do, off_o, off_olo, off_k, off_v, off_dk, off_dv, stage_bytes, off_dq, off_sc, total;
+  __host__ __device__ void init(int nr, int g, int d, int j, int accumulate, int lo) {
+    NR = nr; G = g; D = d; step = j; acc = accumulate; has_lo = lo;
+    const uint32_t qb = (uint32_t)nr * g * d * 2, kb = (uint32_t)nr * d * 2, fb = (uint32_t)nr * d * 4;
+    off_q = 0; off_do = qb; off_o = 2 * qb; off_olo = 3 * qb;
+    off_k = 4 * qb; off_v = off_k + j * kb; off_dk = off_v + j * kb; off_dv = off_dk + j * fb;
+    stage_bytes = (off_dv + j * fb + 127) & ~127u;
+    off_dq = 2 * stage_bytes;
+    off_sc = off_dq;                                    // fp32 [NR][G] x2: Delta, lse2
+    total = off_sc + 2u * nr * g * 4 + 64;              // + 2 mbarriers
+  }
+};
 
-  for (int hh = 0; hh < G; ++hh) {
-    const int h = g * G + hh;
-    const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + hl * E;
-    float o[E], d[E];
-    ld_row<D>(p.o, q_off, o);
-    ld_row<D>(p.dout, q_off, d);
-    if (p.o_lo) {  // O = bf16 out + bf16 residual: Delta from ~16-bit-accurate O
-      float lo[E];
-      ld_row<D>(p.o_lo, q_off, lo);
+__device__ __forceinline__ void bulk_store_1d(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load_1d_(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+template <int D>
+__device__ __forceinline__ void lds_row(const uint8_t* s, float (&x)[D / 16]) {
+  constexpr int E = D / 16;
+  if constexpr (E == 8) {
+    const uint4 u = *reinterpret_cast<const uint4*>(s);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-      for (int e = 0; e < E; ++e) o[e] += lo[e];
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+      x[2 * e] = f.x;
+      x[2 * e + 1] = f.y;
     }
-    float acc = 0.f;
+  } else {
+    const uint2 u = *reinterpret_cast<const uint2*>(s);
+    const uint32_t w[2] = {u.x, u.y};
 #pragma unroll
-    for (int e = 0; e < E; ++e) acc = fmaf(o[e], d[e], acc);
-    const float delta = half_allsum(acc);  // Delta_r = dO_r . O_r
-    const size_t li = ((size_t)b * p.Hq + h) * p.L + r;
-    const float l2 = p.lse_in[li] * kLog2e;
-    if (hl == 0) {
-      if (valid) {
-        p.delta[li] = delta;
-        p.lse2[li] = l2;
-      }
-      sdel[hh] = delta;
-      sl2[hh] = l2;
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e) sdq[hh * D + hl * E + e] = 0.f;
-  }
-  __syncwarp();
-  if (valid && !p.accumulate) {
-    float4* dk4 = reinterpret_cast<float4*>(p.dk + kv_off);
-    float4* dv4 = reinterpret_cast<float4*>(p.dv + kv_off);
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int e = 0; e < E / 4; ++e) {
-      dk4[e] = z;
-      dv4[e] = z;
+    for (int e = 0; e < 2; ++e) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+      x[2 * e] = f.x;
+      x[2 * e + 1] = f.y;
     }
   }
-  const bool act = valid && (r < T);  // diagonal keys exist only for rows r < T_b (Alg. 2 m_pad)
-  // steps in chunks of 4: all K_i / V_i rows (and dK_i / dV_i for the RMW) of a chunk are
-  // loaded together and the 8 dot products of a head are reduced with interleaved shuffles.
-  constexpr int CH = 4;
-  for (int i0 = 0; i0 < p.step; i0 += CH) {
-    const int ni = min(CH, p.step - i0);
-    float kk[CH][E], vv[CH][E], dk[CH][E], dv[CH][E];
-#pragma unroll
-    for (int u = 0; u < CH; ++u) {
-      if (u < ni) {
-        ld_row<D>(p.ks[i0 + u], kv_off, kk[u]);
-        ld_row<D>(p.vs[i0 + u], kv_off, vv[u]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) kk[u][e] = vv[u][e] = 0.f;
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) ttt_bwd_pre_kernel(const __grid_constant__ Params p, PreLayout lay) {
+  constexpr int E = D / 16;
+  extern __shared__ __align__(128) uint8_t psm[];
+  const int tid = threadIdx.x, hl = tid & 15, lr = tid >> 4;
+  const int NR = lay.NR, G = p.G, j = p.step;
+  const long nrows = (long)p.B * p.L * p.Hkv;
+  const long ngroups = (nrows + NR - 1) / NR;
+  uint64_t* full = reinterpret_cast<uint64_t*>(psm + lay.total - 64);
+  float* sdel = reinterpret_cast<float*>(psm + lay.off_sc);
+  float* sl2 = sdel + NR * G;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](long grp, int st) {  // thread 0 only
+    const long w0 = grp * NR;
+    const int nv = (int)min((long)NR, nrows - w0);
+    uint8_t* base = psm + st * lay.stage_bytes;
+    const uint32_t qb = (uint32_t)nv * G * D * 2, kb = (uint32_t)nv * D * 2, fb = (uint32_t)nv * D * 4;
+    uint32_t bytes = 3 * qb + j * 2 * kb + (lay.has_lo ? qb : 0) + (lay.acc ? j * 2 * fb : 0);
+    mbar_expect_tx(&full[st], bytes);
+    const size_t qo = (size_t)w0 * G * D, ko = (size_t)w0 * D;
+    bulk_load_1d_(base + lay.off_q, reinterpret_cast<const __nv_bfloat16*>(p.q) + qo, qb, &full[st]);
+    bulk_load_1d_(base + lay.off_do, reinterpret_cast<const __nv_bfloat16*>(p.dout) + qo, qb, &full[st]);
+    bulk_load_1d_(base + lay.off_o, reinterpret_cast<const __nv_bfloat16*>(p.o) + qo, qb, &full[st]);
+    if (lay.has_lo)
+      bulk_load_1d_(base + lay.off_olo, reinterpret_cast<const __nv_bfloat16*>(p.o_lo) + qo, qb, &full[st]);
+    for (int i = 0; i < j; ++i) {
+      bulk_load_1d_(base + lay.off_k + i * (NR * D * 2), reinterpret_cast<const __nv_bfloat16*>(p.ks[i]) + ko, kb,
+                    &full[st]);
+      bulk_load_1d_(base + lay.off_v + i * (NR * D * 2), reinterpret_cast<const __nv_bfloat16*>(p.vs[i]) + ko, kb,
+                    &full[st]);
+      if (lay.acc) {
+        bulk_load_1d_(base + lay.off_dk + i * (NR * D * 4), p.dks[i] + ko, fb, &full[st]);
+        bulk_load_1d_(base + lay.off_dv + i * (NR * D * 4), p.dvs[i] + ko, fb, &full[st]);
       }
-#pragma unroll
-      for (int e = 0; e < E; ++e) dk[u][e] = dv[u][e] = 0.f;
     }
+  };
+  long grp = blockIdx.x;
+  if (tid == 0 && grp < ngroups) issue(grp, 0);
+  for (int n = 0; grp < ngroups; ++n, grp += gridDim.x) {
+    const int st = n & 1;
+    const long nxt = grp + gridDim.x;
+    if (tid == 0 && nxt < ngroups) {
+      bulk_wait_read0();  // bulk stores of group n-1 (same stage as n+1) have read their smem
+      issue(nxt, st ^ 1);
+    }
+    mbar_wait(&full[st], (n >> 1) & 1);
+    uint8_t* base = psm + st * lay.stage_bytes;
+    const long w = grp * NR + lr;
+    // ghost threads (lr >= NR) alias row 0 for loads and shuffles but store nothing
+    const bool ghost = lr >= NR;
+    const bool valid = w < nrows && !ghost;
+    const long wc = valid ? w : (ghost ? grp * NR : nrows - 1);
+    const int g = (int)(wc % p.Hkv);
+    const int r = (int)((wc / p.Hkv) % p.L);
+    const int b = (int)(wc / ((long)p.Hkv * p.L));
+    const bool act = valid && r < p.seq_lens[b];  // diagonal keys exist only for rows r < T_b
+    const int lrc = lr < NR ? lr : 0;
+    // ---- Delta, lse2 per head; dq accumulators zeroed ----
     for (int hh = 0; hh < G; ++hh) {
+      const uint32_t ro = ((uint32_t)(lrc * G + hh) * D + hl * E) * 2;
+      float o[E], d[E];
+      lds_row<D>(base + lay.off_o + ro, o);
+      lds_row<D>(base + lay.off_do + ro, d);
+      if (lay.has_lo) {
+        float lo[E];
+        lds_row<D>(base + lay.off_olo + ro, lo);
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[e] += lo[e];
+      }
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc = fmaf(o[e], d[e], acc);
+      const float delta = half_allsum(acc);  // Delta_r = dO_r . O_r
       const int h = g * G + hh;
-      const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + hl * E;
-      float qq[E], dd[E];
-      ld_row<D>(p.q, q_off, qq);
-      ld_row<D>(p.dout, q_off, dd);
-      float s[CH], dp[CH];
-#pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        s[u] = 0.f;
-        dp[u] = 0.f;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          s[u] = fmaf(qq[e], kk[u][e], s[u]);
-          dp[u] = fmaf(dd[e], vv[u][e], dp[u]);
+      const size_t li = ((size_t)b * p.Hq + h) * p.L + r;
+      const float l2 = p.lse_in[li] * kLog2e;
+      if (hl == 0 && !ghost) {
+        if (valid) {
+          p.delta[li] = delta;
+          p.lse2[li] = l2;
         }
+        sdel[lrc * G + hh] = delta;
+        sl2[lrc * G + hh] = l2;
       }
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-#pragma unroll
-        for (int u = 0; u < CH; ++u) {
-          s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
-          dp[u] += __shfl_xor_sync(0xffffffffu, dp[u], o);
-        }
-      }
-      const float l2 = sl2[hh], del = sdel[hh];
-      float dqa[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) dqa[e] = 0.f;
-#pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        const float pr = (act && u < ni) ? ex2(s[u] * p.scale_log2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
-        const float cds = p.scale * pr * (dp[u] - del);                           // c ds_i, ds_i = p_i (dp_i - Delta)
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          dk[u][e] = fmaf(cds, qq[e], dk[u][e]);
-          dv[u][e] = fmaf(pr, dd[e], dv[u][e]);
-          dqa[e] = fmaf(cds, kk[u][e], dqa[e]);
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) sdq[hh * D + hl * E + e] += dqa[e];
     }
-    if (valid) {
+    if (!lay.acc && !ghost) {  // overwrite mode: step gradients start from zero in the stage
+      for (int i = 0; i < j; ++i) {
+        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + lrc * D + hl * E;
+        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + lrc * D + hl * E;
 #pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        if (u >= ni) break;
-        float4* dk4 = reinterpret_cast<float4*>(p.dks[i0 + u] + kv_off);
-        float4* dv4 = reinterpret_cast<float4*>(p.dvs[i0 + u] + kv_off);
+        for (int e = 0; e < E; ++e) dkr[e] = dvr[e] = 0.f;
+      }
+      if (valid) {  // dK_0 / dV_0 rows: the main kernel adds into them
+        float4* dk4 = reinterpret_cast<float4*>(p.dk + (size_t)w * D + hl * E);
+        float4* dv4 = reinterpret_cast<float4*>(p.dv + (size_t)w * D + hl * E);
 #pragma unroll
-        for (int e = 0; e < E / 4; ++e) {
-          float4 a = make_float4(dk[u][4 * e], dk[u][4 * e + 1], dk[u][4 * e + 2], dk[u][4 * e + 3]);
-          float4 c = make_float4(dv[u][4 * e], dv[u][4 * e + 1], dv[u][4 * e + 2], dv[u][4 * e + 3]);
-          if (p.accumulate) {
-            const float4 a0 = dk4[e], c0 = dv4[e];
-            a.x += a0.x; a.y += a0.y; a.z += a0.z; a.w += a0.w;
-            c.x += c0.x; c.y += c0.y; c.z += c0.z; c.w += c0.w;
+        for (int e = 0; e < E / 4; ++e) dk4[e] = dv4[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    __syncwarp();
+    __syncthreads();  // Delta / lse2 of every row visible (ghost rows read row 0)
+    // ---- TTT diagonal keys (Alg. 2 M_suffix): p_i, dp_i, ds_i; dq, dK_i, dV_i ----
+    for (int hh = 0; hh < G; ++hh) {
+      const uint32_t ro = ((uint32_t)(lrc * G + hh) * D + hl * E) * 2;
+      float qq[E], dd[E], dq[E];
+      lds_row<D>(base + lay.off_q + ro, qq);
+      lds_row<D>(base + lay.off_do + ro, dd);
+#pragma unroll
+      for (int e = 0; e < E; ++e) dq[e] = 0.f;
+      const float l2 = sl2[lrc * G + hh], del = sdel[lrc * G + hh];
+      for (int i = 0; i < j; ++i) {
+        float kk[E], vv[E];
+        lds_row<D>(base + lay.off_k + i * (NR * D * 2) + (lrc * D + hl * E) * 2, kk);
+        lds_row<D>(base + lay.off_v + i * (NR * D * 2) + (lrc * D + hl * E) * 2, vv);
+        float s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          s = fmaf(qq[e], kk[e], s);
+          dp = fmaf(dd[e], vv[e], dp);
+        }
+#pragma unroll
+        for (int o2 = 8; o2 > 0; o2 >>= 1) {
+          s += __shfl_xor_sync(0xffffffffu, s, o2);
+          dp += __shfl_xor_sync(0xffffffffu, dp, o2);
+        }
+        const float pr = act ? ex2(s * p.scale_log2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
+        const float cds = p.scale * pr * (dp - del);              // c ds_i, ds_i = p_i (dp_i - Delta)
+        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + lrc * D + hl * E;
+        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + lrc * D + hl * E;
+#pragma unroll
+        for (int e = 0; e < E; ++e) dq[e] = fmaf(cds, kk[e], dq[e]);
+        if (!ghost) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            dkr[e] = fmaf(cds, qq[e], dkr[e]);
+            dvr[e] = fmaf(pr, dd[e], dvr[e]);
           }
-          dk4[e] = a;
-          dv4[e] = c;
         }
       }
-    }
-  }
-  __syncwarp();
-  if (valid) {
-    for (int hh = 0; hh < G; ++hh) {
-      const int h = g * G + hh;
-      float* dst = p.dq_acc + dqacc_index(p, b, h, r, hl * E);
+      if (valid) {
+        const int h = g * G + hh;
+        float* dst = p.dq_acc + dqacc_index(p, b, h, r, hl * E);
 #pragma unroll
-      for (int e = 0; e < E / 4; ++e)
-        reinterpret_cast<float4*>(dst)[e] =
-            make_float4(sdq[hh * D + hl * E + 4 * e], sdq[hh * D + hl * E + 4 * e + 1],
-                        sdq[hh * D + hl * E + 4 * e + 2], sdq[hh * D + hl * E + 4 * e + 3]);
+        for (int e = 0; e < E / 4; ++e)
+          reinterpret_cast<float4*>(dst)[e] = make_float4(dq[4 * e], dq[4 * e + 1], dq[4 * e + 2], dq[4 * e + 3]);
+      }
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      const long w0 = grp * NR;
+      const int nv = (int)min((long)NR, nrows - w0);
+      for (int i = 0; i < j; ++i) {
+        bulk_store_1d(p.dks[i] + (size_t)w0 * D, base + lay.off_dk + i * (NR * D * 4), (uint32_t)nv * D * 4);
+        bulk_store_1d(p.dvs[i] + (size_t)w0 * D, base + lay.off_dv + i * (NR * D * 4), (uint32_t)nv * D * 4);
+      }
+      bulk_commit();
     }
   }
+  if (tid == 0) bulk_wait0();
 }
 
 // ------------------------------------------------------------------ kernel 2
@@ -658,21 +721,26 @@ template <int D>
 cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t st) {
   Params p = p_in;
   p.head_split = pick_head_split(p);
-  // 1. pre-pass
+  // 1. pre-pass (TMA-staged, persistent)
   {
-    const int rows_per_block = 2 * std::max(1, std::min(4, 32 / std::max(1, p.G)));
-    const size_t smem = (size_t)rows_per_block * (p.G * D + 2 * p.G) * sizeof(float);
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
+    PreLayout lay;
+    int nr = 8;
+    for (; nr > 1; nr >>= 1) {
+      lay.init(nr, p.G, D, p.step, p.accumulate, p.o_lo != nullptr);
+      if (lay.total <= 220 * 1024) break;
     }
+    lay.init(nr, p.G, D, p.step, p.accumulate, p.o_lo != nullptr);
+    if (lay.total > 227 * 1024) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)lay.total);
+    if (e != cudaSuccess) return e;
     const long rows = (long)p.B * p.L * p.Hkv;
+    const long groups = (rows + nr - 1) / nr;
+    const int blocks = (int)std::min<long>(groups, 148);
     prof_mark(kKindBwdPre, true, st);
-    ttt_bwd_pre_kernel<D><<<(unsigned)((rows + rows_per_block - 1) / rows_per_block), rows_per_block * 16, smem, st>>>(
-        p, rows_per_block);
+    ttt_bwd_pre_kernel<D><<<blocks, 128, lay.total, st>>>(p, lay);
     prof_mark(kKindBwdPre, false, st);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   // 2. main tensor-core kernel

@@ -21,6 +21,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "ptx_sm100.cuh"
 #include "ttt_params.cuh"
 
@@ -326,88 +328,166 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // softmax over i (Alg. 1 "concat s_i"):
 //   A_d = log2 sum_i 2^{t_i},  O_d = sum_i 2^{t_i - A_d} V_i[r]
 // written into lse (log2 units) and out (bf16); the main kernel merges them.
-// HBM-streaming: one half-warp per (b, r, kv head g), 16-byte loads; the
-// K_i / V_i rows are read once per group and shared by its G query heads.
+// HBM-streaming, TMA-staged: a persistent block walks groups of NR consecutive
+// (b, r, g) rows; q (NR*G*D), K_i and V_i (NR*D each) of a group are single
+// contiguous blocks moved by 1-D cp.async.bulk into a double-buffered stage.
+struct DiagLayout {
+  int NR;
+  uint32_t off_q, off_k, off_v, stage_bytes, total;
+  __host__ __device__ void init(int nr, int g, int d, int j) {
+    NR = nr;
+    off_q = 0;
+    off_k = (uint32_t)nr * g * d * 2;
+    off_v = off_k + (uint32_t)j * nr * d * 2;
+    stage_bytes = (off_v + (uint32_t)j * nr * d * 2 + 127) & ~127u;
+    total = 2 * stage_bytes + 64;
+  }
+};
+
 template <int D>
-__global__ void __launch_bounds__(256) ttt_fwd_diag_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(256) ttt_fwd_diag_kernel(const __grid_constant__ Params p, DiagLayout lay) {
   constexpr int E = D / 16;
-  const int hl = threadIdx.x & 15;
-  const long wid = (long)blockIdx.x * 16 + (threadIdx.x >> 4);
+  extern __shared__ __align__(128) uint8_t dsm[];
+  const int tid = threadIdx.x, hl = tid & 15, lr = tid >> 4;
+  const int NR = lay.NR, G = p.G, j = p.step;
   const long nrows = (long)p.B * p.L * p.Hkv;
-  const bool valid = wid < nrows;
-  const long w = valid ? wid : nrows - 1;  // clamp: shuffles stay warp-uniform
-  const int g = (int)(w % p.Hkv);
-  const int r = (int)((w / p.Hkv) % p.L);
-  const int b = (int)(w / ((long)p.Hkv * p.L));
-  const bool act = valid && r < p.seq_lens[b];
-  const size_t kv_off = (((size_t)b * p.L + r) * p.Hkv + g) * D + hl * E;
-  for (int hh = 0; hh < p.G; ++hh) {
-    const int h = g * p.G + hh;
-    const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + hl * E;
-    float qf[E], o[E];
-    ld_row<D>(p.q, q_off, qf);
+  const long ngroups = (nrows + NR - 1) / NR;
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + lay.total - 64);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](long grp, int st) {  // thread 0 only
+    const long w0 = grp * NR;
+    const int nv = (int)min((long)NR, nrows - w0);
+    uint8_t* base = dsm + st * lay.stage_bytes;
+    const uint32_t qb = (uint32_t)nv * G * D * 2, kb = (uint32_t)nv * D * 2;
+    mbar_expect_tx(&full[st], qb + 2 * j * kb);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(base + lay.off_q)),
+                 "l"(reinterpret_cast<const __nv_bfloat16*>(p.q) + (size_t)w0 * G * D), "r"(qb),
+                 "r"(smem_u32(&full[st]))
+                 : "memory");
+    for (int i = 0; i < j; ++i) {
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(base + lay.off_k + i * NR * D * 2)),
+                   "l"(reinterpret_cast<const __nv_bfloat16*>(p.ks[i]) + (size_t)w0 * D), "r"(kb),
+                   "r"(smem_u32(&full[st]))
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(base + lay.off_v + i * NR * D * 2)),
+                   "l"(reinterpret_cast<const __nv_bfloat16*>(p.vs[i]) + (size_t)w0 * D), "r"(kb),
+                   "r"(smem_u32(&full[st]))
+                   : "memory");
+    }
+  };
+  long grp = blockIdx.x;
+  if (tid == 0 && grp < ngroups) issue(grp, 0);
+  for (int n = 0; grp < ngroups; ++n, grp += gridDim.x) {
+    const int st = n & 1;
+    const long nxt = grp + gridDim.x;
+    if (tid == 0 && nxt < ngroups) issue(nxt, st ^ 1);  // stage st^1 was released by the last __syncthreads
+    mbar_wait(&full[st], (n >> 1) & 1);
+    const uint8_t* base = dsm + st * lay.stage_bytes;
+    const long w = grp * NR + lr;
+    const bool ghost = lr >= NR;
+    const bool valid = w < nrows && !ghost;
+    const long wc = valid ? w : grp * NR;
+    const int lrc = ghost ? 0 : (int)(wc - grp * NR);
+    const int g = (int)(wc % p.Hkv);
+    const int r = (int)((wc / p.Hkv) % p.L);
+    const int b = (int)(wc / ((long)p.Hkv * p.L));
+    const bool act = valid && r < p.seq_lens[b];
+    for (int hh = 0; hh < G; ++hh) {
+      float qf[E], o[E];
+      {
+        const uint8_t* qs = base + lay.off_q + ((uint32_t)(lrc * G + hh) * D + hl * E) * 2;
+        const uint4 u = *reinterpret_cast<const uint4*>(qs);
+        if constexpr (E == 8) {
+          const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int e = 0; e < E; ++e) o[e] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    constexpr int CH = 4;  // steps per chunk: loads and shuffle chains of a chunk overlap
-    for (int i0 = 0; i0 < p.step; i0 += CH) {
-      const int ni = min(CH, p.step - i0);
-      float kk[CH][E], vv[CH][E], t[CH];
-#pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        if (u < ni) {
-          ld_row<D>(p.ks[i0 + u], kv_off, kk[u]);
-          ld_row<D>(p.vs[i0 + u], kv_off, vv[u]);
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+            qf[2 * e] = f.x;
+            qf[2 * e + 1] = f.y;
+          }
         } else {
+          const uint2 u2 = *reinterpret_cast<const uint2*>(qs);
+          const uint32_t wv[2] = {u2.x, u2.y};
 #pragma unroll
-          for (int e = 0; e < E; ++e) kk[u][e] = vv[u][e] = 0.f;
+          for (int e = 0; e < 2; ++e) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+            qf[2 * e] = f.x;
+            qf[2 * e + 1] = f.y;
+          }
         }
-        t[u] = 0.f;
-#pragma unroll
-        for (int e = 0; e < E; ++e) t[u] = fmaf(qf[e], kk[u][e], t[u]);
       }
 #pragma unroll
-      for (int o2 = 8; o2 > 0; o2 >>= 1) {
+      for (int e = 0; e < E; ++e) o[e] = 0.f;
+      float m = -INFINITY, l = 0.f;
+      for (int i = 0; i < j; ++i) {
+        float kk[E], vv[E];
+        const uint32_t ro = (uint32_t)(i * NR + lrc) * D * 2 + hl * E * 2;
+        {
+          const uint8_t* kp = base + lay.off_k + ro;
+          const uint8_t* vp = base + lay.off_v + ro;
+          if constexpr (E == 8) {
+            const uint4 uk = *reinterpret_cast<const uint4*>(kp), uv = *reinterpret_cast<const uint4*>(vp);
+            const uint32_t wk[4] = {uk.x, uk.y, uk.z, uk.w}, wvv[4] = {uv.x, uv.y, uv.z, uv.w};
 #pragma unroll
-        for (int u = 0; u < CH; ++u) t[u] += __shfl_xor_sync(0xffffffffu, t[u], o2);
+            for (int e = 0; e < 4; ++e) {
+              const float2 fk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wk[e]));
+              const float2 fv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wvv[e]));
+              kk[2 * e] = fk.x; kk[2 * e + 1] = fk.y;
+              vv[2 * e] = fv.x; vv[2 * e + 1] = fv.y;
+            }
+          } else {
+            const uint2 uk = *reinterpret_cast<const uint2*>(kp), uv = *reinterpret_cast<const uint2*>(vp);
+            const uint32_t wk[2] = {uk.x, uk.y}, wvv[2] = {uv.x, uv.y};
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const float2 fk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wk[e]));
+              const float2 fv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wvv[e]));
+              kk[2 * e] = fk.x; kk[2 * e + 1] = fk.y;
+              vv[2 * e] = fv.x; vv[2 * e + 1] = fv.y;
+            }
+          }
+        }
+        float acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc = fmaf(qf[e], kk[e], acc);
+        const float t = half_allsum(acc) * p.scale_log2;  // s_i = c q_r . k_i (log2 units)
+        const float mn = fmaxf(m, t);
+        const float a = ex2(m - mn), wgt = ex2(t - mn);
+        l = l * a + wgt;
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[e] = fmaf(wgt, vv[e], o[e] * a);
+        m = mn;
       }
-      float mn = m;
-#pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        t[u] = u < ni ? t[u] * p.scale_log2 : -INFINITY;  // s_i = c q_r . k_i (log2 units)
-        mn = fmaxf(mn, t[u]);
+      if (act) {
+        const int h = g * G + hh;
+        const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + hl * E;
+        const float inv = 1.f / l;
+        __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
+        if constexpr (E == 8) {
+          uint4 u;
+          u.x = pack_bf16(o[0] * inv, o[1] * inv);
+          u.y = pack_bf16(o[2] * inv, o[3] * inv);
+          u.z = pack_bf16(o[4] * inv, o[5] * inv);
+          u.w = pack_bf16(o[6] * inv, o[7] * inv);
+          *reinterpret_cast<uint4*>(op) = u;
+        } else {
+          uint2 u;
+          u.x = pack_bf16(o[0] * inv, o[1] * inv);
+          u.y = pack_bf16(o[2] * inv, o[3] * inv);
+          *reinterpret_cast<uint2*>(op) = u;
+        }
+        if (hl == 0) p.lse[((size_t)b * p.Hq + h) * p.L + r] = m + log2f(l);
       }
-      const float a = ex2(m - mn);
-      l *= a;
-#pragma unroll
-      for (int e = 0; e < E; ++e) o[e] *= a;
-#pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        const float wgt = ex2(t[u] - mn);
-        l += wgt;
-#pragma unroll
-        for (int e = 0; e < E; ++e) o[e] = fmaf(wgt, vv[u][e], o[e]);
-      }
-      m = mn;
     }
-    if (act) {
-      const float inv = 1.f / l;
-      __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
-      if constexpr (E == 8) {
-        uint4 u;
-        u.x = pack_bf16(o[0] * inv, o[1] * inv);
-        u.y = pack_bf16(o[2] * inv, o[3] * inv);
-        u.z = pack_bf16(o[4] * inv, o[5] * inv);
-        u.w = pack_bf16(o[6] * inv, o[7] * inv);
-        *reinterpret_cast<uint4*>(op) = u;
-      } else {
-        uint2 u;
-        u.x = pack_bf16(o[0] * inv, o[1] * inv);
-        u.y = pack_bf16(o[2] * inv, o[3] * inv);
-        *reinterpret_cast<uint2*>(op) = u;
-      }
-      if (hl == 0) p.lse[((size_t)b * p.Hq + h) * p.L + r] = m + log2f(l);
-    }
+    __syncthreads();  // stage st fully consumed before it is refilled
   }
 }
 
@@ -421,9 +501,23 @@ cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, cudaStream_t st) 
     attr_set = true;
   }
   if (p.step > 0) {
+    DiagLayout lay;
+    int nr = 16;
+    for (; nr > 1; nr >>= 1) {
+      lay.init(nr, p.G, D, p.step);
+      if (lay.total <= 200 * 1024) break;
+    }
+    lay.init(nr, p.G, D, p.step);
+    if (lay.total > 227 * 1024) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(ttt_fwd_diag_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)lay.total);
+    if (e != cudaSuccess) return e;
     const long rows = (long)p.B * p.L * p.Hkv;
+    const long groups = (rows + nr - 1) / nr;
+    const int per_sm = lay.total <= 110 * 1024 ? 2 : 1;
+    const int blocks = (int)std::min<long>(groups, 148L * per_sm);
     prof_mark(kKindFwdDiag, true, st);
-    ttt_fwd_diag_kernel<D><<<(unsigned)((rows + 15) / 16), 256, 0, st>>>(p);
+    ttt_fwd_diag_kernel<D><<<blocks, 256, lay.total, st>>>(p, lay);
     prof_mark(kKindFwdDiag, false, st);
   }
   const int npairs = (p.G + 1) / 2;
