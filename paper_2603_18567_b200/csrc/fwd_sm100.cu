@@ -27,6 +27,19 @@
 #include "ttt_params.cuh"
 
 namespace tttk {
+#ifdef TTT_TRACE
+__device__ unsigned long long g_ttt_ftrace[4][kTraceCap];
+__device__ unsigned int g_ttt_ftrace_cta;
+#define g_ttt_trace g_ttt_ftrace
+#define g_ttt_trace_cta g_ttt_ftrace_cta
+extern "C" int ttt_debug_ftrace_read(void* host, unsigned int cta) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(host, g_ttt_ftrace, sizeof(g_ttt_ftrace)) != cudaSuccess) return 1;
+  unsigned long long z[4 * 1024] = {};
+  for (int r = 0; r < 4; ++r) cudaMemcpyToSymbol(g_ttt_ftrace, z, sizeof(z), (size_t)r * kTraceCap * 8);
+  return cudaMemcpyToSymbol(g_ttt_ftrace_cta, &cta, sizeof(cta)) != cudaSuccess;
+}
+#endif
 namespace {
 
 constexpr int kFwdThreads = 320;
@@ -137,8 +150,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           umma_ts(tbase + 256 + slot * 128, tbase + slot * 128 + ks * 8, sdesc_sw128(va + ks * 2048, 16384, 1024),
                   idO, (acc || ks > 0) ? 1u : 0u);
       };
+      TTT_TRACE_DECL(0);
+      TTT_TRACE_EV(0, 9, 0);
       mbar_wait(&bars.q, 0);
       mbar_wait(&bars.k_full[0], 0);
+      TTT_TRACE_EV(0, 8, 0);
       tc_fence_after();
       issue_S(0, 0);
       umma_commit(&bars.s_full[0]);
@@ -152,7 +168,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const bool more = n + 1 < nkv;
         const int kst = (n + 1) & 1, kph = ((n + 1) >> 1) & 1;
         mbar_wait(&bars.v_full[vst], vph);
+        TTT_TRACE_EV(0, 1, n);
         mbar_wait(&bars.p_full[0], n & 1);
+        TTT_TRACE_EV(0, 2, n);
         tc_fence_after();
         issue_PV(0, vst, n > 0);
         if (more) {
@@ -165,6 +183,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         if (has1) {
           mbar_wait(&bars.p_full[1], n & 1);
+          TTT_TRACE_EV(0, 3, n);
           tc_fence_after();
           issue_PV(1, vst, n > 0);
           umma_commit(&bars.v_empty[vst]);
@@ -194,8 +213,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const uint32_t tO = tbase + lane_off + 256 + slot * 128;
       const float sl2 = p.scale_log2;
       float m_run = -INFINITY, l_run = 0.f;
+      TTT_TRACE_DECL(1);
+      TTT_TRACE_DECL(2);
       for (int n = 0; n < nkv; ++n) {
         mbar_wait(&bars.s_full[slot], n & 1);
+        if (threadIdx.x == 0) TTT_TRACE_EV(1, 1, n);
+        if (threadIdx.x == 128) TTT_TRACE_EV(2, 1, n);
         tc_fence_after();
         float s[128];
 #pragma unroll
@@ -254,6 +277,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars.p_full[slot]);
+        if (threadIdx.x == 0) TTT_TRACE_EV(1, 2, n);
+        if (threadIdx.x == 128) TTT_TRACE_EV(2, 2, n);
       }
       // ---- epilogue: merge the diagonal partial (fwd_diag_kernel), normalise, store ----
       // The j diagonal keys of row r (Alg. 1 "concat s_i") were reduced
@@ -270,7 +295,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int c = 0; c < D / 8; ++c) od[c] = *reinterpret_cast<const uint4*>(orow + c * 8);
       }
+      if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, 0);
       mbar_wait(&bars.o_full[slot], 0);
+      if (threadIdx.x == 0) TTT_TRACE_EV(1, 4, 0);
       tc_fence_after();
       const float m_f = fmaxf(m_run, A_d);
       const float alpha = ex2(m_run - m_f);
@@ -316,6 +343,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
+      if (threadIdx.x == 0) TTT_TRACE_EV(1, 5, 0);
     }
   }
   tc_fence_before();
