@@ -233,20 +233,18 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
     stream = torch.cuda.current_stream(dev)
     S = shape.ttt_steps
 
-    # draft-layer gradient bucket (synthetic stand-in), bf16, split per bwd call
-    buckets, works = [], []
+    # draft-layer gradient bucket (synthetic stand-in), bf16, one bucket per bwd call
+    from paper_2603_18567_b200.dp import GradBuckets, max_over_ranks
+    grads = GradBuckets(DRAFT_PARAMS if world > 1 else 1, S, dtype=torch.bfloat16, device=dev)
     if world > 1:
-        grad = torch.randn(DRAFT_PARAMS, device=dev, dtype=torch.float32).to(torch.bfloat16)
-        buckets = list(torch.chunk(grad, S))
+        grads.flat.normal_()
 
     def on_bwd(i):
-        if world > 1:
-            works.append(dist.all_reduce(buckets[i], op=dist.ReduceOp.AVG, async_op=True))
+        grads.release(i)
 
     def one_step():
         u.step(stream, on_bwd)
-        while works:
-            works.pop().wait()
+        grads.finish()
 
     for _ in range(args.warmup):
         one_step()
@@ -267,11 +265,7 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         if dist is not None:
             dist.barrier()
         wall = time.perf_counter() - w0
-    ms = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
+    ms = max_over_ranks(e0.elapsed_time(e1), device=dev)
     ms_per_step = ms / args.steps
     tokens_per_step = shape.batch * shape.seq_len * world
     value = tokens_per_step / (ms_per_step / 1e3)
@@ -319,6 +313,7 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         "roofline": roof,
         "kernels_ms_per_step": {k: v[0] / prof_steps for k, v in kern.items()},
         "gpu_launches": launches_per_step * args.steps,
+        "grad_allreduce_bytes_per_step": grads.nbytes if world > 1 else 0,
         "wall_s_timed_region": wall,
         "clocks": clk.summary(),
     }

@@ -75,6 +75,7 @@ int validate_desc(const ttt_attn_desc* d, int step) {
   if (d->num_q_heads % d->num_kv_heads) return TTT_ERR_INVALID_ARG;
   if (d->dtype != TTT_BF16 && d->dtype != TTT_FP32_CHECK) return TTT_ERR_INVALID_ARG;
   if (d->head_dim != 64 && d->head_dim != 128) return TTT_ERR_UNSUPPORTED;
+  if (d->num_q_heads / d->num_kv_heads > 32) return TTT_ERR_UNSUPPORTED;  // GQA group <= 32 heads
   if (!(d->softmax_scale >= 0.f) || std::isinf(d->softmax_scale)) return TTT_ERR_INVALID_ARG;
   if (step < 0 || step >= TTT_MAX_STEPS) return TTT_ERR_STEP_RANGE;
   if (d->dtype == TTT_BF16 && (d->seq_len % kTile)) return TTT_ERR_UNSUPPORTED;

@@ -74,20 +74,21 @@ __device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int
 // (b, r, g) rows. For such a group every operand is ONE contiguous block in HBM
 // (q / dO / O / O_lo: NR*G*D bf16; K_i, V_i: NR*D bf16; dK_i, dV_i: NR*D fp32), so
 // thread 0 moves each with a single 1-D cp.async.bulk into a double-buffered
-// stage; dK_i / dV_i are accumulated in place in shared memory and written back
-// with bulk stores. 16 lanes per row, D/16 contiguous elements per lane.
+// stage. One HALF-warp per (row, query head): Delta, the diagonal p_i / ds_i and
+// dq stay in registers; dK_i / dV_i (sums over the G heads) are accumulated with
+// shared-memory atomics in the stage and written back with bulk stores. Lane hl
+// owns elements [hl*E/2, +E/2) and [D/2 + hl*E/2, +E/2): every half-warp smem
+// access is contiguous (bank-conflict free).
 struct PreLayout {
   int NR, G, D, step, acc, has_lo;
-  uint32_t off_q, off_do, off_o, off_olo, off_k, off_v, off_dk, off_dv, stage_bytes, off_dq, off_sc, total;
+  uint32_t off_q, off_do, off_o, off_olo, off_k, off_v, off_dk, off_dv, stage_bytes, total;
   __host__ __device__ void init(int nr, int g, int d, int j, int accumulate, int lo) {
     NR = nr; G = g; D = d; step = j; acc = accumulate; has_lo = lo;
     const uint32_t qb = (uint32_t)nr * g * d * 2, kb = (uint32_t)nr * d * 2, fb = (uint32_t)nr * d * 4;
     off_q = 0; off_do = qb; off_o = 2 * qb; off_olo = 3 * qb;
     off_k = 4 * qb; off_v = off_k + j * kb; off_dk = off_v + j * kb; off_dv = off_dk + j * fb;
     stage_bytes = (off_dv + j * fb + 127) & ~127u;
-    off_dq = 2 * stage_bytes;
-    off_sc = off_dq;                                    // fp32 [NR][G] x2: Delta, lse2
-    total = off_sc + 2u * nr * g * 4 + 64;              // + 2 mbarriers
+    total = 2 * stage_bytes + 64;  // + 2 mbarriers
   }
 };
 
@@ -103,41 +104,44 @@ __device__ __forceinline__ void bulk_load_1d_(void* dst, const void* src, uint32
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// split-lane bf16 row chunk: E/2 elements at hl*E/2 and at D/2 + hl*E/2 -> fp32
 template <int D>
-__device__ __forceinline__ void lds_row(const uint8_t* s, float (&x)[D / 16]) {
-  constexpr int E = D / 16;
-  if constexpr (E == 8) {
-    const uint4 u = *reinterpret_cast<const uint4*>(s);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+__device__ __forceinline__ void lds_split(const uint8_t* row, int hl, float (&x)[D / 16]) {
+  constexpr int H = D / 32;  // elements per half (4 for D=128, 2 for D=64)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-      x[2 * e] = f.x;
-      x[2 * e + 1] = f.y;
-    }
-  } else {
-    const uint2 u = *reinterpret_cast<const uint2*>(s);
-    const uint32_t w[2] = {u.x, u.y};
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-      x[2 * e] = f.x;
-      x[2 * e + 1] = f.y;
+  for (int part = 0; part < 2; ++part) {
+    const uint8_t* src = row + (part * (D / 2) + hl * H) * 2;
+    if constexpr (H == 4) {
+      const uint2 u = *reinterpret_cast<const uint2*>(src);
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      x[part * 4 + 0] = a.x; x[part * 4 + 1] = a.y; x[part * 4 + 2] = c.x; x[part * 4 + 3] = c.y;
+    } else {
+      const uint32_t u = *reinterpret_cast<const uint32_t*>(src);
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+      x[part * 2 + 0] = a.x; x[part * 2 + 1] = a.y;
     }
   }
 }
+template <int D>
+__device__ __forceinline__ int split_col(int hl, int e) {  // D index of lane element e
+  constexpr int H = D / 32;
+  return (e < H) ? hl * H + e : D / 2 + hl * H + (e - H);
+}
 
 template <int D>
-__global__ void __launch_bounds__(128) ttt_bwd_pre_kernel(const __grid_constant__ Params p, PreLayout lay) {
+__global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant__ Params p, PreLayout lay) {
   constexpr int E = D / 16;
   extern __shared__ __align__(128) uint8_t psm[];
-  const int tid = threadIdx.x, hl = tid & 15, lr = tid >> 4;
+  const int tid = threadIdx.x, hl = tid & 15, pair = tid >> 4;
   const int NR = lay.NR, G = p.G, j = p.step;
   const long nrows = (long)p.B * p.L * p.Hkv;
   const long ngroups = (nrows + NR - 1) / NR;
   uint64_t* full = reinterpret_cast<uint64_t*>(psm + lay.total - 64);
-  float* sdel = reinterpret_cast<float*>(psm + lay.off_sc);
-  float* sl2 = sdel + NR * G;
+  // half-warp `pair` -> (row lr, head hh); ghosts (pair >= NR*G) mirror pair 0 without storing
+  const bool ghost = pair >= NR * G;
+  const int pc = ghost ? 0 : pair;
+  const int lr = pc / G, hh = pc % G;
   if (tid == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(128) ttt_bwd_pre_kernel(const __grid_constant_
     const int nv = (int)min((long)NR, nrows - w0);
     uint8_t* base = psm + st * lay.stage_bytes;
     const uint32_t qb = (uint32_t)nv * G * D * 2, kb = (uint32_t)nv * D * 2, fb = (uint32_t)nv * D * 4;
-    uint32_t bytes = 3 * qb + j * 2 * kb + (lay.has_lo ? qb : 0) + (lay.acc ? j * 2 * fb : 0);
+    const uint32_t bytes = 3 * qb + j * 2 * kb + (lay.has_lo ? qb : 0) + (lay.acc ? j * 2 * fb : 0);
     mbar_expect_tx(&full[st], bytes);
     const size_t qo = (size_t)w0 * G * D, ko = (size_t)w0 * D;
     bulk_load_1d_(base + lay.off_q, reinterpret_cast<const __nv_bfloat16*>(p.q) + qo, qb, &full[st]);
@@ -177,107 +181,98 @@ __global__ void __launch_bounds__(128) ttt_bwd_pre_kernel(const __grid_constant_
       bulk_wait_read0();  // bulk stores of group n-1 (same stage as n+1) have read their smem
       issue(nxt, st ^ 1);
     }
-    mbar_wait(&full[st], (n >> 1) & 1);
     uint8_t* base = psm + st * lay.stage_bytes;
     const long w = grp * NR + lr;
-    // ghost threads (lr >= NR) alias row 0 for loads and shuffles but store nothing
-    const bool ghost = lr >= NR;
-    const bool valid = w < nrows && !ghost;
-    const long wc = valid ? w : (ghost ? grp * NR : nrows - 1);
+    const bool valid = !ghost && w < nrows;
+    const long wc = w < nrows ? w : grp * NR;
     const int g = (int)(wc % p.Hkv);
     const int r = (int)((wc / p.Hkv) % p.L);
     const int b = (int)(wc / ((long)p.Hkv * p.L));
+    const int h = g * G + hh;
     const bool act = valid && r < p.seq_lens[b];  // diagonal keys exist only for rows r < T_b
-    const int lrc = lr < NR ? lr : 0;
-    // ---- Delta, lse2 per head; dq accumulators zeroed ----
-    for (int hh = 0; hh < G; ++hh) {
-      const uint32_t ro = ((uint32_t)(lrc * G + hh) * D + hl * E) * 2;
-      float o[E], d[E];
-      lds_row<D>(base + lay.off_o + ro, o);
-      lds_row<D>(base + lay.off_do + ro, d);
-      if (lay.has_lo) {
-        float lo[E];
-        lds_row<D>(base + lay.off_olo + ro, lo);
+    if (!lay.acc && valid && hh == 0) {
+      // overwrite mode: zero this row of the staged dK_i / dV_i (the stage is not loaded) and of
+      // dK_0 / dV_0 in HBM (the main kernel adds into them)
+      for (int i = 0; i < j; ++i) {
+        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + lr * D;
+        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + lr * D;
 #pragma unroll
-        for (int e = 0; e < E; ++e) o[e] += lo[e];
+        for (int e = 0; e < E; ++e) dkr[split_col<D>(hl, e)] = dvr[split_col<D>(hl, e)] = 0.f;
       }
-      float acc = 0.f;
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc = fmaf(o[e], d[e], acc);
-      const float delta = half_allsum(acc);  // Delta_r = dO_r . O_r
-      const int h = g * G + hh;
-      const size_t li = ((size_t)b * p.Hq + h) * p.L + r;
-      const float l2 = p.lse_in[li] * kLog2e;
-      if (hl == 0 && !ghost) {
-        if (valid) {
-          p.delta[li] = delta;
-          p.lse2[li] = l2;
-        }
-        sdel[lrc * G + hh] = delta;
-        sl2[lrc * G + hh] = l2;
+      for (int e = 0; e < E; ++e) {
+        p.dk[(size_t)w * D + split_col<D>(hl, e)] = 0.f;
+        p.dv[(size_t)w * D + split_col<D>(hl, e)] = 0.f;
       }
     }
-    if (!lay.acc && !ghost) {  // overwrite mode: step gradients start from zero in the stage
-      for (int i = 0; i < j; ++i) {
-        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + lrc * D + hl * E;
-        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + lrc * D + hl * E;
+    mbar_wait(&full[st], (n >> 1) & 1);
+    __syncthreads();  // zeroed stage rows visible before any atomics
+    const uint32_t ro = (uint32_t)(lr * G + hh) * D * 2;
+    float o[E], dd[E], qq[E], dq[E];
+    lds_split<D>(base + lay.off_o + ro, hl, o);
+    lds_split<D>(base + lay.off_do + ro, hl, dd);
+    if (lay.has_lo) {
+      float lo[E];
+      lds_split<D>(base + lay.off_olo + ro, hl, lo);
 #pragma unroll
-        for (int e = 0; e < E; ++e) dkr[e] = dvr[e] = 0.f;
-      }
-      if (valid) {  // dK_0 / dV_0 rows: the main kernel adds into them
-        float4* dk4 = reinterpret_cast<float4*>(p.dk + (size_t)w * D + hl * E);
-        float4* dv4 = reinterpret_cast<float4*>(p.dv + (size_t)w * D + hl * E);
-#pragma unroll
-        for (int e = 0; e < E / 4; ++e) dk4[e] = dv4[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      for (int e = 0; e < E; ++e) o[e] += lo[e];
     }
-    __syncwarp();
-    __syncthreads();  // Delta / lse2 of every row visible (ghost rows read row 0)
-    // ---- TTT diagonal keys (Alg. 2 M_suffix): p_i, dp_i, ds_i; dq, dK_i, dV_i ----
-    for (int hh = 0; hh < G; ++hh) {
-      const uint32_t ro = ((uint32_t)(lrc * G + hh) * D + hl * E) * 2;
-      float qq[E], dd[E], dq[E];
-      lds_row<D>(base + lay.off_q + ro, qq);
-      lds_row<D>(base + lay.off_do + ro, dd);
+    float acc = 0.f;
 #pragma unroll
-      for (int e = 0; e < E; ++e) dq[e] = 0.f;
-      const float l2 = sl2[lrc * G + hh], del = sdel[lrc * G + hh];
-      for (int i = 0; i < j; ++i) {
-        float kk[E], vv[E];
-        lds_row<D>(base + lay.off_k + i * (NR * D * 2) + (lrc * D + hl * E) * 2, kk);
-        lds_row<D>(base + lay.off_v + i * (NR * D * 2) + (lrc * D + hl * E) * 2, vv);
-        float s = 0.f, dp = 0.f;
+    for (int e = 0; e < E; ++e) acc = fmaf(o[e], dd[e], acc);
+    const float del = half_allsum(acc);  // Delta_r = dO_r . O_r
+    const size_t li = ((size_t)b * p.Hq + h) * p.L + r;
+    const float l2 = p.lse_in[li] * kLog2e;
+    if (valid && hl == 0) {
+      p.delta[li] = del;
+      p.lse2[li] = l2;
+    }
+    lds_split<D>(base + lay.off_q + ro, hl, qq);
+#pragma unroll
+    for (int e = 0; e < E; ++e) dq[e] = 0.f;
+    // ---- TTT diagonal keys (Alg. 2 M_suffix): p_i, dp_i, ds_i -> dq, dK_i, dV_i ----
+    for (int i = 0; i < j; ++i) {
+      float kk[E], vv[E];
+      lds_split<D>(base + lay.off_k + (i * NR + lr) * D * 2, hl, kk);
+      lds_split<D>(base + lay.off_v + (i * NR + lr) * D * 2, hl, vv);
+      float s = 0.f, dp = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        s = fmaf(qq[e], kk[e], s);
+        dp = fmaf(dd[e], vv[e], dp);
+      }
+#pragma unroll
+      for (int o2 = 8; o2 > 0; o2 >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o2);
+        dp += __shfl_xor_sync(0xffffffffu, dp, o2);
+      }
+      const float pr = act ? ex2(s * p.scale_log2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
+      const float cds = p.scale * pr * (dp - del);              // c ds_i, ds_i = p_i (dp_i - Delta)
+#pragma unroll
+      for (int e = 0; e < E; ++e) dq[e] = fmaf(cds, kk[e], dq[e]);
+      if (act) {  // dK_i[r] += c ds_i q_h, dV_i[r] += p_i dO_h, summed over the G heads
+        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + lr * D;
+        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + lr * D;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          s = fmaf(qq[e], kk[e], s);
-          dp = fmaf(dd[e], vv[e], dp);
-        }
-#pragma unroll
-        for (int o2 = 8; o2 > 0; o2 >>= 1) {
-          s += __shfl_xor_sync(0xffffffffu, s, o2);
-          dp += __shfl_xor_sync(0xffffffffu, dp, o2);
-        }
-        const float pr = act ? ex2(s * p.scale_log2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
-        const float cds = p.scale * pr * (dp - del);              // c ds_i, ds_i = p_i (dp_i - Delta)
-        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + lrc * D + hl * E;
-        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + lrc * D + hl * E;
-#pragma unroll
-        for (int e = 0; e < E; ++e) dq[e] = fmaf(cds, kk[e], dq[e]);
-        if (!ghost) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            dkr[e] = fmaf(cds, qq[e], dkr[e]);
-            dvr[e] = fmaf(pr, dd[e], dvr[e]);
-          }
+          atomicAdd(dkr + split_col<D>(hl, e), cds * qq[e]);
+          atomicAdd(dvr + split_col<D>(hl, e), pr * dd[e]);
         }
       }
-      if (valid) {
-        const int h = g * G + hh;
-        float* dst = p.dq_acc + dqacc_index(p, b, h, r, hl * E);
+    }
+    if (valid) {
+      float* dst = p.dq_acc + dqacc_index(p, b, h, r, 0);
+      // tiled dq_acc: column d lives at chunk d/32, offset d%32 of row r
 #pragma unroll
-        for (int e = 0; e < E / 4; ++e)
-          reinterpret_cast<float4*>(dst)[e] = make_float4(dq[4 * e], dq[4 * e + 1], dq[4 * e + 2], dq[4 * e + 3]);
+      for (int part = 0; part < 2; ++part) {
+        const int d0 = part * (D / 2) + hl * (E / 2);
+        float* q4 = p.dq_acc + dqacc_index(p, b, h, r, d0);
+        if constexpr (E / 2 == 4)
+          *reinterpret_cast<float4*>(q4) = make_float4(dq[part * 4], dq[part * 4 + 1], dq[part * 4 + 2], dq[part * 4 + 3]);
+        else
+          *reinterpret_cast<float2*>(q4) = make_float2(dq[part * 2], dq[part * 2 + 1]);
       }
+      (void)dst;
     }
     fence_async_smem();
     __syncthreads();
@@ -724,7 +719,7 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
   // 1. pre-pass (TMA-staged, persistent)
   {
     PreLayout lay;
-    int nr = 8;
+    int nr = std::max(1, 32 / p.G);  // 32 half-warps (512 threads) of (row, head) pairs
     for (; nr > 1; nr >>= 1) {
       lay.init(nr, p.G, D, p.step, p.accumulate, p.o_lo != nullptr);
       if (lay.total <= 220 * 1024) break;
@@ -738,7 +733,8 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
     const long groups = (rows + nr - 1) / nr;
     const int blocks = (int)std::min<long>(groups, 148);
     prof_mark(kKindBwdPre, true, st);
-    ttt_bwd_pre_kernel<D><<<blocks, 128, lay.total, st>>>(p, lay);
+    const int threads = std::min(512, std::max(32, ((nr * p.G * 16 + 31) / 32) * 32));
+    ttt_bwd_pre_kernel<D><<<blocks, threads, lay.total, st>>>(p, lay);
     prof_mark(kKindBwdPre, false, st);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

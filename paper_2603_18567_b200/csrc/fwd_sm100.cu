@@ -220,60 +220,72 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 1, n);
         if (threadIdx.x == 128) TTT_TRACE_EV(2, 1, n);
         tc_fence_after();
-        float s[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t raw[32];
-          tmem_ld32(tS + c * 32, raw);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(raw[i]);
-        }
+        uint32_t raw[128];
+        tmem_ld128(tS, raw);
         const int kv0 = n * kTile;
         const bool partial = (n == qt) || (kv0 + kTile > T);
-        float mx = -INFINITY;
+        // row max of the raw scores (scale > 0 commutes with max): 8 independent chains
+        float mx8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
         if (partial) {
           const int lim = min(r + 1, T) - kv0;  // allowed columns c < lim  (k <= r and k < T)
 #pragma unroll
           for (int c = 0; c < 128; ++c) {
-            const float x = c < lim ? s[c] * sl2 : -INFINITY;
-            s[c] = x;
-            mx = fmaxf(mx, x);
+            const float x = c < lim ? __uint_as_float(raw[c]) : -INFINITY;
+            raw[c] = __float_as_uint(x);
+            mx8[c & 7] = fmaxf(mx8[c & 7], x);
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < 128; ++c) {
-            s[c] *= sl2;
-            mx = fmaxf(mx, s[c]);
-          }
+          for (int c = 0; c < 128; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(raw[c]));
         }
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
         const float m_new = fmaxf(m_run, mx);
         const bool need = m_new > m_run + kRescaleThreshold;
         if (__any_sync(0xffffffffu, need)) {
           const float alpha = ex2(m_run - m_new);
-          if (n > 0) {  // PV_{n-1} is complete: s_full's commit covers it
-#pragma unroll
-            for (int c = 0; c < D; c += 32) {
+          if (n > 0) {  // PV_{n-1} is complete: s_full's commit covers it (rare path: 32-col chunks)
+            const uint64_t a2 = f2pack(alpha, alpha);
+#pragma unroll 1
+            for (int c0 = 0; c0 < D; c0 += 32) {
               uint32_t o[32];
-              tmem_ld32(tO + c, o);
+              tmem_ld32(tO + c0, o);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tmem_st32(tO + c, o);
+              for (int i = 0; i < 32; i += 2) {
+                float lo, hi;
+                f2unpack(fmul2(f2pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), a2), lo, hi);
+                o[i] = __float_as_uint(lo);
+                o[i + 1] = __float_as_uint(hi);
+              }
+              tmem_st32(tO + c0, o);
             }
           }
           l_run *= alpha;
           m_run = m_new;
         }
-        float rs = 0.f;
+        // P = 2^(s c log2e - m): one FFMA2 per pair, 4 independent pair-sum chains (FADD2)
+        const uint64_t sl2x2 = f2pack(sl2, sl2), negm = f2pack(-m_run, -m_run);
+        uint64_t rs2[4] = {0, 0, 0, 0};
         uint32_t pk[64];
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
-          const float e0 = ex2(s[2 * c] - m_run), e1 = ex2(s[2 * c + 1] - m_run);
-          rs += e0 + e1;
+          float x0, x1;
+          f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
+          const float e0 = ex2(x0), e1 = ex2(x1);
+          rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
           pk[c] = pack_bf16(e0, e1);
         }
-        l_run += rs;
-        tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+        {
+          float a0, a1, b0, b1, c0, c1, d0, d1;
+          f2unpack(rs2[0], a0, a1);
+          f2unpack(rs2[1], b0, b1);
+          f2unpack(rs2[2], c0, c1);
+          f2unpack(rs2[3], d0, d1);
+          l_run += ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
+        }
+        tmem_st64(tS, pk);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars.p_full[slot]);
@@ -373,14 +385,18 @@ struct DiagLayout {
 };
 
 template <int D>
-__global__ void __launch_bounds__(256) ttt_fwd_diag_kernel(const __grid_constant__ Params p, DiagLayout lay) {
-  constexpr int E = D / 16;
+__global__ void __launch_bounds__(512) ttt_fwd_diag_kernel(const __grid_constant__ Params p, DiagLayout lay) {
+  constexpr int E = D / 16, H = D / 32;
   extern __shared__ __align__(128) uint8_t dsm[];
-  const int tid = threadIdx.x, hl = tid & 15, lr = tid >> 4;
+  const int tid = threadIdx.x, hl = tid & 15, pair = tid >> 4;
   const int NR = lay.NR, G = p.G, j = p.step;
   const long nrows = (long)p.B * p.L * p.Hkv;
   const long ngroups = (nrows + NR - 1) / NR;
   uint64_t* full = reinterpret_cast<uint64_t*>(dsm + lay.total - 64);
+  // one half-warp per (row, query head); lane hl owns elements [hl*H, +H) and [D/2 + hl*H, +H)
+  const bool ghost = pair >= NR * G;
+  const int pc = ghost ? 0 : pair;
+  const int lr = pc / G, hh = pc % G;
   if (tid == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
@@ -411,6 +427,22 @@ __global__ void __launch_bounds__(256) ttt_fwd_diag_kernel(const __grid_constant
                    : "memory");
     }
   };
+  auto lds = [&](const uint8_t* row, float (&x)[E]) {
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const uint8_t* src = row + (part * (D / 2) + hl * H) * 2;
+      if constexpr (H == 4) {
+        const uint2 u = *reinterpret_cast<const uint2*>(src);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        x[part * 4 + 0] = a.x; x[part * 4 + 1] = a.y; x[part * 4 + 2] = c.x; x[part * 4 + 3] = c.y;
+      } else {
+        const uint32_t u = *reinterpret_cast<const uint32_t*>(src);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+        x[part * 2 + 0] = a.x; x[part * 2 + 1] = a.y;
+      }
+    }
+  };
   long grp = blockIdx.x;
   if (tid == 0 && grp < ngroups) issue(grp, 0);
   for (int n = 0; grp < ngroups; ++n, grp += gridDim.x) {
@@ -420,100 +452,47 @@ __global__ void __launch_bounds__(256) ttt_fwd_diag_kernel(const __grid_constant
     mbar_wait(&full[st], (n >> 1) & 1);
     const uint8_t* base = dsm + st * lay.stage_bytes;
     const long w = grp * NR + lr;
-    const bool ghost = lr >= NR;
-    const bool valid = w < nrows && !ghost;
-    const long wc = valid ? w : grp * NR;
-    const int lrc = ghost ? 0 : (int)(wc - grp * NR);
+    const bool valid = !ghost && w < nrows;
+    const long wc = w < nrows ? w : grp * NR;
     const int g = (int)(wc % p.Hkv);
     const int r = (int)((wc / p.Hkv) % p.L);
     const int b = (int)(wc / ((long)p.Hkv * p.L));
     const bool act = valid && r < p.seq_lens[b];
-    for (int hh = 0; hh < G; ++hh) {
-      float qf[E], o[E];
-      {
-        const uint8_t* qs = base + lay.off_q + ((uint32_t)(lrc * G + hh) * D + hl * E) * 2;
-        const uint4 u = *reinterpret_cast<const uint4*>(qs);
-        if constexpr (E == 8) {
-          const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+    float qf[E], o[E];
+    lds(base + lay.off_q + (uint32_t)(lr * G + hh) * D * 2, qf);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
-            qf[2 * e] = f.x;
-            qf[2 * e + 1] = f.y;
-          }
-        } else {
-          const uint2 u2 = *reinterpret_cast<const uint2*>(qs);
-          const uint32_t wv[2] = {u2.x, u2.y};
+    for (int e = 0; e < E; ++e) o[e] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    for (int i = 0; i < j; ++i) {
+      float kk[E], vv[E];
+      lds(base + lay.off_k + (uint32_t)(i * NR + lr) * D * 2, kk);
+      lds(base + lay.off_v + (uint32_t)(i * NR + lr) * D * 2, vv);
+      float acc = 0.f;
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
-            qf[2 * e] = f.x;
-            qf[2 * e + 1] = f.y;
-          }
-        }
+      for (int e = 0; e < E; ++e) acc = fmaf(qf[e], kk[e], acc);
+      const float t = half_allsum(acc) * p.scale_log2;  // s_i = c q_r . k_i (log2 units)
+      const float mn = fmaxf(m, t);
+      const float a = ex2(m - mn), wgt = ex2(t - mn);
+      l = l * a + wgt;
+#pragma unroll
+      for (int e = 0; e < E; ++e) o[e] = fmaf(wgt, vv[e], o[e] * a);
+      m = mn;
+    }
+    if (act) {
+      const int h = g * G + hh;
+      const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D;
+      const float inv = 1.f / l;
+      __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        __nv_bfloat16* dst = op + part * (D / 2) + hl * H;
+        if constexpr (H == 4)
+          *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(o[part * 4] * inv, o[part * 4 + 1] * inv),
+                                                      pack_bf16(o[part * 4 + 2] * inv, o[part * 4 + 3] * inv));
+        else
+          *reinterpret_cast<uint32_t*>(dst) = pack_bf16(o[part * 2] * inv, o[part * 2 + 1] * inv);
       }
-#pragma unroll
-      for (int e = 0; e < E; ++e) o[e] = 0.f;
-      float m = -INFINITY, l = 0.f;
-      for (int i = 0; i < j; ++i) {
-        float kk[E], vv[E];
-        const uint32_t ro = (uint32_t)(i * NR + lrc) * D * 2 + hl * E * 2;
-        {
-          const uint8_t* kp = base + lay.off_k + ro;
-          const uint8_t* vp = base + lay.off_v + ro;
-          if constexpr (E == 8) {
-            const uint4 uk = *reinterpret_cast<const uint4*>(kp), uv = *reinterpret_cast<const uint4*>(vp);
-            const uint32_t wk[4] = {uk.x, uk.y, uk.z, uk.w}, wvv[4] = {uv.x, uv.y, uv.z, uv.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 fk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wk[e]));
-              const float2 fv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wvv[e]));
-              kk[2 * e] = fk.x; kk[2 * e + 1] = fk.y;
-              vv[2 * e] = fv.x; vv[2 * e + 1] = fv.y;
-            }
-          } else {
-            const uint2 uk = *reinterpret_cast<const uint2*>(kp), uv = *reinterpret_cast<const uint2*>(vp);
-            const uint32_t wk[2] = {uk.x, uk.y}, wvv[2] = {uv.x, uv.y};
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const float2 fk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wk[e]));
-              const float2 fv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wvv[e]));
-              kk[2 * e] = fk.x; kk[2 * e + 1] = fk.y;
-              vv[2 * e] = fv.x; vv[2 * e + 1] = fv.y;
-            }
-          }
-        }
-        float acc = 0.f;
-#pragma unroll
-        for (int e = 0; e < E; ++e) acc = fmaf(qf[e], kk[e], acc);
-        const float t = half_allsum(acc) * p.scale_log2;  // s_i = c q_r . k_i (log2 units)
-        const float mn = fmaxf(m, t);
-        const float a = ex2(m - mn), wgt = ex2(t - mn);
-        l = l * a + wgt;
-#pragma unroll
-        for (int e = 0; e < E; ++e) o[e] = fmaf(wgt, vv[e], o[e] * a);
-        m = mn;
-      }
-      if (act) {
-        const int h = g * G + hh;
-        const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D + hl * E;
-        const float inv = 1.f / l;
-        __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
-        if constexpr (E == 8) {
-          uint4 u;
-          u.x = pack_bf16(o[0] * inv, o[1] * inv);
-          u.y = pack_bf16(o[2] * inv, o[3] * inv);
-          u.z = pack_bf16(o[4] * inv, o[5] * inv);
-          u.w = pack_bf16(o[6] * inv, o[7] * inv);
-          *reinterpret_cast<uint4*>(op) = u;
-        } else {
-          uint2 u;
-          u.x = pack_bf16(o[0] * inv, o[1] * inv);
-          u.y = pack_bf16(o[2] * inv, o[3] * inv);
-          *reinterpret_cast<uint2*>(op) = u;
-        }
-        if (hl == 0) p.lse[((size_t)b * p.Hq + h) * p.L + r] = m + log2f(l);
-      }
+      if (hl == 0) p.lse[((size_t)b * p.Hq + h) * p.L + r] = m + log2f(l);
     }
     __syncthreads();  // stage st fully consumed before it is refilled
   }
@@ -530,7 +509,7 @@ cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, cudaStream_t st) 
   }
   if (p.step > 0) {
     DiagLayout lay;
-    int nr = 16;
+    int nr = std::max(1, 32 / p.G);  // 32 half-warps (512 threads) of (row, head) pairs
     for (; nr > 1; nr >>= 1) {
       lay.init(nr, p.G, D, p.step);
       if (lay.total <= 200 * 1024) break;
@@ -545,7 +524,8 @@ cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, cudaStream_t st) 
     const int per_sm = lay.total <= 110 * 1024 ? 2 : 1;
     const int blocks = (int)std::min<long>(groups, 148L * per_sm);
     prof_mark(kKindFwdDiag, true, st);
-    ttt_fwd_diag_kernel<D><<<blocks, 256, lay.total, st>>>(p, lay);
+    const int threads = std::min(512, std::max(32, ((nr * p.G * 16 + 31) / 32) * 32));
+    ttt_fwd_diag_kernel<D><<<blocks, threads, lay.total, st>>>(p, lay);
     prof_mark(kKindFwdDiag, false, st);
   }
   const int npairs = (p.G + 1) / 2;

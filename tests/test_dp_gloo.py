@@ -1,0 +1,70 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the data-parallel host logic
+used by bench.py at N > 1: sequence sharding, bucketed gradient all-reduce with
+averaging, and the max-over-ranks timing rule."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_18567_b200.dp import GradBuckets, max_over_ranks, shard_sequences
+
+
+def test_shard_sequences_partition():
+    for gb in (1, 7, 8, 64):
+        for world in (1, 2, 3, 8):
+            seen = []
+            for r in range(world):
+                lo, hi = shard_sequences(gb, world, r)
+                assert hi - lo in (gb // world, gb // world + 1)
+                seen += list(range(lo, hi))
+            assert seen == list(range(gb))
+    with pytest.raises(ValueError):
+        shard_sequences(8, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gb = GradBuckets(1001, 7, dtype=torch.float32)
+        # rank-dependent pattern: element e of rank r = (r + 1) * e
+        gb.flat.copy_(torch.arange(1001, dtype=torch.float32) * (rank + 1))
+        for i in reversed(range(7)):  # released in backward order
+            gb.release(i)
+        gb.finish()
+        want = torch.arange(1001, dtype=torch.float32) * sum(r + 1 for r in range(world)) / world
+        ok_avg = torch.allclose(gb.flat, want)
+        t = max_over_ranks(10.0 + rank)
+        q.put((rank, ok_avg, t, shard_sequences(64, world, rank)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_grad_buckets_allreduce_and_max_timing_world2():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    for rank, ok_avg, t, shard in res:
+        assert ok_avg, f"rank {rank}: bucketed all-reduce average wrong"
+        assert t == 11.0, "max over ranks"
+    assert res[0][3] == (0, 32) and res[1][3] == (32, 64)
