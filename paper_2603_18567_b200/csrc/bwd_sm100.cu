@@ -81,14 +81,15 @@ __device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int
 // access is contiguous (bank-conflict free).
 struct PreLayout {
   int NR, G, D, step, acc, has_lo;
-  uint32_t off_q, off_do, off_o, off_olo, off_k, off_v, off_dk, off_dv, stage_bytes, total;
+  uint32_t off_q, off_do, off_o, off_olo, off_k, off_v, off_dk, off_dv, stage_bytes, off_sc, total;
   __host__ __device__ void init(int nr, int g, int d, int j, int accumulate, int lo) {
     NR = nr; G = g; D = d; step = j; acc = accumulate; has_lo = lo;
     const uint32_t qb = (uint32_t)nr * g * d * 2, kb = (uint32_t)nr * d * 2, fb = (uint32_t)nr * d * 4;
     off_q = 0; off_do = qb; off_o = 2 * qb; off_olo = 3 * qb;
     off_k = 4 * qb; off_v = off_k + j * kb; off_dk = off_v + j * kb; off_dv = off_dk + j * fb;
     stage_bytes = (off_dv + j * fb + 127) & ~127u;
-    total = 2 * stage_bytes + 64;  // + 2 mbarriers
+    off_sc = 2 * stage_bytes;                            // fp32 [NR][j][G][2]: (p_i, c ds_i) per head
+    total = off_sc + ((uint32_t)nr * (j > 0 ? j : 1) * g * 8 + 127) / 128 * 128 + 64;  // + 2 mbarriers
   }
 };
 
@@ -190,15 +191,7 @@ __global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant_
     const int b = (int)(wc / ((long)p.Hkv * p.L));
     const int h = g * G + hh;
     const bool act = valid && r < p.seq_lens[b];  // diagonal keys exist only for rows r < T_b
-    if (!lay.acc && valid && hh == 0) {
-      // overwrite mode: zero this row of the staged dK_i / dV_i (the stage is not loaded) and of
-      // dK_0 / dV_0 in HBM (the main kernel adds into them)
-      for (int i = 0; i < j; ++i) {
-        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + lr * D;
-        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + lr * D;
-#pragma unroll
-        for (int e = 0; e < E; ++e) dkr[split_col<D>(hl, e)] = dvr[split_col<D>(hl, e)] = 0.f;
-      }
+    if (!lay.acc && valid && hh == 0) {  // dK_0 / dV_0 rows in HBM: the main kernel adds into them
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         p.dk[(size_t)w * D + split_col<D>(hl, e)] = 0.f;
@@ -206,7 +199,6 @@ __global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant_
       }
     }
     mbar_wait(&full[st], (n >> 1) & 1);
-    __syncthreads();  // zeroed stage rows visible before any atomics
     const uint32_t ro = (uint32_t)(lr * G + hh) * D * 2;
     float o[E], dd[E], qq[E], dq[E];
     lds_split<D>(base + lay.off_o + ro, hl, o);
@@ -230,39 +222,33 @@ __global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant_
     lds_split<D>(base + lay.off_q + ro, hl, qq);
 #pragma unroll
     for (int e = 0; e < E; ++e) dq[e] = 0.f;
-    // ---- TTT diagonal keys (Alg. 2 M_suffix): p_i, dp_i, ds_i -> dq, dK_i, dV_i ----
+    // ---- phase A: per (row, head) the diagonal scalars (Alg. 2 M_suffix) and dq ----
+    float* scal = reinterpret_cast<float*>(psm + lay.off_sc);  // [NR][j][G][2]
     for (int i = 0; i < j; ++i) {
       float kk[E], vv[E];
       lds_split<D>(base + lay.off_k + (i * NR + lr) * D * 2, hl, kk);
       lds_split<D>(base + lay.off_v + (i * NR + lr) * D * 2, hl, vv);
-      float s = 0.f, dp = 0.f;
+      float sdot = 0.f, dp = 0.f;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        s = fmaf(qq[e], kk[e], s);
+        sdot = fmaf(qq[e], kk[e], sdot);
         dp = fmaf(dd[e], vv[e], dp);
       }
 #pragma unroll
       for (int o2 = 8; o2 > 0; o2 >>= 1) {
-        s += __shfl_xor_sync(0xffffffffu, s, o2);
+        sdot += __shfl_xor_sync(0xffffffffu, sdot, o2);
         dp += __shfl_xor_sync(0xffffffffu, dp, o2);
       }
-      const float pr = act ? ex2(s * p.scale_log2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
-      const float cds = p.scale * pr * (dp - del);              // c ds_i, ds_i = p_i (dp_i - Delta)
+      const float pr = act ? ex2(sdot * p.scale_log2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
+      const float cds = p.scale * pr * (dp - del);                 // c ds_i, ds_i = p_i (dp_i - Delta)
 #pragma unroll
       for (int e = 0; e < E; ++e) dq[e] = fmaf(cds, kk[e], dq[e]);
-      if (act) {  // dK_i[r] += c ds_i q_h, dV_i[r] += p_i dO_h, summed over the G heads
-        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + lr * D;
-        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + lr * D;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          atomicAdd(dkr + split_col<D>(hl, e), cds * qq[e]);
-          atomicAdd(dvr + split_col<D>(hl, e), pr * dd[e]);
-        }
+      if (!ghost && hl == 0) {
+        scal[((lr * j + i) * G + hh) * 2 + 0] = pr;
+        scal[((lr * j + i) * G + hh) * 2 + 1] = cds;
       }
     }
     if (valid) {
-      float* dst = p.dq_acc + dqacc_index(p, b, h, r, 0);
-      // tiled dq_acc: column d lives at chunk d/32, offset d%32 of row r
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
         const int d0 = part * (D / 2) + hl * (E / 2);
@@ -272,7 +258,45 @@ __global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant_
         else
           *reinterpret_cast<float2*>(q4) = make_float2(dq[part * 2], dq[part * 2 + 1]);
       }
-      (void)dst;
+    }
+    __syncthreads();  // all (p_i, c ds_i) of the group visible
+    // ---- phase B: per (row, step, D-slice): dK_i = sum_h c ds_h q_h, dV_i = sum_h p_h dO_h ----
+    // (exclusive ownership of each stage row: no atomics; overwrite or accumulate)
+    {
+      const int nitems = NR * j;
+      for (int it = pair; it < nitems; it += blockDim.x / 16) {
+        const int brow = it % NR, i = it / NR;
+        const long wb = grp * NR + brow;
+        if (wb >= nrows) continue;
+        float dk[E], dv[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) dk[e] = dv[e] = 0.f;
+        for (int h2 = 0; h2 < G; ++h2) {
+          const float pr = scal[((brow * j + i) * G + h2) * 2 + 0];
+          const float cds = scal[((brow * j + i) * G + h2) * 2 + 1];
+          float q2[E], d2[E];
+          const uint32_t r2 = (uint32_t)(brow * G + h2) * D * 2;
+          lds_split<D>(base + lay.off_q + r2, hl, q2);
+          lds_split<D>(base + lay.off_do + r2, hl, d2);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            dk[e] = fmaf(cds, q2[e], dk[e]);
+            dv[e] = fmaf(pr, d2[e], dv[e]);
+          }
+        }
+        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + brow * D;
+        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + brow * D;
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          const int d0 = part * (D / 2) + hl * (E / 2);
+#pragma unroll
+          for (int e = 0; e < E / 2; ++e) {
+            const int k2 = part * (E / 2) + e;
+            dkr[d0 + e] = lay.acc ? dkr[d0 + e] + dk[k2] : dk[k2];
+            dvr[d0 + e] = lay.acc ? dvr[d0 + e] + dv[k2] : dv[k2];
+          }
+        }
+      }
     }
     fence_async_smem();
     __syncthreads();
