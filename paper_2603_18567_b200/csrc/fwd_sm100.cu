@@ -269,13 +269,29 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const uint64_t sl2x2 = f2pack(sl2, sl2), negm = f2pack(-m_run, -m_run);
         uint64_t rs2[4] = {0, 0, 0, 0};
         uint32_t pk[64];
+        if (partial) {  // masked columns are -inf: hardware ex2 gives exact zeros
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          float x0, x1;
-          f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
-          const float e0 = ex2(x0), e1 = ex2(x1);
-          rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
-          pk[c] = pack_bf16(e0, e1);
+          for (int c = 0; c < 64; ++c) {
+            float x0, x1;
+            f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
+            const float e0 = ex2(x0), e1 = ex2(x1);
+            rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
+            pk[c] = pack_bf16(e0, e1);
+          }
+        } else {  // full tile: every 4th pair on the FMA pipe (MUFU ex2 is the co-bottleneck)
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            float x0, x1, e0, e1;
+            f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
+            if ((c & 3) == 3) {
+              ex2_emu2(x0, x1, e0, e1);
+            } else {
+              e0 = ex2(x0);
+              e1 = ex2(x1);
+            }
+            rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
+            pk[c] = pack_bf16(e0, e1);
+          }
         }
         {
           float a0, a1, b0, b1, c0, c1, d0, d1;
