@@ -320,7 +320,7 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
     if world == 1 and not args.no_e2e:
         line["e2e"] = run_e2e(u, stream, args, shape)
     if rank == 0 and world == 1 and not args.no_cpu:
-        n, threads, run = oracle_sample(shape, target_s=12.0)
+        n, threads, run = oracle_sample(shape, target_s=15.0)
         sec = run(n)
         line["cpu_baseline"] = {
             "value": n / sec, "unit": UNIT, "cores": threads, "kind": "oracle",
@@ -363,7 +363,7 @@ def run_e2e(u: Unroll, stream, args, shape: Shape):
 
 def ncu_traffic(kernel: str):
     """dram bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")  # copy of the latest profiles/ncu_summary_rNN.json
     if not os.path.exists(p):
         return None
     try:

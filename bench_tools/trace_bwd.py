@@ -55,3 +55,17 @@ for i, v in items.items():
         acc.setdefault(n, []).append(t - s0[0])
 for n, xs in sorted(acc.items(), key=lambda kv: np.median(kv[1])):
     print(f"{n:18s} median offset {np.median(xs):8.0f}")
+# per-warp phase completion spread (role 3)
+w = {}
+for x in buf[3]:
+    x = int(x)
+    if x == 0: continue
+    ev_ = (x >> 12) & 0xFF; it = x & 0xFFF
+    w.setdefault((it, ev_ >= 16), {})[ev_ % 16] = (x >> 20)
+for phase, nm in ((False, "P"), (True, "dS")):
+    rel = {k: [] for k in range(4, 12)}
+    for (it, ph), d in w.items():
+        if ph != phase or len(d) < 8 or it < 4: continue
+        t0_ = min(d.values())
+        for k, t in d.items(): rel[k].append(t - t0_)
+    print(nm, "phase: median lag behind the first warp, by warp:", {k: int(np.median(v)) for k, v in rel.items() if v})

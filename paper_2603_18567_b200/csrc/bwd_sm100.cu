@@ -215,9 +215,9 @@ __global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant_
     const float del = half_allsum(acc);  // Delta_r = dO_r . O_r
     const size_t li = ((size_t)b * p.Hq + h) * p.L + r;
     const float l2 = p.lse_in[li] * kLog2e;
-    if (valid && hl == 0) {
-      p.delta[li] = del;
-      p.lse2[li] = l2;
+    if (valid && hl == 0) {  // stored negated: the main kernel's FFMA2 / FADD2 consume -lse2 and -Delta
+      p.delta[li] = -del;
+      p.lse2[li] = -l2;
     }
     lds_split<D>(base + lay.off_q + ro, hl, qq);
 #pragma unroll
@@ -558,23 +558,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(&bars.s_full, i & 1);
       if (threadIdx.x == 128) TTT_TRACE_EV(1, 1, i);
       tc_fence_after();
-      const float4* Lq = reinterpret_cast<const float4*>(sL + qs * 128 + 64 * hf);
-      const float4* Dq = reinterpret_cast<const float4*>(sDel + qs * 128 + 64 * hf);
+      const float4* Lq = reinterpret_cast<const float4*>(sL + qs * 128 + 64 * hf);    // -lse2
+      const float4* Dq = reinterpret_cast<const float4*>(sDel + qs * 128 + 64 * hf);  // -Delta
       float pr[64];
       {
         uint32_t raw[64];
-        tmem_ld64(tS, raw);
+        tmem_ld64w(tS, raw);
         // allowed (k, q): k <= q and k < T; full tiles (qt > kt, whole key tile < T) skip the test
         const bool full = (qt > kt) && (kt * kTile + kTile <= T);
         const int cmin = (k < T) ? k - qt * kTile - 64 * hf : kTile;  // local columns [cmin, 64) allowed
+        const uint64_t sl2x2 = f2pack(sl2, sl2);
 #pragma unroll
         for (int c4 = 0; c4 < 16; ++c4) {
-          const float4 l4 = Lq[c4];
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+          const float4 l4 = Lq[c4];  // -lse2 of 4 query columns
+          float x0, x1, x2, x3;
+          f2unpack(ffma2(f2pack(__uint_as_float(raw[4 * c4]), __uint_as_float(raw[4 * c4 + 1])), sl2x2,
+                         f2pack(l4.x, l4.y)), x0, x1);
+          f2unpack(ffma2(f2pack(__uint_as_float(raw[4 * c4 + 2]), __uint_as_float(raw[4 * c4 + 3])), sl2x2,
+                         f2pack(l4.z, l4.w)), x2, x3);
+          const float xs[4] = {x0, x1, x2, x3};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int c = 4 * c4 + e;
-            const float x = ex2(fmaf(__uint_as_float(raw[c]), sl2, -lv[e]));
+            const float x = ex2(xs[e]);  // P = exp(S c - lse)
             pr[c] = (full || c >= cmin) ? x : 0.f;
           }
         }
@@ -589,6 +595,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars.p_full);
       if (threadIdx.x == 128) TTT_TRACE_EV(1, 2, i);
+#ifdef TTT_TRACE
+      if (lane == 0) {  // per-warp P-phase completion (role 3: event = warp id)
+        const unsigned long long c_ = clock64();
+        if (blockIdx.x == g_ttt_trace_cta && i < 4000)
+          g_ttt_trace[3][i * 16 + warp] = (c_ << 20) | ((unsigned long long)warp << 12) | (unsigned long long)(i & 0xFFF);
+      }
+#endif
       mbar_wait(&bars.dp_full, i & 1);
       if (threadIdx.x == 128) TTT_TRACE_EV(1, 3, i);
       mbar_wait(&bars.ds_empty, (i & 1) ^ 1);
@@ -600,12 +613,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int e4 = 0; e4 < 8; ++e4) {
-          const float4 d4 = Dq[cc * 8 + e4];
+          const float4 d4 = Dq[cc * 8 + e4];  // -Delta of 4 query columns
           const int c = cc * 32 + 4 * e4;
-          pk[2 * e4] = pack_bf16(pr[c] * (__uint_as_float(raw[4 * e4]) - d4.x),
-                                 pr[c + 1] * (__uint_as_float(raw[4 * e4 + 1]) - d4.y));
-          pk[2 * e4 + 1] = pack_bf16(pr[c + 2] * (__uint_as_float(raw[4 * e4 + 2]) - d4.z),
-                                     pr[c + 3] * (__uint_as_float(raw[4 * e4 + 3]) - d4.w));
+          float a0, a1, b0, b1;
+          f2unpack(fmul2(f2pack(pr[c], pr[c + 1]),
+                         fadd2(f2pack(__uint_as_float(raw[4 * e4]), __uint_as_float(raw[4 * e4 + 1])),
+                               f2pack(d4.x, d4.y))), a0, a1);  // dS = P (dP - Delta)
+          f2unpack(fmul2(f2pack(pr[c + 2], pr[c + 3]),
+                         fadd2(f2pack(__uint_as_float(raw[4 * e4 + 2]), __uint_as_float(raw[4 * e4 + 3])),
+                               f2pack(d4.z, d4.w))), b0, b1);
+          pk[2 * e4] = pack_bf16(a0, a1);
+          pk[2 * e4 + 1] = pack_bf16(b0, b1);
         }
         tmem_st16(tdP + cc * 16, pk);  // dS^T (bf16) over this half's already-read dP^T columns
         // smem dS: row = key row, q columns [64 hf + 32 cc, +32): box hf, 8-column chunks 4 cc + e8
@@ -622,6 +640,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars.ds_full);
       if (threadIdx.x == 128) TTT_TRACE_EV(1, 4, i);
+#ifdef TTT_TRACE
+      if (lane == 0) {  // per-warp dS completion (role 3 second half)
+        const unsigned long long c_ = clock64();
+        if (blockIdx.x == g_ttt_trace_cta && i < 2000)
+          g_ttt_trace[3][32768 + i * 16 + warp] =
+              (c_ << 20) | ((unsigned long long)(16 + warp) << 12) | (unsigned long long)(i & 0xFFF);
+      }
+#endif
     }
     // ---- dK, dV accumulators -> global (fp32 atomics: head splits and steps add up) ----
     mbar_wait(&bars.acc_full, 0);

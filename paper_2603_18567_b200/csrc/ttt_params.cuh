@@ -39,8 +39,8 @@ struct Params {
   float* dv;
   float* dks[TTT_MAX_STEPS];
   float* dvs[TTT_MAX_STEPS];
-  float* delta;   // workspace [B][Hq][L]: Delta = rowsum(dO o O)
-  float* lse2;    // workspace [B][Hq][L]: lse * log2(e)
+  float* delta;   // workspace [B][Hq][L]: -Delta = -rowsum(dO o O)  (stored negated)
+  float* lse2;    // workspace [B][Hq][L]: -lse * log2(e)           (stored negated)
   float* dq_acc;  // workspace fp32, tile-contiguous [B][Hq][L/128][D/32][128][32]
   int seq_lens[TTT_MAX_BATCH];
 };
