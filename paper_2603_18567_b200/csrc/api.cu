@@ -40,12 +40,12 @@ EncodeTiledFn get_encode_fn() {
 }
 
 // BSHD bf16 tensor [B][L][H][D] -> 4-D map (D, H, L, B), box (64, 1, 128, 1), 128B swizzle.
-bool encode_bshd(CUtensorMap* m, const void* ptr, int B, int L, int H, int D) {
+bool encode_bshd(CUtensorMap* m, const void* ptr, int B, int L, int H, int D, int box_rows = 128) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)L, (cuuint64_t)B};
   cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)H * D * 2, (cuuint64_t)L * H * D * 2};
-  cuuint32_t box[4] = {64, 1, 128, 1};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -317,6 +317,7 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
   BwdMaps maps;
   if (!encode_bshd(&maps.q, q, p.B, p.L, p.Hq, p.D) || !encode_bshd(&maps.k, k_base, p.B, p.L, p.Hkv, p.D) ||
       !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D) || !encode_bshd(&maps.dout, dout, p.B, p.L, p.Hq, p.D) ||
+      !encode_bshd(&maps.dout64, dout, p.B, p.L, p.Hq, p.D, 64) ||
       !encode_dqacc(&maps.dqacc, p.dq_acc, (size_t)p.B * p.L * p.Hq * p.D / 32))
     return TTT_ERR_CUDA;
   return cuda_status(launch_bwd_sm100(p, maps, s));

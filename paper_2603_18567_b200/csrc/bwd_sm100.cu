@@ -360,30 +360,60 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
       : "memory");
 }
 
-// Warp roles (16 warps, FA4-style split; setmaxnreg rebalances the register file):
-//   warps 0-3   dQ drain          (thread = query row of TMEM lane quadrant w)
-//   warps 4-11  compute P^T, dS^T (quadrant w & 3, query-column half (w - 4) >> 2)
+// Work item = one 128-query tile (head h, tile qt) split into two 64-query
+// sub-items x = a, b. S^T / dP^T are double-buffered per sub-item in TMEM, so
+// the MMA warp works on one sub-item while a compute warpgroup works on the
+// other. Per tile the MMA issue order is
+//   dV(a) S'(a) dK(a) | dV(b) S'(b) dK(b) | dQ(a+b) | [drain] dP'(a) dP'(b)
+// (S' / dP' belong to the next tile). dQ (M = 128 queries, N = D) aliases the two
+// dP^T buffers, so the next dP waits for the dQ drain only.
+// Warp roles (16 warps; setmaxnreg rebalances the register file):
+//   warps 0-3   dQ drain            (thread = query row of TMEM lane quadrant w)
+//   warps 4-7   compute sub-item a  (thread = key row, 64 query columns)
+//   warps 8-11  compute sub-item b
 //   warp  12    TMEM owner + MMA issuer, warp 13 TMA producer, warps 14-15 idle
 // Per SMSP: {dQ 152, compute 136, compute 136, role 88 / idle 24} <= 512 registers.
+// TMEM: S^T[a] [0,64) S^T[b] [64,128) dP^T[a] [128,192) dP^T[b] [192,256) dV [256,+D) dK [384,+D);
+// P^T / dS^T (bf16, 2 per column) over the first 32 columns of their own S / dP buffer.
+// Shared memory (D = 128): K, V 64 KB | Q 2 x 32 KB | dO 3 x 16 KB ring of 64-row halves |
+// dS 32 KB ([kv][q], two 64-query SW128 boxes) | lse2, Delta 2 KB | dQ staging 4 x 4 KB.
 constexpr int kBwdThreads = 512;
-constexpr int kBwdSmem = 5 * 32768 + 32768 + 2048 + 32768 + 256;  // D = 128 layout (D = 64 uses less)
+
+template <int D>
+struct BwdSmem {
+  static constexpr int TB = kTile * D * 2;  // 128 x D bf16 tile
+  static constexpr int HB = TB / 2;         // 64 x D half tile
+  static constexpr int oK = 0, oV = TB, oQ = 2 * TB, oDO = 4 * TB, oDS = 4 * TB + 3 * HB;
+  static constexpr int oL = oDS + 32768, oDel = oL + 1024, oDQ = oDel + 1024, oBar = oDQ + 16384;
+  static constexpr int bytes = oBar + 256;
+};
+
+struct BwdBars3 {
+  uint64_t kv_full;
+  uint64_t q_full[2], q_empty[2];
+  uint64_t do_full[3], do_empty[3];
+  uint64_t s_full[2], dp_full[2], p_full[2], ds_full[2];
+  uint64_t ds_empty, dq_full, dq_empty, acc_full;
+  uint32_t tmem_base;
+};
 
 template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     ttt_bwd_sm100_kernel(const __grid_constant__ Params p, const __grid_constant__ BwdMaps maps) {
-  constexpr int TB = kTile * D * 2;
+  using SM = BwdSmem<D>;
+  constexpr int TB = SM::TB, HB = SM::HB;
   constexpr int NBOX = D / 64;
   // dynamic smem only (no static __shared__): the window base is 1024-B aligned, checked below
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sK = smem;
-  uint8_t* sV = smem + TB;
-  uint8_t* sQ = smem + 2 * TB;   // 2 stages
-  uint8_t* sDO = smem + 4 * TB;  // 1 stage
-  uint8_t* sDS = smem + 5 * TB;  // 128 x 128 bf16, [kv][q] in two 64-column SW128 boxes
-  float* sL = reinterpret_cast<float*>(smem + 5 * TB + 32768);  // [2][128] lse2
-  float* sDel = sL + 256;                                      // [2][128] Delta
-  uint8_t* sDQ = smem + 5 * TB + 32768 + 2048;                 // 4 warps x 2 x 4 KB dQ staging (SW128)
-  BwdBars& bars = *reinterpret_cast<BwdBars*>(smem + 5 * TB + 32768 + 2048 + 32768);
+  uint8_t* sK = smem + SM::oK;
+  uint8_t* sV = smem + SM::oV;
+  uint8_t* sQ = smem + SM::oQ;    // 2 stages of 128 x D
+  uint8_t* sDO = smem + SM::oDO;  // 3-slot ring of 64 x D halves (boxes of 64 rows x 64 cols)
+  uint8_t* sDS = smem + SM::oDS;  // 128 x 128 bf16, [kv][q], box x = sub-item x
+  float* sL = reinterpret_cast<float*>(smem + SM::oL);     // [2][128] -lse2
+  float* sDel = reinterpret_cast<float*>(smem + SM::oDel);  // [2][128] -Delta
+  uint8_t* sDQ = smem + SM::oDQ;                            // 4 warps x 4 KB dQ staging (SW128)
+  BwdBars3& bars = *reinterpret_cast<BwdBars3*>(smem + SM::oBar);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hsplit = p.head_split;
@@ -398,7 +428,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int T = p.seq_lens[b];
   if (kt * kTile >= T) return;  // every key of the tile is padding: no gradient flows
   const int nq = p.nqt - kt;
-  const int n_items = nh * nq;
+  const int n_items = nh * nq;  // 128-query tiles
   const int h_first = g * p.G + hs * nh;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1 KB alignment
 
@@ -407,13 +437,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars.q_full[i], 1);
       mbar_init(&bars.q_empty[i], 1);
+      mbar_init(&bars.s_full[i], 1);
+      mbar_init(&bars.dp_full[i], 1);
+      mbar_init(&bars.p_full[i], 128);
+      mbar_init(&bars.ds_full[i], 128);
     }
-    mbar_init(&bars.do_full, 1);
-    mbar_init(&bars.do_empty, 1);
-    mbar_init(&bars.s_full, 1);
-    mbar_init(&bars.dp_full, 1);
-    mbar_init(&bars.p_full, 256);
-    mbar_init(&bars.ds_full, 256);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&bars.do_full[i], 1);
+      mbar_init(&bars.do_empty[i], 1);
+    }
     mbar_init(&bars.ds_empty, 1);
     mbar_init(&bars.dq_full, 1);
     mbar_init(&bars.dq_empty, 128);
@@ -443,9 +475,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_load_4d(sK + bx * 16384, &maps.k, &bars.kv_full, bx * 64, g, kt * kTile, b);
         tma_load_4d(sV + bx * 16384, &maps.v, &bars.kv_full, bx * 64, g, kt * kTile, b);
       }
-      for (int i = 0; i < n_items; ++i) {
-        const int h = h_first + i / nq, qt = kt + i % nq;
-        const int qs = i & 1, qph = (i >> 1) & 1;
+      for (int t = 0; t < n_items; ++t) {
+        const int h = h_first + t / nq, qt = kt + t % nq;
+        const int qs = t & 1, qph = (t >> 1) & 1;
         mbar_wait(&bars.q_empty[qs], qph ^ 1);
         mbar_expect_tx(&bars.q_full[qs], TB + 1024);
 #pragma unroll
@@ -454,11 +486,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const size_t li = ((size_t)b * p.Hq + h) * p.L + (size_t)qt * kTile;
         bulk_load_1d(sL + qs * 128, p.lse2 + li, 512, &bars.q_full[qs]);
         bulk_load_1d(sDel + qs * 128, p.delta + li, 512, &bars.q_full[qs]);
-        mbar_wait(&bars.do_empty, (i & 1) ^ 1);
-        mbar_expect_tx(&bars.do_full, TB);
 #pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sDO + bx * 16384, &maps.dout, &bars.do_full, bx * 64, h, qt * kTile, b);
+        for (int x = 0; x < 2; ++x) {
+          const int u = 2 * t + x, slot = u % 3, use = u / 3;
+          mbar_wait(&bars.do_empty[slot], (use & 1) ^ 1);
+          mbar_expect_tx(&bars.do_full[slot], HB);
+#pragma unroll
+          for (int bx = 0; bx < NBOX; ++bx)
+            tma_load_4d(sDO + slot * HB + bx * (HB / NBOX), &maps.dout64, &bars.do_full[slot], bx * 64, h,
+                        qt * kTile + 64 * x, b);
+        }
       }
     }
   } else if (warp == 12) {
@@ -466,111 +503,128 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     reg_dealloc<88>();
     if (lane == 0) {
       TTT_TRACE_DECL(0);
-      constexpr uint32_t idSP = idesc_bf16_f32(128, 128, false, false);  // S^T = K Q^T, dP^T = V dO^T
-      constexpr uint32_t idKV = idesc_bf16_f32(128, D, false, true);     // dV += P^T dO, dK += dS^T Q
-      constexpr uint32_t idDQ = idesc_bf16_f32(128, D, true, true);      // dQ = dS K
+      constexpr uint32_t idSP = idesc_bf16_f32(128, 64, false, false);  // S^T = K Q_x^T, dP^T = V dO_x^T
+      constexpr uint32_t idKV = idesc_bf16_f32(128, D, false, true);    // dV += P^T dO_x, dK += dS^T Q_x
+      constexpr uint32_t idDQ = idesc_bf16_f32(128, D, true, true);     // dQ = dS K
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aDO = smem_u32(sDO),
                      aDS = smem_u32(sDS);
-      auto kmaj = [](uint32_t base, int ks) {
-        return sdesc_sw128(base + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
+      // K-major operands: 128-row tiles (Q) and 64-row halves (dO) share the 8-row x 128 B atom
+      auto kmaj = [](uint32_t base, int ks, uint32_t box_bytes) {
+        return sdesc_sw128(base + (ks >> 2) * box_bytes + (ks & 3) * 32, 16, 1024);
       };
-      auto mnmaj = [](uint32_t base, int ks) { return sdesc_sw128(base + ks * 2048, 16384, 1024); };
-      // P^T / dS^T (bf16, packed 2 per column) of query-column half hf sit at TMEM
-      // columns [64 hf, 64 hf + 32) of the S / dP regions (each half writes over its own S columns)
-      auto pcol = [](int ks) { return (uint32_t)(64 * (ks >> 2) + 8 * (ks & 3)); };
-      auto issue_S = [&](int qs) {
+      auto issue_S = [&](int qs, int x) {  // S^T[x] = K Q_x^T  (Q_x = rows 64x.. of the Q stage)
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) umma_ss(tbase, kmaj(aK, ks), kmaj(aQ + qs * TB, ks), idSP, ks > 0);
+        for (int ks = 0; ks < D / 16; ++ks)
+          umma_ss(tbase + 64 * x, kmaj(aK, ks, 16384), kmaj(aQ + qs * TB + 64 * x * 128, ks, 16384), idSP, ks > 0);
       };
-      auto issue_dP = [&]() {
+      auto issue_dP = [&](int slot, int x) {  // dP^T[x] = V dO_x^T
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) umma_ss(tbase + 128, kmaj(aV, ks), kmaj(aDO, ks), idSP, ks > 0);
+        for (int ks = 0; ks < D / 16; ++ks)
+          umma_ss(tbase + 128 + 64 * x, kmaj(aV, ks, 16384), kmaj(aDO + slot * HB, ks, HB / NBOX), idSP, ks > 0);
+      };
+      auto issue_dV = [&](int slot, int x, bool first) {  // dV += P^T[x] dO_x  (K = 64 queries)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          umma_ts(tbase + 256, tbase + 64 * x + 8 * ks, sdesc_sw128(aDO + slot * HB + ks * 2048, HB / NBOX, 1024),
+                  idKV, (!first || ks > 0) ? 1u : 0u);
+      };
+      auto issue_dK = [&](int qs, int x, bool first) {  // dK += dS^T[x] Q_x
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          umma_ts(tbase + 384, tbase + 128 + 64 * x + 8 * ks,
+                  sdesc_sw128(aQ + qs * TB + (64 * x + 16 * ks) * 128, 16384, 1024), idKV,
+                  (!first || ks > 0) ? 1u : 0u);
       };
       mbar_wait(&bars.kv_full, 0);
       mbar_wait(&bars.q_full[0], 0);
       tc_fence_after();
-      issue_S(0);
-      umma_commit(&bars.s_full);
-      mbar_wait(&bars.do_full, 0);
-      tc_fence_after();
-      issue_dP();
-      umma_commit(&bars.dp_full);
-      for (int i = 0; i < n_items; ++i) {
-        const int qs = i & 1;
-        const bool more = i + 1 < n_items;
-        // dV += P^T dO   (A = P^T in TMEM)
-        TTT_TRACE_EV(0, 1, i);
-        mbar_wait(&bars.p_full, i & 1);
-        TTT_TRACE_EV(0, 2, i);
-        tc_fence_after();
+      issue_S(0, 0);
+      umma_commit(&bars.s_full[0]);
+      issue_S(0, 1);
+      umma_commit(&bars.s_full[1]);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          umma_ts(tbase + 256, tbase + pcol(ks), mnmaj(aDO, ks), idKV, (i > 0 || ks > 0) ? 1u : 0u);
-        umma_commit(&bars.do_empty);
-        // dK += dS^T Q   (A = dS^T in TMEM)
-        mbar_wait(&bars.ds_full, i & 1);
-        TTT_TRACE_EV(0, 3, i);
+      for (int x = 0; x < 2; ++x) {
+        mbar_wait(&bars.do_full[x], 0);
         tc_fence_after();
+        issue_dP(x, x);
+        umma_commit(&bars.dp_full[x]);
+      }
+      for (int t = 0; t < n_items; ++t) {
+        const int qs = t & 1;
+        const bool more = t + 1 < n_items;
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          umma_ts(tbase + 384, tbase + 128 + pcol(ks), mnmaj(aQ + qs * TB, ks), idKV,
-                  (i > 0 || ks > 0) ? 1u : 0u);
-        umma_commit(&bars.q_empty[qs]);
-        // next S^T while this item's dQ is drained
-        if (more) {
-          mbar_wait(&bars.q_full[(i + 1) & 1], ((i + 1) >> 1) & 1);
-          TTT_TRACE_EV(0, 4, i);
+        for (int x = 0; x < 2; ++x) {
+          const int slot = (2 * t + x) % 3;
+          mbar_wait(&bars.p_full[x], t & 1);
+          TTT_TRACE_EV(0, 1 + x, t);
           tc_fence_after();
-          issue_S((i + 1) & 1);
-          umma_commit(&bars.s_full);
+          issue_dV(slot, x, t == 0 && x == 0);
+          umma_commit(&bars.do_empty[slot]);
+          if (more) {  // next tile's S^T[x]: its P^T[x] was just consumed (in-order pipe)
+            if (x == 0) mbar_wait(&bars.q_full[(t + 1) & 1], ((t + 1) >> 1) & 1);
+            tc_fence_after();
+            issue_S((t + 1) & 1, x);
+            umma_commit(&bars.s_full[x]);
+          }
+          mbar_wait(&bars.ds_full[x], t & 1);
+          TTT_TRACE_EV(0, 3 + x, t);
+          tc_fence_after();
+          issue_dK(qs, x, t == 0 && x == 0);
         }
-        // dQ = dS K -> TMEM cols [128, 128+D)  (A = dS from smem, MN-major)
+        umma_commit(&bars.q_empty[qs]);
+        // dQ = dS K for the whole 128-query tile -> TMEM [128, 128+D)  (A = dS from smem, MN-major)
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) umma_ss(tbase + 128, mnmaj(aDS, ks), mnmaj(aK, ks), idDQ, ks > 0);
+        for (int ks = 0; ks < 8; ++ks)
+          umma_ss(tbase + 128, sdesc_sw128(aDS + ks * 2048, 16384, 1024), sdesc_sw128(aK + ks * 2048, 16384, 1024),
+                  idDQ, ks > 0);
         umma_commit(&bars.dq_full);
         umma_commit(&bars.ds_empty);
         if (more) {
-          mbar_wait(&bars.dq_empty, i & 1);
-          TTT_TRACE_EV(0, 5, i);
-          mbar_wait(&bars.do_full, (i + 1) & 1);
-          TTT_TRACE_EV(0, 6, i);
-          tc_fence_after();
-          issue_dP();
-          umma_commit(&bars.dp_full);
+          mbar_wait(&bars.dq_empty, t & 1);
+          TTT_TRACE_EV(0, 5, t);
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            const int u = 2 * (t + 1) + x;
+            mbar_wait(&bars.do_full[u % 3], (u / 3) & 1);
+            tc_fence_after();
+            issue_dP(u % 3, x);
+            umma_commit(&bars.dp_full[x]);
+          }
+          TTT_TRACE_EV(0, 6, t);
         }
       }
       umma_commit(&bars.acc_full);
     }
   } else if (warp >= 4 && warp < 12) {
-    // ================= compute: P^T, dS^T (thread = key row, 64 query columns) =================
+    // ================= compute: P^T, dS^T of sub-item x (thread = key row, 64 query columns) ====
     reg_alloc<136>();
-    const int quad = warp & 3, hf = (warp - 4) >> 2;
+    const int quad = warp & 3, x = (warp - 4) >> 2;
     const int row = quad * 32 + lane;
     const int k = kt * kTile + row;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t tS = tbase + lane_off + 64 * hf, tdP = tbase + lane_off + 128 + 64 * hf;
+    const uint32_t tS = tbase + lane_off + 64 * x, tdP = tbase + lane_off + 128 + 64 * x;
     const float sl2 = p.scale_log2;
+    const uint64_t sl2x2 = f2pack(sl2, sl2);
     TTT_TRACE_DECL(1);
-    for (int i = 0; i < n_items; ++i) {
-      const int qs = i & 1;
-      const int qt = kt + i % nq;
-      mbar_wait(&bars.q_full[qs], (i >> 1) & 1);
-      mbar_wait(&bars.s_full, i & 1);
-      if (threadIdx.x == 128) TTT_TRACE_EV(1, 1, i);
+    for (int t = 0; t < n_items; ++t) {
+      const int qs = t & 1;
+      const int qt = kt + t % nq;
+      mbar_wait(&bars.q_full[qs], (t >> 1) & 1);
+      mbar_wait(&bars.s_full[x], t & 1);
+      if (threadIdx.x == 128) TTT_TRACE_EV(1, 1, t);
       tc_fence_after();
-      const float4* Lq = reinterpret_cast<const float4*>(sL + qs * 128 + 64 * hf);    // -lse2
-      const float4* Dq = reinterpret_cast<const float4*>(sDel + qs * 128 + 64 * hf);  // -Delta
+      const float4* Lq = reinterpret_cast<const float4*>(sL + qs * 128 + 64 * x);    // -lse2
+      const float4* Dq = reinterpret_cast<const float4*>(sDel + qs * 128 + 64 * x);  // -Delta
       float pr[64];
       {
         uint32_t raw[64];
         tmem_ld64w(tS, raw);
         // allowed (k, q): k <= q and k < T; full tiles (qt > kt, whole key tile < T) skip the test
         const bool full = (qt > kt) && (kt * kTile + kTile <= T);
-        const int cmin = (k < T) ? k - qt * kTile - 64 * hf : kTile;  // local columns [cmin, 64) allowed
-        const uint64_t sl2x2 = f2pack(sl2, sl2);
+        const int cmin = (k < T) ? k - qt * kTile - 64 * x : kTile;  // local columns [cmin, 64) allowed
 #pragma unroll
         for (int c4 = 0; c4 < 16; ++c4) {
-          const float4 l4 = Lq[c4];  // -lse2 of 4 query columns
+          const float4 l4 = Lq[c4];
           float x0, x1, x2, x3;
           f2unpack(ffma2(f2pack(__uint_as_float(raw[4 * c4]), __uint_as_float(raw[4 * c4 + 1])), sl2x2,
                          f2pack(l4.x, l4.y)), x0, x1);
@@ -580,8 +634,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int c = 4 * c4 + e;
-            const float x = ex2(xs[e]);  // P = exp(S c - lse)
-            pr[c] = (full || c >= cmin) ? x : 0.f;
+            const float v = ex2(xs[e]);  // P = exp(S c - lse)
+            pr[c] = (full || c >= cmin) ? v : 0.f;
           }
         }
       }
@@ -589,22 +643,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t pk[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(pr[2 * c], pr[2 * c + 1]);
-        tmem_st32(tS, pk);  // P^T over this half's own (already read) S columns
+        tmem_st32(tS, pk);  // P^T over this sub-item's own (already read) S^T columns
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&bars.p_full);
-      if (threadIdx.x == 128) TTT_TRACE_EV(1, 2, i);
-#ifdef TTT_TRACE
-      if (lane == 0) {  // per-warp P-phase completion (role 3: event = warp id)
-        const unsigned long long c_ = clock64();
-        if (blockIdx.x == g_ttt_trace_cta && i < 4000)
-          g_ttt_trace[3][i * 16 + warp] = (c_ << 20) | ((unsigned long long)warp << 12) | (unsigned long long)(i & 0xFFF);
-      }
-#endif
-      mbar_wait(&bars.dp_full, i & 1);
-      if (threadIdx.x == 128) TTT_TRACE_EV(1, 3, i);
-      mbar_wait(&bars.ds_empty, (i & 1) ^ 1);
+      mbar_arrive(&bars.p_full[x]);
+      if (threadIdx.x == 128) TTT_TRACE_EV(1, 2, t);
+      mbar_wait(&bars.dp_full[x], t & 1);
+      mbar_wait(&bars.ds_empty, (t & 1) ^ 1);  // dQ of the previous tile has read the dS buffer
+      if (threadIdx.x == 128) TTT_TRACE_EV(1, 3, t);
       tc_fence_after();
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
@@ -613,7 +660,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int e4 = 0; e4 < 8; ++e4) {
-          const float4 d4 = Dq[cc * 8 + e4];  // -Delta of 4 query columns
+          const float4 d4 = Dq[cc * 8 + e4];
           const int c = cc * 32 + 4 * e4;
           float a0, a1, b0, b1;
           f2unpack(fmul2(f2pack(pr[c], pr[c + 1]),
@@ -625,9 +672,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           pk[2 * e4] = pack_bf16(a0, a1);
           pk[2 * e4 + 1] = pack_bf16(b0, b1);
         }
-        tmem_st16(tdP + cc * 16, pk);  // dS^T (bf16) over this half's already-read dP^T columns
-        // smem dS: row = key row, q columns [64 hf + 32 cc, +32): box hf, 8-column chunks 4 cc + e8
-        uint8_t* boxp = sDS + hf * 16384 + row * 128;
+        tmem_st16(tdP + cc * 16, pk);  // dS^T (bf16) over this sub-item's already-read dP^T columns
+        // smem dS: row = key row, q columns [64 x + 32 cc, +32): box x, 8-column chunks 4 cc + e8
+        uint8_t* boxp = sDS + x * 16384 + row * 128;
 #pragma unroll
         for (int e8 = 0; e8 < 4; ++e8) {
           const int chunk = cc * 4 + e8;
@@ -638,16 +685,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       fence_async_smem();
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&bars.ds_full);
-      if (threadIdx.x == 128) TTT_TRACE_EV(1, 4, i);
-#ifdef TTT_TRACE
-      if (lane == 0) {  // per-warp dS completion (role 3 second half)
-        const unsigned long long c_ = clock64();
-        if (blockIdx.x == g_ttt_trace_cta && i < 2000)
-          g_ttt_trace[3][32768 + i * 16 + warp] =
-              (c_ << 20) | ((unsigned long long)(16 + warp) << 12) | (unsigned long long)(i & 0xFFF);
-      }
-#endif
+      mbar_arrive(&bars.ds_full[x]);
+      if (threadIdx.x == 128) TTT_TRACE_EV(1, 4, t);
     }
     // ---- dK, dV accumulators -> global (fp32 atomics: head splits and steps add up) ----
     mbar_wait(&bars.acc_full, 0);
@@ -655,7 +694,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // tcgen05.ld is warp-collective (.sync.aligned): every lane loads, only rows k < T store
     const bool store = k < T;
     const size_t off = (((size_t)b * p.L + (store ? k : 0)) * p.Hkv + g) * D;
-    const int cbeg = hf * (D / 2);
+    const int cbeg = x * (D / 2);
 #pragma unroll 1
     for (int c0 = cbeg; c0 < cbeg + D / 2; c0 += 32) {
       uint32_t raw[32];
@@ -677,43 +716,42 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp < 4) {
     // ================= dQ drain (warps 0-3, thread = query row) =================
-    // TMEM -> registers (scaled by c) -> warp-private SW128 staging (double buffered) ->
-    // TMA reduce-add into the tile-contiguous fp32 dq_acc (one 32 x 32 box per chunk).
+    // TMEM -> registers (scaled by c) -> warp-private SW128 staging -> TMA reduce-add into
+    // the tile-contiguous fp32 dq_acc (one 32 x 32 box per 32-column chunk).
     reg_alloc<152>();
     const int wq = warp;
     const uint32_t tQ = tbase + ((uint32_t)(wq * 32) << 16) + 128;
-    uint8_t* stage = sDQ + wq * 8192;
+    uint8_t* stage = sDQ + wq * 4096;
     if (lane == 0) tma_prefetch_desc(&maps.dqacc);
     TTT_TRACE_DECL(2);
-    for (int i = 0; i < n_items; ++i) {
-      const int h = h_first + i / nq, qt = kt + i % nq;
-      mbar_wait(&bars.dq_full, i & 1);
-      if (threadIdx.x == 0) TTT_TRACE_EV(2, 1, i);
+    for (int t = 0; t < n_items; ++t) {
+      const int h = h_first + t / nq, qt = kt + t % nq;
+      mbar_wait(&bars.dq_full, t & 1);
+      if (threadIdx.x == 0) TTT_TRACE_EV(2, 1, t);
       tc_fence_after();
       uint32_t v[D];
 #pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 64) tmem_ld64(tQ + c0, *reinterpret_cast<uint32_t(*)[64]>(&v[c0]));
+      for (int c0 = 0; c0 < D; c0 += 64) tmem_ld64w(tQ + c0, *reinterpret_cast<uint32_t(*)[64]>(&v[c0]));
       tc_fence_before();
       mbar_arrive(&bars.dq_empty);
-      if (threadIdx.x == 0) TTT_TRACE_EV(2, 2, i);
+      if (threadIdx.x == 0) TTT_TRACE_EV(2, 2, t);
       const int row_base = (((b * p.Hq + h) * p.nqt + qt) * (D / 32)) * 128 + wq * 32;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
-        uint8_t* buf = stage + (cc & 1) * 4096;
-        if (lane == 0) bulk_wait_read1();  // the reduce that last used this buffer has read it
+        if (lane == 0) bulk_wait_read0();  // the previous reduce has read the staging buffer
         __syncwarp();
+        const float c = p.scale;
 #pragma unroll
         for (int k4 = 0; k4 < 8; ++k4) {
-          const float c = p.scale;
-          float4 val = make_float4(c * __uint_as_float(v[cc * 32 + 4 * k4]), c * __uint_as_float(v[cc * 32 + 4 * k4 + 1]),
-                                   c * __uint_as_float(v[cc * 32 + 4 * k4 + 2]),
-                                   c * __uint_as_float(v[cc * 32 + 4 * k4 + 3]));
-          *reinterpret_cast<float4*>(buf + lane * 128 + ((k4 ^ (lane & 7)) << 4)) = val;
+          const float4 val =
+              make_float4(c * __uint_as_float(v[cc * 32 + 4 * k4]), c * __uint_as_float(v[cc * 32 + 4 * k4 + 1]),
+                          c * __uint_as_float(v[cc * 32 + 4 * k4 + 2]), c * __uint_as_float(v[cc * 32 + 4 * k4 + 3]));
+          *reinterpret_cast<float4*>(stage + lane * 128 + ((k4 ^ (lane & 7)) << 4)) = val;
         }
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_reduce_add_2d(&maps.dqacc, buf, 0, row_base + cc * 128);
+          tma_reduce_add_2d(&maps.dqacc, stage, 0, row_base + cc * 128);
           bulk_commit();
         }
       }
@@ -791,7 +829,7 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
   }
   // 2. main tensor-core kernel
   {
-    const int smem = 5 * kTile * D * 2 + 32768 + 2048 + 32768 + 256;
+    const int smem = BwdSmem<D>::bytes;
     static bool attr_set = false;
     if (!attr_set) {
       cudaError_t e =

@@ -51,6 +51,7 @@ struct FwdMaps {
 };
 struct BwdMaps {
   CUtensorMap q, k, v, dout;
+  CUtensorMap dout64;  // dO with 64-row boxes (the 64-query sub-item halves)
   CUtensorMap dqacc;  // 2-D fp32 view of the tiled dq_acc: {32 cols, rows}, box 32 x 32, SW128
 };
 
