@@ -22,8 +22,8 @@ lib.ttt_debug_trace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
 for _ in range(2):
     ttt.ttt_attn_bwd(desc, j, q, k, v, [], [], out, lse, do, dq, dk, dv, [], [], flags=0, workspace=ws, out_lo=olo)
 lib.ttt_debug_trace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
-names = {0: {1: "mma:wait_p", 2: "mma:got_p", 3: "mma:got_ds", 4: "mma:got_q", 5: "mma:got_dqempty", 6: "mma:got_do"},
-         1: {1: "cmp:got_s", 2: "cmp:p_done", 3: "cmp:got_dp", 4: "cmp:ds_done"},
+names = {0: {1: "mma:got_p_a", 2: "mma:got_p_b", 3: "mma:got_ds_a", 4: "mma:got_ds_b", 5: "mma:got_dqempty", 6: "mma:dP_issued"},
+         1: {1: "cmpA:got_s", 2: "cmpA:p_done", 3: "cmpA:got_dp", 4: "cmpA:ds_done"},
          2: {1: "dq:got_dq", 2: "dq:drained"}}
 ev = []
 for role in range(3):
@@ -40,8 +40,8 @@ for i in sorted(items)[:3] + sorted(items)[20:24]:
     base = items[i][0][0]
     print(f"item {i}: " + "  ".join(f"{n}@{t-base}" for t, n in items[i]))
 # per-item period
-starts = sorted((v[0][0], i) for i, v in items.items() if any(n == "cmp:got_s" for _, n in v))
-ts = [t for t, n, i in ev if n == "cmp:got_s"]
+starts = sorted((v[0][0], i) for i, v in items.items() if any(n == "cmpA:got_s" for _, n in v))
+ts = [t for t, n, i in ev if n == "cmpA:got_s"]
 d = np.diff(ts)
 print("items", len(ts), "period clk median", np.median(d), "mean", d.mean())
 for nm in ["mma:got_p", "mma:got_ds", "mma:got_q", "mma:got_dqempty", "mma:got_do", "cmp:p_done", "cmp:got_dp", "cmp:ds_done", "dq:got_dq", "dq:drained"]:
@@ -49,7 +49,7 @@ for nm in ["mma:got_p", "mma:got_ds", "mma:got_q", "mma:got_dqempty", "mma:got_d
 # average offsets relative to cmp:got_s of the same item
 acc = {}
 for i, v in items.items():
-    s0 = [t for t, n in v if n == "cmp:got_s"]
+    s0 = [t for t, n in v if n == "cmpA:got_s"]
     if not s0: continue
     for t, n in v:
         acc.setdefault(n, []).append(t - s0[0])

@@ -361,12 +361,10 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
 }
 
 // Work item = one 128-query tile (head h, tile qt) split into two 64-query
-// sub-items x = a, b. S^T / dP^T are double-buffered per sub-item in TMEM, so
-// the MMA warp works on one sub-item while a compute warpgroup works on the
-// other. Per tile the MMA issue order is
-//   dV(a) S'(a) dK(a) | dV(b) S'(b) dK(b) | dQ(a+b) | [drain] dP'(a) dP'(b)
-// (S' / dP' belong to the next tile). dQ (M = 128 queries, N = D) aliases the two
-// dP^T buffers, so the next dP waits for the dQ drain only.
+// sub-items x = a, b, each with its own S^T / dP^T buffers in TMEM and its own
+// compute warpgroup. dQ (M = 128 queries, N = D) aliases the two dP^T buffers,
+// so the next dP waits for the dQ drain only; the issue order (MMA warp) keeps
+// the tensor pipe busy with dV while dQ is drained.
 // Warp roles (16 warps; setmaxnreg rebalances the register file):
 //   warps 0-3   dQ drain            (thread = query row of TMEM lane quadrant w)
 //   warps 4-7   compute sub-item a  (thread = key row, 64 query columns)
@@ -535,6 +533,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                   sdesc_sw128(aQ + qs * TB + (64 * x + 16 * ks) * 128, 16384, 1024), idKV,
                   (!first || ks > 0) ? 1u : 0u);
       };
+      // Issue order (program order of this single thread = tensor-pipe order):
+      //   prologue: S(0,a) S(0,b) dP(0,a) dP(0,b) dV(0,a) dV(0,b) S(1,a) S(1,b)
+      //   tile t:   dK(t,a) dK(t,b) dQ(t) | dV(t+1,a) dV(t+1,b) | [dQ drained] dP(t+1,a) dP(t+1,b)
+      //             | S(t+2,a) S(t+2,b)
+      // dV(t+1) fills the pipe while dQ(t) is drained; the compute warps' P(t+1) runs under
+      // dK(t) / dQ(t). A dO half is released only after both of its readers (dV, dP).
+      auto slot_of = [](int t, int x) { return (2 * t + x) % 3; };
+      auto use_of = [](int t, int x) { return ((2 * t + x) / 3) & 1; };
       mbar_wait(&bars.kv_full, 0);
       mbar_wait(&bars.q_full[0], 0);
       tc_fence_after();
@@ -544,28 +550,30 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       umma_commit(&bars.s_full[1]);
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
-        mbar_wait(&bars.do_full[x], 0);
+        mbar_wait(&bars.do_full[slot_of(0, x)], use_of(0, x));
         tc_fence_after();
-        issue_dP(x, x);
+        issue_dP(slot_of(0, x), x);
         umma_commit(&bars.dp_full[x]);
+      }
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        mbar_wait(&bars.p_full[x], 0);
+        tc_fence_after();
+        issue_dV(slot_of(0, x), x, x == 0);
+        umma_commit(&bars.do_empty[slot_of(0, x)]);  // dP(0,x) was issued before: both readers done
+      }
+      if (n_items > 1) {
+        mbar_wait(&bars.q_full[1], 0);
+        tc_fence_after();
+        issue_S(1, 0);
+        umma_commit(&bars.s_full[0]);
+        issue_S(1, 1);
+        umma_commit(&bars.s_full[1]);
       }
       for (int t = 0; t < n_items; ++t) {
         const int qs = t & 1;
-        const bool more = t + 1 < n_items;
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
-          const int slot = (2 * t + x) % 3;
-          mbar_wait(&bars.p_full[x], t & 1);
-          TTT_TRACE_EV(0, 1 + x, t);
-          tc_fence_after();
-          issue_dV(slot, x, t == 0 && x == 0);
-          umma_commit(&bars.do_empty[slot]);
-          if (more) {  // next tile's S^T[x]: its P^T[x] was just consumed (in-order pipe)
-            if (x == 0) mbar_wait(&bars.q_full[(t + 1) & 1], ((t + 1) >> 1) & 1);
-            tc_fence_after();
-            issue_S((t + 1) & 1, x);
-            umma_commit(&bars.s_full[x]);
-          }
           mbar_wait(&bars.ds_full[x], t & 1);
           TTT_TRACE_EV(0, 3 + x, t);
           tc_fence_after();
@@ -579,18 +587,34 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                   idDQ, ks > 0);
         umma_commit(&bars.dq_full);
         umma_commit(&bars.ds_empty);
-        if (more) {
-          mbar_wait(&bars.dq_empty, t & 1);
+        if (t + 1 < n_items) {
+          const int t1 = t + 1;
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {  // dV(t+1, x): P^T(t+1, x) and the dO half are ready
+            mbar_wait(&bars.p_full[x], t1 & 1);
+            TTT_TRACE_EV(0, 1 + x, t1);
+            mbar_wait(&bars.do_full[slot_of(t1, x)], use_of(t1, x));
+            tc_fence_after();
+            issue_dV(slot_of(t1, x), x, false);
+          }
+          mbar_wait(&bars.dq_empty, t & 1);  // dQ(t) drained: the dP^T buffers are free
           TTT_TRACE_EV(0, 5, t);
+          tc_fence_after();
 #pragma unroll
           for (int x = 0; x < 2; ++x) {
-            const int u = 2 * (t + 1) + x;
-            mbar_wait(&bars.do_full[u % 3], (u / 3) & 1);
-            tc_fence_after();
-            issue_dP(u % 3, x);
+            issue_dP(slot_of(t1, x), x);
             umma_commit(&bars.dp_full[x]);
+            umma_commit(&bars.do_empty[slot_of(t1, x)]);
           }
           TTT_TRACE_EV(0, 6, t);
+          if (t + 2 < n_items) {  // S(t+2, x) over P^T(t+1, x), consumed by dV(t+1, x) above
+            mbar_wait(&bars.q_full[(t + 2) & 1], ((t + 2) >> 1) & 1);
+            tc_fence_after();
+            issue_S((t + 2) & 1, 0);
+            umma_commit(&bars.s_full[0]);
+            issue_S((t + 2) & 1, 1);
+            umma_commit(&bars.s_full[1]);
+          }
         }
       }
       umma_commit(&bars.acc_full);
