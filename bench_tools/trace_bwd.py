@@ -22,7 +22,7 @@ lib.ttt_debug_trace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
 for _ in range(2):
     ttt.ttt_attn_bwd(desc, j, q, k, v, [], [], out, lse, do, dq, dk, dv, [], [], flags=0, workspace=ws, out_lo=olo)
 lib.ttt_debug_trace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
-names = {0: {1: "mma:got_p_a", 2: "mma:got_p_b", 3: "mma:got_ds_a", 4: "mma:got_ds_b", 5: "mma:got_dqempty", 6: "mma:dP_issued"},
+names = {0: {1: "mma:got_p_a", 2: "mma:got_p_b", 3: "mma:got_ds_a", 4: "mma:got_ds_b", 5: "mma:got_dqempty", 6: "mma:dP_issued", 7: "mma:dK_a_issued", 8: "mma:dK_b_issued", 9: "mma:dQ_issued", 10: "mma:S_issued"},
          1: {1: "cmpA:got_s", 2: "cmpA:p_done", 3: "cmpA:got_dp", 4: "cmpA:ds_done"},
          2: {1: "dq:got_dq", 2: "dq:drained"}}
 ev = []
@@ -69,3 +69,12 @@ for phase, nm in ((False, "P"), (True, "dS")):
         t0_ = min(d.values())
         for k, t in d.items(): rel[k].append(t - t0_)
     print(nm, "phase: median lag behind the first warp, by warp:", {k: int(np.median(v)) for k, v in rel.items() if v})
+
+# per-warp arrive times relative to cmpA:got_s of the same tile
+gs = {i: t for t, n, i in ev if n == "cmpA:got_s"}
+for phase, nm in ((False, "P arrive"), (True, "dS arrive")):
+    rel = {}
+    for (it, ph), d in w.items():
+        if ph != phase or it not in gs or it < 4: continue
+        for k, t in d.items(): rel.setdefault(k, []).append(t - gs[it])
+    print(nm, "median offset by warp:", {k: int(np.median(v)) for k, v in sorted(rel.items())})

@@ -497,43 +497,44 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp == 12) {
-    // ================= MMA issuer =================
+    // ================= MMA issuer (whole warp, converged; elect.sync inside each issue) =================
     reg_dealloc<88>();
-    if (lane == 0) {
+    {
       TTT_TRACE_DECL(0);
       constexpr uint32_t idSP = idesc_bf16_f32(128, 64, false, false);  // S^T = K Q_x^T, dP^T = V dO_x^T
       constexpr uint32_t idKV = idesc_bf16_f32(128, D, false, true);    // dV += P^T dO_x, dK += dS^T Q_x
       constexpr uint32_t idDQ = idesc_bf16_f32(128, D, true, true);     // dQ = dS K
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aDO = smem_u32(sDO),
-                     aDS = smem_u32(sDS);
-      // K-major operands: 128-row tiles (Q) and 64-row halves (dO) share the 8-row x 128 B atom
-      auto kmaj = [](uint32_t base, int ks, uint32_t box_bytes) {
-        return sdesc_sw128(base + (ks >> 2) * box_bytes + (ks & 3) * 32, 16, 1024);
-      };
+      // descriptor bases (built once; per k-step only a constant is added to the start field)
+      const uint64_t dK_kmaj = sdesc_sw128(smem_u32(sK), 16, 1024), dV_kmaj = sdesc_sw128(smem_u32(sV), 16, 1024);
+      const uint64_t dQ_kmaj = sdesc_sw128(smem_u32(sQ), 16, 1024), dDO_kmaj = sdesc_sw128(smem_u32(sDO), 16, 1024);
+      const uint64_t dDO_mn = sdesc_sw128(smem_u32(sDO), HB / NBOX, 1024), dQ_mn = sdesc_sw128(smem_u32(sQ), 16384, 1024);
+      const uint64_t dDS_mn = sdesc_sw128(smem_u32(sDS), 16384, 1024), dK_mn = sdesc_sw128(smem_u32(sK), 16384, 1024);
+      auto kofs = [](int ks, uint32_t box_bytes) { return (uint32_t)((ks >> 2) * box_bytes + (ks & 3) * 32); };
       auto issue_S = [&](int qs, int x) {  // S^T[x] = K Q_x^T  (Q_x = rows 64x.. of the Q stage)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
-          umma_ss(tbase + 64 * x, kmaj(aK, ks, 16384), kmaj(aQ + qs * TB + 64 * x * 128, ks, 16384), idSP, ks > 0);
+          umma_ss_e(tbase + 64 * x, sdesc_add(dK_kmaj, kofs(ks, 16384)),
+                    sdesc_add(dQ_kmaj, qs * TB + 64 * x * 128 + kofs(ks, 16384)), idSP, ks > 0);
       };
       auto issue_dP = [&](int slot, int x) {  // dP^T[x] = V dO_x^T
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
-          umma_ss(tbase + 128 + 64 * x, kmaj(aV, ks, 16384), kmaj(aDO + slot * HB, ks, HB / NBOX), idSP, ks > 0);
+          umma_ss_e(tbase + 128 + 64 * x, sdesc_add(dV_kmaj, kofs(ks, 16384)),
+                    sdesc_add(dDO_kmaj, slot * HB + kofs(ks, HB / NBOX)), idSP, ks > 0);
       };
       auto issue_dV = [&](int slot, int x, bool first) {  // dV += P^T[x] dO_x  (K = 64 queries)
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
-          umma_ts(tbase + 256, tbase + 64 * x + 8 * ks, sdesc_sw128(aDO + slot * HB + ks * 2048, HB / NBOX, 1024),
-                  idKV, (!first || ks > 0) ? 1u : 0u);
+          umma_ts_e(tbase + 256, tbase + 64 * x + 8 * ks, sdesc_add(dDO_mn, slot * HB + ks * 2048), idKV,
+                    (!first || ks > 0) ? 1u : 0u);
       };
       auto issue_dK = [&](int qs, int x, bool first) {  // dK += dS^T[x] Q_x
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
-          umma_ts(tbase + 384, tbase + 128 + 64 * x + 8 * ks,
-                  sdesc_sw128(aQ + qs * TB + (64 * x + 16 * ks) * 128, 16384, 1024), idKV,
-                  (!first || ks > 0) ? 1u : 0u);
+          umma_ts_e(tbase + 384, tbase + 128 + 64 * x + 8 * ks, sdesc_add(dQ_mn, qs * TB + (64 * x + 16 * ks) * 128),
+                    idKV, (!first || ks > 0) ? 1u : 0u);
       };
-      // Issue order (program order of this single thread = tensor-pipe order):
+      // Issue order (program order of this warp = tensor-pipe order):
       //   prologue: S(0,a) S(0,b) dP(0,a) dP(0,b) dV(0,a) dV(0,b) S(1,a) S(1,b)
       //   tile t:   dK(t,a) dK(t,b) dQ(t) | dV(t+1,a) dV(t+1,b) | [dQ drained] dP(t+1,a) dP(t+1,b)
       //             | S(t+2,a) S(t+2,b)
@@ -545,30 +546,30 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(&bars.q_full[0], 0);
       tc_fence_after();
       issue_S(0, 0);
-      umma_commit(&bars.s_full[0]);
+      umma_commit_e(&bars.s_full[0]);
       issue_S(0, 1);
-      umma_commit(&bars.s_full[1]);
+      umma_commit_e(&bars.s_full[1]);
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
         mbar_wait(&bars.do_full[slot_of(0, x)], use_of(0, x));
         tc_fence_after();
         issue_dP(slot_of(0, x), x);
-        umma_commit(&bars.dp_full[x]);
+        umma_commit_e(&bars.dp_full[x]);
       }
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
         mbar_wait(&bars.p_full[x], 0);
         tc_fence_after();
         issue_dV(slot_of(0, x), x, x == 0);
-        umma_commit(&bars.do_empty[slot_of(0, x)]);  // dP(0,x) was issued before: both readers done
+        umma_commit_e(&bars.do_empty[slot_of(0, x)]);  // dP(0,x) was issued before: both readers done
       }
       if (n_items > 1) {
         mbar_wait(&bars.q_full[1], 0);
         tc_fence_after();
         issue_S(1, 0);
-        umma_commit(&bars.s_full[0]);
+        umma_commit_e(&bars.s_full[0]);
         issue_S(1, 1);
-        umma_commit(&bars.s_full[1]);
+        umma_commit_e(&bars.s_full[1]);
       }
       for (int t = 0; t < n_items; ++t) {
         const int qs = t & 1;
@@ -578,15 +579,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           TTT_TRACE_EV(0, 3 + x, t);
           tc_fence_after();
           issue_dK(qs, x, t == 0 && x == 0);
+          TTT_TRACE_EV(0, 7 + x, t);
         }
-        umma_commit(&bars.q_empty[qs]);
+        umma_commit_e(&bars.q_empty[qs]);
         // dQ = dS K for the whole 128-query tile -> TMEM [128, 128+D)  (A = dS from smem, MN-major)
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          umma_ss(tbase + 128, sdesc_sw128(aDS + ks * 2048, 16384, 1024), sdesc_sw128(aK + ks * 2048, 16384, 1024),
-                  idDQ, ks > 0);
-        umma_commit(&bars.dq_full);
-        umma_commit(&bars.ds_empty);
+          umma_ss_e(tbase + 128, sdesc_add(dDS_mn, ks * 2048), sdesc_add(dK_mn, ks * 2048), idDQ, ks > 0);
+        umma_commit_e(&bars.dq_full);
+        umma_commit_e(&bars.ds_empty);
+        TTT_TRACE_EV(0, 9, t);
         if (t + 1 < n_items) {
           const int t1 = t + 1;
 #pragma unroll
@@ -603,21 +605,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int x = 0; x < 2; ++x) {
             issue_dP(slot_of(t1, x), x);
-            umma_commit(&bars.dp_full[x]);
-            umma_commit(&bars.do_empty[slot_of(t1, x)]);
+            umma_commit_e(&bars.dp_full[x]);
+            umma_commit_e(&bars.do_empty[slot_of(t1, x)]);
           }
           TTT_TRACE_EV(0, 6, t);
           if (t + 2 < n_items) {  // S(t+2, x) over P^T(t+1, x), consumed by dV(t+1, x) above
             mbar_wait(&bars.q_full[(t + 2) & 1], ((t + 2) >> 1) & 1);
             tc_fence_after();
             issue_S((t + 2) & 1, 0);
-            umma_commit(&bars.s_full[0]);
+            umma_commit_e(&bars.s_full[0]);
             issue_S((t + 2) & 1, 1);
-            umma_commit(&bars.s_full[1]);
+            umma_commit_e(&bars.s_full[1]);
+            TTT_TRACE_EV(0, 10, t);
           }
         }
       }
-      umma_commit(&bars.acc_full);
+      umma_commit_e(&bars.acc_full);
     }
   } else if (warp >= 4 && warp < 12) {
     // ================= compute: P^T, dS^T of sub-item x (thread = key row, 64 query columns) ====
@@ -673,6 +676,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars.p_full[x]);
       if (threadIdx.x == 128) TTT_TRACE_EV(1, 2, t);
+#ifdef TTT_TRACE
+      if (lane == 0 && blockIdx.x == g_ttt_trace_cta && t < 2000)
+        g_ttt_trace[3][t * 16 + warp] = (clock64() << 20) | ((unsigned long long)warp << 12) | (unsigned long long)(t & 0xFFF);
+#endif
       mbar_wait(&bars.dp_full[x], t & 1);
       mbar_wait(&bars.ds_empty, (t & 1) ^ 1);  // dQ of the previous tile has read the dS buffer
       if (threadIdx.x == 128) TTT_TRACE_EV(1, 3, t);
@@ -711,6 +718,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars.ds_full[x]);
       if (threadIdx.x == 128) TTT_TRACE_EV(1, 4, t);
+#ifdef TTT_TRACE
+      if (lane == 0 && blockIdx.x == g_ttt_trace_cta && t < 2000)
+        g_ttt_trace[3][32768 + t * 16 + warp] =
+            (clock64() << 20) | ((unsigned long long)(16 + warp) << 12) | (unsigned long long)(t & 0xFFF);
+#endif
     }
     // ---- dK, dV accumulators -> global (fp32 atomics: head splits and steps add up) ----
     mbar_wait(&bars.acc_full, 0);

@@ -129,40 +129,36 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
   } else if (warp == 9) {
-    // ================= MMA issuer (one thread) =================
-    if (lane == 0) {
+    // ================= MMA issuer (whole warp, converged; elect.sync inside each issue) =================
+    {
       constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);  // S = Q K^T, both K-major
       constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);     // O += P V, V MN-major
-      const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+      const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ), 16, 1024), dK0 = sdesc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t dV0 = sdesc_sw128(smem_u32(sV), 16384, 1024);
       auto issue_S = [&](int slot, int kst) {
-        const uint32_t qa = q_addr + slot * TB, ka = k_addr + kst * TB;
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-          umma_ss(tbase + slot * 128, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), idS,
-                  ks > 0);
+          umma_ss_e(tbase + slot * 128, sdesc_add(dQ0, slot * TB + off), sdesc_add(dK0, kst * TB + off), idS, ks > 0);
         }
       };
       auto issue_PV = [&](int slot, int vst, bool acc) {
-        const uint32_t va = v_addr + vst * TB;
 #pragma unroll
         for (int ks = 0; ks < kTile / 16; ++ks)
-          umma_ts(tbase + 256 + slot * 128, tbase + slot * 128 + ks * 8, sdesc_sw128(va + ks * 2048, 16384, 1024),
-                  idO, (acc || ks > 0) ? 1u : 0u);
+          umma_ts_e(tbase + 256 + slot * 128, tbase + slot * 128 + ks * 8, sdesc_add(dV0, vst * TB + ks * 2048), idO,
+                    (acc || ks > 0) ? 1u : 0u);
       };
-      TTT_TRACE_DECL(0);
-      TTT_TRACE_EV(0, 9, 0);
       mbar_wait(&bars.q, 0);
       mbar_wait(&bars.k_full[0], 0);
       TTT_TRACE_EV(0, 8, 0);
       tc_fence_after();
       issue_S(0, 0);
-      umma_commit(&bars.s_full[0]);
+      umma_commit_e(&bars.s_full[0]);
       if (has1) {
         issue_S(1, 0);
-        umma_commit(&bars.s_full[1]);
+        umma_commit_e(&bars.s_full[1]);
       }
-      umma_commit(&bars.k_empty[0]);
+      umma_commit_e(&bars.k_empty[0]);
       for (int n = 0; n < nkv; ++n) {
         const int vst = n & 1, vph = (n >> 1) & 1;
         const bool more = n + 1 < nkv;
@@ -177,26 +173,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           mbar_wait(&bars.k_full[kst], kph);
           tc_fence_after();
           issue_S(0, kst);
-          umma_commit(&bars.s_full[0]);  // also covers PV0_n (commit tracks all prior MMAs)
+          umma_commit_e(&bars.s_full[0]);  // also covers PV0_n (commit tracks all prior MMAs)
         } else {
-          umma_commit(&bars.o_full[0]);
+          umma_commit_e(&bars.o_full[0]);
         }
         if (has1) {
           mbar_wait(&bars.p_full[1], n & 1);
           TTT_TRACE_EV(0, 3, n);
           tc_fence_after();
           issue_PV(1, vst, n > 0);
-          umma_commit(&bars.v_empty[vst]);
+          umma_commit_e(&bars.v_empty[vst]);
           if (more) {
             issue_S(1, kst);
-            umma_commit(&bars.s_full[1]);
-            umma_commit(&bars.k_empty[kst]);
+            umma_commit_e(&bars.s_full[1]);
+            umma_commit_e(&bars.k_empty[kst]);
           } else {
-            umma_commit(&bars.o_full[1]);
+            umma_commit_e(&bars.o_full[1]);
           }
         } else {
-          umma_commit(&bars.v_empty[vst]);
-          if (more) umma_commit(&bars.k_empty[kst]);
+          umma_commit_e(&bars.v_empty[vst]);
+          if (more) umma_commit_e(&bars.k_empty[kst]);
         }
       }
     }
