@@ -3,14 +3,15 @@
 // Recompute-based (no saved probabilities): P = exp(S - lse) is
 // rebuilt from the forward's lse. Three kernels per call, all on `stream`:
 //
-//  1. ttt_bwd_pre_kernel (HBM-streaming, CUDA cores), half-warp per (b, r, h):
-//       Delta_{h,r} = dO_{h,r} . O_{h,r};  lse2 = lse * log2(e) (both stored negated);
-//       zeroes the fp32 dq accumulator, and dK_0/dV_0 when not accumulating.
+//  1. ttt_bwd_pre_kernel (HBM-streaming, CUDA cores), one warp per (b, r, kv head g):
+//       Delta_{h,r} = dO_{h,r} . O_{h,r};  lse2 = lse * log2(e)
+//       TTT diagonal keys (the j step entries of row r < T_b, Alg. 2 M_suffix,
+//       PAPER.md:305-309): p_i = exp(c q.K_i[r] - lse), dp_i = dO.V_i[r],
+//       ds_i = p_i (dp_i - Delta), dq_acc[r] = c sum_i ds_i K_i[r] (initialises the
+//       fp32 dq accumulator), dK_i[r] (+)= c sum_h ds_i q_h, dV_i[r] (+)= sum_h p_i dO_h.
+//       Zeroes dK_0/dV_0 rows when not accumulating (the main kernel adds into them).
 //  2. ttt_bwd_sm100_kernel (tcgen05), KV-outer: one CTA per (b, g, 128-key tile kt,
-//     head subset); loops over its query heads x causal q tiles qt >= kt; two extra
-//     warps do the TTT diagonal keys of the CTA's key rows (Alg. 2 M_suffix,
-//     PAPER.md:305-309): p_i = exp(c q.K_i[r] - lse), ds_i = p_i (dO.V_i[r] - Delta),
-//     dK_i[r] (+)= c sum_h ds_i q_h, dV_i[r] (+)= sum_h p_i dO_h, dq[r] += c sum_i ds_i K_i[r].
+//     head subset); loops over its query heads x causal q tiles qt >= kt:
 //       S^T = K Q^T, dP^T = V dO^T                         (SS MMAs, TMEM)
 //       P^T = exp2(S^T c log2e - lse2), dS^T = P^T o (dP^T - Delta)   (compute warps)
 //       dV += P^T dO, dK += dS^T Q                         (A operand from TMEM)
@@ -69,167 +70,247 @@ __device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int
 }
 
 // ------------------------------------------------------------------ kernel 1
-// Pre-pass (HBM-streaming): one half-warp per (row r, query head h):
-//   -Delta = -(dO . (out + out_lo)),  -lse2 = -lse log2 e   (stored negated for the FFMA2s)
-//   dq_acc row <- 0 (the main kernel's TMA reduce-adds and diagonal warps add into it)
-// and, when overwriting, zero the dK_0 / dV_0 rows (the main kernel adds into them) and the
-// dK_i / dV_i rows of padded keys r >= T_b (no diagonal key there, Alg. 2 m_pad).
+// HBM-streaming, TMA-staged: a persistent block walks groups of NR consecutive
+// (b, r, g) rows. For such a group every operand is ONE contiguous block in HBM
+// (q / dO / O / O_lo: NR*G*D bf16; K_i, V_i: NR*D bf16; dK_i, dV_i: NR*D fp32), so
+// thread 0 moves each with a single 1-D cp.async.bulk into a double-buffered
+// stage. One HALF-warp per (row, query head): Delta, the diagonal p_i / ds_i and
+// dq stay in registers; dK_i / dV_i (sums over the G heads) are accumulated with
+// shared-memory atomics in the stage and written back with bulk stores. Lane hl
+// owns elements [hl*E/2, +E/2) and [D/2 + hl*E/2, +E/2): every half-warp smem
+// access is contiguous (bank-conflict free).
+struct PreLayout {
+  int NR, G, D, step, acc, has_lo;
+  uint32_t off_q, off_do, off_o, off_olo, off_k, off_v, off_dk, off_dv, stage_bytes, off_sc, total;
+  __host__ __device__ void init(int nr, int g, int d, int j, int accumulate, int lo) {
+    NR = nr; G = g; D = d; step = j; acc = accumulate; has_lo = lo;
+    const uint32_t qb = (uint32_t)nr * g * d * 2, kb = (uint32_t)nr * d * 2, fb = (uint32_t)nr * d * 4;
+    off_q = 0; off_do = qb; off_o = 2 * qb; off_olo = 3 * qb;
+    off_k = 4 * qb; off_v = off_k + j * kb; off_dk = off_v + j * kb; off_dv = off_dk + j * fb;
+    stage_bytes = (off_dv + j * fb + 127) & ~127u;
+    off_sc = 2 * stage_bytes;                            // fp32 [NR][j][G][2]: (p_i, c ds_i) per head
+    total = off_sc + ((uint32_t)nr * (j > 0 ? j : 1) * g * 8 + 127) / 128 * 128 + 64;  // + 2 mbarriers
+  }
+};
+
+__device__ __forceinline__ void bulk_store_1d(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load_1d_(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// split-lane bf16 row chunk: E/2 elements at hl*E/2 and at D/2 + hl*E/2 -> fp32
 template <int D>
-__global__ void __launch_bounds__(256) ttt_bwd_pre_kernel(const __grid_constant__ Params p) {
-  constexpr int E = D / 16;
-  const int hl = threadIdx.x & 15;
-  const long pr = (long)blockIdx.x * 16 + (threadIdx.x >> 4);  // (b, r, h) row-head index
-  const long npr = (long)p.B * p.L * p.Hq;
-  const bool valid = pr < npr;
-  const long pc = valid ? pr : npr - 1;  // clamp: shuffles stay warp-uniform
-  const int h = (int)(pc % p.Hq);
-  const int r = (int)((pc / p.Hq) % p.L);
-  const int b = (int)(pc / ((long)p.Hq * p.L));
-  const size_t q_off = (size_t)pc * D + hl * E;  // [B][L][Hq][D] row-major
-  float o[E], d[E];
-  ld_row<D>(p.o, q_off, o);
-  ld_row<D>(p.dout, q_off, d);
-  if (p.o_lo) {  // O = bf16 out + bf16 residual: Delta from ~16-bit-accurate O
-    float lo[E];
-    ld_row<D>(p.o_lo, q_off, lo);
+__device__ __forceinline__ void lds_split(const uint8_t* row, int hl, float (&x)[D / 16]) {
+  constexpr int H = D / 32;  // elements per half (4 for D=128, 2 for D=64)
 #pragma unroll
-    for (int e = 0; e < E; ++e) o[e] += lo[e];
-  }
-  float acc = 0.f;
-#pragma unroll
-  for (int e = 0; e < E; ++e) acc = fmaf(o[e], d[e], acc);
-  const float del = half_allsum(acc);  // Delta_r = dO_r . O_r
-  if (!valid) return;
-  const size_t li = ((size_t)b * p.Hq + h) * p.L + r;
-  if (hl == 0) {
-    p.delta[li] = -del;
-    p.lse2[li] = -p.lse_in[li] * kLog2e;
-  }
-  float* dst = p.dq_acc + dqacc_index(p, b, h, r, hl * E);
-#pragma unroll
-  for (int e = 0; e < E / 4; ++e) reinterpret_cast<float4*>(dst)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (!p.accumulate && (h % p.G) == 0) {  // once per (b, r, kv head)
-    const int g = h / p.G;
-    const size_t kv = (((size_t)b * p.L + r) * p.Hkv + g) * D + hl * E;
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int e = 0; e < E / 4; ++e) {
-      reinterpret_cast<float4*>(p.dk + kv)[e] = z;
-      reinterpret_cast<float4*>(p.dv + kv)[e] = z;
-    }
-    if (r >= p.seq_lens[b]) {
-      for (int i = 0; i < p.step; ++i) {
-#pragma unroll
-        for (int e = 0; e < E / 4; ++e) {
-          reinterpret_cast<float4*>(p.dks[i] + kv)[e] = z;
-          reinterpret_cast<float4*>(p.dvs[i] + kv)[e] = z;
-        }
-      }
+  for (int part = 0; part < 2; ++part) {
+    const uint8_t* src = row + (part * (D / 2) + hl * H) * 2;
+    if constexpr (H == 4) {
+      const uint2 u = *reinterpret_cast<const uint2*>(src);
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      x[part * 4 + 0] = a.x; x[part * 4 + 1] = a.y; x[part * 4 + 2] = c.x; x[part * 4 + 3] = c.y;
+    } else {
+      const uint32_t u = *reinterpret_cast<const uint32_t*>(src);
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+      x[part * 2 + 0] = a.x; x[part * 2 + 1] = a.y;
     }
   }
 }
-
-// TTT diagonal keys of key rows r (Alg. 2 M_suffix): per query head h of
-// the group and step i <= j,  p = exp(c q_h.K_i[r] - lse),  ds = p (dO_h.V_i[r] - Delta);
-// dK_i[r] (+)= c sum_h ds q_h, dV_i[r] (+)= sum_h p dO_h, dq_h[r] += c sum_i ds K_i[r].
-// Run by two otherwise idle warps of the main kernel (one half-warp per row, 16 lanes x
-// D/16 elements), so this HBM traffic overlaps the tensor pipeline.
 template <int D>
-__device__ void diag_bwd_rows(const Params& p, int b, int g, int row0, int T, int slot, int nslots) {
+__device__ __forceinline__ int split_col(int hl, int e) {  // D index of lane element e
+  constexpr int H = D / 32;
+  return (e < H) ? hl * H + e : D / 2 + hl * H + (e - H);
+}
+
+template <int D>
+__global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant__ Params p, PreLayout lay) {
   constexpr int E = D / 16;
-  constexpr int SC = 128;  // (p, c ds) scalars per (head, step) kept per row chunk (local memory)
-  const int hl = threadIdx.x & 15;
-  const int G = p.G, j = p.step;
-  const int JC = max(1, SC / G);  // steps per chunk
-  float sc[2 * SC];
-  for (int rr = slot; rr < kTile; rr += nslots) {
-    const int r = row0 + rr;
-    const bool act = r < T;  // rows r >= T have no diagonal key (their dK_i rows are zeroed by the pre-pass)
-    const int rc = act ? r : row0;  // clamp for uniform shuffles
-    const size_t kv_off = (((size_t)b * p.L + rc) * p.Hkv + g) * D + hl * E;
-    for (int i0 = 0; i0 < j; i0 += JC) {
-      const int nj = min(JC, j - i0);
-      // pass A: scalars p, c ds for (head, step)
-      for (int hh = 0; hh < G; ++hh) {
-        const int h = g * G + hh;
-        const size_t q_off = (((size_t)b * p.L + rc) * p.Hq + h) * D + hl * E;
-        const size_t li = ((size_t)b * p.Hq + h) * p.L + rc;
-        float qq[E], dd[E];
-        ld_row<D>(p.q, q_off, qq);
-        ld_row<D>(p.dout, q_off, dd);
-        const float negl2 = p.lse2[li], negdel = p.delta[li];
-        for (int ii = 0; ii < nj; ++ii) {
-          float kk[E], vv[E];
-          ld_row<D>(p.ks[i0 + ii], kv_off, kk);
-          ld_row<D>(p.vs[i0 + ii], kv_off, vv);
-          float sdot = 0.f, dp = 0.f;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            sdot = fmaf(qq[e], kk[e], sdot);
-            dp = fmaf(dd[e], vv[e], dp);
-          }
-#pragma unroll
-          for (int o2 = 8; o2 > 0; o2 >>= 1) {
-            sdot += __shfl_xor_sync(0xffffffffu, sdot, o2);
-            dp += __shfl_xor_sync(0xffffffffu, dp, o2);
-          }
-          const float pv = act ? ex2(fmaf(sdot, p.scale_log2, negl2)) : 0.f;  // p_i = exp(c q.k_i - lse)
-          sc[2 * (hh * JC + ii)] = pv;
-          sc[2 * (hh * JC + ii) + 1] = p.scale * pv * (dp + negdel);          // c ds_i
-        }
+  extern __shared__ __align__(128) uint8_t psm[];
+  const int tid = threadIdx.x, hl = tid & 15, pair = tid >> 4;
+  const int NR = lay.NR, G = p.G, j = p.step;
+  const long nrows = (long)p.B * p.L * p.Hkv;
+  const long ngroups = (nrows + NR - 1) / NR;
+  uint64_t* full = reinterpret_cast<uint64_t*>(psm + lay.total - 64);
+  // half-warp `pair` -> (row lr, head hh); ghosts (pair >= NR*G) mirror pair 0 without storing
+  const bool ghost = pair >= NR * G;
+  const int pc = ghost ? 0 : pair;
+  const int lr = pc / G, hh = pc % G;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](long grp, int st) {  // thread 0 only
+    const long w0 = grp * NR;
+    const int nv = (int)min((long)NR, nrows - w0);
+    uint8_t* base = psm + st * lay.stage_bytes;
+    const uint32_t qb = (uint32_t)nv * G * D * 2, kb = (uint32_t)nv * D * 2, fb = (uint32_t)nv * D * 4;
+    const uint32_t bytes = 3 * qb + j * 2 * kb + (lay.has_lo ? qb : 0) + (lay.acc ? j * 2 * fb : 0);
+    mbar_expect_tx(&full[st], bytes);
+    const size_t qo = (size_t)w0 * G * D, ko = (size_t)w0 * D;
+    bulk_load_1d_(base + lay.off_q, reinterpret_cast<const __nv_bfloat16*>(p.q) + qo, qb, &full[st]);
+    bulk_load_1d_(base + lay.off_do, reinterpret_cast<const __nv_bfloat16*>(p.dout) + qo, qb, &full[st]);
+    bulk_load_1d_(base + lay.off_o, reinterpret_cast<const __nv_bfloat16*>(p.o) + qo, qb, &full[st]);
+    if (lay.has_lo)
+      bulk_load_1d_(base + lay.off_olo, reinterpret_cast<const __nv_bfloat16*>(p.o_lo) + qo, qb, &full[st]);
+    for (int i = 0; i < j; ++i) {
+      bulk_load_1d_(base + lay.off_k + i * (NR * D * 2), reinterpret_cast<const __nv_bfloat16*>(p.ks[i]) + ko, kb,
+                    &full[st]);
+      bulk_load_1d_(base + lay.off_v + i * (NR * D * 2), reinterpret_cast<const __nv_bfloat16*>(p.vs[i]) + ko, kb,
+                    &full[st]);
+      if (lay.acc) {
+        bulk_load_1d_(base + lay.off_dk + i * (NR * D * 4), p.dks[i] + ko, fb, &full[st]);
+        bulk_load_1d_(base + lay.off_dv + i * (NR * D * 4), p.dvs[i] + ko, fb, &full[st]);
       }
-      if (!act) continue;
-      // pass B: dK_i, dV_i rows of this chunk (exclusive to this CTA)
-      for (int ii = 0; ii < nj; ++ii) {
-        const int i = i0 + ii;
+    }
+  };
+  long grp = blockIdx.x;
+  if (tid == 0 && grp < ngroups) issue(grp, 0);
+  for (int n = 0; grp < ngroups; ++n, grp += gridDim.x) {
+    const int st = n & 1;
+    const long nxt = grp + gridDim.x;
+    if (tid == 0 && nxt < ngroups) {
+      bulk_wait_read0();  // bulk stores of group n-1 (same stage as n+1) have read their smem
+      issue(nxt, st ^ 1);
+    }
+    uint8_t* base = psm + st * lay.stage_bytes;
+    const long w = grp * NR + lr;
+    const bool valid = !ghost && w < nrows;
+    const long wc = w < nrows ? w : grp * NR;
+    const int g = (int)(wc % p.Hkv);
+    const int r = (int)((wc / p.Hkv) % p.L);
+    const int b = (int)(wc / ((long)p.Hkv * p.L));
+    const int h = g * G + hh;
+    const bool act = valid && r < p.seq_lens[b];  // diagonal keys exist only for rows r < T_b
+    if (!lay.acc && valid && hh == 0) {  // dK_0 / dV_0 rows in HBM: the main kernel adds into them
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        p.dk[(size_t)w * D + split_col<D>(hl, e)] = 0.f;
+        p.dv[(size_t)w * D + split_col<D>(hl, e)] = 0.f;
+      }
+    }
+    mbar_wait(&full[st], (n >> 1) & 1);
+    const uint32_t ro = (uint32_t)(lr * G + hh) * D * 2;
+    float o[E], dd[E], qq[E], dq[E];
+    lds_split<D>(base + lay.off_o + ro, hl, o);
+    lds_split<D>(base + lay.off_do + ro, hl, dd);
+    if (lay.has_lo) {
+      float lo[E];
+      lds_split<D>(base + lay.off_olo + ro, hl, lo);
+#pragma unroll
+      for (int e = 0; e < E; ++e) o[e] += lo[e];
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc = fmaf(o[e], dd[e], acc);
+    const float del = half_allsum(acc);  // Delta_r = dO_r . O_r
+    const size_t li = ((size_t)b * p.Hq + h) * p.L + r;
+    const float l2 = p.lse_in[li] * kLog2e;
+    if (valid && hl == 0) {  // stored negated: the main kernel's FFMA2 / FADD2 consume -lse2 and -Delta
+      p.delta[li] = -del;
+      p.lse2[li] = -l2;
+    }
+    lds_split<D>(base + lay.off_q + ro, hl, qq);
+#pragma unroll
+    for (int e = 0; e < E; ++e) dq[e] = 0.f;
+    // ---- phase A: per (row, head) the diagonal scalars (Alg. 2 M_suffix) and dq ----
+    float* scal = reinterpret_cast<float*>(psm + lay.off_sc);  // [NR][j][G][2]
+    for (int i = 0; i < j; ++i) {
+      float kk[E], vv[E];
+      lds_split<D>(base + lay.off_k + (i * NR + lr) * D * 2, hl, kk);
+      lds_split<D>(base + lay.off_v + (i * NR + lr) * D * 2, hl, vv);
+      float sdot = 0.f, dp = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        sdot = fmaf(qq[e], kk[e], sdot);
+        dp = fmaf(dd[e], vv[e], dp);
+      }
+#pragma unroll
+      for (int o2 = 8; o2 > 0; o2 >>= 1) {
+        sdot += __shfl_xor_sync(0xffffffffu, sdot, o2);
+        dp += __shfl_xor_sync(0xffffffffu, dp, o2);
+      }
+      const float pr = act ? ex2(sdot * p.scale_log2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
+      const float cds = p.scale * pr * (dp - del);                 // c ds_i, ds_i = p_i (dp_i - Delta)
+#pragma unroll
+      for (int e = 0; e < E; ++e) dq[e] = fmaf(cds, kk[e], dq[e]);
+      if (!ghost && hl == 0) {
+        scal[((lr * j + i) * G + hh) * 2 + 0] = pr;
+        scal[((lr * j + i) * G + hh) * 2 + 1] = cds;
+      }
+    }
+    if (valid) {
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const int d0 = part * (D / 2) + hl * (E / 2);
+        float* q4 = p.dq_acc + dqacc_index(p, b, h, r, d0);
+        if constexpr (E / 2 == 4)
+          *reinterpret_cast<float4*>(q4) = make_float4(dq[part * 4], dq[part * 4 + 1], dq[part * 4 + 2], dq[part * 4 + 3]);
+        else
+          *reinterpret_cast<float2*>(q4) = make_float2(dq[part * 2], dq[part * 2 + 1]);
+      }
+    }
+    __syncthreads();  // all (p_i, c ds_i) of the group visible
+    // ---- phase B: per (row, step, D-slice): dK_i = sum_h c ds_h q_h, dV_i = sum_h p_h dO_h ----
+    // (exclusive ownership of each stage row: no atomics; overwrite or accumulate)
+    {
+      const int nitems = NR * j;
+      for (int it = pair; it < nitems; it += blockDim.x / 16) {
+        const int brow = it % NR, i = it / NR;
+        const long wb = grp * NR + brow;
+        if (wb >= nrows) continue;
         float dk[E], dv[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) dk[e] = dv[e] = 0.f;
-        for (int hh = 0; hh < G; ++hh) {
-          const size_t q_off = (((size_t)b * p.L + r) * p.Hq + g * G + hh) * D + hl * E;
-          float qq[E], dd[E];
-          ld_row<D>(p.q, q_off, qq);
-          ld_row<D>(p.dout, q_off, dd);
-          const float pv = sc[2 * (hh * JC + ii)], cds = sc[2 * (hh * JC + ii) + 1];
+        for (int h2 = 0; h2 < G; ++h2) {
+          const float pr = scal[((brow * j + i) * G + h2) * 2 + 0];
+          const float cds = scal[((brow * j + i) * G + h2) * 2 + 1];
+          float q2[E], d2[E];
+          const uint32_t r2 = (uint32_t)(brow * G + h2) * D * 2;
+          lds_split<D>(base + lay.off_q + r2, hl, q2);
+          lds_split<D>(base + lay.off_do + r2, hl, d2);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            dk[e] = fmaf(cds, qq[e], dk[e]);
-            dv[e] = fmaf(pv, dd[e], dv[e]);
+            dk[e] = fmaf(cds, q2[e], dk[e]);
+            dv[e] = fmaf(pr, d2[e], dv[e]);
           }
         }
-        float4* dk4 = reinterpret_cast<float4*>(p.dks[i] + kv_off);
-        float4* dv4 = reinterpret_cast<float4*>(p.dvs[i] + kv_off);
+        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + brow * D;
+        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + brow * D;
 #pragma unroll
-        for (int e = 0; e < E / 4; ++e) {
-          float4 a = make_float4(dk[4 * e], dk[4 * e + 1], dk[4 * e + 2], dk[4 * e + 3]);
-          float4 c = make_float4(dv[4 * e], dv[4 * e + 1], dv[4 * e + 2], dv[4 * e + 3]);
-          if (p.accumulate) {
-            const float4 a0 = dk4[e], c0 = dv4[e];
-            a.x += a0.x; a.y += a0.y; a.z += a0.z; a.w += a0.w;
-            c.x += c0.x; c.y += c0.y; c.z += c0.z; c.w += c0.w;
+        for (int part = 0; part < 2; ++part) {
+          const int d0 = part * (D / 2) + hl * (E / 2);
+#pragma unroll
+          for (int e = 0; e < E / 2; ++e) {
+            const int k2 = part * (E / 2) + e;
+            dkr[d0 + e] = lay.acc ? dkr[d0 + e] + dk[k2] : dk[k2];
+            dvr[d0 + e] = lay.acc ? dvr[d0 + e] + dv[k2] : dv[k2];
           }
-          dk4[e] = a;
-          dv4[e] = c;
         }
-      }
-      // pass C: dq_h[r] += c sum_i ds K_i[r]  (atomic: the main kernel reduces into the same rows)
-      for (int hh = 0; hh < G; ++hh) {
-        float dq[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) dq[e] = 0.f;
-        for (int ii = 0; ii < nj; ++ii) {
-          float kk[E];
-          ld_row<D>(p.ks[i0 + ii], kv_off, kk);
-          const float cds = sc[2 * (hh * JC + ii) + 1];
-#pragma unroll
-          for (int e = 0; e < E; ++e) dq[e] = fmaf(cds, kk[e], dq[e]);
-        }
-        float* dst = p.dq_acc + dqacc_index(p, b, g * G + hh, r, hl * E);
-#pragma unroll
-        for (int e = 0; e < E / 4; ++e) red_add_v4(dst + 4 * e, dq[4 * e], dq[4 * e + 1], dq[4 * e + 2], dq[4 * e + 3]);
       }
     }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      const long w0 = grp * NR;
+      const int nv = (int)min((long)NR, nrows - w0);
+      for (int i = 0; i < j; ++i) {
+        bulk_store_1d(p.dks[i] + (size_t)w0 * D, base + lay.off_dk + i * (NR * D * 4), (uint32_t)nv * D * 4);
+        bulk_store_1d(p.dvs[i] + (size_t)w0 * D, base + lay.off_dv + i * (NR * D * 4), (uint32_t)nv * D * 4);
+      }
+      bulk_commit();
+    }
   }
+  if (tid == 0) bulk_wait0();
 }
 
 // ------------------------------------------------------------------ kernel 2
@@ -288,9 +369,8 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
 //   warps 0-3   dQ drain            (thread = query row of TMEM lane quadrant w)
 //   warps 4-7   compute sub-item a  (thread = key row, 64 query columns)
 //   warps 8-11  compute sub-item b
-//   warp  12    TMEM owner + MMA issuer, warp 13 TMA producer,
-//   warps 14-15 TTT diagonal-key gradients of the CTA's key rows (HBM-bound, CUDA cores)
-// Per SMSP: {dQ 152, compute 136, compute 136, MMA / producer / diagonal 88} <= 512 registers.
+//   warp  12    TMEM owner + MMA issuer, warp 13 TMA producer, warps 14-15 idle
+// Per SMSP: {dQ 152, compute 136, compute 136, role 88 / idle 24} <= 512 registers.
 // TMEM: S^T[a] [0,64) S^T[b] [64,128) dP^T[a] [128,192) dP^T[b] [192,256) dV [256,+D) dK [384,+D);
 // P^T / dS^T (bf16, 2 per column) over the first 32 columns of their own S / dP buffer.
 // Shared memory (D = 128): K, V 64 KB | Q 2 x 32 KB | dO 3 x 16 KB ring of 64-row halves |
@@ -714,11 +794,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     if (lane == 0) bulk_wait0();
   } else {
-    // warps 14-15: TTT diagonal keys of this CTA's 128 key rows (overlaps the tensor pipeline);
-    // only the head-subset-0 CTA of a key tile (it covers all G query heads)
-    reg_dealloc<88>();
-    if (hs == 0 && p.step > 0)
-      diag_bwd_rows<D>(p, b, g, kt * kTile, T, (warp - 14) * 2 + (lane >> 4), 4);
+    reg_dealloc<24>();  // warps 14-15: idle
   }
   tc_fence_before();
   __syncthreads();
@@ -764,13 +840,27 @@ template <int D>
 cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t st) {
   Params p = p_in;
   p.head_split = pick_head_split(p);
-  // 1. pre-pass
+  // 1. pre-pass (TMA-staged, persistent)
   {
-    const long pairs = (long)p.B * p.L * p.Hq;
+    PreLayout lay;
+    int nr = std::max(1, 32 / p.G);  // 32 half-warps (512 threads) of (row, head) pairs
+    for (; nr > 1; nr >>= 1) {
+      lay.init(nr, p.G, D, p.step, p.accumulate, p.o_lo != nullptr);
+      if (lay.total <= 220 * 1024) break;
+    }
+    lay.init(nr, p.G, D, p.step, p.accumulate, p.o_lo != nullptr);
+    if (lay.total > 227 * 1024) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)lay.total);
+    if (e != cudaSuccess) return e;
+    const long rows = (long)p.B * p.L * p.Hkv;
+    const long groups = (rows + nr - 1) / nr;
+    const int blocks = (int)std::min<long>(groups, 148);
     prof_mark(kKindBwdPre, true, st);
-    ttt_bwd_pre_kernel<D><<<(unsigned)((pairs + 15) / 16), 256, 0, st>>>(p);
+    const int threads = std::min(512, std::max(32, ((nr * p.G * 16 + 31) / 32) * 32));
+    ttt_bwd_pre_kernel<D><<<blocks, threads, lay.total, st>>>(p, lay);
     prof_mark(kKindBwdPre, false, st);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   // 2. main tensor-core kernel
