@@ -106,6 +106,11 @@ __device__ __forceinline__ void bulk_load_1d_(void* dst, const void* src, uint32
       : "memory");
 }
 // split-lane bf16 row chunk: E/2 elements at hl*E/2 and at D/2 + hl*E/2 -> fp32
+// (bf16 -> fp32 is a 16-bit shift: one SHL / LOP per element)
+__device__ __forceinline__ void bf2_to_f(uint32_t w, float& lo, float& hi) {
+  lo = __uint_as_float(w << 16);
+  hi = __uint_as_float(w & 0xFFFF0000u);
+}
 template <int D>
 __device__ __forceinline__ void lds_split(const uint8_t* row, int hl, float (&x)[D / 16]) {
   constexpr int H = D / 32;  // elements per half (4 for D=128, 2 for D=64)
@@ -114,13 +119,11 @@ __device__ __forceinline__ void lds_split(const uint8_t* row, int hl, float (&x)
     const uint8_t* src = row + (part * (D / 2) + hl * H) * 2;
     if constexpr (H == 4) {
       const uint2 u = *reinterpret_cast<const uint2*>(src);
-      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-      const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-      x[part * 4 + 0] = a.x; x[part * 4 + 1] = a.y; x[part * 4 + 2] = c.x; x[part * 4 + 3] = c.y;
+      bf2_to_f(u.x, x[part * 4 + 0], x[part * 4 + 1]);
+      bf2_to_f(u.y, x[part * 4 + 2], x[part * 4 + 3]);
     } else {
       const uint32_t u = *reinterpret_cast<const uint32_t*>(src);
-      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
-      x[part * 2 + 0] = a.x; x[part * 2 + 1] = a.y;
+      bf2_to_f(u, x[part * 2 + 0], x[part * 2 + 1]);
     }
   }
 }
@@ -130,12 +133,13 @@ __device__ __forceinline__ int split_col(int hl, int e) {  // D index of lane el
   return (e < H) ? hl * H + e : D / 2 + hl * H + (e - H);
 }
 
-template <int D>
+template <int D, int GT>  // GT: GQA group size (compile time; 0 = runtime p.G)
 __global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant__ Params p, PreLayout lay) {
   constexpr int E = D / 16;
   extern __shared__ __align__(128) uint8_t psm[];
   const int tid = threadIdx.x, hl = tid & 15, pair = tid >> 4;
-  const int NR = lay.NR, G = p.G, j = p.step;
+  const int G = GT > 0 ? GT : p.G;
+  const int NR = lay.NR, j = p.step;
   const long nrows = (long)p.B * p.L * p.Hkv;
   const long ngroups = (nrows + NR - 1) / NR;
   uint64_t* full = reinterpret_cast<uint64_t*>(psm + lay.total - 64);
@@ -224,28 +228,35 @@ __global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant_
     for (int e = 0; e < E; ++e) dq[e] = 0.f;
     // ---- phase A: per (row, head) the diagonal scalars (Alg. 2 M_suffix) and dq ----
     float* scal = reinterpret_cast<float*>(psm + lay.off_sc);  // [NR][j][G][2]
-    for (int i = 0; i < j; ++i) {
-      float kk[E], vv[E];
-      lds_split<D>(base + lay.off_k + (i * NR + lr) * D * 2, hl, kk);
-      lds_split<D>(base + lay.off_v + (i * NR + lr) * D * 2, hl, vv);
-      float sdot = 0.f, dp = 0.f;
+    {
+      const uint8_t* kp = base + lay.off_k + lr * D * 2;
+      const uint8_t* vp = base + lay.off_v + lr * D * 2;
+      float* sp = scal + ((lr * j) * G + hh) * 2;
+      const bool wr = !ghost && hl == 0;
+      const float sl2 = p.scale_log2, cs = p.scale;
+      for (int i = 0; i < j; ++i, kp += NR * D * 2, vp += NR * D * 2, sp += 2 * G) {
+        float kk[E], vv[E];
+        lds_split<D>(kp, hl, kk);
+        lds_split<D>(vp, hl, vv);
+        float sdot = 0.f, dp = 0.f;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        sdot = fmaf(qq[e], kk[e], sdot);
-        dp = fmaf(dd[e], vv[e], dp);
-      }
+        for (int e = 0; e < E; ++e) {
+          sdot = fmaf(qq[e], kk[e], sdot);
+          dp = fmaf(dd[e], vv[e], dp);
+        }
 #pragma unroll
-      for (int o2 = 8; o2 > 0; o2 >>= 1) {
-        sdot += __shfl_xor_sync(0xffffffffu, sdot, o2);
-        dp += __shfl_xor_sync(0xffffffffu, dp, o2);
-      }
-      const float pr = act ? ex2(sdot * p.scale_log2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
-      const float cds = p.scale * pr * (dp - del);                 // c ds_i, ds_i = p_i (dp_i - Delta)
+        for (int o2 = 8; o2 > 0; o2 >>= 1) {
+          sdot += __shfl_xor_sync(0xffffffffu, sdot, o2);
+          dp += __shfl_xor_sync(0xffffffffu, dp, o2);
+        }
+        const float pr = act ? ex2(sdot * sl2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
+        const float cds = cs * pr * (dp - del);             // c ds_i, ds_i = p_i (dp_i - Delta)
 #pragma unroll
-      for (int e = 0; e < E; ++e) dq[e] = fmaf(cds, kk[e], dq[e]);
-      if (!ghost && hl == 0) {
-        scal[((lr * j + i) * G + hh) * 2 + 0] = pr;
-        scal[((lr * j + i) * G + hh) * 2 + 1] = cds;
+        for (int e = 0; e < E; ++e) dq[e] = fmaf(cds, kk[e], dq[e]);
+        if (wr) {
+          sp[0] = pr;
+          sp[1] = cds;
+        }
       }
     }
     if (valid) {
@@ -271,13 +282,15 @@ __global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant_
         float dk[E], dv[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) dk[e] = dv[e] = 0.f;
-        for (int h2 = 0; h2 < G; ++h2) {
-          const float pr = scal[((brow * j + i) * G + h2) * 2 + 0];
-          const float cds = scal[((brow * j + i) * G + h2) * 2 + 1];
+        const float* sp = scal + ((brow * j + i) * G) * 2;
+        const uint8_t* qp = base + lay.off_q + brow * G * D * 2;
+        const uint8_t* op = base + lay.off_do + brow * G * D * 2;
+#pragma unroll(GT > 0 ? GT : 1)
+        for (int h2 = 0; h2 < G; ++h2, qp += D * 2, op += D * 2) {
+          const float pr = sp[2 * h2], cds = sp[2 * h2 + 1];
           float q2[E], d2[E];
-          const uint32_t r2 = (uint32_t)(brow * G + h2) * D * 2;
-          lds_split<D>(base + lay.off_q + r2, hl, q2);
-          lds_split<D>(base + lay.off_do + r2, hl, d2);
+          lds_split<D>(qp, hl, q2);
+          lds_split<D>(op, hl, d2);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             dk[e] = fmaf(cds, q2[e], dk[e]);
@@ -289,11 +302,23 @@ __global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant_
 #pragma unroll
         for (int part = 0; part < 2; ++part) {
           const int d0 = part * (D / 2) + hl * (E / 2);
+          if constexpr (E / 2 == 4) {
+            float4 a = make_float4(dk[part * 4], dk[part * 4 + 1], dk[part * 4 + 2], dk[part * 4 + 3]);
+            float4 c = make_float4(dv[part * 4], dv[part * 4 + 1], dv[part * 4 + 2], dv[part * 4 + 3]);
+            if (lay.acc) {
+              const float4 a0 = *reinterpret_cast<const float4*>(dkr + d0), c0 = *reinterpret_cast<const float4*>(dvr + d0);
+              a.x += a0.x; a.y += a0.y; a.z += a0.z; a.w += a0.w;
+              c.x += c0.x; c.y += c0.y; c.z += c0.z; c.w += c0.w;
+            }
+            *reinterpret_cast<float4*>(dkr + d0) = a;
+            *reinterpret_cast<float4*>(dvr + d0) = c;
+          } else {
 #pragma unroll
-          for (int e = 0; e < E / 2; ++e) {
-            const int k2 = part * (E / 2) + e;
-            dkr[d0 + e] = lay.acc ? dkr[d0 + e] + dk[k2] : dk[k2];
-            dvr[d0 + e] = lay.acc ? dvr[d0 + e] + dv[k2] : dv[k2];
+            for (int e = 0; e < E / 2; ++e) {
+              const int k2 = part * (E / 2) + e;
+              dkr[d0 + e] = lay.acc ? dkr[d0 + e] + dk[k2] : dk[k2];
+              dvr[d0 + e] = lay.acc ? dvr[d0 + e] + dv[k2] : dv[k2];
+            }
           }
         }
       }
@@ -850,15 +875,27 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t s
     }
     lay.init(nr, p.G, D, p.step, p.accumulate, p.o_lo != nullptr);
     if (lay.total > 227 * 1024) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)lay.total);
-    if (e != cudaSuccess) return e;
     const long rows = (long)p.B * p.L * p.Hkv;
     const long groups = (rows + nr - 1) / nr;
     const int blocks = (int)std::min<long>(groups, 148);
-    prof_mark(kKindBwdPre, true, st);
     const int threads = std::min(512, std::max(32, ((nr * p.G * 16 + 31) / 32) * 32));
-    ttt_bwd_pre_kernel<D><<<blocks, threads, lay.total, st>>>(p, lay);
+    auto run = [&](auto kern) -> cudaError_t {
+      cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
+      if (e2 != cudaSuccess) return e2;
+      prof_mark(kKindBwdPre, true, st);
+      kern<<<blocks, threads, lay.total, st>>>(p, lay);
+      return cudaSuccess;
+    };
+    cudaError_t e;
+    switch (p.G) {  // compile-time group size for the common GQA ratios
+      case 1: e = run(ttt_bwd_pre_kernel<D, 1>); break;
+      case 2: e = run(ttt_bwd_pre_kernel<D, 2>); break;
+      case 4: e = run(ttt_bwd_pre_kernel<D, 4>); break;
+      case 8: e = run(ttt_bwd_pre_kernel<D, 8>); break;
+      case 16: e = run(ttt_bwd_pre_kernel<D, 16>); break;
+      default: e = run(ttt_bwd_pre_kernel<D, 0>); break;
+    }
+    if (e != cudaSuccess) return e;
     prof_mark(kKindBwdPre, false, st);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -443,15 +443,16 @@ __global__ void __launch_bounds__(512) ttt_fwd_diag_kernel(const __grid_constant
 #pragma unroll
     for (int part = 0; part < 2; ++part) {
       const uint8_t* src = row + (part * (D / 2) + hl * H) * 2;
-      if constexpr (H == 4) {
+      if constexpr (H == 4) {  // bf16 -> fp32: one shift / mask per element
         const uint2 u = *reinterpret_cast<const uint2*>(src);
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-        const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-        x[part * 4 + 0] = a.x; x[part * 4 + 1] = a.y; x[part * 4 + 2] = c.x; x[part * 4 + 3] = c.y;
+        x[part * 4 + 0] = __uint_as_float(u.x << 16);
+        x[part * 4 + 1] = __uint_as_float(u.x & 0xFFFF0000u);
+        x[part * 4 + 2] = __uint_as_float(u.y << 16);
+        x[part * 4 + 3] = __uint_as_float(u.y & 0xFFFF0000u);
       } else {
         const uint32_t u = *reinterpret_cast<const uint32_t*>(src);
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
-        x[part * 2 + 0] = a.x; x[part * 2 + 1] = a.y;
+        x[part * 2 + 0] = __uint_as_float(u << 16);
+        x[part * 2 + 1] = __uint_as_float(u & 0xFFFF0000u);
       }
     }
   };
