@@ -48,7 +48,7 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only when t
 struct FwdBars {
   uint64_t q;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full[2], p_full[2], o_full[2];
+  uint64_t s_full[2], p_lo[2], p_hi[2], o_full[2];  // P published in two 64-column halves
   uint32_t tmem_base;
 };
 
@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bars.v_full[i], 1);
       mbar_init(&bars.v_empty[i], 1);
       mbar_init(&bars.s_full[i], 1);
-      mbar_init(&bars.p_full[i], 128);
+      mbar_init(&bars.p_lo[i], 128);
+      mbar_init(&bars.p_hi[i], 128);
       mbar_init(&bars.o_full[i], 1);
     }
     fence_mbar_init();
@@ -142,11 +143,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           umma_ss_e(tbase + slot * 128, sdesc_add(dQ0, slot * TB + off), sdesc_add(dK0, kst * TB + off), idS, ks > 0);
         }
       };
-      auto issue_PV = [&](int slot, int vst, bool acc) {
+      // O += P V in two halves of the key dimension: keys [0,64) as soon as the softmax warps have
+      // published P's first half (p_lo), keys [64,128) after p_hi
+      auto issue_PV = [&](int slot, int vst, bool acc, int n) {
+        mbar_wait(&bars.p_lo[slot], n & 1);
+        tc_fence_after();
 #pragma unroll
-        for (int ks = 0; ks < kTile / 16; ++ks)
+        for (int ks = 0; ks < 4; ++ks)
           umma_ts_e(tbase + 256 + slot * 128, tbase + slot * 128 + ks * 8, sdesc_add(dV0, vst * TB + ks * 2048), idO,
                     (acc || ks > 0) ? 1u : 0u);
+        mbar_wait(&bars.p_hi[slot], n & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 4; ks < 8; ++ks)
+          umma_ts_e(tbase + 256 + slot * 128, tbase + slot * 128 + ks * 8, sdesc_add(dV0, vst * TB + ks * 2048), idO, 1u);
       };
       mbar_wait(&bars.q, 0);
       mbar_wait(&bars.k_full[0], 0);
@@ -165,10 +175,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int kst = (n + 1) & 1, kph = ((n + 1) >> 1) & 1;
         mbar_wait(&bars.v_full[vst], vph);
         TTT_TRACE_EV(0, 1, n);
-        mbar_wait(&bars.p_full[0], n & 1);
+        issue_PV(0, vst, n > 0, n);
         TTT_TRACE_EV(0, 2, n);
-        tc_fence_after();
-        issue_PV(0, vst, n > 0);
         if (more) {
           mbar_wait(&bars.k_full[kst], kph);
           tc_fence_after();
@@ -178,10 +186,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           umma_commit_e(&bars.o_full[0]);
         }
         if (has1) {
-          mbar_wait(&bars.p_full[1], n & 1);
+          issue_PV(1, vst, n > 0, n);
           TTT_TRACE_EV(0, 3, n);
-          tc_fence_after();
-          issue_PV(1, vst, n > 0);
           umma_commit_e(&bars.v_empty[vst]);
           if (more) {
             issue_S(1, kst);
@@ -261,33 +267,43 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           l_run *= alpha;
           m_run = m_new;
         }
-        // P = 2^(s c log2e - m): one FFMA2 per pair, 4 independent pair-sum chains (FADD2)
+        // P = 2^(s c log2e - m): one FFMA2 per pair, 4 independent pair-sum chains (FADD2),
+        // written to TMEM and published in two 64-column halves (the PV MMA starts on the first)
         const uint64_t sl2x2 = f2pack(sl2, sl2), negm = f2pack(-m_run, -m_run);
         uint64_t rs2[4] = {0, 0, 0, 0};
-        uint32_t pk[64];
-        if (partial) {  // masked columns are -inf: hardware ex2 gives exact zeros
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            float x0, x1;
-            f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
-            const float e0 = ex2(x0), e1 = ex2(x1);
-            rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
-            pk[c] = pack_bf16(e0, e1);
-          }
-        } else {  // full tile: every 4th pair on the FMA pipe (MUFU ex2 is the co-bottleneck)
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t pk[32];
+          if (partial) {  // masked columns are -inf: hardware ex2 gives exact zeros
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            float x0, x1, e0, e1;
-            f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
-            if ((c & 3) == 3) {
-              ex2_emu2(x0, x1, e0, e1);
-            } else {
-              e0 = ex2(x0);
-              e1 = ex2(x1);
+            for (int cc = 0; cc < 32; ++cc) {
+              const int c = hf * 32 + cc;
+              float x0, x1;
+              f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
+              const float e0 = ex2(x0), e1 = ex2(x1);
+              rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
+              pk[cc] = pack_bf16(e0, e1);
             }
-            rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
-            pk[c] = pack_bf16(e0, e1);
+          } else {  // full tile: every 4th pair on the FMA pipe (MUFU ex2 is the co-bottleneck)
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc) {
+              const int c = hf * 32 + cc;
+              float x0, x1, e0, e1;
+              f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
+              if ((c & 3) == 3) {
+                ex2_emu2(x0, x1, e0, e1);
+              } else {
+                e0 = ex2(x0);
+                e1 = ex2(x1);
+              }
+              rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
+              pk[cc] = pack_bf16(e0, e1);
+            }
           }
+          tmem_st32(tS + 32 * hf, pk);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(hf == 0 ? &bars.p_lo[slot] : &bars.p_hi[slot]);
         }
         {
           float a0, a1, b0, b1, c0, c1, d0, d1;
@@ -297,10 +313,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           f2unpack(rs2[3], d0, d1);
           l_run += ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
         }
-        tmem_st64(tS, pk);
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&bars.p_full[slot]);
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 2, n);
         if (threadIdx.x == 128) TTT_TRACE_EV(2, 2, n);
       }
