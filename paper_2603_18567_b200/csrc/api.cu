@@ -251,7 +251,8 @@ int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
   if (d->dtype == TTT_FP32_CHECK) return cuda_status(launch_fwd_check(p, s));
   FwdMaps maps;
   if (!encode_bshd(&maps.q, q, p.B, p.L, p.Hq, p.D) || !encode_bshd(&maps.k, k_base, p.B, p.L, p.Hkv, p.D) ||
-      !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D))
+      !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D) || !encode_bshd(&maps.out, out, p.B, p.L, p.Hq, p.D) ||
+      (p.out_lo && !encode_bshd(&maps.out_lo, p.out_lo, p.B, p.L, p.Hq, p.D)))
     return TTT_ERR_CUDA;
   return cuda_status(launch_fwd_sm100(p, maps, s));
 }

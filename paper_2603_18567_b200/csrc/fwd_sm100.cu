@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // merge is the same online-softmax update as one more "tile".
       const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D;
       const size_t lse_idx = ((size_t)b * p.Hq + h) * p.L + r;
-      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
+      const __nv_bfloat16* orow = reinterpret_cast<const __nv_bfloat16*>(p.out) + q_off;
       const bool has_diag = (r < T) && (p.step > 0);
       uint4 od[D / 8];
       float A_d = -INFINITY;
@@ -335,6 +335,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_wait(&bars.o_full[slot], 0);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 4, 0);
       tc_fence_after();
+      // Staging tiles for the TMA stores (SW128 boxes of 64 columns, same layout the loads use).
+      // o_full[slot] follows every S MMA of the CTA in issue order, so the K stages (slot 0) and
+      // the Q tiles (slot 1) are no longer read by the tensor core.
+      uint8_t* st_hi = slot == 0 ? sK : sQ;
+      uint8_t* st_lo = st_hi + TB;
+      const uint32_t sw = (uint32_t)(row & 7);
       const float m_f = fmaxf(m_run, A_d);
       const float alpha = ex2(m_run - m_f);
       const float beta = has_diag ? ex2(A_d - m_f) : 0.f;
@@ -364,7 +370,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           w.y = pack_bf16(v[2], v[3]);
           w.z = pack_bf16(v[4], v[5]);
           w.w = pack_bf16(v[6], v[7]);
-          *reinterpret_cast<uint4*>(orow + c0 + q4 * 8) = w;
+          const int col = c0 + q4 * 8;
+          const uint32_t soff = (uint32_t)(col >> 6) * 16384u + (uint32_t)row * 128u + ((((uint32_t)(col & 63) >> 3) ^ sw) << 4);
+          *reinterpret_cast<uint4*>(st_hi + soff) = w;
           if (p.out_lo) {  // residual O - bf16(O), so the backward's Delta sees ~16-bit O
             const uint32_t hi[4] = {w.x, w.y, w.z, w.w};
             uint32_t lo[4];
@@ -373,12 +381,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hi[e]));
               lo[e] = pack_bf16(v[2 * e] - hf.x, v[2 * e + 1] - hf.y);
             }
-            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out_lo) + q_off + c0 + q4 * 8) =
-                make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            *reinterpret_cast<uint4*>(st_lo + soff) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
           }
         }
       }
       p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
+      fence_async_smem();
+      named_bar_sync(1 + slot, 128);
+      if (row == 0) {
+#pragma unroll
+        for (int bx = 0; bx < D / 64; ++bx) {
+          tma_store_4d(&maps.out, st_hi + bx * 16384, bx * 64, h, qt * kTile, b);
+          if (p.out_lo) tma_store_4d(&maps.out_lo, st_lo + bx * 16384, bx * 64, h, qt * kTile, b);
+        }
+        bulk_commit();
+        bulk_wait_read0();  // smem must stay valid until the bulk engine has read it
+      }
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 5, 0);
     }
   }

@@ -47,7 +47,7 @@ struct Params {
 
 // Tensor maps for the tcgen05 paths (4-D: D, H, L, B; box 64 x 1 x 128 x 1, SW128)
 struct FwdMaps {
-  CUtensorMap q, k, v;
+  CUtensorMap q, k, v, out, out_lo;
 };
 struct BwdMaps {
   CUtensorMap q, k, v, dout;
