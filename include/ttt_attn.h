@@ -70,7 +70,8 @@ typedef enum { TTT_BF16 = 0, TTT_FP32_CHECK = 1 } ttt_dtype;
 typedef enum {
   TTT_OK = 0,
   TTT_ERR_INVALID_ARG = 1,  /* null pointer, non-positive size, Hq % Hkv != 0, bad flags */
-  TTT_ERR_UNSUPPORTED = 2,  /* head_dim not in {64,128}; Hq/Hkv > 32; BF16 mode needs seq_len % 128 == 0 */
+  TTT_ERR_UNSUPPORTED = 2,  /* head_dim not in {64,128}; Hq/Hkv > 32; BF16 mode needs seq_len % 128 == 0;
+                               batch * seq_len * num_q_heads >= 2^31 */
   TTT_ERR_STEP_RANGE = 3,   /* step < 0 or step >= TTT_MAX_STEPS */
   TTT_ERR_ALIGNMENT = 4,    /* a device pointer not 16-byte aligned */
   TTT_ERR_DEGENERATE = 5,   /* some seq_lens[b] < 1 (a row with no allowed key) or > seq_len */

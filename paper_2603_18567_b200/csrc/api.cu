@@ -14,7 +14,8 @@ namespace tttk {
 cudaError_t launch_zero_f32(float* x, size_t n, cudaStream_t st);
 cudaError_t launch_fwd_check(const Params& p, cudaStream_t st);
 cudaError_t launch_bwd_check(const Params& p, cudaStream_t st);
-cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, cudaStream_t st);
+cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, const DiagMaps& dmaps, cudaStream_t st);
+int fwd_diag_rows_per_group(const Params& p);
 cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, cudaStream_t st);
 }  // namespace tttk
 
@@ -54,6 +55,20 @@ bool encode_bshd(CUtensorMap* m, const void* ptr, int B, int L, int H, int D, in
 }
 
 // tiled fp32 dq accumulator as a 2-D tensor {32, rows}: box {32, 32} (4 KB), 128B swizzle.
+// [rows][D] bf16 view of a BSHD tensor (rows = B*L*H), box 64 columns x box_rows rows, SW128
+bool encode_rows2d(CUtensorMap* m, const void* ptr, long long rows, int D, int box_rows) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool encode_dqacc(CUtensorMap* m, void* ptr, size_t rows) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return false;
@@ -79,6 +94,8 @@ int validate_desc(const ttt_attn_desc* d, int step) {
   if (!(d->softmax_scale >= 0.f) || std::isinf(d->softmax_scale)) return TTT_ERR_INVALID_ARG;
   if (step < 0 || step >= TTT_MAX_STEPS) return TTT_ERR_STEP_RANGE;
   if (d->dtype == TTT_BF16 && (d->seq_len % kTile)) return TTT_ERR_UNSUPPORTED;
+  // row indices (b L + r) Hq + h are decoded in 32-bit arithmetic on the device
+  if ((long long)d->batch * d->seq_len * d->num_q_heads >= (1ll << 31)) return TTT_ERR_UNSUPPORTED;
   if (d->seq_lens) {
     for (int b = 0; b < d->batch; ++b)
       if (d->seq_lens[b] < 1 || d->seq_lens[b] > d->seq_len) return TTT_ERR_DEGENERATE;
@@ -254,7 +271,19 @@ int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
       !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D) || !encode_bshd(&maps.out, out, p.B, p.L, p.Hq, p.D) ||
       (p.out_lo && !encode_bshd(&maps.out_lo, p.out_lo, p.B, p.L, p.Hq, p.D)))
     return TTT_ERR_CUDA;
-  return cuda_status(launch_fwd_sm100(p, maps, s));
+  DiagMaps dmaps;
+  if (p.step > 0) {
+    const int nr = fwd_diag_rows_per_group(p);
+    const long long rows = (long long)p.B * p.L * p.Hq;
+    if (nr <= 0) return TTT_ERR_UNSUPPORTED;
+    if (!encode_rows2d(&dmaps.q, q, rows, p.D, nr * p.G) || !encode_rows2d(&dmaps.out, out, rows, p.D, nr * p.G))
+      return TTT_ERR_CUDA;
+    const long long kv_rows = (long long)p.B * p.L * p.Hkv;
+    for (int i = 0; i < p.step; ++i)
+      if (!encode_rows2d(&dmaps.k[i], p.ks[i], kv_rows, p.D, nr) || !encode_rows2d(&dmaps.v[i], p.vs[i], kv_rows, p.D, nr))
+        return TTT_ERR_CUDA;
+  }
+  return cuda_status(launch_fwd_sm100(p, maps, dmaps, s));
 }
 
 int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_base, const void* v_base,

@@ -190,9 +190,11 @@ __global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant_
     const long w = grp * NR + lr;
     const bool valid = !ghost && w < nrows;
     const long wc = w < nrows ? w : grp * NR;
-    const int g = (int)(wc % p.Hkv);
-    const int r = (int)((wc / p.Hkv) % p.L);
-    const int b = (int)(wc / ((long)p.Hkv * p.L));
+    // 32-bit decode of wc = (b L + r) Hkv + g (host guarantees B L Hq < 2^31)
+    const uint32_t bl = (uint32_t)wc / (uint32_t)p.Hkv;
+    const int g = (int)((uint32_t)wc - bl * (uint32_t)p.Hkv);
+    const int b = (int)(bl / (uint32_t)p.L);
+    const int r = (int)(bl - (uint32_t)b * (uint32_t)p.L);
     const int h = g * G + hh;
     const bool act = valid && r < p.seq_lens[b];  // diagonal keys exist only for rows r < T_b
     if (!lay.acc && valid && hh == 0) {  // dK_0 / dV_0 rows in HBM: the main kernel adds into them
@@ -353,9 +355,6 @@ __device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
-}
-__device__ __forceinline__ void bulk_wait_read1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
 template <uint32_t N>
 __device__ __forceinline__ void reg_alloc() {
@@ -829,16 +828,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // ------------------------------------------------------------------ kernel 3
 // dq[b][r][h][:] = bf16(dq_acc tiled). One thread per 8 consecutive d of one row.
 __global__ void __launch_bounds__(256) ttt_bwd_dq_convert_kernel(const __grid_constant__ Params p) {
-  const size_t n8 = (size_t)p.B * p.L * p.Hq * p.D / 8;
-  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  const int d8 = p.D / 8;
-  for (; i < n8; i += stride) {
-    const int d = (int)(i % d8) * 8;
-    const size_t row = i / d8;  // (b*L + r)*Hq + h
-    const int h = (int)(row % p.Hq);
-    const int r = (int)((row / p.Hq) % p.L);
-    const int b = (int)(row / ((size_t)p.Hq * p.L));
+  // thread -> (row, 8-column chunk); rows (b L + r) Hq + h in 32-bit (B L Hq < 2^31)
+  const uint32_t d8 = (uint32_t)p.D / 8, rows_per_block = blockDim.x / d8;
+  const uint32_t nrows = (uint32_t)p.B * p.L * p.Hq;
+  const int d = (int)(threadIdx.x % d8) * 8;
+  for (uint32_t row = blockIdx.x * rows_per_block + threadIdx.x / d8; row < nrows; row += gridDim.x * rows_per_block) {
+    const uint32_t bl = row / (uint32_t)p.Hq;
+    const int h = (int)(row - bl * (uint32_t)p.Hq);
+    const int b = (int)(bl / (uint32_t)p.L);
+    const int r = (int)(bl - (uint32_t)b * (uint32_t)p.L);
     const float4* src = reinterpret_cast<const float4*>(p.dq_acc + dqacc_index(p, b, h, r, d));
     const float4 a = src[0], c = src[1];
     uint4 o;
@@ -846,7 +844,7 @@ __global__ void __launch_bounds__(256) ttt_bwd_dq_convert_kernel(const __grid_co
     o.y = pack_bf16(a.z, a.w);
     o.z = pack_bf16(c.x, c.y);
     o.w = pack_bf16(c.z, c.w);
-    reinterpret_cast<uint4*>(p.dq)[i] = o;
+    reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.dq) + (size_t)row * p.D + d)[0] = o;
   }
 }
 

@@ -49,6 +49,7 @@ struct FwdBars {
   uint64_t q;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
   uint64_t s_full[2], p_lo[2], p_hi[2], o_full[2];  // P published in two 64-column halves
+  uint64_t s_done, od;  // all S MMAs complete (Q / K smem free); diagonal partial tile landed
   uint32_t tmem_base;
 };
 
@@ -92,6 +93,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bars.p_hi[i], 128);
       mbar_init(&bars.o_full[i], 1);
     }
+    mbar_init(&bars.s_done, 1);
+    mbar_init(&bars.od, 1);
     fence_mbar_init();
   }
   if (warp == 9) {
@@ -127,6 +130,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
           tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, n * kTile, b);
+      }
+      if (p.step > 0) {  // diagonal partial of the two heads into the Q tiles once no S MMA reads them
+        mbar_wait(&bars.s_done, 0);
+        mbar_expect_tx(&bars.od, (has1 ? 2 : 1) * TB);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx) {
+          tma_load_4d(sQ + bx * 16384, &maps.out, &bars.od, bx * 64, h0, qt * kTile, b);
+          if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.out, &bars.od, bx * 64, h0 + 1, qt * kTile, b);
+        }
       }
     }
   } else if (warp == 9) {
@@ -173,6 +185,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int vst = n & 1, vph = (n >> 1) & 1;
         const bool more = n + 1 < nkv;
         const int kst = (n + 1) & 1, kph = ((n + 1) >> 1) & 1;
+        if (!more) umma_commit_e(&bars.s_done);
         mbar_wait(&bars.v_full[vst], vph);
         TTT_TRACE_EV(0, 1, n);
         issue_PV(0, vst, n > 0, n);
@@ -320,26 +333,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // The j diagonal keys of row r (Alg. 1 "concat s_i") were reduced
       // by ttt_fwd_diag_kernel into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum); the
       // merge is the same online-softmax update as one more "tile".
-      const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D;
       const size_t lse_idx = ((size_t)b * p.Hq + h) * p.L + r;
-      const __nv_bfloat16* orow = reinterpret_cast<const __nv_bfloat16*>(p.out) + q_off;
       const bool has_diag = (r < T) && (p.step > 0);
-      uint4 od[D / 8];
-      float A_d = -INFINITY;
-      if (has_diag) {
-        A_d = p.lse[lse_idx];
-#pragma unroll
-        for (int c = 0; c < D / 8; ++c) od[c] = *reinterpret_cast<const uint4*>(orow + c * 8);
-      }
+      const float A_d = has_diag ? p.lse[lse_idx] : -INFINITY;
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, 0);
       mbar_wait(&bars.o_full[slot], 0);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 4, 0);
       tc_fence_after();
-      // Staging tiles for the TMA stores (SW128 boxes of 64 columns, same layout the loads use).
-      // o_full[slot] follows every S MMA of the CTA in issue order, so the K stages (slot 0) and
-      // the Q tiles (slot 1) are no longer read by the tensor core.
-      uint8_t* st_hi = slot == 0 ? sK : sQ;
-      uint8_t* st_lo = st_hi + TB;
+      if (p.step > 0) mbar_wait(&bars.od, 0);
+      // The diagonal partial O_d sits in this slot's Q tile (SW128 boxes); each thread reads its
+      // row there and overwrites it in place with the output, which the TMA store then drains.
+      // out_lo is staged in the K stage of the same index. Both are free: o_full[slot] and
+      // s_done follow every S MMA of the CTA.
+      uint8_t* st_hi = sQ + slot * TB;
+      uint8_t* st_lo = sK + slot * TB;
       const uint32_t sw = (uint32_t)(row & 7);
       const float m_f = fmaxf(m_run, A_d);
       const float alpha = ex2(m_run - m_f);
@@ -356,8 +363,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           float v[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(o[q4 * 8 + e]) * a_n;
+          const int col = c0 + q4 * 8;
+          const uint32_t soff = (uint32_t)(col >> 6) * 16384u + (uint32_t)row * 128u + ((((uint32_t)(col & 63) >> 3) ^ sw) << 4);
           if (has_diag) {
-            const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&od[c0 / 8 + q4]);
+            const uint4 odv = *reinterpret_cast<const uint4*>(st_hi + soff);
+            const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&odv);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 df = __bfloat1622float2(d2[e]);
@@ -370,8 +380,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           w.y = pack_bf16(v[2], v[3]);
           w.z = pack_bf16(v[4], v[5]);
           w.w = pack_bf16(v[6], v[7]);
-          const int col = c0 + q4 * 8;
-          const uint32_t soff = (uint32_t)(col >> 6) * 16384u + (uint32_t)row * 128u + ((((uint32_t)(col & 63) >> 3) ^ sw) << 4);
           *reinterpret_cast<uint4*>(st_hi + soff) = w;
           if (p.out_lo) {  // residual O - bf16(O), so the backward's Delta sees ~16-bit O
             const uint32_t hi[4] = {w.x, w.y, w.z, w.w};
@@ -406,143 +414,259 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 }
 
 // Diagonal pre-pass (TTT-specific): for every row r < T_b
-// and query head h, t_i = c log2(e) q_r . K_i[r] (i = 1..j) reduced with an online
-// softmax over i (Alg. 1 "concat s_i"):
+// and query head h, t_i = c log2(e) q_r . K_i[r] (i = 1..j) reduced by a softmax over i
+// (Alg. 1 "concat s_i"):
 //   A_d = log2 sum_i 2^{t_i},  O_d = sum_i 2^{t_i - A_d} V_i[r]
 // written into lse (log2 units) and out (bf16); the main kernel merges them.
-// HBM-streaming, TMA-staged: a persistent block walks groups of NR consecutive
-// (b, r, g) rows; q (NR*G*D), K_i and V_i (NR*D each) of a group are single
-// contiguous blocks moved by 1-D cp.async.bulk into a double-buffered stage.
+// Per kv row w = (b, r, g) this is two tiny products, S_w = Q_w K_w^T (G x j) and
+// O_w = P_w V_w (G x D). A warp does R rows at once with mma.sync: M = R*G query rows
+// (w', h), N / K = j*R columns (i, w') i-major, and a block-diagonal mask (w' = w') —
+// the padding costs tensor-core slots, which are free here, instead of per-row
+// instructions, which bound the kernel (ncu: a CUDA-core version issued ~1300 and a one-row
+// mma version ~675 instructions per row, at 26-33% of DRAM bandwidth).
+// Staging: a persistent block walks groups of NR consecutive rows through an NS-deep ring of
+// TMA boxes (64 columns, SW128, 1 KB-aligned): q as NR*G rows, K_i and V_i as NR rows each.
+// O overwrites q in place (same swizzle) and one TMA store per box writes the group to out.
+#ifndef TTT_DIAG_STAGE_KB
+#define TTT_DIAG_STAGE_KB 0  // dev override of the stage target (KB); 0 = by j (measured: 72 KB for j <= 2, else 100 KB)
+#endif
 struct DiagLayout {
-  int NR;
-  uint32_t off_q, off_k, off_v, stage_bytes, total;
-  __host__ __device__ void init(int nr, int g, int d, int j) {
+  int NR, NS, R;
+  uint32_t qbox, kbox, off_k, off_v, stage_bytes, total;
+  void init(int nr, int g, int d, int j, int ns, int rr) {
     NR = nr;
-    off_q = 0;
-    off_k = (uint32_t)nr * g * d * 2;
-    off_v = off_k + (uint32_t)j * nr * d * 2;
-    stage_bytes = (off_v + (uint32_t)j * nr * d * 2 + 127) & ~127u;
-    total = 2 * stage_bytes + 64;
+    NS = ns;
+    R = rr;
+    const uint32_t nb = (uint32_t)(d / 64);
+    qbox = (uint32_t)nr * g * 128;
+    kbox = (uint32_t)nr * 128;
+    off_k = qbox * nb;
+    off_v = off_k + (uint32_t)j * nb * kbox;
+    stage_bytes = (off_v + (uint32_t)j * nb * kbox + 1023) & ~1023u;
+    total = 1024 + (uint32_t)ns * stage_bytes + 1024;  // barriers | stages | alignment slack
   }
 };
 
 template <int D>
-__global__ void __launch_bounds__(512) ttt_fwd_diag_kernel(const __grid_constant__ Params p, DiagLayout lay) {
-  constexpr int E = D / 16, H = D / 32;
-  extern __shared__ __align__(128) uint8_t dsm[];
-  const int tid = threadIdx.x, hl = tid & 15, pair = tid >> 4;
-  const int NR = lay.NR, G = p.G, j = p.step;
-  const long nrows = (long)p.B * p.L * p.Hkv;
-  const long ngroups = (nrows + NR - 1) / NR;
-  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + lay.total - 64);
-  // one half-warp per (row, query head); lane hl owns elements [hl*H, +H) and [D/2 + hl*H, +H)
-  const bool ghost = pair >= NR * G;
-  const int pc = ghost ? 0 : pair;
-  const int lr = pc / G, hh = pc % G;
+__global__ void __launch_bounds__(512, 1)
+    ttt_fwd_diag_kernel(const __grid_constant__ Params p, const __grid_constant__ DiagMaps maps, DiagLayout lay) {
+  constexpr int NB = D / 64;
+  extern __shared__ uint8_t dsm_raw[];
+  uint8_t* dsm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+  uint8_t* stages = dsm + 1024;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int G = p.G, j = p.step, NR = lay.NR, NS = lay.NS, R = lay.R;
+  const int nrows = p.B * p.L * p.Hkv;  // < 2^31 (host check)
+  const int ngroups = (nrows + NR - 1) / NR;
+  const int MT = (G + 15) / 16;  // m-tiles per item (R == 1 when G > 16)
   if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](long grp, int st) {  // thread 0 only
-    const long w0 = grp * NR;
-    const int nv = (int)min((long)NR, nrows - w0);
-    uint8_t* base = dsm + st * lay.stage_bytes;
-    const uint32_t qb = (uint32_t)nv * G * D * 2, kb = (uint32_t)nv * D * 2;
-    mbar_expect_tx(&full[st], qb + 2 * j * kb);
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(base + lay.off_q)),
-                 "l"(reinterpret_cast<const __nv_bfloat16*>(p.q) + (size_t)w0 * G * D), "r"(qb),
-                 "r"(smem_u32(&full[st]))
-                 : "memory");
-    for (int i = 0; i < j; ++i) {
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       smem_u32(base + lay.off_k + i * NR * D * 2)),
-                   "l"(reinterpret_cast<const __nv_bfloat16*>(p.ks[i]) + (size_t)w0 * D), "r"(kb),
-                   "r"(smem_u32(&full[st]))
-                   : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       smem_u32(base + lay.off_v + i * NR * D * 2)),
-                   "l"(reinterpret_cast<const __nv_bfloat16*>(p.vs[i]) + (size_t)w0 * D), "r"(kb),
-                   "r"(smem_u32(&full[st]))
-                   : "memory");
-    }
-  };
-  auto lds = [&](const uint8_t* row, float (&x)[E]) {
+  auto issue = [&](int grp, int st) {  // thread 0
+    uint8_t* base = stages + st * lay.stage_bytes;
+    mbar_expect_tx(&full[st], NB * (lay.qbox + 2u * j * lay.kbox));  // full boxes (OOB rows zero-filled)
 #pragma unroll
-    for (int part = 0; part < 2; ++part) {
-      const uint8_t* src = row + (part * (D / 2) + hl * H) * 2;
-      if constexpr (H == 4) {  // bf16 -> fp32: one shift / mask per element
-        const uint2 u = *reinterpret_cast<const uint2*>(src);
-        x[part * 4 + 0] = __uint_as_float(u.x << 16);
-        x[part * 4 + 1] = __uint_as_float(u.x & 0xFFFF0000u);
-        x[part * 4 + 2] = __uint_as_float(u.y << 16);
-        x[part * 4 + 3] = __uint_as_float(u.y & 0xFFFF0000u);
-      } else {
-        const uint32_t u = *reinterpret_cast<const uint32_t*>(src);
-        x[part * 2 + 0] = __uint_as_float(u << 16);
-        x[part * 2 + 1] = __uint_as_float(u & 0xFFFF0000u);
+    for (int bx = 0; bx < NB; ++bx) {
+      tma_load_2d(base + bx * lay.qbox, &maps.q, &full[st], bx * 64, grp * NR * G);
+      for (int i = 0; i < j; ++i) {
+        tma_load_2d(base + lay.off_k + (i * NB + bx) * lay.kbox, &maps.k[i], &full[st], bx * 64, grp * NR);
+        tma_load_2d(base + lay.off_v + (i * NB + bx) * lay.kbox, &maps.v[i], &full[st], bx * 64, grp * NR);
       }
     }
   };
-  long grp = blockIdx.x;
-  if (tid == 0 && grp < ngroups) issue(grp, 0);
-  for (int n = 0; grp < ngroups; ++n, grp += gridDim.x) {
-    const int st = n & 1;
-    const long nxt = grp + gridDim.x;
-    if (tid == 0 && nxt < ngroups) issue(nxt, st ^ 1);  // stage st^1 was released by the last __syncthreads
-    mbar_wait(&full[st], (n >> 1) & 1);
-    const uint8_t* base = dsm + st * lay.stage_bytes;
-    const long w = grp * NR + lr;
-    const bool valid = !ghost && w < nrows;
-    const long wc = w < nrows ? w : grp * NR;
-    const int g = (int)(wc % p.Hkv);
-    const int r = (int)((wc / p.Hkv) % p.L);
-    const int b = (int)(wc / ((long)p.Hkv * p.L));
-    const bool act = valid && r < p.seq_lens[b];
-    float qf[E], o[E];
-    lds(base + lay.off_q + (uint32_t)(lr * G + hh) * D * 2, qf);
-#pragma unroll
-    for (int e = 0; e < E; ++e) o[e] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    for (int i = 0; i < j; ++i) {
-      float kk[E], vv[E];
-      lds(base + lay.off_k + (uint32_t)(i * NR + lr) * D * 2, kk);
-      lds(base + lay.off_v + (uint32_t)(i * NR + lr) * D * 2, vv);
-      float acc = 0.f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc = fmaf(qf[e], kk[e], acc);
-      const float t = half_allsum(acc) * p.scale_log2;  // s_i = c q_r . k_i (log2 units)
-      const float mn = fmaxf(m, t);
-      const float a = ex2(m - mn), wgt = ex2(t - mn);
-      l = l * a + wgt;
-#pragma unroll
-      for (int e = 0; e < E; ++e) o[e] = fmaf(wgt, vv[e], o[e] * a);
-      m = mn;
+  if (tid == 0) {
+    tma_prefetch_desc(&maps.q);
+    tma_prefetch_desc(&maps.out);
+    for (int s = 0; s < (NS > 1 ? NS - 1 : 1); ++s) {
+      const int grp = blockIdx.x + s * gridDim.x;
+      if (grp < ngroups) issue(grp, s);
     }
-    if (act) {
-      const int h = g * G + hh;
-      const size_t q_off = (((size_t)b * p.L + r) * p.Hq + h) * D;
-      const float inv = 1.f / l;
-      __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(p.out) + q_off;
-#pragma unroll
-      for (int part = 0; part < 2; ++part) {
-        __nv_bfloat16* dst = op + part * (D / 2) + hl * H;
-        if constexpr (H == 4)
-          *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(o[part * 4] * inv, o[part * 4 + 1] * inv),
-                                                      pack_bf16(o[part * 4 + 2] * inv, o[part * 4 + 3] * inv));
-        else
-          *reinterpret_cast<uint32_t*>(dst) = pack_bf16(o[part * 2] * inv, o[part * 2 + 1] * inv);
-      }
-      if (hl == 0) p.lse[((size_t)b * p.Hq + h) * p.L + r] = m + log2f(l);
-    }
-    __syncthreads();  // stage st fully consumed before it is refilled
   }
+  const int g8 = lane >> 2, c4 = lane & 3;
+  const float sl2 = p.scale_log2;
+  const int ncols = j * R;
+  // per-thread column bookkeeping (independent of the group): column n = i R + w'
+  int colw[4][2];  // w' of the thread's C-fragment columns, -1 when n >= j R
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n = nt * 8 + 2 * c4 + e;
+      colw[nt][e] = n < ncols ? n % R : -1;
+    }
+  int brow_i[4], brow_w[4];  // ldmatrix row (lanes 0-7 of each 8x8) of B n-tile nt: step i, row w'
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const int n = min(nt * 8 + (lane & 7), ncols - 1);
+    brow_i[nt] = n / R;
+    brow_w[nt] = n % R;
+  }
+  int grp = blockIdx.x;
+  for (int n = 0; grp < ngroups; ++n, grp += gridDim.x) {
+    const int st = n % NS;
+    mbar_wait(&full[st], (n / NS) & 1);
+    uint8_t* base = stages + st * lay.stage_bytes;
+    const uint32_t sb = smem_u32(base);
+    const int w0 = grp * NR, nv = min(NR, nrows - w0);
+    for (int lr0 = warp * R; lr0 < nv; lr0 += nwarps * R) {
+      // rows w' = 0..R-1 of this item: active iff in range and r < T_b (their lse / O are used)
+      uint32_t act = 0;
+      for (int wq = 0; wq < R && lr0 + wq < nv; ++wq) {
+        const uint32_t w = (uint32_t)(w0 + lr0 + wq);
+        const uint32_t bl = w / (uint32_t)p.Hkv;
+        const int b = (int)(bl / (uint32_t)p.L);
+        const int r = (int)(bl - (uint32_t)b * (uint32_t)p.L);
+        if (r < p.seq_lens[b]) act |= 1u << wq;
+      }
+      if (!act) continue;  // warp-uniform
+      for (int mt = 0; mt < MT; ++mt) {
+        // query row m of the tile: (w', h) = (m / G, m % G) when R > 1, head mt*16 + m when R == 1
+        const int mrows = R > 1 ? R * G : min(16, G - mt * 16);
+        // ---- S = Q K^T ----
+        float s[4][4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+        const uint32_t arow = (uint32_t)(lr0 * G + mt * 16 + min((lane & 7) + ((lane >> 3) & 1) * 8, mrows - 1));
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          uint32_t a[4];
+          const uint32_t chunk = (uint32_t)ks * 2 + (lane >> 4);
+          ldsm_x4(sb + (chunk >> 3) * lay.qbox + sw128_off(arow, chunk), a);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            if (nt * 8 < ncols) {
+              const uint32_t bch = (uint32_t)ks * 2 + ((lane >> 3) & 1);
+              const uint32_t brow = (uint32_t)(lr0 + brow_w[nt]);
+              uint32_t bb[2];
+              ldsm_x2(sb + lay.off_k + (uint32_t)(brow_i[nt] * NB + (bch >> 3)) * lay.kbox + sw128_off(brow, bch), bb);
+              mma_16816(s[nt], a, bb[0], bb[1]);
+            }
+          }
+        }
+        // ---- block-diagonal softmax: row m keeps the columns of its own w' ----
+        const int m0r = g8, m1r = g8 + 8;
+        const int wr0 = R > 1 ? m0r / G : 0, wr1 = R > 1 ? m1r / G : 0;
+        const bool ok0 = m0r < mrows && ((act >> wr0) & 1), ok1 = m1r < mrows && ((act >> wr1) & 1);
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            s[nt][e] = (ok0 && colw[nt][e] == wr0) ? s[nt][e] * sl2 : -INFINITY;
+            s[nt][2 + e] = (ok1 && colw[nt][e] == wr1) ? s[nt][2 + e] * sl2 : -INFINITY;
+            mx0 = fmaxf(mx0, s[nt][e]);
+            mx1 = fmaxf(mx1, s[nt][2 + e]);
+          }
+        }
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+        const float b0 = ok0 ? mx0 : 0.f, b1 = ok1 ? mx1 : 0.f;  // rows without columns: p = 0, no NaN
+        float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            s[nt][e] = ex2(s[nt][e] - b0);
+            s[nt][2 + e] = ex2(s[nt][2 + e] - b1);
+            l0 += s[nt][e];
+            l1 += s[nt][2 + e];
+          }
+        }
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+        const float i0 = ok0 ? 1.f / l0 : 0.f, i1 = ok1 ? 1.f / l1 : 0.f;
+        // ---- O = P V (m16n8k8 per 8-column k-tile) ----
+        float o[D / 8][4];
+#pragma unroll
+        for (int dt = 0; dt < D / 8; ++dt) o[dt][0] = o[dt][1] = o[dt][2] = o[dt][3] = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          if (nt * 8 < ncols) {
+            const uint32_t pa0 = pack_bf16(s[nt][0] * i0, s[nt][1] * i0);
+            const uint32_t pa1 = pack_bf16(s[nt][2] * i1, s[nt][3] * i1);
+            const uint32_t vrow = (uint32_t)(lr0 + brow_w[nt]);
+            const uint32_t vbase = sb + lay.off_v + (uint32_t)(brow_i[nt] * NB) * lay.kbox;
+#pragma unroll
+            for (int d4 = 0; d4 < D / 32; ++d4) {
+              const uint32_t ch = (uint32_t)(d4 * 4 + (lane >> 3));
+              uint32_t vb[4];
+              ldsm_x4_t(vbase + (ch >> 3) * lay.kbox + sw128_off(vrow, ch), vb);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) mma_1688(o[d4 * 4 + q], pa0, pa1, vb[q]);
+            }
+          }
+        }
+        // ---- O -> q rows in place (bf16, SW128), A_d -> lse ----
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int m = g8 + hf * 8;
+          if (hf ? ok1 : ok0) {
+            const uint32_t row = (uint32_t)(lr0 * G + mt * 16 + m);
+#pragma unroll
+            for (int dt = 0; dt < D / 8; ++dt) {
+              const uint32_t addr = sb + (uint32_t)(dt >> 3) * lay.qbox + sw128_off(row, (uint32_t)dt) + c4 * 4;
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(pack_bf16(o[dt][2 * hf], o[dt][2 * hf + 1])));
+            }
+            if (c4 == 0) {
+              const uint32_t w = (uint32_t)(w0 + lr0) + (R > 1 ? (uint32_t)(m / G) : 0u);
+              const int h_in = R > 1 ? m % G : mt * 16 + m;
+              const uint32_t bl = w / (uint32_t)p.Hkv;
+              const int g = (int)(w - bl * (uint32_t)p.Hkv);
+              const int b = (int)(bl / (uint32_t)p.L);
+              const int r = (int)(bl - (uint32_t)b * (uint32_t)p.L);
+              p.lse[((size_t)b * p.Hq + g * G + h_in) * p.L + r] = hf ? mx1 + log2f(l1) : mx0 + log2f(l0);
+            }
+          }
+        }
+      }
+    }
+    fence_async_smem();
+    __syncthreads();  // every row of the group written
+    if (tid == 0) {
+#pragma unroll
+      for (int bx = 0; bx < NB; ++bx) tma_store_2d(&maps.out, base + bx * lay.qbox, bx * 64, w0 * G);
+      bulk_commit();
+      if (NS > 1) {
+        bulk_wait_read1();  // the previous group's store has read its stage ...
+        const int rg = grp + (NS - 1) * gridDim.x;
+        if (rg < ngroups) issue(rg, (n + NS - 1) % NS);  // ... refilled NS-1 groups ahead
+      } else {
+        bulk_wait_read0();
+        if (grp + (int)gridDim.x < ngroups) issue(grp + gridDim.x, 0);
+      }
+    }
+  }
+  if (tid == 0) bulk_wait0();
+}
+
+// R rows per warp item: M = R*G <= 16 query rows, j*R <= 32 columns (4 n-tiles); a power of 2.
+// NR rows per group: a multiple of max(8, R) (1 KB-aligned boxes), NR*G <= 256 (TMA box rows),
+// stage ~72-100 KB; 2-4 stages (1 when one 8-row stage is all that fits).
+bool diag_layout(const Params& p, int D, DiagLayout* lay) {
+  int R = 1;
+  while (R * 2 * p.G <= 16 && R * 2 * p.step <= 32) R *= 2;
+  const int gran = std::max(8, R);
+  const int row_bytes = (p.G + 2 * p.step) * D * 2;
+  const int stage_kb = TTT_DIAG_STAGE_KB > 0 ? TTT_DIAG_STAGE_KB : (p.step <= 2 ? 72 : 100);
+  int nr = std::max(gran, (stage_kb * 1024 / row_bytes) / gran * gran);
+  while (nr > gran && nr * p.G > 256) nr -= gran;
+  if (nr * p.G > 256) return false;
+  for (int ns = 4; ns >= 1; --ns) {
+    lay->init(nr, p.G, D, p.step, ns, R);
+    if (lay->total <= 220 * 1024) return true;
+  }
+  return false;
 }
 
 template <int D>
-cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, cudaStream_t st) {
+cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, const DiagMaps& dmaps, cudaStream_t st) {
   const int smem = 6 * kTile * D * 2 + 1024;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
@@ -552,23 +676,14 @@ cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, cudaStream_t st) 
   }
   if (p.step > 0) {
     DiagLayout lay;
-    int nr = std::max(1, 32 / p.G);  // 32 half-warps (512 threads) of (row, head) pairs
-    for (; nr > 1; nr >>= 1) {
-      lay.init(nr, p.G, D, p.step);
-      if (lay.total <= 200 * 1024) break;
-    }
-    lay.init(nr, p.G, D, p.step);
-    if (lay.total > 227 * 1024) return cudaErrorInvalidConfiguration;
+    if (!diag_layout(p, D, &lay)) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(ttt_fwd_diag_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)lay.total);
     if (e != cudaSuccess) return e;
-    const long rows = (long)p.B * p.L * p.Hkv;
-    const long groups = (rows + nr - 1) / nr;
-    const int per_sm = lay.total <= 110 * 1024 ? 2 : 1;
-    const int blocks = (int)std::min<long>(groups, 148L * per_sm);
+    const int rows = p.B * p.L * p.Hkv;
+    const int groups = (rows + lay.NR - 1) / lay.NR;
     prof_mark(kKindFwdDiag, true, st);
-    const int threads = std::min(512, std::max(32, ((nr * p.G * 16 + 31) / 32) * 32));
-    ttt_fwd_diag_kernel<D><<<blocks, threads, lay.total, st>>>(p, lay);
+    ttt_fwd_diag_kernel<D><<<std::min(groups, 148), 512, lay.total, st>>>(p, dmaps, lay);
     prof_mark(kKindFwdDiag, false, st);
   }
   const int npairs = (p.G + 1) / 2;
@@ -581,8 +696,13 @@ cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, cudaStream_t st) 
 
 }  // namespace
 
-cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, cudaStream_t st) {
-  return p.D == 64 ? launch_fwd_d<64>(p, maps, st) : launch_fwd_d<128>(p, maps, st);
+int fwd_diag_rows_per_group(const Params& p) {
+  DiagLayout lay;
+  return diag_layout(p, p.D, &lay) ? lay.NR : 0;
+}
+
+cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, const DiagMaps& dmaps, cudaStream_t st) {
+  return p.D == 64 ? launch_fwd_d<64>(p, maps, dmaps, st) : launch_fwd_d<128>(p, maps, dmaps, st);
 }
 
 }  // namespace tttk

@@ -49,6 +49,11 @@ struct Params {
 struct FwdMaps {
   CUtensorMap q, k, v, out, out_lo;
 };
+// forward diagonal pre-pass: q and out viewed as [B*L*Hq rows][D], box 64 x (NR*G) rows, SW128;
+struct DiagMaps {
+  CUtensorMap q, out;
+  CUtensorMap k[TTT_MAX_STEPS], v[TTT_MAX_STEPS];  // K_i, V_i as [B*L*Hkv rows][D], box 64 x NR
+};
 struct BwdMaps {
   CUtensorMap q, k, v, dout;
   CUtensorMap dout64;  // dO with 64-row boxes (the 64-query sub-item halves)
