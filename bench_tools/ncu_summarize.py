@@ -79,11 +79,17 @@ def launches(csvf, out):
         v = float(r[mv].replace(",", "")) * SCALE.get(r[mu], 1e-9)
         c, t = agg.get(name, (0, 0.0))
         agg[name] = (c + 1, t + v)
-    tot = sum(t for _, t in agg.values())
-    lines = [f"{'kernel':34s} {'launches':>8s} {'total_ms':>10s} {'avg_us':>9s} {'share':>7s}"]
-    for name, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        lines.append(f"{name:34s} {c:8d} {t * 1e3:10.3f} {t / c * 1e6:9.1f} {t / tot:7.1%}")
-    lines.append(f"{'TOTAL':34s} {sum(c for c, _ in agg.values()):8d} {tot * 1e3:10.3f}")
+    ours = {k: v for k, v in agg.items() if k.startswith("ttt_")}
+    tot = sum(t for _, t in ours.values())
+    lines = [f"{'kernel (this library; share of their total)':44s} {'launches':>8s} {'total_ms':>10s} {'avg_us':>9s} {'share':>7s}"]
+    for name, (c, t) in sorted(ours.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"{name:44s} {c:8d} {t * 1e3:10.3f} {t / c * 1e6:9.1f} {t / tot:7.1%}")
+    lines.append(f"{'TOTAL':44s} {sum(c for c, _ in ours.values()):8d} {tot * 1e3:10.3f}")
+    other = {k: v for k, v in agg.items() if not k.startswith("ttt_")}
+    if other:
+        lines.append("other kernels in the captured process (input generation / buffer zeroing at setup, not in the step):")
+        for name, (c, t) in sorted(other.items(), key=lambda kv: -kv[1][1]):
+            lines.append(f"  {name[:80]:80s} {c:5d} {t * 1e3:9.3f} ms")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
