@@ -16,7 +16,8 @@ cudaError_t launch_fwd_check(const Params& p, cudaStream_t st);
 cudaError_t launch_bwd_check(const Params& p, cudaStream_t st);
 cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, const DiagMaps& dmaps, cudaStream_t st);
 int fwd_diag_rows_per_group(const Params& p);
-cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, cudaStream_t st);
+cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st);
+int bwd_pre_rows_per_group(const Params& p);
 }  // namespace tttk
 
 using namespace tttk;
@@ -350,7 +351,21 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
       !encode_bshd(&maps.dout64, dout, p.B, p.L, p.Hq, p.D, 64) ||
       !encode_dqacc(&maps.dqacc, p.dq_acc, (size_t)p.B * p.L * p.Hq * p.D / 32))
     return TTT_ERR_CUDA;
-  return cuda_status(launch_bwd_sm100(p, maps, s));
+  PreMaps pmaps;
+  {
+    const int nr = bwd_pre_rows_per_group(p);
+    if (nr <= 0) return TTT_ERR_UNSUPPORTED;
+    const long long rows = (long long)p.B * p.L * p.Hq, kv_rows = (long long)p.B * p.L * p.Hkv;
+    const int br = nr * p.G;
+    if (!encode_rows2d(&pmaps.dout, dout, rows, p.D, br) || !encode_rows2d(&pmaps.o, out, rows, p.D, br) ||
+        (p.o_lo && !encode_rows2d(&pmaps.olo, p.o_lo, rows, p.D, br)) ||
+        (p.step > 0 && !encode_rows2d(&pmaps.q, q, rows, p.D, br)))
+      return TTT_ERR_CUDA;
+    for (int i = 0; i < p.step; ++i)
+      if (!encode_rows2d(&pmaps.k[i], p.ks[i], kv_rows, p.D, nr) || !encode_rows2d(&pmaps.v[i], p.vs[i], kv_rows, p.D, nr))
+        return TTT_ERR_CUDA;
+  }
+  return cuda_status(launch_bwd_sm100(p, maps, pmaps, s));
 }
 
 }  // extern "C"

@@ -70,274 +70,346 @@ __device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int
 }
 
 // ------------------------------------------------------------------ kernel 1
-// HBM-streaming, TMA-staged: a persistent block walks groups of NR consecutive
-// (b, r, g) rows. For such a group every operand is ONE contiguous block in HBM
-// (q / dO / O / O_lo: NR*G*D bf16; K_i, V_i: NR*D bf16; dK_i, dV_i: NR*D fp32), so
-// thread 0 moves each with a single 1-D cp.async.bulk into a double-buffered
-// stage. One HALF-warp per (row, query head): Delta, the diagonal p_i / ds_i and
-// dq stay in registers; dK_i / dV_i (sums over the G heads) are accumulated with
-// shared-memory atomics in the stage and written back with bulk stores. Lane hl
-// owns elements [hl*E/2, +E/2) and [D/2 + hl*E/2, +E/2): every half-warp smem
-// access is contiguous (bank-conflict free).
+// Diagonal / preprocess pass, an HBM stream. Per kv row w = (b, r, g) with G query heads
+// and the j diagonal keys K_i[r], V_i[r] (Alg. 2 M_suffix):
+//   Delta_h = dO_h . (O_h + O_lo_h),  lse2_h = lse_h log2 e          (all rows)
+//   S = Q K^T, dP = dO V^T          (G x j),  P = 2^(S c log2e - lse2) on the allowed set
+//   dS = P o (dP - Delta);  dq_acc = c dS K  (initialises the fp32 dq accumulator)
+//   dK_i[r] (+)= c dS^T Q,  dV_i[r] (+)= P^T dO     (GQA sums fall out of the products)
+// Tiny matrices per row, so a compute warp takes R rows at once with mma.sync: M = R G query
+// rows (w', h), N = j R columns (i, w') i-major, block-diagonal mask (as in the forward
+// diagonal pass). Delta is the diagonal of dO (O + O_lo)^T on the same tensor pipe.
+// Pipeline: one producer warp TMA-loads groups of NR rows (SW128 boxes: dO, O, O_lo, q as
+// NR G rows, K_i and V_i as NR rows) into an NS-deep ring; compute warps take items
+// round-robin and release a stage through its `empty` mbarrier — no block barriers. Outputs
+// leave straight from the mma fragments: dq_acc (tiled fp32) and -Delta / -lse2 by plain
+// stores, dK_i / dV_i by st.global.v2 (overwrite) or red.global.add.v2 (accumulate; L2 does
+// the read-modify-write), so no stage space is spent on fp32 outputs.
+constexpr int kPreCompute = 8;  // compute warps (+ 1 producer warp)
 struct PreLayout {
-  int NR, G, D, step, acc, has_lo;
-  uint32_t off_q, off_do, off_o, off_olo, off_k, off_v, off_dk, off_dv, stage_bytes, off_sc, total;
-  __host__ __device__ void init(int nr, int g, int d, int j, int accumulate, int lo) {
-    NR = nr; G = g; D = d; step = j; acc = accumulate; has_lo = lo;
-    const uint32_t qb = (uint32_t)nr * g * d * 2, kb = (uint32_t)nr * d * 2, fb = (uint32_t)nr * d * 4;
-    off_q = 0; off_do = qb; off_o = 2 * qb; off_olo = 3 * qb;
-    off_k = 4 * qb; off_v = off_k + j * kb; off_dk = off_v + j * kb; off_dv = off_dk + j * fb;
-    stage_bytes = (off_dv + j * fb + 127) & ~127u;
-    off_sc = 2 * stage_bytes;                            // fp32 [NR][j][G][2]: (p_i, c ds_i) per head
-    total = off_sc + ((uint32_t)nr * (j > 0 ? j : 1) * g * 8 + 127) / 128 * 128 + 64;  // + 2 mbarriers
+  int NR, NS, R, has_lo;
+  uint32_t qbytes, kbytes;  // bytes one TMA box delivers (NR G or NR rows x 128 B)
+  uint32_t qbox, kbox, off_do, off_o, off_olo, off_q, off_k, off_v, stage_bytes, off_scr, total;
+  void init(int nr, int g, int d, int j, int ns, int rr, int lo) {
+    NR = nr;
+    NS = ns;
+    R = rr;
+    has_lo = lo;
+    const uint32_t nb = (uint32_t)(d / 64);
+    qbytes = (uint32_t)nr * g * 128;
+    kbytes = (uint32_t)nr * 128;
+    qbox = (qbytes + 1023) & ~1023u;  // box allocations 1 KB-aligned (SW128)
+    kbox = (kbytes + 1023) & ~1023u;
+    off_do = 0;
+    off_o = off_do + nb * qbox;
+    off_olo = off_o + nb * qbox;
+    off_q = off_olo + (lo ? nb * qbox : 0u);
+    off_k = off_q + (j > 0 ? nb * qbox : 0u);
+    off_v = off_k + (uint32_t)j * nb * kbox;
+    stage_bytes = (off_v + (uint32_t)j * nb * kbox + 1023) & ~1023u;
+    off_scr = 1024 + (uint32_t)ns * stage_bytes;             // per compute warp: P, dS bf16 [16][40]
+    total = off_scr + kPreCompute * 2 * 1280 + 1024;         // + alignment slack
   }
 };
 
-__device__ __forceinline__ void bulk_store_1d(void* gdst, const void* ssrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_load_1d_(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-// split-lane bf16 row chunk: E/2 elements at hl*E/2 and at D/2 + hl*E/2 -> fp32
-// (bf16 -> fp32 is a 16-bit shift: one SHL / LOP per element)
-__device__ __forceinline__ void bf2_to_f(uint32_t w, float& lo, float& hi) {
-  lo = __uint_as_float(w << 16);
-  hi = __uint_as_float(w & 0xFFFF0000u);
-}
 template <int D>
-__device__ __forceinline__ void lds_split(const uint8_t* row, int hl, float (&x)[D / 16]) {
-  constexpr int H = D / 32;  // elements per half (4 for D=128, 2 for D=64)
-#pragma unroll
-  for (int part = 0; part < 2; ++part) {
-    const uint8_t* src = row + (part * (D / 2) + hl * H) * 2;
-    if constexpr (H == 4) {
-      const uint2 u = *reinterpret_cast<const uint2*>(src);
-      bf2_to_f(u.x, x[part * 4 + 0], x[part * 4 + 1]);
-      bf2_to_f(u.y, x[part * 4 + 2], x[part * 4 + 3]);
-    } else {
-      const uint32_t u = *reinterpret_cast<const uint32_t*>(src);
-      bf2_to_f(u, x[part * 2 + 0], x[part * 2 + 1]);
+__global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
+    ttt_bwd_pre_kernel(const __grid_constant__ Params p, const __grid_constant__ PreMaps maps, PreLayout lay) {
+  constexpr int NB = D / 64;
+  extern __shared__ uint8_t psm_raw[];
+  uint8_t* psm = psm_raw + ((1024u - (smem_u32(psm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(psm);
+  uint64_t* empty = full + 8;
+  uint8_t* stages = psm + 1024;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = p.G, j = p.step, NR = lay.NR, NS = lay.NS, R = lay.R;
+  const int nrows = p.B * p.L * p.Hkv;  // < 2^31 (host check)
+  const int ngroups = (nrows + NR - 1) / NR;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kPreCompute);
     }
-  }
-}
-template <int D>
-__device__ __forceinline__ int split_col(int hl, int e) {  // D index of lane element e
-  constexpr int H = D / 32;
-  return (e < H) ? hl * H + e : D / 2 + hl * H + (e - H);
-}
-
-template <int D, int GT>  // GT: GQA group size (compile time; 0 = runtime p.G)
-__global__ void __launch_bounds__(512) ttt_bwd_pre_kernel(const __grid_constant__ Params p, PreLayout lay) {
-  constexpr int E = D / 16;
-  extern __shared__ __align__(128) uint8_t psm[];
-  const int tid = threadIdx.x, hl = tid & 15, pair = tid >> 4;
-  const int G = GT > 0 ? GT : p.G;
-  const int NR = lay.NR, j = p.step;
-  const long nrows = (long)p.B * p.L * p.Hkv;
-  const long ngroups = (nrows + NR - 1) / NR;
-  uint64_t* full = reinterpret_cast<uint64_t*>(psm + lay.total - 64);
-  // half-warp `pair` -> (row lr, head hh); ghosts (pair >= NR*G) mirror pair 0 without storing
-  const bool ghost = pair >= NR * G;
-  const int pc = ghost ? 0 : pair;
-  const int lr = pc / G, hh = pc % G;
-  if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](long grp, int st) {  // thread 0 only
-    const long w0 = grp * NR;
-    const int nv = (int)min((long)NR, nrows - w0);
-    uint8_t* base = psm + st * lay.stage_bytes;
-    const uint32_t qb = (uint32_t)nv * G * D * 2, kb = (uint32_t)nv * D * 2, fb = (uint32_t)nv * D * 4;
-    const uint32_t bytes = 3 * qb + j * 2 * kb + (lay.has_lo ? qb : 0) + (lay.acc ? j * 2 * fb : 0);
-    mbar_expect_tx(&full[st], bytes);
-    const size_t qo = (size_t)w0 * G * D, ko = (size_t)w0 * D;
-    bulk_load_1d_(base + lay.off_q, reinterpret_cast<const __nv_bfloat16*>(p.q) + qo, qb, &full[st]);
-    bulk_load_1d_(base + lay.off_do, reinterpret_cast<const __nv_bfloat16*>(p.dout) + qo, qb, &full[st]);
-    bulk_load_1d_(base + lay.off_o, reinterpret_cast<const __nv_bfloat16*>(p.o) + qo, qb, &full[st]);
-    if (lay.has_lo)
-      bulk_load_1d_(base + lay.off_olo, reinterpret_cast<const __nv_bfloat16*>(p.o_lo) + qo, qb, &full[st]);
-    for (int i = 0; i < j; ++i) {
-      bulk_load_1d_(base + lay.off_k + i * (NR * D * 2), reinterpret_cast<const __nv_bfloat16*>(p.ks[i]) + ko, kb,
-                    &full[st]);
-      bulk_load_1d_(base + lay.off_v + i * (NR * D * 2), reinterpret_cast<const __nv_bfloat16*>(p.vs[i]) + ko, kb,
-                    &full[st]);
-      if (lay.acc) {
-        bulk_load_1d_(base + lay.off_dk + i * (NR * D * 4), p.dks[i] + ko, fb, &full[st]);
-        bulk_load_1d_(base + lay.off_dv + i * (NR * D * 4), p.dvs[i] + ko, fb, &full[st]);
-      }
-    }
-  };
-  long grp = blockIdx.x;
-  if (tid == 0 && grp < ngroups) issue(grp, 0);
-  for (int n = 0; grp < ngroups; ++n, grp += gridDim.x) {
-    const int st = n & 1;
-    const long nxt = grp + gridDim.x;
-    if (tid == 0 && nxt < ngroups) {
-      bulk_wait_read0();  // bulk stores of group n-1 (same stage as n+1) have read their smem
-      issue(nxt, st ^ 1);
-    }
-    uint8_t* base = psm + st * lay.stage_bytes;
-    const long w = grp * NR + lr;
-    const bool valid = !ghost && w < nrows;
-    const long wc = w < nrows ? w : grp * NR;
-    // 32-bit decode of wc = (b L + r) Hkv + g (host guarantees B L Hq < 2^31)
-    const uint32_t bl = (uint32_t)wc / (uint32_t)p.Hkv;
-    const int g = (int)((uint32_t)wc - bl * (uint32_t)p.Hkv);
-    const int b = (int)(bl / (uint32_t)p.L);
-    const int r = (int)(bl - (uint32_t)b * (uint32_t)p.L);
-    const int h = g * G + hh;
-    const bool act = valid && r < p.seq_lens[b];  // diagonal keys exist only for rows r < T_b
-    if (!lay.acc && valid && hh == 0) {  // dK_0 / dV_0 rows in HBM: the main kernel adds into them
+
+  if (warp == 0) {
+    // ================= producer =================
+    if (lane == 0) {
+      tma_prefetch_desc(&maps.dout);
+      tma_prefetch_desc(&maps.o);
+      const uint32_t bytes = NB * ((2u + (lay.has_lo ? 1u : 0u) + (j > 0 ? 1u : 0u)) * lay.qbytes + 2u * j * lay.kbytes);
+      int n = 0;
+      for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++n) {
+        const int st = n % NS;
+        if (n >= NS) mbar_wait(&empty[st], ((n / NS) - 1) & 1);
+        uint8_t* base = stages + st * lay.stage_bytes;
+        mbar_expect_tx(&full[st], bytes);  // full boxes (OOB rows are zero-filled and counted)
+        const int rq = grp * NR * G, rk = grp * NR;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        p.dk[(size_t)w * D + split_col<D>(hl, e)] = 0.f;
-        p.dv[(size_t)w * D + split_col<D>(hl, e)] = 0.f;
-      }
-    }
-    mbar_wait(&full[st], (n >> 1) & 1);
-    const uint32_t ro = (uint32_t)(lr * G + hh) * D * 2;
-    float o[E], dd[E], qq[E], dq[E];
-    lds_split<D>(base + lay.off_o + ro, hl, o);
-    lds_split<D>(base + lay.off_do + ro, hl, dd);
-    if (lay.has_lo) {
-      float lo[E];
-      lds_split<D>(base + lay.off_olo + ro, hl, lo);
-#pragma unroll
-      for (int e = 0; e < E; ++e) o[e] += lo[e];
-    }
-    float acc = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) acc = fmaf(o[e], dd[e], acc);
-    const float del = half_allsum(acc);  // Delta_r = dO_r . O_r
-    const size_t li = ((size_t)b * p.Hq + h) * p.L + r;
-    const float l2 = p.lse_in[li] * kLog2e;
-    if (valid && hl == 0) {  // stored negated: the main kernel's FFMA2 / FADD2 consume -lse2 and -Delta
-      p.delta[li] = -del;
-      p.lse2[li] = -l2;
-    }
-    lds_split<D>(base + lay.off_q + ro, hl, qq);
-#pragma unroll
-    for (int e = 0; e < E; ++e) dq[e] = 0.f;
-    // ---- phase A: per (row, head) the diagonal scalars (Alg. 2 M_suffix) and dq ----
-    float* scal = reinterpret_cast<float*>(psm + lay.off_sc);  // [NR][j][G][2]
-    {
-      const uint8_t* kp = base + lay.off_k + lr * D * 2;
-      const uint8_t* vp = base + lay.off_v + lr * D * 2;
-      float* sp = scal + ((lr * j) * G + hh) * 2;
-      const bool wr = !ghost && hl == 0;
-      const float sl2 = p.scale_log2, cs = p.scale;
-      for (int i = 0; i < j; ++i, kp += NR * D * 2, vp += NR * D * 2, sp += 2 * G) {
-        float kk[E], vv[E];
-        lds_split<D>(kp, hl, kk);
-        lds_split<D>(vp, hl, vv);
-        float sdot = 0.f, dp = 0.f;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          sdot = fmaf(qq[e], kk[e], sdot);
-          dp = fmaf(dd[e], vv[e], dp);
-        }
-#pragma unroll
-        for (int o2 = 8; o2 > 0; o2 >>= 1) {
-          sdot += __shfl_xor_sync(0xffffffffu, sdot, o2);
-          dp += __shfl_xor_sync(0xffffffffu, dp, o2);
-        }
-        const float pr = act ? ex2(sdot * sl2 - l2) : 0.f;  // p_i = exp(c q.k_i - lse)
-        const float cds = cs * pr * (dp - del);             // c ds_i, ds_i = p_i (dp_i - Delta)
-#pragma unroll
-        for (int e = 0; e < E; ++e) dq[e] = fmaf(cds, kk[e], dq[e]);
-        if (wr) {
-          sp[0] = pr;
-          sp[1] = cds;
-        }
-      }
-    }
-    if (valid) {
-#pragma unroll
-      for (int part = 0; part < 2; ++part) {
-        const int d0 = part * (D / 2) + hl * (E / 2);
-        float* q4 = p.dq_acc + dqacc_index(p, b, h, r, d0);
-        if constexpr (E / 2 == 4)
-          *reinterpret_cast<float4*>(q4) = make_float4(dq[part * 4], dq[part * 4 + 1], dq[part * 4 + 2], dq[part * 4 + 3]);
-        else
-          *reinterpret_cast<float2*>(q4) = make_float2(dq[part * 2], dq[part * 2 + 1]);
-      }
-    }
-    __syncthreads();  // all (p_i, c ds_i) of the group visible
-    // ---- phase B: per (row, step, D-slice): dK_i = sum_h c ds_h q_h, dV_i = sum_h p_h dO_h ----
-    // (exclusive ownership of each stage row: no atomics; overwrite or accumulate)
-    {
-      const int nitems = NR * j;
-      for (int it = pair; it < nitems; it += blockDim.x / 16) {
-        const int brow = it % NR, i = it / NR;
-        const long wb = grp * NR + brow;
-        if (wb >= nrows) continue;
-        float dk[E], dv[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) dk[e] = dv[e] = 0.f;
-        const float* sp = scal + ((brow * j + i) * G) * 2;
-        const uint8_t* qp = base + lay.off_q + brow * G * D * 2;
-        const uint8_t* op = base + lay.off_do + brow * G * D * 2;
-#pragma unroll(GT > 0 ? GT : 1)
-        for (int h2 = 0; h2 < G; ++h2, qp += D * 2, op += D * 2) {
-          const float pr = sp[2 * h2], cds = sp[2 * h2 + 1];
-          float q2[E], d2[E];
-          lds_split<D>(qp, hl, q2);
-          lds_split<D>(op, hl, d2);
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            dk[e] = fmaf(cds, q2[e], dk[e]);
-            dv[e] = fmaf(pr, d2[e], dv[e]);
-          }
-        }
-        float* dkr = reinterpret_cast<float*>(base + lay.off_dk + i * (NR * D * 4)) + brow * D;
-        float* dvr = reinterpret_cast<float*>(base + lay.off_dv + i * (NR * D * 4)) + brow * D;
-#pragma unroll
-        for (int part = 0; part < 2; ++part) {
-          const int d0 = part * (D / 2) + hl * (E / 2);
-          if constexpr (E / 2 == 4) {
-            float4 a = make_float4(dk[part * 4], dk[part * 4 + 1], dk[part * 4 + 2], dk[part * 4 + 3]);
-            float4 c = make_float4(dv[part * 4], dv[part * 4 + 1], dv[part * 4 + 2], dv[part * 4 + 3]);
-            if (lay.acc) {
-              const float4 a0 = *reinterpret_cast<const float4*>(dkr + d0), c0 = *reinterpret_cast<const float4*>(dvr + d0);
-              a.x += a0.x; a.y += a0.y; a.z += a0.z; a.w += a0.w;
-              c.x += c0.x; c.y += c0.y; c.z += c0.z; c.w += c0.w;
-            }
-            *reinterpret_cast<float4*>(dkr + d0) = a;
-            *reinterpret_cast<float4*>(dvr + d0) = c;
-          } else {
-#pragma unroll
-            for (int e = 0; e < E / 2; ++e) {
-              const int k2 = part * (E / 2) + e;
-              dkr[d0 + e] = lay.acc ? dkr[d0 + e] + dk[k2] : dk[k2];
-              dvr[d0 + e] = lay.acc ? dvr[d0 + e] + dv[k2] : dv[k2];
-            }
+        for (int bx = 0; bx < NB; ++bx) {
+          tma_load_2d(base + lay.off_do + bx * lay.qbox, &maps.dout, &full[st], bx * 64, rq);
+          tma_load_2d(base + lay.off_o + bx * lay.qbox, &maps.o, &full[st], bx * 64, rq);
+          if (lay.has_lo) tma_load_2d(base + lay.off_olo + bx * lay.qbox, &maps.olo, &full[st], bx * 64, rq);
+          if (j > 0) tma_load_2d(base + lay.off_q + bx * lay.qbox, &maps.q, &full[st], bx * 64, rq);
+          for (int i = 0; i < j; ++i) {
+            tma_load_2d(base + lay.off_k + (i * NB + bx) * lay.kbox, &maps.k[i], &full[st], bx * 64, rk);
+            tma_load_2d(base + lay.off_v + (i * NB + bx) * lay.kbox, &maps.v[i], &full[st], bx * 64, rk);
           }
         }
       }
     }
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      const long w0 = grp * NR;
-      const int nv = (int)min((long)NR, nrows - w0);
-      for (int i = 0; i < j; ++i) {
-        bulk_store_1d(p.dks[i] + (size_t)w0 * D, base + lay.off_dk + i * (NR * D * 4), (uint32_t)nv * D * 4);
-        bulk_store_1d(p.dvs[i] + (size_t)w0 * D, base + lay.off_dv + i * (NR * D * 4), (uint32_t)nv * D * 4);
-      }
-      bulk_commit();
-    }
+    return;
   }
-  if (tid == 0) bulk_wait0();
+
+  // ================= compute warps =================
+  const int cw = warp - 1;
+  const int g8 = lane >> 2, c4 = lane & 3;
+  const float sl2 = p.scale_log2, cs = p.scale;
+  const int ncols = j * R;
+  const int NT = (ncols + 7) / 8;   // 8-column tiles of S / dP (<= 4)
+  const int MT2 = (ncols + 15) / 16;  // 16-row tiles of dK / dV (<= 2)
+  const int MT = (G + 15) / 16;     // 16-row tiles of query rows (R == 1 when G > 16)
+  const int ipg = (NR + R - 1) / R;
+  uint8_t* scrP = psm + lay.off_scr + cw * 2560;  // [16 rows m][40] bf16 (80-B rows: conflict-free)
+  uint8_t* scrS = scrP + 1280;
+  const uint32_t sP = smem_u32(scrP), sS = smem_u32(scrS);
+  int colw[4][2];  // w' of the thread's C-fragment columns, -1 past j R
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n = nt * 8 + 2 * c4 + e;
+      colw[nt][e] = n < ncols ? n % R : -1;
+    }
+  int brow_i[4], brow_w[4];  // ldmatrix row (lane & 7) of column tile nt: step i, row w'
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const int n = ncols > 0 ? min(nt * 8 + (lane & 7), ncols - 1) : 0;
+    brow_i[nt] = n / R;
+    brow_w[nt] = n % R;
+  }
+  int n = 0;
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++n) {
+    const int st = n % NS;
+    mbar_wait(&full[st], (n / NS) & 1);
+    const uint32_t sb = smem_u32(stages + st * lay.stage_bytes);
+    const int w0 = grp * NR, nv = min(NR, nrows - w0);
+    const int nitems = (nv + R - 1) / R;
+    // items of this group owned by this warp: global item id n*ipg + k, round-robin over warps
+    for (int k = (cw - (n * ipg) % kPreCompute + kPreCompute) % kPreCompute; k < nitems; k += kPreCompute) {
+      const int lr0 = k * R;
+      for (int mt = 0; mt < MT; ++mt) {
+        const int mrows = R > 1 ? R * G : min(16, G - mt * 16);
+        // ---- the thread's two query rows (g8, g8 + 8): (w', head), validity, lse2 ----
+        int wr[2], hh[2], bb[2], rr[2], gg[2];
+        bool okr[2], act[2];
+        float l2[2];
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int m = g8 + hf * 8;
+          wr[hf] = R > 1 ? m / G : 0;
+          hh[hf] = R > 1 ? m % G : mt * 16 + m;
+          okr[hf] = m < mrows && lr0 + wr[hf] < nv;
+          const uint32_t w = (uint32_t)(w0 + min(lr0 + wr[hf], nv - 1));
+          const uint32_t bl = w / (uint32_t)p.Hkv;
+          gg[hf] = (int)(w - bl * (uint32_t)p.Hkv);
+          bb[hf] = (int)(bl / (uint32_t)p.L);
+          rr[hf] = (int)(bl - (uint32_t)bb[hf] * (uint32_t)p.L);
+          act[hf] = okr[hf] && rr[hf] < p.seq_lens[bb[hf]];
+          l2[hf] = okr[hf] ? p.lse_in[((size_t)bb[hf] * p.Hq + gg[hf] * G + hh[hf]) * p.L + rr[hf]] * kLog2e : 0.f;
+        }
+        // ---- S = Q K^T, dP = dO V^T, Delta = diag(dO (O + O_lo)^T) ----
+        float s[4][4], dp[4][4], cd[2][4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s[t][e] = dp[t][e] = 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cd[0][e] = cd[1][e] = 0.f;
+        const uint32_t qrow0 = (uint32_t)(lr0 * G + mt * 16);
+        const uint32_t arow = qrow0 + (uint32_t)min((lane & 7) + ((lane >> 3) & 1) * 8, mrows - 1);
+        const uint32_t orow = qrow0 + (uint32_t)min((lane & 7) + ((lane >> 4) & 1) * 8, mrows - 1);  // B: rows m'
+#pragma unroll 2
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t ach = (uint32_t)ks * 2 + (lane >> 4);
+          uint32_t ado[4];
+          ldsm_x4(sb + lay.off_do + (ach >> 3) * lay.qbox + sw128_off(arow, ach), ado);
+          {  // Delta: B = O rows m' (n-tiles m' 0-7, 8-15), k = 16 columns of D
+            const uint32_t och = (uint32_t)ks * 2 + ((lane >> 3) & 1);
+            uint32_t bo[4];
+            ldsm_x4(sb + lay.off_o + (och >> 3) * lay.qbox + sw128_off(orow, och), bo);
+            mma_16816(cd[0], ado, bo[0], bo[1]);
+            mma_16816(cd[1], ado, bo[2], bo[3]);
+            if (lay.has_lo) {
+              ldsm_x4(sb + lay.off_olo + (och >> 3) * lay.qbox + sw128_off(orow, och), bo);
+              mma_16816(cd[0], ado, bo[0], bo[1]);
+              mma_16816(cd[1], ado, bo[2], bo[3]);
+            }
+          }
+          if (ncols > 0) {
+            uint32_t aq[4];
+            ldsm_x4(sb + lay.off_q + (ach >> 3) * lay.qbox + sw128_off(arow, ach), aq);
+            const uint32_t bch = (uint32_t)ks * 2 + ((lane >> 3) & 1);
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              if (nt < NT) {
+                const uint32_t brow = (uint32_t)(lr0 + brow_w[nt]);
+                const uint32_t boff = (uint32_t)(brow_i[nt] * NB + (bch >> 3)) * lay.kbox + sw128_off(brow, bch);
+                uint32_t bk[2], bv[2];
+                ldsm_x2(sb + lay.off_k + boff, bk);
+                ldsm_x2(sb + lay.off_v + boff, bv);
+                mma_16816(s[nt], aq, bk[0], bk[1]);
+                mma_16816(dp[nt], ado, bv[0], bv[1]);
+              }
+            }
+          }
+        }
+        // Delta of row m sits at column m: thread (g8, c4 = g8 / 2), element g8 & 1 (rows g8, g8 + 8)
+        float del[2];
+        {
+          const int src = g8 * 4 + (g8 >> 1);
+          const float d0 = (g8 & 1) ? cd[0][1] : cd[0][0];
+          const float d1 = (g8 & 1) ? cd[1][3] : cd[1][2];
+          del[0] = __shfl_sync(0xffffffffu, d0, src);
+          del[1] = __shfl_sync(0xffffffffu, d1, src);
+        }
+        // ---- P and c dS on the allowed (block-diagonal) entries; bf16 copies to the scratch ----
+        uint32_t pa[4][2], da[4][2];  // A fragments (m16n8k8) of P and c dS per column tile
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          if (nt < NT) {
+            float pv[4], dv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int hf = e >> 1;
+              const bool ok = act[hf] && colw[nt][e & 1] == wr[hf];
+              const float pr = ok ? ex2(s[nt][e] * sl2 - l2[hf]) : 0.f;  // p_i = exp(c q.k_i - lse)
+              pv[e] = pr;
+              dv[e] = cs * pr * (dp[nt][e] - del[hf]);  // c ds_i, ds_i = p_i (dp_i - Delta)
+            }
+            pa[nt][0] = pack_bf16(pv[0], pv[1]);
+            pa[nt][1] = pack_bf16(pv[2], pv[3]);
+            da[nt][0] = pack_bf16(dv[0], dv[1]);
+            da[nt][1] = pack_bf16(dv[2], dv[3]);
+            const uint32_t o0 = (uint32_t)g8 * 80 + (uint32_t)(nt * 8 + 2 * c4) * 2;
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sP + o0), "r"(pa[nt][0]));
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sP + o0 + 640), "r"(pa[nt][1]));
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sS + o0), "r"(da[nt][0]));
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sS + o0 + 640), "r"(da[nt][1]));
+          }
+        }
+        __syncwarp();
+        // ---- dq_acc = c dS K (zeros at j = 0), -Delta, -lse2 ----
+        size_t qbase[2];
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int h = gg[hf] * G + hh[hf];
+          qbase[hf] = ((((size_t)(bb[hf] * p.Hq + h) * p.nqt + (rr[hf] >> 7)) * (D / 32)) * 128 + (rr[hf] & 127)) * 32;
+          if (okr[hf] && c4 == 0) {
+            const size_t li = ((size_t)bb[hf] * p.Hq + h) * p.L + rr[hf];
+            p.delta[li] = -del[hf];  // stored negated: the main kernel's FFMA2 / FADD2 consume -lse2, -Delta
+            p.lse2[li] = -l2[hf];
+          }
+        }
+#pragma unroll
+        for (int d4 = 0; d4 < D / 32; ++d4) {
+          float acc[4][4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            if (nt < NT) {
+              const uint32_t ch = (uint32_t)(d4 * 4 + (lane >> 3));
+              const uint32_t brow = (uint32_t)(lr0 + brow_w[nt]);
+              uint32_t kb[4];
+              ldsm_x4_t(sb + lay.off_k + (uint32_t)(brow_i[nt] * NB + (ch >> 3)) * lay.kbox + sw128_off(brow, ch), kb);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) mma_1688(acc[q], da[nt][0], da[nt][1], kb[q]);
+            }
+          }
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            if (okr[hf]) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int d = (d4 * 4 + q) * 8 + 2 * c4;
+                *reinterpret_cast<float2*>(p.dq_acc + qbase[hf] + (size_t)(d >> 5) * 4096 + (d & 31)) =
+                    make_float2(acc[q][2 * hf], acc[q][2 * hf + 1]);
+              }
+            }
+          }
+        }
+        // ---- dK_i = (c dS)^T Q, dV_i = P^T dO: rows n = (i, w'), K = the 16 query rows ----
+        for (int t2 = 0; t2 < MT2; ++t2) {
+          // A' = (c dS)^T / P^T: ldmatrix.trans of the [m][n] scratch, matrices (m 0-7 | 8-15) x (n 0-7 | 8-15)
+          const int mi = lane >> 3;
+          const uint32_t aoff = (uint32_t)(((mi >> 1) * 8 + (lane & 7)) * 80 + (t2 * 16 + (mi & 1) * 8) * 2);
+          uint32_t ads[4], ap[4];
+          ldsm_x4_t(sS + aoff, ads);
+          ldsm_x4_t(sP + aoff, ap);
+          // output rows of this tile: n = t2*16 + g8 (+8) -> (i, w')
+          int oi[2], ow[2];
+          bool ook[2];
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            const int nn = t2 * 16 + g8 + hf * 8;
+            oi[hf] = nn / R;
+            ow[hf] = nn % R;
+            ook[hf] = nn < ncols && lr0 + ow[hf] < nv;
+          }
+          const uint32_t brow = qrow0 + (uint32_t)min((mi & 1) * 8 + (lane & 7), mrows - 1);  // B' rows m
+#pragma unroll 2
+          for (int dc = 0; dc < D / 8; dc += 2) {
+            const uint32_t ch = (uint32_t)(dc + (mi >> 1));
+            uint32_t bq[4], bo[4];
+            ldsm_x4_t(sb + lay.off_q + (ch >> 3) * lay.qbox + sw128_off(brow, ch), bq);
+            ldsm_x4_t(sb + lay.off_do + (ch >> 3) * lay.qbox + sw128_off(brow, ch), bo);
+            float k0[4] = {0.f, 0.f, 0.f, 0.f}, k1[4] = {0.f, 0.f, 0.f, 0.f};
+            float v0[4] = {0.f, 0.f, 0.f, 0.f}, v1[4] = {0.f, 0.f, 0.f, 0.f};
+            mma_16816(k0, ads, bq[0], bq[1]);
+            mma_16816(k1, ads, bq[2], bq[3]);
+            mma_16816(v0, ap, bo[0], bo[1]);
+            mma_16816(v1, ap, bo[2], bo[3]);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              if (ook[hf]) {
+                const size_t ro = (size_t)(w0 + lr0 + ow[hf]) * D;
+                float* dk = p.dks[oi[hf]] + ro;
+                float* dv = p.dvs[oi[hf]] + ro;
+                const int d0 = dc * 8 + 2 * c4, d1 = d0 + 8;
+                if (p.accumulate) {
+                  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dk + d0), "f"(k0[2 * hf]), "f"(k0[2 * hf + 1]) : "memory");
+                  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dk + d1), "f"(k1[2 * hf]), "f"(k1[2 * hf + 1]) : "memory");
+                  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dv + d0), "f"(v0[2 * hf]), "f"(v0[2 * hf + 1]) : "memory");
+                  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dv + d1), "f"(v1[2 * hf]), "f"(v1[2 * hf + 1]) : "memory");
+                } else if (mt == 0) {
+                  *reinterpret_cast<float2*>(dk + d0) = make_float2(k0[2 * hf], k0[2 * hf + 1]);
+                  *reinterpret_cast<float2*>(dk + d1) = make_float2(k1[2 * hf], k1[2 * hf + 1]);
+                  *reinterpret_cast<float2*>(dv + d0) = make_float2(v0[2 * hf], v0[2 * hf + 1]);
+                  *reinterpret_cast<float2*>(dv + d1) = make_float2(v1[2 * hf], v1[2 * hf + 1]);
+                } else {  // G > 16: later head tiles add to the first tile's values (same thread wrote them)
+                  float2* a = reinterpret_cast<float2*>(dk + d0);
+                  float2* c = reinterpret_cast<float2*>(dk + d1);
+                  float2* e2 = reinterpret_cast<float2*>(dv + d0);
+                  float2* f2 = reinterpret_cast<float2*>(dv + d1);
+                  float2 x = *a; *a = make_float2(x.x + k0[2 * hf], x.y + k0[2 * hf + 1]);
+                  x = *c; *c = make_float2(x.x + k1[2 * hf], x.y + k1[2 * hf + 1]);
+                  x = *e2; *e2 = make_float2(x.x + v0[2 * hf], x.y + v0[2 * hf + 1]);
+                  x = *f2; *f2 = make_float2(x.x + v1[2 * hf], x.y + v1[2 * hf + 1]);
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();  // scratch reused by the next item / head tile
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
 }
 
 // ------------------------------------------------------------------ kernel 2
@@ -859,41 +931,44 @@ int pick_head_split(const Params& p) {
   return hs;
 }
 
+// R rows per warp item (R G <= 16 query rows, j R <= 32 columns, power of 2); NR rows per
+// group: a multiple of R, NR G <= 256 (TMA box rows), stage ~64 KB; 4 down to 1 stages.
+bool pre_layout(const Params& p, int D, PreLayout* lay) {
+  int R = 1;
+  while (R * 2 * p.G <= 16 && R * 2 * p.step <= 32) R *= 2;
+  const int lo = p.o_lo != nullptr;
+  const int row_bytes = ((2 + lo + (p.step > 0)) * p.G + 2 * p.step) * D * 2;
+  for (int nr = std::max(R, (64 * 1024 / row_bytes) / R * R); nr >= R; nr -= R) {
+    if (nr * p.G > 256) continue;
+    for (int ns = 4; ns >= 1; --ns) {
+      lay->init(nr, p.G, D, p.step, ns, R, lo);
+      if (lay->total <= 225 * 1024 && (ns >= 2 || nr == R)) return true;
+    }
+  }
+  return false;
+}
+
 template <int D>
-cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, cudaStream_t st) {
+cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st) {
   Params p = p_in;
   p.head_split = pick_head_split(p);
-  // 1. pre-pass (TMA-staged, persistent)
+  // 1. pre-pass (TMA-staged, persistent, warp-specialised)
   {
     PreLayout lay;
-    int nr = std::max(1, 32 / p.G);  // 32 half-warps (512 threads) of (row, head) pairs
-    for (; nr > 1; nr >>= 1) {
-      lay.init(nr, p.G, D, p.step, p.accumulate, p.o_lo != nullptr);
-      if (lay.total <= 220 * 1024) break;
+    if (!pre_layout(p, D, &lay)) return cudaErrorInvalidConfiguration;
+    if (!p.accumulate) {  // dK_0 / dV_0: the main kernel adds into them
+      const size_t kvb = (size_t)p.B * p.L * p.Hkv * D * sizeof(float);
+      cudaError_t e = cudaMemsetAsync(p.dk, 0, kvb, st);
+      if (e == cudaSuccess) e = cudaMemsetAsync(p.dv, 0, kvb, st);
+      if (e != cudaSuccess) return e;
     }
-    lay.init(nr, p.G, D, p.step, p.accumulate, p.o_lo != nullptr);
-    if (lay.total > 227 * 1024) return cudaErrorInvalidConfiguration;
-    const long rows = (long)p.B * p.L * p.Hkv;
-    const long groups = (rows + nr - 1) / nr;
-    const int blocks = (int)std::min<long>(groups, 148);
-    const int threads = std::min(512, std::max(32, ((nr * p.G * 16 + 31) / 32) * 32));
-    auto run = [&](auto kern) -> cudaError_t {
-      cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
-      if (e2 != cudaSuccess) return e2;
-      prof_mark(kKindBwdPre, true, st);
-      kern<<<blocks, threads, lay.total, st>>>(p, lay);
-      return cudaSuccess;
-    };
-    cudaError_t e;
-    switch (p.G) {  // compile-time group size for the common GQA ratios
-      case 1: e = run(ttt_bwd_pre_kernel<D, 1>); break;
-      case 2: e = run(ttt_bwd_pre_kernel<D, 2>); break;
-      case 4: e = run(ttt_bwd_pre_kernel<D, 4>); break;
-      case 8: e = run(ttt_bwd_pre_kernel<D, 8>); break;
-      case 16: e = run(ttt_bwd_pre_kernel<D, 16>); break;
-      default: e = run(ttt_bwd_pre_kernel<D, 0>); break;
-    }
+    cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)lay.total);
     if (e != cudaSuccess) return e;
+    const int rows = p.B * p.L * p.Hkv;
+    const int groups = (rows + lay.NR - 1) / lay.NR;
+    prof_mark(kKindBwdPre, true, st);
+    ttt_bwd_pre_kernel<D><<<std::min(groups, 148), 32 * (kPreCompute + 1), lay.total, st>>>(p, pmaps, lay);
     prof_mark(kKindBwdPre, false, st);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -939,8 +1014,13 @@ extern "C" int ttt_debug_trace_read(void* host, unsigned int cta) {
 }
 #endif
 
-cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, cudaStream_t st) {
-  return p.D == 64 ? launch_bwd_d<64>(p, maps, st) : launch_bwd_d<128>(p, maps, st);
+int bwd_pre_rows_per_group(const Params& p) {
+  PreLayout lay;
+  return pre_layout(p, p.D, &lay) ? lay.NR : 0;
+}
+
+cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st) {
+  return p.D == 64 ? launch_bwd_d<64>(p, maps, pmaps, st) : launch_bwd_d<128>(p, maps, pmaps, st);
 }
 
 }  // namespace tttk

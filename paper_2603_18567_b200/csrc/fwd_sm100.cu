@@ -432,14 +432,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #endif
 struct DiagLayout {
   int NR, NS, R;
+  uint32_t qbytes, kbytes;  // bytes one TMA box delivers (NR G or NR rows x 128 B)
   uint32_t qbox, kbox, off_k, off_v, stage_bytes, total;
   void init(int nr, int g, int d, int j, int ns, int rr) {
     NR = nr;
     NS = ns;
     R = rr;
     const uint32_t nb = (uint32_t)(d / 64);
-    qbox = (uint32_t)nr * g * 128;
-    kbox = (uint32_t)nr * 128;
+    qbytes = (uint32_t)nr * g * 128;
+    kbytes = (uint32_t)nr * 128;
+    qbox = (qbytes + 1023) & ~1023u;  // box allocations 1 KB-aligned (SW128)
+    kbox = (kbytes + 1023) & ~1023u;
     off_k = qbox * nb;
     off_v = off_k + (uint32_t)j * nb * kbox;
     stage_bytes = (off_v + (uint32_t)j * nb * kbox + 1023) & ~1023u;
@@ -467,7 +470,7 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   auto issue = [&](int grp, int st) {  // thread 0
     uint8_t* base = stages + st * lay.stage_bytes;
-    mbar_expect_tx(&full[st], NB * (lay.qbox + 2u * j * lay.kbox));  // full boxes (OOB rows zero-filled)
+    mbar_expect_tx(&full[st], NB * (lay.qbytes + 2u * j * lay.kbytes));  // full boxes (OOB rows zero-filled)
 #pragma unroll
     for (int bx = 0; bx < NB; ++bx) {
       tma_load_2d(base + bx * lay.qbox, &maps.q, &full[st], bx * 64, grp * NR * G);
@@ -647,20 +650,19 @@ __global__ void __launch_bounds__(512, 1)
 }
 
 // R rows per warp item: M = R*G <= 16 query rows, j*R <= 32 columns (4 n-tiles); a power of 2.
-// NR rows per group: a multiple of max(8, R) (1 KB-aligned boxes), NR*G <= 256 (TMA box rows),
-// stage ~72-100 KB; 2-4 stages (1 when one 8-row stage is all that fits).
+// NR rows per group: a multiple of R with NR*G <= 256 (TMA box rows), stage ~72-100 KB;
+// 4 down to 1 stages.
 bool diag_layout(const Params& p, int D, DiagLayout* lay) {
   int R = 1;
   while (R * 2 * p.G <= 16 && R * 2 * p.step <= 32) R *= 2;
-  const int gran = std::max(8, R);
   const int row_bytes = (p.G + 2 * p.step) * D * 2;
   const int stage_kb = TTT_DIAG_STAGE_KB > 0 ? TTT_DIAG_STAGE_KB : (p.step <= 2 ? 72 : 100);
-  int nr = std::max(gran, (stage_kb * 1024 / row_bytes) / gran * gran);
-  while (nr > gran && nr * p.G > 256) nr -= gran;
-  if (nr * p.G > 256) return false;
-  for (int ns = 4; ns >= 1; --ns) {
-    lay->init(nr, p.G, D, p.step, ns, R);
-    if (lay->total <= 220 * 1024) return true;
+  for (int nr = std::max(R, (stage_kb * 1024 / row_bytes) / R * R); nr >= R; nr -= R) {
+    if (nr * p.G > 256) continue;
+    for (int ns = 4; ns >= 1; --ns) {
+      lay->init(nr, p.G, D, p.step, ns, R);
+      if (lay->total <= 220 * 1024 && (ns >= 2 || nr == R)) return true;
+    }
   }
   return false;
 }

@@ -50,6 +50,11 @@ struct FwdMaps {
   CUtensorMap q, k, v, out, out_lo;
 };
 // forward diagonal pre-pass: q and out viewed as [B*L*Hq rows][D], box 64 x (NR*G) rows, SW128;
+// backward pre-pass (bwd_sm100.cu): 2-D [rows][D] bf16 views, SW128, 64-column boxes
+struct PreMaps {
+  CUtensorMap dout, o, olo, q;                      // [B L Hq rows][D] bf16, box 64 x NR*G
+  CUtensorMap k[TTT_MAX_STEPS], v[TTT_MAX_STEPS];  // [B L Hkv rows][D] bf16, box 64 x NR
+};
 struct DiagMaps {
   CUtensorMap q, out;
   CUtensorMap k[TTT_MAX_STEPS], v[TTT_MAX_STEPS];  // K_i, V_i as [B*L*Hkv rows][D], box 64 x NR
