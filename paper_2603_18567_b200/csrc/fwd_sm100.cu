@@ -424,9 +424,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // the padding costs tensor-core slots, which are free here, instead of per-row
 // instructions, which bound the kernel (ncu: a CUDA-core version issued ~1300 and a one-row
 // mma version ~675 instructions per row, at 26-33% of DRAM bandwidth).
-// Staging: a persistent block walks groups of NR consecutive rows through an NS-deep ring of
-// TMA boxes (64 columns, SW128, 1 KB-aligned): q as NR*G rows, K_i and V_i as NR rows each.
-// O overwrites q in place (same swizzle) and one TMA store per box writes the group to out.
+// Pipeline: a producer warp TMA-loads groups of NR consecutive rows (64-column SW128 boxes: q
+// as NR*G rows, K_i and V_i as NR rows) into an NS-deep ring; 7 compute warps take items
+// round-robin and release a stage through its `empty` mbarrier (no block barriers); O_d and
+// A_d leave straight from the mma fragments.
 #ifndef TTT_DIAG_STAGE_KB
 #define TTT_DIAG_STAGE_KB 0  // dev override of the stage target (KB); 0 = by j (measured: 72 KB for j <= 2, else 100 KB)
 #endif
@@ -450,47 +451,58 @@ struct DiagLayout {
   }
 };
 
+constexpr int kDiagCompute = 7;  // compute warps (+ 1 producer warp): 256 threads, so up to 255 registers
+
 template <int D>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(32 * (kDiagCompute + 1), 1)
     ttt_fwd_diag_kernel(const __grid_constant__ Params p, const __grid_constant__ DiagMaps maps, DiagLayout lay) {
   constexpr int NB = D / 64;
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* dsm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+  uint64_t* empty = full + 8;
   uint8_t* stages = dsm + 1024;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = p.G, j = p.step, NR = lay.NR, NS = lay.NS, R = lay.R;
   const int nrows = p.B * p.L * p.Hkv;  // < 2^31 (host check)
   const int ngroups = (nrows + NR - 1) / NR;
   const int MT = (G + 15) / 16;  // m-tiles per item (R == 1 when G > 16)
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kDiagCompute);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](int grp, int st) {  // thread 0
-    uint8_t* base = stages + st * lay.stage_bytes;
-    mbar_expect_tx(&full[st], NB * (lay.qbytes + 2u * j * lay.kbytes));  // full boxes (OOB rows zero-filled)
+  if (warp == 0) {
+    // ================= producer: q (NR G rows), K_i, V_i (NR rows) boxes per group =================
+    if (lane == 0) {
+      tma_prefetch_desc(&maps.q);
+      int n = 0;
+      for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++n) {
+        const int st = n % NS;
+        if (n >= NS) mbar_wait(&empty[st], ((n / NS) - 1) & 1);
+        uint8_t* base = stages + st * lay.stage_bytes;
+        mbar_expect_tx(&full[st], NB * (lay.qbytes + 2u * j * lay.kbytes));  // OOB rows zero-filled, counted
 #pragma unroll
-    for (int bx = 0; bx < NB; ++bx) {
-      tma_load_2d(base + bx * lay.qbox, &maps.q, &full[st], bx * 64, grp * NR * G);
-      for (int i = 0; i < j; ++i) {
-        tma_load_2d(base + lay.off_k + (i * NB + bx) * lay.kbox, &maps.k[i], &full[st], bx * 64, grp * NR);
-        tma_load_2d(base + lay.off_v + (i * NB + bx) * lay.kbox, &maps.v[i], &full[st], bx * 64, grp * NR);
+        for (int bx = 0; bx < NB; ++bx) {
+          tma_load_2d(base + bx * lay.qbox, &maps.q, &full[st], bx * 64, grp * NR * G);
+          for (int i = 0; i < j; ++i) {
+            tma_load_2d(base + lay.off_k + (i * NB + bx) * lay.kbox, &maps.k[i], &full[st], bx * 64, grp * NR);
+            tma_load_2d(base + lay.off_v + (i * NB + bx) * lay.kbox, &maps.v[i], &full[st], bx * 64, grp * NR);
+          }
+        }
       }
     }
-  };
-  if (tid == 0) {
-    tma_prefetch_desc(&maps.q);
-    tma_prefetch_desc(&maps.out);
-    for (int s = 0; s < (NS > 1 ? NS - 1 : 1); ++s) {
-      const int grp = blockIdx.x + s * gridDim.x;
-      if (grp < ngroups) issue(grp, s);
-    }
+    return;
   }
+  // ================= compute warps: R stacked rows per item, round-robin =================
+  const int cw = warp - 1;
   const int g8 = lane >> 2, c4 = lane & 3;
   const float sl2 = p.scale_log2;
   const int ncols = j * R;
+  const int ipg = (NR + R - 1) / R;
   // per-thread column bookkeeping (independent of the group): column n = i R + w'
   int colw[4][2];  // w' of the thread's C-fragment columns, -1 when n >= j R
 #pragma unroll
@@ -507,14 +519,15 @@ __global__ void __launch_bounds__(512, 1)
     brow_i[nt] = n / R;
     brow_w[nt] = n % R;
   }
-  int grp = blockIdx.x;
-  for (int n = 0; grp < ngroups; ++n, grp += gridDim.x) {
+  int n = 0;
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++n) {
     const int st = n % NS;
     mbar_wait(&full[st], (n / NS) & 1);
-    uint8_t* base = stages + st * lay.stage_bytes;
-    const uint32_t sb = smem_u32(base);
+    const uint32_t sb = smem_u32(stages + st * lay.stage_bytes);
     const int w0 = grp * NR, nv = min(NR, nrows - w0);
-    for (int lr0 = warp * R; lr0 < nv; lr0 += nwarps * R) {
+    const int nitems = (nv + R - 1) / R;
+    for (int k = (cw - (n * ipg) % kDiagCompute + kDiagCompute) % kDiagCompute; k < nitems; k += kDiagCompute) {
+      const int lr0 = k * R;
       // rows w' = 0..R-1 of this item: active iff in range and r < T_b (their lse / O are used)
       uint32_t act = 0;
       for (int wq = 0; wq < R && lr0 + wq < nv; ++wq) {
@@ -524,7 +537,7 @@ __global__ void __launch_bounds__(512, 1)
         const int r = (int)(bl - (uint32_t)b * (uint32_t)p.L);
         if (r < p.seq_lens[b]) act |= 1u << wq;
       }
-      if (!act) continue;  // warp-uniform
+      if (!act) continue;  // warp-uniform; the main kernel ignores such rows
       for (int mt = 0; mt < MT; ++mt) {
         // query row m of the tile: (w', h) = (m / G, m % G) when R > 1, head mt*16 + m when R == 1
         const int mrows = R > 1 ? R * G : min(16, G - mt * 16);
@@ -606,20 +619,18 @@ __global__ void __launch_bounds__(512, 1)
             }
           }
         }
-        // ---- O -> q rows in place (bf16, SW128), A_d -> lse ----
+        // ---- O_d -> out (bf16 pairs straight from the fragments), A_d -> lse ----
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           const int m = g8 + hf * 8;
           if (hf ? ok1 : ok0) {
-            const uint32_t row = (uint32_t)(lr0 * G + mt * 16 + m);
+            const uint32_t w = (uint32_t)(w0 + lr0) + (R > 1 ? (uint32_t)(m / G) : 0u);
+            const int h_in = R > 1 ? m % G : mt * 16 + m;
+            __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + ((size_t)w * G + h_in) * D + 2 * c4;
 #pragma unroll
-            for (int dt = 0; dt < D / 8; ++dt) {
-              const uint32_t addr = sb + (uint32_t)(dt >> 3) * lay.qbox + sw128_off(row, (uint32_t)dt) + c4 * 4;
-              asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(pack_bf16(o[dt][2 * hf], o[dt][2 * hf + 1])));
-            }
+            for (int dt = 0; dt < D / 8; ++dt)
+              *reinterpret_cast<uint32_t*>(orow + dt * 8) = pack_bf16(o[dt][2 * hf], o[dt][2 * hf + 1]);
             if (c4 == 0) {
-              const uint32_t w = (uint32_t)(w0 + lr0) + (R > 1 ? (uint32_t)(m / G) : 0u);
-              const int h_in = R > 1 ? m % G : mt * 16 + m;
               const uint32_t bl = w / (uint32_t)p.Hkv;
               const int g = (int)(w - bl * (uint32_t)p.Hkv);
               const int b = (int)(bl / (uint32_t)p.L);
@@ -630,23 +641,9 @@ __global__ void __launch_bounds__(512, 1)
         }
       }
     }
-    fence_async_smem();
-    __syncthreads();  // every row of the group written
-    if (tid == 0) {
-#pragma unroll
-      for (int bx = 0; bx < NB; ++bx) tma_store_2d(&maps.out, base + bx * lay.qbox, bx * 64, w0 * G);
-      bulk_commit();
-      if (NS > 1) {
-        bulk_wait_read1();  // the previous group's store has read its stage ...
-        const int rg = grp + (NS - 1) * gridDim.x;
-        if (rg < ngroups) issue(rg, (n + NS - 1) % NS);  // ... refilled NS-1 groups ahead
-      } else {
-        bulk_wait_read0();
-        if (grp + (int)gridDim.x < ngroups) issue(grp + gridDim.x, 0);
-      }
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
-  if (tid == 0) bulk_wait0();
 }
 
 // R rows per warp item: M = R*G <= 16 query rows, j*R <= 32 columns (4 n-tiles); a power of 2.
@@ -685,7 +682,7 @@ cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, const DiagMaps& d
     const int rows = p.B * p.L * p.Hkv;
     const int groups = (rows + lay.NR - 1) / lay.NR;
     prof_mark(kKindFwdDiag, true, st);
-    ttt_fwd_diag_kernel<D><<<std::min(groups, 148), 512, lay.total, st>>>(p, dmaps, lay);
+    ttt_fwd_diag_kernel<D><<<std::min(groups, 148), 32 * (kDiagCompute + 1), lay.total, st>>>(p, dmaps, lay);
     prof_mark(kKindFwdDiag, false, st);
   }
   const int npairs = (p.G + 1) / 2;
