@@ -24,10 +24,11 @@ tests/cuda/libumma_probe.so: tests/cuda/umma_probe.cu $(PKG)/csrc/ptx_sm100.cuh
 	$(NVCC) $(NVFLAGS) -shared -o $@ $< 2> build/probe.ptxas.txt || (cat build/probe.ptxas.txt; exit 1)
 
 # dev A/B variant: same sources, extra defines, separate output (not loaded unless TTT_ATTN_LIB points at it)
+VNAME ?= variant
 variant:
-	@mkdir -p build/variant
-	for f in $(SRCS); do $(NVCC) $(NVFLAGS) -c $$f -o build/variant/$$(basename $$f .cu).o 2>/dev/null || exit 1; done
-	$(NVCC) $(ARCH) -shared -o build/libtttattn_variant.so build/variant/*.o
+	@mkdir -p build/$(VNAME)
+	for f in $(SRCS); do $(NVCC) $(NVFLAGS) -c $$f -o build/$(VNAME)/$$(basename $$f .cu).o 2>/dev/null || exit 1; done
+	$(NVCC) $(ARCH) -shared -o build/libtttattn_$(VNAME).so build/$(VNAME)/*.o
 
 clean:
 	rm -rf build $(PKG)/libtttattn.so oracle/liboracle.so tests/cuda/libumma_probe.so

@@ -22,6 +22,7 @@ z = lambda: torch.zeros(s.kv_shape, device=dev)
 dk, dv = z(), z(); dks = [z() for _ in range(S - 1)]; dvs = [z() for _ in range(S - 1)]
 ws = torch.empty(ttt.ttt_attn_workspace_size(desc, S - 1, True), dtype=torch.uint8, device=dev)
 tot_f = tot_b = 0.0
+ksum = {}
 fwd = lambda j: ttt.ttt_attn_fwd(desc, j, q, k, v, ks, vs, out, lse, out_lo=olo)
 bwd = lambda j: ttt.ttt_attn_bwd(desc, j, q, k, v, ks, vs, out, lse, do, dq, dk, dv, dks, dvs, flags=1, workspace=ws, out_lo=olo)
 
@@ -47,14 +48,17 @@ for j in range(S):
     base = B * Hq * L * (L + 1) / 2
     ms, kern = timeit(lambda: fwd(j))
     tot_f += ms
+    for n_, v_ in kern.items(): ksum[n_] = ksum.get(n_, 0.0) + v_[0]
     km = " ".join(f"{n.replace('ttt_','').replace('_kernel','')}={v[0]:.3f}" for n, v in kern.items())
     msg = f"{cfg} j={j} fwd {ms:.3f} ms {4*D*pairs/ms/1e9:.1f} TFLOP/s [{km}]"
     if do_bwd:
         msb, kern = timeit(lambda: bwd(j))
         tot_b += msb
+        for n_, v_ in kern.items(): ksum[n_] = ksum.get(n_, 0.0) + v_[0]
         mm = kern.get("ttt_bwd_sm100_kernel", (0, 1))[0]
         km = " ".join(f"{n.replace('ttt_','').replace('_kernel','')}={v[0]:.3f}" for n, v in kern.items())
         msg += f" | bwd {msb:.3f} ms {8*D*pairs/msb/1e9:.1f} TFLOP/s [{km}] main {8*D*base/mm/1e9:.0f} TF/s"
     print(msg, flush=True)
 P = B * Hq * (S * L * (L + 1) / 2 + L * S * (S - 1) / 2)
 print(f"unroll fwd {tot_f:.3f} ms ({4*D*P/tot_f/1e9:.1f} TFLOP/s)" + (f" bwd {tot_b:.3f} ms ({8*D*P/tot_b/1e9:.1f}) total {12*D*P/(tot_f+tot_b)/1e9:.1f} TFLOP/s" if do_bwd else ""))
+print("kernels ms/unroll: " + " ".join(f"{n.replace('ttt_','').replace('_kernel','')}={v:.3f}" for n, v in ksum.items()))

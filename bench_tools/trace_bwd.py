@@ -22,9 +22,9 @@ lib.ttt_debug_trace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
 for _ in range(2):
     ttt.ttt_attn_bwd(desc, j, q, k, v, [], [], out, lse, do, dq, dk, dv, [], [], flags=0, workspace=ws, out_lo=olo)
 lib.ttt_debug_trace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
-names = {0: {1: "mma:got_p_a", 2: "mma:got_p_b", 3: "mma:got_ds_a", 4: "mma:got_ds_b", 5: "mma:got_dqempty", 6: "mma:dP_issued", 7: "mma:dK_a_issued", 8: "mma:dK_b_issued", 9: "mma:dQ_issued", 10: "mma:S_issued"},
-         1: {1: "cmpA:got_s", 2: "cmpA:p_done", 3: "cmpA:got_dp", 4: "cmpA:ds_done"},
-         2: {1: "dq:got_dq", 2: "dq:drained"}}
+names = {0: {1: "mma:got_p_a", 2: "mma:got_p_b", 3: "mma:got_ds_a", 4: "mma:got_ds_b", 5: "mma:got_dqempty", 6: "mma:dP_issued", 7: "mma:dK_a_issued", 8: "mma:dK_b_issued", 9: "mma:dQ_issued", 10: "mma:S_issued", 11: "mma:got_q", 12: "mma:got_do_a", 13: "mma:got_do_b"},
+         1: {1: "cmpA:got_s", 2: "cmpA:p_done", 3: "cmpA:got_dp", 4: "cmpA:ds_done", 5: "cmpA:s_loaded", 6: "cmpA:p_math_done", 7: "cmpA:got_dsempty"},
+         2: {1: "dq:got_dq", 2: "dq:drained", 11: "prod:q_issue", 12: "prod:do_a_issue", 13: "prod:do_b_issue", 14: "obs:q_arrived", 15: "obs:do_a_arrived", 16: "obs:do_b_arrived"}}
 ev = []
 for role in range(3):
     for x in buf[role]:
@@ -78,3 +78,12 @@ for phase, nm in ((False, "P arrive"), (True, "dS arrive")):
         if ph != phase or it not in gs or it < 4: continue
         for k, t in d.items(): rel.setdefault(k, []).append(t - gs[it])
     print(nm, "median offset by warp:", {k: int(np.median(v)) for k, v in sorted(rel.items())})
+
+# absolute timeline (all roles) over a window of steady-state items
+if "timeline" in sys.argv:
+    gs_sorted = sorted(gs.items())
+    lo = gs[20] if 20 in gs else ev[0][0]
+    hi = gs[23] if 23 in gs else ev[-1][0]
+    for t, n, i in ev:
+        if lo - 2000 <= t <= hi:
+            print(f"{t - lo:7d}  {n:18s} item {i}")

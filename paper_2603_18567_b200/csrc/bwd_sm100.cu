@@ -513,7 +513,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int hsplit = p.head_split;
   const int nh = p.G / hsplit;
   // (b, g, head subset)-major, kv tile fastest (ascending = longest first): the CTAs of one
-  // kv head run together, so its Q / dO tiles and dq_acc rows stay hot in L2.
+  // kv head run together, so its Q / dO tiles and dq_acc rows stay hot in L2. (A global
+  // longest-first order — kv tile slowest — measured slower: 5.3 vs 5.26 ms bwd, 2.73-2.85 vs
+  // 2.63-2.66 ms fwd per unroll in an interleaved A/B, bench_tools/ab.sh.)
   const int kt = (int)blockIdx.x % p.nqt;
   const int grp = (int)blockIdx.x / p.nqt;
   const int hs = grp % hsplit;
@@ -597,7 +599,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     reg_dealloc<88>();
     {
       TTT_TRACE_DECL(0);
-      constexpr uint32_t idSP = idesc_bf16_f32(128, 64, false, false);  // S^T = K Q_x^T, dP^T = V dO_x^T
+      constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);  // S^T = K Q^T
+      constexpr uint32_t idSP = idesc_bf16_f32(128, 64, false, false);  // dP^T = V dO_x^T
       constexpr uint32_t idKV = idesc_bf16_f32(128, D, false, true);    // dV += P^T dO_x, dK += dS^T Q_x
       constexpr uint32_t idDQ = idesc_bf16_f32(128, D, true, true);     // dQ = dS K
       // descriptor bases (built once; per k-step only a constant is added to the start field)
@@ -606,11 +609,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t dDO_mn = sdesc_sw128(smem_u32(sDO), HB / NBOX, 1024), dQ_mn = sdesc_sw128(smem_u32(sQ), 16384, 1024);
       const uint64_t dDS_mn = sdesc_sw128(smem_u32(sDS), 16384, 1024), dK_mn = sdesc_sw128(smem_u32(sK), 16384, 1024);
       auto kofs = [](int ks, uint32_t box_bytes) { return (uint32_t)((ks >> 2) * box_bytes + (ks & 3) * 32); };
-      auto issue_S = [&](int qs, int x) {  // S^T[x] = K Q_x^T  (Q_x = rows 64x.. of the Q stage)
+      // S^T = K Q^T for the whole 128-query tile in one N = 128 MMA chain: columns [0,64) are
+      // sub-item a, [64,128) sub-item b. (An N = 64 SS MMA is SMEM-read bound at 48 clk per
+      // K = 16 step vs 32 of tensor floor — bench_tools/mma_rate.cu — N = 128 runs at the floor.)
+      auto issue_S = [&](int qs) {
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
-          umma_ss_e(tbase + 64 * x, sdesc_add(dK_kmaj, kofs(ks, 16384)),
-                    sdesc_add(dQ_kmaj, qs * TB + 64 * x * 128 + kofs(ks, 16384)), idSP, ks > 0);
+          umma_ss_e(tbase, sdesc_add(dK_kmaj, kofs(ks, 16384)), sdesc_add(dQ_kmaj, qs * TB + kofs(ks, 16384)), idS,
+                    ks > 0);
+        umma_commit_e(&bars.s_full[0]);
+        umma_commit_e(&bars.s_full[1]);
       };
       auto issue_dP = [&](int slot, int x) {  // dP^T[x] = V dO_x^T
 #pragma unroll
@@ -631,41 +639,43 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     idKV, (!first || ks > 0) ? 1u : 0u);
       };
       // Issue order (program order of this warp = tensor-pipe order):
-      //   prologue: S(0,a) S(0,b) dP(0,a) dP(0,b) dV(0,a) dV(0,b) S(1,a) S(1,b)
-      //   tile t:   dK(t,a) dK(t,b) dQ(t) | dV(t+1,a) dV(t+1,b) | [dQ drained] dP(t+1,a) dP(t+1,b)
-      //             | S(t+2,a) S(t+2,b)
-      // dV(t+1) fills the pipe while dQ(t) is drained; the compute warps' P(t+1) runs under
-      // dK(t) / dQ(t). A dO half is released only after both of its readers (dV, dP).
+      //   prologue: S(0) dP(0,a) dP(0,b) dV(0,a) dV(0,b) S(1)
+      //   tile t:   dK(t,a) dK(t,b) dQ(t) | [dQ drained] dP(t+1,a) dP(t+1,b) | dV(t+1,a) dV(t+1,b)
+      //             | S(t+2)
+      // dP(t+1) goes ahead of dV(t+1) so the compute warps find it done when they finish P(t+1)
+      // (their dS phase then follows P without a wait); dV(t+1) runs under that dS phase.
+      // A dO half is released after its second reader (dV).
       auto slot_of = [](int t, int x) { return (2 * t + x) % 3; };
       auto use_of = [](int t, int x) { return ((2 * t + x) / 3) & 1; };
+      auto issue_dP_pair = [&](int t) {
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          mbar_wait(&bars.do_full[slot_of(t, x)], use_of(t, x));
+          tc_fence_after();
+          issue_dP(slot_of(t, x), x);
+          umma_commit_e(&bars.dp_full[x]);
+        }
+      };
+      auto issue_dV_pair = [&](int t) {
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          mbar_wait(&bars.p_full[x], t & 1);
+          TTT_TRACE_EV(0, 1 + x, t);
+          tc_fence_after();
+          issue_dV(slot_of(t, x), x, t == 0 && x == 0);
+          umma_commit_e(&bars.do_empty[slot_of(t, x)]);  // dP(t,x) was issued before: both readers done
+        }
+      };
       mbar_wait(&bars.kv_full, 0);
       mbar_wait(&bars.q_full[0], 0);
       tc_fence_after();
-      issue_S(0, 0);
-      umma_commit_e(&bars.s_full[0]);
-      issue_S(0, 1);
-      umma_commit_e(&bars.s_full[1]);
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        mbar_wait(&bars.do_full[slot_of(0, x)], use_of(0, x));
-        tc_fence_after();
-        issue_dP(slot_of(0, x), x);
-        umma_commit_e(&bars.dp_full[x]);
-      }
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        mbar_wait(&bars.p_full[x], 0);
-        tc_fence_after();
-        issue_dV(slot_of(0, x), x, x == 0);
-        umma_commit_e(&bars.do_empty[slot_of(0, x)]);  // dP(0,x) was issued before: both readers done
-      }
+      issue_S(0);
+      issue_dP_pair(0);
+      issue_dV_pair(0);
       if (n_items > 1) {
         mbar_wait(&bars.q_full[1], 0);
         tc_fence_after();
-        issue_S(1, 0);
-        umma_commit_e(&bars.s_full[0]);
-        issue_S(1, 1);
-        umma_commit_e(&bars.s_full[1]);
+        issue_S(1);
       }
       for (int t = 0; t < n_items; ++t) {
         const int qs = t & 1;
@@ -686,32 +696,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         umma_commit_e(&bars.ds_empty);
         TTT_TRACE_EV(0, 9, t);
         if (t + 1 < n_items) {
-          const int t1 = t + 1;
-#pragma unroll
-          for (int x = 0; x < 2; ++x) {  // dV(t+1, x): P^T(t+1, x) and the dO half are ready
-            mbar_wait(&bars.p_full[x], t1 & 1);
-            TTT_TRACE_EV(0, 1 + x, t1);
-            mbar_wait(&bars.do_full[slot_of(t1, x)], use_of(t1, x));
-            tc_fence_after();
-            issue_dV(slot_of(t1, x), x, false);
-          }
           mbar_wait(&bars.dq_empty, t & 1);  // dQ(t) drained: the dP^T buffers are free
           TTT_TRACE_EV(0, 5, t);
           tc_fence_after();
-#pragma unroll
-          for (int x = 0; x < 2; ++x) {
-            issue_dP(slot_of(t1, x), x);
-            umma_commit_e(&bars.dp_full[x]);
-            umma_commit_e(&bars.do_empty[slot_of(t1, x)]);
-          }
+          issue_dP_pair(t + 1);
           TTT_TRACE_EV(0, 6, t);
-          if (t + 2 < n_items) {  // S(t+2, x) over P^T(t+1, x), consumed by dV(t+1, x) above
+          issue_dV_pair(t + 1);
+          if (t + 2 < n_items) {  // S(t+2) over P^T(t+1), consumed by dV(t+1) above
             mbar_wait(&bars.q_full[(t + 2) & 1], ((t + 2) >> 1) & 1);
             tc_fence_after();
-            issue_S((t + 2) & 1, 0);
-            umma_commit_e(&bars.s_full[0]);
-            issue_S((t + 2) & 1, 1);
-            umma_commit_e(&bars.s_full[1]);
+            issue_S((t + 2) & 1);
             TTT_TRACE_EV(0, 10, t);
           }
         }
@@ -753,12 +747,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                          f2pack(l4.x, l4.y)), x0, x1);
           f2unpack(ffma2(f2pack(__uint_as_float(raw[4 * c4 + 2]), __uint_as_float(raw[4 * c4 + 3])), sl2x2,
                          f2pack(l4.z, l4.w)), x2, x3);
-          const float xs[4] = {x0, x1, x2, x3};
+          float ys[4];
+          if ((c4 & 3) == 3) {  // 1 in 4: 2^x on the FMA pipe (MUFU is the P phase's bottleneck)
+            ex2_emu2(x0, x1, ys[0], ys[1]);
+            ex2_emu2(x2, x3, ys[2], ys[3]);
+          } else {
+            ys[0] = ex2(x0);
+            ys[1] = ex2(x1);
+            ys[2] = ex2(x2);
+            ys[3] = ex2(x3);
+          }
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int c = 4 * c4 + e;
-            const float v = ex2(xs[e]);  // P = exp(S c - lse)
-            pr[c] = (full || c >= cmin) ? v : 0.f;
+            pr[c] = (full || c >= cmin) ? ys[e] : 0.f;  // P = exp(S c - lse)
           }
         }
       }

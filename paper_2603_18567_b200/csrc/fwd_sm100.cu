@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);     // O += P V, V MN-major
       const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ), 16, 1024), dK0 = sdesc_sw128(smem_u32(sK), 16, 1024);
       const uint64_t dV0 = sdesc_sw128(smem_u32(sV), 16384, 1024);
+      TTT_TRACE_DECL(0);
       auto issue_S = [&](int slot, int kst) {
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
