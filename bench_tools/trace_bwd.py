@@ -23,7 +23,7 @@ for _ in range(2):
     ttt.ttt_attn_bwd(desc, j, q, k, v, [], [], out, lse, do, dq, dk, dv, [], [], flags=0, workspace=ws, out_lo=olo)
 lib.ttt_debug_trace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
 names = {0: {1: "mma:got_p_a", 2: "mma:got_p_b", 3: "mma:got_ds_a", 4: "mma:got_ds_b", 5: "mma:got_dqempty", 6: "mma:dP_issued", 7: "mma:dK_a_issued", 8: "mma:dK_b_issued", 9: "mma:dQ_issued", 10: "mma:S_issued", 11: "mma:got_q", 12: "mma:got_do_a", 13: "mma:got_do_b"},
-         1: {1: "cmpA:got_s", 2: "cmpA:p_done", 3: "cmpA:got_dp", 4: "cmpA:ds_done", 5: "cmpA:s_loaded", 6: "cmpA:p_math_done", 7: "cmpA:got_dsempty"},
+         1: {1: "cmpA:got_s", 2: "cmpA:p_done", 3: "cmpA:got_dp", 4: "cmpA:ds_done", 5: "cmpA:s_loaded", 6: "cmpA:p_math_done", 7: "cmpA:got_dsempty", 8: "cmpA:got_acc", 9: "cmpA:epi_done", 10: "cmpA:epi_staged", 11: "cmpA:epi_bar", 12: "cmpA:epi_ld0"},
          2: {1: "dq:got_dq", 2: "dq:drained", 11: "prod:q_issue", 12: "prod:do_a_issue", 13: "prod:do_b_issue", 14: "obs:q_arrived", 15: "obs:do_a_arrived", 16: "obs:do_b_arrived"}}
 ev = []
 for role in range(3):
@@ -87,3 +87,8 @@ if "timeline" in sys.argv:
     for t, n, i in ev:
         if lo - 2000 <= t <= hi:
             print(f"{t - lo:7d}  {n:18s} item {i}")
+
+if "epi" in sys.argv:
+    for t, n, i in ev:
+        if n.startswith("cmpA:epi") or n == "cmpA:got_acc": print(f"{t - ev[0][0]:8d} {n}")
+    print("total clk", ev[-1][0] - ev[0][0])

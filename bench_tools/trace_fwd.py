@@ -17,10 +17,10 @@ out = torch.empty_like(q); olo = torch.empty_like(q); lse = torch.empty(s.batch,
 desc = ttt.make_desc(s.batch, s.seq_len, s.num_q_heads, s.num_kv_heads, s.head_dim)
 lib.ttt_debug_ftrace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
 for _ in range(2):
-    ttt.ttt_attn_fwd(desc, 0, q, k, v, [], [], out, lse, out_lo=olo)
+    ttt.ttt_attn_fwd(desc, 0, q, k, v, [], [], out, lse, out_lo=olo if 'nolo' not in sys.argv else None)
 lib.ttt_debug_ftrace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
 names = {0: {9: "mma:start", 8: "mma:got_q_k0", 1: "mma:got_v", 2: "mma:got_p0", 3: "mma:got_p1"},
-         1: {1: "s0:got_s", 2: "s0:p_done", 3: "s0:loop_end", 4: "s0:got_o", 5: "s0:epi_done"},
+         1: {1: "s0:got_s", 2: "s0:p_done", 3: "s0:loop_end", 4: "s0:got_o", 5: "s0:epi_done", 6: "s0:epi_math_done", 7: "s0:epi_bar", 8: "s0:tma_issued"},
          2: {1: "s1:got_s", 2: "s1:p_done"}}
 ev = []
 for role in range(3):

@@ -822,32 +822,50 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             (clock64() << 20) | ((unsigned long long)(16 + warp) << 12) | (unsigned long long)(t & 0xFFF);
 #endif
     }
-    // ---- dK, dV accumulators -> global (fp32 atomics: head splits and steps add up) ----
+    // ---- dK, dV accumulators -> global (fp32 adds in L2, so head splits and accumulated steps
+    // add up). TMEM rows (thread = key row) are staged in the operand smem (K / V / Q, free once
+    // acc_full follows the last MMA) and read back transposed, so each red.global.add.v4 covers
+    // two 256-B half-rows (4 lines) instead of 32 rows 4 KB apart (that scattered form took ~9.5k
+    // clk per CTA; a TMA bulk reduce-add of the staged tile ~6.5k, being bound near 20 B/clk).
+    // Each warp reads back only the rows it staged (__syncwarp). Rows k >= T are skipped.
     mbar_wait(&bars.acc_full, 0);
+    if (threadIdx.x == 128) TTT_TRACE_EV(1, 8, 0);
     tc_fence_after();
-    // tcgen05.ld is warp-collective (.sync.aligned): every lane loads, only rows k < T store
-    const bool store = k < T;
-    const size_t off = (((size_t)b * p.L + (store ? k : 0)) * p.Hkv + g) * D;
-    const int cbeg = x * (D / 2);
+    constexpr int NCH = D / 64;  // 32-column chunks per half
+    uint8_t* stg = smem + x * 65536 + quad * 4096;  // box i of this half: stg + i * 16384, rows of this warp
 #pragma unroll 1
-    for (int c0 = cbeg; c0 < cbeg + D / 2; c0 += 32) {
+    for (int i = 0; i < 2 * NCH; ++i) {  // boxes: dV chunks | dK chunks of this half's D / 2 columns
+      const int c0 = x * (D / 2) + (i % NCH) * 32;
       uint32_t raw[32];
-      tmem_ld32(tbase + lane_off + 256 + c0, raw);
-      if (store) {
+      tmem_ld32(tbase + lane_off + (i < NCH ? 256 : 384) + c0, raw);
+      const float sc = i < NCH ? 1.f : p.scale;
+      uint8_t* rowp = stg + i * 16384 + lane * 128;
 #pragma unroll
-        for (int e = 0; e < 32; e += 4)
-          red_add_v4(p.dv + off + c0 + e, __uint_as_float(raw[e]), __uint_as_float(raw[e + 1]),
-                     __uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3]));
-      }
-      tmem_ld32(tbase + lane_off + 384 + c0, raw);
-      if (store) {
-        const float c = p.scale;
-#pragma unroll
-        for (int e = 0; e < 32; e += 4)
-          red_add_v4(p.dk + off + c0 + e, c * __uint_as_float(raw[e]), c * __uint_as_float(raw[e + 1]),
-                     c * __uint_as_float(raw[e + 2]), c * __uint_as_float(raw[e + 3]));
+      for (int k4 = 0; k4 < 8; ++k4)
+        *reinterpret_cast<float4*>(rowp + ((k4 ^ (lane & 7)) << 4)) =
+            make_float4(sc * __uint_as_float(raw[4 * k4]), sc * __uint_as_float(raw[4 * k4 + 1]),
+                        sc * __uint_as_float(raw[4 * k4 + 2]), sc * __uint_as_float(raw[4 * k4 + 3]));
+    }
+    __syncwarp();
+    {
+      constexpr int LPR = D / 8;        // lanes per half-row (16 B each): 16 at D = 128, 8 at D = 64
+      constexpr int RPI = 32 / LPR;     // half-rows per instruction
+      const int sub = lane / LPR, c = lane % LPR;  // 16-B chunk c of the half-row
+#pragma unroll 1
+      for (int tsr = 0; tsr < 2; ++tsr) {  // 0: dV, 1: dK
+        float* dst = tsr == 0 ? p.dv : p.dk;
+#pragma unroll 4
+        for (int r0 = 0; r0 < 32; r0 += RPI) {
+          const int lr = r0 + sub, kk = kt * kTile + quad * 32 + lr;
+          const float4 val = *reinterpret_cast<const float4*>(stg + (tsr * NCH + c / 8) * 16384 + lr * 128 +
+                                                              (((c & 7) ^ (lr & 7)) << 4));
+          if (kk < T)
+            red_add_v4(dst + (((size_t)b * p.L + kk) * p.Hkv + g) * D + x * (D / 2) + c * 4, val.x, val.y, val.z,
+                       val.w);
+        }
       }
     }
+    if (threadIdx.x == 128) TTT_TRACE_EV(1, 9, 0);
   } else if (warp < 4) {
     // ================= dQ drain (warps 0-3, thread = query row) =================
     // TMEM -> registers (scaled by c) -> warp-private SW128 staging -> TMA reduce-add into
@@ -890,7 +908,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
     }
-    if (lane == 0) bulk_wait0();
+    if (lane == 0) bulk_wait_read0();
   } else {
     reg_dealloc<24>();  // warps 14-15: idle
   }

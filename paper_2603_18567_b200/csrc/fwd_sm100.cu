@@ -395,8 +395,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
+      if (threadIdx.x == 0) TTT_TRACE_EV(1, 6, 0);
       fence_async_smem();
       named_bar_sync(1 + slot, 128);
+      if (threadIdx.x == 0) TTT_TRACE_EV(1, 7, 0);
       if (row == 0) {
 #pragma unroll
         for (int bx = 0; bx < D / 64; ++bx) {
@@ -404,6 +406,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (p.out_lo) tma_store_4d(&maps.out_lo, st_lo + bx * 16384, bx * 64, h, qt * kTile, b);
         }
         bulk_commit();
+        if (threadIdx.x == 0) TTT_TRACE_EV(1, 8, 0);
         bulk_wait_read0();  // smem must stay valid until the bulk engine has read it
       }
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 5, 0);
