@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tmem_ld128(tS, raw);
         const int kv0 = n * kTile;
         const bool partial = (n == qt) || (kv0 + kTile > T);
-        // row max of the raw scores (scale > 0 commutes with max): 8 independent chains
+        // row max of the raw scores (scale > 0 commutes with max): 8 independent chains of
+        // 3-input max (FMNMX3), two new columns per instruction
         float mx8[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
@@ -250,12 +251,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int c = 0; c < 128; ++c) {
             const float x = c < lim ? __uint_as_float(raw[c]) : -INFINITY;
             raw[c] = __float_as_uint(x);
-            mx8[c & 7] = fmaxf(mx8[c & 7], x);
           }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 128; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(raw[c]));
         }
+#pragma unroll
+        for (int c = 0; c < 128; c += 16)
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            mx8[u] = fmax3(mx8[u], __uint_as_float(raw[c + u]), __uint_as_float(raw[c + 8 + u]));
         const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
         const float m_new = fmaxf(m_run, mx);
