@@ -5,7 +5,10 @@
 
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <mutex>
+#include <queue>
+#include <vector>
 
 #include "../../include/ttt_attn.h"
 #include "ttt_params.cuh"
@@ -118,6 +121,59 @@ void fill_common(Params& p, const ttt_attn_desc* d, int step) {
   p.scale_log2 = p.scale * 1.4426950408889634f;
   for (int b = 0; b < p.B; ++b) p.seq_lens[b] = d->seq_lens ? d->seq_lens[b] : p.L;
 }
+
+}  // namespace
+
+namespace tttk {
+int pick_order_batch(int ngroups, int nranks, int copies, const double* len_of_rank, double overhead,
+                     double bytes_per_group) {
+  struct Key {
+    int ng, nr, cp;
+    double l0, l1, ov, bpg;
+    int best;
+  };
+  static std::mutex mu;
+  static Key cache[8];
+  static int ncache = 0;
+  const double l0 = len_of_rank[0], l1 = len_of_rank[nranks - 1];
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < ncache; ++i) {
+      const Key& k = cache[i];
+      if (k.ng == ngroups && k.nr == nranks && k.cp == copies && k.l0 == l0 && k.l1 == l1 && k.ov == overhead &&
+          k.bpg == bytes_per_group)
+        return k.best;
+    }
+  }
+  constexpr int kSMs = 148;
+  int best = 1;
+  double best_ms = 0.0;
+  for (int bsz = 1; bsz <= std::min(ngroups, 32); ++bsz) {
+    if (bsz > 1 && bsz * bytes_per_group > 80e6) break;
+    std::priority_queue<double, std::vector<double>, std::greater<double>> sm;
+    for (int i = 0; i < kSMs; ++i) sm.push(0.0);
+    double ms = 0.0;
+    for (int g0 = 0; g0 < ngroups; g0 += bsz)
+      for (int r = 0; r < nranks; ++r)
+        for (int g = g0; g < std::min(ngroups, g0 + bsz); ++g)
+          for (int c = 0; c < copies; ++c) {
+            const double t = sm.top() + len_of_rank[r] + overhead;
+            sm.pop();
+            sm.push(t);
+            ms = std::max(ms, t);
+          }
+    if (bsz == 1 || ms < best_ms * 0.995) {  // a larger batch must win clearly (it costs L2 reuse)
+      best = bsz;
+      best_ms = ms;
+    }
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache[ncache < 8 ? ncache++ : 7] = Key{ngroups, nranks, copies, l0, l1, overhead, bytes_per_group, best};
+  return best;
+}
+}  // namespace tttk
+
+namespace {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 

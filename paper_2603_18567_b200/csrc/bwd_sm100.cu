@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "ptx_sm100.cuh"
 #include "ttt_params.cuh"
@@ -516,8 +517,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // kv head run together, so its Q / dO tiles and dq_acc rows stay hot in L2. (A global
   // longest-first order — kv tile slowest — measured slower: 5.3 vs 5.26 ms bwd, 2.73-2.85 vs
   // 2.63-2.66 ms fwd per unroll in an interleaved A/B, bench_tools/ab.sh.)
+#ifdef TTT_ORDER_GROUP
   const int kt = (int)blockIdx.x % p.nqt;
   const int grp = (int)blockIdx.x / p.nqt;
+#else
+  // Batched longest-first: kv heads in batches of p.order_batch; inside a batch kv tile slowest (the
+  // longest CTAs, kt = 0, first), then the batch's heads. The last batch ends with short CTAs (a
+  // small tail), while one batch's Q / dO / dq_acc (~8 x 8 MB at the Llama shape) stay in L2.
+  const int ngrp = p.B * p.Hkv * p.head_split;
+  const int bsz = p.order_batch * p.nqt;
+  const int bat = (int)blockIdx.x / bsz, gbase = bat * p.order_batch;
+  const int gb = min(p.order_batch, ngrp - gbase), rr = (int)blockIdx.x - bat * bsz;
+  const int kt = rr / gb;
+  const int grp = gbase + rr % gb;
+#endif
   const int hs = grp % hsplit;
   const int g = (grp / hsplit) % p.Hkv;
   const int b = grp / (hsplit * p.Hkv);
@@ -972,6 +985,14 @@ template <int D>
 cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st) {
   Params p = p_in;
   p.head_split = pick_head_split(p);
+  {  // CTA order: CTA kt of a group runs (nqt - kt) items of G / head_split heads; ~4.5k clk per
+     // item and ~12k of fixed cost (measured traces); a group's Q, dO, dq_acc: 8 B per q element
+    std::vector<double> len(p.nqt);
+    const int nh = p.G / p.head_split;
+    for (int r = 0; r < p.nqt; ++r) len[r] = (double)nh * (p.nqt - r) * 4.5;
+    p.order_batch = pick_order_batch(p.B * p.Hkv * p.head_split, p.nqt, 1, len.data(), 12.0,
+                                     (double)nh * p.L * D * 8);
+  }
   // 1. pre-pass (TMA-staged, persistent, warp-specialised)
   {
     PreLayout lay;

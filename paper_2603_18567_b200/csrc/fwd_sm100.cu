@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "ptx_sm100.cuh"
 #include "ttt_params.cuh"
@@ -73,9 +74,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int npairs = (p.G + 1) >> 1;
   const int hp = (int)blockIdx.x % npairs;
   const int t_ = (int)blockIdx.x / npairs;
+#ifdef TTT_ORDER_GROUP
   const int qt = p.nqt - 1 - t_ % p.nqt;
   const int g = (t_ / p.nqt) % p.Hkv;
   const int b = t_ / (p.nqt * p.Hkv);
+#else
+  // batched longest-first: (b, g) groups in batches of p.order_batch, q tile slowest inside a batch
+  const int ngrp = p.B * p.Hkv, bsz = p.order_batch * p.nqt;
+  const int bat = t_ / bsz, gbase = bat * p.order_batch;
+  const int gb = min(p.order_batch, ngrp - gbase), rr = t_ - bat * bsz;
+  const int qt = p.nqt - 1 - rr / gb;
+  const int gi = gbase + rr % gb;
+  const int g = gi % p.Hkv;
+  const int b = gi / p.Hkv;
+#endif
   const int h0 = g * p.G + 2 * hp;
   const bool has1 = (2 * hp + 1) < p.G;
   const int T = p.seq_lens[b];
@@ -671,7 +683,14 @@ bool diag_layout(const Params& p, int D, DiagLayout* lay) {
 }
 
 template <int D>
-cudaError_t launch_fwd_d(const Params& p, const FwdMaps& maps, const DiagMaps& dmaps, cudaStream_t st) {
+cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps& dmaps, cudaStream_t st) {
+  Params p = p_in;
+  {  // CTA order: the CTA of q tile qt runs qt + 1 kv tiles (~3.3k clk each) plus ~7k clk of fixed
+     // cost (measured traces); a (b, g) group's K / V: 4 B per kv element
+    std::vector<double> len(p.nqt);
+    for (int r = 0; r < p.nqt; ++r) len[r] = (double)(p.nqt - r) * 3.3;
+    p.order_batch = pick_order_batch(p.B * p.Hkv, p.nqt, (p.G + 1) / 2, len.data(), 7.0, (double)p.L * D * 4);
+  }
   const int smem = 6 * kTile * D * 2 + 1024;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {

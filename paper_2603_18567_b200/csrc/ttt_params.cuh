@@ -12,12 +12,14 @@ namespace tttk {
 
 constexpr int kTile = 128;  // q-tile rows = kv-tile rows (UMMA M = N = 128)
 
+
 struct Params {
   int B, L, Hq, Hkv, D, G;  // G = Hq / Hkv (GQA group size, kv head = h / G)
   int step;                 // j: number of step-list entries (diagonal keys) used
   int accumulate;           // bwd: += into dk/dv
   int nqt;                  // L / 128 (tensor-core path)
   int head_split;           // bwd: CTAs per (b, kv head, kv tile) sharing the G q-heads
+  int order_batch;          // CTA order: (b, kv head[, head subset]) groups per longest-first batch
   float scale;              // c
   float scale_log2;         // c * log2(e)
   // forward / shared inputs
@@ -72,5 +74,13 @@ enum KernelKind {
   kKindBwdConvert = 4, kKindCheckFwd = 5, kKindCheckBwd = 6, kKindZero = 7
 };
 void prof_mark(int kind, bool start, cudaStream_t st);
+
+// Host: CTA-order batch size for a non-persistent grid of `ngroups` groups x `nlen` CTAs whose
+// length is (len_unit(i) + overhead) for the i-th CTA of a group in longest-first order. Picks the
+// batch (groups interleaved longest-first inside a batch) with the smallest simulated makespan
+// over 148 greedy SMs, among batches whose L2 working set stays under ~80 MB.
+// `copies` CTAs share each (group, rank); len_of_rank[i] in units of one work item.
+int pick_order_batch(int ngroups, int nranks, int copies, const double* len_of_rank, double overhead,
+                     double bytes_per_group);
 
 }  // namespace tttk
