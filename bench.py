@@ -37,6 +37,7 @@ METRIC = "TTT attn fwd+bwd tokens/sec (Llama-3.1-8B EAGLE-3 draft shape, ttt_ste
 UNIT = "tokens/s"
 # EAGLE-3 draft layer of Llama-3.1-8B: fc 3d->d, q/k/v/o, MLP 14336, norms, 32000 head
 DRAFT_PARAMS = 424_700_000
+LOSS_ROWS, LOSS_VOCAB = 8 * 2048, 32000  # one TTT step's rows of the Llama draft, 32000-token draft vocab
 
 
 def alg_pairs(s: Shape, seq_lens=None):
@@ -319,6 +320,8 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
     }
     if world == 1 and not args.no_e2e:
         line["e2e"] = run_e2e(u, stream, args, shape)
+    if not args.no_loss:
+        line["next_rows"] = {"loss_inplace": run_loss(args, stream, peaks, world)}
     if rank == 0 and world == 1 and not args.no_cpu:
         n, threads, run = oracle_sample(shape, target_s=15.0)
         sec = run(n)
@@ -329,6 +332,61 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
                        f"tokens-equivalent = {n}")}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def run_loss(args, stream, peaks, world: int):
+    """SURVEY.md §8(f) NEXT #1, measured beside the headline (not part of its step): the masked
+    soft-label loss + Alg. 3 in-place backward (include/ttt_loss.h), one fused pass per TTT step,
+    on one TTT step's rows of the Llama draft (B L = 16384 rows x 32000 vocab, bf16; z + p = 2.1 GB,
+    larger than L2). The timed loop re-runs on the buffer the previous pass overwrote (the cost is
+    data-independent: every element takes one exp2 either way)."""
+    import paper_2603_18567_b200 as ttt
+    rows, vocab = LOSS_ROWS, LOSS_VOCAB
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev).manual_seed(77)
+    z = (torch.randn((rows, vocab), device=dev, generator=g) * 3).to(torch.bfloat16)
+    p = torch.rand((rows, vocab), device=dev, generator=g) ** 8
+    p = (p / p.sum(1, keepdim=True)).to(torch.bfloat16)
+    mask = torch.ones(rows, dtype=torch.uint8, device=dev)
+    stats = torch.empty(2, dtype=torch.float64, device=dev)
+    lse = torch.empty(rows, dtype=torch.float32, device=dev)
+    d = ttt.loss_desc_for(z)
+    ws = torch.empty(ttt.ttt_loss_workspace_size(d), dtype=torch.uint8, device=dev)
+
+    def one():
+        ttt.ttt_loss_fwd_bwd_inplace(d, z, p, mask, stats, ws, lse=lse, stream=stream)
+
+    for _ in range(max(args.warmup, 3)):
+        one()
+    torch.cuda.synchronize()
+    n = max(args.steps, 10)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    ttt.ttt_attn_profile_begin()
+    for _ in range(n):
+        one()
+    torch.cuda.synchronize()
+    kern = ttt.ttt_attn_profile_end()
+    k_ms, k_n = kern["ttt_loss_kernel"]
+    avg = k_ms / k_n
+    # algorithmic bytes per launch: read z, read p, write dL/dz over z (2 B each) + mask, lse, row loss
+    alg_bytes = rows * vocab * 2 * 3 + rows * (1 + 4 + 4)
+    achieved = alg_bytes / (avg / 1e3) / 1e9
+    peak = peaks["hbm_gbs"]
+    return {
+        "workload": f"{rows} rows x {vocab} vocab, bf16, fused loss + in-place grad (TTT_LOSS_MEAN), one TTT step",
+        "ms_per_call": ms, "rows_per_s": rows * world / (ms / 1e3), "unit": "rows/s",
+        "launches_per_call": sum(c for _, c in kern.values()) // n,
+        "roofline": {"kernel": "ttt_loss_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "peak_kind": f"HBM ({peaks['source']})",
+                     "avg_launch_ms": avg, "algorithmic_bytes_per_launch": alg_bytes,
+                     "traffic": ncu_traffic("ttt_loss_kernel")},
+    }
 
 
 def run_e2e(u: Unroll, stream, args, shape: Shape):
@@ -383,6 +441,7 @@ def main():
     ap.add_argument("--config", default="llama8b", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-loss", action="store_true", help="skip the §8(f) loss-kernel measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3

@@ -141,7 +141,7 @@ int ttt_attn_bwd(const ttt_attn_desc* desc, int step,
  * caller's arrays (n_kinds entries, kinds listed by ttt_attn_kernel_name),
  * and disarms. Returns the number of kinds filled, or < 0 on error.
  * This is the only library state; computations never depend on it. */
-#define TTT_KERNEL_KINDS 8
+#define TTT_KERNEL_KINDS 10
 int ttt_attn_profile_begin(void);
 int ttt_attn_profile_end(double* ms_by_kind, int* launches_by_kind, int n_kinds);
 const char* ttt_attn_kernel_name(int kind);

@@ -42,6 +42,14 @@ class Desc(ctypes.Structure):
     ]
 
 
+class LossDesc(ctypes.Structure):
+    """ttt_loss_desc (include/ttt_loss.h)."""
+    _fields_ = [("rows", ctypes.c_int64), ("vocab", ctypes.c_int32), ("dtype", ctypes.c_int32)]
+
+
+TTT_LOSS_MEAN = 1
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -66,6 +74,16 @@ def _load():
     lib.ttt_attn_profile_end.restype = i
     lib.ttt_attn_kernel_name.argtypes = [i]
     lib.ttt_attn_kernel_name.restype = ctypes.c_char_p
+    pl = ctypes.POINTER(LossDesc)
+    f = ctypes.c_float
+    lib.ttt_loss_workspace_size.argtypes = [pl]
+    lib.ttt_loss_workspace_size.restype = sz
+    lib.ttt_loss_fwd.argtypes = [pl, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.ttt_loss_fwd.restype = i
+    lib.ttt_loss_bwd_inplace.argtypes = [pl, vp, vp, vp, vp, f, u, vp, vp, sz, vp]
+    lib.ttt_loss_bwd_inplace.restype = i
+    lib.ttt_loss_fwd_bwd_inplace.argtypes = [pl, vp, vp, vp, vp, f, u, vp, vp, vp, vp, sz, vp]
+    lib.ttt_loss_fwd_bwd_inplace.restype = i
     return lib
 
 
@@ -125,7 +143,7 @@ def _check(code: int):
         raise TTTError(code, ttt_attn_strerror(code))
 
 
-TTT_KERNEL_KINDS = 8
+TTT_KERNEL_KINDS = 10
 
 
 def ttt_attn_kernel_name(kind: int) -> str:
@@ -172,3 +190,44 @@ def ttt_attn_bwd(desc: Desc, step: int, q, k_base, v_base, k_steps, v_steps, out
                              _ptr(lse), _ptr(dout), _ptr(dq), _ptr(dk_base), _ptr(dv_base),
                              _ptr_list(dk_steps[:step]), _ptr_list(dv_steps[:step]), int(flags),
                              _ptr(workspace), ws_bytes, _stream(stream)))
+
+
+# ---- masked soft-label log-softmax loss + Alg. 3 in-place backward (include/ttt_loss.h) ----
+
+def loss_desc_for(z: torch.Tensor) -> LossDesc:
+    """LossDesc from logits z [..., V] (rows = product of the leading dims)."""
+    d = LossDesc()
+    d.vocab = int(z.shape[-1])
+    d.rows = int(z.numel() // max(d.vocab, 1))
+    d.dtype = TTT_FP32_CHECK if z.dtype == torch.float32 else TTT_BF16
+    return d
+
+
+def ttt_loss_workspace_size(desc: LossDesc) -> int:
+    return int(_lib.ttt_loss_workspace_size(ctypes.byref(desc)))
+
+
+def _nbytes(t) -> int:
+    return 0 if t is None else t.numel() * t.element_size()
+
+
+def ttt_loss_fwd(desc: LossDesc, z, p, mask, stats, workspace, lse=None, stream=None) -> None:
+    """Enqueue ttt_loss_fwd: stats (fp64 [2]) = {masked mean loss, masked-row count}."""
+    _check(_lib.ttt_loss_fwd(ctypes.byref(desc), _ptr(z), _ptr(p), _ptr(mask), _ptr(lse), _ptr(stats),
+                             _ptr(workspace), _nbytes(workspace), _stream(stream)))
+
+
+def ttt_loss_bwd_inplace(desc: LossDesc, z, p, mask, workspace, g_scale: float = 1.0, flags: int = TTT_LOSS_MEAN,
+                         g_rows=None, grad=None, stream=None) -> None:
+    """Enqueue Alg. 3: z <- dL/dz in place (or into `grad` when given)."""
+    _check(_lib.ttt_loss_bwd_inplace(ctypes.byref(desc), _ptr(z), _ptr(p), _ptr(mask), _ptr(g_rows),
+                                     float(g_scale), int(flags), _ptr(grad), _ptr(workspace), _nbytes(workspace),
+                                     _stream(stream)))
+
+
+def ttt_loss_fwd_bwd_inplace(desc: LossDesc, z, p, mask, stats, workspace, g_scale: float = 1.0,
+                             flags: int = TTT_LOSS_MEAN, g_rows=None, grad=None, lse=None, stream=None) -> None:
+    """Enqueue the fused loss + Alg. 3 backward (one pass: z, p read once, gradient written over z)."""
+    _check(_lib.ttt_loss_fwd_bwd_inplace(ctypes.byref(desc), _ptr(z), _ptr(p), _ptr(mask), _ptr(g_rows),
+                                         float(g_scale), int(flags), _ptr(grad), _ptr(lse), _ptr(stats),
+                                         _ptr(workspace), _nbytes(workspace), _stream(stream)))

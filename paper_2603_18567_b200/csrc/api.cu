@@ -281,7 +281,8 @@ int ttt_attn_profile_end(double* ms_by_kind, int* launches_by_kind, int n_kinds)
 const char* ttt_attn_kernel_name(int kind) {
   static const char* names[TTT_KERNEL_KINDS] = {
       "ttt_fwd_diag_kernel", "ttt_fwd_sm100_kernel", "ttt_bwd_pre_kernel", "ttt_bwd_sm100_kernel",
-      "ttt_bwd_dq_convert_kernel", "fwd_check_kernel", "bwd_check_kernel", "zero_f32_kernel"};
+      "ttt_bwd_dq_convert_kernel", "fwd_check_kernel", "bwd_check_kernel", "zero_f32_kernel",
+      "ttt_loss_kernel", "ttt_loss_aux_kernel"};
   return (kind >= 0 && kind < TTT_KERNEL_KINDS) ? names[kind] : "unknown";
 }
 

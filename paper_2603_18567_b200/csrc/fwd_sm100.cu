@@ -27,6 +27,11 @@
 #include "ptx_sm100.cuh"
 #include "ttt_params.cuh"
 
+// Pairs (c mod 8) of a full tile whose exp2 runs as an FMA-pipe polynomial instead of MUFU.
+#ifndef TTT_FWD_EMU_MASK
+#define TTT_FWD_EMU_MASK 0x88
+#endif
+
 namespace tttk {
 #ifdef TTT_TRACE
 __device__ unsigned long long g_ttt_ftrace[4][kTraceCap];
@@ -312,13 +317,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
               pk[cc] = pack_bf16(e0, e1);
             }
-          } else {  // full tile: every 4th pair on the FMA pipe (MUFU ex2 is the co-bottleneck)
+          } else {  // full tile: the pairs TTT_FWD_EMU_MASK selects (of every 8) on the FMA pipe
+                    // (MUFU ex2 is the co-bottleneck)
 #pragma unroll
             for (int cc = 0; cc < 32; ++cc) {
               const int c = hf * 32 + cc;
               float x0, x1, e0, e1;
               f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
-              if ((c & 3) == 3) {
+              if ((TTT_FWD_EMU_MASK >> (c & 7)) & 1) {
                 ex2_emu2(x0, x1, e0, e1);
               } else {
                 e0 = ex2(x0);

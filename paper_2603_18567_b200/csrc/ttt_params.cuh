@@ -71,7 +71,8 @@ struct BwdMaps {
 // ttt_attn_profile_begin() armed the calling thread; no-op otherwise.
 enum KernelKind {
   kKindFwdDiag = 0, kKindFwdMain = 1, kKindBwdPre = 2, kKindBwdMain = 3,
-  kKindBwdConvert = 4, kKindCheckFwd = 5, kKindCheckBwd = 6, kKindZero = 7
+  kKindBwdConvert = 4, kKindCheckFwd = 5, kKindCheckBwd = 6, kKindZero = 7,
+  kKindLoss = 8, kKindLossAux = 9
 };
 void prof_mark(int kind, bool start, cudaStream_t st);
 

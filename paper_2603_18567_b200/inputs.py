@@ -119,3 +119,56 @@ def sample_rows(shape: Shape, n_per_head: int, seed: int) -> np.ndarray:
             sel[b, h, 0] = True
             sel[b, h, shape.seq_len - 1] = True
     return sel
+
+
+# ---- loss inputs (recipe in DESIGN.md §4) ----
+
+# Llama-3.1-8B EAGLE-3 draft: 32000-token draft vocabulary; one row per
+# (sequence, position) of a TTT step: B * L = 8 * 2048 rows.
+LOSS_CONFIGS = {
+    "tiny": (128, 1000),
+    "llama8b": (8 * 2048, 32000),
+}
+
+
+@dataclass
+class LossCase:
+    z: torch.Tensor       # [N, V] logits, storage dtype (CPU)
+    p: torch.Tensor       # [N, V] target probabilities, storage dtype (CPU)
+    mask: torch.Tensor    # [N] uint8 loss-position mask
+    g_rows: torch.Tensor  # [N] fp32 per-row weights
+
+
+def make_loss_case(rows: int, vocab: int, dtype: torch.dtype = torch.bfloat16, seed: int = 0,
+                   z_scale: float = 3.0, mask_mode: str = "padded") -> LossCase:
+    """Seeded loss inputs: draft logits z ~ N(0, z_scale^2); target rows p = lam e_k + (1 - lam) d
+    with a random top token k, lam ~ U[0.3, 0.95] and a heavy tail d = u^8 / sum(u^8),
+    u ~ U(0, 1) (one dominant token plus a long tail, like a language model's next-token
+    distribution; stored after rounding, so rows sum to 1 only up to the storage rounding);
+    mask: "all", or "padded" = the last U[0, rows/4) rows plus ~10% scattered rows false
+    (padding and non-assistant positions); per-row weights g_rows ~ U[0.5, 1.5).
+    Seeds: z `seed`, p `seed+1`, mask / weights `seed+2`. Drawn in row chunks (bounded memory)."""
+    rz = np.random.default_rng(seed)
+    rp = np.random.default_rng(seed + 1)
+    z = torch.empty((rows, vocab), dtype=dtype)
+    p = torch.empty((rows, vocab), dtype=dtype)
+    chunk = max(1, (1 << 26) // vocab)
+    for r0 in range(0, rows, chunk):
+        n = min(chunk, rows - r0)
+        z[r0:r0 + n] = to_storage(_normal(rz, (n, vocab), z_scale), dtype)
+        lam = rp.uniform(0.3, 0.95, size=n).astype(np.float32)
+        top = rp.integers(0, vocab, size=n)
+        d = rp.random((n, vocab), dtype=np.float32) ** 8
+        d *= ((1.0 - lam) / d.sum(axis=1, dtype=np.float64)).astype(np.float32)[:, None]
+        d[np.arange(n), top] += lam
+        p[r0:r0 + n] = to_storage(d, dtype)
+    rm = np.random.default_rng(seed + 2)
+    mask = np.ones(rows, dtype=np.uint8)
+    if mask_mode == "padded":
+        pad = int(rm.integers(0, max(rows // 4, 1)))
+        mask[rows - pad:] = 0
+        mask[rm.random(rows) < 0.1] = 0
+        if mask.sum() == 0:
+            mask[0] = 1
+    g_rows = rm.uniform(0.5, 1.5, size=rows).astype(np.float32)
+    return LossCase(z, p, torch.from_numpy(mask), torch.from_numpy(g_rows))

@@ -18,13 +18,14 @@ def _declared_functions():
     for fn in os.listdir(os.path.join(ROOT, "include")):
         if fn.endswith(".h"):
             src = open(os.path.join(ROOT, "include", fn)).read()
-            names += re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(ttt_attn_\w+)\s*\(", src, re.M)
+            names += re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(ttt_(?:attn|loss)_\w+)\s*\(", src, re.M)
     return sorted(set(names))
 
 
 def test_header_symbols_exported():
     names = _declared_functions()
-    assert {"ttt_attn_fwd", "ttt_attn_bwd", "ttt_attn_workspace_size", "ttt_attn_strerror"} <= set(names)
+    assert {"ttt_attn_fwd", "ttt_attn_bwd", "ttt_attn_workspace_size", "ttt_attn_strerror",
+            "ttt_loss_fwd", "ttt_loss_bwd_inplace", "ttt_loss_fwd_bwd_inplace", "ttt_loss_workspace_size"} <= set(names)
     lib = ctypes.CDLL(_lib.LIB_PATH)
     for n in names:
         assert hasattr(lib, n), n
@@ -87,3 +88,59 @@ def test_workspace_size():
     assert ws >= rows * 4 * 2 + rows * 128 * 4
     assert ttt.ttt_attn_workspace_size(d, 6, False) == 0
     assert ttt.ttt_attn_workspace_size(ttt.make_desc(8, 2048, 32, 8, 96), 0, True) == 0
+
+
+def _loss_desc(rows=16, vocab=32000, dtype=ttt.TTT_BF16):
+    d = ttt.LossDesc()
+    d.rows, d.vocab, d.dtype = rows, vocab, dtype
+    return d
+
+
+@pytest.mark.parametrize("kw,call,code", [
+    (dict(rows=0), "fwd", 1), (dict(vocab=1), "fwd", 1), (dict(dtype=7), "fwd", 1),
+    (dict(vocab=262152), "fwd", 2),            # beyond the register-resident row capacity
+    (dict(vocab=131076, dtype=1), "bwd", 2),
+    (dict(vocab=32769), "bwd", 2),             # odd vocab (element path) capacity 32768
+    (dict(), "ws_small", 6), (dict(), "ws_misaligned", 4), (dict(), "flags", 1),
+    (dict(), "no_stats", 1), (dict(vocab=33), "z_odd", 4),
+])
+def test_loss_validation_codes(kw, call, code):
+    d = _loss_desc(**kw)
+    ws_n = ttt.ttt_loss_workspace_size(d) if call not in ("fwd",) or code != 1 else 0
+    ws_n = max(ws_n, 4096)
+    z, p, st, m = FakeT(0x10000000), FakeT(0x20000000), FakeT(0x30000000), FakeT(0x40000000)
+    ws = FakeT(0x50000000)
+
+    class WS(FakeT):
+        def __init__(self, ptr, n):
+            super().__init__(ptr)
+            self.n = n
+
+        def numel(self):
+            return self.n
+
+        def element_size(self):
+            return 1
+    wsb = WS(0x50000000, ws_n)
+    with pytest.raises(ttt.TTTError) as e:
+        if call == "fwd":
+            ttt.ttt_loss_fwd(d, z, p, m, st, wsb)
+        elif call == "bwd":
+            ttt.ttt_loss_bwd_inplace(d, z, p, m, wsb)
+        elif call == "ws_small":
+            ttt.ttt_loss_fwd(d, z, p, m, st, WS(0x50000000, 64))
+        elif call == "ws_misaligned":
+            ttt.ttt_loss_fwd(d, z, p, m, st, WS(0x50000008, ws_n + 64))
+        elif call == "flags":
+            ttt.ttt_loss_bwd_inplace(d, z, p, m, wsb, flags=6)
+        elif call == "no_stats":
+            ttt.ttt_loss_fwd(d, z, p, m, None, wsb)
+        elif call == "z_odd":
+            ttt.ttt_loss_bwd_inplace(d, FakeT(0x10000001), p, m, wsb)
+    assert e.value.code == code
+    del ws
+
+
+def test_loss_workspace_size():
+    assert ttt.ttt_loss_workspace_size(_loss_desc(rows=1000)) >= 1000 * 4
+    assert ttt.ttt_loss_workspace_size(_loss_desc(rows=0)) == 0

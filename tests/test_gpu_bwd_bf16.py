@@ -94,7 +94,7 @@ def test_bwd_bf16_gradient_identities(cuda_ok):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg", ["llama8b", "qwen235b"])
+@pytest.mark.parametrize("cfg", ["llama8b", "qwen235b", "longctx"])
 def test_bwd_bf16_full_size_row_subset(cuda_ok, cfg):
     shape = CONFIGS[cfg]
     case = make_case(shape, dtype=torch.bfloat16, seed=0, lens="full", steps=1)
@@ -114,3 +114,38 @@ def test_bwd_bf16_full_size_row_subset(cuda_ok, cfg):
     _check_grads(cfg, dq, g, og, j, mask_q=selq)
     # rows with dO = 0 have dS = 0 everywhere -> dq exactly 0
     assert np.abs(np32(dq)[~selq]).max() == 0.0
+
+
+def test_bwd_bf16_shrinking_lengths_per_step(cuda_ok):
+    """Variant of reading R6: step j passes T_b - j
+    (labels of the last j positions do not exist) through the per-call seq_lens; one
+    unroll in reverse order with accumulated dK/dV against the per-step oracle sums."""
+    import paper_2603_18567_b200 as ttt
+    shape = Shape(2, 384, 8, 2, 128, 4)
+    case = make_case(shape, dtype=torch.bfloat16, seed=5, lens="ragged")
+    dc = DeviceCase(case)
+    S = shape.ttt_steps
+    acc = dc.alloc_grads(S - 1)
+    parts = {"dk_base": [], "dv_base": [], "dk_steps": [[] for _ in range(S - 1)],
+             "dv_steps": [[] for _ in range(S - 1)]}
+    for j in reversed(range(S)):
+        lens_j = [max(1, int(t) - j) for t in case.seq_lens]
+        dc.desc = ttt.desc_for(dc.q[0], dc.k, seq_lens=lens_j)
+        out, lse = dc.fwd(j)
+        dq = dc.bwd(j, out, lse, acc, accumulate=(j != S - 1))
+        torch.cuda.synchronize()
+        o_out, o_lse = oracle.fwd(*oracle_inputs(case, j), seq_lens=lens_j)
+        assert_close(f"shrink out j={j}", np32(out), o_out, **TOL_BF16)
+        assert_close(f"shrink lse j={j}", np32(lse), o_lse, **TOL_BF16)
+        og = oracle.bwd(*oracle_inputs(case, j), np32(case.dout[j]), seq_lens=lens_j)
+        assert_close(f"shrink dq j={j}", np32(dq), og["dq"], **TOL_BF16)
+        parts["dk_base"].append(og["dk_base"])
+        parts["dv_base"].append(og["dv_base"])
+        for i in range(j):
+            parts["dk_steps"][i].append(og["dk_steps"][i])
+            parts["dv_steps"][i].append(og["dv_steps"][i])
+    assert_close_sum("shrink acc dk_base", np32(acc["dk_base"]), parts["dk_base"], **TOL_BF16)
+    assert_close_sum("shrink acc dv_base", np32(acc["dv_base"]), parts["dv_base"], **TOL_BF16)
+    for i in range(S - 1):
+        assert_close_sum(f"shrink acc dk_{i+1}", np32(acc["dk_steps"][i]), parts["dk_steps"][i], **TOL_BF16)
+        assert_close_sum(f"shrink acc dv_{i+1}", np32(acc["dv_steps"][i]), parts["dv_steps"][i], **TOL_BF16)

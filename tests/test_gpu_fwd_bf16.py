@@ -62,7 +62,7 @@ def test_fwd_bf16_masked_inputs_inert(cuda_ok):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg", ["llama8b", "qwen235b"])
+@pytest.mark.parametrize("cfg", ["llama8b", "qwen235b", "longctx"])
 def test_fwd_bf16_full_size_sampled_rows(cuda_ok, cfg):
     """Full BASELINE.json shape, the launch configuration bench.py times;
     oracle on sampled rows (rows are independent in the forward)."""
