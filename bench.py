@@ -390,33 +390,55 @@ def run_loss(args, stream, peaks, world: int):
 
 
 def run_e2e(u: Unroll, stream, args, shape: Shape):
-    """Same metric through the public API with host buffers: every step copies
-    the unroll's inputs H2D from pinned memory and reads the accumulated base
-    gradients dK_0, dV_0 back D2H (the unroll's result), copies included."""
+    """Same metric through the public API with host buffers: every step copies the unroll's
+    inputs H2D from pinned memory and reads the accumulated base gradients dK_0, dV_0 back
+    D2H (the unroll's result), copies included. Inputs are double-buffered like a data
+    loader's prefetch: step i+1's H2D copies run on a copy stream while step i computes
+    (each buffer set is refilled only after the step that read it has finished)."""
+    u2 = Unroll(shape, seed=4321, dev=stream.device)
+    sets = [u, u2]
     host_in = [t.cpu().pin_memory() for t in u.inputs]
     host_out = [torch.empty(u.dk.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
     h2d = sum(t.numel() * t.element_size() for t in host_in)
     d2h = sum(t.numel() * t.element_size() for t in host_out)
-    n = max(2, min(args.steps, 5))
+    n = max(3, min(args.steps, 6))
+    cstream = torch.cuda.Stream(device=stream.device)
+    ev = lambda: torch.cuda.Event()
+    h2d_done, comp_done = [ev(), ev()], [ev(), ev()]
 
-    def step():
-        for d, h in zip(u.inputs, host_in):
-            d.copy_(h, non_blocking=True)
-        u.step(stream)
-        host_out[0].copy_(u.dk, non_blocking=True)
-        host_out[1].copy_(u.dv, non_blocking=True)
+    def copy_in(k):
+        with torch.cuda.stream(cstream):
+            cstream.wait_event(comp_done[k])
+            for d, h in zip(sets[k].inputs, host_in):
+                d.copy_(h, non_blocking=True)
+            h2d_done[k].record(cstream)
 
-    step()
+    def run(steps):
+        for k in range(2):
+            comp_done[k].record(stream)
+        copy_in(0)
+        for i in range(steps):
+            k = i % 2
+            if i + 1 < steps:
+                copy_in(1 - k)
+            stream.wait_event(h2d_done[k])
+            sets[k].step(stream)
+            host_out[0].copy_(sets[k].dk, non_blocking=True)
+            host_out[1].copy_(sets[k].dv, non_blocking=True)
+            comp_done[k].record(stream)
+
+    run(2)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(n):
-        step()
+    run(n)
+    stream.wait_stream(cstream)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
     return {"value": shape.batch * shape.seq_len / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n,
+            "overlap": "double-buffered inputs: step i+1's H2D on a copy stream under step i's compute"}
 
 
 def ncu_traffic(kernel: str):

@@ -1,0 +1,108 @@
+"""torch.autograd wrappers over the C-ABI (argument marshalling only; every step of
+the computation runs in libtttattn.so's kernels). SURVEY.md §8(b) "Python side".
+
+``ttt_attention(q, k_base, v_base, k_steps, v_steps, step)``
+    TTT step ``j = step`` (Alg. 1/2): out [B, L, Hq, D].
+    Backward calls ``ttt_attn_bwd`` for this step in overwrite mode; autograd itself sums
+    the contributions of the S steps of an unroll into K_0 / V_0 / K_i / V_i (the kernel's
+    TTT_ACCUMULATE_DKV path is the fused alternative bench.py times). Gradients of K/V come
+    out of the kernel in fp32 and are returned in the inputs' dtype.
+
+``soft_label_loss(z, p, mask)``
+    Masked soft-label log-softmax loss (reading R17) whose backward is Alg. 3
+     IN PLACE: the logits buffer z is overwritten with dL/dz and handed
+    to autograd as the gradient, so no [N, V] gradient buffer is allocated. z must not be
+    read again after backward (its storage then holds the gradient) — the paper's trick.
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib as L
+
+
+class _TTTAttention(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, step: int, seq_lens, scale: float, q, k_base, v_base, *kv_steps):
+        j = int(step)
+        k_steps, v_steps = list(kv_steps[:j]), list(kv_steps[j:2 * j])
+        desc = L.desc_for(q, k_base, seq_lens=seq_lens, softmax_scale=scale)
+        B, Lq, Hq, D = q.shape
+        out = torch.empty_like(q)
+        out_lo = torch.empty_like(q) if q.dtype == torch.bfloat16 else None
+        lse = torch.empty((B, Hq, Lq), dtype=torch.float32, device=q.device)
+        L.ttt_attn_fwd(desc, j, q, k_base, v_base, k_steps, v_steps, out, lse, out_lo=out_lo)
+        ctx.j, ctx.desc = j, desc
+        ctx.save_for_backward(q, k_base, v_base, out, lse, *([out_lo] if out_lo is not None else []),
+                              *k_steps, *v_steps)
+        ctx.has_lo = out_lo is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        j, desc = ctx.j, ctx.desc
+        saved = ctx.saved_tensors
+        q, k_base, v_base, out, lse = saved[:5]
+        rest = saved[5:]
+        out_lo = rest[0] if ctx.has_lo else None
+        rest = rest[1:] if ctx.has_lo else rest
+        k_steps, v_steps = list(rest[:j]), list(rest[j:2 * j])
+        dout = dout.contiguous()
+        dq = torch.empty_like(q)
+        f32 = lambda t: torch.empty(t.shape, dtype=torch.float32, device=t.device)
+        dk, dv = f32(k_base), f32(v_base)
+        dks, dvs = [f32(t) for t in k_steps], [f32(t) for t in v_steps]
+        ws = torch.empty(max(L.ttt_attn_workspace_size(desc, j, True), 16), dtype=torch.uint8, device=q.device)
+        L.ttt_attn_bwd(desc, j, q, k_base, v_base, k_steps, v_steps, out, lse, dout, dq, dk, dv, dks, dvs,
+                       flags=0, workspace=ws, out_lo=out_lo)
+        cast = lambda g, like: g.to(like.dtype)
+        grads = [cast(dk, k_base), cast(dv, v_base)] + [cast(g, t) for g, t in zip(dks, k_steps)] + \
+                [cast(g, t) for g, t in zip(dvs, v_steps)]
+        return (None, None, None, dq, *grads)
+
+
+def ttt_attention(q: torch.Tensor, k_base: torch.Tensor, v_base: torch.Tensor,
+                  k_steps: Sequence[torch.Tensor], v_steps: Sequence[torch.Tensor], step: int,
+                  seq_lens: Optional[Sequence[int]] = None, softmax_scale: float = 0.0) -> torch.Tensor:
+    """Differentiable TTT attention of step ``step`` (uses k_steps[:step], v_steps[:step]).
+    BSHD tensors, contiguous, on the GPU: q [B, L, Hq, D], K/V [B, L, Hkv, D]."""
+    j = int(step)
+    ks, vs = list(k_steps[:j]), list(v_steps[:j])
+    if len(ks) != j or len(vs) != j:
+        raise ValueError(f"step {j} needs {j} step K/V tensors, got {len(ks)} / {len(vs)}")
+    lens = None if seq_lens is None else [int(x) for x in seq_lens]
+    return _TTTAttention.apply(j, lens, float(softmax_scale), q, k_base, v_base, *ks, *vs)
+
+
+class _SoftLabelLoss(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, z, p, mask, g_rows):
+        desc = L.loss_desc_for(z)
+        ws = torch.empty(L.ttt_loss_workspace_size(desc), dtype=torch.uint8, device=z.device)
+        stats = torch.empty(2, dtype=torch.float64, device=z.device)
+        L.ttt_loss_fwd(desc, z, p, mask, stats, ws)
+        ctx.desc, ctx.ws = desc, ws
+        ctx.save_for_backward(z, p, mask, g_rows)
+        return stats[0].to(torch.float32)
+
+    @staticmethod
+    def backward(ctx, g):
+        z, p, mask, g_rows = ctx.saved_tensors
+        ws = ctx.ws
+        # Alg. 3 in place: z <- dL/dz. The upstream scalar g enters as g_scale; it is read on the
+        # host (one sync) because the C-ABI takes g_scale by value.
+        L.ttt_loss_bwd_inplace(ctx.desc, z, p, mask, ws, g_scale=float(g), flags=L.TTT_LOSS_MEAN,
+                               g_rows=g_rows)
+        return z, None, None, None
+
+
+def soft_label_loss(z: torch.Tensor, p: torch.Tensor, mask: Optional[torch.Tensor] = None,
+                    g_rows: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Masked mean soft-label loss over rows of z [N, V] (bf16 or fp32) against target
+    probabilities p [N, V]; mask uint8 [N] (None = all rows), g_rows optional fp32 [N] row
+    weights. Backward overwrites z with dL/dz (Alg. 3, in place) and returns it as z's grad."""
+    if mask is None:
+        mask = torch.ones(z.shape[0], dtype=torch.uint8, device=z.device)
+    return _SoftLabelLoss.apply(z, p, mask.to(torch.uint8), g_rows)
