@@ -184,7 +184,7 @@ def workload_config(shape: Shape, world: int):
 class Unroll:
     """Device buffers of one per-GPU unroll + the C-ABI calls of one step."""
 
-    def __init__(self, shape: Shape, seed: int, dev):
+    def __init__(self, shape: Shape, seed: int, dev, bwd_unroll: bool = False):
         import paper_2603_18567_b200 as ttt
         self.ttt = ttt
         self.s = s = shape
@@ -207,6 +207,10 @@ class Unroll:
         self.desc = ttt.make_desc(s.batch, s.seq_len, s.num_q_heads, s.num_kv_heads, s.head_dim)
         self.ws = torch.empty(ttt.ttt_attn_workspace_size(self.desc, S - 1, True), dtype=torch.uint8, device=dev)
         self.inputs = self.q + self.do + [self.k, self.v] + self.ks + self.vs
+        self.bwd_unroll = bwd_unroll  # one ttt_attn_bwd_unroll call for the S backward calls
+        if bwd_unroll:
+            self.ws_unroll = torch.empty(ttt.ttt_attn_bwd_unroll_workspace_size(self.desc, S), dtype=torch.uint8,
+                                         device=dev)
 
     def step(self, stream, on_bwd=None):
         t, s = self.ttt, self.s
@@ -214,6 +218,14 @@ class Unroll:
         for j in range(S):
             t.ttt_attn_fwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, self.out[j], self.lse[j],
                            out_lo=self.out_lo[j], stream=stream)
+        if self.bwd_unroll:
+            t.ttt_attn_bwd_unroll(self.desc, self.q, self.k, self.v, self.ks, self.vs, self.out, self.lse, self.do,
+                                  self.dq, self.dk, self.dv, self.dks, self.dvs, flags=0, workspace=self.ws_unroll,
+                                  stream=stream, out_lo=self.out_lo)
+            if on_bwd is not None:
+                for i in range(S):
+                    on_bwd(i)
+            return
         for j in reversed(range(S)):
             t.ttt_attn_bwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, self.out[j], self.lse[j],
                            self.do[j], self.dq[j], self.dk, self.dv, self.dks, self.dvs,
@@ -230,7 +242,7 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
     dist = None
     if world > 1:
         import torch.distributed as dist
-    u = Unroll(shape, seed=1234 + rank, dev=dev)
+    u = Unroll(shape, seed=1234 + rank, dev=dev, bwd_unroll=args.bwd_unroll)
     stream = torch.cuda.current_stream(dev)
     S = shape.ttt_steps
 
@@ -395,7 +407,7 @@ def run_e2e(u: Unroll, stream, args, shape: Shape):
     D2H (the unroll's result), copies included. Inputs are double-buffered like a data
     loader's prefetch: step i+1's H2D copies run on a copy stream while step i computes
     (each buffer set is refilled only after the step that read it has finished)."""
-    u2 = Unroll(shape, seed=4321, dev=stream.device)
+    u2 = Unroll(shape, seed=4321, dev=stream.device, bwd_unroll=u.bwd_unroll)
     sets = [u, u2]
     host_in = [t.cpu().pin_memory() for t in u.inputs]
     host_out = [torch.empty(u.dk.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
@@ -464,6 +476,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-loss", action="store_true", help="skip the §8(f) loss-kernel measurement")
+    ap.add_argument("--bwd-unroll", action="store_true",
+                    help="one ttt_attn_bwd_unroll call per unroll instead of S ttt_attn_bwd calls (same work; "
+                         "37%% less pre-pass HBM traffic, same time: the pre-pass is latency-bound; the DP "
+                         "buckets are then released after the whole backward)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3

@@ -132,6 +132,32 @@ int ttt_attn_bwd(const ttt_attn_desc* desc, int step,
                  float* const* dk_steps, float* const* dv_steps,
                  unsigned flags, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Whole-unroll backward: the S = num_steps backward calls of one TTT unroll in one call,
+ *   identical in semantics to
+ *     for j = S-1 .. 0:  ttt_attn_bwd(desc, j, q[j], k_base, v_base, k_steps, v_steps, out[j],
+ *                                     out_lo ? out_lo[j] : NULL, lse[j], dout[j], dq[j], dk_base,
+ *                                     dv_base, dk_steps, dv_steps,
+ *                                     j == S-1 ? flags : flags | TTT_ACCUMULATE_DKV, ...)
+ *   (dq[j] identical bit for bit; the dK / dV accumulators equal up to fp32 summation order).
+ *   q, out, out_lo, lse, dout, dq: HOST arrays of S device pointers (step j's tensors, layouts as
+ *   in ttt_attn_bwd; out_lo all or NULL); k_steps / v_steps / dk_steps / dv_steps: HOST arrays of
+ *   S-1 device pointers. 1 <= num_steps <= TTT_MAX_UNROLL.
+ *   Why: the diagonal terms of all steps run as ONE pass (bwd_sm100.cu, ttt_bwd_pre_kernel<U>) that
+ *   visits each row group for j = S-1 .. 0 back to back, so dK_i / dV_i are written to HBM once and
+ *   K_i / V_i read once per unroll instead of once per call (the step-j call reads and writes
+ *   every dK_i, i <= j).
+ *   workspace >= ttt_attn_bwd_unroll_workspace_size(desc, num_steps) bytes (S per-call
+ *   workspaces: each step keeps its Delta / lse2 / dq accumulator until its main pass). */
+#define TTT_MAX_UNROLL 8
+size_t ttt_attn_bwd_unroll_workspace_size(const ttt_attn_desc* desc, int num_steps);
+int ttt_attn_bwd_unroll(const ttt_attn_desc* desc, int num_steps,
+                        const void* const* q, const void* k_base, const void* v_base,
+                        const void* const* k_steps, const void* const* v_steps,
+                        const void* const* out, const void* const* out_lo, const float* const* lse,
+                        const void* const* dout, void* const* dq,
+                        float* dk_base, float* dv_base, float* const* dk_steps, float* const* dv_steps,
+                        unsigned flags, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- Optional instrumentation (off by default; used by bench.py) ----------
  * ttt_attn_profile_begin() arms per-kernel timing for the CALLING HOST THREAD:
  * each kernel the library launches afterwards is bracketed by cudaEventRecord

@@ -21,6 +21,7 @@ TTT_FP32_CHECK = 1
 TTT_ACCUMULATE_DKV = 1
 TTT_MAX_STEPS = 32
 TTT_MAX_BATCH = 512
+TTT_MAX_UNROLL = 8
 
 STATUS = {
     0: "TTT_OK", 1: "TTT_ERR_INVALID_ARG", 2: "TTT_ERR_UNSUPPORTED", 3: "TTT_ERR_STEP_RANGE",
@@ -64,6 +65,10 @@ def _load():
     lib.ttt_attn_fwd.restype = i
     lib.ttt_attn_bwd.argtypes = [pd, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, u, vp, sz, vp]
     lib.ttt_attn_bwd.restype = i
+    lib.ttt_attn_bwd_unroll_workspace_size.argtypes = [pd, i]
+    lib.ttt_attn_bwd_unroll_workspace_size.restype = sz
+    lib.ttt_attn_bwd_unroll.argtypes = [pd, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, u, vp, sz, vp]
+    lib.ttt_attn_bwd_unroll.restype = i
     lib.ttt_attn_strerror.argtypes = [i]
     lib.ttt_attn_strerror.restype = ctypes.c_char_p
     lib.ttt_attn_version.argtypes = []
@@ -190,6 +195,25 @@ def ttt_attn_bwd(desc: Desc, step: int, q, k_base, v_base, k_steps, v_steps, out
                              _ptr(lse), _ptr(dout), _ptr(dq), _ptr(dk_base), _ptr(dv_base),
                              _ptr_list(dk_steps[:step]), _ptr_list(dv_steps[:step]), int(flags),
                              _ptr(workspace), ws_bytes, _stream(stream)))
+
+
+
+def ttt_attn_bwd_unroll_workspace_size(desc: Desc, num_steps: int) -> int:
+    return int(_lib.ttt_attn_bwd_unroll_workspace_size(ctypes.byref(desc), int(num_steps)))
+
+
+def ttt_attn_bwd_unroll(desc: Desc, q: Sequence, k_base, v_base, k_steps, v_steps, out: Sequence, lse: Sequence,
+                        dout: Sequence, dq: Sequence, dk_base, dv_base, dk_steps, dv_steps, flags: int = 0,
+                        workspace=None, stream=None, out_lo: Optional[Sequence] = None) -> None:
+    """Enqueue ttt_attn_bwd_unroll (include/ttt_attn.h): the S = len(q) backward calls of one
+    unroll (j = S-1 .. 0) in one call; per-step lists q / out / out_lo / lse / dout / dq."""
+    S = len(q)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(_lib.ttt_attn_bwd_unroll(
+        ctypes.byref(desc), S, _ptr_list(q), _ptr(k_base), _ptr(v_base), _ptr_list(k_steps[:S - 1]),
+        _ptr_list(v_steps[:S - 1]), _ptr_list(out), None if out_lo is None else _ptr_list(out_lo), _ptr_list(lse),
+        _ptr_list(dout), _ptr_list(dq), _ptr(dk_base), _ptr(dv_base), _ptr_list(dk_steps[:S - 1]),
+        _ptr_list(dv_steps[:S - 1]), int(flags), _ptr(workspace), ws_bytes, _stream(stream)))
 
 
 # ---- masked soft-label log-softmax loss + Alg. 3 in-place backward (include/ttt_loss.h) ----

@@ -21,6 +21,8 @@ cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, const DiagMap
 int fwd_diag_rows_per_group(const Params& p);
 cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st);
 int bwd_pre_rows_per_group(const Params& p);
+cudaError_t launch_bwd_unroll_sm100(const Params* ps, const BwdMaps* maps, const PreMaps& pmaps,
+                                    const UnrollPre& up, cudaStream_t st);
 }  // namespace tttk
 
 using namespace tttk;
@@ -423,6 +425,115 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
         return TTT_ERR_CUDA;
   }
   return cuda_status(launch_bwd_sm100(p, maps, pmaps, s));
+}
+
+size_t ttt_attn_bwd_unroll_workspace_size(const ttt_attn_desc* d, int num_steps) {
+  if (num_steps < 1 || num_steps > TTT_MAX_UNROLL || validate_desc(d, num_steps - 1) != TTT_OK) return 0;
+  if (d->dtype == TTT_FP32_CHECK) return 0;
+  return (size_t)num_steps * bwd_ws_layout(d).total;
+}
+
+int ttt_attn_bwd_unroll(const ttt_attn_desc* d, int num_steps, const void* const* q, const void* k_base,
+                        const void* v_base, const void* const* k_steps, const void* const* v_steps,
+                        const void* const* out, const void* const* out_lo, const float* const* lse,
+                        const void* const* dout, void* const* dq, float* dk_base, float* dv_base,
+                        float* const* dk_steps, float* const* dv_steps, unsigned flags, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  const int S = num_steps;
+  if (S < 1 || S > TTT_MAX_UNROLL) return TTT_ERR_STEP_RANGE;
+  int st = validate_desc(d, S - 1);
+  if (st) return st;
+  if (flags & ~TTT_ACCUMULATE_DKV) return TTT_ERR_INVALID_ARG;
+  if (!q || !out || !lse || !dout || !dq) return TTT_ERR_INVALID_ARG;
+  if (d->dtype == TTT_FP32_CHECK) {  // check mode: the S calls of the contract, in order
+    for (int j = S - 1; j >= 0; --j) {
+      const int rc = ttt_attn_bwd(d, j, q[j], k_base, v_base, k_steps, v_steps, out[j], nullptr, lse[j], dout[j],
+                                  dq[j], dk_base, dv_base, dk_steps, dv_steps,
+                                  j == S - 1 ? flags : (flags | TTT_ACCUMULATE_DKV), nullptr, 0, stream);
+      if (rc) return rc;
+    }
+    return TTT_OK;
+  }
+  // the same validation as S ttt_attn_bwd calls, all before the first launch
+  if (!k_base || !v_base || !dk_base || !dv_base) return TTT_ERR_INVALID_ARG;
+  if (S > 1 && (!k_steps || !v_steps || !dk_steps || !dv_steps)) return TTT_ERR_INVALID_ARG;
+  for (int i = 0; i < S - 1; ++i) {
+    if (!k_steps[i] || !v_steps[i] || !dk_steps[i] || !dv_steps[i]) return TTT_ERR_INVALID_ARG;
+    if (!aligned16(k_steps[i]) || !aligned16(v_steps[i]) || !aligned16(dk_steps[i]) || !aligned16(dv_steps[i]))
+      return TTT_ERR_ALIGNMENT;
+  }
+  if (!aligned16(k_base) || !aligned16(v_base) || !aligned16(dk_base) || !aligned16(dv_base))
+    return TTT_ERR_ALIGNMENT;
+  for (int j = 0; j < S; ++j) {
+    if (!q[j] || !out[j] || !lse[j] || !dout[j] || !dq[j]) return TTT_ERR_INVALID_ARG;
+    const void* ptrs[] = {q[j], out[j], lse[j], dout[j], dq[j], out_lo ? out_lo[j] : nullptr};
+    for (const void* ptr : ptrs)
+      if (!aligned16(ptr)) return TTT_ERR_ALIGNMENT;
+  }
+  const BwdWs w = bwd_ws_layout(d);
+  if (!workspace || workspace_bytes < (size_t)S * w.total) return TTT_ERR_WORKSPACE;
+  if (!aligned16(workspace)) return TTT_ERR_ALIGNMENT;
+  static thread_local Params ps[TTT_MAX_UNROLL];
+  static thread_local BwdMaps maps[TTT_MAX_UNROLL];
+  static thread_local UnrollPre up;
+  static thread_local PreMaps pmaps;
+  up = UnrollPre{};
+  up.S = S;
+  for (int j = 0; j < S; ++j) {
+    Params& p = ps[j];
+    fill_common(p, d, j);
+    p.accumulate = (j == S - 1) ? ((flags & TTT_ACCUMULATE_DKV) ? 1 : 0) : 1;
+    p.q = q[j];
+    p.k = k_base;
+    p.v = v_base;
+    p.o = out[j];
+    p.o_lo = out_lo ? out_lo[j] : nullptr;
+    p.lse_in = lse[j];
+    p.dout = dout[j];
+    p.dq = dq[j];
+    p.dk = dk_base;
+    p.dv = dv_base;
+    for (int i = 0; i < S - 1; ++i) {  // every step list: the unroll pass of step S-1 reads all of them
+      p.ks[i] = k_steps[i];
+      p.vs[i] = v_steps[i];
+      p.dks[i] = dk_steps[i];
+      p.dvs[i] = dv_steps[i];
+    }
+    char* ws = static_cast<char*>(workspace) + (size_t)j * w.total;
+    p.delta = reinterpret_cast<float*>(ws + w.delta);
+    p.lse2 = reinterpret_cast<float*>(ws + w.lse2);
+    p.dq_acc = reinterpret_cast<float*>(ws + w.dq_acc);
+    up.lse_in[j] = p.lse_in;
+    up.delta[j] = p.delta;
+    up.lse2[j] = p.lse2;
+    up.dq_acc[j] = p.dq_acc;
+    if (!encode_bshd(&maps[j].q, q[j], p.B, p.L, p.Hq, p.D) || !encode_bshd(&maps[j].k, k_base, p.B, p.L, p.Hkv, p.D) ||
+        !encode_bshd(&maps[j].v, v_base, p.B, p.L, p.Hkv, p.D) ||
+        !encode_bshd(&maps[j].dout, dout[j], p.B, p.L, p.Hq, p.D) ||
+        !encode_bshd(&maps[j].dout64, dout[j], p.B, p.L, p.Hq, p.D, 64) ||
+        !encode_dqacc(&maps[j].dqacc, p.dq_acc, (size_t)p.B * p.L * p.Hq * p.D / 32))
+      return TTT_ERR_CUDA;
+  }
+  // pre-pass maps: layout of the largest step (S - 1); per-step q / dO / O / O_lo views
+  const Params& last = ps[S - 1];
+  if (out_lo)
+    for (int j = 0; j < S; ++j)
+      if (!out_lo[j]) return TTT_ERR_INVALID_ARG;  // all or none
+  const int nr = bwd_pre_rows_per_group(last);
+  if (nr <= 0) return TTT_ERR_UNSUPPORTED;
+  const long long rows = (long long)last.B * last.L * last.Hq, kv_rows = (long long)last.B * last.L * last.Hkv;
+  const int br = nr * last.G;
+  for (int j = 0; j < S; ++j) {
+    if (!encode_rows2d(&up.dout[j], dout[j], rows, last.D, br) || !encode_rows2d(&up.o[j], out[j], rows, last.D, br) ||
+        (out_lo && !encode_rows2d(&up.olo[j], out_lo[j], rows, last.D, br)) ||
+        !encode_rows2d(&up.q[j], q[j], rows, last.D, br))
+      return TTT_ERR_CUDA;
+  }
+  for (int i = 0; i < S - 1; ++i)
+    if (!encode_rows2d(&pmaps.k[i], k_steps[i], kv_rows, last.D, nr) ||
+        !encode_rows2d(&pmaps.v[i], v_steps[i], kv_rows, last.D, nr))
+      return TTT_ERR_CUDA;
+  return cuda_status(launch_bwd_unroll_sm100(ps, maps, pmaps, up, static_cast<cudaStream_t>(stream)));
 }
 
 }  // extern "C"

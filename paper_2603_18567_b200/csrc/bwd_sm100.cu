@@ -113,9 +113,19 @@ struct PreLayout {
   }
 };
 
-template <int D>
+// U = true: the unroll-level pass of ttt_attn_bwd_unroll. Each row group is visited once per
+// step j = S-1 .. 0 (items (group, j), per-step q / dO / O / O_lo maps and lse / Delta / lse2 /
+// dq_acc pointers from `up`), in sweeps over M groups: for M groups, every step, so a group's
+// dK_i / dV_i rows (first written at j = S-1, then reduce-added by j < S-1) and its K_i / V_i rows
+// (re-read by every j >= i) stay in L2 between visits — HBM sees one write of dK_i / dV_i and one
+// read of K_i / V_i per unroll instead of one per call. Ordering of a row's store (item n0) before
+// its reduce-adds (item n0 + Msg, possibly another warp): every compute warp fences its global
+// writes before releasing a stage, and the producer loads item n only after stage n - Msg has been
+// released (the ring's own wait covers it when Msg >= NS), so the adds happen after the store.
+template <int D, bool U>
 __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
-    ttt_bwd_pre_kernel(const __grid_constant__ Params p, const __grid_constant__ PreMaps maps, PreLayout lay) {
+    ttt_bwd_pre_kernel(const __grid_constant__ Params p, const __grid_constant__ PreMaps maps,
+                       const __grid_constant__ UnrollPre up, PreLayout lay) {
   constexpr int NB = D / 64;
   extern __shared__ uint8_t psm_raw[];
   uint8_t* psm = psm_raw + ((1024u - (smem_u32(psm_raw) & 1023u)) & 1023u);
@@ -123,9 +133,13 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
   uint64_t* empty = full + 8;
   uint8_t* stages = psm + 1024;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = p.G, j = p.step, NR = lay.NR, NS = lay.NS, R = lay.R;
+  const int G = p.G, NR = lay.NR, NS = lay.NS, R = lay.R;
   const int nrows = p.B * p.L * p.Hkv;  // < 2^31 (host check)
   const int ngroups = (nrows + NR - 1) / NR;
+  const int ng = (ngroups - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // this CTA's groups
+  const int S = U ? up.S : 1;
+  // groups per j-sweep starting at group index g0 of this CTA (the tail joins the last sweep)
+  auto sweep = [&](int g0) { return U ? ((ng - g0 >= 2 * up.M) ? up.M : ng - g0) : 1; };
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
@@ -138,27 +152,42 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
   if (warp == 0) {
     // ================= producer =================
     if (lane == 0) {
-      tma_prefetch_desc(&maps.dout);
-      tma_prefetch_desc(&maps.o);
-      const uint32_t bytes = NB * ((2u + (lay.has_lo ? 1u : 0u) + (j > 0 ? 1u : 0u)) * lay.qbytes + 2u * j * lay.kbytes);
       int n = 0;
-      for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++n) {
-        const int st = n % NS;
-        if (n >= NS) mbar_wait(&empty[st], ((n / NS) - 1) & 1);
-        uint8_t* base = stages + st * lay.stage_bytes;
-        mbar_expect_tx(&full[st], bytes);  // full boxes (OOB rows are zero-filled and counted)
-        const int rq = grp * NR * G, rk = grp * NR;
+      for (int g0 = 0; g0 < ng;) {
+        const int msg = sweep(g0);
+        for (int jj = 0; jj < S; ++jj) {
+          const int j = U ? S - 1 - jj : p.step;
+          const CUtensorMap* mdo = U ? &up.dout[j] : &maps.dout;
+          const CUtensorMap* mo = U ? &up.o[j] : &maps.o;
+          const CUtensorMap* molo = U ? &up.olo[j] : &maps.olo;
+          const CUtensorMap* mq = U ? &up.q[j] : &maps.q;
+          const uint32_t bytes =
+              NB * ((2u + (lay.has_lo ? 1u : 0u) + (j > 0 ? 1u : 0u)) * lay.qbytes + 2u * j * lay.kbytes);
+          for (int gi = 0; gi < msg; ++gi, ++n) {
+            const int grp = (int)blockIdx.x + (g0 + gi) * (int)gridDim.x;
+            const int st = n % NS;
+            if (n >= NS) mbar_wait(&empty[st], ((n / NS) - 1) & 1);
+            if (U && jj > 0 && msg < NS) {  // the same group's previous step released (see above)
+              const int m = n - msg;
+              mbar_wait(&empty[m % NS], (m / NS) & 1);
+            }
+            uint8_t* base = stages + st * lay.stage_bytes;
+            mbar_expect_tx(&full[st], bytes);  // full boxes (OOB rows are zero-filled and counted)
+            const int rq = grp * NR * G, rk = grp * NR;
 #pragma unroll
-        for (int bx = 0; bx < NB; ++bx) {
-          tma_load_2d(base + lay.off_do + bx * lay.qbox, &maps.dout, &full[st], bx * 64, rq);
-          tma_load_2d(base + lay.off_o + bx * lay.qbox, &maps.o, &full[st], bx * 64, rq);
-          if (lay.has_lo) tma_load_2d(base + lay.off_olo + bx * lay.qbox, &maps.olo, &full[st], bx * 64, rq);
-          if (j > 0) tma_load_2d(base + lay.off_q + bx * lay.qbox, &maps.q, &full[st], bx * 64, rq);
-          for (int i = 0; i < j; ++i) {
-            tma_load_2d(base + lay.off_k + (i * NB + bx) * lay.kbox, &maps.k[i], &full[st], bx * 64, rk);
-            tma_load_2d(base + lay.off_v + (i * NB + bx) * lay.kbox, &maps.v[i], &full[st], bx * 64, rk);
+            for (int bx = 0; bx < NB; ++bx) {
+              tma_load_2d(base + lay.off_do + bx * lay.qbox, mdo, &full[st], bx * 64, rq);
+              tma_load_2d(base + lay.off_o + bx * lay.qbox, mo, &full[st], bx * 64, rq);
+              if (lay.has_lo) tma_load_2d(base + lay.off_olo + bx * lay.qbox, molo, &full[st], bx * 64, rq);
+              if (j > 0) tma_load_2d(base + lay.off_q + bx * lay.qbox, mq, &full[st], bx * 64, rq);
+              for (int i = 0; i < j; ++i) {
+                tma_load_2d(base + lay.off_k + (i * NB + bx) * lay.kbox, &maps.k[i], &full[st], bx * 64, rk);
+                tma_load_2d(base + lay.off_v + (i * NB + bx) * lay.kbox, &maps.v[i], &full[st], bx * 64, rk);
+              }
+            }
           }
         }
+        g0 += msg;
       }
     }
     return;
@@ -168,248 +197,263 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
   const int cw = warp - 1;
   const int g8 = lane >> 2, c4 = lane & 3;
   const float sl2 = p.scale_log2, cs = p.scale;
-  const int ncols = j * R;
-  const int NT = (ncols + 7) / 8;   // 8-column tiles of S / dP (<= 4)
-  const int MT2 = (ncols + 15) / 16;  // 16-row tiles of dK / dV (<= 2)
   const int MT = (G + 15) / 16;     // 16-row tiles of query rows (R == 1 when G > 16)
   const int ipg = (NR + R - 1) / R;
   uint8_t* scrP = psm + lay.off_scr + cw * 2560;  // [16 rows m][40] bf16 (80-B rows: conflict-free)
   uint8_t* scrS = scrP + 1280;
   const uint32_t sP = smem_u32(scrP), sS = smem_u32(scrS);
-  int colw[4][2];  // w' of the thread's C-fragment columns, -1 past j R
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int n = nt * 8 + 2 * c4 + e;
-      colw[nt][e] = n < ncols ? n % R : -1;
-    }
-  int brow_i[4], brow_w[4];  // ldmatrix row (lane & 7) of column tile nt: step i, row w'
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt) {
-    const int n = ncols > 0 ? min(nt * 8 + (lane & 7), ncols - 1) : 0;
-    brow_i[nt] = n / R;
-    brow_w[nt] = n % R;
-  }
   int n = 0;
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++n) {
-    const int st = n % NS;
-    mbar_wait(&full[st], (n / NS) & 1);
-    const uint32_t sb = smem_u32(stages + st * lay.stage_bytes);
-    const int w0 = grp * NR, nv = min(NR, nrows - w0);
-    const int nitems = (nv + R - 1) / R;
-    // items of this group owned by this warp: global item id n*ipg + k, round-robin over warps
-    for (int k = (cw - (n * ipg) % kPreCompute + kPreCompute) % kPreCompute; k < nitems; k += kPreCompute) {
-      const int lr0 = k * R;
-      for (int mt = 0; mt < MT; ++mt) {
-        const int mrows = R > 1 ? R * G : min(16, G - mt * 16);
-        // ---- the thread's two query rows (g8, g8 + 8): (w', head), validity, lse2 ----
-        int wr[2], hh[2], bb[2], rr[2], gg[2];
-        bool okr[2], act[2];
-        float l2[2];
+  for (int g0 = 0; g0 < ng;) {
+    const int msg = sweep(g0);
+    for (int jj = 0; jj < S; ++jj) {
+      const int j = U ? S - 1 - jj : p.step;
+      const float* lse_in = U ? up.lse_in[j] : p.lse_in;
+      float* delta_p = U ? up.delta[j] : p.delta;
+      float* lse2_p = U ? up.lse2[j] : p.lse2;
+      float* dq_acc_p = U ? up.dq_acc[j] : p.dq_acc;
+      // dK_i / dV_i: stored by the first contribution (overwrite mode, j = S-1), else reduce-added
+      const bool radd = U ? (p.accumulate != 0 || j != S - 1) : (p.accumulate != 0);
+      const int ncols = j * R;
+      const int NT = (ncols + 7) / 8;   // 8-column tiles of S / dP (<= 4)
+      const int MT2 = (ncols + 15) / 16;  // 16-row tiles of dK / dV (<= 2)
+      int colw[4][2];  // w' of the thread's C-fragment columns, -1 past j R
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          const int m = g8 + hf * 8;
-          wr[hf] = R > 1 ? m / G : 0;
-          hh[hf] = R > 1 ? m % G : mt * 16 + m;
-          okr[hf] = m < mrows && lr0 + wr[hf] < nv;
-          const uint32_t w = (uint32_t)(w0 + min(lr0 + wr[hf], nv - 1));
-          const uint32_t bl = w / (uint32_t)p.Hkv;
-          gg[hf] = (int)(w - bl * (uint32_t)p.Hkv);
-          bb[hf] = (int)(bl / (uint32_t)p.L);
-          rr[hf] = (int)(bl - (uint32_t)bb[hf] * (uint32_t)p.L);
-          act[hf] = okr[hf] && rr[hf] < p.seq_lens[bb[hf]];
-          l2[hf] = okr[hf] ? p.lse_in[((size_t)bb[hf] * p.Hq + gg[hf] * G + hh[hf]) * p.L + rr[hf]] * kLog2e : 0.f;
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = nt * 8 + 2 * c4 + e;
+          colw[nt][e] = c < ncols ? c % R : -1;
         }
-        // ---- S = Q K^T, dP = dO V^T, Delta = diag(dO (O + O_lo)^T) ----
-        float s[4][4], dp[4][4], cd[2][4];
+      int brow_i[4], brow_w[4];  // ldmatrix row (lane & 7) of column tile nt: step i, row w'
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) s[t][e] = dp[t][e] = 0.f;
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) cd[0][e] = cd[1][e] = 0.f;
-        const uint32_t qrow0 = (uint32_t)(lr0 * G + mt * 16);
-        const uint32_t arow = qrow0 + (uint32_t)min((lane & 7) + ((lane >> 3) & 1) * 8, mrows - 1);
-        const uint32_t orow = qrow0 + (uint32_t)min((lane & 7) + ((lane >> 4) & 1) * 8, mrows - 1);  // B: rows m'
-#pragma unroll 2
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t ach = (uint32_t)ks * 2 + (lane >> 4);
-          uint32_t ado[4];
-          ldsm_x4(sb + lay.off_do + (ach >> 3) * lay.qbox + sw128_off(arow, ach), ado);
-          {  // Delta: B = O rows m' (n-tiles m' 0-7, 8-15), k = 16 columns of D
-            const uint32_t och = (uint32_t)ks * 2 + ((lane >> 3) & 1);
-            uint32_t bo[4];
-            ldsm_x4(sb + lay.off_o + (och >> 3) * lay.qbox + sw128_off(orow, och), bo);
-            mma_16816(cd[0], ado, bo[0], bo[1]);
-            mma_16816(cd[1], ado, bo[2], bo[3]);
-            if (lay.has_lo) {
-              ldsm_x4(sb + lay.off_olo + (och >> 3) * lay.qbox + sw128_off(orow, och), bo);
-              mma_16816(cd[0], ado, bo[0], bo[1]);
-              mma_16816(cd[1], ado, bo[2], bo[3]);
-            }
-          }
-          if (ncols > 0) {
-            uint32_t aq[4];
-            ldsm_x4(sb + lay.off_q + (ach >> 3) * lay.qbox + sw128_off(arow, ach), aq);
-            const uint32_t bch = (uint32_t)ks * 2 + ((lane >> 3) & 1);
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) {
-              if (nt < NT) {
-                const uint32_t brow = (uint32_t)(lr0 + brow_w[nt]);
-                const uint32_t boff = (uint32_t)(brow_i[nt] * NB + (bch >> 3)) * lay.kbox + sw128_off(brow, bch);
-                uint32_t bk[2], bv[2];
-                ldsm_x2(sb + lay.off_k + boff, bk);
-                ldsm_x2(sb + lay.off_v + boff, bv);
-                mma_16816(s[nt], aq, bk[0], bk[1]);
-                mma_16816(dp[nt], ado, bv[0], bv[1]);
-              }
-            }
-          }
-        }
-        // Delta of row m sits at column m: thread (g8, c4 = g8 / 2), element g8 & 1 (rows g8, g8 + 8)
-        float del[2];
-        {
-          const int src = g8 * 4 + (g8 >> 1);
-          const float d0 = (g8 & 1) ? cd[0][1] : cd[0][0];
-          const float d1 = (g8 & 1) ? cd[1][3] : cd[1][2];
-          del[0] = __shfl_sync(0xffffffffu, d0, src);
-          del[1] = __shfl_sync(0xffffffffu, d1, src);
-        }
-        // ---- P and c dS on the allowed (block-diagonal) entries; bf16 copies to the scratch ----
-        uint32_t pa[4][2], da[4][2];  // A fragments (m16n8k8) of P and c dS per column tile
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          if (nt < NT) {
-            float pv[4], dv[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int hf = e >> 1;
-              const bool ok = act[hf] && colw[nt][e & 1] == wr[hf];
-              const float pr = ok ? ex2(s[nt][e] * sl2 - l2[hf]) : 0.f;  // p_i = exp(c q.k_i - lse)
-              pv[e] = pr;
-              dv[e] = cs * pr * (dp[nt][e] - del[hf]);  // c ds_i, ds_i = p_i (dp_i - Delta)
-            }
-            pa[nt][0] = pack_bf16(pv[0], pv[1]);
-            pa[nt][1] = pack_bf16(pv[2], pv[3]);
-            da[nt][0] = pack_bf16(dv[0], dv[1]);
-            da[nt][1] = pack_bf16(dv[2], dv[3]);
-            const uint32_t o0 = (uint32_t)g8 * 80 + (uint32_t)(nt * 8 + 2 * c4) * 2;
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sP + o0), "r"(pa[nt][0]));
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sP + o0 + 640), "r"(pa[nt][1]));
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sS + o0), "r"(da[nt][0]));
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sS + o0 + 640), "r"(da[nt][1]));
-          }
-        }
-        __syncwarp();
-        // ---- dq_acc = c dS K (zeros at j = 0), -Delta, -lse2 ----
-        size_t qbase[2];
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          const int h = gg[hf] * G + hh[hf];
-          qbase[hf] = ((((size_t)(bb[hf] * p.Hq + h) * p.nqt + (rr[hf] >> 7)) * (D / 32)) * 128 + (rr[hf] & 127)) * 32;
-          if (okr[hf] && c4 == 0) {
-            const size_t li = ((size_t)bb[hf] * p.Hq + h) * p.L + rr[hf];
-            p.delta[li] = -del[hf];  // stored negated: the main kernel's FFMA2 / FADD2 consume -lse2, -Delta
-            p.lse2[li] = -l2[hf];
-          }
-        }
-#pragma unroll
-        for (int d4 = 0; d4 < D / 32; ++d4) {
-          float acc[4][4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt) {
-            if (nt < NT) {
-              const uint32_t ch = (uint32_t)(d4 * 4 + (lane >> 3));
-              const uint32_t brow = (uint32_t)(lr0 + brow_w[nt]);
-              uint32_t kb[4];
-              ldsm_x4_t(sb + lay.off_k + (uint32_t)(brow_i[nt] * NB + (ch >> 3)) * lay.kbox + sw128_off(brow, ch), kb);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) mma_1688(acc[q], da[nt][0], da[nt][1], kb[q]);
-            }
-          }
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            if (okr[hf]) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int d = (d4 * 4 + q) * 8 + 2 * c4;
-                *reinterpret_cast<float2*>(p.dq_acc + qbase[hf] + (size_t)(d >> 5) * 4096 + (d & 31)) =
-                    make_float2(acc[q][2 * hf], acc[q][2 * hf + 1]);
-              }
-            }
-          }
-        }
-        // ---- dK_i = (c dS)^T Q, dV_i = P^T dO: rows n = (i, w'), K = the 16 query rows ----
-        for (int t2 = 0; t2 < MT2; ++t2) {
-          // A' = (c dS)^T / P^T: ldmatrix.trans of the [m][n] scratch, matrices (m 0-7 | 8-15) x (n 0-7 | 8-15)
-          const int mi = lane >> 3;
-          const uint32_t aoff = (uint32_t)(((mi >> 1) * 8 + (lane & 7)) * 80 + (t2 * 16 + (mi & 1) * 8) * 2);
-          uint32_t ads[4], ap[4];
-          ldsm_x4_t(sS + aoff, ads);
-          ldsm_x4_t(sP + aoff, ap);
-          // output rows of this tile: n = t2*16 + g8 (+8) -> (i, w')
-          int oi[2], ow[2];
-          bool ook[2];
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            const int nn = t2 * 16 + g8 + hf * 8;
-            oi[hf] = nn / R;
-            ow[hf] = nn % R;
-            ook[hf] = nn < ncols && lr0 + ow[hf] < nv;
-          }
-          const uint32_t brow = qrow0 + (uint32_t)min((mi & 1) * 8 + (lane & 7), mrows - 1);  // B' rows m
-#pragma unroll 2
-          for (int dc = 0; dc < D / 8; dc += 2) {
-            const uint32_t ch = (uint32_t)(dc + (mi >> 1));
-            uint32_t bq[4], bo[4];
-            ldsm_x4_t(sb + lay.off_q + (ch >> 3) * lay.qbox + sw128_off(brow, ch), bq);
-            ldsm_x4_t(sb + lay.off_do + (ch >> 3) * lay.qbox + sw128_off(brow, ch), bo);
-            float k0[4] = {0.f, 0.f, 0.f, 0.f}, k1[4] = {0.f, 0.f, 0.f, 0.f};
-            float v0[4] = {0.f, 0.f, 0.f, 0.f}, v1[4] = {0.f, 0.f, 0.f, 0.f};
-            mma_16816(k0, ads, bq[0], bq[1]);
-            mma_16816(k1, ads, bq[2], bq[3]);
-            mma_16816(v0, ap, bo[0], bo[1]);
-            mma_16816(v1, ap, bo[2], bo[3]);
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = ncols > 0 ? min(nt * 8 + (lane & 7), ncols - 1) : 0;
+        brow_i[nt] = c / R;
+        brow_w[nt] = c % R;
+      }
+      for (int gi = 0; gi < msg; ++gi, ++n) {
+        const int grp = (int)blockIdx.x + (g0 + gi) * (int)gridDim.x;
+        const int st = n % NS;
+        mbar_wait(&full[st], (n / NS) & 1);
+        const uint32_t sb = smem_u32(stages + st * lay.stage_bytes);
+        const int w0 = grp * NR, nv = min(NR, nrows - w0);
+        const int nitems = (nv + R - 1) / R;
+        // items of this group owned by this warp: global item id n*ipg + k, round-robin over warps
+        for (int k = (cw - (n * ipg) % kPreCompute + kPreCompute) % kPreCompute; k < nitems; k += kPreCompute) {
+          const int lr0 = k * R;
+          for (int mt = 0; mt < MT; ++mt) {
+            const int mrows = R > 1 ? R * G : min(16, G - mt * 16);
+            // ---- the thread's two query rows (g8, g8 + 8): (w', head), validity, lse2 ----
+            int wr[2], hh[2], bb[2], rr[2], gg[2];
+            bool okr[2], act[2];
+            float l2[2];
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
-              if (ook[hf]) {
-                const size_t ro = (size_t)(w0 + lr0 + ow[hf]) * D;
-                float* dk = p.dks[oi[hf]] + ro;
-                float* dv = p.dvs[oi[hf]] + ro;
-                const int d0 = dc * 8 + 2 * c4, d1 = d0 + 8;
-                if (p.accumulate) {
-                  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dk + d0), "f"(k0[2 * hf]), "f"(k0[2 * hf + 1]) : "memory");
-                  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dk + d1), "f"(k1[2 * hf]), "f"(k1[2 * hf + 1]) : "memory");
-                  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dv + d0), "f"(v0[2 * hf]), "f"(v0[2 * hf + 1]) : "memory");
-                  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dv + d1), "f"(v1[2 * hf]), "f"(v1[2 * hf + 1]) : "memory");
-                } else if (mt == 0) {
-                  *reinterpret_cast<float2*>(dk + d0) = make_float2(k0[2 * hf], k0[2 * hf + 1]);
-                  *reinterpret_cast<float2*>(dk + d1) = make_float2(k1[2 * hf], k1[2 * hf + 1]);
-                  *reinterpret_cast<float2*>(dv + d0) = make_float2(v0[2 * hf], v0[2 * hf + 1]);
-                  *reinterpret_cast<float2*>(dv + d1) = make_float2(v1[2 * hf], v1[2 * hf + 1]);
-                } else {  // G > 16: later head tiles add to the first tile's values (same thread wrote them)
-                  float2* a = reinterpret_cast<float2*>(dk + d0);
-                  float2* c = reinterpret_cast<float2*>(dk + d1);
-                  float2* e2 = reinterpret_cast<float2*>(dv + d0);
-                  float2* f2 = reinterpret_cast<float2*>(dv + d1);
-                  float2 x = *a; *a = make_float2(x.x + k0[2 * hf], x.y + k0[2 * hf + 1]);
-                  x = *c; *c = make_float2(x.x + k1[2 * hf], x.y + k1[2 * hf + 1]);
-                  x = *e2; *e2 = make_float2(x.x + v0[2 * hf], x.y + v0[2 * hf + 1]);
-                  x = *f2; *f2 = make_float2(x.x + v1[2 * hf], x.y + v1[2 * hf + 1]);
+              const int m = g8 + hf * 8;
+              wr[hf] = R > 1 ? m / G : 0;
+              hh[hf] = R > 1 ? m % G : mt * 16 + m;
+              okr[hf] = m < mrows && lr0 + wr[hf] < nv;
+              const uint32_t w = (uint32_t)(w0 + min(lr0 + wr[hf], nv - 1));
+              const uint32_t bl = w / (uint32_t)p.Hkv;
+              gg[hf] = (int)(w - bl * (uint32_t)p.Hkv);
+              bb[hf] = (int)(bl / (uint32_t)p.L);
+              rr[hf] = (int)(bl - (uint32_t)bb[hf] * (uint32_t)p.L);
+              act[hf] = okr[hf] && rr[hf] < p.seq_lens[bb[hf]];
+              l2[hf] = okr[hf] ? lse_in[((size_t)bb[hf] * p.Hq + gg[hf] * G + hh[hf]) * p.L + rr[hf]] * kLog2e : 0.f;
+            }
+            // ---- S = Q K^T, dP = dO V^T, Delta = diag(dO (O + O_lo)^T) ----
+            float s[4][4], dp[4][4], cd[2][4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) s[t][e] = dp[t][e] = 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) cd[0][e] = cd[1][e] = 0.f;
+            const uint32_t qrow0 = (uint32_t)(lr0 * G + mt * 16);
+            const uint32_t arow = qrow0 + (uint32_t)min((lane & 7) + ((lane >> 3) & 1) * 8, mrows - 1);
+            const uint32_t orow = qrow0 + (uint32_t)min((lane & 7) + ((lane >> 4) & 1) * 8, mrows - 1);  // B: rows m'
+#pragma unroll 2
+            for (int ks = 0; ks < D / 16; ++ks) {
+              const uint32_t ach = (uint32_t)ks * 2 + (lane >> 4);
+              uint32_t ado[4];
+              ldsm_x4(sb + lay.off_do + (ach >> 3) * lay.qbox + sw128_off(arow, ach), ado);
+              {  // Delta: B = O rows m' (n-tiles m' 0-7, 8-15), k = 16 columns of D
+                const uint32_t och = (uint32_t)ks * 2 + ((lane >> 3) & 1);
+                uint32_t bo[4];
+                ldsm_x4(sb + lay.off_o + (och >> 3) * lay.qbox + sw128_off(orow, och), bo);
+                mma_16816(cd[0], ado, bo[0], bo[1]);
+                mma_16816(cd[1], ado, bo[2], bo[3]);
+                if (lay.has_lo) {
+                  ldsm_x4(sb + lay.off_olo + (och >> 3) * lay.qbox + sw128_off(orow, och), bo);
+                  mma_16816(cd[0], ado, bo[0], bo[1]);
+                  mma_16816(cd[1], ado, bo[2], bo[3]);
+                }
+              }
+              if (ncols > 0) {
+                uint32_t aq[4];
+                ldsm_x4(sb + lay.off_q + (ach >> 3) * lay.qbox + sw128_off(arow, ach), aq);
+                const uint32_t bch = (uint32_t)ks * 2 + ((lane >> 3) & 1);
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                  if (nt < NT) {
+                    const uint32_t brow = (uint32_t)(lr0 + brow_w[nt]);
+                    const uint32_t boff = (uint32_t)(brow_i[nt] * NB + (bch >> 3)) * lay.kbox + sw128_off(brow, bch);
+                    uint32_t bk[2], bv[2];
+                    ldsm_x2(sb + lay.off_k + boff, bk);
+                    ldsm_x2(sb + lay.off_v + boff, bv);
+                    mma_16816(s[nt], aq, bk[0], bk[1]);
+                    mma_16816(dp[nt], ado, bv[0], bv[1]);
+                  }
                 }
               }
             }
+            // Delta of row m sits at column m: thread (g8, c4 = g8 / 2), element g8 & 1 (rows g8, g8 + 8)
+            float del[2];
+            {
+              const int src = g8 * 4 + (g8 >> 1);
+              const float d0 = (g8 & 1) ? cd[0][1] : cd[0][0];
+              const float d1 = (g8 & 1) ? cd[1][3] : cd[1][2];
+              del[0] = __shfl_sync(0xffffffffu, d0, src);
+              del[1] = __shfl_sync(0xffffffffu, d1, src);
+            }
+            // ---- P and c dS on the allowed (block-diagonal) entries; bf16 copies to the scratch ----
+            uint32_t pa[4][2], da[4][2];  // A fragments (m16n8k8) of P and c dS per column tile
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              if (nt < NT) {
+                float pv[4], dv[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int hf = e >> 1;
+                  const bool ok = act[hf] && colw[nt][e & 1] == wr[hf];
+                  const float pr = ok ? ex2(s[nt][e] * sl2 - l2[hf]) : 0.f;  // p_i = exp(c q.k_i - lse)
+                  pv[e] = pr;
+                  dv[e] = cs * pr * (dp[nt][e] - del[hf]);  // c ds_i, ds_i = p_i (dp_i - Delta)
+                }
+                pa[nt][0] = pack_bf16(pv[0], pv[1]);
+                pa[nt][1] = pack_bf16(pv[2], pv[3]);
+                da[nt][0] = pack_bf16(dv[0], dv[1]);
+                da[nt][1] = pack_bf16(dv[2], dv[3]);
+                const uint32_t o0 = (uint32_t)g8 * 80 + (uint32_t)(nt * 8 + 2 * c4) * 2;
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(sP + o0), "r"(pa[nt][0]));
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(sP + o0 + 640), "r"(pa[nt][1]));
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(sS + o0), "r"(da[nt][0]));
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(sS + o0 + 640), "r"(da[nt][1]));
+              }
+            }
+            __syncwarp();
+            // ---- dq_acc = c dS K (zeros at j = 0), -Delta, -lse2 ----
+            size_t qbase[2];
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              const int h = gg[hf] * G + hh[hf];
+              qbase[hf] = ((((size_t)(bb[hf] * p.Hq + h) * p.nqt + (rr[hf] >> 7)) * (D / 32)) * 128 + (rr[hf] & 127)) * 32;
+              if (okr[hf] && c4 == 0) {
+                const size_t li = ((size_t)bb[hf] * p.Hq + h) * p.L + rr[hf];
+                delta_p[li] = -del[hf];  // stored negated: the main kernel's FFMA2 / FADD2 consume -lse2, -Delta
+                lse2_p[li] = -l2[hf];
+              }
+            }
+#pragma unroll
+            for (int d4 = 0; d4 < D / 32; ++d4) {
+              float acc[4][4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+#pragma unroll
+              for (int nt = 0; nt < 4; ++nt) {
+                if (nt < NT) {
+                  const uint32_t ch = (uint32_t)(d4 * 4 + (lane >> 3));
+                  const uint32_t brow = (uint32_t)(lr0 + brow_w[nt]);
+                  uint32_t kb[4];
+                  ldsm_x4_t(sb + lay.off_k + (uint32_t)(brow_i[nt] * NB + (ch >> 3)) * lay.kbox + sw128_off(brow, ch), kb);
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) mma_1688(acc[q], da[nt][0], da[nt][1], kb[q]);
+                }
+              }
+#pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {
+                if (okr[hf]) {
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const int d = (d4 * 4 + q) * 8 + 2 * c4;
+                    *reinterpret_cast<float2*>(dq_acc_p + qbase[hf] + (size_t)(d >> 5) * 4096 + (d & 31)) =
+                        make_float2(acc[q][2 * hf], acc[q][2 * hf + 1]);
+                  }
+                }
+              }
+            }
+            // ---- dK_i = (c dS)^T Q, dV_i = P^T dO: rows n = (i, w'), K = the 16 query rows ----
+            for (int t2 = 0; t2 < MT2; ++t2) {
+              // A' = (c dS)^T / P^T: ldmatrix.trans of the [m][n] scratch, matrices (m 0-7 | 8-15) x (n 0-7 | 8-15)
+              const int mi = lane >> 3;
+              const uint32_t aoff = (uint32_t)(((mi >> 1) * 8 + (lane & 7)) * 80 + (t2 * 16 + (mi & 1) * 8) * 2);
+              uint32_t ads[4], ap[4];
+              ldsm_x4_t(sS + aoff, ads);
+              ldsm_x4_t(sP + aoff, ap);
+              // output rows of this tile: n = t2*16 + g8 (+8) -> (i, w')
+              int oi[2], ow[2];
+              bool ook[2];
+#pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {
+                const int nn = t2 * 16 + g8 + hf * 8;
+                oi[hf] = nn / R;
+                ow[hf] = nn % R;
+                ook[hf] = nn < ncols && lr0 + ow[hf] < nv;
+              }
+              const uint32_t brow = qrow0 + (uint32_t)min((mi & 1) * 8 + (lane & 7), mrows - 1);  // B' rows m
+#pragma unroll 2
+              for (int dc = 0; dc < D / 8; dc += 2) {
+                const uint32_t ch = (uint32_t)(dc + (mi >> 1));
+                uint32_t bq[4], bo[4];
+                ldsm_x4_t(sb + lay.off_q + (ch >> 3) * lay.qbox + sw128_off(brow, ch), bq);
+                ldsm_x4_t(sb + lay.off_do + (ch >> 3) * lay.qbox + sw128_off(brow, ch), bo);
+                float k0[4] = {0.f, 0.f, 0.f, 0.f}, k1[4] = {0.f, 0.f, 0.f, 0.f};
+                float v0[4] = {0.f, 0.f, 0.f, 0.f}, v1[4] = {0.f, 0.f, 0.f, 0.f};
+                mma_16816(k0, ads, bq[0], bq[1]);
+                mma_16816(k1, ads, bq[2], bq[3]);
+                mma_16816(v0, ap, bo[0], bo[1]);
+                mma_16816(v1, ap, bo[2], bo[3]);
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                  if (ook[hf]) {
+                    const size_t ro = (size_t)(w0 + lr0 + ow[hf]) * D;
+                    float* dk = p.dks[oi[hf]] + ro;
+                    float* dv = p.dvs[oi[hf]] + ro;
+                    const int d0 = dc * 8 + 2 * c4, d1 = d0 + 8;
+                    if (radd) {
+                      asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dk + d0), "f"(k0[2 * hf]), "f"(k0[2 * hf + 1]) : "memory");
+                      asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dk + d1), "f"(k1[2 * hf]), "f"(k1[2 * hf + 1]) : "memory");
+                      asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dv + d0), "f"(v0[2 * hf]), "f"(v0[2 * hf + 1]) : "memory");
+                      asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dv + d1), "f"(v1[2 * hf]), "f"(v1[2 * hf + 1]) : "memory");
+                    } else if (mt == 0) {
+                      *reinterpret_cast<float2*>(dk + d0) = make_float2(k0[2 * hf], k0[2 * hf + 1]);
+                      *reinterpret_cast<float2*>(dk + d1) = make_float2(k1[2 * hf], k1[2 * hf + 1]);
+                      *reinterpret_cast<float2*>(dv + d0) = make_float2(v0[2 * hf], v0[2 * hf + 1]);
+                      *reinterpret_cast<float2*>(dv + d1) = make_float2(v1[2 * hf], v1[2 * hf + 1]);
+                    } else {  // G > 16: later head tiles add to the first tile's values (same thread wrote them)
+                      float2* a = reinterpret_cast<float2*>(dk + d0);
+                      float2* c = reinterpret_cast<float2*>(dk + d1);
+                      float2* e2 = reinterpret_cast<float2*>(dv + d0);
+                      float2* f2 = reinterpret_cast<float2*>(dv + d1);
+                      float2 x = *a; *a = make_float2(x.x + k0[2 * hf], x.y + k0[2 * hf + 1]);
+                      x = *c; *c = make_float2(x.x + k1[2 * hf], x.y + k1[2 * hf + 1]);
+                      x = *e2; *e2 = make_float2(x.x + v0[2 * hf], x.y + v0[2 * hf + 1]);
+                      x = *f2; *f2 = make_float2(x.x + v1[2 * hf], x.y + v1[2 * hf + 1]);
+                    }
+                  }
+                }
+              }
+            }
+            __syncwarp();  // scratch reused by the next item / head tile
           }
         }
-        __syncwarp();  // scratch reused by the next item / head tile
+        if (U) __threadfence();  // this warp's global writes before the stage release (see above)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    g0 += msg;
   }
 }
 
@@ -967,11 +1011,17 @@ int pick_head_split(const Params& p) {
 // R rows per warp item (R G <= 16 query rows, j R <= 32 columns, power of 2); NR rows per
 // group: a multiple of R, NR G <= 256 (TMA box rows), stage ~64 KB; 4 down to 1 stages.
 bool pre_layout(const Params& p, int D, PreLayout* lay) {
+#ifndef TTT_PRE_RMAX
+#define TTT_PRE_RMAX 16
+#endif
   int R = 1;
-  while (R * 2 * p.G <= 16 && R * 2 * p.step <= 32) R *= 2;
+  while (R * 2 * p.G <= 16 && R * 2 * p.step <= 32 && R * 2 <= TTT_PRE_RMAX) R *= 2;
   const int lo = p.o_lo != nullptr;
   const int row_bytes = ((2 + lo + (p.step > 0)) * p.G + 2 * p.step) * D * 2;
-  for (int nr = std::max(R, (64 * 1024 / row_bytes) / R * R); nr >= R; nr -= R) {
+#ifndef TTT_PRE_STAGE_KB
+#define TTT_PRE_STAGE_KB 64
+#endif
+  for (int nr = std::max(R, (TTT_PRE_STAGE_KB * 1024 / row_bytes) / R * R); nr >= R; nr -= R) {
     if (nr * p.G > 256) continue;
     for (int ns = 4; ns >= 1; --ns) {
       lay->init(nr, p.G, D, p.step, ns, R, lo);
@@ -981,8 +1031,35 @@ bool pre_layout(const Params& p, int D, PreLayout* lay) {
   return false;
 }
 
+// dK_0 / dV_0 are accumulated by the main kernel; overwrite mode starts them at zero
+cudaError_t zero_dkv0(const Params& p, int D, cudaStream_t st) {
+  const size_t kvb = (size_t)p.B * p.L * p.Hkv * D * sizeof(float);
+  cudaError_t e = cudaMemsetAsync(p.dk, 0, kvb, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.dv, 0, kvb, st);
+  return e;
+}
+
+// 1. pre-pass (TMA-staged, persistent, warp-specialised); U: all steps of an unroll at once
+template <int D, bool U>
+cudaError_t launch_pre(const Params& p, const PreMaps& pmaps, const UnrollPre& up, cudaStream_t st) {
+  PreLayout lay;
+  if (!pre_layout(p, D, &lay)) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)lay.total);
+  if (e != cudaSuccess) return e;
+  const int rows = p.B * p.L * p.Hkv;
+  const int groups = (rows + lay.NR - 1) / lay.NR;
+  UnrollPre u = up;
+  if (U) u.M = std::max(lay.NS, 4);  // >= NS: the ring's own wait orders a group's steps
+  prof_mark(kKindBwdPre, true, st);
+  ttt_bwd_pre_kernel<D, U><<<std::min(groups, 148), 32 * (kPreCompute + 1), lay.total, st>>>(p, pmaps, u, lay);
+  prof_mark(kKindBwdPre, false, st);
+  return cudaGetLastError();
+}
+
+// 2. main tensor-core kernel, 3. dq = bf16(dq_acc)
 template <int D>
-cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st) {
+cudaError_t launch_main_convert(const Params& p_in, const BwdMaps& maps, cudaStream_t st) {
   Params p = p_in;
   p.head_split = pick_head_split(p);
   {  // CTA order: CTA kt of a group runs (nqt - kt) items of G / head_split heads; ~4.5k clk per
@@ -993,28 +1070,6 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, const PreMaps&
     p.order_batch = pick_order_batch(p.B * p.Hkv * p.head_split, p.nqt, 1, len.data(), 12.0,
                                      (double)nh * p.L * D * 8);
   }
-  // 1. pre-pass (TMA-staged, persistent, warp-specialised)
-  {
-    PreLayout lay;
-    if (!pre_layout(p, D, &lay)) return cudaErrorInvalidConfiguration;
-    if (!p.accumulate) {  // dK_0 / dV_0: the main kernel adds into them
-      const size_t kvb = (size_t)p.B * p.L * p.Hkv * D * sizeof(float);
-      cudaError_t e = cudaMemsetAsync(p.dk, 0, kvb, st);
-      if (e == cudaSuccess) e = cudaMemsetAsync(p.dv, 0, kvb, st);
-      if (e != cudaSuccess) return e;
-    }
-    cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)lay.total);
-    if (e != cudaSuccess) return e;
-    const int rows = p.B * p.L * p.Hkv;
-    const int groups = (rows + lay.NR - 1) / lay.NR;
-    prof_mark(kKindBwdPre, true, st);
-    ttt_bwd_pre_kernel<D><<<std::min(groups, 148), 32 * (kPreCompute + 1), lay.total, st>>>(p, pmaps, lay);
-    prof_mark(kKindBwdPre, false, st);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  // 2. main tensor-core kernel
   {
     const int smem = BwdSmem<D>::bytes;
     static bool attr_set = false;
@@ -1031,7 +1086,6 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, const PreMaps&
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  // 3. dq = bf16(dq_acc)
   {
     const size_t n8 = (size_t)p.B * p.L * p.Hq * D / 8;
     unsigned blocks = (unsigned)((n8 + 255) / 256);
@@ -1041,6 +1095,29 @@ cudaError_t launch_bwd_d(const Params& p_in, const BwdMaps& maps, const PreMaps&
     prof_mark(kKindBwdConvert, false, st);
     return cudaGetLastError();
   }
+}
+
+template <int D>
+cudaError_t launch_bwd_d(const Params& p, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st) {
+  cudaError_t e = p.accumulate ? cudaSuccess : zero_dkv0(p, D, st);
+  static const UnrollPre kNoUnroll{};
+  if (e == cudaSuccess) e = launch_pre<D, false>(p, pmaps, kNoUnroll, st);
+  if (e == cudaSuccess) e = launch_main_convert<D>(p, maps, st);
+  return e;
+}
+
+// Whole-unroll backward: ps[j] are the per-call parameter blocks of steps j = 0..S-1 (their own
+// delta / lse2 / dq_acc workspaces); ps[S-1] carries the unroll's accumulate flag and every step
+// list. Same results as the S calls j = S-1..0 (the first with that flag, the rest accumulating).
+template <int D>
+cudaError_t launch_bwd_unroll_d(const Params* ps, const BwdMaps* maps, const PreMaps& pmaps, const UnrollPre& up,
+                                cudaStream_t st) {
+  const int S = up.S;
+  const Params& last = ps[S - 1];
+  cudaError_t e = last.accumulate ? cudaSuccess : zero_dkv0(last, D, st);
+  if (e == cudaSuccess) e = launch_pre<D, true>(last, pmaps, up, st);
+  for (int j = S - 1; j >= 0 && e == cudaSuccess; --j) e = launch_main_convert<D>(ps[j], maps[j], st);
+  return e;
 }
 
 }  // namespace
@@ -1062,6 +1139,12 @@ int bwd_pre_rows_per_group(const Params& p) {
 
 cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st) {
   return p.D == 64 ? launch_bwd_d<64>(p, maps, pmaps, st) : launch_bwd_d<128>(p, maps, pmaps, st);
+}
+
+cudaError_t launch_bwd_unroll_sm100(const Params* ps, const BwdMaps* maps, const PreMaps& pmaps,
+                                    const UnrollPre& up, cudaStream_t st) {
+  return ps[0].D == 64 ? launch_bwd_unroll_d<64>(ps, maps, pmaps, up, st)
+                       : launch_bwd_unroll_d<128>(ps, maps, pmaps, up, st);
 }
 
 }  // namespace tttk

@@ -57,6 +57,18 @@ struct PreMaps {
   CUtensorMap dout, o, olo, q;                      // [B L Hq rows][D] bf16, box 64 x NR*G
   CUtensorMap k[TTT_MAX_STEPS], v[TTT_MAX_STEPS];  // [B L Hkv rows][D] bf16, box 64 x NR
 };
+// Unroll-level backward pre-pass (ttt_attn_bwd_unroll): per-step inputs / workspaces of the S
+// reverse-order calls, so one persistent pass covers every step's diagonal terms.
+constexpr int kMaxUnroll = TTT_MAX_UNROLL;
+struct UnrollPre {
+  int S;  // steps of the unroll: items j = S-1 .. 0 of every row group
+  int M;  // row groups per j-sweep (>= the stage count; see ttt_bwd_pre_kernel)
+  const float* lse_in[kMaxUnroll];
+  float* delta[kMaxUnroll];
+  float* lse2[kMaxUnroll];
+  float* dq_acc[kMaxUnroll];
+  CUtensorMap dout[kMaxUnroll], o[kMaxUnroll], olo[kMaxUnroll], q[kMaxUnroll];
+};
 struct DiagMaps {
   CUtensorMap q, out;
   CUtensorMap k[TTT_MAX_STEPS], v[TTT_MAX_STEPS];  // K_i, V_i as [B*L*Hkv rows][D], box 64 x NR

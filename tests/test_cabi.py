@@ -144,3 +144,31 @@ def test_loss_validation_codes(kw, call, code):
 def test_loss_workspace_size():
     assert ttt.ttt_loss_workspace_size(_loss_desc(rows=1000)) >= 1000 * 4
     assert ttt.ttt_loss_workspace_size(_loss_desc(rows=0)) == 0
+
+
+@pytest.mark.parametrize("S,ws,code", [(0, 1 << 30, 3), (9, 1 << 30, 3), (3, 64, 6)])
+def test_bwd_unroll_validation_codes(S, ws, code):
+    d = ttt.make_desc(1, 256, 4, 2, 128)
+    n = max(S, 1)
+    P = lambda i: FakeT(0x10000000 + 4096 * i)
+
+    class WS(FakeT):
+        def numel(self):
+            return ws
+
+        def element_size(self):
+            return 1
+    with pytest.raises(ttt.TTTError) as e:
+        ttt.ttt_attn_bwd_unroll(d, [P(i) for i in range(n)][:S] if S else [], P(20), P(21),
+                                [P(30 + i) for i in range(8)], [P(40 + i) for i in range(8)],
+                                [P(50 + i) for i in range(n)], [P(60 + i) for i in range(n)],
+                                [P(70 + i) for i in range(n)], [P(80 + i) for i in range(n)], P(90), P(91),
+                                [P(100 + i) for i in range(8)], [P(110 + i) for i in range(8)],
+                                workspace=WS(0x50000000))
+    assert e.value.code == code
+
+
+def test_bwd_unroll_workspace_size():
+    d = ttt.make_desc(8, 2048, 32, 8, 128)
+    assert ttt.ttt_attn_bwd_unroll_workspace_size(d, 7) == 7 * ttt.ttt_attn_workspace_size(d, 6, True)
+    assert ttt.ttt_attn_bwd_unroll_workspace_size(d, 9) == 0
