@@ -334,6 +334,8 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         line["e2e"] = run_e2e(u, stream, args, shape)
     if not args.no_loss:
         line["next_rows"] = {"loss_inplace": run_loss(args, stream, peaks, world)}
+        if world == 1:
+            line["next_rows"]["longctx"] = run_longctx(args, stream, peaks)
     if rank == 0 and world == 1 and not args.no_cpu:
         n, threads, run = oracle_sample(shape, target_s=15.0)
         sec = run(n)
@@ -399,6 +401,33 @@ def run_loss(args, stream, peaks, world: int):
                      "avg_launch_ms": avg, "algorithmic_bytes_per_launch": alg_bytes,
                      "traffic": ncu_traffic("ttt_loss_kernel")},
     }
+
+
+def run_longctx(args, stream, peaks):
+    """BASELINE.json configs[3] beside the headline: one 7-step unroll of a single L = 16384
+    sequence (Llama-3.1-8B draft heads), fwd + bwd, on one GPU. Across GPUs this shape splits by
+    kv-head block (dp.seq_to_head), each rank running this same kernel
+    sequence on Hq/N, Hkv/N heads."""
+    shape = CONFIGS["longctx"]
+    u = Unroll(shape, seed=99, dev=stream.device)
+    for _ in range(2):
+        u.step(stream)
+    torch.cuda.synchronize()
+    n = 3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        u.step(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    per_step_pairs, _ = alg_pairs(shape)
+    tflops = 12 * shape.head_dim * sum(per_step_pairs) / (ms / 1e3) / 1e12
+    del u
+    torch.cuda.empty_cache()
+    return {"workload": "long-context: 1 x L=16384, 32/8 heads, D=128, ttt_steps=7, bf16, fwd+bwd unroll",
+            "ms_per_step": ms, "tokens_per_s": shape.batch * shape.seq_len / (ms / 1e3), "steps": n,
+            "tflops": tflops, "frac_of_bf16_peak": tflops / peaks["bf16_tflops_sustained"]}
 
 
 def run_e2e(u: Unroll, stream, args, shape: Shape):

@@ -67,3 +67,38 @@ def max_over_ranks(x: float, device="cpu", group=None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+# ---- head-parallel long context (SURVEY.md §8(f) NEXT #3) --------------------------------------
+# A B = 1 sequence of L >= 16K cannot be split by sequence without an exchange inside the attention.
+# Split by kv-head group instead (Ulysses-style): the projections produce sequence shards
+# [L/N, H, D] per rank; one all-to-all turns them into head shards [L, H/N, D] (every query row,
+# a contiguous block of H/N heads — with Hkv % N == 0 a GQA group never straddles ranks), the TTT
+# attention runs locally on (Hq/N, Hkv/N) heads with no communication, and the inverse all-to-all
+# returns out / dq / dk / dv to sequence shards.
+
+def seq_to_head(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """[L/N, H, D] sequence shard (rank r holds rows r L/N ..) -> [L, H/N, D] head shard (rank r
+    holds heads r H/N ..). Collective over `group` (all ranks call it)."""
+    Ls, H, D = x.shape
+    if H % world:
+        raise ValueError("heads must divide by the world size")
+    send = x.reshape(Ls, world, H // world, D).permute(1, 0, 2, 3).contiguous()  # [dest rank][rows][h][d]
+    if world == 1:
+        return send.reshape(Ls, H, D)
+    recv = torch.empty_like(send)  # [source rank = row block][rows][h][d]
+    dist.all_to_all_single(recv, send, group=group)
+    return recv.reshape(world * Ls, H // world, D)
+
+
+def head_to_seq(y: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """Inverse of seq_to_head: [L, H/N, D] head shard -> [L/N, H, D] sequence shard."""
+    L, Hs, D = y.shape
+    if L % world:
+        raise ValueError("rows must divide by the world size")
+    send = y.reshape(world, L // world, Hs, D).contiguous()  # [dest rank = row block][rows][h][d]
+    if world == 1:
+        return send.reshape(L, Hs, D)
+    recv = torch.empty_like(send)  # [source rank = head block][rows][h][d]
+    dist.all_to_all_single(recv, send, group=group)
+    return recv.permute(1, 0, 2, 3).reshape(L // world, world * Hs, D)

@@ -68,3 +68,46 @@ def test_grad_buckets_allreduce_and_max_timing_world2():
         assert ok_avg, f"rank {rank}: bucketed all-reduce average wrong"
         assert t == 11.0, "max over ranks"
     assert res[0][3] == (0, 32) and res[1][3] == (32, 64)
+
+
+def _a2a_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_18567_b200.dp import head_to_seq, seq_to_head
+        L, H, D = 12, 8, 5
+        full = torch.arange(L * H * D, dtype=torch.float32).reshape(L, H, D)  # known to every rank
+        Ls, Hs = L // world, H // world
+        shard = full[rank * Ls:(rank + 1) * Ls].clone()
+        heads = seq_to_head(shard, world)
+        ok_fwd = torch.equal(heads, full[:, rank * Hs:(rank + 1) * Hs])
+        back = head_to_seq(heads * 2.0, world)
+        ok_inv = torch.equal(back, shard * 2.0)
+        q.put((rank, ok_fwd, ok_inv))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_head_parallel_all_to_all_world2():
+    """Ulysses-style exchange for head-parallel long context (dp.seq_to_head / head_to_seq):
+    rank r ends with every row of heads [r H/N, (r+1) H/N), and the inverse restores the shard."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok_fwd, ok_inv in res:
+        assert ok_fwd, f"rank {rank}: seq_to_head wrong"
+        assert ok_inv, f"rank {rank}: head_to_seq wrong"
+
+
+def test_head_parallel_single_rank_identity():
+    from paper_2603_18567_b200.dp import head_to_seq, seq_to_head
+    x = torch.randn(6, 4, 3)
+    assert torch.equal(seq_to_head(x, 1), x) and torch.equal(head_to_seq(x, 1), x)
