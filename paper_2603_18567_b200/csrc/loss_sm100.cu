@@ -72,11 +72,6 @@ struct VecT<float, 1> {
   using type = float;
 };
 
-__device__ __forceinline__ float elem(const uint4& v, int i, __nv_bfloat16*) {
-  const uint32_t w = (&v.x)[i >> 1];
-  return __uint_as_float((i & 1) ? (w & 0xffff0000u) : (w << 16));
-}
-__device__ __forceinline__ float elem(const uint4& v, int i, float*) { return __uint_as_float((&v.x)[i]); }
 __device__ __forceinline__ float elem(const __nv_bfloat16& v, int, __nv_bfloat16*) { return __bfloat162float(v); }
 __device__ __forceinline__ float elem(const float& v, int, float*) { return v; }
 
@@ -338,6 +333,58 @@ __global__ void __launch_bounds__(kLossThreads, (NV <= 4 ? 65536 / (kLossThreads
   if (cs > 1) cg::this_cluster().sync();  // no CTA leaves while its partials may still be read
 }
 
+// Persistent variant for rows that fit one CTA (z and p rows <= 64 KB each): the next row is
+// bulk-copied (cp.async.bulk, mbarrier completion) into shared memory while the current row is
+// reduced and written from registers, then moved smem -> registers in one conflict-free pass
+// and the row after it is requested. HBM reads stay in flight across row boundaries (the
+// one-row-per-CTA kernel leaves an SM's memory pipe idle from its last load to the next CTA's
+// first). 128 KB of smem + 128 registers: one 512-thread CTA per SM.
+template <typename T, int E, int NV>
+__global__ void __launch_bounds__(kLossThreads, 1) ttt_loss_ring_kernel(const LossParams P) {
+  using V = typename VecT<T, E>::type;
+  static_assert(E > 1, "vector path only");
+  __shared__ Stats parts[kLossThreads / 32];
+  __shared__ __align__(8) uint64_t landed;
+  extern __shared__ __align__(128) uint8_t ring[];  // [z row | p row], each padded to 16 B
+  const int nvec = P.vocab / E;
+  const uint32_t row_bytes = (uint32_t)P.vocab * (uint32_t)sizeof(T);
+  V* sz = reinterpret_cast<V*>(ring);
+  V* sp = reinterpret_cast<V*>(ring + row_bytes);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&landed, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto request = [&](int64_t row) {  // one thread
+    mbar_expect_tx(&landed, 2 * row_bytes);
+    bulk_load(sz, static_cast<const T*>(P.z) + (size_t)row * P.vocab, row_bytes, &landed);
+    bulk_load(sp, static_cast<const T*>(P.p) + (size_t)row * P.vocab, row_bytes, &landed);
+  };
+  int64_t row = blockIdx.x;
+  if (row >= P.rows) return;
+  if (tid == 0) request(row);
+  V zv[NV], pv[NV];
+  uint32_t phase = 0;
+  while (row < P.rows) {
+    mbar_wait(&landed, phase);
+    phase ^= 1u;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int idx = tid + i * kLossThreads;
+      if (idx < nvec) {
+        zv[i] = sz[idx];
+        pv[i] = sp[idx];
+      }
+    }
+    __syncthreads();  // the ring is free: every thread holds its share of this row
+    const int64_t next = row + gridDim.x;
+    if (tid == 0 && next < P.rows) request(next);
+    process_row<T, E, NV>(P, row, tid, nvec, 0, zv, pv, parts);
+    row = next;
+  }
+}
+
 // Masked-row count for TTT_LOSS_MEAN (one CTA; fixed order).
 __global__ void __launch_bounds__(1024) ttt_loss_count_kernel(const uint8_t* mask, int64_t rows, int* count) {
   __shared__ int part[32];
@@ -448,8 +495,31 @@ cudaError_t launch_loss_t(LossParams P, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, ttt_loss_kernel<T, E, NV>, P);
 }
 
+template <typename T, int E, int NV>
+cudaError_t launch_loss_ring_t(const LossParams& P, cudaStream_t st) {
+  const int smem = 2 * ((P.vocab * (int)sizeof(T) + 15) & ~15);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ttt_loss_ring_kernel<T, E, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         2 * 65536);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = P.rows < (int64_t)sms ? P.rows : (int64_t)sms;
+  ttt_loss_ring_kernel<T, E, NV><<<(unsigned)grid, kLossThreads, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
 template <typename T, int E>
 cudaError_t launch_loss_e(const LossParams& P, int nv, cudaStream_t st) {
+#ifndef TTT_LOSS_NO_RING
+  if constexpr (E > 1) {
+    if (P.cs == 1 && nv == 8 && P.vocab * (int)sizeof(T) <= 65536) return launch_loss_ring_t<T, E, 8>(P, st);
+  }
+#endif
   switch (nv) {
     case 1: return launch_loss_t<T, E, 1>(P, st);
     case 4: return launch_loss_t<T, E, 4>(P, st);
