@@ -336,6 +336,7 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         line["next_rows"] = {"loss_inplace": run_loss(args, stream, peaks, world)}
         if world == 1:
             line["next_rows"]["longctx"] = run_longctx(args, stream, peaks)
+        line["next_rows"]["tree_verify"] = run_tree(args, stream, peaks)
     if rank == 0 and world == 1 and not args.no_cpu:
         n, threads, run = oracle_sample(shape, target_s=15.0)
         sec = run(n)
@@ -401,6 +402,43 @@ def run_loss(args, stream, peaks, world: int):
                      "avg_launch_ms": avg, "algorithmic_bytes_per_launch": alg_bytes,
                      "traffic": ncu_traffic("ttt_loss_kernel")},
     }
+
+
+def run_tree(args, stream, peaks):
+    """SURVEY.md §8(f) NEXT #4, beside the headline: tree-attention verification (ttt_tree_attn_fwd)
+    with the Llama-3.1-8B target's attention heads (32 q / 8 kv, D = 128): 8 sequences, 4096
+    context tokens each, a 64-node draft tree per sequence (the inference-side use of EAGLE-3)."""
+    import paper_2603_18567_b200 as ttt
+    B, n, P, Hq, Hkv, D = 8, 64, 4096, 32, 8, 128
+    dev = stream.device
+    g = torch.Generator(device=dev).manual_seed(5)
+    mk = lambda *shp: torch.randn(shp, device=dev, generator=g).to(torch.bfloat16)
+    q, k, v = mk(B, n, Hq, D), mk(B, P + n, Hkv, D), mk(B, P + n, Hkv, D)
+    par = torch.randint(0, 1 << 20, (B, n), device=dev, generator=g)
+    parents = torch.where(torch.arange(n, device=dev) > 0, par % torch.arange(n, device=dev).clamp(min=1), -1)
+    parents = parents.to(torch.int32).contiguous()
+    out = torch.empty_like(q)
+    lse = torch.empty(B, Hq, n, device=dev)
+    d = ttt.tree_desc(B, n, P + n, Hq, Hkv, D, [P] * B)
+    ws = torch.empty(ttt.ttt_tree_attn_workspace_size(d), dtype=torch.uint8, device=dev)
+    one = lambda: ttt.ttt_tree_attn_fwd(d, q, k, v, parents, out, lse, ws, stream=stream)
+    for _ in range(3):
+        one()
+    torch.cuda.synchronize()
+    iters = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(iters):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    kv_bytes = 2 * B * (P + n) * Hkv * D * 2
+    return {"workload": f"{B} seqs x {P} context + {n}-node draft tree, 32/8 heads, D=128, bf16 (target verify)",
+            "ms_per_call": ms, "tree_tokens_per_s": B * n / (ms / 1e3),
+            "roofline": {"bound": "hbm", "achieved": (kv_bytes + 2 * 2 * B * n * Hq * D) / (ms / 1e3) / 1e9,
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "note": "K/V cache read once; 128 CTAs (8 seqs x 8 kv heads x 2 head pairs) < 148 SMs"}}
 
 
 def run_longctx(args, stream, peaks):

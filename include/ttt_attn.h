@@ -158,6 +158,31 @@ int ttt_attn_bwd_unroll(const ttt_attn_desc* desc, int num_steps,
                         float* dk_base, float* dv_base, float* const* dk_steps, float* const* dv_steps,
                         unsigned flags, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Tree-attention verification (inference side) ----------------
+ * The target's forward over a draft token tree: query t (tree node t, t < num_tree) attends every
+ * context key of its sequence (rows [0, P_b) of the cache) and the cache rows P_b + u of its
+ * ancestors u and itself — "each candidate token attends only to its ancestors" (
+ * SPEC.md:507-509, 528; readings R21-R22). Same tcgen05 pipeline as ttt_attn_fwd.
+ *   q        bf16 [batch][num_tree][Hq][D]             in   (the tree tokens' queries)
+ *   k_cache, v_cache bf16 [batch][kv_len][Hkv][D]      in   (prefix rows then the tree's own rows)
+ *   parents  DEVICE int32 [batch][num_tree]            in   parent node index, -1 = child of the
+ *            context tip; nodes in topological order (a parent index >= t is treated as -1)
+ *   out      bf16 [batch][num_tree][Hq][D]             out
+ *   lse      fp32 [batch][Hq][num_tree]                out  natural-log logsumexp over the allowed keys
+ *   workspace >= ttt_tree_attn_workspace_size(desc) bytes (the per-node ancestor bit masks).
+ * Errors: 1 <= num_tree <= TTT_MAX_TREE, 0 <= prefix_lens[b], prefix_lens[b] + num_tree <= kv_len
+ * (else TTT_ERR_DEGENERATE), head_dim 64 / 128; BF16 only. */
+#define TTT_MAX_TREE 64
+typedef struct {
+  int32_t batch, num_tree, kv_len, num_q_heads, num_kv_heads, head_dim;
+  float softmax_scale;         /* 0 => 1/sqrt(head_dim) */
+  const int32_t* prefix_lens;  /* HOST int32[batch]: P_b, the verified context length */
+} ttt_tree_desc;
+size_t ttt_tree_attn_workspace_size(const ttt_tree_desc* desc);
+int ttt_tree_attn_fwd(const ttt_tree_desc* desc, const void* q, const void* k_cache, const void* v_cache,
+                      const int32_t* parents, void* out, float* lse, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
 /* ---- Optional instrumentation (off by default; used by bench.py) ----------
  * ttt_attn_profile_begin() arms per-kernel timing for the CALLING HOST THREAD:
  * each kernel the library launches afterwards is bracketed by cudaEventRecord

@@ -12,4 +12,5 @@ from ._lib import (  # noqa: F401
     ttt_attn_workspace_size, ttt_attn_profile_begin, ttt_attn_profile_end, ttt_attn_kernel_name,
     TTT_LOSS_MEAN, LossDesc, loss_desc_for, ttt_loss_workspace_size, ttt_loss_fwd, ttt_loss_bwd_inplace,
     ttt_loss_fwd_bwd_inplace, TTT_MAX_UNROLL, ttt_attn_bwd_unroll, ttt_attn_bwd_unroll_workspace_size,
+    TTT_MAX_TREE, TreeDesc, tree_desc, ttt_tree_attn_fwd, ttt_tree_attn_workspace_size,
 )

@@ -43,6 +43,16 @@ class Desc(ctypes.Structure):
     ]
 
 
+class TreeDesc(ctypes.Structure):
+    """ttt_tree_desc (include/ttt_attn.h)."""
+    _fields_ = [("batch", ctypes.c_int32), ("num_tree", ctypes.c_int32), ("kv_len", ctypes.c_int32),
+                ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("softmax_scale", ctypes.c_float), ("prefix_lens", ctypes.POINTER(ctypes.c_int32))]
+
+
+TTT_MAX_TREE = 64
+
+
 class LossDesc(ctypes.Structure):
     """ttt_loss_desc (include/ttt_loss.h)."""
     _fields_ = [("rows", ctypes.c_int64), ("vocab", ctypes.c_int32), ("dtype", ctypes.c_int32)]
@@ -69,6 +79,11 @@ def _load():
     lib.ttt_attn_bwd_unroll_workspace_size.restype = sz
     lib.ttt_attn_bwd_unroll.argtypes = [pd, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, u, vp, sz, vp]
     lib.ttt_attn_bwd_unroll.restype = i
+    ptd = ctypes.POINTER(TreeDesc)
+    lib.ttt_tree_attn_workspace_size.argtypes = [ptd]
+    lib.ttt_tree_attn_workspace_size.restype = sz
+    lib.ttt_tree_attn_fwd.argtypes = [ptd, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.ttt_tree_attn_fwd.restype = i
     lib.ttt_attn_strerror.argtypes = [i]
     lib.ttt_attn_strerror.restype = ctypes.c_char_p
     lib.ttt_attn_version.argtypes = []
@@ -214,6 +229,29 @@ def ttt_attn_bwd_unroll(desc: Desc, q: Sequence, k_base, v_base, k_steps, v_step
         _ptr_list(v_steps[:S - 1]), _ptr_list(out), None if out_lo is None else _ptr_list(out_lo), _ptr_list(lse),
         _ptr_list(dout), _ptr_list(dq), _ptr(dk_base), _ptr(dv_base), _ptr_list(dk_steps[:S - 1]),
         _ptr_list(dv_steps[:S - 1]), int(flags), _ptr(workspace), ws_bytes, _stream(stream)))
+
+
+
+def tree_desc(batch: int, num_tree: int, kv_len: int, num_q_heads: int, num_kv_heads: int, head_dim: int,
+              prefix_lens: Sequence[int], softmax_scale: float = 0.0) -> TreeDesc:
+    d = TreeDesc()
+    d.batch, d.num_tree, d.kv_len = int(batch), int(num_tree), int(kv_len)
+    d.num_q_heads, d.num_kv_heads, d.head_dim = int(num_q_heads), int(num_kv_heads), int(head_dim)
+    d.softmax_scale = float(softmax_scale)
+    arr = (ctypes.c_int32 * int(batch))(*[int(x) for x in prefix_lens])
+    d._keepalive = arr
+    d.prefix_lens = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32))
+    return d
+
+
+def ttt_tree_attn_workspace_size(desc: TreeDesc) -> int:
+    return int(_lib.ttt_tree_attn_workspace_size(ctypes.byref(desc)))
+
+
+def ttt_tree_attn_fwd(desc: TreeDesc, q, k_cache, v_cache, parents, out, lse, workspace, stream=None) -> None:
+    """Enqueue ttt_tree_attn_fwd (include/ttt_attn.h): tree-attention verification forward."""
+    _check(_lib.ttt_tree_attn_fwd(ctypes.byref(desc), _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(parents),
+                                  _ptr(out), _ptr(lse), _ptr(workspace), _nbytes(workspace), _stream(stream)))
 
 
 # ---- masked soft-label log-softmax loss + Alg. 3 in-place backward (include/ttt_loss.h) ----

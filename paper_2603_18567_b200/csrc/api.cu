@@ -21,6 +21,7 @@ cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, const DiagMap
 int fwd_diag_rows_per_group(const Params& p);
 cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st);
 int bwd_pre_rows_per_group(const Params& p);
+cudaError_t launch_tree_sm100(const Params& p, const FwdMaps& maps, const int32_t* parents, cudaStream_t st);
 cudaError_t launch_bwd_unroll_sm100(const Params* ps, const BwdMaps* maps, const PreMaps& pmaps,
                                     const UnrollPre& up, cudaStream_t st);
 }  // namespace tttk
@@ -425,6 +426,60 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
         return TTT_ERR_CUDA;
   }
   return cuda_status(launch_bwd_sm100(p, maps, pmaps, s));
+}
+
+size_t ttt_tree_attn_workspace_size(const ttt_tree_desc* d) {
+  if (!d || d->batch < 1 || d->num_tree < 1 || d->num_tree > TTT_MAX_TREE) return 0;
+  return align256((size_t)d->batch * d->num_tree * 8);
+}
+
+int ttt_tree_attn_fwd(const ttt_tree_desc* d, const void* q, const void* k_cache, const void* v_cache,
+                      const int32_t* parents, void* out, float* lse, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+  if (!d || !q || !k_cache || !v_cache || !parents || !out || !lse || !d->prefix_lens) return TTT_ERR_INVALID_ARG;
+  if (d->batch < 1 || d->batch > TTT_MAX_BATCH || d->num_tree < 1 || d->kv_len < 1 || d->num_q_heads < 1 ||
+      d->num_kv_heads < 1 || d->num_q_heads % d->num_kv_heads)
+    return TTT_ERR_INVALID_ARG;
+  if (d->num_tree > TTT_MAX_TREE) return TTT_ERR_UNSUPPORTED;
+  if (d->head_dim != 64 && d->head_dim != 128) return TTT_ERR_UNSUPPORTED;
+  if (d->num_q_heads / d->num_kv_heads > 32) return TTT_ERR_UNSUPPORTED;
+  if (!(d->softmax_scale >= 0.f) || std::isinf(d->softmax_scale)) return TTT_ERR_INVALID_ARG;
+  if ((long long)d->batch * d->kv_len * d->num_kv_heads >= (1ll << 31)) return TTT_ERR_UNSUPPORTED;
+  for (int b = 0; b < d->batch; ++b)
+    if (d->prefix_lens[b] < 0 || d->prefix_lens[b] + d->num_tree > d->kv_len) return TTT_ERR_DEGENERATE;
+  const void* ptrs[] = {q, k_cache, v_cache, out, lse};
+  for (const void* ptr : ptrs)
+    if (!aligned16(ptr)) return TTT_ERR_ALIGNMENT;
+  if (!workspace || workspace_bytes < ttt_tree_attn_workspace_size(d)) return TTT_ERR_WORKSPACE;
+  if (!aligned16(workspace)) return TTT_ERR_ALIGNMENT;
+  Params p;
+  std::memset(&p, 0, sizeof(p));
+  p.B = d->batch;
+  p.L = d->num_tree;
+  p.Hq = d->num_q_heads;
+  p.Hkv = d->num_kv_heads;
+  p.D = d->head_dim;
+  p.G = p.Hq / p.Hkv;
+  p.step = 0;
+  p.nqt = 1;
+  p.scale = d->softmax_scale > 0.f ? d->softmax_scale : 1.0f / std::sqrt((float)p.D);
+  p.scale_log2 = p.scale * 1.4426950408889634f;
+  for (int b = 0; b < p.B; ++b) p.seq_lens[b] = d->prefix_lens[b];
+  p.tree_n = d->num_tree;
+  p.tree_mask = static_cast<const unsigned long long*>(workspace);
+  p.q = q;
+  p.k = k_cache;
+  p.v = v_cache;
+  p.out = out;
+  p.out_lo = nullptr;
+  p.lse = lse;
+  FwdMaps maps;
+  if (!encode_bshd(&maps.q, q, p.B, d->num_tree, p.Hq, p.D) ||
+      !encode_bshd(&maps.k, k_cache, p.B, d->kv_len, p.Hkv, p.D) ||
+      !encode_bshd(&maps.v, v_cache, p.B, d->kv_len, p.Hkv, p.D) ||
+      !encode_bshd(&maps.out, out, p.B, d->num_tree, p.Hq, p.D))
+    return TTT_ERR_CUDA;
+  return cuda_status(launch_tree_sm100(p, maps, parents, static_cast<cudaStream_t>(stream)));
 }
 
 size_t ttt_attn_bwd_unroll_workspace_size(const ttt_attn_desc* d, int num_steps) {

@@ -59,7 +59,11 @@ struct FwdBars {
   uint32_t tmem_base;
 };
 
-template <int D>
+// TREE = true: tree-attention verification (ttt_tree_attn_fwd) on the
+// same pipeline: one q tile of the n <= 64 tree tokens per (b, head pair); keys = the prefix
+// (all allowed) followed by the tree tokens' own keys, allowed per query row by its
+// ancestor-or-self bit mask; no diagonal step keys.
+template <int D, bool TREE>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     ttt_fwd_sm100_kernel(const __grid_constant__ Params p, const __grid_constant__ FwdMaps maps) {
   constexpr int TB = kTile * D * 2;  // bytes of one 128 x D bf16 tile
@@ -95,8 +99,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #endif
   const int h0 = g * p.G + 2 * hp;
   const bool has1 = (2 * hp + 1) < p.G;
-  const int T = p.seq_lens[b];
-  const int nkv = min(qt + 1, (T + kTile - 1) / kTile);  // BlockMask: skip k0 > q0+127 and k0 >= T
+  const int T = p.seq_lens[b];  // TREE: prefix length P_b
+  const int nkv = TREE ? (T + p.tree_n + kTile - 1) / kTile
+                       : min(qt + 1, (T + kTile - 1) / kTile);  // BlockMask: skip k0 > q0+127 and k0 >= T
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.q, 1);
@@ -246,6 +251,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const uint32_t tO = tbase + lane_off + 256 + slot * 128;
       const float sl2 = p.scale_log2;
       float m_run = -INFINITY, l_run = 0.f;
+      // TREE: this row's ancestor-or-self mask (rows >= n are tile padding)
+      const bool tree_row = TREE && r < p.tree_n;
+      const unsigned long long tree_am = tree_row ? p.tree_mask[(size_t)b * p.tree_n + r] : 0ull;
       TTT_TRACE_DECL(1);
       TTT_TRACE_DECL(2);
       for (int n = 0; n < nkv; ++n) {
@@ -256,18 +264,43 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         uint32_t raw[128];
         tmem_ld128(tS, raw);
         const int kv0 = n * kTile;
-        const bool partial = (n == qt) || (kv0 + kTile > T);
+        const bool partial = TREE ? (kv0 + kTile > T) : ((n == qt) || (kv0 + kTile > T));
         // row max of the raw scores (scale > 0 commutes with max): 8 independent chains of
         // 3-input max (FMNMX3), two new columns per instruction
         float mx8[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
         if (partial) {
-          const int lim = min(r + 1, T) - kv0;  // allowed columns c < lim  (k <= r and k < T)
+          if constexpr (TREE) {
+            // column c = key kv0 + c: prefix key (< P) or tree key u = kv0 + c - P of this row's
+            // ancestor-or-self mask; rows past the tree (padding of the tile) keep key 0 only
+            uint32_t w[4];
+            const unsigned long long am = tree_am;
 #pragma unroll
-          for (int c = 0; c < 128; ++c) {
-            const float x = c < lim ? __uint_as_float(raw[c]) : -INFINITY;
-            raw[c] = __float_as_uint(x);
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int c0 = q4 * 32, lo = T - kv0 - c0;  // columns c0 + i < lo are prefix keys
+              uint32_t pre = lo >= 32 ? 0xffffffffu : (lo <= 0 ? 0u : ((1u << lo) - 1u));
+              // tree bits: column c0 + i holds u = c0 + i - (T - kv0) = i - lo
+              uint32_t tb = 0u;
+              if (lo < 32 && lo > -64) {
+                const int sh = lo;  // bit i of tb = bit (i - sh) of am
+                tb = sh >= 0 ? (uint32_t)(am << sh) : (uint32_t)(am >> (-sh));
+              }
+              w[q4] = pre | tb;
+            }
+            if (!tree_row) w[0] = w[1] = w[2] = w[3] = 0u, w[0] = (kv0 == 0) ? 1u : 0u;
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+              const float x = ((w[c >> 5] >> (c & 31)) & 1u) ? __uint_as_float(raw[c]) : -INFINITY;
+              raw[c] = __float_as_uint(x);
+            }
+          } else {
+            const int lim = min(r + 1, T) - kv0;  // allowed columns c < lim  (k <= r and k < T)
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+              const float x = c < lim ? __uint_as_float(raw[c]) : -INFINITY;
+              raw[c] = __float_as_uint(x);
+            }
           }
         }
 #pragma unroll
@@ -355,7 +388,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // by ttt_fwd_diag_kernel into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum); the
       // merge is the same online-softmax update as one more "tile".
       const size_t lse_idx = ((size_t)b * p.Hq + h) * p.L + r;
-      const bool has_diag = (r < T) && (p.step > 0);
+      const bool has_diag = !TREE && (r < T) && (p.step > 0);
       const float A_d = has_diag ? p.lse[lse_idx] : -INFINITY;
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, 0);
       mbar_wait(&bars.o_full[slot], 0);
@@ -414,7 +447,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
         }
       }
-      p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
+      if (!TREE || tree_row) p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 6, 0);
       fence_async_smem();
       named_bar_sync(1 + slot, 128);
@@ -700,7 +733,7 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
   const int smem = 6 * kTile * D * 2 + 1024;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(ttt_fwd_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(ttt_fwd_sm100_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -719,7 +752,7 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
   const int npairs = (p.G + 1) / 2;
   const int grid = p.nqt * p.B * p.Hkv * npairs;
   prof_mark(kKindFwdMain, true, st);
-  ttt_fwd_sm100_kernel<D><<<grid, kFwdThreads, smem, st>>>(p, maps);
+  ttt_fwd_sm100_kernel<D, false><<<grid, kFwdThreads, smem, st>>>(p, maps);
   prof_mark(kKindFwdMain, false, st);
   return cudaGetLastError();
 }
@@ -733,6 +766,49 @@ int fwd_diag_rows_per_group(const Params& p) {
 
 cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, const DiagMaps& dmaps, cudaStream_t st) {
   return p.D == 64 ? launch_fwd_d<64>(p, maps, dmaps, st) : launch_fwd_d<128>(p, maps, dmaps, st);
+}
+
+// ancestor-or-self masks of the draft trees (parents precede children); a parent
+// index that is not an earlier node ends the walk (the node then hangs off the context tip)
+__global__ void ttt_tree_mask_kernel(const int32_t* parents, int B, int n, unsigned long long* mask) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B * n) return;
+  const int b = i / n, t = i - b * n;
+  const int32_t* par = parents + (size_t)b * n;
+  unsigned long long m = 1ull << t;
+  int u = par[t], prev = t;
+  while (u >= 0 && u < prev) {
+    m |= 1ull << u;
+    prev = u;
+    u = par[u];
+  }
+  mask[i] = m;
+}
+
+template <int D>
+cudaError_t launch_tree_d(const Params& p_in, const FwdMaps& maps, const int32_t* parents, cudaStream_t st) {
+  Params p = p_in;
+  p.nqt = 1;
+  p.order_batch = p.B * p.Hkv;
+  const int smem = 6 * kTile * D * 2 + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(ttt_fwd_sm100_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int nm = p.B * p.tree_n;
+  ttt_tree_mask_kernel<<<(nm + 127) / 128, 128, 0, st>>>(parents, p.B, p.tree_n,
+                                                        const_cast<unsigned long long*>(p.tree_mask));
+  const int grid = p.B * p.Hkv * ((p.G + 1) / 2);
+  prof_mark(kKindFwdMain, true, st);
+  ttt_fwd_sm100_kernel<D, true><<<grid, kFwdThreads, smem, st>>>(p, maps);
+  prof_mark(kKindFwdMain, false, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tree_sm100(const Params& p, const FwdMaps& maps, const int32_t* parents, cudaStream_t st) {
+  return p.D == 64 ? launch_tree_d<64>(p, maps, parents, st) : launch_tree_d<128>(p, maps, parents, st);
 }
 
 }  // namespace tttk

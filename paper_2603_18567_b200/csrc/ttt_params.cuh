@@ -45,6 +45,9 @@ struct Params {
   float* lse2;    // workspace [B][Hq][L]: -lse * log2(e)           (stored negated)
   float* dq_acc;  // workspace fp32, tile-contiguous [B][Hq][L/128][D/32][128][32]
   int seq_lens[TTT_MAX_BATCH];
+  // tree-attention verification (ttt_tree_attn_fwd): seq_lens = prefix lengths, L = tree size
+  int tree_n;                              // n tree tokens (queries), <= 64
+  const unsigned long long* tree_mask;     // [B][n] ancestor-or-self bit masks (bit u = tree key u)
 };
 
 // Tensor maps for the tcgen05 paths (4-D: D, H, L, B; box 64 x 1 x 128 x 1, SW128)

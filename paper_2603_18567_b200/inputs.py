@@ -172,3 +172,33 @@ def make_loss_case(rows: int, vocab: int, dtype: torch.dtype = torch.bfloat16, s
             mask[0] = 1
     g_rows = rm.uniform(0.5, 1.5, size=rows).astype(np.float32)
     return LossCase(z, p, torch.from_numpy(mask), torch.from_numpy(g_rows))
+
+
+# ---- tree-attention verification inputs ----
+
+@dataclass
+class TreeCase:
+    q: torch.Tensor        # [B, n, Hq, D]
+    k: torch.Tensor        # [B, Lk, Hkv, D]: prefix rows then the tree's own rows
+    v: torch.Tensor
+    parents: torch.Tensor  # int32 [B, n], topological (parent < child), -1 = context tip
+    prefix_lens: list
+
+
+def make_tree_case(batch: int, n: int, prefix_lens, num_q_heads: int, num_kv_heads: int, head_dim: int,
+                   dtype=torch.bfloat16, seed: int = 0, kv_len=None) -> TreeCase:
+    """Seeded draft trees: node t's parent is uniform over {-1, 0, .., t-1} with -1 drawn at
+    probability 1/8 (EAGLE-style wide-and-shallow trees hang most nodes off a few roots);
+    q, k, v ~ N(0, 1) -> storage dtype; rows past P_b + n of the cache are noise (never attended).
+    Seeds: tensors `seed`, parents `seed + 1`."""
+    rng = np.random.default_rng(seed)
+    Lk = kv_len or (max(prefix_lens) + n)
+    q = to_storage(_normal(rng, (batch, n, num_q_heads, head_dim)), dtype)
+    k = to_storage(_normal(rng, (batch, Lk, num_kv_heads, head_dim)), dtype)
+    v = to_storage(_normal(rng, (batch, Lk, num_kv_heads, head_dim)), dtype)
+    rp = np.random.default_rng(seed + 1)
+    par = np.full((batch, n), -1, dtype=np.int32)
+    for b in range(batch):
+        for t in range(1, n):
+            par[b, t] = -1 if rp.random() < 0.125 else int(rp.integers(0, t))
+    return TreeCase(q, k, v, torch.from_numpy(par), [int(x) for x in prefix_lens])

@@ -18,7 +18,7 @@ def _declared_functions():
     for fn in os.listdir(os.path.join(ROOT, "include")):
         if fn.endswith(".h"):
             src = open(os.path.join(ROOT, "include", fn)).read()
-            names += re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(ttt_(?:attn|loss)_\w+)\s*\(", src, re.M)
+            names += re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(ttt_(?:attn|loss|tree)_\w+)\s*\(", src, re.M)
     return sorted(set(names))
 
 
@@ -172,3 +172,22 @@ def test_bwd_unroll_workspace_size():
     d = ttt.make_desc(8, 2048, 32, 8, 128)
     assert ttt.ttt_attn_bwd_unroll_workspace_size(d, 7) == 7 * ttt.ttt_attn_workspace_size(d, 6, True)
     assert ttt.ttt_attn_bwd_unroll_workspace_size(d, 9) == 0
+
+
+@pytest.mark.parametrize("kw,code", [(dict(num_tree=65), 2), (dict(num_tree=0), 1), (dict(head_dim=96), 2),
+                                     (dict(prefix=[100, 4097]), 5), (dict(prefix=[-1, 0]), 5),
+                                     (dict(ws=8), 6)])
+def test_tree_validation_codes(kw, code):
+    n = kw.get("num_tree", 8)
+    d = ttt.tree_desc(2, n, 4104, 4, 2, kw.get("head_dim", 128), kw.get("prefix", [100, 200]))
+    P = lambda i: FakeT(0x10000000 + 4096 * i)
+
+    class WS(FakeT):
+        def numel(self):
+            return kw.get("ws", 4096)
+
+        def element_size(self):
+            return 1
+    with pytest.raises(ttt.TTTError) as e:
+        ttt.ttt_tree_attn_fwd(d, P(0), P(1), P(2), P(3), P(4), P(5), WS(0x50000000))
+    assert e.value.code == code
