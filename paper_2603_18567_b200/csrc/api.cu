@@ -22,6 +22,8 @@ int fwd_diag_rows_per_group(const Params& p);
 cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st);
 int bwd_pre_rows_per_group(const Params& p);
 cudaError_t launch_tree_sm100(const Params& p, const FwdMaps& maps, const int32_t* parents, cudaStream_t st);
+cudaError_t launch_tree_combine(const void* part, const float* lse_part, int nsplit, int B, int n, int Hq, int D,
+                                void* out, float* lse, cudaStream_t st);
 cudaError_t launch_bwd_unroll_sm100(const Params* ps, const BwdMaps* maps, const PreMaps& pmaps,
                                     const UnrollPre& up, cudaStream_t st);
 }  // namespace tttk
@@ -428,9 +430,38 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
   return cuda_status(launch_bwd_sm100(p, maps, pmaps, s));
 }
 
+// Context splits per (sequence, kv head, head pair), only when those CTAs would leave more than
+// half of the 148 SMs idle: enough splits for about one CTA per SM, at most one per kv tile of the
+// shortest sequence (splits are never empty), at most 16. (Measured: splitting 128 CTAs into
+// 3 x 128 was slower, 98 vs 75 us, each CTA's fixed cost repeating per split.)
+int tree_splits(const ttt_tree_desc* d) {
+  const int base = d->batch * d->num_kv_heads * ((d->num_q_heads / d->num_kv_heads + 1) / 2);
+  if (2 * base > 148) return 1;
+  int min_tiles = 1 << 30;
+  for (int b = 0; b < d->batch; ++b) min_tiles = std::min(min_tiles, (d->prefix_lens[b] + d->num_tree + 127) / 128);
+  const int s = 148 / base;
+  return std::max(1, std::min(std::min(s, 16), min_tiles));
+}
+struct TreeWs {
+  size_t mask, part, lse, total;
+  int splits;
+};
+TreeWs tree_ws_layout(const ttt_tree_desc* d) {
+  TreeWs w{};
+  w.splits = tree_splits(d);
+  w.mask = 0;
+  w.part = align256((size_t)d->batch * d->num_tree * 8);
+  w.lse = w.part;
+  if (w.splits > 1) w.lse += align256((size_t)w.splits * d->batch * d->num_tree * d->num_q_heads * d->head_dim * 2);
+  w.total = w.lse + (w.splits > 1 ? align256((size_t)w.splits * d->batch * d->num_q_heads * d->num_tree * 4) : 0);
+  return w;
+}
+
 size_t ttt_tree_attn_workspace_size(const ttt_tree_desc* d) {
-  if (!d || d->batch < 1 || d->num_tree < 1 || d->num_tree > TTT_MAX_TREE) return 0;
-  return align256((size_t)d->batch * d->num_tree * 8);
+  if (!d || !d->prefix_lens || d->batch < 1 || d->batch > TTT_MAX_BATCH || d->num_tree < 1 ||
+      d->num_tree > TTT_MAX_TREE || d->num_kv_heads < 1 || d->num_q_heads < d->num_kv_heads)
+    return 0;
+  return tree_ws_layout(d).total;
 }
 
 int ttt_tree_attn_fwd(const ttt_tree_desc* d, const void* q, const void* k_cache, const void* v_cache,
@@ -450,7 +481,8 @@ int ttt_tree_attn_fwd(const ttt_tree_desc* d, const void* q, const void* k_cache
   const void* ptrs[] = {q, k_cache, v_cache, out, lse};
   for (const void* ptr : ptrs)
     if (!aligned16(ptr)) return TTT_ERR_ALIGNMENT;
-  if (!workspace || workspace_bytes < ttt_tree_attn_workspace_size(d)) return TTT_ERR_WORKSPACE;
+  const TreeWs tw = tree_ws_layout(d);
+  if (!workspace || workspace_bytes < tw.total) return TTT_ERR_WORKSPACE;
   if (!aligned16(workspace)) return TTT_ERR_ALIGNMENT;
   Params p;
   std::memset(&p, 0, sizeof(p));
@@ -466,20 +498,28 @@ int ttt_tree_attn_fwd(const ttt_tree_desc* d, const void* q, const void* k_cache
   p.scale_log2 = p.scale * 1.4426950408889634f;
   for (int b = 0; b < p.B; ++b) p.seq_lens[b] = d->prefix_lens[b];
   p.tree_n = d->num_tree;
-  p.tree_mask = static_cast<const unsigned long long*>(workspace);
+  char* wsb = static_cast<char*>(workspace);
+  p.tree_mask = reinterpret_cast<const unsigned long long*>(wsb + tw.mask);
+  p.tree_splits = tw.splits;
+  void* part = tw.splits > 1 ? static_cast<void*>(wsb + tw.part) : out;      // per-split partial outputs
+  float* lse_part = tw.splits > 1 ? reinterpret_cast<float*>(wsb + tw.lse) : lse;
   p.q = q;
   p.k = k_cache;
   p.v = v_cache;
-  p.out = out;
+  p.out = part;
   p.out_lo = nullptr;
-  p.lse = lse;
+  p.lse = lse_part;
   FwdMaps maps;
   if (!encode_bshd(&maps.q, q, p.B, d->num_tree, p.Hq, p.D) ||
       !encode_bshd(&maps.k, k_cache, p.B, d->kv_len, p.Hkv, p.D) ||
       !encode_bshd(&maps.v, v_cache, p.B, d->kv_len, p.Hkv, p.D) ||
-      !encode_bshd(&maps.out, out, p.B, d->num_tree, p.Hq, p.D))
+      !encode_bshd(&maps.out, part, p.B * tw.splits, d->num_tree, p.Hq, p.D))
     return TTT_ERR_CUDA;
-  return cuda_status(launch_tree_sm100(p, maps, parents, static_cast<cudaStream_t>(stream)));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_tree_sm100(p, maps, parents, s);
+  if (e == cudaSuccess && tw.splits > 1)
+    e = launch_tree_combine(part, lse_part, tw.splits, p.B, d->num_tree, p.Hq, p.D, out, lse, s);
+  return cuda_status(e);
 }
 
 size_t ttt_attn_bwd_unroll_workspace_size(const ttt_attn_desc* d, int num_steps) {

@@ -83,25 +83,43 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int npairs = (p.G + 1) >> 1;
   const int hp = (int)blockIdx.x % npairs;
   const int t_ = (int)blockIdx.x / npairs;
+  int qt, g, b, split = 0;
+  if constexpr (TREE) {  // (split of the context, b, g); the q tile is the tree
+    const int gi = t_ % (p.B * p.Hkv);
+    split = t_ / (p.B * p.Hkv);
+    qt = 0;
+    g = gi % p.Hkv;
+    b = gi / p.Hkv;
+  } else {
 #ifdef TTT_ORDER_GROUP
-  const int qt = p.nqt - 1 - t_ % p.nqt;
-  const int g = (t_ / p.nqt) % p.Hkv;
-  const int b = t_ / (p.nqt * p.Hkv);
+    qt = p.nqt - 1 - t_ % p.nqt;
+    g = (t_ / p.nqt) % p.Hkv;
+    b = t_ / (p.nqt * p.Hkv);
 #else
-  // batched longest-first: (b, g) groups in batches of p.order_batch, q tile slowest inside a batch
-  const int ngrp = p.B * p.Hkv, bsz = p.order_batch * p.nqt;
-  const int bat = t_ / bsz, gbase = bat * p.order_batch;
-  const int gb = min(p.order_batch, ngrp - gbase), rr = t_ - bat * bsz;
-  const int qt = p.nqt - 1 - rr / gb;
-  const int gi = gbase + rr % gb;
-  const int g = gi % p.Hkv;
-  const int b = gi / p.Hkv;
+    // batched longest-first: (b, g) groups in batches of p.order_batch, q tile slowest inside a batch
+    const int ngrp = p.B * p.Hkv, bsz = p.order_batch * p.nqt;
+    const int bat = t_ / bsz, gbase = bat * p.order_batch;
+    const int gb = min(p.order_batch, ngrp - gbase), rr = t_ - bat * bsz;
+    qt = p.nqt - 1 - rr / gb;
+    const int gi = gbase + rr % gb;
+    g = gi % p.Hkv;
+    b = gi / p.Hkv;
 #endif
+  }
   const int h0 = g * p.G + 2 * hp;
   const bool has1 = (2 * hp + 1) < p.G;
   const int T = p.seq_lens[b];  // TREE: prefix length P_b
-  const int nkv = TREE ? (T + p.tree_n + kTile - 1) / kTile
-                       : min(qt + 1, (T + kTile - 1) / kTile);  // BlockMask: skip k0 > q0+127 and k0 >= T
+  // TREE: kv tiles [kvt0, kvt0 + nkv) of this context split (balanced, never empty: host keeps
+  // splits <= tiles); the tree result of a split goes to partial buffers merged by a combine pass
+  int kvt0 = 0, nkv;
+  if constexpr (TREE) {
+    const int tiles = (T + p.tree_n + kTile - 1) / kTile;
+    kvt0 = split * tiles / p.tree_splits;
+    nkv = (split + 1) * tiles / p.tree_splits - kvt0;
+  } else {
+    nkv = min(qt + 1, (T + kTile - 1) / kTile);  // BlockMask: skip k0 > q0+127 and k0 >= T
+  }
+  const int bst = TREE ? split * p.B + b : b;  // batch index of this CTA's out / lse rows
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.q, 1);
@@ -146,12 +164,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_expect_tx(&bars.k_full[st], TB);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, g, n * kTile, b);
+          tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, g, (kvt0 + n) * kTile, b);
         mbar_wait(&bars.v_empty[st], ph ^ 1);
         mbar_expect_tx(&bars.v_full[st], TB);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, n * kTile, b);
+          tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, (kvt0 + n) * kTile, b);
       }
       if (p.step > 0) {  // diagonal partial of the two heads into the Q tiles once no S MMA reads them
         mbar_wait(&bars.s_done, 0);
@@ -263,7 +281,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc_fence_after();
         uint32_t raw[128];
         tmem_ld128(tS, raw);
-        const int kv0 = n * kTile;
+        const int kv0 = (kvt0 + n) * kTile;
         const bool partial = TREE ? (kv0 + kTile > T) : ((n == qt) || (kv0 + kTile > T));
         // row max of the raw scores (scale > 0 commutes with max): 8 independent chains of
         // 3-input max (FMNMX3), two new columns per instruction
@@ -335,7 +353,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         // P = 2^(s c log2e - m): one FFMA2 per pair, 4 independent pair-sum chains (FADD2),
         // written to TMEM and published in two 64-column halves (the PV MMA starts on the first)
-        const uint64_t sl2x2 = f2pack(sl2, sl2), negm = f2pack(-m_run, -m_run);
+        // TREE: a row may have no allowed key in this context split yet (m = -inf): exponents
+        // against 0 give exact zeros instead of NaN
+        const float m_use = (TREE && m_run == -INFINITY) ? 0.f : m_run;
+        const uint64_t sl2x2 = f2pack(sl2, sl2), negm = f2pack(-m_use, -m_use);
         uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
@@ -387,7 +408,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // The j diagonal keys of row r (Alg. 1 "concat s_i") were reduced
       // by ttt_fwd_diag_kernel into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum); the
       // merge is the same online-softmax update as one more "tile".
-      const size_t lse_idx = ((size_t)b * p.Hq + h) * p.L + r;
+      const size_t lse_idx = ((size_t)bst * p.Hq + h) * p.L + r;
       const bool has_diag = !TREE && (r < T) && (p.step > 0);
       const float A_d = has_diag ? p.lse[lse_idx] : -INFINITY;
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, 0);
@@ -403,10 +424,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       uint8_t* st_lo = sK + slot * TB;
       const uint32_t sw = (uint32_t)(row & 7);
       const float m_f = fmaxf(m_run, A_d);
-      const float alpha = ex2(m_run - m_f);
+      const float alpha = (TREE && m_f == -INFINITY) ? 0.f : ex2(m_run - m_f);
       const float beta = has_diag ? ex2(A_d - m_f) : 0.f;
       const float l_f = l_run * alpha + beta;
-      const float inv_l = 1.f / l_f;
+      // TREE: a row with no allowed key in this split leaves O = 0 and lse = -inf (weight 0 in
+      // the combine pass)
+      const float inv_l = (TREE && l_f == 0.f) ? 0.f : 1.f / l_f;
       const float a_n = alpha * inv_l, b_n = beta * inv_l;
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
@@ -455,7 +478,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (row == 0) {
 #pragma unroll
         for (int bx = 0; bx < D / 64; ++bx) {
-          tma_store_4d(&maps.out, st_hi + bx * 16384, bx * 64, h, qt * kTile, b);
+          tma_store_4d(&maps.out, st_hi + bx * 16384, bx * 64, h, qt * kTile, bst);
           if (p.out_lo) tma_store_4d(&maps.out_lo, st_lo + bx * 16384, bx * 64, h, qt * kTile, b);
         }
         bulk_commit();
@@ -785,6 +808,29 @@ __global__ void ttt_tree_mask_kernel(const int32_t* parents, int B, int n, unsig
   mask[i] = m;
 }
 
+// merge the context splits of the tree pass: out = sum_s 2^(lse_s - lse) out_s, lse = logsumexp_s lse_s
+// (natural log; one warp per (b, node, head) row, lanes over D)
+__global__ void ttt_tree_combine_kernel(const __nv_bfloat16* part, const float* lse_part, int nsplit, int B, int n,
+                                        int Hq, int D, __nv_bfloat16* out, float* lse) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= B * n * Hq) return;
+  const int h = row % Hq, t = (row / Hq) % n, b = row / (Hq * n);
+  float m = -INFINITY;
+  for (int s = 0; s < nsplit; ++s) m = fmaxf(m, lse_part[(((size_t)s * B + b) * Hq + h) * n + t]);
+  float wsum = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const int per = D / 32;  // 2 or 4 consecutive elements per lane
+  for (int s = 0; s < nsplit; ++s) {
+    const float w = __expf(lse_part[(((size_t)s * B + b) * Hq + h) * n + t] - m);
+    wsum += w;
+    const __nv_bfloat16* src = part + ((((size_t)s * B + b) * n + t) * Hq + h) * D + lane * per;
+    for (int e = 0; e < per; ++e) acc[e] = fmaf(w, __bfloat162float(src[e]), acc[e]);
+  }
+  const float inv = 1.f / wsum;
+  __nv_bfloat16* dst = out + (((size_t)b * n + t) * Hq + h) * D + lane * per;
+  for (int e = 0; e < per; ++e) dst[e] = __float2bfloat16_rn(acc[e] * inv);
+  if (lane == 0) lse[((size_t)b * Hq + h) * n + t] = m + __logf(wsum);
+}
+
 template <int D>
 cudaError_t launch_tree_d(const Params& p_in, const FwdMaps& maps, const int32_t* parents, cudaStream_t st) {
   Params p = p_in;
@@ -800,10 +846,18 @@ cudaError_t launch_tree_d(const Params& p_in, const FwdMaps& maps, const int32_t
   const int nm = p.B * p.tree_n;
   ttt_tree_mask_kernel<<<(nm + 127) / 128, 128, 0, st>>>(parents, p.B, p.tree_n,
                                                         const_cast<unsigned long long*>(p.tree_mask));
-  const int grid = p.B * p.Hkv * ((p.G + 1) / 2);
+  const int grid = p.B * p.Hkv * ((p.G + 1) / 2) * p.tree_splits;
   prof_mark(kKindFwdMain, true, st);
   ttt_fwd_sm100_kernel<D, true><<<grid, kFwdThreads, smem, st>>>(p, maps);
   prof_mark(kKindFwdMain, false, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tree_combine(const void* part, const float* lse_part, int nsplit, int B, int n, int Hq, int D,
+                                void* out, float* lse, cudaStream_t st) {
+  const int rows = B * n * Hq;
+  ttt_tree_combine_kernel<<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(part), lse_part, nsplit,
+                                                          B, n, Hq, D, static_cast<__nv_bfloat16*>(out), lse);
   return cudaGetLastError();
 }
 

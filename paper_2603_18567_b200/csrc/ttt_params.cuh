@@ -48,6 +48,7 @@ struct Params {
   // tree-attention verification (ttt_tree_attn_fwd): seq_lens = prefix lengths, L = tree size
   int tree_n;                              // n tree tokens (queries), <= 64
   const unsigned long long* tree_mask;     // [B][n] ancestor-or-self bit masks (bit u = tree key u)
+  int tree_splits;                         // context splits per (b, kv head); > 1: partial out / lse
 };
 
 // Tensor maps for the tcgen05 paths (4-D: D, H, L, B; box 64 x 1 x 128 x 1, SW128)

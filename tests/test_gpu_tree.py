@@ -18,6 +18,8 @@ CASES = [  # (batch, n, prefix_lens, Hq, Hkv, D)
     (3, 33, [0, 127, 500], 8, 2, 64),   # empty prefix, tile-aligned edges, D = 64
     (2, 64, [1000, 2047], 32, 8, 128),  # TTT_MAX_TREE nodes, Llama-3.1-8B target heads
     (1, 64, [64], 5, 5, 128),           # odd head pairs (MHA, G = 1)
+    (1, 50, [2040], 8, 2, 128),         # context split over 4 CTAs; tree keys straddle the last two tiles
+    (2, 64, [4000, 700], 4, 2, 128),    # uneven contexts, splits by the shorter one
 ]
 
 
