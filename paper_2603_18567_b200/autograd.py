@@ -8,6 +8,12 @@ the computation runs in libtttattn.so's kernels). SURVEY.md §8(b) "Python side"
     TTT_ACCUMULATE_DKV path is the fused alternative bench.py times). Gradients of K/V come
     out of the kernel in fp32 and are returned in the inputs' dtype.
 
+``ttt_attention_unroll(qs, k_base, v_base, k_steps, v_steps)``
+    All S steps of one unroll as one autograd node: forward = S ttt_attn_fwd calls, backward =
+    one ttt_attn_bwd_unroll call whose fp32 dK / dV accumulators sum the steps' contributions
+    before a single cast to the inputs' dtype (the per-step wrapper lets autograd add S bf16
+    gradients instead).
+
 ``soft_label_loss(z, p, mask)``
     Masked soft-label log-softmax loss (reading R17) whose backward is Alg. 3
      IN PLACE: the logits buffer z is overwritten with dL/dz and handed
@@ -74,6 +80,66 @@ def ttt_attention(q: torch.Tensor, k_base: torch.Tensor, v_base: torch.Tensor,
         raise ValueError(f"step {j} needs {j} step K/V tensors, got {len(ks)} / {len(vs)}")
     lens = None if seq_lens is None else [int(x) for x in seq_lens]
     return _TTTAttention.apply(j, lens, float(softmax_scale), q, k_base, v_base, *ks, *vs)
+
+
+class _TTTAttentionUnroll(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, S: int, seq_lens, scale: float, k_base, v_base, *rest):
+        qs, ks, vs = list(rest[:S]), list(rest[S:2 * S - 1]), list(rest[2 * S - 1:3 * S - 2])
+        desc = L.desc_for(qs[0], k_base, seq_lens=seq_lens, softmax_scale=scale)
+        B, Lq, Hq, D = qs[0].shape
+        outs, los, lses = [], [], []
+        for j in range(S):
+            out = torch.empty_like(qs[j])
+            lo = torch.empty_like(qs[j]) if qs[j].dtype == torch.bfloat16 else None
+            lse = torch.empty((B, Hq, Lq), dtype=torch.float32, device=qs[j].device)
+            L.ttt_attn_fwd(desc, j, qs[j], k_base, v_base, ks, vs, out, lse, out_lo=lo)
+            outs.append(out)
+            los.append(lo)
+            lses.append(lse)
+        ctx.S, ctx.desc, ctx.has_lo = S, desc, los[0] is not None
+        ctx.save_for_backward(k_base, v_base, *qs, *ks, *vs, *outs, *lses, *(los if ctx.has_lo else []))
+        return tuple(outs)
+
+    @staticmethod
+    def backward(ctx, *douts):
+        S, desc = ctx.S, ctx.desc
+        t = ctx.saved_tensors
+        k_base, v_base = t[0], t[1]
+        o = 2
+        qs = list(t[o:o + S]); o += S
+        ks = list(t[o:o + S - 1]); o += S - 1
+        vs = list(t[o:o + S - 1]); o += S - 1
+        outs = list(t[o:o + S]); o += S
+        lses = list(t[o:o + S]); o += S
+        los = list(t[o:o + S]) if ctx.has_lo else None
+        douts = [d.contiguous() if d is not None else torch.zeros_like(outs[j]) for j, d in enumerate(douts)]
+        dqs = [torch.empty_like(q) for q in qs]
+        f32 = lambda x: torch.empty(x.shape, dtype=torch.float32, device=x.device)
+        dk, dv = f32(k_base), f32(v_base)
+        dks, dvs = [f32(x) for x in ks], [f32(x) for x in vs]
+        ws = torch.empty(max(L.ttt_attn_bwd_unroll_workspace_size(desc, S), 16), dtype=torch.uint8,
+                         device=k_base.device)
+        L.ttt_attn_bwd_unroll(desc, qs, k_base, v_base, ks, vs, outs, lses, douts, dqs, dk, dv, dks, dvs,
+                              flags=0, workspace=ws, out_lo=los)
+        cast = lambda g, like: g.to(like.dtype)
+        return (None, None, None, cast(dk, k_base), cast(dv, v_base), *dqs,
+                *[cast(g, x) for g, x in zip(dks, ks)], *[cast(g, x) for g, x in zip(dvs, vs)])
+
+
+def ttt_attention_unroll(qs: Sequence[torch.Tensor], k_base: torch.Tensor, v_base: torch.Tensor,
+                         k_steps: Sequence[torch.Tensor], v_steps: Sequence[torch.Tensor],
+                         seq_lens: Optional[Sequence[int]] = None, softmax_scale: float = 0.0):
+    """Differentiable TTT unroll: returns [out_0, ..., out_{S-1}] for S = len(qs) steps
+    (step j uses k_steps[:j], v_steps[:j]); backward is one ttt_attn_bwd_unroll call."""
+    S = len(qs)
+    if S < 1 or S > L.TTT_MAX_UNROLL:
+        raise ValueError(f"1 <= steps <= {L.TTT_MAX_UNROLL}")
+    ks, vs = list(k_steps[:S - 1]), list(v_steps[:S - 1])
+    if len(ks) != S - 1 or len(vs) != S - 1:
+        raise ValueError(f"{S} steps need {S - 1} step K/V tensors")
+    lens = None if seq_lens is None else [int(x) for x in seq_lens]
+    return list(_TTTAttentionUnroll.apply(S, lens, float(softmax_scale), k_base, v_base, *qs, *ks, *vs))
 
 
 class _SoftLabelLoss(torch.autograd.Function):

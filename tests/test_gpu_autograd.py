@@ -7,7 +7,7 @@ import torch
 
 import oracle
 from oracle import loss as OL
-from paper_2603_18567_b200.autograd import soft_label_loss, ttt_attention
+from paper_2603_18567_b200.autograd import soft_label_loss, ttt_attention, ttt_attention_unroll
 from paper_2603_18567_b200.inputs import Shape, make_case, make_loss_case
 from tests.gpu_helpers import TOL_BF16, assert_close, assert_close_sum, np32, oracle_inputs
 
@@ -67,3 +67,34 @@ def test_autograd_soft_label_loss_inplace(cuda_ok, dtype):
     err = np.abs(got - ref)
     assert (err <= rtol * np.abs(ref) + atol).all(), err.max()
     assert z.data_ptr() == ptr and torch.equal(z.detach(), z0.grad.to(dtype))  # the gradient lives in z's buffer
+
+
+def test_autograd_unroll_matches_oracle_and_per_step(cuda_ok):
+    """ttt_attention_unroll (one autograd node, backward = ttt_attn_bwd_unroll with fp32
+    accumulation) vs the oracle summed over steps, and vs the per-step wrapper."""
+    shape = Shape(1, 256, 8, 2, 128, 3)
+    case = make_case(shape, dtype=torch.bfloat16, seed=8, lens="ragged")
+    dev = lambda t: t.cuda().contiguous().requires_grad_(True)
+    qs = [dev(x) for x in case.q]
+    kb, vb = dev(case.k_base), dev(case.v_base)
+    ks, vs = [dev(x) for x in case.k_steps], [dev(x) for x in case.v_steps]
+    lens = [int(x) for x in case.seq_lens]
+    S = shape.ttt_steps
+    outs = ttt_attention_unroll(qs, kb, vb, ks, vs, seq_lens=lens)
+    total = sum((outs[j].float() * case.dout[j].cuda().float()).sum() for j in range(S))
+    total.backward()
+    parts = {"k": [], "v": [], "ks": [[] for _ in range(S - 1)], "vs": [[] for _ in range(S - 1)]}
+    for j in range(S):
+        og = oracle.bwd(*oracle_inputs(case, j), np32(case.dout[j]), seq_lens=case.seq_lens)
+        assert_close(f"unroll-autograd dq_{j}", np32(qs[j].grad), og["dq"], **TOL_BF16)
+        parts["k"].append(og["dk_base"])
+        parts["v"].append(og["dv_base"])
+        for i in range(j):
+            parts["ks"][i].append(og["dk_steps"][i])
+            parts["vs"][i].append(og["dv_steps"][i])
+    tol = dict(atol=TOL_BF16["atol"] * 1.5, rtol=TOL_BF16["rtol"] * 1.5)  # + one bf16 rounding of the sum
+    assert_close_sum("unroll-autograd dk_base", np32(kb.grad), parts["k"], **tol)
+    assert_close_sum("unroll-autograd dv_base", np32(vb.grad), parts["v"], **tol)
+    for i in range(S - 1):
+        assert_close_sum(f"unroll-autograd dk_{i+1}", np32(ks[i].grad), parts["ks"][i], **tol)
+        assert_close_sum(f"unroll-autograd dv_{i+1}", np32(vs[i].grad), parts["vs"][i], **tol)
