@@ -400,7 +400,7 @@ def run_loss(args, stream, peaks, world: int):
         "roofline": {"kernel": "ttt_loss_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "peak_kind": f"HBM ({peaks['source']})",
                      "avg_launch_ms": avg, "algorithmic_bytes_per_launch": alg_bytes,
-                     "traffic": ncu_traffic("ttt_loss_kernel")},
+                     "traffic": ncu_traffic("ttt_loss_ring_kernel") or ncu_traffic("ttt_loss_kernel")},
     }
 
 

@@ -435,7 +435,7 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
 // shortest sequence (splits are never empty), at most 16. (Measured: splitting 128 CTAs into
 // 3 x 128 was slower, 98 vs 75 us, each CTA's fixed cost repeating per split.)
 int tree_splits(const ttt_tree_desc* d) {
-  const int base = d->batch * d->num_kv_heads * ((d->num_q_heads / d->num_kv_heads + 1) / 2);
+  const int base = d->batch * d->num_kv_heads * ((d->num_q_heads / d->num_kv_heads + 3) / 4);
   if (2 * base > 148) return 1;
   int min_tiles = 1 << 30;
   for (int b = 0; b < d->batch; ++b) min_tiles = std::min(min_tiles, (d->prefix_lens[b] + d->num_tree + 127) / 128);
@@ -510,10 +510,10 @@ int ttt_tree_attn_fwd(const ttt_tree_desc* d, const void* q, const void* k_cache
   p.out_lo = nullptr;
   p.lse = lse_part;
   FwdMaps maps;
-  if (!encode_bshd(&maps.q, q, p.B, d->num_tree, p.Hq, p.D) ||
+  if (!encode_bshd(&maps.q, q, p.B, d->num_tree, p.Hq, p.D, 64) ||
       !encode_bshd(&maps.k, k_cache, p.B, d->kv_len, p.Hkv, p.D) ||
       !encode_bshd(&maps.v, v_cache, p.B, d->kv_len, p.Hkv, p.D) ||
-      !encode_bshd(&maps.out, part, p.B * tw.splits, d->num_tree, p.Hq, p.D))
+      !encode_bshd(&maps.out, part, p.B * tw.splits, d->num_tree, p.Hq, p.D, 64))
     return TTT_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = launch_tree_sm100(p, maps, parents, s);

@@ -80,7 +80,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   // ---- work decode: (b, g)-major so one kv head's K/V stay hot in L2; within
   // it the longest (highest) q tiles first; head pairs of a tile adjacent ----
-  const int npairs = (p.G + 1) >> 1;
+  // TTT: two heads per CTA (one per slot). TREE: four heads (n <= 64 tree rows each; slot s holds
+  // heads 4 hp + 2 s in rows [0, 64) and 4 hp + 2 s + 1 in rows [64, 128)), so no row is padding.
+  const int npairs = TREE ? (p.G + 3) >> 2 : (p.G + 1) >> 1;
   const int hp = (int)blockIdx.x % npairs;
   const int t_ = (int)blockIdx.x / npairs;
   int qt, g, b, split = 0;
@@ -106,8 +108,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     b = gi / p.Hkv;
 #endif
   }
-  const int h0 = g * p.G + 2 * hp;
-  const bool has1 = (2 * hp + 1) < p.G;
+  const int h0 = g * p.G + (TREE ? 4 : 2) * hp;
+  const int nheads = TREE ? min(4, p.G - 4 * hp) : min(2, p.G - 2 * hp);  // heads of this CTA
+  const bool has1 = TREE ? nheads > 2 : nheads > 1;
   const int T = p.seq_lens[b];  // TREE: prefix length P_b
   // TREE: kv tiles [kvt0, kvt0 + nkv) of this context split (balanced, never empty: host keeps
   // splits <= tiles); the tree result of a split goes to partial buffers merged by a combine pass
@@ -152,11 +155,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tma_prefetch_desc(&maps.q);
       tma_prefetch_desc(&maps.k);
       tma_prefetch_desc(&maps.v);
-      mbar_expect_tx(&bars.q, (has1 ? 2 : 1) * TB);
+      if constexpr (TREE) {  // 64-row boxes: head h0 + k -> slot k / 2, rows 64 (k % 2) ..
+        mbar_expect_tx(&bars.q, nheads * (TB / 2));
 #pragma unroll
-      for (int bx = 0; bx < NBOX; ++bx) {
-        tma_load_4d(sQ + bx * 16384, &maps.q, &bars.q, bx * 64, h0, qt * kTile, b);
-        if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.q, &bars.q, bx * 64, h0 + 1, qt * kTile, b);
+        for (int bx = 0; bx < NBOX; ++bx)
+          for (int k = 0; k < nheads; ++k)
+            tma_load_4d(sQ + (k >> 1) * TB + bx * 16384 + (k & 1) * 8192, &maps.q, &bars.q, bx * 64, h0 + k, 0, b);
+      } else {
+        mbar_expect_tx(&bars.q, (has1 ? 2 : 1) * TB);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx) {
+          tma_load_4d(sQ + bx * 16384, &maps.q, &bars.q, bx * 64, h0, qt * kTile, b);
+          if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.q, &bars.q, bx * 64, h0 + 1, qt * kTile, b);
+        }
       }
       for (int n = 0; n < nkv; ++n) {
         const int st = n & 1, ph = (n >> 1) & 1;
@@ -262,15 +273,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int wq = warp & 3;
     if (slot == 0 || has1) {
       const int row = wq * 32 + lane;
-      const int r = qt * kTile + row;
-      const int h = h0 + slot;
+      // TREE: row = 64 (head within the slot) + tree node
+      const int r = TREE ? (row & 63) : qt * kTile + row;
+      const int h = TREE ? h0 + 2 * slot + (row >> 6) : h0 + slot;
       const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
       const uint32_t tS = tbase + lane_off + slot * 128;
       const uint32_t tO = tbase + lane_off + 256 + slot * 128;
       const float sl2 = p.scale_log2;
       float m_run = -INFINITY, l_run = 0.f;
       // TREE: this row's ancestor-or-self mask (rows >= n are tile padding)
-      const bool tree_row = TREE && r < p.tree_n;
+      const bool tree_row = TREE && r < p.tree_n && (2 * slot + (row >> 6)) < nheads;
       const unsigned long long tree_am = tree_row ? p.tree_mask[(size_t)b * p.tree_n + r] : 0ull;
       TTT_TRACE_DECL(1);
       TTT_TRACE_DECL(2);
@@ -478,8 +490,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (row == 0) {
 #pragma unroll
         for (int bx = 0; bx < D / 64; ++bx) {
-          tma_store_4d(&maps.out, st_hi + bx * 16384, bx * 64, h, qt * kTile, bst);
-          if (p.out_lo) tma_store_4d(&maps.out_lo, st_lo + bx * 16384, bx * 64, h, qt * kTile, b);
+          if constexpr (TREE) {  // the slot's two heads, 64-row boxes
+            for (int k = 2 * slot; k < min(2 * slot + 2, nheads); ++k)
+              tma_store_4d(&maps.out, st_hi + bx * 16384 + (k & 1) * 8192, bx * 64, h0 + k, 0, bst);
+          } else {
+            tma_store_4d(&maps.out, st_hi + bx * 16384, bx * 64, h, qt * kTile, bst);
+            if (p.out_lo) tma_store_4d(&maps.out_lo, st_lo + bx * 16384, bx * 64, h, qt * kTile, b);
+          }
         }
         bulk_commit();
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 8, 0);
@@ -846,7 +863,7 @@ cudaError_t launch_tree_d(const Params& p_in, const FwdMaps& maps, const int32_t
   const int nm = p.B * p.tree_n;
   ttt_tree_mask_kernel<<<(nm + 127) / 128, 128, 0, st>>>(parents, p.B, p.tree_n,
                                                         const_cast<unsigned long long*>(p.tree_mask));
-  const int grid = p.B * p.Hkv * ((p.G + 1) / 2) * p.tree_splits;
+  const int grid = p.B * p.Hkv * ((p.G + 3) / 4) * p.tree_splits;
   prof_mark(kKindFwdMain, true, st);
   ttt_fwd_sm100_kernel<D, true><<<grid, kFwdThreads, smem, st>>>(p, maps);
   prof_mark(kKindFwdMain, false, st);
