@@ -438,9 +438,9 @@ def run_tree(args, stream, peaks):
             "ms_per_call": ms, "tree_tokens_per_s": B * n / (ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": (kv_bytes + 2 * 2 * B * n * Hq * D) / (ms / 1e3) / 1e9,
                          "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "note": ("K/V cache read once; not HBM-bound: 128 CTAs (8 seqs x 8 kv heads x 2 head "
-                                  "pairs) each walk 33 kv tiles through the forward pipeline, and at n = 64 half "
-                                  "of every 128-row q tile is padding")}}
+                         "note": ("K/V cache read once; latency-bound: 8 seqs x 8 kv heads x 2 context splits = "
+                                  "128 CTAs (4 heads x 64 tree rows each) walk ~17 kv tiles through the forward "
+                                  "pipeline, then a combine pass merges the splits")}}
 
 
 def run_longctx(args, stream, peaks):

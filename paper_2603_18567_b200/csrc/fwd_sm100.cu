@@ -343,7 +343,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const float m_new = fmaxf(m_run, mx);
         const bool need = m_new > m_run + kRescaleThreshold;
         if (__any_sync(0xffffffffu, need)) {
-          const float alpha = ex2(m_run - m_new);
+          // (TREE: a lane whose row has no allowed key yet has m_run = m_new = -inf; its alpha is 0,
+          // not 2^NaN — the branch is warp-uniform)
+          const float alpha = (TREE && m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
           if (n > 0) {  // PV_{n-1} is complete: s_full's commit covers it (rare path: 32-col chunks)
             const uint64_t a2 = f2pack(alpha, alpha);
 #pragma unroll 1

@@ -20,6 +20,7 @@ CASES = [  # (batch, n, prefix_lens, Hq, Hkv, D)
     (1, 64, [64], 5, 5, 128),           # odd head pairs (MHA, G = 1)
     (1, 50, [2040], 8, 2, 128),         # context split over 4 CTAs; tree keys straddle the last two tiles
     (2, 64, [4000, 700], 4, 2, 128),    # uneven contexts, splits by the shorter one
+    (1, 64, [1000], 8, 2, 128),         # one tile per split: nodes 0-23 have no key in the last split
 ]
 
 
