@@ -234,12 +234,31 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
       for (int gi = 0; gi < msg; ++gi, ++n) {
         const int grp = (int)blockIdx.x + (g0 + gi) * (int)gridDim.x;
         const int st = n % NS;
-        mbar_wait(&full[st], (n / NS) & 1);
-        const uint32_t sb = smem_u32(stages + st * lay.stage_bytes);
         const int w0 = grp * NR, nv = min(NR, nrows - w0);
         const int nitems = (nv + R - 1) / R;
         // items of this group owned by this warp: global item id n*ipg + k, round-robin over warps
-        for (int k = (cw - (n * ipg) % kPreCompute + kPreCompute) % kPreCompute; k < nitems; k += kPreCompute) {
+        const int k_first = (cw - (n * ipg) % kPreCompute + kPreCompute) % kPreCompute;
+        // the first item's lse rows are a global load: issue it before waiting for the stage's TMA
+        // data so its latency overlaps that wait (it sat on the item's critical path)
+        float lse_pf[2] = {0.f, 0.f};
+        if (k_first < nitems) {
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            const int m = g8 + hf * 8;
+            const int mrows0 = R > 1 ? R * G : min(16, G);
+            const int wr0 = R > 1 ? m / G : 0, hh0 = R > 1 ? m % G : m;
+            if (m < mrows0 && k_first * R + wr0 < nv) {
+              const uint32_t w = (uint32_t)(w0 + k_first * R + wr0);
+              const uint32_t bl = w / (uint32_t)p.Hkv;
+              const int g_ = (int)(w - bl * (uint32_t)p.Hkv), b_ = (int)(bl / (uint32_t)p.L);
+              const int r_ = (int)(bl - (uint32_t)b_ * (uint32_t)p.L);
+              lse_pf[hf] = lse_in[((size_t)b_ * p.Hq + g_ * G + hh0) * p.L + r_];
+            }
+          }
+        }
+        mbar_wait(&full[st], (n / NS) & 1);
+        const uint32_t sb = smem_u32(stages + st * lay.stage_bytes);
+        for (int k = k_first; k < nitems; k += kPreCompute) {
           const int lr0 = k * R;
           for (int mt = 0; mt < MT; ++mt) {
             const int mrows = R > 1 ? R * G : min(16, G - mt * 16);
@@ -259,7 +278,10 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
               bb[hf] = (int)(bl / (uint32_t)p.L);
               rr[hf] = (int)(bl - (uint32_t)bb[hf] * (uint32_t)p.L);
               act[hf] = okr[hf] && rr[hf] < p.seq_lens[bb[hf]];
-              l2[hf] = okr[hf] ? lse_in[((size_t)bb[hf] * p.Hq + gg[hf] * G + hh[hf]) * p.L + rr[hf]] * kLog2e : 0.f;
+              l2[hf] = okr[hf] ? ((k == k_first && mt == 0) ? lse_pf[hf]
+                                                          : lse_in[((size_t)bb[hf] * p.Hq + gg[hf] * G + hh[hf]) * p.L + rr[hf]]) *
+                                     kLog2e
+                               : 0.f;
             }
             // ---- S = Q K^T, dP = dO V^T, Delta = diag(dO (O + O_lo)^T) ----
             float s[4][4], dp[4][4], cd[2][4];
