@@ -337,6 +337,7 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         if world == 1:
             line["next_rows"]["longctx"] = run_longctx(args, stream, peaks)
         line["next_rows"]["tree_verify"] = run_tree(args, stream, peaks)
+        line["next_rows"]["qkv_rope"] = run_rope(args, stream, peaks)
     if rank == 0 and world == 1 and not args.no_cpu:
         n, threads, run = oracle_sample(shape, target_s=15.0)
         sec = run(n)
@@ -402,6 +403,40 @@ def run_loss(args, stream, peaks, world: int):
                      "avg_launch_ms": avg, "algorithmic_bytes_per_launch": alg_bytes,
                      "traffic": ncu_traffic("ttt_loss_ring_kernel") or ncu_traffic("ttt_loss_kernel")},
     }
+
+
+def run_rope(args, stream, peaks):
+    """SURVEY.md §8(f) NEXT #2 part, beside the headline: one TTT step's fused q/k/v projection
+    output (B L = 16384 rows x (32 + 2 x 8) heads x 128, bf16) -> RoPE'd q and the step's K / V
+    slots (ttt_qkv_rope_split), one HBM pass."""
+    import paper_2603_18567_b200 as ttt
+    B, L, Hq, Hkv, D = 8, 2048, 32, 8, 128
+    dev = stream.device
+    g = torch.Generator(device=dev).manual_seed(11)
+    qkv = torch.randn(B, L, Hq + 2 * Hkv, D, device=dev, generator=g).to(torch.bfloat16)
+    q = torch.empty(B, L, Hq, D, dtype=torch.bfloat16, device=dev)
+    k = torch.empty(B, L, Hkv, D, dtype=torch.bfloat16, device=dev)
+    v = torch.empty_like(k)
+    d = ttt.rope_desc(B, L, Hq, Hkv, D, 500000.0)
+    ws = torch.empty(ttt.ttt_rope_workspace_size(d), dtype=torch.uint8, device=dev)
+    one = lambda: ttt.ttt_qkv_rope_split(d, qkv, q, k, v, ws, stream=stream)
+    for _ in range(3):
+        one()
+    torch.cuda.synchronize()
+    iters = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(iters):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    nbytes = 2 * 2 * qkv.numel()  # read qkv, write q / k / v
+    return {"workload": f"{B} x {L} rows, {Hq}+2x{Hkv} heads x {D}, bf16, rotate-half RoPE (base 5e5) + K/V slots",
+            "ms_per_call": ms,
+            "roofline": {"bound": "hbm", "achieved": nbytes / (ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": nbytes / (ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                         "algorithmic_bytes_per_call": nbytes}}
 
 
 def run_tree(args, stream, peaks):

@@ -183,6 +183,23 @@ int ttt_tree_attn_fwd(const ttt_tree_desc* desc, const void* q, const void* k_ca
                       const int32_t* parents, void* out, float* lse, void* workspace, size_t workspace_bytes,
                       void* stream);
 
+/* ---- The TTT step's fresh projections into attention inputs (SURVEY.md §8(f) NEXT #2 part) ----
+ * qkv (bf16 [batch][seq_len][Hq + 2 Hkv][D]: a fused q/k/v projection's output, q heads first)
+ * -> q [batch][seq_len][Hq][D], k_slot / v_slot [batch][seq_len][Hkv][D] (e.g. k_steps[j-1] /
+ * v_steps[j-1] of ttt_attn_fwd, written in place), q and k rotated by rotate-half RoPE:
+ *   theta_i = pos * rope_base^(-2i/D),  x'_i = x_i cos - x_{i+D/2} sin,  x'_{i+D/2} = x_{i+D/2} cos + x_i sin
+ * at pos = row index 0..seq_len-1 ("a TTT step reuses position ids 0..T_pad-1"), or
+ * positions (DEVICE int32 [batch][seq_len]) when not NULL. One HBM pass; angles from an fp64-built
+ * cos / sin table in the workspace (>= ttt_rope_workspace_size(desc, positions != NULL) bytes).
+ * head_dim a multiple of 16; all pointers 16-byte aligned. */
+typedef struct {
+  int32_t batch, seq_len, num_q_heads, num_kv_heads, head_dim;
+  float rope_base;  /* e.g. 500000 (Llama-3.1) */
+} ttt_rope_desc;
+size_t ttt_rope_workspace_size(const ttt_rope_desc* desc, int per_sequence_positions);
+int ttt_qkv_rope_split(const ttt_rope_desc* desc, const void* qkv, const int32_t* positions, void* q,
+                       void* k_slot, void* v_slot, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- Optional instrumentation (off by default; used by bench.py) ----------
  * ttt_attn_profile_begin() arms per-kernel timing for the CALLING HOST THREAD:
  * each kernel the library launches afterwards is bracketed by cudaEventRecord

@@ -53,6 +53,12 @@ class TreeDesc(ctypes.Structure):
 TTT_MAX_TREE = 64
 
 
+class RopeDesc(ctypes.Structure):
+    """ttt_rope_desc (include/ttt_attn.h)."""
+    _fields_ = [("batch", ctypes.c_int32), ("seq_len", ctypes.c_int32), ("num_q_heads", ctypes.c_int32),
+                ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("rope_base", ctypes.c_float)]
+
+
 class LossDesc(ctypes.Structure):
     """ttt_loss_desc (include/ttt_loss.h)."""
     _fields_ = [("rows", ctypes.c_int64), ("vocab", ctypes.c_int32), ("dtype", ctypes.c_int32)]
@@ -84,6 +90,11 @@ def _load():
     lib.ttt_tree_attn_workspace_size.restype = sz
     lib.ttt_tree_attn_fwd.argtypes = [ptd, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.ttt_tree_attn_fwd.restype = i
+    prd = ctypes.POINTER(RopeDesc)
+    lib.ttt_rope_workspace_size.argtypes = [prd, i]
+    lib.ttt_rope_workspace_size.restype = sz
+    lib.ttt_qkv_rope_split.argtypes = [prd, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.ttt_qkv_rope_split.restype = i
     lib.ttt_attn_strerror.argtypes = [i]
     lib.ttt_attn_strerror.restype = ctypes.c_char_p
     lib.ttt_attn_version.argtypes = []
@@ -252,6 +263,27 @@ def ttt_tree_attn_fwd(desc: TreeDesc, q, k_cache, v_cache, parents, out, lse, wo
     """Enqueue ttt_tree_attn_fwd (include/ttt_attn.h): tree-attention verification forward."""
     _check(_lib.ttt_tree_attn_fwd(ctypes.byref(desc), _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(parents),
                                   _ptr(out), _ptr(lse), _ptr(workspace), _nbytes(workspace), _stream(stream)))
+
+
+
+def rope_desc(batch: int, seq_len: int, num_q_heads: int, num_kv_heads: int, head_dim: int,
+              rope_base: float = 500000.0) -> RopeDesc:
+    d = RopeDesc()
+    d.batch, d.seq_len, d.num_q_heads, d.num_kv_heads, d.head_dim = (
+        int(batch), int(seq_len), int(num_q_heads), int(num_kv_heads), int(head_dim))
+    d.rope_base = float(rope_base)
+    return d
+
+
+def ttt_rope_workspace_size(desc: RopeDesc, per_sequence_positions: bool = False) -> int:
+    return int(_lib.ttt_rope_workspace_size(ctypes.byref(desc), int(bool(per_sequence_positions))))
+
+
+def ttt_qkv_rope_split(desc: RopeDesc, qkv, q, k_slot, v_slot, workspace, positions=None, stream=None) -> None:
+    """Enqueue ttt_qkv_rope_split (include/ttt_attn.h): RoPE'd q and the step's K / V slots from a
+    fused q/k/v projection output, one HBM pass."""
+    _check(_lib.ttt_qkv_rope_split(ctypes.byref(desc), _ptr(qkv), _ptr(positions), _ptr(q), _ptr(k_slot),
+                                   _ptr(v_slot), _ptr(workspace), _nbytes(workspace), _stream(stream)))
 
 
 # ---- masked soft-label log-softmax loss + Alg. 3 in-place backward (include/ttt_loss.h) ----

@@ -18,7 +18,7 @@ def _declared_functions():
     for fn in os.listdir(os.path.join(ROOT, "include")):
         if fn.endswith(".h"):
             src = open(os.path.join(ROOT, "include", fn)).read()
-            names += re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(ttt_(?:attn|loss|tree)_\w+)\s*\(", src, re.M)
+            names += re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(ttt_(?:attn|loss|tree|rope|qkv)_\w+)\s*\(", src, re.M)
     return sorted(set(names))
 
 
@@ -191,3 +191,16 @@ def test_tree_validation_codes(kw, code):
     with pytest.raises(ttt.TTTError) as e:
         ttt.ttt_tree_attn_fwd(d, P(0), P(1), P(2), P(3), P(4), P(5), WS(0x50000000))
     assert e.value.code == code
+
+
+def test_rope_validation_codes():
+    d = ttt.rope_desc(1, 8, 4, 2, 40)
+    P = lambda i: FakeT(0x10000000 + 4096 * i)
+    with pytest.raises(ttt.TTTError) as e:
+        ttt.ttt_qkv_rope_split(d, P(0), P(1), P(2), P(3), None)
+    assert e.value.code == 2  # head_dim % 16
+    d = ttt.rope_desc(1, 8, 4, 2, 64)
+    with pytest.raises(ttt.TTTError) as e:
+        ttt.ttt_qkv_rope_split(d, FakeT(0x10000008), P(1), P(2), P(3), None)
+    assert e.value.code == 4
+    assert ttt.ttt_rope_workspace_size(d) == 8 * 32 * 8 and ttt.ttt_rope_workspace_size(d, True) == 8 * 32 * 8
