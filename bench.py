@@ -247,8 +247,10 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
     S = shape.ttt_steps
 
     # draft-layer gradient bucket (synthetic stand-in), bf16, one bucket per bwd call
-    from paper_2603_18567_b200.dp import GradBuckets, max_over_ranks
-    grads = GradBuckets(DRAFT_PARAMS if world > 1 else 1, S, dtype=torch.bfloat16, device=dev)
+    from paper_2603_18567_b200.dp import GradBuckets, Zero2Buckets, max_over_ranks
+    Buckets = Zero2Buckets if args.zero2 else GradBuckets
+    grads = Buckets(DRAFT_PARAMS if world > 1 else 1, S, dtype=torch.bfloat16, device=dev)
+    params = torch.zeros_like(grads.flat) if args.zero2 and world > 1 else None
     if world > 1:
         grads.flat.normal_()
 
@@ -258,6 +260,8 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
     def one_step():
         u.step(stream, on_bwd)
         grads.finish()
+        if params is not None:  # ZeRO-2: the updated parameter shards are re-replicated
+            grads.gather_params(params)
 
     for _ in range(args.warmup):
         one_step()
@@ -327,6 +331,8 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         "kernels_ms_per_step": {k: v[0] / prof_steps for k, v in kern.items()},
         "gpu_launches": launches_per_step * args.steps,
         "grad_allreduce_bytes_per_step": grads.nbytes if world > 1 else 0,
+        "grad_exchange": ("zero2 reduce-scatter + param all-gather" if args.zero2 else "bucketed all-reduce (AVG)")
+        if world > 1 else "none (1 GPU)",
         "wall_s_timed_region": wall,
         "clocks": clk.summary(),
     }
@@ -580,6 +586,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-loss", action="store_true", help="skip the §8(f) loss-kernel measurement")
+    ap.add_argument("--zero2", action="store_true",
+                    help="ZeRO-2 draft gradient exchange (reduce-scatter per backward call + parameter all-gather "
+                         "after the step, PAPER.md:281) instead of the bucketed all-reduce")
     ap.add_argument("--bwd-unroll", action="store_true",
                     help="one ttt_attn_bwd_unroll call per unroll instead of S ttt_attn_bwd calls (same work; "
                          "37%% less pre-pass HBM traffic, same time: the pre-pass is latency-bound; the DP "

@@ -102,3 +102,52 @@ def head_to_seq(y: torch.Tensor, world: int, group=None) -> torch.Tensor:
     recv = torch.empty_like(send)  # [source rank = head block][rows][h][d]
     dist.all_to_all_single(recv, send, group=group)
     return recv.permute(1, 0, 2, 3).reshape(L // world, world * Hs, D)
+
+
+class Zero2Buckets(GradBuckets):
+    """ZeRO-2 form of the draft gradient exchange (the draft model uses ZeRO-2,
+    gradient and optimizer-state sharding): `release(i)` reduce-scatters bucket i (each rank keeps
+    the averaged 1/N shard it owns — what its optimizer shard updates), and `gather_params()` is
+    the post-update all-gather of those shards into the full replicated buffer. Per step this moves
+    the bytes of one all-reduce, split around the optimizer step. Buckets are padded to a multiple
+    of the world size."""
+
+    def __init__(self, numel: int, n: int, dtype=torch.bfloat16, device="cpu", group=None):
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        per = -(-numel // n)                      # ceil: elements per bucket
+        per = -(-per // world) * world            # padded to a multiple of the world size
+        self.world = world
+        self.flat = torch.zeros(per * n, dtype=dtype, device=device)
+        self.buckets = list(torch.chunk(self.flat, n))
+        self.shards = [torch.empty(per // world, dtype=dtype, device=device) for _ in range(n)]
+        self.group = group
+        self.works = []
+
+    def release(self, i: int) -> None:
+        if self.world == 1:
+            self.shards[i].copy_(self.buckets[i])
+            return
+        self.works.append(dist.reduce_scatter_tensor(self.shards[i], self.buckets[i], op=dist.ReduceOp.SUM,
+                                                     group=self.group, async_op=True))
+
+    def finish(self) -> None:
+        while self.works:
+            self.works.pop(0).wait()
+        if self.world > 1:
+            for s in self.shards:
+                s.mul_(1.0 / self.world)
+
+    def gather_params(self, params_flat: torch.Tensor) -> None:
+        """All-gather the per-rank shards of `params_flat` (same bucketing as the gradients)."""
+        if self.world == 1:
+            return
+        n = len(self.buckets)
+        chunks = list(torch.chunk(params_flat, n))
+        rank = dist.get_rank(self.group)
+        works = []
+        for c in chunks:
+            per = c.numel() // self.world
+            mine = c[rank * per:(rank + 1) * per].clone()
+            works.append(dist.all_gather_into_tensor(c, mine, group=self.group, async_op=True))
+        for w in works:
+            w.wait()

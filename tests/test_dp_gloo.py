@@ -111,3 +111,50 @@ def test_head_parallel_single_rank_identity():
     from paper_2603_18567_b200.dp import head_to_seq, seq_to_head
     x = torch.randn(6, 4, 3)
     assert torch.equal(seq_to_head(x, 1), x) and torch.equal(head_to_seq(x, 1), x)
+
+
+def _zero2_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_18567_b200.dp import Zero2Buckets
+        zb = Zero2Buckets(1000, 3, dtype=torch.float32)
+        n = zb.flat.numel()
+        zb.flat.copy_(torch.arange(n, dtype=torch.float32) * (rank + 1))
+        for i in reversed(range(3)):
+            zb.release(i)
+        zb.finish()
+        avg = torch.arange(n, dtype=torch.float32) * sum(r + 1 for r in range(world)) / world
+        ok_rs = True
+        for i, (b, s) in enumerate(zip(torch.chunk(avg, 3), zb.shards)):
+            per = s.numel()
+            ok_rs &= torch.allclose(s, b[rank * per:(rank + 1) * per])
+        params = torch.zeros(n)
+        for i, c in enumerate(torch.chunk(params, 3)):   # each rank fills only its own shard
+            per = c.numel() // world
+            c[rank * per:(rank + 1) * per] = 100.0 * (rank + 1) + i
+        zb.gather_params(params)
+        want = torch.cat([torch.cat([torch.full((c.numel() // world,), 100.0 * (r + 1) + i) for r in range(world)])
+                          for i, c in enumerate(torch.chunk(torch.zeros(n), 3))])
+        q.put((rank, ok_rs, bool(torch.equal(params, want))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_zero2_reduce_scatter_and_param_all_gather_world2():
+    """ZeRO-2 exchange: each rank gets the averaged shard it owns; the all-gather
+    re-replicates the updated parameter shards."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_zero2_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok_rs, ok_ag in res:
+        assert ok_rs, f"rank {rank}: reduce-scatter shard wrong"
+        assert ok_ag, f"rank {rank}: param all-gather wrong"
