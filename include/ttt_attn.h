@@ -199,6 +199,10 @@ typedef struct {
 size_t ttt_rope_workspace_size(const ttt_rope_desc* desc, int per_sequence_positions);
 int ttt_qkv_rope_split(const ttt_rope_desc* desc, const void* qkv, const int32_t* positions, void* q,
                        void* k_slot, void* v_slot, void* workspace, size_t workspace_bytes, void* stream);
+/* Its backward (the adjoint): dqkv [batch][seq_len][Hq + 2 Hkv][D] = [R(-theta) dq | R(-theta) dk | dv]. */
+int ttt_qkv_rope_join_bwd(const ttt_rope_desc* desc, const void* dq, const void* dk_slot, const void* dv_slot,
+                          const int32_t* positions, void* dqkv, void* workspace, size_t workspace_bytes,
+                          void* stream);
 
 /* ---- Optional instrumentation (off by default; used by bench.py) ----------
  * ttt_attn_profile_begin() arms per-kernel timing for the CALLING HOST THREAD:

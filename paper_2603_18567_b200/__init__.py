@@ -13,5 +13,5 @@ from ._lib import (  # noqa: F401
     TTT_LOSS_MEAN, LossDesc, loss_desc_for, ttt_loss_workspace_size, ttt_loss_fwd, ttt_loss_bwd_inplace,
     ttt_loss_fwd_bwd_inplace, TTT_MAX_UNROLL, ttt_attn_bwd_unroll, ttt_attn_bwd_unroll_workspace_size,
     TTT_MAX_TREE, TreeDesc, tree_desc, ttt_tree_attn_fwd, ttt_tree_attn_workspace_size,
-    RopeDesc, rope_desc, ttt_qkv_rope_split, ttt_rope_workspace_size,
+    RopeDesc, rope_desc, ttt_qkv_rope_split, ttt_rope_workspace_size, ttt_qkv_rope_join_bwd,
 )

@@ -95,6 +95,8 @@ def _load():
     lib.ttt_rope_workspace_size.restype = sz
     lib.ttt_qkv_rope_split.argtypes = [prd, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.ttt_qkv_rope_split.restype = i
+    lib.ttt_qkv_rope_join_bwd.argtypes = [prd, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.ttt_qkv_rope_join_bwd.restype = i
     lib.ttt_attn_strerror.argtypes = [i]
     lib.ttt_attn_strerror.restype = ctypes.c_char_p
     lib.ttt_attn_version.argtypes = []
@@ -284,6 +286,13 @@ def ttt_qkv_rope_split(desc: RopeDesc, qkv, q, k_slot, v_slot, workspace, positi
     fused q/k/v projection output, one HBM pass."""
     _check(_lib.ttt_qkv_rope_split(ctypes.byref(desc), _ptr(qkv), _ptr(positions), _ptr(q), _ptr(k_slot),
                                    _ptr(v_slot), _ptr(workspace), _nbytes(workspace), _stream(stream)))
+
+
+
+def ttt_qkv_rope_join_bwd(desc: RopeDesc, dq, dk_slot, dv_slot, dqkv, workspace, positions=None, stream=None) -> None:
+    """Enqueue ttt_qkv_rope_join_bwd: the adjoint of ttt_qkv_rope_split (gradients -> dqkv)."""
+    _check(_lib.ttt_qkv_rope_join_bwd(ctypes.byref(desc), _ptr(dq), _ptr(dk_slot), _ptr(dv_slot), _ptr(positions),
+                                      _ptr(dqkv), _ptr(workspace), _nbytes(workspace), _stream(stream)))
 
 
 # ---- masked soft-label log-softmax loss + Alg. 3 in-place backward (include/ttt_loss.h) ----

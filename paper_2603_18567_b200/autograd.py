@@ -14,6 +14,10 @@ the computation runs in libtttattn.so's kernels). SURVEY.md §8(b) "Python side"
     before a single cast to the inputs' dtype (the per-step wrapper lets autograd add S bf16
     gradients instead).
 
+``qkv_rope_split(qkv, num_q_heads, num_kv_heads, rope_base)``
+    The fused q/k/v projection output -> RoPE'd q and the step's K / V (ttt_qkv_rope_split);
+    backward = ttt_qkv_rope_join_bwd (the rotation's adjoint).
+
 ``soft_label_loss(z, p, mask)``
     Masked soft-label log-softmax loss (reading R17) whose backward is Alg. 3
      IN PLACE: the logits buffer z is overwritten with dL/dz and handed
@@ -140,6 +144,40 @@ def ttt_attention_unroll(qs: Sequence[torch.Tensor], k_base: torch.Tensor, v_bas
         raise ValueError(f"{S} steps need {S - 1} step K/V tensors")
     lens = None if seq_lens is None else [int(x) for x in seq_lens]
     return list(_TTTAttentionUnroll.apply(S, lens, float(softmax_scale), k_base, v_base, *qs, *ks, *vs))
+
+
+class _QkvRopeSplit(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, qkv, Hq: int, Hkv: int, base: float, positions):
+        B, Lr, H, D = qkv.shape
+        d = L.rope_desc(B, Lr, Hq, Hkv, D, base)
+        ws = torch.empty(max(L.ttt_rope_workspace_size(d, positions is not None), 16), dtype=torch.uint8,
+                         device=qkv.device)
+        q = torch.empty(B, Lr, Hq, D, dtype=qkv.dtype, device=qkv.device)
+        k = torch.empty(B, Lr, Hkv, D, dtype=qkv.dtype, device=qkv.device)
+        v = torch.empty_like(k)
+        L.ttt_qkv_rope_split(d, qkv.contiguous(), q, k, v, ws, positions=positions)
+        ctx.d, ctx.ws, ctx.positions, ctx.shape = d, ws, positions, qkv.shape
+        return q, k, v
+
+    @staticmethod
+    def backward(ctx, dq, dk, dv):
+        z = lambda g, like_shape: g.contiguous() if g is not None else torch.zeros(
+            like_shape, dtype=torch.bfloat16, device=ctx.ws.device)
+        B, Lr, H, D = ctx.shape
+        dq = z(dq, (B, Lr, ctx.d.num_q_heads, D))
+        dk = z(dk, (B, Lr, ctx.d.num_kv_heads, D))
+        dv = z(dv, (B, Lr, ctx.d.num_kv_heads, D))
+        dqkv = torch.empty(ctx.shape, dtype=dq.dtype, device=dq.device)
+        L.ttt_qkv_rope_join_bwd(ctx.d, dq, dk, dv, dqkv, ctx.ws, positions=ctx.positions)
+        return dqkv, None, None, None, None
+
+
+def qkv_rope_split(qkv: torch.Tensor, num_q_heads: int, num_kv_heads: int, rope_base: float = 500000.0,
+                   positions: Optional[torch.Tensor] = None):
+    """qkv bf16 [B, L, Hq + 2 Hkv, D] -> (q, k, v): q and k RoPE'd at positions 0..L-1 (or the given
+    int32 [B, L] positions), v copied; differentiable (backward = the rotation's adjoint)."""
+    return _QkvRopeSplit.apply(qkv, int(num_q_heads), int(num_kv_heads), float(rope_base), positions)
 
 
 class _SoftLabelLoss(torch.autograd.Function):

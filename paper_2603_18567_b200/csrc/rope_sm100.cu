@@ -75,6 +75,54 @@ __global__ void __launch_bounds__(256) ttt_qkv_rope_kernel(const __nv_bfloat16* 
   }
 }
 
+// backward of the split: dqkv = [R(-theta) dq | R(-theta) dk | dv] in the fused layout (the
+// rotation is orthogonal, so its adjoint is the rotation by -theta)
+__global__ void __launch_bounds__(256) ttt_qkv_rope_join_kernel(const __nv_bfloat16* __restrict__ dq,
+                                                                const __nv_bfloat16* __restrict__ dk,
+                                                                const __nv_bfloat16* __restrict__ dv,
+                                                                const float2* __restrict__ table, int per_seq_table,
+                                                                int B, int L, int Hq, int Hkv, int D,
+                                                                __nv_bfloat16* __restrict__ dqkv) {
+  const int half = D / 2, cpp = half / 8;
+  const int H = Hq + 2 * Hkv;
+  const long long items = (long long)B * L * H * cpp;
+  for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(it % cpp);
+    const long long rh = it / cpp;
+    const int h = (int)(rh % H);
+    const long long bl = rh / H;
+    const __nv_bfloat16* src;
+    if (h < Hq) src = dq + (bl * Hq + h) * D;
+    else if (h < Hq + Hkv) src = dk + (bl * Hkv + (h - Hq)) * D;
+    else src = dv + (bl * Hkv + (h - Hq - Hkv)) * D;
+    const uint4 a = *reinterpret_cast<const uint4*>(src + c * 8);
+    const uint4 bb = *reinterpret_cast<const uint4*>(src + half + c * 8);
+    __nv_bfloat16* dst = dqkv + rh * D + c * 8;
+    if (h >= Hq + Hkv) {
+      *reinterpret_cast<uint4*>(dst) = a;
+      *reinterpret_cast<uint4*>(dst + half) = bb;
+      continue;
+    }
+    const float2* tb = table + (per_seq_table ? bl : bl % L) * half + c * 8;
+    const __nv_bfloat162* g1 = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&bb);
+    uint4 o1, o2;
+    __nv_bfloat162* y1 = reinterpret_cast<__nv_bfloat162*>(&o1);
+    __nv_bfloat162* y2 = reinterpret_cast<__nv_bfloat162*>(&o2);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 u = __bfloat1622float2(g1[e]), w = __bfloat1622float2(g2[e]);
+      const float2 cs0 = tb[2 * e], cs1 = tb[2 * e + 1];
+      // [dx_i, dx_{i+D/2}] = R(-theta) [dy_i, dy_{i+D/2}]
+      y1[e] = __floats2bfloat162_rn(u.x * cs0.x + w.x * cs0.y, u.y * cs1.x + w.y * cs1.y);
+      y2[e] = __floats2bfloat162_rn(w.x * cs0.x - u.x * cs0.y, w.y * cs1.x - u.y * cs1.y);
+    }
+    *reinterpret_cast<uint4*>(dst) = o1;
+    *reinterpret_cast<uint4*>(dst + half) = o2;
+  }
+}
+
 bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
@@ -112,6 +160,33 @@ int ttt_qkv_rope_split(const ttt_rope_desc* d, const void* qkv, const int32_t* p
       static_cast<const __nv_bfloat16*>(qkv), table, positions != nullptr, d->batch, d->seq_len, d->num_q_heads,
       d->num_kv_heads, d->head_dim, static_cast<__nv_bfloat16*>(q), static_cast<__nv_bfloat16*>(k_slot),
       static_cast<__nv_bfloat16*>(v_slot));
+  return cudaGetLastError() == cudaSuccess ? TTT_OK : TTT_ERR_CUDA;
+}
+
+int ttt_qkv_rope_join_bwd(const ttt_rope_desc* d, const void* dq, const void* dk_slot, const void* dv_slot,
+                          const int32_t* positions, void* dqkv, void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace tttk;
+  if (!d || !dq || !dk_slot || !dv_slot || !dqkv) return TTT_ERR_INVALID_ARG;
+  if (d->batch < 1 || d->seq_len < 1 || d->num_q_heads < 1 || d->num_kv_heads < 1 || !(d->rope_base > 1.f))
+    return TTT_ERR_INVALID_ARG;
+  if (d->head_dim < 16 || d->head_dim % 16) return TTT_ERR_UNSUPPORTED;
+  if (!a16(dq) || !a16(dk_slot) || !a16(dv_slot) || !a16(dqkv) || !a16(workspace)) return TTT_ERR_ALIGNMENT;
+  const size_t need = ttt_rope_workspace_size(d, positions != nullptr);
+  if (!workspace || workspace_bytes < need) return TTT_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int half = d->head_dim / 2;
+  const int rows = positions ? d->batch * d->seq_len : d->seq_len;
+  float2* table = static_cast<float2*>(workspace);
+  cudaGetLastError();
+  ttt_rope_table_kernel<<<(rows * half + 255) / 256, 256, 0, st>>>(positions, rows, d->seq_len, half,
+                                                                   (double)d->rope_base, table);
+  const long long items = (long long)d->batch * d->seq_len * (d->num_q_heads + 2 * d->num_kv_heads) * (half / 8);
+  long long blocks = (items + 255) / 256;
+  if (blocks > 148LL * 16) blocks = 148LL * 16;
+  ttt_qkv_rope_join_kernel<<<(unsigned)blocks, 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(dq), static_cast<const __nv_bfloat16*>(dk_slot),
+      static_cast<const __nv_bfloat16*>(dv_slot), table, positions != nullptr, d->batch, d->seq_len,
+      d->num_q_heads, d->num_kv_heads, d->head_dim, static_cast<__nv_bfloat16*>(dqkv));
   return cudaGetLastError() == cudaSuccess ? TTT_OK : TTT_ERR_CUDA;
 }
 

@@ -32,3 +32,35 @@ def test_qkv_rope_split_vs_oracle(B, L, Hq, Hkv, D, use_pos):
         err = np.abs(got - want)
         assert (err <= 2.0 ** -8 * np.abs(want) + 1e-6).all(), f"{name}: max_abs={err.max():.3e}"
     assert torch.equal(v.cpu(), qkv[:, :, Hq + Hkv:])   # V is copied bit for bit
+
+
+def _torch_rope(x, pos, base):
+    """float64 torch mirror of oracle.rope.rope_rotate (autograd reference)."""
+    D = x.shape[-1]
+    half = D // 2
+    inv = base ** (-torch.arange(half, dtype=torch.float64) * 2.0 / D)
+    th = pos.to(torch.float64)[..., None] * inv
+    c, s = th.cos()[..., None, :], th.sin()[..., None, :]
+    x1, x2 = x[..., :half], x[..., half:]
+    return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
+
+
+def test_qkv_rope_join_bwd_and_autograd():
+    """The backward kernel is the adjoint: dqkv matches torch float64 autograd of the rotation."""
+    from paper_2603_18567_b200.autograd import qkv_rope_split
+    B, L, Hq, Hkv, D = 2, 96, 8, 2, 128
+    g = torch.Generator().manual_seed(3)
+    qkv = torch.randn(B, L, Hq + 2 * Hkv, D, generator=g).to(torch.bfloat16)
+    wq, wk, wv = (torch.randn(B, L, h, D, generator=g).to(torch.bfloat16) for h in (Hq, Hkv, Hkv))
+    x = qkv.cuda().requires_grad_(True)
+    q, k, v = qkv_rope_split(x, Hq, Hkv, 500000.0)
+    ((q.float() * wq.cuda().float()).sum() + (k.float() * wk.cuda().float()).sum()
+     + (v.float() * wv.cuda().float()).sum()).backward()
+    xr = qkv.double().requires_grad_(True)
+    pos = torch.arange(L)
+    qr = _torch_rope(xr[:, :, :Hq], pos, 500000.0)
+    kr = _torch_rope(xr[:, :, Hq:Hq + Hkv], pos, 500000.0)
+    ((qr * wq.double()).sum() + (kr * wk.double()).sum() + (xr[:, :, Hq + Hkv:] * wv.double()).sum()).backward()
+    got, want = x.grad.double().cpu(), xr.grad
+    assert ((got - want).abs() <= 2.0 ** -8 * want.abs() + 1e-6).all(), (got - want).abs().max().item()
+    np.testing.assert_allclose(q.detach().double().cpu().numpy(), qr.detach().numpy(), rtol=2.0 ** -8, atol=1e-6)
