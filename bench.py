@@ -212,12 +212,21 @@ class Unroll:
             self.ws_unroll = torch.empty(ttt.ttt_attn_bwd_unroll_workspace_size(self.desc, S), dtype=torch.uint8,
                                          device=dev)
 
-    def step(self, stream, on_bwd=None):
+    def step(self, stream, on_bwd=None, marks=None):
+        """One unroll. `marks` (optional): dict of CUDA events recorded around every call,
+        marks[("fwd", j)] / marks[("bwd", j)] = (start, end), for per-step times."""
         t, s = self.ttt, self.s
         S = s.ttt_steps
+        ev = lambda key: marks.setdefault(key, (torch.cuda.Event(enable_timing=True),
+                                                torch.cuda.Event(enable_timing=True))) if marks is not None else None
         for j in range(S):
+            e = ev(("fwd", j))
+            if e:
+                e[0].record(stream)
             t.ttt_attn_fwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, self.out[j], self.lse[j],
                            out_lo=self.out_lo[j], stream=stream)
+            if e:
+                e[1].record(stream)
         if self.bwd_unroll:
             t.ttt_attn_bwd_unroll(self.desc, self.q, self.k, self.v, self.ks, self.vs, self.out, self.lse, self.do,
                                   self.dq, self.dk, self.dv, self.dks, self.dvs, flags=0, workspace=self.ws_unroll,
@@ -227,10 +236,15 @@ class Unroll:
                     on_bwd(i)
             return
         for j in reversed(range(S)):
+            e = ev(("bwd", j))
+            if e:
+                e[0].record(stream)
             t.ttt_attn_bwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, self.out[j], self.lse[j],
                            self.do[j], self.dq[j], self.dk, self.dv, self.dks, self.dvs,
                            flags=0 if j == S - 1 else t.TTT_ACCUMULATE_DKV, workspace=self.ws, stream=stream,
                            out_lo=self.out_lo[j])
+            if e:
+                e[1].record(stream)
             if on_bwd is not None:
                 on_bwd(S - 1 - j)
 
@@ -295,6 +309,16 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     kern = ttt.ttt_attn_profile_end()
     launches_per_step = sum(n for _, n in kern.values()) // prof_steps
+    # per-TTT-step call times (the paper measures the final step), separate pass
+    per_step = {"fwd_ms": [0.0] * S, "bwd_ms": [0.0] * S}
+    if not u.bwd_unroll:
+        reps = 3
+        for _ in range(reps):
+            marks = {}
+            u.step(stream, marks=marks)
+            torch.cuda.synchronize()
+            for (kind, j), (a, b) in marks.items():
+                per_step[f"{kind}_ms"][j] += a.elapsed_time(b) / reps
 
     peaks = load_peaks()
     per_step_pairs, base_pairs = alg_pairs(shape)
@@ -329,6 +353,7 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         "flops_convention": "algorithmic 12*D per allowed (q,k) pair (fwd 4D + bwd 8D; recompute excluded)",
         "roofline": roof,
         "kernels_ms_per_step": {k: v[0] / prof_steps for k, v in kern.items()},
+        "per_ttt_step_ms": per_step,
         "gpu_launches": launches_per_step * args.steps,
         "grad_allreduce_bytes_per_step": grads.nbytes if world > 1 else 0,
         "grad_exchange": ("zero2 reduce-scatter + param all-gather" if args.zero2 else "bucketed all-reduce (AVG)")
