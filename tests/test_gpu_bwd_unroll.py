@@ -110,3 +110,39 @@ def test_bwd_unroll_full_size_llama_equals_per_call(cuda_ok):
     case = make_case(shape, dtype=torch.bfloat16, seed=0, lens="full")
     dc = DeviceCase(case)
     _assert_equivalent("llama8b", shape.ttt_steps, *_run_both(dc, shape.ttt_steps, False))
+
+
+def test_bwd_unroll_fp32_check_mode(cuda_ok):
+    """FP32_CHECK: ttt_attn_bwd_unroll runs the S per-call check kernels; vs the oracle at 1e-5."""
+    from tests.gpu_helpers import TOL_FP32
+    shape = Shape(1, 128, 4, 2, 64, 3)
+    case = make_case(shape, dtype=torch.float32, seed=6, lens="ragged")
+    dc = DeviceCase(case)
+    S = shape.ttt_steps
+    outs, lses = [], []
+    for j in range(S):
+        o, l = dc.fwd(j)
+        outs.append(o)
+        lses.append(l)
+    g = dc.alloc_grads(S - 1)
+    dqs = [torch.empty_like(dc.q[0]) for _ in range(S)]
+    ttt.ttt_attn_bwd_unroll(dc.desc, dc.q[:S], dc.k, dc.v, dc.ks, dc.vs, outs, lses, dc.dout[:S], dqs,
+                            g["dk_base"], g["dv_base"], g["dk_steps"], g["dv_steps"])
+    torch.cuda.synchronize()
+    parts = {"dk_base": [], "dv_base": []}
+    for j in range(S):
+        og = oracle.bwd(*oracle_inputs(case, j), np32(case.dout[j]), seq_lens=case.seq_lens)
+        assert_close_sum(f"check dq_{j}", np32(dqs[j]), [og["dq"]], **TOL_FP32)
+        parts["dk_base"].append(og["dk_base"])
+        parts["dv_base"].append(og["dv_base"])
+    assert_close_sum("check dk_base", np32(g["dk_base"]), parts["dk_base"], **TOL_FP32)
+    assert_close_sum("check dv_base", np32(g["dv_base"]), parts["dv_base"], **TOL_FP32)
+
+
+@pytest.mark.slow
+def test_bwd_unroll_qwen_shape_equals_per_call(cuda_ok):
+    """Qwen3-235B-A22B draft shape (64 q / 4 kv heads, G = 16: head-split CTAs, L = 4096)."""
+    shape = CONFIGS["qwen235b"]
+    case = make_case(shape, dtype=torch.bfloat16, seed=1, lens="full")
+    dc = DeviceCase(case)
+    _assert_equivalent("qwen235b", shape.ttt_steps, *_run_both(dc, shape.ttt_steps, False))
