@@ -1,4 +1,4 @@
-# A/B: programmatic dependent launch on / off (TTT_NO_PDL=1), whole-step bench, alternating
+# A/B: programmatic dependent launch on / off (TTT_NO_PDL=1; the PDL build was reverted — kept as the record of the measurement)
 timeout 900 python -m pytest tests/test_gpu_fwd_bf16.py tests/test_gpu_bwd_bf16.py tests/test_gpu_bwd_unroll.py -x -q 2>&1 | tail -1
 for r in 1 2 3; do
   for v in 0 1; do
