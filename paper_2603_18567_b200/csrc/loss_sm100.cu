@@ -2,14 +2,16 @@
 // (Alg. 3; §4.2.1 "Memory-Efficient Gradient Computation",
 // PAPER.md:338-340). C-ABI in include/ttt_loss.h; readings R17-R20 in DESIGN.md.
 //
-// HBM-bound row kernel. One row (V logits + V target probabilities) is split
-// over a thread-block cluster of CS CTAs x 256 threads; every thread loads its
-// NV 16-byte vectors of z and p ONCE into registers (streaming loads), the row
-// statistics (max, sum of exp, sum p, sum p z) are reduced warp -> CTA ->
-// cluster (DSMEM, fixed rank order, so every CTA of the cluster holds bit-
-// identical statistics), and the gradient of Alg. 3 is written straight from
-// the registers over z. Bytes per row: read z, read p, write grad (fused mode)
-// — the minimum for an in-place backward; nothing of size [N][V] is allocated.
+// HBM-bound row kernels. Every thread of a 512-thread CTA holds its NV 16-byte
+// vectors of one row's z and p in registers; the row statistics (max, sum of
+// exp, sum p, sum p z) are reduced warp -> CTA (-> cluster through DSMEM when a
+// row needs several CTAs), in a fixed order so every CTA holds bit-identical
+// statistics, and the gradient of Alg. 3 is written straight from the registers
+// over z. Rows of <= 64 KB per tensor take the persistent ttt_loss_ring_kernel
+// (the next row bulk-copied into smem under the current row's math); larger rows
+// one row per CTA / cluster (ttt_loss_kernel). Bytes per row: read z, read p,
+// write grad (fused mode) — the minimum for an in-place backward; nothing of size
+// [N][V] is allocated.
 #include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -314,10 +316,10 @@ __device__ __forceinline__ void process_row(const LossParams& P, int64_t row, in
   }
 }
 
-// One row per cluster of CS CTAs (grid = rows x CS). A persistent variant that walks rows
-// with a register double buffer (next row's loads in flight during the current row's
-// reduction) measured slower at the bench shape (894 vs 690 us: 2 CTAs / SM at 128
-// registers); overlap comes from 4 co-resident CTAs per SM instead.
+// One row per CTA or cluster of CS CTAs (grid = rows x CS), for rows the ring kernel does not
+// take (odd vocab, or > 64 KB per tensor). A persistent variant that kept the next row in a
+// second register set measured slower (894 vs 690 us at the bench shape: 2 CTAs / SM at 128
+// registers); the smem-staged ring kernel below is the persistent form that paid off.
 template <typename T, int E, int NV>
 __global__ void __launch_bounds__(kLossThreads, (NV <= 4 ? 65536 / (kLossThreads * 64) : 1)) ttt_loss_kernel(const LossParams P) {
   using V = typename VecT<T, E>::type;
