@@ -5,8 +5,9 @@
 // DESIGN.md R23-R25). C-ABI ttt_qkv_rope_split in include/ttt_attn.h.
 //
 // HBM-bound: read 2 B and write 2 B per element. The angles are shared by every head of a row,
-// so cos / sin come from a table built once per call in fp64 (theta = pos * base^(-2i/D) reaches
-// 10^4 rad at L = 16K, where an fp32 product would already be off by ~1e-3 rad).
+// so cos / sin come from a table built once per call: theta = pos * base^(-2i/D) in fp64 (it
+// reaches 10^4 rad at L = 16K, where an fp32 product would already be off by ~1e-3 rad), reduced
+// to [-pi, pi] in fp64, then an fp32 sincosf of the small angle.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -23,28 +24,30 @@ __global__ void ttt_rope_table_kernel(const int32_t* positions, int rows, int L,
   if (i >= rows * half) return;
   const int r = i / half, f = i - r * half;
   const double pos = positions ? (double)positions[r] : (double)(r % L);
-  const double theta = pos * pow(base, -2.0 * f / (2.0 * half));
-  double s, c;
-  sincos(theta, &s, &c);
-  table[i] = make_float2((float)c, (float)s);
+  const double theta = pos * exp2(-2.0 * f / (2.0 * half) * log2(base));
+  // reduce to [-pi, pi] in fp64 (theta reaches ~1e4 rad), then an fp32 sincos of the small angle
+  const double kTwoPi = 6.283185307179586476925286766559;
+  const float red = (float)(theta - kTwoPi * rint(theta / kTwoPi));
+  float s, c;
+  sincosf(red, &s, &c);
+  table[i] = make_float2(c, s);
 }
 
-// one item = 8 consecutive pair indices i of one (b, l, head): 16 B of each half
+// one CTA per (b, l) row; a thread item = 8 consecutive pair indices i of one head: 16 B of each
+// half (32-bit index math only; the row's table entry is shared by all its heads)
 __global__ void __launch_bounds__(256) ttt_qkv_rope_kernel(const __nv_bfloat16* __restrict__ qkv,
                                                            const float2* __restrict__ table, int per_seq_table,
-                                                           int B, int L, int Hq, int Hkv, int D,
+                                                           int L, int Hq, int Hkv, int D,
                                                            __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k,
                                                            __nv_bfloat16* __restrict__ v) {
   const int half = D / 2, cpp = half / 8;  // 8-element chunks per half
   const int H = Hq + 2 * Hkv;
-  const long long items = (long long)B * L * H * cpp;
-  for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < items;
-       it += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(it % cpp);
-    const long long rh = it / cpp;  // (b, l, h)
-    const int h = (int)(rh % H);
-    const long long bl = rh / H;    // b * L + l
-    const __nv_bfloat16* src = qkv + rh * D + c * 8;
+  const size_t bl = blockIdx.x;  // b * L + l
+  const float2* trow = table + (per_seq_table ? bl : bl % (size_t)L) * half;
+  const __nv_bfloat16* srow = qkv + bl * (size_t)H * D;
+  for (int i = threadIdx.x; i < H * cpp; i += blockDim.x) {
+    const int h = i / cpp, c = i - h * cpp;
+    const __nv_bfloat16* src = srow + h * D + c * 8;
     const uint4 a = *reinterpret_cast<const uint4*>(src);
     const uint4 bb = *reinterpret_cast<const uint4*>(src + half);
     __nv_bfloat16* dst;
@@ -56,7 +59,7 @@ __global__ void __launch_bounds__(256) ttt_qkv_rope_kernel(const __nv_bfloat16* 
       *reinterpret_cast<uint4*>(dst + half + c * 8) = bb;
       continue;
     }
-    const float2* tb = table + (per_seq_table ? bl : bl % L) * half + c * 8;
+    const float2* tb = trow + c * 8;
     const __nv_bfloat162* x1 = reinterpret_cast<const __nv_bfloat162*>(&a);
     const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&bb);
     uint4 o1, o2;
@@ -76,35 +79,33 @@ __global__ void __launch_bounds__(256) ttt_qkv_rope_kernel(const __nv_bfloat16* 
 }
 
 // backward of the split: dqkv = [R(-theta) dq | R(-theta) dk | dv] in the fused layout (the
-// rotation is orthogonal, so its adjoint is the rotation by -theta)
+// rotation is orthogonal, so its adjoint is the rotation by -theta); same row-per-CTA layout
 __global__ void __launch_bounds__(256) ttt_qkv_rope_join_kernel(const __nv_bfloat16* __restrict__ dq,
                                                                 const __nv_bfloat16* __restrict__ dk,
                                                                 const __nv_bfloat16* __restrict__ dv,
                                                                 const float2* __restrict__ table, int per_seq_table,
-                                                                int B, int L, int Hq, int Hkv, int D,
+                                                                int L, int Hq, int Hkv, int D,
                                                                 __nv_bfloat16* __restrict__ dqkv) {
   const int half = D / 2, cpp = half / 8;
   const int H = Hq + 2 * Hkv;
-  const long long items = (long long)B * L * H * cpp;
-  for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < items;
-       it += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(it % cpp);
-    const long long rh = it / cpp;
-    const int h = (int)(rh % H);
-    const long long bl = rh / H;
+  const size_t bl = blockIdx.x;
+  const float2* trow = table + (per_seq_table ? bl : bl % (size_t)L) * half;
+  __nv_bfloat16* drow = dqkv + bl * (size_t)H * D;
+  for (int i = threadIdx.x; i < H * cpp; i += blockDim.x) {
+    const int h = i / cpp, c = i - h * cpp;
     const __nv_bfloat16* src;
     if (h < Hq) src = dq + (bl * Hq + h) * D;
     else if (h < Hq + Hkv) src = dk + (bl * Hkv + (h - Hq)) * D;
     else src = dv + (bl * Hkv + (h - Hq - Hkv)) * D;
     const uint4 a = *reinterpret_cast<const uint4*>(src + c * 8);
     const uint4 bb = *reinterpret_cast<const uint4*>(src + half + c * 8);
-    __nv_bfloat16* dst = dqkv + rh * D + c * 8;
+    __nv_bfloat16* dst = drow + h * D + c * 8;
     if (h >= Hq + Hkv) {
       *reinterpret_cast<uint4*>(dst) = a;
       *reinterpret_cast<uint4*>(dst + half) = bb;
       continue;
     }
-    const float2* tb = table + (per_seq_table ? bl : bl % L) * half + c * 8;
+    const float2* tb = trow + c * 8;
     const __nv_bfloat162* g1 = reinterpret_cast<const __nv_bfloat162*>(&a);
     const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&bb);
     uint4 o1, o2;
@@ -143,6 +144,7 @@ int ttt_qkv_rope_split(const ttt_rope_desc* d, const void* qkv, const int32_t* p
   if (d->batch < 1 || d->seq_len < 1 || d->num_q_heads < 1 || d->num_kv_heads < 1 || !(d->rope_base > 1.f))
     return TTT_ERR_INVALID_ARG;
   if (d->head_dim < 16 || d->head_dim % 16) return TTT_ERR_UNSUPPORTED;
+  if ((long long)d->batch * d->seq_len >= (1ll << 31)) return TTT_ERR_UNSUPPORTED;  // one CTA per row
   if (!a16(qkv) || !a16(q) || !a16(k_slot) || !a16(v_slot) || !a16(workspace)) return TTT_ERR_ALIGNMENT;
   const size_t need = ttt_rope_workspace_size(d, positions != nullptr);
   if (!workspace || workspace_bytes < need) return TTT_ERR_WORKSPACE;
@@ -153,11 +155,9 @@ int ttt_qkv_rope_split(const ttt_rope_desc* d, const void* qkv, const int32_t* p
   cudaGetLastError();
   ttt_rope_table_kernel<<<(rows * half + 255) / 256, 256, 0, st>>>(positions, rows, d->seq_len, half,
                                                                    (double)d->rope_base, table);
-  const long long items = (long long)d->batch * d->seq_len * (d->num_q_heads + 2 * d->num_kv_heads) * (half / 8);
-  long long blocks = (items + 255) / 256;
-  if (blocks > 148LL * 16) blocks = 148LL * 16;
-  ttt_qkv_rope_kernel<<<(unsigned)blocks, 256, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(qkv), table, positions != nullptr, d->batch, d->seq_len, d->num_q_heads,
+  const unsigned rows_bl = (unsigned)(d->batch * d->seq_len);
+  ttt_qkv_rope_kernel<<<rows_bl, 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(qkv), table, positions != nullptr, d->seq_len, d->num_q_heads,
       d->num_kv_heads, d->head_dim, static_cast<__nv_bfloat16*>(q), static_cast<__nv_bfloat16*>(k_slot),
       static_cast<__nv_bfloat16*>(v_slot));
   return cudaGetLastError() == cudaSuccess ? TTT_OK : TTT_ERR_CUDA;
@@ -180,13 +180,11 @@ int ttt_qkv_rope_join_bwd(const ttt_rope_desc* d, const void* dq, const void* dk
   cudaGetLastError();
   ttt_rope_table_kernel<<<(rows * half + 255) / 256, 256, 0, st>>>(positions, rows, d->seq_len, half,
                                                                    (double)d->rope_base, table);
-  const long long items = (long long)d->batch * d->seq_len * (d->num_q_heads + 2 * d->num_kv_heads) * (half / 8);
-  long long blocks = (items + 255) / 256;
-  if (blocks > 148LL * 16) blocks = 148LL * 16;
-  ttt_qkv_rope_join_kernel<<<(unsigned)blocks, 256, 0, st>>>(
+  const unsigned rows_bl = (unsigned)(d->batch * d->seq_len);
+  ttt_qkv_rope_join_kernel<<<rows_bl, 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(dq), static_cast<const __nv_bfloat16*>(dk_slot),
-      static_cast<const __nv_bfloat16*>(dv_slot), table, positions != nullptr, d->batch, d->seq_len,
-      d->num_q_heads, d->num_kv_heads, d->head_dim, static_cast<__nv_bfloat16*>(dqkv));
+      static_cast<const __nv_bfloat16*>(dv_slot), table, positions != nullptr, d->seq_len, d->num_q_heads,
+      d->num_kv_heads, d->head_dim, static_cast<__nv_bfloat16*>(dqkv));
   return cudaGetLastError() == cudaSuccess ? TTT_OK : TTT_ERR_CUDA;
 }
 
