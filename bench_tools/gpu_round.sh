@@ -11,3 +11,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ttt_loss_ring -s 1 -c 1 -o gpurun_out/${T}_loss_full python bench_tools/prof_loss.py > gpurun_out/${T}_loss_ncu.log 2>&1
 cat gpurun_out/${T}_pytest.txt gpurun_out/${T}_smoke.txt | tail -8; tail -c 2500 gpurun_out/${T}_bench.json
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ttt_ -c 5 -o gpurun_out/${T}_attn_full python bench_tools/prof_one.py llama8b 6 > gpurun_out/${T}_attn_ncu.log 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:"ttt_fwd_sm100|ttt_qkv_rope_kernel" -c 2 -o gpurun_out/${T}_next_full python bench_tools/prof_next.py > gpurun_out/${T}_next_ncu.log 2>&1
