@@ -171,11 +171,13 @@ int ttt_attn_bwd_unroll(const ttt_attn_desc* desc, int num_steps,
  *   lse      fp32 [batch][Hq][num_tree]                out  natural-log logsumexp over the allowed keys
  *   workspace >= ttt_tree_attn_workspace_size(desc) bytes (the per-node ancestor bit masks).
  * Errors: 1 <= num_tree <= TTT_MAX_TREE, 0 <= prefix_lens[b], prefix_lens[b] + num_tree <= kv_len
- * (else TTT_ERR_DEGENERATE), head_dim 64 / 128; BF16 only. */
+ * (else TTT_ERR_DEGENERATE), head_dim 64 / 128. dtype TTT_FP32_CHECK: every tensor fp32, a
+ * CUDA-core kernel that checks the semantics at 1e-5 (no workspace needed). */
 #define TTT_MAX_TREE 64
 typedef struct {
   int32_t batch, num_tree, kv_len, num_q_heads, num_kv_heads, head_dim;
   float softmax_scale;         /* 0 => 1/sqrt(head_dim) */
+  int32_t dtype;               /* TTT_BF16 (tensor-core path) or TTT_FP32_CHECK (fp32 CUDA-core check path) */
   const int32_t* prefix_lens;  /* HOST int32[batch]: P_b, the verified context length */
 } ttt_tree_desc;
 size_t ttt_tree_attn_workspace_size(const ttt_tree_desc* desc);

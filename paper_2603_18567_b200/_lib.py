@@ -47,7 +47,8 @@ class TreeDesc(ctypes.Structure):
     """ttt_tree_desc (include/ttt_attn.h)."""
     _fields_ = [("batch", ctypes.c_int32), ("num_tree", ctypes.c_int32), ("kv_len", ctypes.c_int32),
                 ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
-                ("softmax_scale", ctypes.c_float), ("prefix_lens", ctypes.POINTER(ctypes.c_int32))]
+                ("softmax_scale", ctypes.c_float), ("dtype", ctypes.c_int32),
+                ("prefix_lens", ctypes.POINTER(ctypes.c_int32))]
 
 
 TTT_MAX_TREE = 64
@@ -246,8 +247,9 @@ def ttt_attn_bwd_unroll(desc: Desc, q: Sequence, k_base, v_base, k_steps, v_step
 
 
 def tree_desc(batch: int, num_tree: int, kv_len: int, num_q_heads: int, num_kv_heads: int, head_dim: int,
-              prefix_lens: Sequence[int], softmax_scale: float = 0.0) -> TreeDesc:
+              prefix_lens: Sequence[int], softmax_scale: float = 0.0, dtype: int = TTT_BF16) -> TreeDesc:
     d = TreeDesc()
+    d.dtype = int(dtype)
     d.batch, d.num_tree, d.kv_len = int(batch), int(num_tree), int(kv_len)
     d.num_q_heads, d.num_kv_heads, d.head_dim = int(num_q_heads), int(num_kv_heads), int(head_dim)
     d.softmax_scale = float(softmax_scale)

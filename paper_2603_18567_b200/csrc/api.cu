@@ -22,6 +22,7 @@ int fwd_diag_rows_per_group(const Params& p);
 cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st);
 int bwd_pre_rows_per_group(const Params& p);
 cudaError_t launch_tree_sm100(const Params& p, const FwdMaps& maps, const int32_t* parents, cudaStream_t st);
+cudaError_t launch_tree_check(const Params& p, cudaStream_t st);
 cudaError_t launch_tree_combine(const void* part, const float* lse_part, int nsplit, int B, int n, int Hq, int D,
                                 void* out, float* lse, cudaStream_t st);
 cudaError_t launch_bwd_unroll_sm100(const Params* ps, const BwdMaps* maps, const PreMaps& pmaps,
@@ -478,9 +479,30 @@ int ttt_tree_attn_fwd(const ttt_tree_desc* d, const void* q, const void* k_cache
   if ((long long)d->batch * d->kv_len * d->num_kv_heads >= (1ll << 31)) return TTT_ERR_UNSUPPORTED;
   for (int b = 0; b < d->batch; ++b)
     if (d->prefix_lens[b] < 0 || d->prefix_lens[b] + d->num_tree > d->kv_len) return TTT_ERR_DEGENERATE;
+  if (d->dtype != TTT_BF16 && d->dtype != TTT_FP32_CHECK) return TTT_ERR_INVALID_ARG;
   const void* ptrs[] = {q, k_cache, v_cache, out, lse};
   for (const void* ptr : ptrs)
     if (!aligned16(ptr)) return TTT_ERR_ALIGNMENT;
+  if (d->dtype == TTT_FP32_CHECK) {  // fp32 CUDA-core check path, no workspace
+    Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.B = d->batch;
+    p.Hq = d->num_q_heads;
+    p.Hkv = d->num_kv_heads;
+    p.D = d->head_dim;
+    p.G = p.Hq / p.Hkv;
+    p.scale = d->softmax_scale > 0.f ? d->softmax_scale : 1.0f / std::sqrt((float)p.D);
+    for (int b = 0; b < p.B; ++b) p.seq_lens[b] = d->prefix_lens[b];
+    p.tree_n = d->num_tree;
+    p.tree_kv_len = d->kv_len;
+    p.tree_parents = parents;
+    p.q = q;
+    p.k = k_cache;
+    p.v = v_cache;
+    p.out = out;
+    p.lse = lse;
+    return cuda_status(launch_tree_check(p, static_cast<cudaStream_t>(stream)));
+  }
   const TreeWs tw = tree_ws_layout(d);
   if (!workspace || workspace_bytes < tw.total) return TTT_ERR_WORKSPACE;
   if (!aligned16(workspace)) return TTT_ERR_ALIGNMENT;

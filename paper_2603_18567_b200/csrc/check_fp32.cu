@@ -157,6 +157,70 @@ cudaError_t launch_fwd_check(const Params& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Tree-attention verification, fp32 check path: one warp per (b, node t, head h) row; keys =
+// the P_b context rows, then the tree rows of t's ancestors and t itself (walking the parents).
+template <int D>
+__global__ void __launch_bounds__(256) tree_check_kernel(const Params p) {
+  constexpr int E = D / 32;
+  const int lane = threadIdx.x & 31;
+  const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int n = p.tree_n;
+  if (warp >= (long)p.B * n * p.Hq) return;
+  const int h = (int)(warp % p.Hq);
+  const int t = (int)((warp / p.Hq) % n);
+  const int b = (int)(warp / ((long)p.Hq * n));
+  const int g = h / p.G;
+  const int P = p.seq_lens[b];
+  const float* qrow = (const float*)p.q + (((size_t)b * n + t) * p.Hq + h) * D;
+  float qv[E], acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    qv[e] = qrow[lane + 32 * e];
+    acc[e] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  const size_t kv_stride = (size_t)p.Hkv * D;
+  const float* K = (const float*)p.k + ((size_t)b * p.tree_kv_len * p.Hkv + g) * D;
+  const float* V = (const float*)p.v + ((size_t)b * p.tree_kv_len * p.Hkv + g) * D;
+  auto visit = [&](int k) {
+    const float* krow = K + k * kv_stride;
+    const float* vrow = V + k * kv_stride;
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) s = fmaf(qv[e], krow[lane + 32 * e], s);
+    s = warp_sum(s) * p.scale;
+    const float mn = fmaxf(m, s);
+    const float a = expf(m - mn), w = expf(s - mn);
+    l = l * a + w;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = fmaf(w, vrow[lane + 32 * e], acc[e] * a);
+    m = mn;
+  };
+  for (int k = 0; k < P; ++k) visit(k);
+  const int32_t* par = p.tree_parents + (size_t)b * n;
+  int u = t, prev = t + 1;
+  while (u >= 0 && u < prev) {  // t, parent(t), ... (a parent index >= the child ends the walk)
+    visit(P + u);
+    prev = u;
+    u = par[u];
+  }
+  float* orow = (float*)p.out + (((size_t)b * n + t) * p.Hq + h) * D;
+  const float inv = 1.f / l;
+#pragma unroll
+  for (int e = 0; e < E; ++e) orow[lane + 32 * e] = acc[e] * inv;
+  if (lane == 0) p.lse[((size_t)b * p.Hq + h) * n + t] = m + logf(l);
+}
+
+cudaError_t launch_tree_check(const Params& p, cudaStream_t st) {
+  const long rows = (long)p.B * p.Hq * p.tree_n;
+  const int blocks = (int)((rows + 7) / 8);
+  prof_mark(kKindCheckFwd, true, st);
+  if (p.D == 64) tree_check_kernel<64><<<blocks, 256, 0, st>>>(p);
+  else tree_check_kernel<128><<<blocks, 256, 0, st>>>(p);
+  prof_mark(kKindCheckFwd, false, st);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bwd_check(const Params& p, cudaStream_t st) {
   const long rows = (long)p.B * p.Hq * p.L;
   const int blocks = (int)((rows + 7) / 8);

@@ -49,6 +49,8 @@ struct Params {
   int tree_n;                              // n tree tokens (queries), <= 64
   const unsigned long long* tree_mask;     // [B][n] ancestor-or-self bit masks (bit u = tree key u)
   int tree_splits;                         // context splits per (b, kv head); > 1: partial out / lse
+  int tree_kv_len;                         // rows of the K / V cache (check path)
+  const int32_t* tree_parents;             // [B][n] parent indices (check path)
 };
 
 // Tensor maps for the tcgen05 paths (4-D: D, H, L, B; box 64 x 1 x 128 x 1, SW128)

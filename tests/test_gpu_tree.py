@@ -21,15 +21,18 @@ CASES = [  # (batch, n, prefix_lens, Hq, Hkv, D)
     (1, 50, [2040], 8, 2, 128),         # context split over 4 CTAs; tree keys straddle the last two tiles
     (2, 64, [4000, 700], 4, 2, 128),    # uneven contexts, splits by the shorter one
     (1, 64, [1000], 8, 2, 128),         # one tile per split: nodes 0-23 have no key in the last split
+    (1, 48, [3000], 64, 4, 128),        # Qwen3-235B target heads (G = 16: four head quads per kv head)
 ]
 
 
 def _run(c, extra_rows=0):
     B, n = c.q.shape[:2]
     Hq, Hkv, D = c.q.shape[2], c.k.shape[2], c.q.shape[3]
-    d = ttt.tree_desc(B, n, c.k.shape[1], Hq, Hkv, D, c.prefix_lens)
+    fp32 = c.q.dtype == torch.float32
+    d = ttt.tree_desc(B, n, c.k.shape[1], Hq, Hkv, D, c.prefix_lens,
+                      dtype=ttt.TTT_FP32_CHECK if fp32 else ttt.TTT_BF16)
     dev = lambda t: t.cuda().contiguous()
-    out = torch.empty(B, n, Hq, D, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty(B, n, Hq, D, dtype=c.q.dtype, device="cuda")
     lse = torch.empty(B, Hq, n, dtype=torch.float32, device="cuda")
     ws = torch.empty(ttt.ttt_tree_attn_workspace_size(d), dtype=torch.uint8, device="cuda")
     ttt.ttt_tree_attn_fwd(d, dev(c.q), dev(c.k), dev(c.v), dev(c.parents), out, lse, ws)
@@ -60,3 +63,14 @@ def test_tree_chain_and_deterministic():
     f = lambda t: t.float().numpy()
     o_out, _ = OT.tree_attention(f(c.q), f(c.k), f(c.v), c.prefix_lens, c.parents.numpy())
     assert np.abs(a[0] - o_out).max() <= 2e-2 + 1e-2 * np.abs(o_out).max()
+
+
+@pytest.mark.parametrize("case", CASES[:4] + CASES[6:7], ids=lambda c: f"fp32_B{c[0]}n{c[1]}")
+def test_tree_attention_fp32_check_mode(case):
+    """TTT_FP32_CHECK: the CUDA-core fp32 path against the oracle at the north_star 1e-5."""
+    B, n, P, Hq, Hkv, D = case
+    c = make_tree_case(B, n, P, Hq, Hkv, D, dtype=torch.float32, seed=n + 1, kv_len=max(P) + n + 3)
+    out, lse = _run(c)
+    o_out, o_lse = OT.tree_attention(c.q.numpy(), c.k.numpy(), c.v.numpy(), P, c.parents.numpy())
+    np.testing.assert_allclose(out, o_out, rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(lse, o_lse, rtol=1e-5, atol=1e-5)
