@@ -367,6 +367,9 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         line["next_rows"] = {"loss_inplace": run_loss(args, stream, peaks, world)}
         if world == 1:
             line["next_rows"]["longctx"] = run_longctx(args, stream, peaks)
+            line["next_rows"]["qwen235b"] = run_config(
+                "qwen235b", stream, peaks,
+                "Qwen3-235B-A22B draft shape (BASELINE configs[2]): 1 x L=4096, 64/4 heads, D=128, ttt_steps=7, bf16")
         line["next_rows"]["tree_verify"] = run_tree(args, stream, peaks)
         line["next_rows"]["qkv_rope"] = run_rope(args, stream, peaks)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -509,12 +512,9 @@ def run_tree(args, stream, peaks):
                                   "pipeline, then a combine pass merges the splits")}}
 
 
-def run_longctx(args, stream, peaks):
-    """BASELINE.json configs[3] beside the headline: one 7-step unroll of a single L = 16384
-    sequence (Llama-3.1-8B draft heads), fwd + bwd, on one GPU. Across GPUs this shape splits by
-    kv-head block (dp.seq_to_head), each rank running this same kernel
-    sequence on Hq/N, Hkv/N heads."""
-    shape = CONFIGS["longctx"]
+def run_config(name: str, stream, peaks, workload: str):
+    """A BASELINE.json configuration beside the headline: one 7-step unroll (fwd + bwd) on one GPU."""
+    shape = CONFIGS[name]
     u = Unroll(shape, seed=99, dev=stream.device)
     for _ in range(2):
         u.step(stream)
@@ -531,9 +531,16 @@ def run_longctx(args, stream, peaks):
     tflops = 12 * shape.head_dim * sum(per_step_pairs) / (ms / 1e3) / 1e12
     del u
     torch.cuda.empty_cache()
-    return {"workload": "long-context: 1 x L=16384, 32/8 heads, D=128, ttt_steps=7, bf16, fwd+bwd unroll",
-            "ms_per_step": ms, "tokens_per_s": shape.batch * shape.seq_len / (ms / 1e3), "steps": n,
-            "tflops": tflops, "frac_of_bf16_peak": tflops / peaks["bf16_tflops_sustained"]}
+    return {"workload": workload, "ms_per_step": ms, "tokens_per_s": shape.batch * shape.seq_len / (ms / 1e3),
+            "steps": n, "tflops": tflops, "frac_of_bf16_peak": tflops / peaks["bf16_tflops_sustained"]}
+
+
+def run_longctx(args, stream, peaks):
+    """BASELINE.json configs[3]: 1 x L = 16384, Llama-3.1-8B draft heads. Across GPUs this shape
+    splits by kv-head block (dp.seq_to_head), each rank running this same
+    kernel sequence on Hq/N, Hkv/N heads."""
+    return run_config("longctx", stream, peaks,
+                      "long-context: 1 x L=16384, 32/8 heads, D=128, ttt_steps=7, bf16, fwd+bwd unroll")
 
 
 def run_e2e(u: Unroll, stream, args, shape: Shape):
