@@ -543,6 +543,73 @@ def run_longctx(args, stream, peaks):
                       "long-context: 1 x L=16384, 32/8 heads, D=128, ttt_steps=7, bf16, fwd+bwd unroll")
 
 
+def run_head_parallel(args, shape: Shape, rank: int, world: int, local_rank: int):
+    """--head-parallel: one long sequence split over N GPUs by kv-head
+    block. Every rank starts from sequence shards [L/N, H, D] of q_j / dO_j / K / V (as
+    sequence-parallel projections produce them), one NCCL all-to-all per tensor turns them into head
+    shards [L, H/N, D] (dp.seq_to_head), the rank runs the whole unroll on Hq/N, Hkv/N heads with no
+    communication inside the attention, and out_j, dq_j, dK, dV go back to sequence shards
+    (dp.head_to_seq). Strong scaling: the total work is fixed. (The exchange is gloo-tested and the
+    head-block result is checked equal to the full problem on one GPU, tests/test_gpu_head_parallel.py.)"""
+    import torch.distributed as dist
+
+    from paper_2603_18567_b200.dp import head_to_seq, max_over_ranks, seq_to_head
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B, L, Hq, Hkv, D, S = shape.batch, shape.seq_len, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, shape.ttt_steps
+    if B != 1 or Hkv % world or L % world:
+        raise SystemExit("--head-parallel needs batch 1 and Hkv, L divisible by the GPU count")
+    local = Shape(1, L, Hq // world, Hkv // world, D, S)
+    u = Unroll(local, seed=1234 + rank, dev=dev)
+    stream = torch.cuda.current_stream(dev)
+    g = torch.Generator(device=dev).manual_seed(77 + rank)
+    shard = lambda H: torch.randn((L // world, H, D), device=dev, generator=g).to(torch.bfloat16)
+    q_sh, do_sh = [shard(Hq) for _ in range(S)], [shard(Hq) for _ in range(S)]
+    kv_sh = [shard(Hkv) for _ in range(2 * S)]  # K_0, V_0, K_1.., V_1..
+
+    def one_step():
+        for j in range(S):
+            u.q[j].view(L, Hq // world, D).copy_(seq_to_head(q_sh[j], world))
+            u.do[j].view(L, Hq // world, D).copy_(seq_to_head(do_sh[j], world))
+        kv = [u.k, u.v] + u.ks + u.vs
+        for t, sh in zip(kv, kv_sh):
+            t.view(L, Hkv // world, D).copy_(seq_to_head(sh, world))
+        u.step(stream)
+        outs = [head_to_seq(x.view(L, Hq // world, D), world) for x in u.out + u.dq]
+        grads = [head_to_seq(x.view(L, Hkv // world, D), world) for x in [u.dk, u.dv] + u.dks + u.dvs]
+        return outs, grads
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1), device=dev) / args.steps
+    per_step_pairs, _ = alg_pairs(shape)
+    tflops = 12 * D * sum(per_step_pairs) / (ms / 1e3) / 1e12
+    peaks = load_peaks()
+    line = {
+        "metric": METRIC, "value": L / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch Philox N(0,1) -> bf16)",
+        "config": {"workload": f"long-context head-parallel: 1 x L={L}, {Hq}/{Hkv} heads split over {world} GPUs, "
+                               f"ttt_steps={S}, incl. the seq<->head all-to-alls", "global_batch": 1,
+                   "seq_len": L, "parallelism": f"head-parallel{world}"},
+        "tflops_per_gpu": tflops / world, "frac_of_bf16_peak": tflops / world / peaks["bf16_tflops_sustained"],
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_e2e(u: Unroll, stream, args, shape: Shape):
     """Same metric through the public API with host buffers: every step copies the unroll's
     inputs H2D from pinned memory and reads the accumulated base gradients dK_0, dV_0 back
@@ -618,6 +685,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-loss", action="store_true", help="skip the §8(f) loss-kernel measurement")
+    ap.add_argument("--head-parallel", action="store_true",
+                    help="split one long sequence (e.g. --config longctx) over the GPUs by kv-head block "
+                         "(NCCL all-to-alls around the attention; strong scaling)")
     ap.add_argument("--zero2", action="store_true",
                     help="ZeRO-2 draft gradient exchange (reduce-scatter per backward call + parameter all-gather "
                          "after the step, PAPER.md:281) instead of the bucketed all-reduce")
@@ -635,14 +705,20 @@ def main():
     if args.impl == "reference":
         run_reference(args, shape, rank, world)
         return
-    if world > 1:
+    if world > 1 or args.head_parallel:
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if world == 1:  # single-rank head-parallel run (plumbing check): a 1-process NCCL group
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank), rank=rank, world_size=world)
     try:
-        run_ours(args, shape, rank, world, local_rank)
+        if args.head_parallel:
+            run_head_parallel(args, shape, rank, world, local_rank)
+        else:
+            run_ours(args, shape, rank, world, local_rank)
     finally:
-        if world > 1:
+        if world > 1 or args.head_parallel:
             import torch.distributed as dist
             dist.destroy_process_group()
 
