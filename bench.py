@@ -1,14 +1,21 @@
 #!/usr/bin/env python
 """bench.py — TTT unrolled attention fwd+bwd on B200 (the driver's bench contract).
 
-One bench "step" = one TTT unroll of the EAGLE-3 draft layer attention at the
-Llama-3.1-8B draft shape (BASELINE.json configs[1]: B=8, L=2048, 32 q / 8 kv
-heads, head_dim 128, ttt_steps 7, bf16): 7 forward calls (j = 0..6) then 7
-backward calls (j = 6..0, the first overwriting, the rest accumulating
-dK/dV), all through the C-ABI (libtttattn.so). At N > 1 GPUs each rank runs
-the same per-GPU unroll on its own sequences (data parallel by sequence, weak
-scaling) and the draft-layer gradient bucket is all-reduced over NCCL,
-bucket i released after backward call i (DDP-style overlap).
+One bench "step" = one optimizer step of the EAGLE-3 draft layer's TTT attention:
+the rank's micro-batches, each one TTT unroll (7 forward calls j = 0..6, then 7
+backward calls j = 6..0, the first overwriting, the rest accumulating dK/dV), all
+through the C-ABI (libtttattn.so), then ONE draft-gradient exchange.
+
+  N = 1 (default --config llama8b): BASELINE.json configs[1], the Llama-3.1-8B draft
+        shape B=8, L=2048, 32 q / 8 kv heads, head_dim 128, ttt_steps 7, bf16 — one
+        micro-batch per step.
+  N > 1 (default --config dp): BASELINE.json configs[4], the DP scaling sweep — global
+        batch 64 x L=4096 per optimizer step, 64/N sequences per rank as micro-batches
+        of 8 (strong scaling), the draft-layer gradient bucket all-reduced over NCCL once
+        per optimizer step after the last micro-batch's backward (the draft's parameters
+        are shared by every TTT step and micro-batch, so their gradients are final only
+        then). The N = 1 point of this sweep is reported beside the headline as
+        next_rows.dp_sweep_n1.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -164,20 +171,35 @@ def run_reference(args, shape: Shape, rank: int, world: int):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(shape, world),
+        "scaling": "strong" if args.config == "dp" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": workload_config(shape, world, args.config),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(shape: Shape, world: int):
-    return {"workload": "llama3.1-8b-eagle3-draft TTT attention unroll (fwd j=0..6 + bwd j=6..0)",
-            "batch_per_gpu": shape.batch, "global_batch": shape.batch * world, "seq_len": shape.seq_len,
-            "num_q_heads": shape.num_q_heads, "num_kv_heads": shape.num_kv_heads, "head_dim": shape.head_dim,
-            "ttt_steps": shape.ttt_steps, "seq_lens": "full (T_b = L)", "parallelism": f"dp{world}",
-            "l2": "inputs larger than L2 (~5 GB touched per step vs 126 MB L2); no flush"}
+def global_batch_of(cfg: str, shape: Shape, world: int) -> int:
+    """Sequences per optimizer step, all ranks: configs[4] fixes 64 (strong scaling); the other
+    configs run one micro-batch per rank (weak scaling)."""
+    return 64 if cfg == "dp" else shape.batch * world
+
+
+def workload_config(shape: Shape, world: int, cfg: str = "llama8b"):
+    gb = global_batch_of(cfg, shape, world)
+    names = {"llama8b": "llama3.1-8b-eagle3-draft TTT attention unroll (fwd j=0..6 + bwd j=6..0)",
+             "dp": "DP sweep (BASELINE configs[4]): llama3.1-8b-eagle3-draft TTT attention, global batch 64 x "
+                   "L=4096 per optimizer step, micro-batches of 8, one NCCL grad all-reduce per step"}
+    per_rank = gb // world
+    return {"workload": names.get(cfg, f"{cfg} TTT attention unroll"), "config": cfg,
+            "batch_per_gpu": per_rank, "micro_batch": shape.batch,
+            "micro_batches_per_rank": -(-per_rank // shape.batch), "global_batch": gb,
+            "seq_len": shape.seq_len, "num_q_heads": shape.num_q_heads, "num_kv_heads": shape.num_kv_heads,
+            "head_dim": shape.head_dim, "ttt_steps": shape.ttt_steps, "seq_lens": "full (T_b = L)",
+            "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2 (~5 GB touched per unroll vs 126 MB L2); no flush in the headline; "
+                  "cold_l2 = the same unroll after a 512 MB L2 flush"}
 
 
 # --------------------------------------------------------------------------- our arm
@@ -207,36 +229,41 @@ class Unroll:
         self.desc = ttt.make_desc(s.batch, s.seq_len, s.num_q_heads, s.num_kv_heads, s.head_dim)
         self.ws = torch.empty(ttt.ttt_attn_workspace_size(self.desc, S - 1, True), dtype=torch.uint8, device=dev)
         self.inputs = self.q + self.do + [self.k, self.v] + self.ks + self.vs
+        # every result of the unroll (what a caller reads back): out_j, lse_j, dq_j, dK_0, dV_0, dK_i, dV_i
+        self.outputs = self.out + self.lse + self.dq + [self.dk, self.dv] + self.dks + self.dvs
         self.bwd_unroll = bwd_unroll  # one ttt_attn_bwd_unroll call for the S backward calls
         if bwd_unroll:
             self.ws_unroll = torch.empty(ttt.ttt_attn_bwd_unroll_workspace_size(self.desc, S), dtype=torch.uint8,
                                          device=dev)
 
-    def step(self, stream, on_bwd=None, marks=None):
+    def step(self, stream, marks=None):
         """One unroll. `marks` (optional): dict of CUDA events recorded around every call,
         marks[("fwd", j)] / marks[("bwd", j)] = (start, end), for per-step times."""
         t, s = self.ttt, self.s
         S = s.ttt_steps
         ev = lambda key: marks.setdefault(key, (torch.cuda.Event(enable_timing=True),
                                                 torch.cuda.Event(enable_timing=True))) if marks is not None else None
+        nvtx = torch.cuda.nvtx
         for j in range(S):
             e = ev(("fwd", j))
+            nvtx.range_push(f"ttt fwd j={j}")
             if e:
                 e[0].record(stream)
             t.ttt_attn_fwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, self.out[j], self.lse[j],
                            out_lo=self.out_lo[j], stream=stream)
             if e:
                 e[1].record(stream)
+            nvtx.range_pop()
         if self.bwd_unroll:
+            nvtx.range_push("ttt bwd unroll")
             t.ttt_attn_bwd_unroll(self.desc, self.q, self.k, self.v, self.ks, self.vs, self.out, self.lse, self.do,
                                   self.dq, self.dk, self.dv, self.dks, self.dvs, flags=0, workspace=self.ws_unroll,
                                   stream=stream, out_lo=self.out_lo)
-            if on_bwd is not None:
-                for i in range(S):
-                    on_bwd(i)
+            nvtx.range_pop()
             return
         for j in reversed(range(S)):
             e = ev(("bwd", j))
+            nvtx.range_push(f"ttt bwd j={j}")
             if e:
                 e[0].record(stream)
             t.ttt_attn_bwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, self.out[j], self.lse[j],
@@ -245,37 +272,47 @@ class Unroll:
                            out_lo=self.out_lo[j])
             if e:
                 e[1].record(stream)
-            if on_bwd is not None:
-                on_bwd(S - 1 - j)
+            nvtx.range_pop()
+
+
+def pick_peak(peaks, clocks):
+    """roofline peak matching the clock record of the timed region: the burst bf16 figure when the
+    SMs ran near their max clock (>= 90%), the sustained (power-capped) one otherwise."""
+    sm, mx = clocks.get("sm_mhz"), clocks.get("sm_max_mhz")
+    if sm is not None and mx and sm >= 0.9 * mx:
+        return peaks["bf16_tflops"], "burst"
+    return peaks["bf16_tflops_sustained"], "sustained"
 
 
 def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
     import paper_2603_18567_b200 as ttt
+    from paper_2603_18567_b200.dp import GradBuckets, OptimizerStep, Zero2Buckets, max_over_ranks
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-    u = Unroll(shape, seed=1234 + rank, dev=dev, bwd_unroll=args.bwd_unroll)
+    cfg = args.config
+    gb = global_batch_of(cfg, shape, world)
     stream = torch.cuda.current_stream(dev)
     S = shape.ttt_steps
 
-    # draft-layer gradient bucket (synthetic stand-in), bf16, one bucket per bwd call
-    from paper_2603_18567_b200.dp import GradBuckets, Zero2Buckets, max_over_ranks
+    # draft-layer gradient bucket (synthetic stand-in of the draft's parameter gradients, DESIGN.md §7), bf16,
+    # 7 buckets; exchanged once per optimizer step after the last micro-batch's backward (dp.OptimizerStep)
     Buckets = Zero2Buckets if args.zero2 else GradBuckets
-    grads = Buckets(DRAFT_PARAMS if world > 1 else 1, S, dtype=torch.bfloat16, device=dev)
+    grads = Buckets(DRAFT_PARAMS if world > 1 else 1, 7, dtype=torch.bfloat16, device=dev)
     params = torch.zeros_like(grads.flat) if args.zero2 and world > 1 else None
     if world > 1:
         grads.flat.normal_()
-
-    def on_bwd(i):
-        grads.release(i)
+    opt = OptimizerStep(grads, gb, shape.batch, world, rank, params)
+    # micro-batch buffer sets (two alternate when a rank runs several micro-batches per step)
+    sets = [Unroll(shape, seed=1234 + rank, dev=dev, bwd_unroll=args.bwd_unroll)]
+    if len(opt.micro) > 1:
+        sets.append(Unroll(shape, seed=5678 + rank, dev=dev, bwd_unroll=args.bwd_unroll))
+    u = sets[0]
 
     def one_step():
-        u.step(stream, on_bwd)
-        grads.finish()
-        if params is not None:  # ZeRO-2: the updated parameter shards are re-replicated
-            grads.gather_params(params)
+        opt.run(lambda m, lo, hi: sets[m % len(sets)].step(stream))
 
     for _ in range(args.warmup):
         one_step()
@@ -289,8 +326,10 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         w0 = time.perf_counter()
         e0.record(stream)
+        torch.cuda.nvtx.range_push(f"timed region: {args.steps} steps")
         for _ in range(args.steps):
             one_step()
+        torch.cuda.nvtx.range_pop()
         e1.record(stream)
         torch.cuda.synchronize()
         if dist is not None:
@@ -298,8 +337,9 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         wall = time.perf_counter() - w0
     ms = max_over_ranks(e0.elapsed_time(e1), device=dev)
     ms_per_step = ms / args.steps
-    tokens_per_step = shape.batch * shape.seq_len * world
+    tokens_per_step = gb * shape.seq_len
     value = tokens_per_step / (ms_per_step / 1e3)
+    clocks = clk.summary()
 
     # ---------------- per-kernel attribution (separate pass, CUDA events on the launch stream) ----------
     prof_steps = 2
@@ -319,12 +359,27 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
             torch.cuda.synchronize()
             for (kind, j), (a, b) in marks.items():
                 per_step[f"{kind}_ms"][j] += a.elapsed_time(b) / reps
+    # cold L2 (SURVEY.md §8d "report both warm and cold"): one unroll right after a 512 MB write
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    cold = []
+    for _ in range(3):
+        flush.zero_()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        u.step(stream)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        cold.append(c0.elapsed_time(c1))
+    del flush
+    warm_unroll_ms = ms_per_step / len(opt.micro) if world == 1 else None
 
     peaks = load_peaks()
+    peak, peak_kind = pick_peak(peaks, clocks)
     per_step_pairs, base_pairs = alg_pairs(shape)
     D = shape.head_dim
-    flops_step = 12 * D * sum(per_step_pairs)  # algorithmic: fwd 4D + bwd 8D per allowed pair
-    tflops = flops_step * world / (ms_per_step / 1e3) / 1e12 / world  # per GPU
+    n_unrolls = gb // shape.batch  # unrolls (micro-batches) per optimizer step, all ranks
+    flops_step = 12 * D * sum(per_step_pairs) * n_unrolls  # algorithmic: fwd 4D + bwd 8D per allowed pair
+    tflops = flops_step / (ms_per_step / 1e3) / 1e12 / world  # per GPU
     # dominant kernel -> roofline
     dom = max(kern.items(), key=lambda kv: kv[1][0])
     dom_name, (dom_ms, dom_n) = dom
@@ -336,33 +391,39 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
     if dom_name in per_launch_flops:
         avg_ms = dom_ms / dom_n
         achieved = per_launch_flops[dom_name] / (avg_ms / 1e3) / 1e12
-        peak = peaks["bf16_tflops_sustained"]
         roof = {"kernel": dom_name, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "peak_kind": f"bf16 sustained ({peaks['source']}, MEASURED_PEAKS.json)",
-                "frac_of_burst": achieved / peaks["bf16_tflops"], "avg_launch_ms": avg_ms,
+                "frac": achieved / peak,
+                "peak_kind": f"bf16 {peak_kind} ({peaks['source']}, MEASURED_PEAKS.json), chosen by the timed "
+                             f"region's clock record",
+                "frac_of_burst": achieved / peaks["bf16_tflops"],
+                "frac_of_sustained": achieved / peaks["bf16_tflops_sustained"], "avg_launch_ms": avg_ms,
                 "share_of_step": dom_ms / prof_steps / ms_per_step if world == 1 else None,
                 "traffic": ncu_traffic(dom_name), "algorithmic_flops_per_launch": per_launch_flops[dom_name]}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if cfg == "dp" else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch Philox N(0,1) -> bf16, random per rank)",
-        "config": workload_config(shape, world),
-        "tflops_per_gpu": tflops, "frac_of_bf16_peak": tflops / peaks["bf16_tflops_sustained"],
+        "config": workload_config(shape, world, cfg),
+        "tflops_per_gpu": tflops, "frac_of_bf16_peak": tflops / peak, "bf16_peak_kind": peak_kind,
         "frac_of_bf16_burst_peak": tflops / peaks["bf16_tflops"],
+        "frac_of_bf16_sustained_peak": tflops / peaks["bf16_tflops_sustained"],
         "flops_convention": "algorithmic 12*D per allowed (q,k) pair (fwd 4D + bwd 8D; recompute excluded)",
         "roofline": roof,
         "kernels_ms_per_step": {k: v[0] / prof_steps for k, v in kern.items()},
         "per_ttt_step_ms": per_step,
+        "cold_l2": {"ms_per_unroll": statistics.median(cold), "warm_ms_per_unroll": warm_unroll_ms,
+                    "flush": "512 MB device write before each unroll (not timed)"},
         "gpu_launches": launches_per_step * args.steps,
         "grad_allreduce_bytes_per_step": grads.nbytes if world > 1 else 0,
         "grad_exchange": ("zero2 reduce-scatter + param all-gather" if args.zero2 else "bucketed all-reduce (AVG)")
-        if world > 1 else "none (1 GPU)",
+        + ", once per optimizer step after the last micro-batch's backward" if world > 1 else "none (1 GPU)",
         "wall_s_timed_region": wall,
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
-    if world == 1 and not args.no_e2e:
-        line["e2e"] = run_e2e(u, stream, args, shape)
+    if not args.no_e2e:
+        line["e2e"] = run_e2e(sets, opt, stream, args, shape, gb, dev)
     if not args.no_loss:
         line["next_rows"] = {"loss_inplace": run_loss(args, stream, peaks, world)}
         if world == 1:
@@ -370,6 +431,10 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
             line["next_rows"]["qwen235b"] = run_config(
                 "qwen235b", stream, peaks,
                 "Qwen3-235B-A22B draft shape (BASELINE configs[2]): 1 x L=4096, 64/4 heads, D=128, ttt_steps=7, bf16")
+            if cfg != "dp":
+                del sets, u, opt
+                torch.cuda.empty_cache()
+                line["next_rows"]["dp_sweep_n1"] = run_dp_n1(args, stream, peaks)
         line["next_rows"]["tree_verify"] = run_tree(args, stream, peaks)
         line["next_rows"]["qkv_rope"] = run_rope(args, stream, peaks)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -382,6 +447,36 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
                        f"tokens-equivalent = {n}")}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def run_dp_n1(args, stream, peaks):
+    """The N = 1 point of the BASELINE configs[4] DP sweep (global batch 64 x L = 4096 per optimizer
+    step = 8 micro-batches of 8 on one GPU), so the sweep's scaling can be read against it (the N > 1
+    bench lines run this config by default)."""
+    from paper_2603_18567_b200.dp import GradBuckets, OptimizerStep
+    shape = CONFIGS["dp"]
+    dev = stream.device
+    sets = [Unroll(shape, seed=91, dev=dev), Unroll(shape, seed=92, dev=dev)]
+    opt = OptimizerStep(GradBuckets(1, 7, device=dev), 64, shape.batch, 1, 0)
+    one = lambda: opt.run(lambda m, lo, hi: sets[m % 2].step(stream))
+    one()
+    torch.cuda.synchronize()
+    n = 2
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    per_step_pairs, _ = alg_pairs(shape)
+    tflops = 12 * shape.head_dim * sum(per_step_pairs) * 8 / (ms / 1e3) / 1e12
+    del sets
+    torch.cuda.empty_cache()
+    return {"workload": "BASELINE configs[4] at N=1: global batch 64 x L=4096 (8 micro-batches of 8), 32/8 heads, "
+                        "D=128, ttt_steps=7, bf16", "ms_per_step": ms, "tokens_per_s": 64 * 4096 / (ms / 1e3),
+            "steps": n, "tflops": tflops, "frac_of_bf16_burst_peak": tflops / peaks["bf16_tflops"],
+            "frac_of_bf16_sustained_peak": tflops / peaks["bf16_tflops_sustained"]}
 
 
 def run_loss(args, stream, peaks, world: int):
@@ -610,56 +705,75 @@ def run_head_parallel(args, shape: Shape, rank: int, world: int, local_rank: int
         print(json.dumps(line), flush=True)
 
 
-def run_e2e(u: Unroll, stream, args, shape: Shape):
-    """Same metric through the public API with host buffers: every step copies the unroll's
-    inputs H2D from pinned memory and reads the accumulated base gradients dK_0, dV_0 back
-    D2H (the unroll's result), copies included. Inputs are double-buffered like a data
-    loader's prefetch: step i+1's H2D copies run on a copy stream while step i computes
-    (each buffer set is refilled only after the step that read it has finished)."""
-    u2 = Unroll(shape, seed=4321, dev=stream.device, bwd_unroll=u.bwd_unroll)
-    sets = [u, u2]
+def run_e2e(sets, opt, stream, args, shape: Shape, gb: int, dev):
+    """Same metric through the public API with host buffers. Every micro-batch's inputs (q_j, dO_j,
+    K_0, V_0, K_i, V_i) are copied H2D from pinned memory and EVERY result of its unroll (out_j,
+    lse_j, dq_j, dK_0, dV_0, dK_i, dV_i) is read back D2H into pinned memory, copies inside the timed
+    region. Buffers are double-buffered like a data loader's prefetch: micro-batch i+1's H2D runs on
+    a copy stream while micro-batch i computes, and micro-batch i's D2H on a second copy stream while
+    micro-batch i+1 computes (a buffer set is refilled only after its results were read back)."""
+    import paper_2603_18567_b200  # noqa: F401
+    if len(sets) == 1:
+        sets = [sets[0], Unroll(shape, seed=4321, dev=dev, bwd_unroll=sets[0].bwd_unroll)]
+    u = sets[0]
     host_in = [t.cpu().pin_memory() for t in u.inputs]
-    host_out = [torch.empty(u.dk.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+    host_out = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in u.outputs] for _ in range(2)]
     h2d = sum(t.numel() * t.element_size() for t in host_in)
-    d2h = sum(t.numel() * t.element_size() for t in host_out)
+    d2h = sum(t.numel() * t.element_size() for t in host_out[0])
+    per_step = len(opt.micro)
     n = max(3, min(args.steps, 6))
-    cstream = torch.cuda.Stream(device=stream.device)
+    cin, cout = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     ev = lambda: torch.cuda.Event()
-    h2d_done, comp_done = [ev(), ev()], [ev(), ev()]
+    h2d_done, comp_done, d2h_done = [ev(), ev()], [ev(), ev()], [ev(), ev()]
+    state = {"i": 0, "total": 0}
 
     def copy_in(k):
-        with torch.cuda.stream(cstream):
-            cstream.wait_event(comp_done[k])
+        with torch.cuda.stream(cin):
+            cin.wait_event(comp_done[k])
             for d, h in zip(sets[k].inputs, host_in):
                 d.copy_(h, non_blocking=True)
-            h2d_done[k].record(cstream)
+            h2d_done[k].record(cin)
+
+    def micro(m, lo, hi):
+        i = state["i"]
+        k = i % 2
+        if i + 1 < state["total"]:
+            copy_in(1 - k)
+        stream.wait_event(h2d_done[k])
+        stream.wait_event(d2h_done[k])
+        sets[k].step(stream)
+        comp_done[k].record(stream)
+        with torch.cuda.stream(cout):
+            cout.wait_event(comp_done[k])
+            for h, d in zip(host_out[k], sets[k].outputs):
+                h.copy_(d, non_blocking=True)
+            d2h_done[k].record(cout)
+        state["i"] = i + 1
 
     def run(steps):
+        state["i"], state["total"] = 0, steps * per_step
         for k in range(2):
             comp_done[k].record(stream)
+            d2h_done[k].record(stream)
         copy_in(0)
-        for i in range(steps):
-            k = i % 2
-            if i + 1 < steps:
-                copy_in(1 - k)
-            stream.wait_event(h2d_done[k])
-            sets[k].step(stream)
-            host_out[0].copy_(sets[k].dk, non_blocking=True)
-            host_out[1].copy_(sets[k].dv, non_blocking=True)
-            comp_done[k].record(stream)
+        for _ in range(steps):
+            opt.run(micro)
 
     run(2)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     run(n)
-    stream.wait_stream(cstream)
+    stream.wait_stream(cin)
+    stream.wait_stream(cout)
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / n
-    return {"value": shape.batch * shape.seq_len / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n,
-            "overlap": "double-buffered inputs: step i+1's H2D on a copy stream under step i's compute"}
+    from paper_2603_18567_b200.dp import max_over_ranks
+    ms = max_over_ranks(e0.elapsed_time(e1), device=dev) / n
+    return {"value": gb * shape.seq_len / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": h2d * per_step, "d2h_bytes_per_step": d2h * per_step, "steps": n,
+            "overlap": "double-buffered micro-batches: H2D of the next and D2H of the previous on two copy "
+                       "streams under the current one's compute; D2H = every output of each unroll"}
 
 
 def ncu_traffic(kernel: str):
@@ -681,7 +795,8 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="llama8b", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="workload (default: llama8b = BASELINE configs[1] at N = 1, dp = configs[4] at N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-loss", action="store_true", help="skip the §8(f) loss-kernel measurement")
@@ -701,6 +816,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config is None:
+        args.config = "llama8b" if world == 1 or args.head_parallel else "dp"
     shape = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, shape, rank, world)

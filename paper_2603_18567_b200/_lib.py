@@ -177,6 +177,42 @@ def _check(code: int):
         raise TTTError(code, ttt_attn_strerror(code))
 
 
+def _validate(spec, *, device=None):
+    """Host-side checks of the torch tensors handed to a C-ABI call: the C side sees
+    only raw pointers, so a non-contiguous view, a dtype mismatch or a tensor on another device
+    would otherwise read or write the wrong bytes. `spec`: (name, tensor, dtype | None, shape |
+    None) tuples; entries that are not torch tensors (None, or the pointer stand-ins of the
+    CPU-only validation tests) are skipped. Raises TTTError(TTT_ERR_INVALID_ARG)."""
+    dev = device
+    for name, t, dt, shape in spec:
+        if not isinstance(t, torch.Tensor):
+            continue
+        if not t.is_cuda:
+            raise TTTError(1, f"{name} must be a CUDA tensor (got {t.device})")
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise TTTError(1, f"{name} is on {t.device}, the other arguments on {dev}")
+        if not t.is_contiguous():
+            raise TTTError(1, f"{name} must be contiguous (row-major); pass .contiguous()")
+        if dt is not None and t.dtype != dt:
+            raise TTTError(1, f"{name} must be {dt} (got {t.dtype})")
+        if shape is not None and tuple(t.shape) != tuple(shape):
+            raise TTTError(1, f"{name} must have shape {tuple(shape)} (got {tuple(t.shape)})")
+    return dev
+
+
+def _attn_shapes(desc: "Desc"):
+    B, L, Hq, Hkv, D = desc.batch, desc.seq_len, desc.num_q_heads, desc.num_kv_heads, desc.head_dim
+    dt = torch.float32 if desc.dtype == TTT_FP32_CHECK else torch.bfloat16
+    return dt, (B, L, Hq, D), (B, L, Hkv, D), (B, Hq, L)
+
+
+def _check_list(name: str, ts, n: int):
+    if len(ts) < n:
+        raise TTTError(1, f"{name} has {len(ts)} entries, step needs {n}")
+
+
 TTT_KERNEL_KINDS = 10
 
 
@@ -208,6 +244,13 @@ def ttt_attn_workspace_size(desc: Desc, step: int, is_bwd: bool) -> int:
 def ttt_attn_fwd(desc: Desc, step: int, q, k_base, v_base, k_steps, v_steps, out, lse,
                  out_lo=None, workspace=None, stream=None) -> None:
     """Enqueue ttt_attn_fwd (include/ttt_attn.h) on `stream` (default: current)."""
+    dt, qs, kvs, ls = _attn_shapes(desc)
+    _check_list("k_steps", k_steps, step)
+    _check_list("v_steps", v_steps, step)
+    _validate([("q", q, dt, qs), ("k_base", k_base, dt, kvs), ("v_base", v_base, dt, kvs), ("out", out, dt, qs),
+               ("out_lo", out_lo, torch.bfloat16, qs), ("lse", lse, torch.float32, ls)]
+              + [(f"k_steps[{i}]", k_steps[i], dt, kvs) for i in range(max(step, 0))]
+              + [(f"v_steps[{i}]", v_steps[i], dt, kvs) for i in range(max(step, 0))])
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(_lib.ttt_attn_fwd(ctypes.byref(desc), int(step), _ptr(q), _ptr(k_base), _ptr(v_base),
                              _ptr_list(k_steps[:step]), _ptr_list(v_steps[:step]), _ptr(out), _ptr(out_lo),
@@ -218,6 +261,19 @@ def ttt_attn_bwd(desc: Desc, step: int, q, k_base, v_base, k_steps, v_steps, out
                  dq, dk_base, dv_base, dk_steps, dv_steps, flags: int = 0, workspace=None,
                  stream=None, out_lo=None) -> None:
     """Enqueue ttt_attn_bwd (include/ttt_attn.h) on `stream` (default: current)."""
+    dt, qs, kvs, ls = _attn_shapes(desc)
+    f32 = torch.float32
+    for nm, lst in (("k_steps", k_steps), ("v_steps", v_steps), ("dk_steps", dk_steps), ("dv_steps", dv_steps)):
+        _check_list(nm, lst, step)
+    n = max(step, 0)
+    _validate([("q", q, dt, qs), ("k_base", k_base, dt, kvs), ("v_base", v_base, dt, kvs), ("out", out, dt, qs),
+               ("out_lo", out_lo, torch.bfloat16, qs), ("lse", lse, f32, ls), ("dout", dout, dt, qs),
+               ("dq", dq, dt, qs), ("dk_base", dk_base, f32, kvs), ("dv_base", dv_base, f32, kvs)]
+              + [(f"k_steps[{i}]", k_steps[i], dt, kvs) for i in range(n)]
+              + [(f"v_steps[{i}]", v_steps[i], dt, kvs) for i in range(n)]
+              + [(f"dk_steps[{i}]", dk_steps[i], f32, kvs) for i in range(n)]
+              + [(f"dv_steps[{i}]", dv_steps[i], f32, kvs) for i in range(n)]
+              + [("workspace", workspace, None, None)])
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(_lib.ttt_attn_bwd(ctypes.byref(desc), int(step), _ptr(q), _ptr(k_base), _ptr(v_base),
                              _ptr_list(k_steps[:step]), _ptr_list(v_steps[:step]), _ptr(out), _ptr(out_lo),
@@ -237,6 +293,25 @@ def ttt_attn_bwd_unroll(desc: Desc, q: Sequence, k_base, v_base, k_steps, v_step
     """Enqueue ttt_attn_bwd_unroll (include/ttt_attn.h): the S = len(q) backward calls of one
     unroll (j = S-1 .. 0) in one call; per-step lists q / out / out_lo / lse / dout / dq."""
     S = len(q)
+    dt, qs, kvs, ls = _attn_shapes(desc)
+    f32 = torch.float32
+    for nm, lst in (("out", out), ("lse", lse), ("dout", dout), ("dq", dq)):
+        _check_list(nm, lst, S)
+    if out_lo is not None:
+        _check_list("out_lo", out_lo, S)
+    for nm, lst in (("k_steps", k_steps), ("v_steps", v_steps), ("dk_steps", dk_steps), ("dv_steps", dv_steps)):
+        _check_list(nm, lst, S - 1)
+    spec = [("k_base", k_base, dt, kvs), ("v_base", v_base, dt, kvs), ("dk_base", dk_base, f32, kvs),
+            ("dv_base", dv_base, f32, kvs), ("workspace", workspace, None, None)]
+    for j in range(S):
+        spec += [(f"q[{j}]", q[j], dt, qs), (f"out[{j}]", out[j], dt, qs), (f"lse[{j}]", lse[j], f32, ls),
+                 (f"dout[{j}]", dout[j], dt, qs), (f"dq[{j}]", dq[j], dt, qs)]
+        if out_lo is not None:
+            spec.append((f"out_lo[{j}]", out_lo[j], torch.bfloat16, qs))
+    for i in range(max(S - 1, 0)):
+        spec += [(f"k_steps[{i}]", k_steps[i], dt, kvs), (f"v_steps[{i}]", v_steps[i], dt, kvs),
+                 (f"dk_steps[{i}]", dk_steps[i], f32, kvs), (f"dv_steps[{i}]", dv_steps[i], f32, kvs)]
+    _validate(spec)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(_lib.ttt_attn_bwd_unroll(
         ctypes.byref(desc), S, _ptr_list(q), _ptr(k_base), _ptr(v_base), _ptr_list(k_steps[:S - 1]),
@@ -265,6 +340,12 @@ def ttt_tree_attn_workspace_size(desc: TreeDesc) -> int:
 
 def ttt_tree_attn_fwd(desc: TreeDesc, q, k_cache, v_cache, parents, out, lse, workspace, stream=None) -> None:
     """Enqueue ttt_tree_attn_fwd (include/ttt_attn.h): tree-attention verification forward."""
+    dt = torch.float32 if desc.dtype == TTT_FP32_CHECK else torch.bfloat16
+    B, n, KV, Hq, Hkv, D = desc.batch, desc.num_tree, desc.kv_len, desc.num_q_heads, desc.num_kv_heads, desc.head_dim
+    _validate([("q", q, dt, (B, n, Hq, D)), ("k_cache", k_cache, dt, (B, KV, Hkv, D)),
+               ("v_cache", v_cache, dt, (B, KV, Hkv, D)), ("parents", parents, torch.int32, (B, n)),
+               ("out", out, dt, (B, n, Hq, D)), ("lse", lse, torch.float32, (B, Hq, n)),
+               ("workspace", workspace, None, None)])
     _check(_lib.ttt_tree_attn_fwd(ctypes.byref(desc), _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(parents),
                                   _ptr(out), _ptr(lse), _ptr(workspace), _nbytes(workspace), _stream(stream)))
 
@@ -286,6 +367,11 @@ def ttt_rope_workspace_size(desc: RopeDesc, per_sequence_positions: bool = False
 def ttt_qkv_rope_split(desc: RopeDesc, qkv, q, k_slot, v_slot, workspace, positions=None, stream=None) -> None:
     """Enqueue ttt_qkv_rope_split (include/ttt_attn.h): RoPE'd q and the step's K / V slots from a
     fused q/k/v projection output, one HBM pass."""
+    B, Lr, Hq, Hkv, D = desc.batch, desc.seq_len, desc.num_q_heads, desc.num_kv_heads, desc.head_dim
+    bf = torch.bfloat16
+    _validate([("qkv", qkv, bf, (B, Lr, Hq + 2 * Hkv, D)), ("positions", positions, torch.int32, (B, Lr)),
+               ("q", q, bf, (B, Lr, Hq, D)), ("k_slot", k_slot, bf, (B, Lr, Hkv, D)),
+               ("v_slot", v_slot, bf, (B, Lr, Hkv, D)), ("workspace", workspace, None, None)])
     _check(_lib.ttt_qkv_rope_split(ctypes.byref(desc), _ptr(qkv), _ptr(positions), _ptr(q), _ptr(k_slot),
                                    _ptr(v_slot), _ptr(workspace), _nbytes(workspace), _stream(stream)))
 
@@ -293,6 +379,11 @@ def ttt_qkv_rope_split(desc: RopeDesc, qkv, q, k_slot, v_slot, workspace, positi
 
 def ttt_qkv_rope_join_bwd(desc: RopeDesc, dq, dk_slot, dv_slot, dqkv, workspace, positions=None, stream=None) -> None:
     """Enqueue ttt_qkv_rope_join_bwd: the adjoint of ttt_qkv_rope_split (gradients -> dqkv)."""
+    B, Lr, Hq, Hkv, D = desc.batch, desc.seq_len, desc.num_q_heads, desc.num_kv_heads, desc.head_dim
+    bf = torch.bfloat16
+    _validate([("dq", dq, bf, (B, Lr, Hq, D)), ("dk_slot", dk_slot, bf, (B, Lr, Hkv, D)),
+               ("dv_slot", dv_slot, bf, (B, Lr, Hkv, D)), ("positions", positions, torch.int32, (B, Lr)),
+               ("dqkv", dqkv, bf, (B, Lr, Hq + 2 * Hkv, D)), ("workspace", workspace, None, None)])
     _check(_lib.ttt_qkv_rope_join_bwd(ctypes.byref(desc), _ptr(dq), _ptr(dk_slot), _ptr(dv_slot), _ptr(positions),
                                       _ptr(dqkv), _ptr(workspace), _nbytes(workspace), _stream(stream)))
 
@@ -316,8 +407,21 @@ def _nbytes(t) -> int:
     return 0 if t is None else t.numel() * t.element_size()
 
 
+def _loss_validate(desc: LossDesc, z, p, mask, g_rows=None, grad=None, lse=None, stats=None, workspace=None):
+    dt = torch.float32 if desc.dtype == TTT_FP32_CHECK else torch.bfloat16
+    N, V = desc.rows, desc.vocab
+    _validate([("z", z, dt, None), ("p", p, dt, None), ("grad", grad, dt, None), ("mask", mask, torch.uint8, None),
+               ("g_rows", g_rows, torch.float32, None), ("lse", lse, torch.float32, None),
+               ("stats", stats, torch.float64, None), ("workspace", workspace, None, None)])
+    for nm, t, n in (("z", z, N * V), ("p", p, N * V), ("grad", grad, N * V), ("mask", mask, N),
+                     ("g_rows", g_rows, N), ("lse", lse, N), ("stats", stats, 2)):
+        if isinstance(t, torch.Tensor) and t.numel() != n:
+            raise TTTError(1, f"{nm} has {t.numel()} elements, expected {n}")
+
+
 def ttt_loss_fwd(desc: LossDesc, z, p, mask, stats, workspace, lse=None, stream=None) -> None:
     """Enqueue ttt_loss_fwd: stats (fp64 [2]) = {masked mean loss, masked-row count}."""
+    _loss_validate(desc, z, p, mask, lse=lse, stats=stats, workspace=workspace)
     _check(_lib.ttt_loss_fwd(ctypes.byref(desc), _ptr(z), _ptr(p), _ptr(mask), _ptr(lse), _ptr(stats),
                              _ptr(workspace), _nbytes(workspace), _stream(stream)))
 
@@ -325,6 +429,7 @@ def ttt_loss_fwd(desc: LossDesc, z, p, mask, stats, workspace, lse=None, stream=
 def ttt_loss_bwd_inplace(desc: LossDesc, z, p, mask, workspace, g_scale: float = 1.0, flags: int = TTT_LOSS_MEAN,
                          g_rows=None, grad=None, stream=None) -> None:
     """Enqueue Alg. 3: z <- dL/dz in place (or into `grad` when given)."""
+    _loss_validate(desc, z, p, mask, g_rows=g_rows, grad=grad, workspace=workspace)
     _check(_lib.ttt_loss_bwd_inplace(ctypes.byref(desc), _ptr(z), _ptr(p), _ptr(mask), _ptr(g_rows),
                                      float(g_scale), int(flags), _ptr(grad), _ptr(workspace), _nbytes(workspace),
                                      _stream(stream)))
@@ -333,6 +438,7 @@ def ttt_loss_bwd_inplace(desc: LossDesc, z, p, mask, workspace, g_scale: float =
 def ttt_loss_fwd_bwd_inplace(desc: LossDesc, z, p, mask, stats, workspace, g_scale: float = 1.0,
                              flags: int = TTT_LOSS_MEAN, g_rows=None, grad=None, lse=None, stream=None) -> None:
     """Enqueue the fused loss + Alg. 3 backward (one pass: z, p read once, gradient written over z)."""
+    _loss_validate(desc, z, p, mask, g_rows=g_rows, grad=grad, lse=lse, stats=stats, workspace=workspace)
     _check(_lib.ttt_loss_fwd_bwd_inplace(ctypes.byref(desc), _ptr(z), _ptr(p), _ptr(mask), _ptr(g_rows),
                                          float(g_scale), int(flags), _ptr(grad), _ptr(lse), _ptr(stats),
                                          _ptr(workspace), _nbytes(workspace), _stream(stream)))

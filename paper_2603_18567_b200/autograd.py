@@ -37,7 +37,9 @@ class _TTTAttention(torch.autograd.Function):
     @staticmethod
     def forward(ctx, step: int, seq_lens, scale: float, q, k_base, v_base, *kv_steps):
         j = int(step)
-        k_steps, v_steps = list(kv_steps[:j]), list(kv_steps[j:2 * j])
+        c = lambda t: t.contiguous()  # the C-ABI takes raw row-major pointers (views are copied here)
+        q, k_base, v_base = c(q), c(k_base), c(v_base)
+        k_steps, v_steps = [c(t) for t in kv_steps[:j]], [c(t) for t in kv_steps[j:2 * j]]
         desc = L.desc_for(q, k_base, seq_lens=seq_lens, softmax_scale=scale)
         B, Lq, Hq, D = q.shape
         out = torch.empty_like(q)
@@ -89,7 +91,10 @@ def ttt_attention(q: torch.Tensor, k_base: torch.Tensor, v_base: torch.Tensor,
 class _TTTAttentionUnroll(torch.autograd.Function):
     @staticmethod
     def forward(ctx, S: int, seq_lens, scale: float, k_base, v_base, *rest):
-        qs, ks, vs = list(rest[:S]), list(rest[S:2 * S - 1]), list(rest[2 * S - 1:3 * S - 2])
+        c = lambda t: t.contiguous()
+        k_base, v_base = c(k_base), c(v_base)
+        qs = [c(t) for t in rest[:S]]
+        ks, vs = [c(t) for t in rest[S:2 * S - 1]], [c(t) for t in rest[2 * S - 1:3 * S - 2]]
         desc = L.desc_for(qs[0], k_base, seq_lens=seq_lens, softmax_scale=scale)
         B, Lq, Hq, D = qs[0].shape
         outs, los, lses = [], [], []
@@ -149,6 +154,7 @@ def ttt_attention_unroll(qs: Sequence[torch.Tensor], k_base: torch.Tensor, v_bas
 class _QkvRopeSplit(torch.autograd.Function):
     @staticmethod
     def forward(ctx, qkv, Hq: int, Hkv: int, base: float, positions):
+        qkv = qkv.contiguous()
         B, Lr, H, D = qkv.shape
         d = L.rope_desc(B, Lr, Hq, Hkv, D, base)
         ws = torch.empty(max(L.ttt_rope_workspace_size(d, positions is not None), 16), dtype=torch.uint8,
@@ -156,7 +162,7 @@ class _QkvRopeSplit(torch.autograd.Function):
         q = torch.empty(B, Lr, Hq, D, dtype=qkv.dtype, device=qkv.device)
         k = torch.empty(B, Lr, Hkv, D, dtype=qkv.dtype, device=qkv.device)
         v = torch.empty_like(k)
-        L.ttt_qkv_rope_split(d, qkv.contiguous(), q, k, v, ws, positions=positions)
+        L.ttt_qkv_rope_split(d, qkv, q, k, v, ws, positions=positions)
         ctx.d, ctx.ws, ctx.positions, ctx.shape = d, ws, positions, qkv.shape
         return q, k, v
 
@@ -183,22 +189,34 @@ def qkv_rope_split(qkv: torch.Tensor, num_q_heads: int, num_kv_heads: int, rope_
 class _SoftLabelLoss(torch.autograd.Function):
     @staticmethod
     def forward(ctx, z, p, mask, g_rows):
+        if not z.is_contiguous():
+            raise ValueError("soft_label_loss: z must be contiguous (its buffer is overwritten in place by "
+                             "the backward; a copy would defeat Alg. 3)")
+        p, mask = p.contiguous(), mask.contiguous()
+        g_rows = None if g_rows is None else g_rows.contiguous()
         desc = L.loss_desc_for(z)
         ws = torch.empty(L.ttt_loss_workspace_size(desc), dtype=torch.uint8, device=z.device)
         stats = torch.empty(2, dtype=torch.float64, device=z.device)
         L.ttt_loss_fwd(desc, z, p, mask, stats, ws)
-        ctx.desc, ctx.ws = desc, ws
+        ctx.desc, ctx.ws, ctx.done = desc, ws, False
         ctx.save_for_backward(z, p, mask, g_rows)
         return stats[0].to(torch.float32)
 
     @staticmethod
     def backward(ctx, g):
+        if ctx.done:
+            raise RuntimeError("soft_label_loss: backward ran already; z now holds dL/dz (Alg. 3 in place), "
+                               "so a second backward (retain_graph=True) cannot recompute it")
         z, p, mask, g_rows = ctx.saved_tensors
         ws = ctx.ws
         # Alg. 3 in place: z <- dL/dz. The upstream scalar g enters as g_scale; it is read on the
         # host (one sync) because the C-ABI takes g_scale by value.
         L.ttt_loss_bwd_inplace(ctx.desc, z, p, mask, ws, g_scale=float(g), flags=L.TTT_LOSS_MEAN,
                                g_rows=g_rows)
+        ctx.done = True
+        # z's storage now holds the gradient: bump its version counter so any other autograd node
+        # that saved z (e.g. a z-loss on the same logits) fails loudly instead of reading dL/dz
+        torch.autograd.graph.increment_version(z)
         return z, None, None, None
 
 

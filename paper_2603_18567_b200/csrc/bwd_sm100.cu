@@ -1094,13 +1094,9 @@ cudaError_t launch_main_convert(const Params& p_in, const BwdMaps& maps, cudaStr
   }
   {
     const int smem = BwdSmem<D>::bytes;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaError_t e =
-          cudaFuncSetAttribute(ttt_bwd_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      attr_set = true;
-    }
+    static std::atomic<unsigned long long> attr_done{0};
+    cudaError_t ea = set_smem_attr(ttt_bwd_sm100_kernel<D>, smem, attr_done);
+    if (ea != cudaSuccess) return ea;
     const int grid = p.nqt * p.B * p.Hkv * p.head_split;
     prof_mark(kKindBwdMain, true, st);
     ttt_bwd_sm100_kernel<D><<<grid, kBwdThreads, smem, st>>>(p, maps);

@@ -773,11 +773,10 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
     p.order_batch = pick_order_batch(p.B * p.Hkv, p.nqt, (p.G + 1) / 2, len.data(), 7.0, (double)p.L * D * 4);
   }
   const int smem = 6 * kTile * D * 2 + 1024;
-  static bool attr_set = false;  // benign race: idempotent attribute set
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(ttt_fwd_sm100_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static std::atomic<unsigned long long> attr_done{0};
+  {
+    cudaError_t e = set_smem_attr(ttt_fwd_sm100_kernel<D, false>, smem, attr_done);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   if (p.step > 0) {
     DiagLayout lay;
@@ -856,11 +855,10 @@ cudaError_t launch_tree_d(const Params& p_in, const FwdMaps& maps, const int32_t
   p.nqt = 1;
   p.order_batch = p.B * p.Hkv;
   const int smem = 6 * kTile * D * 2 + 1024;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(ttt_fwd_sm100_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static std::atomic<unsigned long long> attr_done{0};
+  {
+    cudaError_t e = set_smem_attr(ttt_fwd_sm100_kernel<D, true>, smem, attr_done);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int nm = p.B * p.tree_n;
   ttt_tree_mask_kernel<<<(nm + 127) / 128, 128, 0, st>>>(parents, p.B, p.tree_n,

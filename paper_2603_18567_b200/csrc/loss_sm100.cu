@@ -500,12 +500,10 @@ cudaError_t launch_loss_t(LossParams P, cudaStream_t st) {
 template <typename T, int E, int NV>
 cudaError_t launch_loss_ring_t(const LossParams& P, cudaStream_t st) {
   const int smem = 2 * ((P.vocab * (int)sizeof(T) + 15) & ~15);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ttt_loss_ring_kernel<T, E, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         2 * 65536);
+  static std::atomic<unsigned long long> attr_done{0};  // per device
+  {
+    cudaError_t e = set_smem_attr(ttt_loss_ring_kernel<T, E, NV>, 2 * 65536, attr_done);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   int sms = 148;
   int dev = 0;

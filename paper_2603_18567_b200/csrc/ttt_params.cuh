@@ -2,6 +2,7 @@
 // the kernels. Passed BY VALUE (kernel params live in constant bank), so a call
 // keeps no state in the library.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -99,6 +100,20 @@ void prof_mark(int kind, bool start, cudaStream_t st);
 // batch (groups interleaved longest-first inside a batch) with the smallest simulated makespan
 // over 148 greedy SMs, among batches whose L2 working set stays under ~80 MB.
 // `copies` CTAs share each (group, rank); len_of_rank[i] in units of one work item.
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per (function, device context): set it once
+// per device ordinal (bit d of `done`), thread-safely; devices >= 64 set it on every launch.
+template <typename F>
+inline cudaError_t set_smem_attr(F* fn, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
 int pick_order_batch(int ngroups, int nranks, int copies, const double* len_of_rank, double overhead,
                      double bytes_per_group);
 

@@ -26,14 +26,26 @@ def shard_sequences(global_batch: int, world: int, rank: int) -> Tuple[int, int]
     return lo, hi
 
 
+def micro_batches(global_batch: int, micro: int, world: int, rank: int) -> List[Tuple[int, int]]:
+    """The sequence ranges [lo, hi) of `rank`'s micro-batches for one optimizer step: its
+    contiguous shard of the global batch (shard_sequences) cut into chunks of `micro` sequences
+    (BASELINE configs[4]: global batch 64 at 1/2/4/8 GPUs, micro-batches of 8 -> 64/N per rank)."""
+    if micro < 1:
+        raise ValueError("micro-batch size must be >= 1")
+    lo, hi = shard_sequences(global_batch, world, rank)
+    return [(a, min(a + micro, hi)) for a in range(lo, hi, micro)]
+
+
 class GradBuckets:
     """A flat draft-layer gradient buffer split into `n` buckets.
 
-    `release(i)` starts an asynchronous all-reduce of bucket i (issued right
-    after the backward call that finalises it, so it overlaps the remaining
-    backward calls on the communication stream); `finish()` waits for all of
-    them and applies the 1/world average. On NCCL the collective runs on its own
-    stream ordered after the current stream's work at release time.
+    The draft layer's parameters are shared by every TTT step and every micro-batch of an
+    optimizer step, so a parameter gradient is final only after the LAST micro-batch's step-0
+    backward. `release_all()` is therefore called once per optimizer step, after that backward:
+    it starts the asynchronous all-reduces of the buckets in reverse parameter order (the order
+    a layer-by-layer backward would finish them); `finish()` waits for all of them and applies
+    the 1/world average. On NCCL the collectives run on NCCL's stream ordered after the current
+    stream's work at release time. `release(i)` (one bucket) stays for finer-grained callers.
     """
 
     def __init__(self, numel: int, n: int, dtype=torch.bfloat16, device="cpu", group=None):
@@ -48,6 +60,11 @@ class GradBuckets:
         self.works.append(dist.all_reduce(self.buckets[i], op=dist.ReduceOp.SUM, group=self.group,
                                           async_op=True))
 
+    def release_all(self) -> None:
+        """Once per optimizer step, after the last micro-batch's full backward (see class doc)."""
+        for i in reversed(range(len(self.buckets))):
+            self.release(i)
+
     def finish(self) -> None:
         world = dist.get_world_size(self.group) if dist.is_initialized() else 1
         while self.works:
@@ -58,6 +75,31 @@ class GradBuckets:
     @property
     def nbytes(self) -> int:
         return self.flat.numel() * self.flat.element_size()
+
+
+class OptimizerStep:
+    """One data-parallel optimizer step of draft training (BASELINE configs[4]):
+    the rank runs its micro-batches (micro_batches(): 64/N sequences per rank as chunks of 8),
+    each adding its draft-parameter gradients into `buckets.flat` (gradient accumulation, no
+    communication), then ONE exchange — `buckets.release_all()` after the last micro-batch's
+    backward, `finish()` — and, for ZeRO-2 buckets, the post-update parameter all-gather.
+    `micro_step(m, lo, hi)` runs micro-batch m over sequences [lo, hi)."""
+
+    def __init__(self, buckets: "GradBuckets", global_batch: int, micro: int, world: int, rank: int,
+                 params_flat: torch.Tensor = None):
+        self.buckets = buckets
+        self.micro = micro_batches(global_batch, micro, world, rank)
+        self.params_flat = params_flat
+        self.exchanges = 0
+
+    def run(self, micro_step) -> None:
+        for m, (lo, hi) in enumerate(self.micro):
+            micro_step(m, lo, hi)
+        self.buckets.release_all()
+        self.buckets.finish()
+        if self.params_flat is not None and isinstance(self.buckets, Zero2Buckets):
+            self.buckets.gather_params(self.params_flat)
+        self.exchanges += 1
 
 
 def max_over_ranks(x: float, device="cpu", group=None) -> float:

@@ -9,7 +9,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2603_18567_b200.dp import GradBuckets, max_over_ranks, shard_sequences
+from paper_2603_18567_b200.dp import (GradBuckets, OptimizerStep, Zero2Buckets, max_over_ranks, micro_batches,
+                                      shard_sequences)
 
 
 def test_shard_sequences_partition():
@@ -158,3 +159,80 @@ def test_zero2_reduce_scatter_and_param_all_gather_world2():
     for rank, ok_rs, ok_ag in res:
         assert ok_rs, f"rank {rank}: reduce-scatter shard wrong"
         assert ok_ag, f"rank {rank}: param all-gather wrong"
+
+
+def test_micro_batches_cover_global_batch():
+    """BASELINE configs[4]: global batch 64, micro-batches of 8 -> 64/N sequences per rank."""
+    for world in (1, 2, 4, 8):
+        allseq = []
+        for r in range(world):
+            mb = micro_batches(64, 8, world, r)
+            assert len(mb) == 8 // world
+            assert all(hi - lo == 8 for lo, hi in mb)
+            allseq += [s for lo, hi in mb for s in range(lo, hi)]
+        assert allseq == list(range(64))
+    assert micro_batches(10, 4, 1, 0) == [(0, 4), (4, 8), (8, 10)]
+
+
+def _opt_worker(rank, world, port, q, zero2):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, nb = 1000, 7
+        Buckets = Zero2Buckets if zero2 else GradBuckets
+        gb = Buckets(n, nb, dtype=torch.float64)
+        calls = {"all_reduce": 0, "reduce_scatter": 0}
+        orig_ar, orig_rs = dist.all_reduce, dist.reduce_scatter_tensor
+
+        def ar(*a, **k):
+            calls["all_reduce"] += 1
+            return orig_ar(*a, **k)
+
+        def rs(*a, **k):
+            calls["reduce_scatter"] += 1
+            return orig_rs(*a, **k)
+        dist.all_reduce, dist.reduce_scatter_tensor = ar, rs
+        seen = []
+        e = torch.arange(gb.flat.numel(), dtype=torch.float64)
+
+        def micro_step(m, lo, hi):
+            # gradient accumulation: sequence s contributes (s + 1) * e to every parameter gradient
+            assert sum(calls.values()) == 0, "no exchange before the last micro-batch's backward"
+            seen.extend(range(lo, hi))
+            gb.flat.add_(e * sum(s + 1 for s in range(lo, hi)))
+        step = OptimizerStep(gb, 64, 8, world, rank)
+        step.run(micro_step)
+        dist.all_reduce, dist.reduce_scatter_tensor = orig_ar, orig_rs
+        want = e * sum(s + 1 for s in range(64)) / world  # the mean over ranks of the summed gradients
+        if zero2:
+            per = gb.flat.numel() // nb // world
+            ok = all(torch.allclose(gb.shards[i], want[i * per * world + rank * per:i * per * world + (rank + 1) * per])
+                     for i in range(nb))
+        else:
+            ok = torch.allclose(gb.flat, want)
+        q.put((rank, ok, step.exchanges, dict(calls), seen))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("zero2", [False, True])
+def test_optimizer_step_one_exchange_after_micro_batches_world2(zero2):
+    """One optimizer step at N = 2: 4 micro-batches of 8 sequences per rank, gradients accumulated
+    locally, then exactly one exchange (n_buckets collectives) after the last micro-batch."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_opt_worker, args=(r, world, port, q, zero2)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    seen_all = []
+    for rank, ok, nex, calls, seen in res:
+        assert ok, f"rank {rank}: averaged gradients wrong"
+        assert nex == 1
+        assert calls["reduce_scatter" if zero2 else "all_reduce"] == 7
+        seen_all += seen
+    assert sorted(seen_all) == list(range(64))

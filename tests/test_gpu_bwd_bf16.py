@@ -46,6 +46,7 @@ def test_bwd_bf16_small(cuda_ok, name, shape, lens):
     acc = dc.alloc_grads(S - 1)
     parts = {"dk_base": [], "dv_base": [], "dk_steps": [[] for _ in range(S - 1)],
              "dv_steps": [[] for _ in range(S - 1)]}
+    total = dc.alloc_grads(S - 1)  # fp32 sum of the per-call (overwrite-mode) outputs
     for j in reversed(range(S)):
         out, lse = dc.fwd(j)
         g = dc.alloc_grads(S - 1)
@@ -53,6 +54,11 @@ def test_bwd_bf16_small(cuda_ok, name, shape, lens):
             t.fill_(77.0)  # overwrite mode must not read these
         dq = dc.bwd(j, out, lse, g, accumulate=False)
         dc.bwd(j, out, lse, acc, accumulate=True)
+        total["dk_base"] += g["dk_base"]
+        total["dv_base"] += g["dv_base"]
+        for i in range(j):
+            total["dk_steps"][i] += g["dk_steps"][i]
+            total["dv_steps"][i] += g["dv_steps"][i]
         torch.cuda.synchronize()
         og = oracle.bwd(*oracle_inputs(case, j), np32(case.dout[j]), seq_lens=case.seq_lens)
         _check_grads(name, dq, g, og, j)
@@ -61,6 +67,13 @@ def test_bwd_bf16_small(cuda_ok, name, shape, lens):
         for i in range(j):
             parts["dk_steps"][i].append(og["dk_steps"][i])
             parts["dv_steps"][i].append(og["dv_steps"][i])
+    # accumulate mode == the fp32 sum of the per-call outputs (each held to the plain bound above), so
+    # reading R16's summed bound is exactly the triangle inequality over checked calls
+    for key in ("dk_base", "dv_base"):
+        torch.testing.assert_close(acc[key], total[key], rtol=1e-5, atol=1e-5)
+    for i in range(S - 1):
+        torch.testing.assert_close(acc["dk_steps"][i], total["dk_steps"][i], rtol=1e-5, atol=1e-5)
+        torch.testing.assert_close(acc["dv_steps"][i], total["dv_steps"][i], rtol=1e-5, atol=1e-5)
     assert_close_sum(f"{name} acc dk_base", np32(acc["dk_base"]), parts["dk_base"], **TOL_BF16)
     assert_close_sum(f"{name} acc dv_base", np32(acc["dv_base"]), parts["dv_base"], **TOL_BF16)
     for i in range(S - 1):
