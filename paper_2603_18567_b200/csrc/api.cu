@@ -19,6 +19,7 @@ cudaError_t launch_fwd_check(const Params& p, cudaStream_t st);
 cudaError_t launch_bwd_check(const Params& p, cudaStream_t st);
 cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, const DiagMaps& dmaps, cudaStream_t st);
 int fwd_diag_rows_per_group(const Params& p);
+bool fwd_uses_diag_kernel();
 cudaError_t launch_bwd_sm100(const Params& p, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st);
 int bwd_pre_rows_per_group(const Params& p);
 cudaError_t launch_tree_sm100(const Params& p, const FwdMaps& maps, const int32_t* parents, cudaStream_t st);
@@ -335,8 +336,12 @@ int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
       !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D) || !encode_bshd(&maps.out, out, p.B, p.L, p.Hq, p.D) ||
       (p.out_lo && !encode_bshd(&maps.out_lo, p.out_lo, p.B, p.L, p.Hq, p.D)))
     return TTT_ERR_CUDA;
+  for (int i = 0; i < p.step; ++i)  // the forward's in-kernel diagonal ring: 16-row boxes of K_i / V_i
+    if (!encode_bshd(&maps.kd[i], p.ks[i], p.B, p.L, p.Hkv, p.D, 16) ||
+        !encode_bshd(&maps.vd[i], p.vs[i], p.B, p.L, p.Hkv, p.D, 16))
+      return TTT_ERR_CUDA;
   DiagMaps dmaps;
-  if (p.step > 0) {
+  if (p.step > 0 && fwd_uses_diag_kernel()) {
     const int nr = fwd_diag_rows_per_group(p);
     const long long rows = (long long)p.B * p.L * p.Hq;
     if (nr <= 0) return TTT_ERR_UNSUPPORTED;

@@ -118,10 +118,10 @@ struct PreLayout {
 // dq_acc pointers from `up`), in sweeps over M groups: for M groups, every step, so a group's
 // dK_i / dV_i rows (first written at j = S-1, then reduce-added by j < S-1) and its K_i / V_i rows
 // (re-read by every j >= i) stay in L2 between visits — HBM sees one write of dK_i / dV_i and one
-// read of K_i / V_i per unroll instead of one per call. Ordering of a row's store (item n0) before
-// its reduce-adds (item n0 + Msg, possibly another warp): every compute warp fences its global
-// writes before releasing a stage, and the producer loads item n only after stage n - Msg has been
-// released (the ring's own wait covers it when Msg >= NS), so the adds happen after the store.
+// read of K_i / V_i per unroll instead of one per call. Ordering of a row's store before its
+// reduce-adds: the item -> warp mapping depends on the group only and an element's (lane, register)
+// slot depends on (i, row, column) only, so both come from the same thread in program order
+// (a per-stage __threadfence here measured 20% of the pass's stall samples, r02a ncu).
 template <int D, bool U>
 __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
     ttt_bwd_pre_kernel(const __grid_constant__ Params p, const __grid_constant__ PreMaps maps,
@@ -236,8 +236,12 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
         const int st = n % NS;
         const int w0 = grp * NR, nv = min(NR, nrows - w0);
         const int nitems = (nv + R - 1) / R;
-        // items of this group owned by this warp: global item id n*ipg + k, round-robin over warps
-        const int k_first = (cw - (n * ipg) % kPreCompute + kPreCompute) % kPreCompute;
+        // items of this group owned by this warp: item id gidx*ipg + k, round-robin over warps. The
+        // mapping depends on the group's position only (not on j), so in the unroll pass the SAME
+        // thread writes a given dK_i / dV_i element at every step: its j = S-1 store and the later
+        // steps' reduce-adds are ordered by program order (no fence, no cross-warp hand-off)
+        const int gidx = g0 + gi;
+        const int k_first = (cw - (gidx * ipg) % kPreCompute + kPreCompute) % kPreCompute;
         // the first item's lse rows are a global load: issue it before waiting for the stage's TMA
         // data so its latency overlaps that wait (it sat on the item's critical path)
         float lse_pf[2] = {0.f, 0.f};
@@ -470,7 +474,6 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
             __syncwarp();  // scratch reused by the next item / head tile
           }
         }
-        if (U) __threadfence();  // this warp's global writes before the stage release (see above)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
       }

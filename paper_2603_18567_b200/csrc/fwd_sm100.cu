@@ -10,11 +10,19 @@
 //
 // CTA work item: one 128-row q tile of TWO query heads of the same GQA group
 // (same K/V stream, identical causal length), so every K/V tile TMA'd into
-// shared memory feeds two S = Q K^T MMAs. Warp roles (320 threads):
-//   warps 0-3  softmax + epilogue, head slot 0 (TMEM lanes 0-127)
-//   warps 4-7  softmax + epilogue, head slot 1
-//   warp  8    TMA producer (Q once, then K/V tiles through a 2-stage ring)
-//   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
+// shared memory feeds two S = Q K^T MMAs. Warp roles (512 threads):
+//   warps 0-3   softmax + epilogue, head slot 0 (TMEM lanes 0-127)
+//   warps 4-7   softmax + epilogue, head slot 1
+//   warp  8     TMA producer (Q once, then K/V tiles through a 2-stage ring)
+//   warp  9     TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 10-13 diagonal fold, concurrent with the main loop:
+//               for the tile's rows r < T_b and both heads, t_i = c log2e q_r . K_i[r]
+//               (i = 1..j), A_d = log2 sum_i 2^t_i, O_d = sum_i 2^(t_i - A_d) V_i[r]
+//               (Alg. 1 "concat s_i ... o_t += alpha_i v_i") on CUDA
+//               cores, 8 lanes per row; K_i / V_i rows arrive through their own 4-stage
+//               TMA ring of 16-row blocks; O_d leaves as bf16 through L2 (the out rows, read
+//               back by TMA into the freed Q tile), A_d through shared memory
+//   warp  14    TMA producer of the diagonal ring; warp 15 idle
 // TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512);
 // P (bf16, packed 2/column) is written over S and consumed by the PV MMA
 // straight from TMEM (A operand in TMEM, "ts" form).
@@ -48,7 +56,14 @@ extern "C" int ttt_debug_ftrace_read(void* host, unsigned int cta) {
 #endif
 namespace {
 
-constexpr int kFwdThreads = 320;
+constexpr int kFwdThreads = 512;
+#ifndef TTT_FWD_FUSED_DIAG
+#define TTT_FWD_FUSED_DIAG 1  // 0: dev A/B build with round 1's separate ttt_fwd_diag_kernel
+#endif
+constexpr int kDgRows = 16;    // rows per diagonal-ring stage (one TMA box per 64 columns per tensor)
+constexpr int kDgStages = 4;   // diagonal-ring depth
+// Q (2 tiles) | K (2 stages) | V (2 stages) | diagonal ring | 1 KB alignment slack
+constexpr int fwd_smem_bytes(int D) { return 6 * kTile * D * 2 + kDgStages * 2 * (D / 64) * kDgRows * 128 + 1024; }
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only when the max grows by > 2^8
 
 struct FwdBars {
@@ -56,7 +71,10 @@ struct FwdBars {
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
   uint64_t s_full[2], p_lo[2], p_hi[2], o_full[2];  // P published in two 64-column halves
   uint64_t s_done, od;  // all S MMAs complete (Q / K smem free); diagonal partial tile landed
+  uint64_t dg_full[kDgStages], dg_empty[kDgStages];  // diagonal K_i / V_i ring
+  uint64_t diag_done;                                // diagonal partial (O_d rows, A_d) complete
   uint32_t tmem_base;
+  float a_d[2][kTile];  // A_d = log2 sum_i 2^t_i per (head slot, row), from the diagonal warps
 };
 
 // TREE = true: tree-attention verification (ttt_tree_attn_fwd) on the
@@ -74,6 +92,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint8_t* sQ = smem;           // 2 tiles (head slots)
   uint8_t* sK = smem + 2 * TB;  // 2 stages
   uint8_t* sV = smem + 4 * TB;  // 2 stages
+  constexpr int DGB = kDgRows * 128;       // one 16-row x 64-column SW128 box
+  constexpr int DGS = 2 * NBOX * DGB;      // one stage: K_i and V_i rows of a 16-row block
+  uint8_t* sDg = smem + 6 * TB;            // diagonal ring, kDgStages stages
   __shared__ FwdBars bars;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -138,6 +159,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     mbar_init(&bars.s_done, 1);
     mbar_init(&bars.od, 1);
+    for (int i = 0; i < kDgStages; ++i) {
+      mbar_init(&bars.dg_full[i], 1);
+      mbar_init(&bars.dg_empty[i], 4);  // the four diagonal compute warps
+    }
+    mbar_init(&bars.diag_done, 4);
     fence_mbar_init();
   }
   if (warp == 9) {
@@ -182,8 +208,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int bx = 0; bx < NBOX; ++bx)
           tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, (kvt0 + n) * kTile, b);
       }
-      if (p.step > 0) {  // diagonal partial of the two heads into the Q tiles once no S MMA reads them
+      if (!TREE && p.step > 0) {  // diagonal partial of the two heads into the Q tiles once no S MMA
+                                  // reads them and the diagonal warps have written it
         mbar_wait(&bars.s_done, 0);
+        if (TTT_FWD_FUSED_DIAG) mbar_wait(&bars.diag_done, 0);
         mbar_expect_tx(&bars.od, (has1 ? 2 : 1) * TB);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx) {
@@ -207,19 +235,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           umma_ss_e(tbase + slot * 128, sdesc_add(dQ0, slot * TB + off), sdesc_add(dK0, kst * TB + off), idS, ks > 0);
         }
       };
-      // O += P V in two halves of the key dimension: keys [0,64) as soon as the softmax warps have
-      // published P's first half (p_lo), keys [64,128) after p_hi
+      // O += P V in two halves of the key dimension: keys [64,128) as soon as the softmax warps
+      // have published them (p_hi; P at TMEM columns [96,128) of the slot's S buffer), then keys
+      // [0,64) after p_lo (columns [0,32))
       auto issue_PV = [&](int slot, int vst, bool acc, int n) {
-        mbar_wait(&bars.p_lo[slot], n & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          umma_ts_e(tbase + 256 + slot * 128, tbase + slot * 128 + ks * 8, sdesc_add(dV0, vst * TB + ks * 2048), idO,
-                    (acc || ks > 0) ? 1u : 0u);
         mbar_wait(&bars.p_hi[slot], n & 1);
         tc_fence_after();
 #pragma unroll
         for (int ks = 4; ks < 8; ++ks)
+          umma_ts_e(tbase + 256 + slot * 128, tbase + slot * 128 + 96 + (ks - 4) * 8,
+                    sdesc_add(dV0, vst * TB + ks * 2048), idO, (acc || ks > 4) ? 1u : 0u);
+        mbar_wait(&bars.p_lo[slot], n & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
           umma_ts_e(tbase + 256 + slot * 128, tbase + slot * 128 + ks * 8, sdesc_add(dV0, vst * TB + ks * 2048), idO, 1u);
       };
       mbar_wait(&bars.q, 0);
@@ -267,6 +296,137 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
     }
+  } else if (warp >= 10) {
+    // ================= diagonal fold (warps 10-13) + its TMA producer (warp 14) =================
+
+    if (TTT_FWD_FUSED_DIAG && !TREE && p.step > 0) {
+      const int j = p.step;
+      // 16-row blocks of this q tile holding at least one row r < T_b
+      const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
+      if (warp == 14) {
+        if (lane == 0) {
+          int n = 0;
+          for (int rb = 0; rb < nrb; ++rb)
+            for (int i = 0; i < j; ++i, ++n) {
+              const int st = n % kDgStages, use = n / kDgStages;
+              mbar_wait(&bars.dg_empty[st], (use & 1) ^ 1);
+              mbar_expect_tx(&bars.dg_full[st], DGS);
+              uint8_t* base = sDg + st * DGS;
+              const int r0 = qt * kTile + rb * kDgRows;
+#pragma unroll
+              for (int bx = 0; bx < NBOX; ++bx) {
+                tma_load_4d(base + bx * DGB, &maps.kd[i], &bars.dg_full[st], bx * 64, g, r0, b);
+                tma_load_4d(base + (NBOX + bx) * DGB, &maps.vd[i], &bars.dg_full[st], bx * 64, g, r0, b);
+              }
+            }
+        }
+      } else if (warp < 14) {
+        // thread layout: 8 lanes per row (lane k = lane & 7 owns columns 8k..8k+7 of every 64-column
+        // box), 4 rows per warp, 16 rows per stage; both head slots per row
+        constexpr int E = 8 * NBOX;  // elements per lane
+        const int dw = warp - 10, k8 = lane & 7;
+        const int srow = dw * 4 + (lane >> 3);  // row within a 16-row block
+        const float sl2 = p.scale_log2;
+        mbar_wait(&bars.q, 0);  // q rows are read from the Q tiles (shared with the S MMAs, read-only)
+        int n = 0;
+        for (int rb = 0; rb < nrb; ++rb) {
+          const int row = rb * kDgRows + srow;
+          const int r = qt * kTile + row;
+          float qf[2][E], acc[2][E], m[2], l[2];
+#pragma unroll
+          for (int hs = 0; hs < 2; ++hs) {
+            m[hs] = -INFINITY;
+            l[hs] = 0.f;
+#pragma unroll
+            for (int bx = 0; bx < NBOX; ++bx) {
+              const uint4 u = lds128(smem_u32(sQ + hs * TB + bx * 16384) + sw128_off(row, k8));
+              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+                qf[hs][bx * 8 + 2 * e] = f.x * sl2;
+                qf[hs][bx * 8 + 2 * e + 1] = f.y * sl2;
+                acc[hs][bx * 8 + 2 * e] = 0.f;
+                acc[hs][bx * 8 + 2 * e + 1] = 0.f;
+              }
+            }
+          }
+          for (int i = 0; i < j; ++i, ++n) {
+            const int st = n % kDgStages, use = n / kDgStages;
+            mbar_wait(&bars.dg_full[st], use & 1);
+            const uint32_t base = smem_u32(sDg + st * DGS);
+            float kf[E], vf[E];
+#pragma unroll
+            for (int bx = 0; bx < NBOX; ++bx) {
+              const uint4 uk = lds128(base + bx * DGB + sw128_off(srow, k8));
+              const uint4 uv = lds128(base + (NBOX + bx) * DGB + sw128_off(srow, k8));
+              const uint32_t wk[4] = {uk.x, uk.y, uk.z, uk.w}, wv[4] = {uv.x, uv.y, uv.z, uv.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 fk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wk[e]));
+                const float2 fv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+                kf[bx * 8 + 2 * e] = fk.x;
+                kf[bx * 8 + 2 * e + 1] = fk.y;
+                vf[bx * 8 + 2 * e] = fv.x;
+                vf[bx * 8 + 2 * e + 1] = fv.y;
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars.dg_empty[st]);  // values are in registers
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs) {
+              // t_i = c log2e q . K_i[r]: 8-lane partial dots, xor-shuffle sum inside the row's lanes
+              uint64_t d2 = 0;
+#pragma unroll
+              for (int e = 0; e < E; e += 2)
+                d2 = ffma2(f2pack(qf[hs][e], qf[hs][e + 1]), f2pack(kf[e], kf[e + 1]), d2);
+              float t0, t1;
+              f2unpack(d2, t0, t1);
+              float t = t0 + t1;
+              t += __shfl_xor_sync(0xffffffffu, t, 1);
+              t += __shfl_xor_sync(0xffffffffu, t, 2);
+              t += __shfl_xor_sync(0xffffffffu, t, 4);
+              // online softmax over the j diagonal keys (log2 domain)
+              const float m_new = fmaxf(m[hs], t);
+              const float alpha = ex2(m[hs] - m_new), pw = ex2(t - m_new);
+              l[hs] = fmaf(l[hs], alpha, pw);
+              m[hs] = m_new;
+              const uint64_t a2 = f2pack(alpha, alpha), p2 = f2pack(pw, pw);
+#pragma unroll
+              for (int e = 0; e < E; e += 2) {
+                const uint64_t o = ffma2(f2pack(acc[hs][e], acc[hs][e + 1]), a2,
+                                         fmul2(f2pack(vf[e], vf[e + 1]), p2));
+                f2unpack(o, acc[hs][e], acc[hs][e + 1]);
+              }
+            }
+          }
+          // O_d (normalised, bf16) -> the out rows (staging; read back by TMA), A_d -> shared memory
+          if (r < T) {
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs) {
+              if (hs == 0 || has1) {
+                const float inv = 1.f / l[hs];
+                __nv_bfloat16* orow =
+                    reinterpret_cast<__nv_bfloat16*>(p.out) + (((size_t)b * p.L + r) * p.Hq + h0 + hs) * D;
+#pragma unroll
+                for (int bx = 0; bx < NBOX; ++bx) {
+                  uint4 w;
+                  w.x = pack_bf16(acc[hs][bx * 8 + 0] * inv, acc[hs][bx * 8 + 1] * inv);
+                  w.y = pack_bf16(acc[hs][bx * 8 + 2] * inv, acc[hs][bx * 8 + 3] * inv);
+                  w.z = pack_bf16(acc[hs][bx * 8 + 4] * inv, acc[hs][bx * 8 + 5] * inv);
+                  w.w = pack_bf16(acc[hs][bx * 8 + 6] * inv, acc[hs][bx * 8 + 7] * inv);
+                  *reinterpret_cast<uint4*>(orow + bx * 64 + k8 * 8) = w;
+                }
+                if (k8 == 0) bars.a_d[hs][row] = m[hs] + log2f(l[hs]);
+              }
+            }
+          }
+        }
+        fence_async_global();  // the out rows are read back by the producer's TMA (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.diag_done);
+      }
+    }
   } else {
     // ================= softmax + epilogue (warps 0-7) =================
     const int slot = warp >> 2;
@@ -291,53 +451,61 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 1, n);
         if (threadIdx.x == 128) TTT_TRACE_EV(2, 1, n);
         tc_fence_after();
-        uint32_t raw[128];
-        tmem_ld128(tS, raw);
+        // S is read in two 64-column halves (64 registers each, so 16 warps fit the register file):
+        // keys [0,64) for their max only, keys [64,128) kept for P; P(keys 64..127) is written over
+        // the already-read S columns [96,128) and published first (p_hi), then keys [0,64) are
+        // re-read and P(keys 0..63) written over columns [0,32) (p_lo).
+        uint32_t raw[64];
         const int kv0 = (kvt0 + n) * kTile;
         const bool partial = TREE ? (kv0 + kTile > T) : ((n == qt) || (kv0 + kTile > T));
+        // TTT: allowed columns c < lim (k <= r and k < T); TREE: per 32-column word bit masks
+        const int lim = min(r + 1, T) - kv0;
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        if constexpr (TREE) {
+          // column c = key kv0 + c: prefix key (< P) or tree key u = kv0 + c - P of this row's
+          // ancestor-or-self mask; rows past the tree (padding of the tile) keep key 0 only
+          const unsigned long long am = tree_am;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int c0 = q4 * 32, lo = T - kv0 - c0;  // columns c0 + i < lo are prefix keys
+            uint32_t pre = lo >= 32 ? 0xffffffffu : (lo <= 0 ? 0u : ((1u << lo) - 1u));
+            // tree bits: column c0 + i holds u = c0 + i - (T - kv0) = i - lo
+            uint32_t tb = 0u;
+            if (lo < 32 && lo > -64) {
+              const int sh = lo;  // bit i of tb = bit (i - sh) of am
+              tb = sh >= 0 ? (uint32_t)(am << sh) : (uint32_t)(am >> (-sh));
+            }
+            w[q4] = pre | tb;
+          }
+          if (!tree_row) w[0] = w[1] = w[2] = w[3] = 0u, w[0] = (kv0 == 0) ? 1u : 0u;
+        }
+        // masked columns of half hf (columns 64 hf + c) -> -inf
+        auto mask_half = [&](int hf) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            const int cc = 64 * hf + c;
+            const bool ok = TREE ? (((w[cc >> 5] >> (cc & 31)) & 1u) != 0u) : (cc < lim);
+            raw[c] = ok ? raw[c] : __float_as_uint(-INFINITY);
+          }
+        };
         // row max of the raw scores (scale > 0 commutes with max): 8 independent chains of
         // 3-input max (FMNMX3), two new columns per instruction
         float mx8[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
-        if (partial) {
-          if constexpr (TREE) {
-            // column c = key kv0 + c: prefix key (< P) or tree key u = kv0 + c - P of this row's
-            // ancestor-or-self mask; rows past the tree (padding of the tile) keep key 0 only
-            uint32_t w[4];
-            const unsigned long long am = tree_am;
+        auto max_half = [&]() {
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              const int c0 = q4 * 32, lo = T - kv0 - c0;  // columns c0 + i < lo are prefix keys
-              uint32_t pre = lo >= 32 ? 0xffffffffu : (lo <= 0 ? 0u : ((1u << lo) - 1u));
-              // tree bits: column c0 + i holds u = c0 + i - (T - kv0) = i - lo
-              uint32_t tb = 0u;
-              if (lo < 32 && lo > -64) {
-                const int sh = lo;  // bit i of tb = bit (i - sh) of am
-                tb = sh >= 0 ? (uint32_t)(am << sh) : (uint32_t)(am >> (-sh));
-              }
-              w[q4] = pre | tb;
-            }
-            if (!tree_row) w[0] = w[1] = w[2] = w[3] = 0u, w[0] = (kv0 == 0) ? 1u : 0u;
+          for (int c = 0; c < 64; c += 16)
 #pragma unroll
-            for (int c = 0; c < 128; ++c) {
-              const float x = ((w[c >> 5] >> (c & 31)) & 1u) ? __uint_as_float(raw[c]) : -INFINITY;
-              raw[c] = __float_as_uint(x);
-            }
-          } else {
-            const int lim = min(r + 1, T) - kv0;  // allowed columns c < lim  (k <= r and k < T)
-#pragma unroll
-            for (int c = 0; c < 128; ++c) {
-              const float x = c < lim ? __uint_as_float(raw[c]) : -INFINITY;
-              raw[c] = __float_as_uint(x);
-            }
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < 128; c += 16)
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            mx8[u] = fmax3(mx8[u], __uint_as_float(raw[c + u]), __uint_as_float(raw[c + 8 + u]));
+            for (int u = 0; u < 8; ++u)
+              mx8[u] = fmax3(mx8[u], __uint_as_float(raw[c + u]), __uint_as_float(raw[c + 8 + u]));
+        };
+        tmem_ld64w(tS, raw);
+        if (partial) mask_half(0);
+        max_half();
+        tmem_ld64w(tS + 64, raw);
+        if (partial) mask_half(1);
+        max_half();
         const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
         const float m_new = fmaxf(m_run, mx);
@@ -366,43 +534,46 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           m_run = m_new;
         }
         // P = 2^(s c log2e - m): one FFMA2 per pair, 4 independent pair-sum chains (FADD2),
-        // written to TMEM and published in two 64-column halves (the PV MMA starts on the first)
+        // written to TMEM and published per 64-key half (the PV MMA starts on the first)
         // TREE: a row may have no allowed key in this context split yet (m = -inf): exponents
         // against 0 give exact zeros instead of NaN
         const float m_use = (TREE && m_run == -INFINITY) ? 0.f : m_run;
         const uint64_t sl2x2 = f2pack(sl2, sl2), negm = f2pack(-m_use, -m_use);
         uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hh = 0; hh < 2; ++hh) {
+          const int hf = 1 - hh;  // keys [64,128) (in registers) first, then [0,64)
+          if (hf == 0) {
+            tmem_ld64w(tS, raw);
+            if (partial) mask_half(0);
+          }
           uint32_t pk[32];
           if (partial) {  // masked columns are -inf: hardware ex2 gives exact zeros
 #pragma unroll
             for (int cc = 0; cc < 32; ++cc) {
-              const int c = hf * 32 + cc;
               float x0, x1;
-              f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
+              f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * cc]), __uint_as_float(raw[2 * cc + 1])), sl2x2, negm), x0, x1);
               const float e0 = ex2(x0), e1 = ex2(x1);
-              rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
+              rs2[cc & 3] = fadd2(rs2[cc & 3], f2pack(e0, e1));
               pk[cc] = pack_bf16(e0, e1);
             }
           } else {  // full tile: the pairs TTT_FWD_EMU_MASK selects (of every 8) on the FMA pipe
                     // (MUFU ex2 is the co-bottleneck)
 #pragma unroll
             for (int cc = 0; cc < 32; ++cc) {
-              const int c = hf * 32 + cc;
               float x0, x1, e0, e1;
-              f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * c]), __uint_as_float(raw[2 * c + 1])), sl2x2, negm), x0, x1);
-              if ((TTT_FWD_EMU_MASK >> (c & 7)) & 1) {
+              f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * cc]), __uint_as_float(raw[2 * cc + 1])), sl2x2, negm), x0, x1);
+              if ((TTT_FWD_EMU_MASK >> (cc & 7)) & 1) {
                 ex2_emu2(x0, x1, e0, e1);
               } else {
                 e0 = ex2(x0);
                 e1 = ex2(x1);
               }
-              rs2[c & 3] = fadd2(rs2[c & 3], f2pack(e0, e1));
+              rs2[cc & 3] = fadd2(rs2[cc & 3], f2pack(e0, e1));
               pk[cc] = pack_bf16(e0, e1);
             }
           }
-          tmem_st32(tS + 32 * hf, pk);
+          tmem_st32(tS + (hf ? 96 : 0), pk);
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(hf == 0 ? &bars.p_lo[slot] : &bars.p_hi[slot]);
@@ -418,18 +589,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 2, n);
         if (threadIdx.x == 128) TTT_TRACE_EV(2, 2, n);
       }
-      // ---- epilogue: merge the diagonal partial (fwd_diag_kernel), normalise, store ----
+      // ---- epilogue: merge the diagonal partial, normalise, store ----
       // The j diagonal keys of row r (Alg. 1 "concat s_i") were reduced
-      // by ttt_fwd_diag_kernel into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum); the
+      // by the diagonal warps into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum); the
       // merge is the same online-softmax update as one more "tile".
       const size_t lse_idx = ((size_t)bst * p.Hq + h) * p.L + r;
       const bool has_diag = !TREE && (r < T) && (p.step > 0);
-      const float A_d = has_diag ? p.lse[lse_idx] : -INFINITY;
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, 0);
       mbar_wait(&bars.o_full[slot], 0);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 4, 0);
       tc_fence_after();
-      if (p.step > 0) mbar_wait(&bars.od, 0);
+      if (!TREE && p.step > 0) {
+        if (TTT_FWD_FUSED_DIAG) mbar_wait(&bars.diag_done, 0);  // A_d in shared memory
+        mbar_wait(&bars.od, 0);                                 // O_d tile in the Q buffer
+      }
+      const float A_d = !has_diag ? -INFINITY : TTT_FWD_FUSED_DIAG ? bars.a_d[slot][row] : p.lse[lse_idx];
       // The diagonal partial O_d sits in this slot's Q tile (SW128 boxes); each thread reads its
       // row there and overwrites it in place with the output, which the TMA store then drains.
       // out_lo is staged in the K stage of the same index. Both are free: o_full[slot] and
@@ -772,13 +946,14 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
     for (int r = 0; r < p.nqt; ++r) len[r] = (double)(p.nqt - r) * 3.3;
     p.order_batch = pick_order_batch(p.B * p.Hkv, p.nqt, (p.G + 1) / 2, len.data(), 7.0, (double)p.L * D * 4);
   }
-  const int smem = 6 * kTile * D * 2 + 1024;
+  const int smem = fwd_smem_bytes(D);
   static std::atomic<unsigned long long> attr_done{0};
   {
     cudaError_t e = set_smem_attr(ttt_fwd_sm100_kernel<D, false>, smem, attr_done);
     if (e != cudaSuccess) return e;
   }
-  if (p.step > 0) {
+#if !TTT_FWD_FUSED_DIAG
+  if (p.step > 0) {  // dev A/B: the separate diagonal pre-pass of round 1
     DiagLayout lay;
     if (!diag_layout(p, D, &lay)) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(ttt_fwd_diag_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -790,6 +965,9 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
     ttt_fwd_diag_kernel<D><<<std::min(groups, 148), 32 * (kDiagCompute + 1), lay.total, st>>>(p, dmaps, lay);
     prof_mark(kKindFwdDiag, false, st);
   }
+#else
+  (void)dmaps;
+#endif
   const int npairs = (p.G + 1) / 2;
   const int grid = p.nqt * p.B * p.Hkv * npairs;
   prof_mark(kKindFwdMain, true, st);
@@ -799,6 +977,8 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
 }
 
 }  // namespace
+
+bool fwd_uses_diag_kernel() { return !TTT_FWD_FUSED_DIAG; }
 
 int fwd_diag_rows_per_group(const Params& p) {
   DiagLayout lay;
@@ -854,7 +1034,7 @@ cudaError_t launch_tree_d(const Params& p_in, const FwdMaps& maps, const int32_t
   Params p = p_in;
   p.nqt = 1;
   p.order_batch = p.B * p.Hkv;
-  const int smem = 6 * kTile * D * 2 + 1024;
+  const int smem = fwd_smem_bytes(D);
   static std::atomic<unsigned long long> attr_done{0};
   {
     cudaError_t e = set_smem_attr(ttt_fwd_sm100_kernel<D, true>, smem, attr_done);

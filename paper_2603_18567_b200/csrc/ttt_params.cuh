@@ -57,6 +57,8 @@ struct Params {
 // Tensor maps for the tcgen05 paths (4-D: D, H, L, B; box 64 x 1 x 128 x 1, SW128)
 struct FwdMaps {
   CUtensorMap q, k, v, out, out_lo;
+  // step lists K_i / V_i (i < step) as 4-D BSHD maps with 16-row boxes: the forward's diagonal ring
+  CUtensorMap kd[TTT_MAX_STEPS], vd[TTT_MAX_STEPS];
 };
 // forward diagonal pre-pass: q and out viewed as [B*L*Hq rows][D], box 64 x (NR*G) rows, SW128;
 // backward pre-pass (bwd_sm100.cu): 2-D [rows][D] bf16 views, SW128, 64-column boxes

@@ -81,7 +81,8 @@ def test_full_size_ragged_row_subset(cuda_ok):
 
 def test_nan_poison_in_skipped_tiles(cuda_ok):
     """NaN in every K_0 / V_0 tile that lies wholly at or beyond T_b (never loaded: the BlockMask
-    skips it) leaves every output bitwise identical; gradients of those keys are exactly 0."""
+    skips it) leaves the forward bitwise identical and the backward NaN-free and equal up to its
+    fp32 reduction order; gradients of those keys are exactly 0."""
     shape = Shape(2, 512, 8, 2, 128, 4)
     case = make_case(shape, dtype=torch.bfloat16, seed=13, lens="ragged")
     case.seq_lens = np.array([130, 300], dtype=np.int32)
@@ -100,13 +101,17 @@ def test_nan_poison_in_skipped_tiles(cuda_ok):
         torch.cuda.synchronize()
         res.append((out, lse, dq, g))
     (o0, l0, q0, g0), (o1, l1, q1, g1) = res
-    assert torch.equal(o0, o1) and torch.equal(l0, l1) and torch.equal(q0, q1)
+    # the forward is deterministic: bitwise equal; the backward's fp32 reductions (dq_acc, and dK / dV
+    # when several CTAs share a kv tile) add in a run-dependent order: equal up to that rounding
+    assert torch.equal(o0, o1) and torch.equal(l0, l1)
+    assert not torch.isnan(q1.float()).any()
+    torch.testing.assert_close(q1, q0, rtol=1e-2, atol=1e-3)
     for key in ("dk_base", "dv_base"):
-        assert torch.equal(g0[key], g1[key]), key
-        assert not torch.isnan(g1[key]).any()
+        assert not torch.isnan(g1[key]).any(), key
+        torch.testing.assert_close(g1[key], g0[key], rtol=1e-5, atol=1e-5)
     for i in range(j):
-        assert torch.equal(g0["dk_steps"][i], g1["dk_steps"][i])
-        assert torch.equal(g0["dv_steps"][i], g1["dv_steps"][i])
+        torch.testing.assert_close(g1["dk_steps"][i], g0["dk_steps"][i], rtol=1e-5, atol=1e-5)
+        torch.testing.assert_close(g1["dv_steps"][i], g0["dv_steps"][i], rtol=1e-5, atol=1e-5)
     for b, T in enumerate(case.seq_lens):
         assert g1["dk_base"][b, int(T):].abs().max().item() == 0.0
         assert g1["dv_base"][b, int(T):].abs().max().item() == 0.0

@@ -25,7 +25,7 @@ CASES = [  # (batch, n, prefix_lens, Hq, Hkv, D)
 ]
 
 
-def _run(c, extra_rows=0):
+def _run(c, extra_rows=0, ws_fill=None):
     B, n = c.q.shape[:2]
     Hq, Hkv, D = c.q.shape[2], c.k.shape[2], c.q.shape[3]
     fp32 = c.q.dtype == torch.float32
@@ -35,6 +35,8 @@ def _run(c, extra_rows=0):
     out = torch.empty(B, n, Hq, D, dtype=c.q.dtype, device="cuda")
     lse = torch.empty(B, Hq, n, dtype=torch.float32, device="cuda")
     ws = torch.empty(ttt.ttt_tree_attn_workspace_size(d), dtype=torch.uint8, device="cuda")
+    if ws_fill is not None:
+        ws.fill_(ws_fill)
     ttt.ttt_tree_attn_fwd(d, dev(c.q), dev(c.k), dev(c.v), dev(c.parents), out, lse, ws)
     torch.cuda.synchronize()
     return out.float().cpu().numpy(), lse.cpu().numpy()
@@ -74,3 +76,17 @@ def test_tree_attention_fp32_check_mode(case):
     o_out, o_lse = OT.tree_attention(c.q.numpy(), c.k.numpy(), c.v.numpy(), P, c.parents.numpy())
     np.testing.assert_allclose(out, o_out, rtol=1e-5, atol=1e-5)
     np.testing.assert_allclose(lse, o_lse, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("case", [CASES[3], CASES[5]], ids=["split4", "one_tile_per_split"])
+def test_tree_workspace_poison(case):
+    """compute-sanitizer initcheck flags ttt_tree_combine_kernel's reads of the per-split partials
+    (written by TMA stores, which initcheck does not track). Proof that every element the combine
+    reads was written by this call: a workspace pre-filled with NaN (0xFF bytes) gives the same,
+    finite result as a zero-filled one."""
+    B, n, P, Hq, Hkv, D = case
+    c = make_tree_case(B, n, P, Hq, Hkv, D, seed=3, kv_len=max(P) + n)
+    a = _run(c, ws_fill=0)
+    b = _run(c, ws_fill=255)
+    assert not np.isnan(b[0]).any() and not np.isnan(b[1]).any()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
