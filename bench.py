@@ -206,7 +206,7 @@ def workload_config(shape: Shape, world: int, cfg: str = "llama8b"):
 class Unroll:
     """Device buffers of one per-GPU unroll + the C-ABI calls of one step."""
 
-    def __init__(self, shape: Shape, seed: int, dev, bwd_unroll: bool = False):
+    def __init__(self, shape: Shape, seed: int, dev, bwd_unroll: bool = True):
         import paper_2603_18567_b200 as ttt
         self.ttt = ttt
         self.s = s = shape
@@ -350,15 +350,17 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
     kern = ttt.ttt_attn_profile_end()
     launches_per_step = sum(n for _, n in kern.values()) // prof_steps
     # per-TTT-step call times (the paper measures the final step), separate pass
-    per_step = {"fwd_ms": [0.0] * S, "bwd_ms": [0.0] * S}
-    if not u.bwd_unroll:
-        reps = 3
-        for _ in range(reps):
-            marks = {}
-            u.step(stream, marks=marks)
-            torch.cuda.synchronize()
-            for (kind, j), (a, b) in marks.items():
-                per_step[f"{kind}_ms"][j] += a.elapsed_time(b) / reps
+    # (the backward split per step through S ttt_attn_bwd calls: the unroll call has no per-step boundary)
+    per_step = {"fwd_ms": [0.0] * S, "bwd_ms": [0.0] * S, "bwd_api": "ttt_attn_bwd per call"}
+    reps = 3
+    unroll_mode, u.bwd_unroll = u.bwd_unroll, False
+    for _ in range(reps):
+        marks = {}
+        u.step(stream, marks=marks)
+        torch.cuda.synchronize()
+        for (kind, j), (a, b) in marks.items():
+            per_step[f"{kind}_ms"][j] += a.elapsed_time(b) / reps
+    u.bwd_unroll = unroll_mode
     # cold L2 (SURVEY.md §8d "report both warm and cold"): one unroll right after a 512 MB write
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     cold = []
@@ -410,6 +412,7 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         "frac_of_bf16_burst_peak": tflops / peaks["bf16_tflops"],
         "frac_of_bf16_sustained_peak": tflops / peaks["bf16_tflops_sustained"],
         "flops_convention": "algorithmic 12*D per allowed (q,k) pair (fwd 4D + bwd 8D; recompute excluded)",
+        "bwd_api": "ttt_attn_bwd_unroll (one call per unroll)" if u.bwd_unroll else "ttt_attn_bwd x S",
         "roofline": roof,
         "kernels_ms_per_step": {k: v[0] / prof_steps for k, v in kern.items()},
         "per_ttt_step_ms": per_step,
@@ -806,11 +809,12 @@ def main():
     ap.add_argument("--zero2", action="store_true",
                     help="ZeRO-2 draft gradient exchange (reduce-scatter per backward call + parameter all-gather "
                          "after the step, PAPER.md:281) instead of the bucketed all-reduce")
-    ap.add_argument("--bwd-unroll", action="store_true",
-                    help="one ttt_attn_bwd_unroll call per unroll instead of S ttt_attn_bwd calls (same work; "
-                         "37%% less pre-pass HBM traffic, same time: the pre-pass is latency-bound; the DP "
-                         "buckets are then released after the whole backward)")
+    ap.add_argument("--bwd-percall", action="store_true",
+                    help="S ttt_attn_bwd calls per unroll instead of one ttt_attn_bwd_unroll call (the default: "
+                         "one diagonal pass for all steps, dK_i / dV_i written once, each step's dq conversion "
+                         "inside the next step's tensor-core pass)")
     args = ap.parse_args()
+    args.bwd_unroll = not args.bwd_percall
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3
     world = int(os.environ.get("WORLD_SIZE", "1"))

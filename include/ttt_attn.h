@@ -123,7 +123,9 @@ int ttt_attn_fwd(const ttt_attn_desc* desc, int step,
  *   dk_base, dv_base          fp32 [B][L][Hkv][D]  dL/dK_0, dL/dV_0
  *   dk_steps, dv_steps        HOST arrays of `step` device ptrs, fp32 [B][L][Hkv][D]
  *   flags     TTT_ACCUMULATE_DKV or 0
- *   workspace >= ttt_attn_workspace_size(desc, step, 1) bytes of device memory. */
+ *   workspace >= ttt_attn_workspace_size(desc, step, 1) bytes of device memory (BF16: Delta, lse2 and
+ *             the fp32 dq accumulator; FP32_CHECK: fp64 dK / dV accumulators, (2 + 2 step) x
+ *             B L Hkv D x 8 bytes, so the check path's sums over all rows stay within 1e-5). */
 int ttt_attn_bwd(const ttt_attn_desc* desc, int step,
                  const void* q, const void* k_base, const void* v_base,
                  const void* const* k_steps, const void* const* v_steps,

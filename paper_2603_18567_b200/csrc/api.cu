@@ -17,6 +17,7 @@ namespace tttk {
 cudaError_t launch_zero_f32(float* x, size_t n, cudaStream_t st);
 cudaError_t launch_fwd_check(const Params& p, cudaStream_t st);
 cudaError_t launch_bwd_check(const Params& p, cudaStream_t st);
+size_t check_bwd_ws_bytes(const Params& p);
 cudaError_t launch_fwd_sm100(const Params& p, const FwdMaps& maps, const DiagMaps& dmaps, cudaStream_t st);
 int fwd_diag_rows_per_group(const Params& p);
 bool fwd_uses_diag_kernel();
@@ -297,7 +298,12 @@ const char* ttt_attn_version(void) { return "libtttattn 0.1 sm_100a (tcgen05/TME
 
 size_t ttt_attn_workspace_size(const ttt_attn_desc* d, int step, int is_bwd) {
   if (validate_desc(d, step) != TTT_OK) return 0;
-  if (!is_bwd || d->dtype == TTT_FP32_CHECK) return 0;
+  if (!is_bwd) return 0;
+  if (d->dtype == TTT_FP32_CHECK) {  // fp64 dK / dV accumulators of the check path
+    Params p;
+    fill_common(p, d, step);
+    return check_bwd_ws_bytes(p);
+  }
   return bwd_ws_layout(d).total;
 }
 
@@ -394,16 +400,11 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t kv_elems = (size_t)p.B * p.L * p.Hkv * p.D;
+  (void)kv_elems;
   if (d->dtype == TTT_FP32_CHECK) {
-    if (!p.accumulate) {
-      cudaError_t e = launch_zero_f32(p.dk, kv_elems, s);
-      if (e == cudaSuccess) e = launch_zero_f32(p.dv, kv_elems, s);
-      for (int i = 0; i < step && e == cudaSuccess; ++i) {
-        e = launch_zero_f32(p.dks[i], kv_elems, s);
-        if (e == cudaSuccess) e = launch_zero_f32(p.dvs[i], kv_elems, s);
-      }
-      if (e != cudaSuccess) return TTT_ERR_CUDA;
-    }
+    if (!workspace || workspace_bytes < check_bwd_ws_bytes(p)) return TTT_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return TTT_ERR_ALIGNMENT;
+    p.dacc = static_cast<double*>(workspace);
     return cuda_status(launch_bwd_check(p, s));
   }
   const BwdWs w = bwd_ws_layout(d);
@@ -551,7 +552,7 @@ int ttt_tree_attn_fwd(const ttt_tree_desc* d, const void* q, const void* k_cache
 
 size_t ttt_attn_bwd_unroll_workspace_size(const ttt_attn_desc* d, int num_steps) {
   if (num_steps < 1 || num_steps > TTT_MAX_UNROLL || validate_desc(d, num_steps - 1) != TTT_OK) return 0;
-  if (d->dtype == TTT_FP32_CHECK) return 0;
+  if (d->dtype == TTT_FP32_CHECK) return ttt_attn_workspace_size(d, num_steps - 1, 1);  // calls run in order
   return (size_t)num_steps * bwd_ws_layout(d).total;
 }
 
@@ -571,7 +572,8 @@ int ttt_attn_bwd_unroll(const ttt_attn_desc* d, int num_steps, const void* const
     for (int j = S - 1; j >= 0; --j) {
       const int rc = ttt_attn_bwd(d, j, q[j], k_base, v_base, k_steps, v_steps, out[j], nullptr, lse[j], dout[j],
                                   dq[j], dk_base, dv_base, dk_steps, dv_steps,
-                                  j == S - 1 ? flags : (flags | TTT_ACCUMULATE_DKV), nullptr, 0, stream);
+                                  j == S - 1 ? flags : (flags | TTT_ACCUMULATE_DKV), workspace, workspace_bytes,
+                                  stream);
       if (rc) return rc;
     }
     return TTT_OK;

@@ -96,7 +96,9 @@ __global__ void __launch_bounds__(256) bwd_check_kernel(const Params p) {
   }
   delta = warp_sum(delta);  // Delta_r = dO_r . O_r
   const float lse = p.lse_in[((size_t)b * p.Hq + h) * p.L + r];
-  auto visit = [&](const float* krow, const float* vrow, float* dkrow, float* dvrow) {
+  // dK / dV contributions of every row meet in fp64 accumulators (workspace): an fp32 sum of up to
+  // (rows x heads) terms in arbitrary order would drift past 1e-5 where the terms cancel
+  auto visit = [&](const float* krow, const float* vrow, double* dkrow, double* dvrow) {
     float s = 0.f, dp = 0.f;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -110,26 +112,45 @@ __global__ void __launch_bounds__(256) bwd_check_kernel(const Params p) {
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       dq[e] = fmaf(p.scale * ds, krow[lane + 32 * e], dq[e]);   // dQ += c dS K
-      atomicAdd(dkrow + lane + 32 * e, p.scale * ds * qv[e]);    // dK += c dS^T Q
-      atomicAdd(dvrow + lane + 32 * e, pr * dov[e]);             // dV += P^T dO
+      atomicAdd(dkrow + lane + 32 * e, (double)(p.scale * ds) * (double)qv[e]);  // dK += c dS^T Q
+      atomicAdd(dvrow + lane + 32 * e, (double)pr * (double)dov[e]);             // dV += P^T dO
     }
   };
   const size_t kv_stride = (size_t)p.Hkv * D;
   const size_t base = ((size_t)b * p.L * p.Hkv + g) * D;
   const float* K0 = (const float*)p.k + base;
   const float* V0 = (const float*)p.v + base;
+  const size_t kv_elems = (size_t)p.B * p.L * p.Hkv * D;
+  double* dk0 = p.dacc;
+  double* dv0 = p.dacc + kv_elems;
   const int nbase = r < T ? r + 1 : T;
   for (int k = 0; k < nbase; ++k)
-    visit(K0 + k * kv_stride, V0 + k * kv_stride, p.dk + base + k * kv_stride, p.dv + base + k * kv_stride);
+    visit(K0 + k * kv_stride, V0 + k * kv_stride, dk0 + base + k * kv_stride, dv0 + base + k * kv_stride);
   if (r < T) {
     const size_t off = (((size_t)b * p.L + r) * p.Hkv + g) * D;
     for (int i = 0; i < p.step; ++i)
-      visit((const float*)p.ks[i] + off, (const float*)p.vs[i] + off, p.dks[i] + off, p.dvs[i] + off);
+      visit((const float*)p.ks[i] + off, (const float*)p.vs[i] + off, p.dacc + (2 + i) * kv_elems + off,
+            p.dacc + (2 + p.step + i) * kv_elems + off);
   }
   float* dqrow = (float*)p.dq + qoff;
 #pragma unroll
   for (int e = 0; e < E; ++e) dqrow[lane + 32 * e] = dq[e];
 }
+
+// dK / dV outputs (+)= fp32(the fp64 accumulators): array a of [dK_0, dV_0, dK_1.., dV_1..]
+__global__ void check_dkv_finalize_kernel(const Params p, size_t kv_elems) {
+  const size_t n = (size_t)(2 + 2 * p.step) * kv_elems;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int a = (int)(i / kv_elems);
+    const size_t e = i - (size_t)a * kv_elems;
+    float* dst = a == 0 ? p.dk : a == 1 ? p.dv : a < 2 + p.step ? p.dks[a - 2] : p.dvs[a - 2 - p.step];
+    const float v = (float)p.dacc[i];
+    dst[e] = p.accumulate ? dst[e] + v : v;
+  }
+}
+
+size_t check_bwd_ws_bytes(const Params& p) { return (size_t)(2 + 2 * p.step) * p.B * p.L * p.Hkv * p.D * 8; }
 
 __global__ void zero_f32_kernel(float* __restrict__ x, size_t n) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -224,10 +245,16 @@ cudaError_t launch_tree_check(const Params& p, cudaStream_t st) {
 cudaError_t launch_bwd_check(const Params& p, cudaStream_t st) {
   const long rows = (long)p.B * p.Hq * p.L;
   const int blocks = (int)((rows + 7) / 8);
+  cudaError_t e = cudaMemsetAsync(p.dacc, 0, check_bwd_ws_bytes(p), st);
+  if (e != cudaSuccess) return e;
   prof_mark(kKindCheckBwd, true, st);
   if (p.D == 64) bwd_check_kernel<64><<<blocks, 256, 0, st>>>(p);
   else bwd_check_kernel<128><<<blocks, 256, 0, st>>>(p);
   prof_mark(kKindCheckBwd, false, st);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t kv_elems = (size_t)p.B * p.L * p.Hkv * p.D;
+  check_dkv_finalize_kernel<<<148 * 8, 256, 0, st>>>(p, kv_elems);
   return cudaGetLastError();
 }
 

@@ -3,6 +3,8 @@ C-ABI binding, run the oracle on the same bits, compare with allclose
 semantics |gpu - oracle| <= atol + rtol * |oracle|."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -74,7 +76,9 @@ class DeviceCase:
         s = self.case.shape
         out = torch.empty(s.q_shape, dtype=self.dt, device=self.dev)
         lse = torch.empty((s.batch, s.num_q_heads, s.seq_len), dtype=torch.float32, device=self.dev)
-        self.out_lo = torch.empty_like(out) if self.dt == torch.bfloat16 else None
+        # TTT_TEST_NO_OUTLO=1: run without the O - bf16(O) residual (Delta from the bf16 out alone)
+        use_lo = self.dt == torch.bfloat16 and os.environ.get("TTT_TEST_NO_OUTLO", "0") != "1"
+        self.out_lo = torch.empty_like(out) if use_lo else None
         ttt.ttt_attn_fwd(self.desc, j, self.q[j], self.k, self.v, self.ks, self.vs, out, lse,
                          out_lo=self.out_lo, stream=stream)
         return out, lse
