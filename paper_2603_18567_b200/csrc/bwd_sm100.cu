@@ -86,7 +86,10 @@ __device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int
 // leave straight from the mma fragments: dq_acc (tiled fp32) and -Delta / -lse2 by plain
 // stores, dK_i / dV_i by st.global.v2 (overwrite) or red.global.add.v2 (accumulate; L2 does
 // the read-modify-write), so no stage space is spent on fp32 outputs.
-constexpr int kPreCompute = 8;  // compute warps (+ 1 producer warp)
+#ifndef TTT_PRE_WARPS
+#define TTT_PRE_WARPS 8
+#endif
+constexpr int kPreCompute = TTT_PRE_WARPS;  // compute warps (+ 1 producer warp)
 struct PreLayout {
   int NR, NS, R, has_lo;
   uint32_t qbytes, kbytes;  // bytes one TMA box delivers (NR G or NR rows x 128 B)
@@ -482,33 +485,6 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
   }
 }
 
-// dq = bf16(dq accumulator) for this CTA's share of the rows: one thread per 8 consecutive d of a
-// row, `nthr` threads of the CTA starting at thread `t0`; the share is blockIdx.x of gridDim.x
-// (32-bit row decode: B L Hq < 2^31)
-__device__ __forceinline__ void convert_dq_share(const Params& p, const float* src, void* dst, int t, int nthr) {
-  const uint32_t d8 = (uint32_t)p.D / 8;
-  const uint32_t nrows = (uint32_t)p.B * p.L * p.Hq;
-  const uint32_t per = (nrows + gridDim.x - 1) / gridDim.x;
-  const uint32_t r0 = blockIdx.x * per, r1 = min(nrows, r0 + per);
-  const uint32_t nitems = (r1 > r0 ? r1 - r0 : 0u) * d8;
-  for (uint32_t it = (uint32_t)t; it < nitems; it += (uint32_t)nthr) {
-    const uint32_t row = r0 + it / d8;
-    const int d = (int)(it % d8) * 8;
-    const uint32_t bl = row / (uint32_t)p.Hq;
-    const int h = (int)(row - bl * (uint32_t)p.Hq);
-    const int b = (int)(bl / (uint32_t)p.L);
-    const int r = (int)(bl - (uint32_t)b * (uint32_t)p.L);
-    const float4* sp = reinterpret_cast<const float4*>(src + dqacc_index(p, b, h, r, d));
-    const float4 a = __ldcs(sp), c = __ldcs(sp + 1);  // streamed: read once
-    uint4 o;
-    o.x = pack_bf16(a.x, a.y);
-    o.y = pack_bf16(a.z, a.w);
-    o.z = pack_bf16(c.x, c.y);
-    o.w = pack_bf16(c.z, c.w);
-    __stcs(reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dst) + (size_t)row * p.D + d), o);
-  }
-}
-
 // ------------------------------------------------------------------ kernel 2
 struct BwdBars {
   uint64_t kv_full;
@@ -631,10 +607,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int g = (grp / hsplit) % p.Hkv;
   const int b = grp / (hsplit * p.Hkv);
   const int T = p.seq_lens[b];
-  if (kt * kTile >= T) {  // every key of the tile is padding: no gradient flows
-    if (p.conv_src) convert_dq_share(p, p.conv_src, p.conv_dst, threadIdx.x, kBwdThreads);
-    return;
-  }
+  if (kt * kTile >= T) return;  // every key of the tile is padding: no gradient flows
   const int nq = p.nqt - kt;
   const int n_items = nh * nq;  // 128-query tiles
   const int h_first = g * p.G + hs * nh;
@@ -1022,10 +995,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     if (lane == 0) bulk_wait_read0();
   } else {
-    // warps 14-15 (SMSPs 2 / 3: 152 + 136 + 136 + 88 <= 512 registers per lane): the unroll path's
-    // dq conversion of the previous step (HBM traffic under this kernel's tensor-bound work)
-    reg_dealloc<88>();
-    if (p.conv_src) convert_dq_share(p, p.conv_src, p.conv_dst, threadIdx.x - 14 * 32, 64);
+    reg_dealloc<24>();  // warps 14-15: idle (a dq conversion of the previous unroll step here measured
+                        // 5.78 vs 4.47 ms of main passes per unroll, r02c: reverted)
   }
   tc_fence_before();
   __syncthreads();
@@ -1171,16 +1142,7 @@ cudaError_t launch_bwd_unroll_d(const Params* ps, const BwdMaps* maps, const Pre
   const Params& last = ps[S - 1];
   cudaError_t e = last.accumulate ? cudaSuccess : zero_dkv0(last, D, st);
   if (e == cudaSuccess) e = launch_pre<D, true>(last, pmaps, up, st);
-  // main(j) also converts step j + 1's finished dq accumulator (idle warps); step 0's is converted
-  // by the convert kernel after the last main pass
-  for (int j = S - 1; j >= 0 && e == cudaSuccess; --j) {
-    Params pj = ps[j];
-    if (j + 1 < S) {
-      pj.conv_src = ps[j + 1].dq_acc;
-      pj.conv_dst = ps[j + 1].dq;
-    }
-    e = launch_main_convert<D>(pj, maps[j], st, /*convert=*/j == 0);
-  }
+  for (int j = S - 1; j >= 0 && e == cudaSuccess; --j) e = launch_main_convert<D>(ps[j], maps[j], st);
   return e;
 }
 

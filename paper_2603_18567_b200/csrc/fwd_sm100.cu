@@ -57,6 +57,12 @@ extern "C" int ttt_debug_ftrace_read(void* host, unsigned int cta) {
 namespace {
 
 constexpr int kFwdThreads = 512;
+#ifndef TTT_FWD_DIAG_PREFETCH
+#define TTT_FWD_DIAG_PREFETCH 0
+#endif
+#ifndef TTT_FWD_DIAG_MODE
+#define TTT_FWD_DIAG_MODE 0  // dev timing probes only: 1 = diagonal warps skip the math, 2 = skip the loads
+#endif
 #ifndef TTT_FWD_FUSED_DIAG
 #define TTT_FWD_FUSED_DIAG 1  // 0: dev A/B build with round 1's separate ttt_fwd_diag_kernel
 #endif
@@ -305,9 +311,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
       if (warp == 14) {
         if (lane == 0) {
-          // L2 prefetch of every K_i / V_i box this CTA will stream (the ring keeps only 4 x 8 KB in
-          // flight, too little to cover HBM latency: measured +0.02 ms per step j without it)
-          for (int rb = 0; rb < nrb; ++rb)
+          // dev A/B: L2 prefetch of every K_i / V_i box this CTA will stream (measured no gain, r02c)
+          if (TTT_FWD_DIAG_PREFETCH)
+            for (int rb = 0; rb < nrb; ++rb)
             for (int i = 0; i < j; ++i)
 #pragma unroll
               for (int bx = 0; bx < NBOX; ++bx) {
@@ -319,6 +325,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             for (int i = 0; i < j; ++i, ++n) {
               const int st = n % kDgStages, use = n / kDgStages;
               mbar_wait(&bars.dg_empty[st], (use & 1) ^ 1);
+              if (TTT_FWD_DIAG_MODE == 2) {  // dev probe: no loads
+                mbar_arrive(&bars.dg_full[st]);
+                continue;
+              }
               mbar_expect_tx(&bars.dg_full[st], DGS);
               uint8_t* base = sDg + st * DGS;
               const int r0 = qt * kTile + rb * kDgRows;
@@ -382,6 +392,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars.dg_empty[st]);  // values are in registers
+            if (TTT_FWD_DIAG_MODE == 1) continue;             // dev probe: no math
 #pragma unroll
             for (int hs = 0; hs < 2; ++hs) {
               // t_i = c log2e q . K_i[r]: 8-lane partial dots, xor-shuffle sum inside the row's lanes

@@ -45,10 +45,6 @@ struct Params {
   float* delta;   // workspace [B][Hq][L]: -Delta = -rowsum(dO o O)  (stored negated)
   float* lse2;    // workspace [B][Hq][L]: -lse * log2(e)           (stored negated)
   float* dq_acc;  // workspace fp32, tile-contiguous [B][Hq][L/128][D/32][128][32]
-  // bwd main kernel, unroll path: the finished dq accumulator of the step run before this one
-  // (conv_src, tiled like dq_acc) converted to bf16 dq (conv_dst) by otherwise idle warps
-  const float* conv_src;
-  void* conv_dst;
   // fp32 check path backward: fp64 accumulators [dK_0 | dV_0 | dK_1..dK_j | dV_1..dV_j] (workspace)
   double* dacc;
   int seq_lens[TTT_MAX_BATCH];

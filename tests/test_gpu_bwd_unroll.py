@@ -126,8 +126,9 @@ def test_bwd_unroll_fp32_check_mode(cuda_ok):
         lses.append(l)
     g = dc.alloc_grads(S - 1)
     dqs = [torch.empty_like(dc.q[0]) for _ in range(S)]
+    ws = torch.empty(ttt.ttt_attn_bwd_unroll_workspace_size(dc.desc, S), dtype=torch.uint8, device="cuda")
     ttt.ttt_attn_bwd_unroll(dc.desc, dc.q[:S], dc.k, dc.v, dc.ks, dc.vs, outs, lses, dc.dout[:S], dqs,
-                            g["dk_base"], g["dv_base"], g["dk_steps"], g["dv_steps"])
+                            g["dk_base"], g["dv_base"], g["dk_steps"], g["dv_steps"], workspace=ws)
     torch.cuda.synchronize()
     parts = {"dk_base": [], "dv_base": []}
     for j in range(S):
