@@ -370,53 +370,77 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               }
             }
           }
-          for (int i = 0; i < j; ++i, ++n) {
-            const int st = n % kDgStages, use = n / kDgStages;
-            mbar_wait(&bars.dg_full[st], use & 1);
-            const uint32_t base = smem_u32(sDg + st * DGS);
-            float kf[E], vf[E];
+          // Stages two at a time (i, i + 1): their dot products, shuffles and exps are independent,
+          // and the running max only moves (a warp-uniform rescale) when a score exceeds it by
+          // 2^8 — the j-long chain of an exact online softmax was the fused pass's critical path.
+          for (int i = 0; i < j; i += 2) {
+            const int ns = min(2, j - i);
+            uint32_t kw[2][E / 2], vw[2][E / 2];  // packed bf16 pairs of K_i, V_i (this lane's columns)
 #pragma unroll
-            for (int bx = 0; bx < NBOX; ++bx) {
-              const uint4 uk = lds128(base + bx * DGB + sw128_off(srow, k8));
-              const uint4 uv = lds128(base + (NBOX + bx) * DGB + sw128_off(srow, k8));
-              const uint32_t wk[4] = {uk.x, uk.y, uk.z, uk.w}, wv[4] = {uv.x, uv.y, uv.z, uv.w};
+            for (int u = 0; u < 2; ++u) {
+              if (u < ns) {
+                const int st = (n + u) % kDgStages, use = (n + u) / kDgStages;
+                mbar_wait(&bars.dg_full[st], use & 1);
+                const uint32_t base = smem_u32(sDg + st * DGS);
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 fk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wk[e]));
-                const float2 fv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
-                kf[bx * 8 + 2 * e] = fk.x;
-                kf[bx * 8 + 2 * e + 1] = fk.y;
-                vf[bx * 8 + 2 * e] = fv.x;
-                vf[bx * 8 + 2 * e + 1] = fv.y;
+                for (int bx = 0; bx < NBOX; ++bx) {
+                  const uint4 uk = lds128(base + bx * DGB + sw128_off(srow, k8));
+                  const uint4 uv = lds128(base + (NBOX + bx) * DGB + sw128_off(srow, k8));
+                  kw[u][bx * 4 + 0] = uk.x; kw[u][bx * 4 + 1] = uk.y; kw[u][bx * 4 + 2] = uk.z; kw[u][bx * 4 + 3] = uk.w;
+                  vw[u][bx * 4 + 0] = uv.x; vw[u][bx * 4 + 1] = uv.y; vw[u][bx * 4 + 2] = uv.z; vw[u][bx * 4 + 3] = uv.w;
+                }
+              } else {
+#pragma unroll
+                for (int e = 0; e < E / 2; ++e) kw[u][e] = vw[u][e] = 0u;
               }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bars.dg_empty[st]);  // values are in registers
-            if (TTT_FWD_DIAG_MODE == 1) continue;             // dev probe: no math
+            if (lane == 0)
+              for (int u = 0; u < ns; ++u) mbar_arrive(&bars.dg_empty[(n + u) % kDgStages]);  // values in registers
+            n += ns;
+            if (TTT_FWD_DIAG_MODE == 1) continue;  // dev probe: no math
+            // t = c log2e q . K_i[r] for (head, stage): 8-lane partial dots (two FFMA2 chains each)
+            float t[2][2];
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                uint64_t d0 = 0, d1 = 0;
+#pragma unroll
+                for (int e = 0; e < E / 2; e += 2) {
+                  d0 = ffma2(f2pack(qf[hs][2 * e], qf[hs][2 * e + 1]), bf2_to_f2(kw[u][e]), d0);
+                  d1 = ffma2(f2pack(qf[hs][2 * e + 2], qf[hs][2 * e + 3]), bf2_to_f2(kw[u][e + 1]), d1);
+                }
+                float a0, a1, b0, b1;
+                f2unpack(d0, a0, a1);
+                f2unpack(d1, b0, b1);
+                t[hs][u] = (a0 + a1) + (b0 + b1);
+              }
+#pragma unroll
+            for (int sh = 1; sh < 8; sh <<= 1)
+#pragma unroll
+              for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) t[hs][u] += __shfl_xor_sync(0xffffffffu, t[hs][u], sh);
 #pragma unroll
             for (int hs = 0; hs < 2; ++hs) {
-              // t_i = c log2e q . K_i[r]: 8-lane partial dots, xor-shuffle sum inside the row's lanes
-              uint64_t d2 = 0;
+              const float tmax = ns > 1 ? fmaxf(t[hs][0], t[hs][1]) : t[hs][0];
+              if (__any_sync(0xffffffffu, tmax > m[hs] + 8.f)) {  // rare: the max moved (always at i = 0)
+                const float m_new = fmaxf(m[hs], tmax);
+                const float alpha = ex2(m[hs] - m_new);  // 0 when m was -inf
+                l[hs] *= alpha;
 #pragma unroll
-              for (int e = 0; e < E; e += 2)
-                d2 = ffma2(f2pack(qf[hs][e], qf[hs][e + 1]), f2pack(kf[e], kf[e + 1]), d2);
-              float t0, t1;
-              f2unpack(d2, t0, t1);
-              float t = t0 + t1;
-              t += __shfl_xor_sync(0xffffffffu, t, 1);
-              t += __shfl_xor_sync(0xffffffffu, t, 2);
-              t += __shfl_xor_sync(0xffffffffu, t, 4);
-              // online softmax over the j diagonal keys (log2 domain)
-              const float m_new = fmaxf(m[hs], t);
-              const float alpha = ex2(m[hs] - m_new), pw = ex2(t - m_new);
-              l[hs] = fmaf(l[hs], alpha, pw);
-              m[hs] = m_new;
-              const uint64_t a2 = f2pack(alpha, alpha), p2 = f2pack(pw, pw);
+                for (int e = 0; e < E; ++e) acc[hs][e] *= alpha;
+                m[hs] = m_new;
+              }
+              const float p0 = ex2(t[hs][0] - m[hs]), p1 = ns > 1 ? ex2(t[hs][1] - m[hs]) : 0.f;
+              l[hs] += p0 + p1;
+              const uint64_t p02 = f2pack(p0, p0), p12 = f2pack(p1, p1);
 #pragma unroll
-              for (int e = 0; e < E; e += 2) {
-                const uint64_t o = ffma2(f2pack(acc[hs][e], acc[hs][e + 1]), a2,
-                                         fmul2(f2pack(vf[e], vf[e + 1]), p2));
-                f2unpack(o, acc[hs][e], acc[hs][e + 1]);
+              for (int e = 0; e < E / 2; ++e) {
+                uint64_t o = ffma2(bf2_to_f2(vw[0][e]), p02, f2pack(acc[hs][2 * e], acc[hs][2 * e + 1]));
+                o = ffma2(bf2_to_f2(vw[1][e]), p12, o);
+                f2unpack(o, acc[hs][2 * e], acc[hs][2 * e + 1]);
               }
             }
           }
