@@ -40,6 +40,9 @@ __device__ unsigned int g_ttt_trace_cta;
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef TTT_BWD_PREFETCH
+#define TTT_BWD_PREFETCH 2  // items of L2-prefetch lookahead for Q / dO in the main kernel (0 = off)
+#endif
 
 __device__ __forceinline__ float warp_allsum(float x) {
 #pragma unroll
@@ -659,6 +662,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int t = 0; t < n_items; ++t) {
         const int h = h_first + t / nq, qt = kt + t % nq;
         const int qs = t & 1, qph = (t >> 1) & 1;
+        if (TTT_BWD_PREFETCH && t + TTT_BWD_PREFETCH < n_items) {
+          // L2 prefetch of a later item's Q and dO tiles: the 2-slot Q / 3-half dO rings give ~1 item
+          // of lookahead, less than a TMA load's latency when the tile is not in L2 (r02e trace: the
+          // MMA pipe idled ~0.8k clk per item waiting for dO halves)
+          const int tp = t + TTT_BWD_PREFETCH;
+          const int hp = h_first + tp / nq, qtp = kt + tp % nq;
+#pragma unroll
+          for (int bx = 0; bx < NBOX; ++bx) {
+            tma_prefetch_4d(&maps.q, bx * 64, hp, qtp * kTile, b);
+            tma_prefetch_4d(&maps.dout, bx * 64, hp, qtp * kTile, b);
+          }
+        }
         mbar_wait(&bars.q_empty[qs], qph ^ 1);
         mbar_expect_tx(&bars.q_full[qs], TB + 1024);
 #pragma unroll
