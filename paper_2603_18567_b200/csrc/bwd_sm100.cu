@@ -41,7 +41,8 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 #ifndef TTT_BWD_PREFETCH
-#define TTT_BWD_PREFETCH 2  // items of L2-prefetch lookahead for Q / dO in the main kernel (0 = off)
+#define TTT_BWD_PREFETCH 0  // dev: items of L2-prefetch lookahead for Q / dO in the main kernel (2 measured
+                            // 5.03 vs 4.76 ms per unroll, r02f: off)
 #endif
 
 __device__ __forceinline__ float warp_allsum(float x) {
@@ -653,6 +654,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tma_prefetch_desc(&maps.k);
       tma_prefetch_desc(&maps.v);
       tma_prefetch_desc(&maps.dout);
+#ifdef TTT_TRACE
+      int trace_n_2 = 32768;  // the producer's events after the dQ drain warp's (role 2, index 0..)
+#endif
       mbar_expect_tx(&bars.kv_full, 2 * TB);
 #pragma unroll
       for (int bx = 0; bx < NBOX; ++bx) {
@@ -682,6 +686,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const size_t li = ((size_t)b * p.Hq + h) * p.L + (size_t)qt * kTile;
         bulk_load_1d(sL + qs * 128, p.lse2 + li, 512, &bars.q_full[qs]);
         bulk_load_1d(sDel + qs * 128, p.delta + li, 512, &bars.q_full[qs]);
+        TTT_TRACE_EV(2, 11, t);
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
           const int u = 2 * t + x, slot = u % 3, use = u / 3;
@@ -691,6 +696,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int bx = 0; bx < NBOX; ++bx)
             tma_load_4d(sDO + slot * HB + bx * (HB / NBOX), &maps.dout64, &bars.do_full[slot], bx * 64, h,
                         qt * kTile + 64 * x, b);
+          TTT_TRACE_EV(2, 12 + x, t);
         }
       }
     }
@@ -751,6 +757,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
           mbar_wait(&bars.do_full[slot_of(t, x)], use_of(t, x));
+          TTT_TRACE_EV(0, 12 + x, t);
           tc_fence_after();
           issue_dP(slot_of(t, x), x);
           umma_commit_e(&bars.dp_full[x]);
@@ -804,6 +811,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           issue_dV_pair(t + 1);
           if (t + 2 < n_items) {  // S(t+2) over P^T(t+1), consumed by dV(t+1) above
             mbar_wait(&bars.q_full[(t + 2) & 1], ((t + 2) >> 1) & 1);
+            TTT_TRACE_EV(0, 11, t + 2);
             tc_fence_after();
             issue_S((t + 2) & 1);
             TTT_TRACE_EV(0, 10, t);
