@@ -40,6 +40,12 @@ __device__ unsigned int g_ttt_trace_cta;
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef TTT_BWD_DQ_RED
+#define TTT_BWD_DQ_RED 0  // dev: dQ drain by red.global.add.v4 instead of staged TMA reduce-adds
+#endif
+#ifndef TTT_BWD_ORDER
+#define TTT_BWD_ORDER 0  // dev: MMA issue order of an item's dP / dV halves (see the MMA warp)
+#endif
 #ifndef TTT_BWD_PREFETCH
 #define TTT_BWD_PREFETCH 0  // dev: items of L2-prefetch lookahead for Q / dO in the main kernel (2 measured
                             // 5.03 vs 4.76 ms per unroll, r02f: off)
@@ -806,9 +812,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           mbar_wait(&bars.dq_empty, t & 1);  // dQ(t) drained: the dP^T buffers are free
           TTT_TRACE_EV(0, 5, t);
           tc_fence_after();
+#if TTT_BWD_ORDER == 1
+          // dP(t+1,a) dV(t+1,a) dP(t+1,b) dV(t+1,b): dO half (t+1,a) is released (dV done) earlier, so
+          // the producer's load of dO(t+2,b) into that slot starts sooner (r02g trace: that load's
+          // ~3.5k clk latency stalled dP(t+2,b))
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            const int u = t + 1;
+            mbar_wait(&bars.do_full[slot_of(u, x)], use_of(u, x));
+            tc_fence_after();
+            issue_dP(slot_of(u, x), x);
+            umma_commit_e(&bars.dp_full[x]);
+            mbar_wait(&bars.p_full[x], u & 1);
+            tc_fence_after();
+            issue_dV(slot_of(u, x), x, false);
+            umma_commit_e(&bars.do_empty[slot_of(u, x)]);
+          }
+          TTT_TRACE_EV(0, 6, t);
+#else
           issue_dP_pair(t + 1);
           TTT_TRACE_EV(0, 6, t);
           issue_dV_pair(t + 1);
+#endif
           if (t + 2 < n_items) {  // S(t+2) over P^T(t+1), consumed by dV(t+1) above
             mbar_wait(&bars.q_full[(t + 2) & 1], ((t + 2) >> 1) & 1);
             TTT_TRACE_EV(0, 11, t + 2);
@@ -996,6 +1021,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_arrive(&bars.dq_empty);
       if (threadIdx.x == 0) TTT_TRACE_EV(2, 2, t);
       const int row_base = (((b * p.Hq + h) * p.nqt + qt) * (D / 32)) * 128 + wq * 32;
+#if TTT_BWD_DQ_RED
+      {  // dev variant: reduce-add straight from registers (LSU path; the TMA unit then only loads)
+        float* dst = p.dq_acc + (size_t)(row_base + lane) * 32;
+        const float c = p.scale;
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc)
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4)
+            red_add_v4(dst + (size_t)cc * 4096 + 4 * k4, c * __uint_as_float(v[cc * 32 + 4 * k4]),
+                       c * __uint_as_float(v[cc * 32 + 4 * k4 + 1]), c * __uint_as_float(v[cc * 32 + 4 * k4 + 2]),
+                       c * __uint_as_float(v[cc * 32 + 4 * k4 + 3]));
+      }
+      if (false)
+#endif
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         if (lane == 0) bulk_wait_read0();  // the previous reduce has read the staging buffer
