@@ -100,14 +100,29 @@ __device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int
 #define TTT_PRE_WARPS 8
 #endif
 constexpr int kPreCompute = TTT_PRE_WARPS;  // compute warps (+ 1 producer warp)
+// n / d for 0 <= n < 2^31 by multiply-high (Granlund-Montgomery): the pre-pass decodes a kv row
+// w = (b L + r) Hkv + g per query row and item, and runtime divisions were ~20 instructions each
+struct FastDiv {
+  uint32_t d, mul, shift;
+  void init(uint32_t div) {
+    d = div;
+    shift = 0;
+    while ((1u << shift) < div) ++shift;
+    mul = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << shift) - div)) / div + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, mul) + n) >> shift; }
+};
 struct PreLayout {
-  int NR, NS, R, has_lo;
+  int NR, NS, R, lgR, has_lo;
+  FastDiv div_hkv, div_L;
   uint32_t qbytes, kbytes;  // bytes one TMA box delivers (NR G or NR rows x 128 B)
   uint32_t qbox, kbox, off_do, off_o, off_olo, off_q, off_k, off_v, stage_bytes, off_scr, total;
   void init(int nr, int g, int d, int j, int ns, int rr, int lo) {
     NR = nr;
     NS = ns;
     R = rr;
+    lgR = 0;
+    while ((1 << lgR) < rr) ++lgR;
     has_lo = lo;
     const uint32_t nb = (uint32_t)(d / 64);
     qbytes = (uint32_t)nr * g * 128;
@@ -136,7 +151,7 @@ struct PreLayout {
 // slot depends on (i, row, column) only, so both come from the same thread in program order
 // (a per-stage __threadfence here measured 20% of the pass's stall samples, r02a ncu).
 template <int D, bool U>
-__global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
+__global__ void __maxnreg__(224)
     ttt_bwd_pre_kernel(const __grid_constant__ Params p, const __grid_constant__ PreMaps maps,
                        const __grid_constant__ UnrollPre up, PreLayout lay) {
   constexpr int NB = D / 64;
@@ -211,7 +226,22 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
   const int g8 = lane >> 2, c4 = lane & 3;
   const float sl2 = p.scale_log2, cs = p.scale;
   const int MT = (G + 15) / 16;     // 16-row tiles of query rows (R == 1 when G > 16)
-  const int ipg = (NR + R - 1) / R;
+  const int ipg = (NR + R - 1) >> lay.lgR;
+  // the thread's two fragment rows m = g8, g8 + 8 of a 16-row tile: (row w' of the item, head) when
+  // R > 1 (R G <= 16 rows); for R == 1 the head is mt 16 + m (computed per tile)
+  int wr_m[2], hh_m[2];
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+    const int m = g8 + hf * 8;
+    wr_m[hf] = R > 1 ? m / G : 0;
+    hh_m[hf] = R > 1 ? m % G : m;
+  }
+  auto decode = [&](uint32_t w, int& b_, int& r_, int& g_) {  // w = (b L + r) Hkv + g
+    const uint32_t bl = lay.div_hkv.div(w);
+    g_ = (int)(w - bl * (uint32_t)p.Hkv);
+    b_ = (int)lay.div_L.div(bl);
+    r_ = (int)(bl - (uint32_t)b_ * (uint32_t)p.L);
+  };
   uint8_t* scrP = psm + lay.off_scr + cw * 2560;  // [16 rows m][40] bf16 (80-B rows: conflict-free)
   uint8_t* scrS = scrP + 1280;
   const uint32_t sP = smem_u32(scrP), sS = smem_u32(scrS);
@@ -235,20 +265,20 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = nt * 8 + 2 * c4 + e;
-          colw[nt][e] = c < ncols ? c % R : -1;
+          colw[nt][e] = c < ncols ? (c & (R - 1)) : -1;
         }
       int brow_i[4], brow_w[4];  // ldmatrix row (lane & 7) of column tile nt: step i, row w'
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         const int c = ncols > 0 ? min(nt * 8 + (lane & 7), ncols - 1) : 0;
-        brow_i[nt] = c / R;
-        brow_w[nt] = c % R;
+        brow_i[nt] = c >> lay.lgR;
+        brow_w[nt] = c & (R - 1);
       }
       for (int gi = 0; gi < msg; ++gi, ++n) {
         const int grp = (int)blockIdx.x + (g0 + gi) * (int)gridDim.x;
         const int st = n % NS;
         const int w0 = grp * NR, nv = min(NR, nrows - w0);
-        const int nitems = (nv + R - 1) / R;
+        const int nitems = (nv + R - 1) >> lay.lgR;
         // items of this group owned by this warp: item id gidx*ipg + k, round-robin over warps. The
         // mapping depends on the group's position only (not on j), so in the unroll pass the SAME
         // thread writes a given dK_i / dV_i element at every step: its j = S-1 store and the later
@@ -263,12 +293,10 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
           for (int hf = 0; hf < 2; ++hf) {
             const int m = g8 + hf * 8;
             const int mrows0 = R > 1 ? R * G : min(16, G);
-            const int wr0 = R > 1 ? m / G : 0, hh0 = R > 1 ? m % G : m;
+            const int wr0 = wr_m[hf], hh0 = hh_m[hf];
             if (m < mrows0 && k_first * R + wr0 < nv) {
-              const uint32_t w = (uint32_t)(w0 + k_first * R + wr0);
-              const uint32_t bl = w / (uint32_t)p.Hkv;
-              const int g_ = (int)(w - bl * (uint32_t)p.Hkv), b_ = (int)(bl / (uint32_t)p.L);
-              const int r_ = (int)(bl - (uint32_t)b_ * (uint32_t)p.L);
+              int b_, r_, g_;
+              decode((uint32_t)(w0 + k_first * R + wr0), b_, r_, g_);
               lse_pf[hf] = lse_in[((size_t)b_ * p.Hq + g_ * G + hh0) * p.L + r_];
             }
           }
@@ -286,14 +314,10 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
               const int m = g8 + hf * 8;
-              wr[hf] = R > 1 ? m / G : 0;
-              hh[hf] = R > 1 ? m % G : mt * 16 + m;
+              wr[hf] = wr_m[hf];
+              hh[hf] = R > 1 ? hh_m[hf] : mt * 16 + m;
               okr[hf] = m < mrows && lr0 + wr[hf] < nv;
-              const uint32_t w = (uint32_t)(w0 + min(lr0 + wr[hf], nv - 1));
-              const uint32_t bl = w / (uint32_t)p.Hkv;
-              gg[hf] = (int)(w - bl * (uint32_t)p.Hkv);
-              bb[hf] = (int)(bl / (uint32_t)p.L);
-              rr[hf] = (int)(bl - (uint32_t)bb[hf] * (uint32_t)p.L);
+              decode((uint32_t)(w0 + min(lr0 + wr[hf], nv - 1)), bb[hf], rr[hf], gg[hf]);
               act[hf] = okr[hf] && rr[hf] < p.seq_lens[bb[hf]];
               l2[hf] = okr[hf] ? ((k == k_first && mt == 0) ? lse_pf[hf]
                                                           : lse_in[((size_t)bb[hf] * p.Hq + gg[hf] * G + hh[hf]) * p.L + rr[hf]]) *
@@ -436,8 +460,8 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
 #pragma unroll
               for (int hf = 0; hf < 2; ++hf) {
                 const int nn = t2 * 16 + g8 + hf * 8;
-                oi[hf] = nn / R;
-                ow[hf] = nn % R;
+                oi[hf] = nn >> lay.lgR;
+                ow[hf] = nn & (R - 1);
                 ook[hf] = nn < ncols && lr0 + ow[hf] < nv;
               }
               const uint32_t brow = qrow0 + (uint32_t)min((mi & 1) * 8 + (lane & 7), mrows - 1);  // B' rows m
@@ -1116,7 +1140,11 @@ bool pre_layout(const Params& p, int D, PreLayout* lay) {
     if (nr * p.G > 256) continue;
     for (int ns = 4; ns >= 1; --ns) {
       lay->init(nr, p.G, D, p.step, ns, R, lo);
-      if (lay->total <= 225 * 1024 && (ns >= 2 || nr == R)) return true;
+      if (lay->total <= 225 * 1024 && (ns >= 2 || nr == R)) {
+        lay->div_hkv.init((uint32_t)p.Hkv);
+        lay->div_L.init((uint32_t)p.L);
+        return true;
+      }
     }
   }
   return false;
