@@ -151,7 +151,7 @@ struct PreLayout {
 // slot depends on (i, row, column) only, so both come from the same thread in program order
 // (a per-stage __threadfence here measured 20% of the pass's stall samples, r02a ncu).
 template <int D, bool U>
-__global__ void __maxnreg__(224)
+__global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
     ttt_bwd_pre_kernel(const __grid_constant__ Params p, const __grid_constant__ PreMaps maps,
                        const __grid_constant__ UnrollPre up, PreLayout lay) {
   constexpr int NB = D / 64;

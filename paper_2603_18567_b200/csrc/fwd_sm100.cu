@@ -104,6 +104,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __shared__ FwdBars bars;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef TTT_TRACE
+  if (blockIdx.x == g_ttt_trace_cta && threadIdx.x == 0)
+    g_ttt_trace[1][kTraceCap - 2] = (clock64() << 20) | (9ull << 12);  // CTA start
+#endif
 
   // ---- work decode: (b, g)-major so one kv head's K/V stay hot in L2; within
   // it the longest (highest) q tiles first; head pairs of a tile adjacent ----
@@ -728,6 +732,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc(tbase, 512);
+#ifdef TTT_TRACE
+  if (blockIdx.x == g_ttt_trace_cta && threadIdx.x == 0)
+    g_ttt_trace[1][kTraceCap - 3] = (clock64() << 20) | (10ull << 12);  // CTA end
+#endif
 }
 
 // Diagonal pre-pass (TTT-specific): for every row r < T_b
