@@ -206,7 +206,7 @@ def workload_config(shape: Shape, world: int, cfg: str = "llama8b"):
 class Unroll:
     """Device buffers of one per-GPU unroll + the C-ABI calls of one step."""
 
-    def __init__(self, shape: Shape, seed: int, dev, bwd_unroll: bool = True):
+    def __init__(self, shape: Shape, seed: int, dev, bwd_unroll: bool = False):
         import paper_2603_18567_b200 as ttt
         self.ttt = ttt
         self.s = s = shape
@@ -809,12 +809,11 @@ def main():
     ap.add_argument("--zero2", action="store_true",
                     help="ZeRO-2 draft gradient exchange (reduce-scatter per backward call + parameter all-gather "
                          "after the step, PAPER.md:281) instead of the bucketed all-reduce")
-    ap.add_argument("--bwd-percall", action="store_true",
-                    help="S ttt_attn_bwd calls per unroll instead of one ttt_attn_bwd_unroll call (the default: "
-                         "one diagonal pass for all steps, dK_i / dV_i written once, each step's dq conversion "
-                         "inside the next step's tensor-core pass)")
+    ap.add_argument("--bwd-unroll", action="store_true",
+                    help="one ttt_attn_bwd_unroll call per unroll instead of S ttt_attn_bwd calls. Needs every "
+                         "step's dO up front, which chained TTT training does not have (step j's output feeds "
+                         "step j+1, so dO_j exists only after step j+1's backward): a what-if, not the headline")
     args = ap.parse_args()
-    args.bwd_unroll = not args.bwd_percall
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3
     world = int(os.environ.get("WORLD_SIZE", "1"))
