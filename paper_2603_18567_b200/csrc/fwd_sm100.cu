@@ -667,17 +667,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // the combine pass)
       const float inv_l = (TREE && l_f == 0.f) ? 0.f : 1.f / l_f;
       const float a_n = alpha * inv_l, b_n = beta * inv_l;
+      // per 64-column box: one 64-column TMEM load (a single wait), the box written to the staging tile,
+      // then its TMA store issued right away so it drains under the next box's math (measured: the
+      // epilogue, o_full -> CTA end, took ~8k clk with four 32-column load waits and one store at the end)
 #pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 32) {
-        uint32_t o[32];
-        tmem_ld32(tO + c0, o);
+      for (int bx = 0; bx < NBOX; ++bx) {
+        uint32_t o[64];
+        tmem_ld64w(tO + bx * 64, o);
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
+        for (int q4 = 0; q4 < 8; ++q4) {
           float v[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(o[q4 * 8 + e]) * a_n;
-          const int col = c0 + q4 * 8;
-          const uint32_t soff = (uint32_t)(col >> 6) * 16384u + (uint32_t)row * 128u + ((((uint32_t)(col & 63) >> 3) ^ sw) << 4);
+          const uint32_t soff = (uint32_t)bx * 16384u + (uint32_t)row * 128u + ((((uint32_t)q4) ^ sw) << 4);
           if (has_diag) {
             const uint4 odv = *reinterpret_cast<const uint4*>(st_hi + soff);
             const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&odv);
@@ -705,15 +707,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             *reinterpret_cast<uint4*>(st_lo + soff) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
           }
         }
-      }
-      if (!TREE || tree_row) p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
-      if (threadIdx.x == 0) TTT_TRACE_EV(1, 6, 0);
-      fence_async_smem();
-      named_bar_sync(1 + slot, 128);
-      if (threadIdx.x == 0) TTT_TRACE_EV(1, 7, 0);
-      if (row == 0) {
-#pragma unroll
-        for (int bx = 0; bx < D / 64; ++bx) {
+        fence_async_smem();
+        named_bar_sync(1 + slot, 128);
+        if (row == 0) {
           if constexpr (TREE) {  // the slot's two heads, 64-row boxes
             for (int k = 2 * slot; k < min(2 * slot + 2, nheads); ++k)
               tma_store_4d(&maps.out, st_hi + bx * 16384 + (k & 1) * 8192, bx * 64, h0 + k, 0, bst);
@@ -721,8 +717,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tma_store_4d(&maps.out, st_hi + bx * 16384, bx * 64, h, qt * kTile, bst);
             if (p.out_lo) tma_store_4d(&maps.out_lo, st_lo + bx * 16384, bx * 64, h, qt * kTile, b);
           }
+          bulk_commit();
         }
-        bulk_commit();
+      }
+      if (threadIdx.x == 0) TTT_TRACE_EV(1, 6, 0);
+      if (!TREE || tree_row) p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
+      if (row == 0) {
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 8, 0);
         bulk_wait_read0();  // smem must stay valid until the bulk engine has read it
       }
