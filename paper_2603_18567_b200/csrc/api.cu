@@ -81,6 +81,20 @@ bool encode_rows2d(CUtensorMap* m, const void* ptr, long long rows, int D, int b
   return r == CUDA_SUCCESS;
 }
 
+// BSHD bf16 tensor -> 4-D map with box (D, 1, box_rows, 1), no swizzle: whole rows of one head
+bool encode_bshd_rows(CUtensorMap* m, const void* ptr, int B, int L, int H, int D, int box_rows) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)L, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)H * D * 2, (cuuint64_t)L * H * D * 2};
+  cuuint32_t box[4] = {(cuuint32_t)D, 1, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool encode_dqacc(CUtensorMap* m, void* ptr, size_t rows) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return false;
@@ -343,8 +357,8 @@ int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
       (p.out_lo && !encode_bshd(&maps.out_lo, p.out_lo, p.B, p.L, p.Hq, p.D)))
     return TTT_ERR_CUDA;
   for (int i = 0; i < p.step; ++i)  // the forward's in-kernel diagonal ring: 16-row boxes of K_i / V_i
-    if (!encode_bshd(&maps.kd[i], p.ks[i], p.B, p.L, p.Hkv, p.D, 16) ||
-        !encode_bshd(&maps.vd[i], p.vs[i], p.B, p.L, p.Hkv, p.D, 16))
+    if (!encode_bshd_rows(&maps.kd[i], p.ks[i], p.B, p.L, p.Hkv, p.D, 16) ||
+        !encode_bshd_rows(&maps.vd[i], p.vs[i], p.B, p.L, p.Hkv, p.D, 16))
       return TTT_ERR_CUDA;
   DiagMaps dmaps;
   if (p.step > 0 && fwd_uses_diag_kernel()) {

@@ -57,9 +57,6 @@ extern "C" int ttt_debug_ftrace_read(void* host, unsigned int cta) {
 namespace {
 
 constexpr int kFwdThreads = 512;
-#ifndef TTT_FWD_DIAG_PREFETCH
-#define TTT_FWD_DIAG_PREFETCH 0
-#endif
 #ifndef TTT_FWD_DIAG_MODE
 #define TTT_FWD_DIAG_MODE 0  // dev timing probes only: 1 = diagonal warps skip the math, 2 = skip the loads
 #endif
@@ -98,7 +95,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint8_t* sQ = smem;           // 2 tiles (head slots)
   uint8_t* sK = smem + 2 * TB;  // 2 stages
   uint8_t* sV = smem + 4 * TB;  // 2 stages
-  constexpr int DGB = kDgRows * 128;       // one 16-row x 64-column SW128 box
+  constexpr int DGB = kDgRows * 128;       // 16 rows x 64 columns of bf16 (a tensor's block is NBOX x DGB)
   constexpr int DGS = 2 * NBOX * DGB;      // one stage: K_i and V_i rows of a 16-row block
   uint8_t* sDg = smem + 6 * TB;            // diagonal ring, kDgStages stages
   __shared__ FwdBars bars;
@@ -315,15 +312,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
       if (warp == 14) {
         if (lane == 0) {
-          // dev A/B: L2 prefetch of every K_i / V_i box this CTA will stream (measured no gain, r02c)
-          if (TTT_FWD_DIAG_PREFETCH)
-            for (int rb = 0; rb < nrb; ++rb)
-            for (int i = 0; i < j; ++i)
-#pragma unroll
-              for (int bx = 0; bx < NBOX; ++bx) {
-                tma_prefetch_4d(&maps.kd[i], bx * 64, g, qt * kTile + rb * kDgRows, b);
-                tma_prefetch_4d(&maps.vd[i], bx * 64, g, qt * kTile + rb * kDgRows, b);
-              }
           int n = 0;
           for (int rb = 0; rb < nrb; ++rb)
             for (int i = 0; i < j; ++i, ++n) {
@@ -337,10 +325,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               uint8_t* base = sDg + st * DGS;
               const int r0 = qt * kTile + rb * kDgRows;
 #pragma unroll
-              for (int bx = 0; bx < NBOX; ++bx) {
-                tma_load_4d(base + bx * DGB, &maps.kd[i], &bars.dg_full[st], bx * 64, g, r0, b);
-                tma_load_4d(base + (NBOX + bx) * DGB, &maps.vd[i], &bars.dg_full[st], bx * 64, g, r0, b);
-              }
+              // one box per tensor: 16 rows x D columns, no swizzle (rows of D x 2 bytes)
+              tma_load_4d(base, &maps.kd[i], &bars.dg_full[st], 0, g, r0, b);
+              tma_load_4d(base + NBOX * DGB, &maps.vd[i], &bars.dg_full[st], 0, g, r0, b);
             }
         }
       } else if (warp < 14) {
@@ -388,8 +375,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 const uint32_t base = smem_u32(sDg + st * DGS);
 #pragma unroll
                 for (int bx = 0; bx < NBOX; ++bx) {
-                  const uint4 uk = lds128(base + bx * DGB + sw128_off(srow, k8));
-                  const uint4 uv = lds128(base + (NBOX + bx) * DGB + sw128_off(srow, k8));
+                  const uint32_t off = (uint32_t)srow * (D * 2) + bx * 128 + k8 * 16;  // row-major rows
+                  const uint4 uk = lds128(base + off);
+                  const uint4 uv = lds128(base + NBOX * DGB + off);
                   kw[u][bx * 4 + 0] = uk.x; kw[u][bx * 4 + 1] = uk.y; kw[u][bx * 4 + 2] = uk.z; kw[u][bx * 4 + 3] = uk.w;
                   vw[u][bx * 4 + 0] = uv.x; vw[u][bx * 4 + 1] = uv.y; vw[u][bx * 4 + 2] = uv.z; vw[u][bx * 4 + 3] = uv.w;
                 }
