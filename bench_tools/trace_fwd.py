@@ -23,16 +23,17 @@ for _ in range(2):
 lib.ttt_debug_ftrace_read(ctypes.c_void_p(buf.ctypes.data), ctypes.c_uint(cta))
 names = {0: {9: "mma:start", 8: "mma:got_q_k0", 1: "mma:got_v", 2: "mma:got_p0", 3: "mma:got_p1"},
          1: {9: "cta:start", 10: "cta:end", 1: "s0:got_s", 2: "s0:p_done", 3: "s0:loop_end", 4: "s0:got_o", 5: "s0:epi_done", 6: "s0:epi_math_done", 7: "s0:epi_bar", 8: "s0:tma_issued"},
-         2: {1: "s1:got_s", 2: "s1:p_done"}}
+         2: {1: "s1:got_s", 2: "s1:p_done"},
+         3: {1: "dg:stage_full", 2: "dg:done", 3: "dgp:issued", 4: "dg:start"}}
 ev = []
-for role in range(3):
+for role in range(4):
     for x in buf[role]:
         x = int(x)
         if x == 0: continue
         ev.append((x >> 20, names[role].get((x >> 12) & 0xFF, str((x >> 12) & 0xFF)), x & 0xFFF))
 ev.sort()
 t0 = ev[0][0]
-for t, n, i in ev[:400]:
+for t, n, i in ev[:1000]:
     print(f"{t - t0:8d} {n:14s} {i}")
 got = [t for t, n, i in ev if n == "s0:got_s"]
 st = [t for t, n, i in ev if n == "cta:start"]

@@ -312,6 +312,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
       if (warp == 14) {
         if (lane == 0) {
+#ifdef TTT_TRACE
+          int trace_n_3 = 32768;
+#endif
           int n = 0;
           for (int rb = 0; rb < nrb; ++rb)
             for (int i = 0; i < j; ++i, ++n) {
@@ -328,6 +331,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               // one box per tensor: 16 rows x D columns, no swizzle (rows of D x 2 bytes)
               tma_load_4d(base, &maps.kd[i], &bars.dg_full[st], 0, g, r0, b);
               tma_load_4d(base + NBOX * DGB, &maps.vd[i], &bars.dg_full[st], 0, g, r0, b);
+              TTT_TRACE_EV(3, 3, n);
             }
         }
       } else if (warp < 14) {
@@ -338,6 +342,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int srow = dw * 4 + (lane >> 3);  // row within a 16-row block
         const float sl2 = p.scale_log2;
         mbar_wait(&bars.q, 0);  // q rows are read from the Q tiles (shared with the S MMAs, read-only)
+        TTT_TRACE_DECL(3);
+        if (threadIdx.x == 320) TTT_TRACE_EV(3, 4, 0);
         int n = 0;
         for (int rb = 0; rb < nrb; ++rb) {
           const int row = rb * kDgRows + srow;
@@ -372,6 +378,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               if (u < ns) {
                 const int st = (n + u) % kDgStages, use = (n + u) / kDgStages;
                 mbar_wait(&bars.dg_full[st], use & 1);
+                if (threadIdx.x == 320) TTT_TRACE_EV(3, 1, n + u);
                 const uint32_t base = smem_u32(sDg + st * DGS);
 #pragma unroll
                 for (int bx = 0; bx < NBOX; ++bx) {
@@ -458,6 +465,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             }
           }
         }
+        if (threadIdx.x == 320) TTT_TRACE_EV(3, 2, n);
         fence_async_global();  // the out rows are read back by the producer's TMA (async proxy)
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.diag_done);

@@ -102,6 +102,25 @@ class OptimizerStep:
         self.exchanges += 1
 
 
+def exchange_grads(model: torch.nn.Module, buckets: "GradBuckets") -> None:
+    """The draft's real parameter gradients through the exchange: flatten them (parameter order) into
+    `buckets.flat`, reduce (release_all + finish: the bucketed all-reduce averages in place; ZeRO-2
+    reduce-scatters into the owned shards), and for the all-reduce form write the averaged values
+    back into the parameters' .grad. Called once per optimizer step after the last micro-batch."""
+    params = [p for p in model.parameters() if p.grad is not None]
+    n = sum(p.numel() for p in params)
+    if n > buckets.flat.numel():
+        raise ValueError("gradient buffer too small for the model")
+    torch.cat([p.grad.reshape(-1).to(buckets.flat.dtype) for p in params], out=buckets.flat[:n])
+    buckets.release_all()
+    buckets.finish()
+    if not isinstance(buckets, Zero2Buckets):
+        off = 0
+        for p in params:
+            p.grad.copy_(buckets.flat[off:off + p.numel()].view_as(p.grad))
+            off += p.numel()
+
+
 def max_over_ranks(x: float, device="cpu", group=None) -> float:
     """The multi-GPU timing rule: a step takes as long as its slowest rank."""
     if not dist.is_initialized() or dist.get_world_size(group) == 1:

@@ -9,8 +9,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2603_18567_b200.dp import (GradBuckets, OptimizerStep, Zero2Buckets, max_over_ranks, micro_batches,
-                                      shard_sequences)
+from paper_2603_18567_b200.dp import (GradBuckets, OptimizerStep, Zero2Buckets, exchange_grads, max_over_ranks,
+                                      micro_batches, shard_sequences)
 
 
 def test_shard_sequences_partition():
@@ -236,3 +236,39 @@ def test_optimizer_step_one_exchange_after_micro_batches_world2(zero2):
         assert calls["reduce_scatter" if zero2 else "all_reduce"] == 7
         seen_all += seen
     assert sorted(seen_all) == list(range(64))
+
+
+def _model_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.manual_seed(0)  # identical initial parameters on every rank
+        model = torch.nn.Sequential(torch.nn.Linear(16, 32), torch.nn.SiLU(), torch.nn.Linear(32, 8)).double()
+        g = torch.Generator().manual_seed(100 + rank)  # different data per rank
+        x = torch.randn(64, 16, generator=g, dtype=torch.float64)
+        model(x).pow(2).mean().backward()
+        local = [p.grad.clone() for p in model.parameters()]
+        n = sum(p.numel() for p in model.parameters())
+        exchange_grads(model, GradBuckets(n, 3, dtype=torch.float64))
+        q.put((rank, local, [p.grad.clone() for p in model.parameters()]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exchange_real_model_grads_world2():
+    """Real parameter gradients (a small MLP's backward on per-rank data) through the bucketed
+    all-reduce: every rank ends with the mean of the ranks' local gradients."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_model_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    mean = [(a + b) / 2 for a, b in zip(res[0][1], res[1][1])]
+    for rank, _, got in res:
+        for g, m in zip(got, mean):
+            assert torch.allclose(g, m, atol=1e-12), rank
