@@ -19,10 +19,11 @@
 //  3. ttt_bwd_dq_convert_kernel: dq = bf16(dq_acc).
 // dq_acc is a tile-contiguous fp32 workspace (see dqacc_index) reduced into by TMA.
 //
-// Warp roles of the main kernel (320 threads):
-//   warps 0-3 compute (thread = key row, TMEM lanes 0-127), warps 4-7 dQ drain
-//   (thread = query row), warp 8 TMA producer, warp 9 TMEM owner + MMA issuer.
-// TMEM columns: S^T/P^T [0,128) dP^T/dS^T/dQ [128,256) dV [256,256+D) dK [384,384+D).
+// Warp roles of the main kernel (512 threads, setmaxnreg-rebalanced; see ttt_bwd_sm100_kernel):
+//   warps 0-3 dQ drain (thread = query row), warps 4-7 / 8-11 compute for the 64-query sub-items
+//   a / b (thread = key row, TMEM lanes 0-127), warp 12 TMEM owner + MMA issuer, warp 13 TMA
+//   producer, warps 14-15 idle.
+// TMEM columns: S^T[a,b] [0,128) dP^T[a,b] / dS^T, aliased by dQ [128,256) dV [256,256+D) dK [384,384+D).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
