@@ -60,6 +60,9 @@ constexpr int kFwdThreads = 512;
 #ifndef TTT_FWD_DIAG_MODE
 #define TTT_FWD_DIAG_MODE 0  // dev timing probes only: 1 = diagonal warps skip the math, 2 = skip the loads
 #endif
+#ifndef TTT_FWD_PERSIST
+#define TTT_FWD_PERSIST 1  // dev A/B: 0 = one item per CTA (the kernel's item loop then runs once)
+#endif
 #ifndef TTT_FWD_FUSED_DIAG
 #define TTT_FWD_FUSED_DIAG 1  // 0: dev A/B build with round 1's separate ttt_fwd_diag_kernel
 #endif
@@ -182,8 +185,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bars.dg_full[i], 1);
       mbar_init(&bars.dg_empty[i], 4);  // the four diagonal compute warps
     }
-    mbar_init(&bars.diag_done[0], 4);
-    mbar_init(&bars.diag_done[1], 4);
+    mbar_init(&bars.diag_done[0], 128);  // every thread of the diagonal warps (its reads of the Q tile
+    mbar_init(&bars.diag_done[1], 128);  // and writes of the O_d / A_d rows precede its own arrive)
     fence_mbar_init();
   }
   if (warp == 9) {
@@ -514,8 +517,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
           if (threadIdx.x == 320) TTT_TRACE_EV(3, 2, n);
           __threadfence_block();  // the O_d rows (and A_d) before diag_done: the epilogue reads them
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars.diag_done[it & 1]);
+          mbar_arrive(&bars.diag_done[it & 1]);
         }
       }
     }
@@ -1084,7 +1086,7 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
     if (dev < 64) sms[dev] = nsm;
   }
-  const int grid = std::min(items, nsm);
+  const int grid = TTT_FWD_PERSIST ? std::min(items, nsm) : items;
   prof_mark(kKindFwdMain, true, st);
   ttt_fwd_sm100_kernel<D, false><<<grid, kFwdThreads, smem, st>>>(p, maps);
   prof_mark(kKindFwdMain, false, st);
