@@ -60,6 +60,9 @@ constexpr int kFwdThreads = 512;
 #ifndef TTT_FWD_DIAG_MODE
 #define TTT_FWD_DIAG_MODE 0  // dev timing probes only: 1 = diagonal warps skip the math, 2 = skip the loads
 #endif
+#ifndef TTT_FWD_PROBE
+#define TTT_FWD_PROBE 0  // dev timing probes only (wrong results): 1 = skip out_lo, 2 = skip the O_d loads
+#endif
 #ifndef TTT_FWD_PERSIST
 #define TTT_FWD_PERSIST 1  // dev A/B: 0 = one item per CTA (the kernel's item loop then runs once)
 #endif
@@ -735,7 +738,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(o[q4 * 8 + e]) * a_n;
           const uint32_t soff = (uint32_t)bx * 16384u + (uint32_t)row * 128u + ((((uint32_t)q4) ^ sw) << 4);
-          if (has_diag) {
+          if (has_diag && !(TTT_FWD_PROBE & 2)) {
             const uint4 odv = __ldcg(reinterpret_cast<const uint4*>(od_row + bx * 64 + q4 * 8));
             const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&odv);
 #pragma unroll
@@ -751,7 +754,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           wv.z = pack_bf16(v[4], v[5]);
           wv.w = pack_bf16(v[6], v[7]);
           *reinterpret_cast<uint4*>(st_hi + soff) = wv;
-          if (!TREE && p.out_lo) {  // residual O - bf16(O), so the backward's Delta sees ~16-bit O
+          if (!TREE && p.out_lo && !(TTT_FWD_PROBE & 1)) {  // residual O - bf16(O): the backward's Delta sees ~16-bit O
             const uint32_t hi[4] = {wv.x, wv.y, wv.z, wv.w};
             uint32_t lo[4];
 #pragma unroll
