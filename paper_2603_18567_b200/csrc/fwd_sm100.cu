@@ -79,8 +79,9 @@ struct FwdBars {
   uint64_t q;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
   uint64_t s_full[2], p_lo[2], p_hi[2], o_full[2];  // P published in two 64-column halves
-  uint64_t s_done;       // the item's S MMAs complete (its Q tiles are free for the next item)
-  uint64_t stg_free[2];  // a slot's out staging in the V stages has been read by its TMA stores
+  uint64_t s_done;       // the item's S MMAs complete
+  uint64_t od;           // the item's diagonal partial O_d landed in the Q tiles
+  uint64_t stg_free[2];  // a slot's epilogue is done with the Q tile / V stage it staged in
   uint64_t dg_full[kDgStages], dg_empty[kDgStages];  // diagonal K_i / V_i ring
   // the item's diagonal partial (O_d rows, A_d) complete; by item parity, so the diagonal warps of
   // item it+1 cannot complete a phase the epilogue of item it is still to wait for
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bars.stg_free[i], 1);
     }
     mbar_init(&bars.s_done, 1);
+    mbar_init(&bars.od, 1);
     for (int i = 0; i < kDgStages; ++i) {
       mbar_init(&bars.dg_full[i], 1);
       mbar_init(&bars.dg_empty[i], 4);  // the four diagonal compute warps
@@ -210,14 +212,34 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       int gt = 0;                // K / V tiles loaded so far (ring position)
       int n1 = 0;                // items with a slot-1 head so far
       bool prev_has1 = false;
+      auto load_k = [&](const Item& w, int n) {
+        const int gi = gt + n, st = gi & 1, ph = (gi >> 1) & 1;
+        mbar_wait(&bars.k_empty[st], ph ^ 1);
+        mbar_expect_tx(&bars.k_full[st], TB);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, w.g, (w.kvt0 + n) * kTile, w.b);
+      };
+      auto load_v = [&](const Item& w, int n) {
+        const int gi = gt + n, st = gi & 1, ph = (gi >> 1) & 1;
+        mbar_wait(&bars.v_empty[st], ph ^ 1);
+        mbar_expect_tx(&bars.v_full[st], TB);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, w.g, (w.kvt0 + n) * kTile, w.b);
+      };
       for (int it = 0;; ++it) {
         const int k = item_of(it);
         if (k < 0) break;
         Item w;
         decode(k, w);
-        if (it > 0) {  // the Q tiles are free: every S MMA and the diagonal warps of item it-1 are done
-          mbar_wait(&bars.s_done, (it - 1) & 1);
-          if (diag_on) mbar_wait(&bars.diag_done[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        // K_0 tile 0 first: its stage is free once the previous item's S MMAs are done, before the
+        // previous epilogue ends
+        load_k(w, 0);
+        if (it > 0) {  // the previous epilogue is done with the Q tiles (O_d, out_lo staging) and the V
+                       // stages (out staging): its stores have read them
+          mbar_wait(&bars.stg_free[0], (it - 1) & 1);
+          if (prev_has1) mbar_wait(&bars.stg_free[1], (n1 - 1) & 1);
         }
         if constexpr (TREE) {  // 64-row boxes: head h0 + k -> slot k / 2, rows 64 (k % 2) ..
           mbar_expect_tx(&bars.q, w.nheads * (TB / 2));
@@ -234,22 +256,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             if (w.has1) tma_load_4d(sQ + TB + bx * 16384, &maps.q, &bars.q, bx * 64, w.h0 + 1, w.qt * kTile, w.b);
           }
         }
-        for (int n = 0; n < w.nkv; ++n) {
-          const int gi = gt + n, st = gi & 1, ph = (gi >> 1) & 1;
-          mbar_wait(&bars.k_empty[st], ph ^ 1);
-          mbar_expect_tx(&bars.k_full[st], TB);
+        load_v(w, 0);
+        for (int n = 1; n < w.nkv; ++n) {
+          load_k(w, n);
+          load_v(w, n);
+        }
+        if (diag_on) {  // the diagonal partial O_d of the two heads into the Q tiles, once no S MMA and
+                        // no diagonal warp reads them
+          mbar_wait(&bars.s_done, it & 1);
+          mbar_wait(&bars.diag_done[it & 1], (it >> 1) & 1);
+          mbar_expect_tx(&bars.od, (w.has1 ? 2 : 1) * TB);
 #pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx)
-            tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, w.g, (w.kvt0 + n) * kTile, w.b);
-          if (n == 0 && it > 0) {  // the previous epilogue staged out in the V stages: wait until stored
-            mbar_wait(&bars.stg_free[0], (it - 1) & 1);
-            if (prev_has1) mbar_wait(&bars.stg_free[1], (n1 - 1) & 1);
+          for (int bx = 0; bx < NBOX; ++bx) {
+            tma_load_4d(sQ + bx * 16384, &maps.out, &bars.od, bx * 64, w.h0, w.qt * kTile, w.b);
+            if (w.has1) tma_load_4d(sQ + TB + bx * 16384, &maps.out, &bars.od, bx * 64, w.h0 + 1, w.qt * kTile, w.b);
           }
-          mbar_wait(&bars.v_empty[st], ph ^ 1);
-          mbar_expect_tx(&bars.v_full[st], TB);
-#pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx)
-            tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, w.g, (w.kvt0 + n) * kTile, w.b);
         }
         gt += w.nkv;
         prev_has1 = w.has1;
@@ -519,7 +540,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
         }
           if (threadIdx.x == 320) TTT_TRACE_EV(3, 2, n);
-          __threadfence_block();  // the O_d rows (and A_d) before diag_done: the epilogue reads them
+          // the O_d rows (generic-proxy writes) are read back by the producer's TMA (async proxy) and
+          // A_d by the epilogue: a proxy fence and a CTA fence, then this thread's arrive
+          fence_async_global();
+          __threadfence_block();
           mbar_arrive(&bars.diag_done[it & 1]);
         }
       }
@@ -710,12 +734,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 4, 0);
       tc_fence_after();
       if (!TREE && p.step > 0) {
-        if (TTT_FWD_FUSED_DIAG) mbar_wait(&bars.diag_done[it & 1], (it >> 1) & 1);  // O_d rows in out, A_d in lse
+        // O_d tile in the Q buffer (the producer loaded it after diag_done); A_d in the lse rows
+        if (TTT_FWD_FUSED_DIAG) mbar_wait(&bars.od, it & 1);
       }
       const float A_d = !has_diag ? -INFINITY : __ldcg(p.lse + lse_idx);  // log2 units, from the diagonal pass
-      // out is staged in this slot's V stage (free: every PV of the item is complete, the next item's
-      // V loads wait for stg_free) and TMA-stored per 64-column box; out_lo is stored from registers
+      // O_d is read from this slot's Q tile (SW128 boxes), out is staged in this slot's V stage and
+      // out_lo in place of O_d in the Q tile; all free: every MMA of the item is complete, the
+      // diagonal warps are done, and the next item's Q / V loads wait for stg_free
       uint8_t* st_hi = sV + slot * TB;
+      uint8_t* st_q = sQ + slot * TB;
       const uint32_t sw = (uint32_t)(row & 7);
       const float m_f = fmaxf(m_run, A_d);
       const float alpha = (TREE && m_f == -INFINITY) ? 0.f : ex2(m_run - m_f);
@@ -725,9 +752,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // the combine pass)
       const float inv_l = (TREE && l_f == 0.f) ? 0.f : 1.f / l_f;
       const float a_n = alpha * inv_l, b_n = beta * inv_l;
-      const size_t grow = (((size_t)b * p.L + r) * p.Hq + h) * D;  // TTT: this thread's out / out_lo row
-      const __nv_bfloat16* od_row = reinterpret_cast<const __nv_bfloat16*>(p.out) + grow;
-      __nv_bfloat16* lo_row = reinterpret_cast<__nv_bfloat16*>(p.out_lo) + grow;
 #pragma unroll
       for (int bx = 0; bx < NBOX; ++bx) {
         uint32_t o[64];
@@ -739,7 +763,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(o[q4 * 8 + e]) * a_n;
           const uint32_t soff = (uint32_t)bx * 16384u + (uint32_t)row * 128u + ((((uint32_t)q4) ^ sw) << 4);
           if (has_diag && !(TTT_FWD_PROBE & 2)) {
-            const uint4 odv = __ldcg(reinterpret_cast<const uint4*>(od_row + bx * 64 + q4 * 8));
+            const uint4 odv = *reinterpret_cast<const uint4*>(st_q + soff);
             const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&odv);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -762,7 +786,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hi[e]));
               lo[e] = pack_bf16(v[2 * e] - hf.x, v[2 * e + 1] - hf.y);
             }
-            *reinterpret_cast<uint4*>(lo_row + bx * 64 + q4 * 8) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            *reinterpret_cast<uint4*>(st_q + soff) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
           }
         }
         fence_async_smem();
@@ -773,6 +797,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               tma_store_4d(&maps.out, st_hi + bx * 16384 + (kk & 1) * 8192, bx * 64, h0 + kk, 0, bst);
           } else {
             tma_store_4d(&maps.out, st_hi + bx * 16384, bx * 64, h, qt * kTile, bst);
+            if (p.out_lo) tma_store_4d(&maps.out_lo, st_q + bx * 16384, bx * 64, h, qt * kTile, b);
           }
           bulk_commit();
         }
