@@ -1079,7 +1079,12 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
      // cost (measured traces); a (b, g) group's K / V: 4 B per kv element
     std::vector<double> len(p.nqt);
     for (int r = 0; r < p.nqt; ++r) len[r] = (double)(p.nqt - r) * 3.3;
-    p.order_batch = pick_order_batch(p.B * p.Hkv, p.nqt, (p.G + 1) / 2, len.data(), 7.0, (double)p.L * D * 4);
+    // persistent kernel: items in one globally longest-first batch, so the snake assignment over the
+    // CTAs is near LPT-balanced (simulated: within ~1-2% of the ideal makespan vs 5-20% for batched
+    // orders); the working set of one q-tile level is every (b, g) group's K / V (64 MB at the Llama shape)
+    p.order_batch = TTT_FWD_PERSIST ? p.B * p.Hkv
+                                    : pick_order_batch(p.B * p.Hkv, p.nqt, (p.G + 1) / 2, len.data(), 7.0,
+                                                       (double)p.L * D * 4);
   }
   const int smem = fwd_smem_bytes(D);
   static std::atomic<unsigned long long> attr_done{0};
