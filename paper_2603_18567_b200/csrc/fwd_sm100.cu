@@ -569,6 +569,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const bool has1 = w.has1;
       const int cnt = slot ? c1 : gt;              // this slot's tile counter before the item
       const int ocnt = slot ? n1 : it;             // this slot's item counter
+      const int gt0 = gt;                          // K / V ring position of the item's first tile
       gt += nkv;
       if (has1) {
         c1 += nkv;
@@ -728,8 +729,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const size_t lse_idx = ((size_t)bst * p.Hq + h) * p.L + r;
       const bool has_diag = !TREE && (r < T) && (p.step > 0);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, 0);
-      // every PV of the item (both slots): the out staging goes into the V stages
-      if (has1) mbar_wait(&bars.o_full[1], (n1 - 1) & 1);  // (n1 counts this item already)
       mbar_wait(&bars.o_full[slot], ocnt & 1);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 4, 0);
       tc_fence_after();
@@ -741,7 +740,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // O_d is read from this slot's Q tile (SW128 boxes), out is staged in this slot's V stage and
       // out_lo in place of O_d in the Q tile; all free: every MMA of the item is complete, the
       // diagonal warps are done, and the next item's Q / V loads wait for stg_free
-      uint8_t* st_hi = sV + slot * TB;
+      // slot 1 stages in the V stage of the item's last tile (free at o_full[1]), slot 0 in the other one,
+      // last read by tile nkv - 2 (or an earlier item), whose PVs o_full[0] covers, so neither slot
+      // waits for the other's last PV
+      uint8_t* st_hi = sV + ((gt0 + nkv - (slot == 0 ? 0 : 1)) & 1) * TB;
       uint8_t* st_q = sQ + slot * TB;
       const uint32_t sw = (uint32_t)(row & 7);
       const float m_f = fmaxf(m_run, A_d);
