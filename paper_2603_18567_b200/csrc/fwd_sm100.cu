@@ -60,12 +60,6 @@ constexpr int kFwdThreads = 512;
 #ifndef TTT_FWD_DIAG_MODE
 #define TTT_FWD_DIAG_MODE 0  // dev timing probes only: 1 = diagonal warps skip the math, 2 = skip the loads
 #endif
-#ifndef TTT_FWD_PROBE
-#define TTT_FWD_PROBE 0  // dev timing probes only (wrong results): 1 = skip out_lo, 2 = skip the O_d loads
-#endif
-#ifndef TTT_FWD_PERSIST
-#define TTT_FWD_PERSIST 1  // dev A/B: 0 = one item per CTA (the kernel's item loop then runs once)
-#endif
 #ifndef TTT_FWD_FUSED_DIAG
 #define TTT_FWD_FUSED_DIAG 1  // 0: dev A/B build with round 1's separate ttt_fwd_diag_kernel
 #endif
@@ -79,14 +73,11 @@ struct FwdBars {
   uint64_t q;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
   uint64_t s_full[2], p_lo[2], p_hi[2], o_full[2];  // P published in two 64-column halves
-  uint64_t s_done;       // the item's S MMAs complete
-  uint64_t od;           // the item's diagonal partial O_d landed in the Q tiles
-  uint64_t stg_free[2];  // a slot's epilogue is done with the Q tile / V stage it staged in
+  uint64_t s_done, od;  // all S MMAs complete (Q / K smem free); diagonal partial tile landed
   uint64_t dg_full[kDgStages], dg_empty[kDgStages];  // diagonal K_i / V_i ring
-  // the item's diagonal partial (O_d rows, A_d) complete; by item parity, so the diagonal warps of
-  // item it+1 cannot complete a phase the epilogue of item it is still to wait for
-  uint64_t diag_done[2];
+  uint64_t diag_done;                                // diagonal partial (O_d rows, A_d) complete
   uint32_t tmem_base;
+  float a_d[2][kTile];  // A_d = log2 sum_i 2^t_i per (head slot, row), from the diagonal warps
 };
 
 // TREE = true: tree-attention verification (ttt_tree_attn_fwd) on the
@@ -103,7 +94,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;           // 2 tiles (head slots)
   uint8_t* sK = smem + 2 * TB;  // 2 stages
-  uint8_t* sV = smem + 4 * TB;  // 2 stages; between items also the out staging of the epilogue
+  uint8_t* sV = smem + 4 * TB;  // 2 stages
   constexpr int DGB = kDgRows * 128;       // 16 rows x 64 columns of bf16 (a tensor's block is NBOX x DGB)
   constexpr int DGS = 2 * NBOX * DGB;      // one stage: K_i and V_i rows of a 16-row block
   uint8_t* sDg = smem + 6 * TB;            // diagonal ring, kDgStages stages
@@ -115,61 +106,51 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     g_ttt_trace[1][kTraceCap - 2] = (clock64() << 20) | (9ull << 12);  // CTA start
 #endif
 
-  // ---- work items. TTT: (b, g, head pair, q tile) in batched longest-first order ((b, g) groups
-  // in batches of p.order_batch so a kv head's K / V stay hot in L2, q tile slowest inside a batch);
-  // the kernel is persistent: CTA c walks items c, 2G-1-c, 2G+c, ... (snake order over the sorted
-  // list, G = gridDim.x), so the next item's Q / K loads and first S MMAs run under the current
-  // item's last tile and epilogue, and TMEM / barriers are set up once. TREE: one item per CTA.
-  // TTT: two heads per item (one per slot). TREE: four heads (n <= 64 tree rows each; slot s holds
+  // ---- work decode: (b, g)-major so one kv head's K/V stay hot in L2; within
+  // it the longest (highest) q tiles first; head pairs of a tile adjacent ----
+  // TTT: two heads per CTA (one per slot). TREE: four heads (n <= 64 tree rows each; slot s holds
   // heads 4 hp + 2 s in rows [0, 64) and 4 hp + 2 s + 1 in rows [64, 128)), so no row is padding.
   const int npairs = TREE ? (p.G + 3) >> 2 : (p.G + 1) >> 1;
-  const int n_items = TREE ? (int)gridDim.x : p.nqt * p.B * p.Hkv * npairs;
-  auto item_of = [&](int it) -> int {
-    if constexpr (TREE) return it == 0 ? (int)blockIdx.x : -1;
-    const int G = (int)gridDim.x;
-    const int k = it * G + ((it & 1) ? (G - 1 - (int)blockIdx.x) : (int)blockIdx.x);
-    return k < n_items ? k : -1;
-  };
-  struct Item {
-    int qt, g, b, h0, nheads, T, kvt0, nkv, bst;
-    bool has1;
-  };
-  auto decode = [&](int k, Item& w) {
-    const int hp = k % npairs;
-    const int t_ = k / npairs;
-    int split = 0;
-    if constexpr (TREE) {  // (split of the context, b, g); the q tile is the tree
-      const int gi = t_ % (p.B * p.Hkv);
-      split = t_ / (p.B * p.Hkv);
-      w.qt = 0;
-      w.g = gi % p.Hkv;
-      w.b = gi / p.Hkv;
-    } else {
-      const int ngrp = p.B * p.Hkv, bsz = p.order_batch * p.nqt;
-      const int bat = t_ / bsz, gbase = bat * p.order_batch;
-      const int gb = min(p.order_batch, ngrp - gbase), rr = t_ - bat * bsz;
-      w.qt = p.nqt - 1 - rr / gb;
-      const int gi = gbase + rr % gb;
-      w.g = gi % p.Hkv;
-      w.b = gi / p.Hkv;
-    }
-    w.h0 = w.g * p.G + (TREE ? 4 : 2) * hp;
-    w.nheads = TREE ? min(4, p.G - 4 * hp) : min(2, p.G - 2 * hp);
-    w.has1 = TREE ? w.nheads > 2 : w.nheads > 1;
-    w.T = p.seq_lens[w.b];  // TREE: prefix length P_b
-    // TREE: kv tiles [kvt0, kvt0 + nkv) of this context split (balanced, never empty: host keeps
-    // splits <= tiles); the tree result of a split goes to partial buffers merged by a combine pass
-    if constexpr (TREE) {
-      const int tiles = (w.T + p.tree_n + kTile - 1) / kTile;
-      w.kvt0 = split * tiles / p.tree_splits;
-      w.nkv = (split + 1) * tiles / p.tree_splits - w.kvt0;
-    } else {
-      w.kvt0 = 0;
-      w.nkv = min(w.qt + 1, (w.T + kTile - 1) / kTile);  // BlockMask: skip k0 > q0+127 and k0 >= T
-    }
-    w.bst = TREE ? split * p.B + w.b : w.b;  // batch index of the item's out / lse rows
-  };
-  const bool diag_on = TTT_FWD_FUSED_DIAG && !TREE && p.step > 0;
+  const int hp = (int)blockIdx.x % npairs;
+  const int t_ = (int)blockIdx.x / npairs;
+  int qt, g, b, split = 0;
+  if constexpr (TREE) {  // (split of the context, b, g); the q tile is the tree
+    const int gi = t_ % (p.B * p.Hkv);
+    split = t_ / (p.B * p.Hkv);
+    qt = 0;
+    g = gi % p.Hkv;
+    b = gi / p.Hkv;
+  } else {
+#ifdef TTT_ORDER_GROUP
+    qt = p.nqt - 1 - t_ % p.nqt;
+    g = (t_ / p.nqt) % p.Hkv;
+    b = t_ / (p.nqt * p.Hkv);
+#else
+    // batched longest-first: (b, g) groups in batches of p.order_batch, q tile slowest inside a batch
+    const int ngrp = p.B * p.Hkv, bsz = p.order_batch * p.nqt;
+    const int bat = t_ / bsz, gbase = bat * p.order_batch;
+    const int gb = min(p.order_batch, ngrp - gbase), rr = t_ - bat * bsz;
+    qt = p.nqt - 1 - rr / gb;
+    const int gi = gbase + rr % gb;
+    g = gi % p.Hkv;
+    b = gi / p.Hkv;
+#endif
+  }
+  const int h0 = g * p.G + (TREE ? 4 : 2) * hp;
+  const int nheads = TREE ? min(4, p.G - 4 * hp) : min(2, p.G - 2 * hp);  // heads of this CTA
+  const bool has1 = TREE ? nheads > 2 : nheads > 1;
+  const int T = p.seq_lens[b];  // TREE: prefix length P_b
+  // TREE: kv tiles [kvt0, kvt0 + nkv) of this context split (balanced, never empty: host keeps
+  // splits <= tiles); the tree result of a split goes to partial buffers merged by a combine pass
+  int kvt0 = 0, nkv;
+  if constexpr (TREE) {
+    const int tiles = (T + p.tree_n + kTile - 1) / kTile;
+    kvt0 = split * tiles / p.tree_splits;
+    nkv = (split + 1) * tiles / p.tree_splits - kvt0;
+  } else {
+    nkv = min(qt + 1, (T + kTile - 1) / kTile);  // BlockMask: skip k0 > q0+127 and k0 >= T
+  }
+  const int bst = TREE ? split * p.B + b : b;  // batch index of this CTA's out / lse rows
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.q, 1);
@@ -182,7 +163,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bars.p_lo[i], 128);
       mbar_init(&bars.p_hi[i], 128);
       mbar_init(&bars.o_full[i], 1);
-      mbar_init(&bars.stg_free[i], 1);
     }
     mbar_init(&bars.s_done, 1);
     mbar_init(&bars.od, 1);
@@ -190,8 +170,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bars.dg_full[i], 1);
       mbar_init(&bars.dg_empty[i], 4);  // the four diagonal compute warps
     }
-    mbar_init(&bars.diag_done[0], 128);  // every thread of the diagonal warps (its reads of the Q tile
-    mbar_init(&bars.diag_done[1], 128);  // and writes of the O_d / A_d rows precede its own arrive)
+    mbar_init(&bars.diag_done, 128);  // every thread of the diagonal warps arrives after its own reads / writes
     fence_mbar_init();
   }
   if (warp == 9) {
@@ -209,81 +188,53 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tma_prefetch_desc(&maps.q);
       tma_prefetch_desc(&maps.k);
       tma_prefetch_desc(&maps.v);
-      int gt = 0;                // K / V tiles loaded so far (ring position)
-      int n1 = 0;                // items with a slot-1 head so far
-      bool prev_has1 = false;
-      auto load_k = [&](const Item& w, int n) {
-        const int gi = gt + n, st = gi & 1, ph = (gi >> 1) & 1;
+      if constexpr (TREE) {  // 64-row boxes: head h0 + k -> slot k / 2, rows 64 (k % 2) ..
+        mbar_expect_tx(&bars.q, nheads * (TB / 2));
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          for (int k = 0; k < nheads; ++k)
+            tma_load_4d(sQ + (k >> 1) * TB + bx * 16384 + (k & 1) * 8192, &maps.q, &bars.q, bx * 64, h0 + k, 0, b);
+      } else {
+        mbar_expect_tx(&bars.q, (has1 ? 2 : 1) * TB);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx) {
+          tma_load_4d(sQ + bx * 16384, &maps.q, &bars.q, bx * 64, h0, qt * kTile, b);
+          if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.q, &bars.q, bx * 64, h0 + 1, qt * kTile, b);
+        }
+      }
+      for (int n = 0; n < nkv; ++n) {
+        const int st = n & 1, ph = (n >> 1) & 1;
         mbar_wait(&bars.k_empty[st], ph ^ 1);
         mbar_expect_tx(&bars.k_full[st], TB);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, w.g, (w.kvt0 + n) * kTile, w.b);
-      };
-      auto load_v = [&](const Item& w, int n) {
-        const int gi = gt + n, st = gi & 1, ph = (gi >> 1) & 1;
+          tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, g, (kvt0 + n) * kTile, b);
         mbar_wait(&bars.v_empty[st], ph ^ 1);
         mbar_expect_tx(&bars.v_full[st], TB);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, w.g, (w.kvt0 + n) * kTile, w.b);
-      };
-      for (int it = 0;; ++it) {
-        const int k = item_of(it);
-        if (k < 0) break;
-        Item w;
-        decode(k, w);
-        // K_0 tile 0 first: its stage is free once the previous item's S MMAs are done, before the
-        // previous epilogue ends
-        load_k(w, 0);
-        if (it > 0) {  // the previous epilogue is done with the Q tiles (O_d, out_lo staging) and the V
-                       // stages (out staging): its stores have read them
-          mbar_wait(&bars.stg_free[0], (it - 1) & 1);
-          if (prev_has1) mbar_wait(&bars.stg_free[1], (n1 - 1) & 1);
-        }
-        if constexpr (TREE) {  // 64-row boxes: head h0 + k -> slot k / 2, rows 64 (k % 2) ..
-          mbar_expect_tx(&bars.q, w.nheads * (TB / 2));
+          tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, (kvt0 + n) * kTile, b);
+      }
+      if (!TREE && p.step > 0) {  // diagonal partial of the two heads into the Q tiles once no S MMA
+                                  // reads them and the diagonal warps have written it
+        mbar_wait(&bars.s_done, 0);
+        if (TTT_FWD_FUSED_DIAG) mbar_wait(&bars.diag_done, 0);
+        mbar_expect_tx(&bars.od, (has1 ? 2 : 1) * TB);
 #pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx)
-            for (int kk = 0; kk < w.nheads; ++kk)
-              tma_load_4d(sQ + (kk >> 1) * TB + bx * 16384 + (kk & 1) * 8192, &maps.q, &bars.q, bx * 64, w.h0 + kk,
-                          0, w.b);
-        } else {
-          mbar_expect_tx(&bars.q, (w.has1 ? 2 : 1) * TB);
-#pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx) {
-            tma_load_4d(sQ + bx * 16384, &maps.q, &bars.q, bx * 64, w.h0, w.qt * kTile, w.b);
-            if (w.has1) tma_load_4d(sQ + TB + bx * 16384, &maps.q, &bars.q, bx * 64, w.h0 + 1, w.qt * kTile, w.b);
-          }
+        for (int bx = 0; bx < NBOX; ++bx) {
+          tma_load_4d(sQ + bx * 16384, &maps.out, &bars.od, bx * 64, h0, qt * kTile, b);
+          if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.out, &bars.od, bx * 64, h0 + 1, qt * kTile, b);
         }
-        load_v(w, 0);
-        for (int n = 1; n < w.nkv; ++n) {
-          load_k(w, n);
-          load_v(w, n);
-        }
-        if (diag_on) {  // the diagonal partial O_d of the two heads into the Q tiles, once no S MMA and
-                        // no diagonal warp reads them
-          mbar_wait(&bars.s_done, it & 1);
-          mbar_wait(&bars.diag_done[it & 1], (it >> 1) & 1);
-          mbar_expect_tx(&bars.od, (w.has1 ? 2 : 1) * TB);
-#pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx) {
-            tma_load_4d(sQ + bx * 16384, &maps.out, &bars.od, bx * 64, w.h0, w.qt * kTile, w.b);
-            if (w.has1) tma_load_4d(sQ + TB + bx * 16384, &maps.out, &bars.od, bx * 64, w.h0 + 1, w.qt * kTile, w.b);
-          }
-        }
-        gt += w.nkv;
-        prev_has1 = w.has1;
-        n1 += w.has1 ? 1 : 0;
       }
     }
   } else if (warp == 9) {
     // ================= MMA issuer (whole warp, converged; elect.sync inside each issue) =================
-    constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);  // S = Q K^T, both K-major
-    constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);     // O += P V, V MN-major
-    const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ), 16, 1024), dK0 = sdesc_sw128(smem_u32(sK), 16, 1024);
-    const uint64_t dV0 = sdesc_sw128(smem_u32(sV), 16384, 1024);
-    TTT_TRACE_DECL(0);
+    {
+      constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);  // S = Q K^T, both K-major
+      constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);     // O += P V, V MN-major
+      const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ), 16, 1024), dK0 = sdesc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t dV0 = sdesc_sw128(smem_u32(sV), 16384, 1024);
+      TTT_TRACE_DECL(0);
       auto issue_S = [&](int slot, int kst) {
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
@@ -307,33 +258,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int ks = 0; ks < 4; ++ks)
           umma_ts_e(tbase + 256 + slot * 128, tbase + slot * 128 + ks * 8, sdesc_add(dV0, vst * TB + ks * 2048), idO, 1u);
       };
-    int gt = 0, c1 = 0, n1 = 0;  // tiles so far (slot 0 = ring position), slot-1 tiles, slot-1 items
-    for (int it = 0;; ++it) {
-      const int k = item_of(it);
-      if (k < 0) break;
-      Item w;
-      decode(k, w);
-      const bool has1 = w.has1;
-      mbar_wait(&bars.q, it & 1);
-      mbar_wait(&bars.k_full[gt & 1], (gt >> 1) & 1);
+      mbar_wait(&bars.q, 0);
+      mbar_wait(&bars.k_full[0], 0);
       TTT_TRACE_EV(0, 8, 0);
       tc_fence_after();
-      issue_S(0, gt & 1);
+      issue_S(0, 0);
       umma_commit_e(&bars.s_full[0]);
       if (has1) {
-        issue_S(1, gt & 1);
+        issue_S(1, 0);
         umma_commit_e(&bars.s_full[1]);
       }
-      umma_commit_e(&bars.k_empty[gt & 1]);
-      for (int n = 0; n < w.nkv; ++n) {
-        const int g0 = gt + n, g1 = c1 + n;  // the slots' tile counters (barrier phases)
-        const int vst = g0 & 1, vph = (g0 >> 1) & 1;
-        const bool more = n + 1 < w.nkv;
-        const int kst = (g0 + 1) & 1, kph = ((g0 + 1) >> 1) & 1;
+      umma_commit_e(&bars.k_empty[0]);
+      for (int n = 0; n < nkv; ++n) {
+        const int vst = n & 1, vph = (n >> 1) & 1;
+        const bool more = n + 1 < nkv;
+        const int kst = (n + 1) & 1, kph = ((n + 1) >> 1) & 1;
         if (!more) umma_commit_e(&bars.s_done);
         mbar_wait(&bars.v_full[vst], vph);
         TTT_TRACE_EV(0, 1, n);
-        issue_PV(0, vst, n > 0, g0);
+        issue_PV(0, vst, n > 0, n);
         TTT_TRACE_EV(0, 2, n);
         if (more) {
           mbar_wait(&bars.k_full[kst], kph);
@@ -344,7 +287,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           umma_commit_e(&bars.o_full[0]);
         }
         if (has1) {
-          issue_PV(1, vst, n > 0, g1);
+          issue_PV(1, vst, n > 0, n);
           TTT_TRACE_EV(0, 3, n);
           umma_commit_e(&bars.v_empty[vst]);
           if (more) {
@@ -359,46 +302,37 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (more) umma_commit_e(&bars.k_empty[kst]);
         }
       }
-      gt += w.nkv;
-      if (has1) {
-        c1 += w.nkv;
-        ++n1;
-      }
     }
   } else if (warp >= 10) {
     // ================= diagonal fold (warps 10-13) + its TMA producer (warp 14) =================
-    if (diag_on) {
+
+    if (TTT_FWD_FUSED_DIAG && !TREE && p.step > 0) {
       const int j = p.step;
+      // 16-row blocks of this q tile holding at least one row r < T_b
+      const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
       if (warp == 14) {
         if (lane == 0) {
 #ifdef TTT_TRACE
           int trace_n_3 = 32768;
 #endif
           int n = 0;
-          for (int it = 0;; ++it) {
-            const int k = item_of(it);
-            if (k < 0) break;
-            Item w;
-            decode(k, w);
-            // 16-row blocks of this q tile holding at least one row r < T_b
-            const int nrb = w.T > w.qt * kTile ? min(kTile / kDgRows, (w.T - w.qt * kTile + kDgRows - 1) / kDgRows) : 0;
-            for (int rb = 0; rb < nrb; ++rb)
-              for (int i = 0; i < j; ++i, ++n) {
-                const int st = n % kDgStages, use = n / kDgStages;
-                mbar_wait(&bars.dg_empty[st], (use & 1) ^ 1);
-                if (TTT_FWD_DIAG_MODE == 2) {  // dev probe: no loads
-                  mbar_arrive(&bars.dg_full[st]);
-                  continue;
-                }
-                mbar_expect_tx(&bars.dg_full[st], DGS);
-                uint8_t* base = sDg + st * DGS;
-                const int r0 = w.qt * kTile + rb * kDgRows;
-                // one box per tensor: 16 rows x D columns, no swizzle (rows of D x 2 bytes)
-                tma_load_4d(base, &maps.kd[i], &bars.dg_full[st], 0, w.g, r0, w.b);
-                tma_load_4d(base + NBOX * DGB, &maps.vd[i], &bars.dg_full[st], 0, w.g, r0, w.b);
-                TTT_TRACE_EV(3, 3, n);
+          for (int rb = 0; rb < nrb; ++rb)
+            for (int i = 0; i < j; ++i, ++n) {
+              const int st = n % kDgStages, use = n / kDgStages;
+              mbar_wait(&bars.dg_empty[st], (use & 1) ^ 1);
+              if (TTT_FWD_DIAG_MODE == 2) {  // dev probe: no loads
+                mbar_arrive(&bars.dg_full[st]);
+                continue;
               }
-          }
+              mbar_expect_tx(&bars.dg_full[st], DGS);
+              uint8_t* base = sDg + st * DGS;
+              const int r0 = qt * kTile + rb * kDgRows;
+#pragma unroll
+              // one box per tensor: 16 rows x D columns, no swizzle (rows of D x 2 bytes)
+              tma_load_4d(base, &maps.kd[i], &bars.dg_full[st], 0, g, r0, b);
+              tma_load_4d(base + NBOX * DGB, &maps.vd[i], &bars.dg_full[st], 0, g, r0, b);
+              TTT_TRACE_EV(3, 3, n);
+            }
         }
       } else if (warp < 14) {
         // thread layout: 8 lanes per row (lane k = lane & 7 owns columns 8k..8k+7 of every 64-column
@@ -407,40 +341,32 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int dw = warp - 10, k8 = lane & 7;
         const int srow = dw * 4 + (lane >> 3);  // row within a 16-row block
         const float sl2 = p.scale_log2;
+        mbar_wait(&bars.q, 0);  // q rows are read from the Q tiles (shared with the S MMAs, read-only)
         TTT_TRACE_DECL(3);
+        if (threadIdx.x == 320) TTT_TRACE_EV(3, 4, 0);
         int n = 0;
-        for (int it = 0;; ++it) {
-          const int k = item_of(it);
-          if (k < 0) break;
-          Item w;
-          decode(k, w);
-          const int qt = w.qt, T = w.T, b = w.b, h0 = w.h0;
-          const bool has1 = w.has1;
-          const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
-          mbar_wait(&bars.q, it & 1);  // q rows are read from the Q tiles (shared with the S MMAs, read-only)
-          if (threadIdx.x == 320) TTT_TRACE_EV(3, 4, 0);
-          for (int rb = 0; rb < nrb; ++rb) {
-            const int row = rb * kDgRows + srow;
-            const int r = qt * kTile + row;
-            float qf[2][E], acc[2][E], m[2], l[2];
+        for (int rb = 0; rb < nrb; ++rb) {
+          const int row = rb * kDgRows + srow;
+          const int r = qt * kTile + row;
+          float qf[2][E], acc[2][E], m[2], l[2];
 #pragma unroll
-            for (int hs = 0; hs < 2; ++hs) {
-              m[hs] = -INFINITY;
-              l[hs] = 0.f;
+          for (int hs = 0; hs < 2; ++hs) {
+            m[hs] = -INFINITY;
+            l[hs] = 0.f;
 #pragma unroll
-              for (int bx = 0; bx < NBOX; ++bx) {
-                const uint4 u = lds128(smem_u32(sQ + hs * TB + bx * 16384) + sw128_off(row, k8));
-                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+            for (int bx = 0; bx < NBOX; ++bx) {
+              const uint4 u = lds128(smem_u32(sQ + hs * TB + bx * 16384) + sw128_off(row, k8));
+              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
-                  qf[hs][bx * 8 + 2 * e] = f.x * sl2;
-                  qf[hs][bx * 8 + 2 * e + 1] = f.y * sl2;
-                  acc[hs][bx * 8 + 2 * e] = 0.f;
-                  acc[hs][bx * 8 + 2 * e + 1] = 0.f;
-                }
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+                qf[hs][bx * 8 + 2 * e] = f.x * sl2;
+                qf[hs][bx * 8 + 2 * e + 1] = f.y * sl2;
+                acc[hs][bx * 8 + 2 * e] = 0.f;
+                acc[hs][bx * 8 + 2 * e + 1] = 0.f;
               }
             }
+          }
           // Stages two at a time (i, i + 1): their dot products, shuffles and exps are independent,
           // and the running max only moves (a warp-uniform rescale) when a score exceeds it by
           // 2^8 — the j-long chain of an exact online softmax was the fused pass's critical path.
@@ -517,7 +443,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               }
             }
           }
-          // O_d (normalised, bf16) -> the out rows (read back by the epilogue), A_d -> shared memory
+          // O_d (normalised, bf16) -> the out rows (staging; read back by TMA), A_d -> shared memory
           if (r < T) {
 #pragma unroll
             for (int hs = 0; hs < 2; ++hs) {
@@ -534,60 +460,45 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                   w.w = pack_bf16(acc[hs][bx * 8 + 6] * inv, acc[hs][bx * 8 + 7] * inv);
                   *reinterpret_cast<uint4*>(orow + bx * 64 + k8 * 8) = w;
                 }
-                if (k8 == 0) p.lse[((size_t)b * p.Hq + h0 + hs) * p.L + r] = m[hs] + log2f(l[hs]);  // A_d (log2)
+                if (k8 == 0) bars.a_d[hs][row] = m[hs] + log2f(l[hs]);
               }
             }
           }
         }
-          if (threadIdx.x == 320) TTT_TRACE_EV(3, 2, n);
-          // the O_d rows (generic-proxy writes) are read back by the producer's TMA (async proxy) and
-          // A_d by the epilogue: a proxy fence and a CTA fence, then this thread's arrive
-          fence_async_global();
-          __threadfence_block();
-          mbar_arrive(&bars.diag_done[it & 1]);
-        }
+        if (threadIdx.x == 320) TTT_TRACE_EV(3, 2, n);
+        fence_async_global();  // the out rows are read back by the producer's TMA (async proxy)
+        __threadfence_block();
+        mbar_arrive(&bars.diag_done);
       }
     }
   } else {
     // ================= softmax + epilogue (warps 0-7) =================
     const int slot = warp >> 2;
     const int wq = warp & 3;
-    const int row = wq * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const uint32_t tS = tbase + lane_off + slot * 128;
-    const uint32_t tO = tbase + lane_off + 256 + slot * 128;
-    const float sl2 = p.scale_log2;
-    TTT_TRACE_DECL(1);
-    TTT_TRACE_DECL(2);
-    int gt = 0, c1 = 0, n1 = 0;  // as in the MMA warp: barrier phases of the slots
-    for (int it = 0;; ++it) {
-      const int k = item_of(it);
-      if (k < 0) break;
-      Item w;
-      decode(k, w);
-      const int qt = w.qt, T = w.T, b = w.b, h0 = w.h0, nheads = w.nheads, nkv = w.nkv, kvt0 = w.kvt0, bst = w.bst;
-      const bool has1 = w.has1;
-      const int cnt = slot ? c1 : gt;              // this slot's tile counter before the item
-      const int ocnt = slot ? n1 : it;             // this slot's item counter
-      const int gt0 = gt;                          // K / V ring position of the item's first tile
-      gt += nkv;
-      if (has1) {
-        c1 += nkv;
-        ++n1;
-      }
-      if (slot == 1 && !has1) continue;
+    if (slot == 0 || has1) {
+      const int row = wq * 32 + lane;
       // TREE: row = 64 (head within the slot) + tree node
       const int r = TREE ? (row & 63) : qt * kTile + row;
       const int h = TREE ? h0 + 2 * slot + (row >> 6) : h0 + slot;
+      const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+      const uint32_t tS = tbase + lane_off + slot * 128;
+      const uint32_t tO = tbase + lane_off + 256 + slot * 128;
+      const float sl2 = p.scale_log2;
       float m_run = -INFINITY, l_run = 0.f;
       // TREE: this row's ancestor-or-self mask (rows >= n are tile padding)
       const bool tree_row = TREE && r < p.tree_n && (2 * slot + (row >> 6)) < nheads;
       const unsigned long long tree_am = tree_row ? p.tree_mask[(size_t)b * p.tree_n + r] : 0ull;
+      TTT_TRACE_DECL(1);
+      TTT_TRACE_DECL(2);
       for (int n = 0; n < nkv; ++n) {
-        mbar_wait(&bars.s_full[slot], (cnt + n) & 1);
+        mbar_wait(&bars.s_full[slot], n & 1);
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 1, n);
         if (threadIdx.x == 128) TTT_TRACE_EV(2, 1, n);
         tc_fence_after();
+        // S is read in two 64-column halves (64 registers each, so 16 warps fit the register file):
+        // keys [0,64) for their max only, keys [64,128) kept for P; P(keys 64..127) is written over
+        // the already-read S columns [96,128) and published first (p_hi), then keys [0,64) are
+        // re-read and P(keys 0..63) written over columns [0,32) (p_lo).
         uint32_t raw[64];
         const int kv0 = (kvt0 + n) * kTile;
         const bool partial = TREE ? (kv0 + kTile > T) : ((n == qt) || (kv0 + kTile > T));
@@ -724,27 +635,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       // ---- epilogue: merge the diagonal partial, normalise, store ----
       // The j diagonal keys of row r (Alg. 1 "concat s_i") were reduced
-      // by the diagonal warps into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum, in the out rows);
-      // the merge is the same online-softmax update as one more "tile".
+      // by the diagonal warps into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum); the
+      // merge is the same online-softmax update as one more "tile".
       const size_t lse_idx = ((size_t)bst * p.Hq + h) * p.L + r;
       const bool has_diag = !TREE && (r < T) && (p.step > 0);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, 0);
-      mbar_wait(&bars.o_full[slot], ocnt & 1);
+      mbar_wait(&bars.o_full[slot], 0);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 4, 0);
       tc_fence_after();
       if (!TREE && p.step > 0) {
-        // O_d tile in the Q buffer (the producer loaded it after diag_done); A_d in the lse rows
-        if (TTT_FWD_FUSED_DIAG) mbar_wait(&bars.od, it & 1);
+        if (TTT_FWD_FUSED_DIAG) mbar_wait(&bars.diag_done, 0);  // A_d in shared memory
+        mbar_wait(&bars.od, 0);                                 // O_d tile in the Q buffer
       }
-      const float A_d = !has_diag ? -INFINITY : __ldcg(p.lse + lse_idx);  // log2 units, from the diagonal pass
-      // O_d is read from this slot's Q tile (SW128 boxes), out is staged in this slot's V stage and
-      // out_lo in place of O_d in the Q tile; all free: every MMA of the item is complete, the
-      // diagonal warps are done, and the next item's Q / V loads wait for stg_free
-      // slot 1 stages in the V stage of the item's last tile (free at o_full[1]), slot 0 in the other one,
-      // last read by tile nkv - 2 (or an earlier item), whose PVs o_full[0] covers, so neither slot
-      // waits for the other's last PV
-      uint8_t* st_hi = sV + ((gt0 + nkv - (slot == 0 ? 0 : 1)) & 1) * TB;
-      uint8_t* st_q = sQ + slot * TB;
+      const float A_d = !has_diag ? -INFINITY : TTT_FWD_FUSED_DIAG ? bars.a_d[slot][row] : p.lse[lse_idx];
+      // The diagonal partial O_d sits in this slot's Q tile (SW128 boxes); each thread reads its
+      // row there and overwrites it in place with the output, which the TMA store then drains.
+      // out_lo is staged in the K stage of the same index. Both are free: o_full[slot] and
+      // s_done follow every S MMA of the CTA.
+      uint8_t* st_hi = sQ + slot * TB;
+      uint8_t* st_lo = sK + slot * TB;
       const uint32_t sw = (uint32_t)(row & 7);
       const float m_f = fmaxf(m_run, A_d);
       const float alpha = (TREE && m_f == -INFINITY) ? 0.f : ex2(m_run - m_f);
@@ -754,6 +663,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // the combine pass)
       const float inv_l = (TREE && l_f == 0.f) ? 0.f : 1.f / l_f;
       const float a_n = alpha * inv_l, b_n = beta * inv_l;
+      // per 64-column box: one 64-column TMEM load (a single wait), the box written to the staging tile,
+      // then its TMA store issued right away so it drains under the next box's math (measured: the
+      // epilogue, o_full -> CTA end, took ~8k clk with four 32-column load waits and one store at the end)
 #pragma unroll
       for (int bx = 0; bx < NBOX; ++bx) {
         uint32_t o[64];
@@ -764,8 +676,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(o[q4 * 8 + e]) * a_n;
           const uint32_t soff = (uint32_t)bx * 16384u + (uint32_t)row * 128u + ((((uint32_t)q4) ^ sw) << 4);
-          if (has_diag && !(TTT_FWD_PROBE & 2)) {
-            const uint4 odv = *reinterpret_cast<const uint4*>(st_q + soff);
+          if (has_diag) {
+            const uint4 odv = *reinterpret_cast<const uint4*>(st_hi + soff);
             const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&odv);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -774,32 +686,32 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               v[2 * e + 1] = fmaf(b_n, df.y, v[2 * e + 1]);
             }
           }
-          uint4 wv;
-          wv.x = pack_bf16(v[0], v[1]);
-          wv.y = pack_bf16(v[2], v[3]);
-          wv.z = pack_bf16(v[4], v[5]);
-          wv.w = pack_bf16(v[6], v[7]);
-          *reinterpret_cast<uint4*>(st_hi + soff) = wv;
-          if (!TREE && p.out_lo && !(TTT_FWD_PROBE & 1)) {  // residual O - bf16(O): the backward's Delta sees ~16-bit O
-            const uint32_t hi[4] = {wv.x, wv.y, wv.z, wv.w};
+          uint4 w;
+          w.x = pack_bf16(v[0], v[1]);
+          w.y = pack_bf16(v[2], v[3]);
+          w.z = pack_bf16(v[4], v[5]);
+          w.w = pack_bf16(v[6], v[7]);
+          *reinterpret_cast<uint4*>(st_hi + soff) = w;
+          if (p.out_lo) {  // residual O - bf16(O), so the backward's Delta sees ~16-bit O
+            const uint32_t hi[4] = {w.x, w.y, w.z, w.w};
             uint32_t lo[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hi[e]));
               lo[e] = pack_bf16(v[2 * e] - hf.x, v[2 * e + 1] - hf.y);
             }
-            *reinterpret_cast<uint4*>(st_q + soff) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            *reinterpret_cast<uint4*>(st_lo + soff) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
           }
         }
         fence_async_smem();
         named_bar_sync(1 + slot, 128);
         if (row == 0) {
           if constexpr (TREE) {  // the slot's two heads, 64-row boxes
-            for (int kk = 2 * slot; kk < min(2 * slot + 2, nheads); ++kk)
-              tma_store_4d(&maps.out, st_hi + bx * 16384 + (kk & 1) * 8192, bx * 64, h0 + kk, 0, bst);
+            for (int k = 2 * slot; k < min(2 * slot + 2, nheads); ++k)
+              tma_store_4d(&maps.out, st_hi + bx * 16384 + (k & 1) * 8192, bx * 64, h0 + k, 0, bst);
           } else {
             tma_store_4d(&maps.out, st_hi + bx * 16384, bx * 64, h, qt * kTile, bst);
-            if (p.out_lo) tma_store_4d(&maps.out_lo, st_q + bx * 16384, bx * 64, h, qt * kTile, b);
+            if (p.out_lo) tma_store_4d(&maps.out_lo, st_lo + bx * 16384, bx * 64, h, qt * kTile, b);
           }
           bulk_commit();
         }
@@ -808,8 +720,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (!TREE || tree_row) p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
       if (row == 0) {
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 8, 0);
-        bulk_wait_read0();  // the staging must stay valid until the bulk engine has read it
-        mbar_arrive(&bars.stg_free[slot]);
+        bulk_wait_read0();  // smem must stay valid until the bulk engine has read it
       }
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 5, 0);
     }
@@ -1081,12 +992,7 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
      // cost (measured traces); a (b, g) group's K / V: 4 B per kv element
     std::vector<double> len(p.nqt);
     for (int r = 0; r < p.nqt; ++r) len[r] = (double)(p.nqt - r) * 3.3;
-    // persistent kernel: items in one globally longest-first batch, so the snake assignment over the
-    // CTAs is near LPT-balanced (simulated: within ~1-2% of the ideal makespan vs 5-20% for batched
-    // orders); the working set of one q-tile level is every (b, g) group's K / V (64 MB at the Llama shape)
-    p.order_batch = TTT_FWD_PERSIST ? p.B * p.Hkv
-                                    : pick_order_batch(p.B * p.Hkv, p.nqt, (p.G + 1) / 2, len.data(), 7.0,
-                                                       (double)p.L * D * 4);
+    p.order_batch = pick_order_batch(p.B * p.Hkv, p.nqt, (p.G + 1) / 2, len.data(), 7.0, (double)p.L * D * 4);
   }
   const int smem = fwd_smem_bytes(D);
   static std::atomic<unsigned long long> attr_done{0};
@@ -1111,17 +1017,7 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
   (void)dmaps;
 #endif
   const int npairs = (p.G + 1) / 2;
-  const int items = p.nqt * p.B * p.Hkv * npairs;
-  // persistent: one CTA per SM walks the items (snake order, see the kernel)
-  static int sms[64] = {0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
-  int nsm = dev < 64 ? sms[dev] : 0;
-  if (nsm == 0) {
-    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
-    if (dev < 64) sms[dev] = nsm;
-  }
-  const int grid = TTT_FWD_PERSIST ? std::min(items, nsm) : items;
+  const int grid = p.nqt * p.B * p.Hkv * npairs;
   prof_mark(kKindFwdMain, true, st);
   ttt_fwd_sm100_kernel<D, false><<<grid, kFwdThreads, smem, st>>>(p, maps);
   prof_mark(kKindFwdMain, false, st);
