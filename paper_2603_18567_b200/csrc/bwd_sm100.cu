@@ -41,6 +41,9 @@ __device__ unsigned int g_ttt_trace_cta;
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef TTT_BWD_DK_SS
+#define TTT_BWD_DK_SS 1  // dK from the shared-memory dS^T (SS MMA) and dQ issued between dK(a) and dK(b)
+#endif
 #ifndef TTT_BWD_DQ_RED
 #define TTT_BWD_DQ_RED 0  // dev: dQ drain by red.global.add.v4 instead of staged TMA reduce-adds
 #endif
@@ -745,6 +748,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t dQ_kmaj = sdesc_sw128(smem_u32(sQ), 16, 1024), dDO_kmaj = sdesc_sw128(smem_u32(sDO), 16, 1024);
       const uint64_t dDO_mn = sdesc_sw128(smem_u32(sDO), HB / NBOX, 1024), dQ_mn = sdesc_sw128(smem_u32(sQ), 16384, 1024);
       const uint64_t dDS_mn = sdesc_sw128(smem_u32(sDS), 16384, 1024), dK_mn = sdesc_sw128(smem_u32(sK), 16384, 1024);
+      const uint64_t dDS_k = sdesc_sw128(smem_u32(sDS), 16, 1024);  // dS^T boxes as a K-major A operand
       auto kofs = [](int ks, uint32_t box_bytes) { return (uint32_t)((ks >> 2) * box_bytes + (ks & 3) * 32); };
       // S^T = K Q^T for the whole 128-query tile in one N = 128 MMA chain: columns [0,64) are
       // sub-item a, [64,128) sub-item b. (An N = 64 SS MMA is SMEM-read bound at 48 clk per
@@ -771,9 +775,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       };
       auto issue_dK = [&](int qs, int x, bool first) {  // dK += dS^T[x] Q_x
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
+        for (int ks = 0; ks < 4; ++ks) {
+#if TTT_BWD_DK_SS
+          // A = dS^T[x] from shared memory ([kv][q] box x is K-major for M = keys, K = queries), so the
+          // dQ MMA may overwrite the dP^T / dS^T TMEM columns before dK(t, b) runs
+          umma_ss_e(tbase + 384, sdesc_add(dDS_k, x * 16384 + ks * 32), sdesc_add(dQ_mn, qs * TB + (64 * x + 16 * ks) * 128),
+                    idKV, (!first || ks > 0) ? 1u : 0u);
+#else
           umma_ts_e(tbase + 384, tbase + 128 + 64 * x + 8 * ks, sdesc_add(dQ_mn, qs * TB + (64 * x + 16 * ks) * 128),
                     idKV, (!first || ks > 0) ? 1u : 0u);
+#endif
+        }
       };
       // Issue order (program order of this warp = tensor-pipe order):
       //   prologue: S(0) dP(0,a) dP(0,b) dV(0,a) dV(0,b) S(1)
@@ -817,6 +829,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       for (int t = 0; t < n_items; ++t) {
         const int qs = t & 1;
+#if TTT_BWD_DK_SS
+        // dK(t,a) on dS(a); then dQ(t) as soon as dS(b) is in, then dK(t,b): the dQ drain overlaps dK(t,b)
+        // instead of idling the pipe before dP(t+1) (r02g trace: ~0.4k clk per item)
+        mbar_wait(&bars.ds_full[0], t & 1);
+        TTT_TRACE_EV(0, 3, t);
+        tc_fence_after();
+        issue_dK(qs, 0, t == 0);
+        TTT_TRACE_EV(0, 7, t);
+        mbar_wait(&bars.ds_full[1], t & 1);
+        TTT_TRACE_EV(0, 4, t);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          umma_ss_e(tbase + 128, sdesc_add(dDS_mn, ks * 2048), sdesc_add(dK_mn, ks * 2048), idDQ, ks > 0);
+        umma_commit_e(&bars.dq_full);
+        issue_dK(qs, 1, false);
+        TTT_TRACE_EV(0, 8, t);
+        umma_commit_e(&bars.q_empty[qs]);
+        umma_commit_e(&bars.ds_empty);
+#else
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
           mbar_wait(&bars.ds_full[x], t & 1);
@@ -832,6 +864,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           umma_ss_e(tbase + 128, sdesc_add(dDS_mn, ks * 2048), sdesc_add(dK_mn, ks * 2048), idDQ, ks > 0);
         umma_commit_e(&bars.dq_full);
         umma_commit_e(&bars.ds_empty);
+#endif
         TTT_TRACE_EV(0, 9, t);
         if (t + 1 < n_items) {
           mbar_wait(&bars.dq_empty, t & 1);  // dQ(t) drained: the dP^T buffers are free
@@ -959,7 +992,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           pk[2 * e4] = pack_bf16(a0, a1);
           pk[2 * e4 + 1] = pack_bf16(b0, b1);
         }
-        tmem_st16(tdP + cc * 16, pk);  // dS^T (bf16) over this sub-item's already-read dP^T columns
+        if (!TTT_BWD_DK_SS) tmem_st16(tdP + cc * 16, pk);  // dS^T (bf16) over this sub-item's read dP^T columns
         // smem dS: row = key row, q columns [64 x + 32 cc, +32): box x, 8-column chunks 4 cc + e8
         uint8_t* boxp = sDS + x * 16384 + row * 128;
 #pragma unroll
@@ -970,7 +1003,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
       fence_async_smem();
-      tmem_st_wait();
+      if (!TTT_BWD_DK_SS) tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars.ds_full[x]);
       if (threadIdx.x == 128) TTT_TRACE_EV(1, 4, t);
