@@ -42,7 +42,7 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 #ifndef TTT_BWD_DK_SS
-#define TTT_BWD_DK_SS 1  // dK from the shared-memory dS^T (SS MMA) and dQ issued between dK(a) and dK(b)
+#define TTT_BWD_DK_SS 0  // dev: 1 = dK as an SS MMA from the shared-memory dS^T with dQ between dK(a) and dK(b) (r02t: 4.73 vs 4.61 ms, slower)
 #endif
 #ifndef TTT_BWD_DQ_RED
 #define TTT_BWD_DQ_RED 0  // dev: dQ drain by red.global.add.v4 instead of staged TMA reduce-adds
