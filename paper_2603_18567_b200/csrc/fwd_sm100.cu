@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     mbar_init(&bars.od, 1);
     for (int i = 0; i < kDgStages; ++i) {
       mbar_init(&bars.dg_full[i], 1);
-      mbar_init(&bars.dg_empty[i], has1 ? 2 : 1);  // the two head-slot warps of a block
+      mbar_init(&bars.dg_empty[i], 4);  // the four diagonal compute warps
     }
     mbar_init(&bars.diag_done, 128);  // every thread of the diagonal warps arrives after its own reads / writes
     fence_mbar_init();
@@ -310,153 +310,162 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int j = p.step;
       // 16-row blocks of this q tile holding at least one row r < T_b
       const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
-      // stage order: row blocks in pairs (2 rbp, 2 rbp + 1), for each pair i = 1..j, the pair's blocks
-      // interleaved; warp w = 10 + 2 sub + hs takes head slot hs of the blocks 2 rbp + sub
       if (warp == 14) {
         if (lane == 0) {
 #ifdef TTT_TRACE
           int trace_n_3 = 32768;
 #endif
           int n = 0;
-          for (int rbp = 0; 2 * rbp < nrb; ++rbp)
-            for (int i = 0; i < j; ++i)
-              for (int sub = 0; sub < 2; ++sub) {
-                const int rb = 2 * rbp + sub;
-                if (rb >= nrb) continue;
-                const int st = n % kDgStages, use = n / kDgStages;
-                mbar_wait(&bars.dg_empty[st], (use & 1) ^ 1);
-                if (TTT_FWD_DIAG_MODE == 2) {  // dev probe: no loads
-                  mbar_arrive(&bars.dg_full[st]);
-                  ++n;
-                  continue;
-                }
-                mbar_expect_tx(&bars.dg_full[st], DGS);
-                uint8_t* base = sDg + st * DGS;
-                const int r0 = qt * kTile + rb * kDgRows;
-#pragma unroll
-                for (int bx = 0; bx < NBOX; ++bx) {
-                  tma_load_4d(base + bx * DGB, &maps.kd[i], &bars.dg_full[st], bx * 64, g, r0, b);
-                  tma_load_4d(base + (NBOX + bx) * DGB, &maps.vd[i], &bars.dg_full[st], bx * 64, g, r0, b);
-                }
-                TTT_TRACE_EV(3, 3, n);
-                ++n;
+          for (int rb = 0; rb < nrb; ++rb)
+            for (int i = 0; i < j; ++i, ++n) {
+              const int st = n % kDgStages, use = n / kDgStages;
+              mbar_wait(&bars.dg_empty[st], (use & 1) ^ 1);
+              if (TTT_FWD_DIAG_MODE == 2) {  // dev probe: no loads
+                mbar_arrive(&bars.dg_full[st]);
+                continue;
               }
+              mbar_expect_tx(&bars.dg_full[st], DGS);
+              uint8_t* base = sDg + st * DGS;
+              const int r0 = qt * kTile + rb * kDgRows;
+#pragma unroll
+              // one box per tensor: 16 rows x D columns, no swizzle (rows of D x 2 bytes)
+              tma_load_4d(base, &maps.kd[i], &bars.dg_full[st], 0, g, r0, b);
+              tma_load_4d(base + NBOX * DGB, &maps.vd[i], &bars.dg_full[st], 0, g, r0, b);
+              TTT_TRACE_EV(3, 3, n);
+            }
         }
       } else if (warp < 14) {
-        // Tensor cores (mma.sync m16n8k16) for the tiny per-row products of a 16-row block, one head
-        // per warp: S = Q_blk K_blk^T (16 x 16; row r needs only its diagonal entry S[r][r] =
-        // q_r . K_i[r]) and O_d += diag(p) V_blk (16 x D). The padding costs tensor-core slots, not
-        // CUDA-core issue slots, which the softmax warps need (a CUDA-core version of this loop cost
-        // ~0.4 ms per unroll, r02d / r02q probes).
-        constexpr int KS = D / 16, NT = D / 8;
-        const int hs = (warp - 10) & 1, sub = (warp - 10) >> 1;
-        if (hs == 1 && !has1) {
-          // single-head CTA: this warp has no head; its blocks' stages count one consumer (see init)
-        } else {
-          const int g8 = lane >> 2, c4 = lane & 3;
-          const float sl2 = p.scale_log2;
-          const bool holder = c4 == (g8 >> 1);           // holds the diagonal entries of rows g8, g8 + 8
-          const int src = g8 * 4 + (g8 >> 1);            // the holder lane of this thread's quad
-          const uint32_t qbase = smem_u32(sQ + hs * TB);
-          mbar_wait(&bars.q, 0);  // q rows are read from the Q tiles (shared with the S MMAs, read-only)
-          TTT_TRACE_DECL(3);
-          if (threadIdx.x == 320) TTT_TRACE_EV(3, 4, 0);
-          for (int rbp = 0; 2 * rbp < nrb; ++rbp) {
-            const int rb = 2 * rbp + sub;
-            const int npair = min(2, nrb - 2 * rbp);
-            if (rb >= nrb) continue;
-            // Q fragments of the block (A operand, row-major 16 x D), kept for all j stages
-            uint32_t qa[KS][4];
-            {
-              const uint32_t arow = (uint32_t)(rb * kDgRows + (lane & 7) + ((lane >> 3) & 1) * 8);
+        // thread layout: 8 lanes per row (lane k = lane & 7 owns columns 8k..8k+7 of every 64-column
+        // box), 4 rows per warp, 16 rows per stage; both head slots per row
+        constexpr int E = 8 * NBOX;  // elements per lane
+        const int dw = warp - 10, k8 = lane & 7;
+        const int srow = dw * 4 + (lane >> 3);  // row within a 16-row block
+        const float sl2 = p.scale_log2;
+        mbar_wait(&bars.q, 0);  // q rows are read from the Q tiles (shared with the S MMAs, read-only)
+        TTT_TRACE_DECL(3);
+        if (threadIdx.x == 320) TTT_TRACE_EV(3, 4, 0);
+        int n = 0;
+        for (int rb = 0; rb < nrb; ++rb) {
+          const int row = rb * kDgRows + srow;
+          const int r = qt * kTile + row;
+          float qf[2][E], acc[2][E], m[2], l[2];
 #pragma unroll
-              for (int ks = 0; ks < KS; ++ks) {
-                const uint32_t ch = (uint32_t)ks * 2 + (lane >> 4);
-                ldsm_x4(qbase + (ch >> 3) * 16384 + sw128_off(arow, ch), qa[ks]);
+          for (int hs = 0; hs < 2; ++hs) {
+            m[hs] = -INFINITY;
+            l[hs] = 0.f;
+#pragma unroll
+            for (int bx = 0; bx < NBOX; ++bx) {
+              const uint4 u = lds128(smem_u32(sQ + hs * TB + bx * 16384) + sw128_off(row, k8));
+              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+                qf[hs][bx * 8 + 2 * e] = f.x * sl2;
+                qf[hs][bx * 8 + 2 * e + 1] = f.y * sl2;
+                acc[hs][bx * 8 + 2 * e] = 0.f;
+                acc[hs][bx * 8 + 2 * e + 1] = 0.f;
               }
-            }
-            float o[NT][4];
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
-            float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows g8, g8 + 8
-            for (int i = 0; i < j; ++i) {
-              const int n = 2 * j * rbp + i * npair + (npair == 2 ? sub : 0);
-              const int st = n % kDgStages, use = n / kDgStages;
-              mbar_wait(&bars.dg_full[st], use & 1);
-              if (threadIdx.x == 320) TTT_TRACE_EV(3, 1, n);
-              const uint32_t kb = smem_u32(sDg + st * DGS), vb = kb + NBOX * DGB;
-              if (TTT_FWD_DIAG_MODE != 1) {
-                // ---- S = Q K^T over the block: two n-tiles of 8 keys ----
-                float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-                const uint32_t brow = (uint32_t)((lane & 7) + ((lane >> 4) & 1) * 8);
-#pragma unroll
-                for (int ks = 0; ks < KS; ++ks) {
-                  const uint32_t ch = (uint32_t)ks * 2 + ((lane >> 3) & 1);
-                  uint32_t bfr[4];
-                  ldsm_x4(kb + (ch >> 3) * DGB + sw128_off(brow, ch), bfr);
-                  mma_16816(s0, qa[ks], bfr[0], bfr[1]);
-                  mma_16816(s1, qa[ks], bfr[2], bfr[3]);
-                }
-                // ---- the diagonal S[r][r] of rows g8 (n-tile 0) and g8 + 8 (n-tile 1), to the quad ----
-                const float t0 = __shfl_sync(0xffffffffu, (g8 & 1) ? s0[1] : s0[0], src) * sl2;
-                const float t1 = __shfl_sync(0xffffffffu, (g8 & 1) ? s1[3] : s1[2], src) * sl2;
-                // ---- online softmax over the j diagonal keys (log2 domain; lazy 2^8 rescale) ----
-                if (__any_sync(0xffffffffu, t0 > m0 + 8.f || t1 > m1 + 8.f)) {
-                  const float n0 = fmaxf(m0, t0), n1 = fmaxf(m1, t1);
-                  const float a0 = ex2(m0 - n0), a1 = ex2(m1 - n1);  // 0 while m = -inf
-                  l0 *= a0;
-                  l1 *= a1;
-#pragma unroll
-                  for (int nt = 0; nt < NT; ++nt) {
-                    o[nt][0] *= a0;
-                    o[nt][1] *= a0;
-                    o[nt][2] *= a1;
-                    o[nt][3] *= a1;
-                  }
-                  m0 = n0;
-                  m1 = n1;
-                }
-                const float p0 = ex2(t0 - m0), p1 = ex2(t1 - m1);
-                l0 += p0;
-                l1 += p1;
-                // ---- O += diag(p) V: A = the 16 x 16 diagonal matrix of p (bf16), B = V rows ----
-                uint32_t pa[4] = {0u, 0u, 0u, 0u};
-                if (holder) {
-                  pa[0] = (g8 & 1) ? pack_bf16(0.f, p0) : pack_bf16(p0, 0.f);  // (g8, g8)
-                  pa[3] = (g8 & 1) ? pack_bf16(0.f, p1) : pack_bf16(p1, 0.f);  // (g8 + 8, g8 + 8)
-                }
-                const uint32_t vrow = (uint32_t)((lane & 7) + ((lane >> 3) & 1) * 8);
-#pragma unroll
-                for (int c2 = 0; c2 < NT / 2; ++c2) {
-                  const uint32_t ch = (uint32_t)c2 * 2 + (lane >> 4);
-                  uint32_t vfr[4];
-                  ldsm_x4_t(vb + (ch >> 3) * DGB + sw128_off(vrow, ch), vfr);
-                  mma_16816(o[2 * c2], pa, vfr[0], vfr[1]);
-                  mma_16816(o[2 * c2 + 1], pa, vfr[2], vfr[3]);
-                }
-              }
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&bars.dg_empty[st]);
-            }
-            // ---- O_d (normalised, bf16) -> the out rows (read back by TMA), A_d -> shared memory ----
-            const int row0 = rb * kDgRows + g8, row1 = row0 + 8;
-            const int r0g = qt * kTile + row0, r1g = qt * kTile + row1;
-            const float i0 = 1.f / l0, i1 = 1.f / l1;
-            __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out);
-            const size_t o0 = (((size_t)b * p.L + r0g) * p.Hq + h0 + hs) * D + 2 * c4;
-            const size_t o1 = (((size_t)b * p.L + r1g) * p.Hq + h0 + hs) * D + 2 * c4;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              if (r0g < T) *reinterpret_cast<uint32_t*>(ob + o0 + nt * 8) = pack_bf16(o[nt][0] * i0, o[nt][1] * i0);
-              if (r1g < T) *reinterpret_cast<uint32_t*>(ob + o1 + nt * 8) = pack_bf16(o[nt][2] * i1, o[nt][3] * i1);
-            }
-            if (c4 == 0) {
-              if (r0g < T) bars.a_d[hs][row0] = m0 + log2f(l0);
-              if (r1g < T) bars.a_d[hs][row1] = m1 + log2f(l1);
             }
           }
-          if (threadIdx.x == 320) TTT_TRACE_EV(3, 2, 0);
+          // Stages two at a time (i, i + 1): their dot products, shuffles and exps are independent,
+          // and the running max only moves (a warp-uniform rescale) when a score exceeds it by
+          // 2^8 — the j-long chain of an exact online softmax was the fused pass's critical path.
+          for (int i = 0; i < j; i += 2) {
+            const int ns = min(2, j - i);
+            uint32_t kw[2][E / 2], vw[2][E / 2];  // packed bf16 pairs of K_i, V_i (this lane's columns)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              if (u < ns) {
+                const int st = (n + u) % kDgStages, use = (n + u) / kDgStages;
+                mbar_wait(&bars.dg_full[st], use & 1);
+                if (threadIdx.x == 320) TTT_TRACE_EV(3, 1, n + u);
+                const uint32_t base = smem_u32(sDg + st * DGS);
+#pragma unroll
+                for (int bx = 0; bx < NBOX; ++bx) {
+                  const uint32_t off = (uint32_t)srow * (D * 2) + bx * 128 + k8 * 16;  // row-major rows
+                  const uint4 uk = lds128(base + off);
+                  const uint4 uv = lds128(base + NBOX * DGB + off);
+                  kw[u][bx * 4 + 0] = uk.x; kw[u][bx * 4 + 1] = uk.y; kw[u][bx * 4 + 2] = uk.z; kw[u][bx * 4 + 3] = uk.w;
+                  vw[u][bx * 4 + 0] = uv.x; vw[u][bx * 4 + 1] = uv.y; vw[u][bx * 4 + 2] = uv.z; vw[u][bx * 4 + 3] = uv.w;
+                }
+              } else {
+#pragma unroll
+                for (int e = 0; e < E / 2; ++e) kw[u][e] = vw[u][e] = 0u;
+              }
+            }
+            __syncwarp();
+            if (lane == 0)
+              for (int u = 0; u < ns; ++u) mbar_arrive(&bars.dg_empty[(n + u) % kDgStages]);  // values in registers
+            n += ns;
+            if (TTT_FWD_DIAG_MODE == 1) continue;  // dev probe: no math
+            // t = c log2e q . K_i[r] for (head, stage): 8-lane partial dots (two FFMA2 chains each)
+            float t[2][2];
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                uint64_t d0 = 0, d1 = 0;
+#pragma unroll
+                for (int e = 0; e < E / 2; e += 2) {
+                  d0 = ffma2(f2pack(qf[hs][2 * e], qf[hs][2 * e + 1]), bf2_to_f2(kw[u][e]), d0);
+                  d1 = ffma2(f2pack(qf[hs][2 * e + 2], qf[hs][2 * e + 3]), bf2_to_f2(kw[u][e + 1]), d1);
+                }
+                float a0, a1, b0, b1;
+                f2unpack(d0, a0, a1);
+                f2unpack(d1, b0, b1);
+                t[hs][u] = (a0 + a1) + (b0 + b1);
+              }
+#pragma unroll
+            for (int sh = 1; sh < 8; sh <<= 1)
+#pragma unroll
+              for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) t[hs][u] += __shfl_xor_sync(0xffffffffu, t[hs][u], sh);
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs) {
+              const float tmax = ns > 1 ? fmaxf(t[hs][0], t[hs][1]) : t[hs][0];
+              if (__any_sync(0xffffffffu, tmax > m[hs] + 8.f)) {  // rare: the max moved (always at i = 0)
+                const float m_new = fmaxf(m[hs], tmax);
+                const float alpha = ex2(m[hs] - m_new);  // 0 when m was -inf
+                l[hs] *= alpha;
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc[hs][e] *= alpha;
+                m[hs] = m_new;
+              }
+              const float p0 = ex2(t[hs][0] - m[hs]), p1 = ns > 1 ? ex2(t[hs][1] - m[hs]) : 0.f;
+              l[hs] += p0 + p1;
+              const uint64_t p02 = f2pack(p0, p0), p12 = f2pack(p1, p1);
+#pragma unroll
+              for (int e = 0; e < E / 2; ++e) {
+                uint64_t o = ffma2(bf2_to_f2(vw[0][e]), p02, f2pack(acc[hs][2 * e], acc[hs][2 * e + 1]));
+                o = ffma2(bf2_to_f2(vw[1][e]), p12, o);
+                f2unpack(o, acc[hs][2 * e], acc[hs][2 * e + 1]);
+              }
+            }
+          }
+          // O_d (normalised, bf16) -> the out rows (staging; read back by TMA), A_d -> shared memory
+          if (r < T) {
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs) {
+              if (hs == 0 || has1) {
+                const float inv = 1.f / l[hs];
+                __nv_bfloat16* orow =
+                    reinterpret_cast<__nv_bfloat16*>(p.out) + (((size_t)b * p.L + r) * p.Hq + h0 + hs) * D;
+#pragma unroll
+                for (int bx = 0; bx < NBOX; ++bx) {
+                  uint4 w;
+                  w.x = pack_bf16(acc[hs][bx * 8 + 0] * inv, acc[hs][bx * 8 + 1] * inv);
+                  w.y = pack_bf16(acc[hs][bx * 8 + 2] * inv, acc[hs][bx * 8 + 3] * inv);
+                  w.z = pack_bf16(acc[hs][bx * 8 + 4] * inv, acc[hs][bx * 8 + 5] * inv);
+                  w.w = pack_bf16(acc[hs][bx * 8 + 6] * inv, acc[hs][bx * 8 + 7] * inv);
+                  *reinterpret_cast<uint4*>(orow + bx * 64 + k8 * 8) = w;
+                }
+                if (k8 == 0) bars.a_d[hs][row] = m[hs] + log2f(l[hs]);
+              }
+            }
+          }
         }
+        if (threadIdx.x == 320) TTT_TRACE_EV(3, 2, n);
         fence_async_global();  // the out rows are read back by the producer's TMA (async proxy)
         __threadfence_block();
         mbar_arrive(&bars.diag_done);
