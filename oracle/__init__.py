@@ -10,6 +10,9 @@ Contents
     analytic backward — in fp64, threaded over (b, kv-group).
   * :func:`alg1_row`: Alg. 1 "TTT Attention" (PAPER.md:139-162) literally, for
     one query row, as an independent third formulation.
+  * :func:`fwd_packed` / :func:`bwd_packed`: packed batches (rows of sequence b at
+    [cu[b], cu[b+1]), no padding), each sequence alone through fwd / bwd with
+    Q_LEN = T_b (pinned in tests/test_oracle_packed.py).
 
 Parity status: every function here is pinned by tests/test_oracle_*.py
 (worked examples, closed forms, library routines, finite differences, exact
@@ -157,6 +160,52 @@ def bwd(q, k_base, v_base, k_steps, v_steps, dout, seq_lens=None, scale=0.0, row
     if st != 0:
         raise ValueError(f"oracle bwd: bad arguments (status {st})")
     return {"dq": dq, "dk_base": dkb, "dv_base": dvb, "dk_steps": dks, "dv_steps": dvs}
+
+
+def _packed_spans(cu_seqlens):
+    cu = np.asarray(cu_seqlens, dtype=np.int64)
+    assert cu.ndim == 1 and cu[0] == 0 and np.all(np.diff(cu) >= 1)
+    return [(int(cu[b]), int(cu[b + 1])) for b in range(len(cu) - 1)]
+
+
+def fwd_packed(q, k_base, v_base, k_steps, v_steps, cu_seqlens, scale=0.0, nthreads=None):
+    """Oracle forward of a PACKED batch: sequence b is rows
+    [cu[b], cu[b+1]) of q [N,Hq,D] / k_base, v_base, k_steps[i], v_steps[i] [N,Hkv,D], with no
+    padding rows. It is Alg. 2 run on each sequence alone with Q_LEN = T_b = cu[b+1] - cu[b]
+    (m_pad is then vacuous) — the plain definition, one sequence at a
+    time through :func:`fwd`. Returns (out fp64 [N,Hq,D], lse fp64 [Hq,N])."""
+    q = np.asarray(q); Hq = q.shape[1]
+    N = q.shape[0]
+    out = np.empty((N,) + q.shape[1:], dtype=np.float64)
+    lse = np.empty((Hq, N), dtype=np.float64)
+    for r0, r1 in _packed_spans(cu_seqlens):
+        sl = lambda a: np.asarray(a)[None, r0:r1]
+        o, l = fwd(sl(q), sl(k_base), sl(v_base), [sl(x) for x in k_steps], [sl(x) for x in v_steps],
+                   scale=scale, nthreads=nthreads)
+        out[r0:r1] = o[0]
+        lse[:, r0:r1] = l[0]
+    return out, lse
+
+
+def bwd_packed(q, k_base, v_base, k_steps, v_steps, dout, cu_seqlens, scale=0.0, nthreads=None):
+    """Oracle backward of a packed batch (see :func:`fwd_packed`): each sequence alone through
+    :func:`bwd` with L = T_b. Returns the dict of :func:`bwd` in the packed layout ([N,H,D])."""
+    q = np.asarray(q)
+    N, Hkv, D = q.shape[0], np.asarray(k_base).shape[1], q.shape[2]
+    j = len(k_steps)
+    res = {"dq": np.empty(q.shape, dtype=np.float64), "dk_base": np.empty((N, Hkv, D)),
+           "dv_base": np.empty((N, Hkv, D)), "dk_steps": [np.empty((N, Hkv, D)) for _ in range(j)],
+           "dv_steps": [np.empty((N, Hkv, D)) for _ in range(j)]}
+    for r0, r1 in _packed_spans(cu_seqlens):
+        sl = lambda a: np.asarray(a)[None, r0:r1]
+        g = bwd(sl(q), sl(k_base), sl(v_base), [sl(x) for x in k_steps], [sl(x) for x in v_steps], sl(dout),
+                scale=scale, nthreads=nthreads)
+        for key in ("dq", "dk_base", "dv_base"):
+            res[key][r0:r1] = g[key][0]
+        for i in range(j):
+            res["dk_steps"][i][r0:r1] = g["dk_steps"][i][0]
+            res["dv_steps"][i][r0:r1] = g["dv_steps"][i][0]
+    return res
 
 
 def alg1_row(q_t, K_train, V_train, k_pred, v_pred, scale):
