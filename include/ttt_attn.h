@@ -88,6 +88,15 @@ typedef struct {
   int32_t dtype;          /* ttt_dtype */
   float softmax_scale;    /* c; 0 => 1/sqrt(head_dim) */
   const int32_t* seq_lens;/* HOST int32[batch]: T_b, 1 <= T_b <= L (Alg. 2 T); NULL => all T_b = L */
+  const int32_t* cu_seqlens;/* HOST int32[batch + 1] or NULL (padded layout). Non-NULL: PACKED layout
+                             (SURVEY.md §8(f) NEXT #3): sequence b is rows [cu_seqlens[b], cu_seqlens[b+1])
+                             — T_b = the difference >= 1, cu_seqlens[0] = 0 — of q / out / out_lo / dq /
+                             dout [N][Hq][D] and k_base / v_base / k_steps[i] / v_steps[i] / dk_* / dv_*
+                             [N][Hkv][D], N = cu_seqlens[batch], with no padding rows; lse is [Hq][N].
+                             Semantics: each sequence alone is Alg. 2 with Q_LEN = T_b (PAPER.md:294, 300,
+                             307: m_pad vacuous), i.e. the padded result's rows r < T_b. seq_lens must be
+                             NULL; seq_len is ignored (>= 1); BF16 mode has no multiple-of-128 requirement.
+                             N x num_q_heads < 2^31. Zero-initialise the struct for the padded layout. */
 } ttt_attn_desc;
 
 /* flags for ttt_attn_bwd */

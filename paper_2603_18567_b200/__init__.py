@@ -18,7 +18,7 @@ import importlib
 
 _EXPORTS = (
     "TTT_ACCUMULATE_DKV", "TTT_BF16", "TTT_FP32_CHECK", "TTT_MAX_BATCH", "TTT_MAX_STEPS", "Desc", "TTTError",
-    "desc_for", "make_desc", "ttt_attn_bwd", "ttt_attn_fwd", "ttt_attn_strerror", "ttt_attn_version",
+    "desc_for", "make_desc", "packed_desc", "ttt_attn_bwd", "ttt_attn_fwd", "ttt_attn_strerror", "ttt_attn_version",
     "ttt_attn_workspace_size", "ttt_attn_profile_begin", "ttt_attn_profile_end", "ttt_attn_kernel_name",
     "TTT_LOSS_MEAN", "LossDesc", "loss_desc_for", "ttt_loss_workspace_size", "ttt_loss_fwd", "ttt_loss_bwd_inplace",
     "ttt_loss_fwd_bwd_inplace", "TTT_MAX_UNROLL", "ttt_attn_bwd_unroll", "ttt_attn_bwd_unroll_workspace_size",

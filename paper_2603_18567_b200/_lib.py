@@ -40,7 +40,13 @@ class Desc(ctypes.Structure):
         ("batch", ctypes.c_int32), ("seq_len", ctypes.c_int32), ("num_q_heads", ctypes.c_int32),
         ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("dtype", ctypes.c_int32),
         ("softmax_scale", ctypes.c_float), ("seq_lens", ctypes.POINTER(ctypes.c_int32)),
+        ("cu_seqlens", ctypes.POINTER(ctypes.c_int32)),
     ]
+
+    @property
+    def packed_rows(self) -> Optional[int]:
+        """N = cu_seqlens[batch] for a packed desc, else None."""
+        return self.cu_seqlens[self.batch] if self.cu_seqlens else None
 
 
 class TreeDesc(ctypes.Structure):
@@ -134,7 +140,9 @@ def ttt_attn_version() -> str:
 
 def make_desc(batch: int, seq_len: int, num_q_heads: int, num_kv_heads: int, head_dim: int,
               dtype: int = TTT_BF16, softmax_scale: float = 0.0,
-              seq_lens: Optional[Sequence[int]] = None) -> Desc:
+              seq_lens: Optional[Sequence[int]] = None, cu_seqlens: Optional[Sequence[int]] = None) -> Desc:
+    """ttt_attn_desc. cu_seqlens (batch + 1 offsets, host ints) selects the packed layout: q [N, Hq, D],
+    k / v [N, Hkv, D], lse [Hq, N] with N = cu_seqlens[-1]; seq_len is then ignored."""
     d = Desc()
     d.batch, d.seq_len, d.num_q_heads, d.num_kv_heads, d.head_dim = (
         int(batch), int(seq_len), int(num_q_heads), int(num_kv_heads), int(head_dim))
@@ -143,7 +151,22 @@ def make_desc(batch: int, seq_len: int, num_q_heads: int, num_kv_heads: int, hea
         arr = (ctypes.c_int32 * int(batch))(*[int(x) for x in seq_lens])
         d._seq_lens_keepalive = arr  # keep the host array alive with the desc
         d.seq_lens = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32))
+    if cu_seqlens is not None:
+        cu = [int(x) for x in cu_seqlens]
+        if len(cu) != int(batch) + 1:
+            raise TTTError(1, f"cu_seqlens needs batch + 1 = {int(batch) + 1} entries (got {len(cu)})")
+        carr = (ctypes.c_int32 * len(cu))(*cu)
+        d._cu_keepalive = carr
+        d.cu_seqlens = ctypes.cast(carr, ctypes.POINTER(ctypes.c_int32))
     return d
+
+
+def packed_desc(cu_seqlens: Sequence[int], num_q_heads: int, num_kv_heads: int, head_dim: int,
+                dtype: int = TTT_BF16, softmax_scale: float = 0.0) -> Desc:
+    """Desc of a packed batch: sequence b = rows [cu_seqlens[b], cu_seqlens[b+1])."""
+    cu = [int(x) for x in cu_seqlens]
+    return make_desc(len(cu) - 1, max(1, max(b - a for a, b in zip(cu[:-1], cu[1:]))), num_q_heads, num_kv_heads,
+                     head_dim, dtype, softmax_scale, None, cu)
 
 
 def desc_for(q: torch.Tensor, k_base: torch.Tensor, seq_lens=None, softmax_scale: float = 0.0) -> Desc:
@@ -205,6 +228,9 @@ def _validate(spec, *, device=None):
 def _attn_shapes(desc: "Desc"):
     B, L, Hq, Hkv, D = desc.batch, desc.seq_len, desc.num_q_heads, desc.num_kv_heads, desc.head_dim
     dt = torch.float32 if desc.dtype == TTT_FP32_CHECK else torch.bfloat16
+    N = desc.packed_rows
+    if N is not None:  # packed layout
+        return dt, (N, Hq, D), (N, Hkv, D), (Hq, N)
     return dt, (B, L, Hq, D), (B, L, Hkv, D), (B, Hq, L)
 
 

@@ -119,6 +119,14 @@ int validate_desc(const ttt_attn_desc* d, int step) {
   if (d->num_q_heads / d->num_kv_heads > 32) return TTT_ERR_UNSUPPORTED;  // GQA group <= 32 heads
   if (!(d->softmax_scale >= 0.f) || std::isinf(d->softmax_scale)) return TTT_ERR_INVALID_ARG;
   if (step < 0 || step >= TTT_MAX_STEPS) return TTT_ERR_STEP_RANGE;
+  if (d->cu_seqlens) {  // packed layout
+    if (d->seq_lens) return TTT_ERR_INVALID_ARG;
+    if (d->cu_seqlens[0] != 0) return TTT_ERR_INVALID_ARG;
+    for (int b = 0; b < d->batch; ++b)
+      if ((long long)d->cu_seqlens[b + 1] - d->cu_seqlens[b] < 1) return TTT_ERR_DEGENERATE;
+    if ((long long)d->cu_seqlens[d->batch] * d->num_q_heads >= (1ll << 31)) return TTT_ERR_UNSUPPORTED;
+    return TTT_OK;
+  }
   if (d->dtype == TTT_BF16 && (d->seq_len % kTile)) return TTT_ERR_UNSUPPORTED;
   // row indices (b L + r) Hq + h are decoded in 32-bit arithmetic on the device
   if ((long long)d->batch * d->seq_len * d->num_q_heads >= (1ll << 31)) return TTT_ERR_UNSUPPORTED;
@@ -141,8 +149,35 @@ void fill_common(Params& p, const ttt_attn_desc* d, int step) {
   p.nqt = p.L / kTile;
   p.scale = d->softmax_scale > 0.f ? d->softmax_scale : 1.0f / std::sqrt((float)p.D);
   p.scale_log2 = p.scale * 1.4426950408889634f;
+  if (d->cu_seqlens) {  // packed: one [nrows][H][D] view, each sequence's tiles numbered in turn
+    p.packed = 1;
+    int maxT = 1, tiles = 0;
+    for (int b = 0; b < p.B; ++b) {
+      const int T = d->cu_seqlens[b + 1] - d->cu_seqlens[b];
+      p.seq_lens[b] = T;
+      p.row0[b] = d->cu_seqlens[b];
+      p.tile0[b] = tiles;
+      tiles += (T + kTile - 1) / kTile;
+      maxT = std::max(maxT, T);
+    }
+    p.nrows = p.row0[p.B] = d->cu_seqlens[p.B];
+    p.ntiles = p.tile0[p.B] = tiles;
+    p.L = (maxT + kTile - 1) / kTile * kTile;  // bounds only (host heuristics); no tensor is [B][L]
+    p.nqt = p.L / kTile;
+    return;
+  }
   for (int b = 0; b < p.B; ++b) p.seq_lens[b] = d->seq_lens ? d->seq_lens[b] : p.L;
+  for (int b = 0; b <= p.B; ++b) {
+    p.row0[b] = b * p.L;
+    p.tile0[b] = b * p.nqt;
+  }
+  p.nrows = p.B * p.L;
+  p.ntiles = p.B * p.nqt;
 }
+
+// tensor-map extents of a [B][L][H][D] tensor: (B, L) padded, (1, nrows) packed
+int map_b(const Params& p) { return p.packed ? 1 : p.B; }
+int map_l(const Params& p) { return p.packed ? p.nrows : p.L; }
 
 }  // namespace
 
@@ -204,7 +239,13 @@ struct BwdWs {
 };
 BwdWs bwd_ws_layout(const ttt_attn_desc* d) {
   BwdWs w{};
-  const size_t rows = (size_t)d->batch * d->num_q_heads * d->seq_len;
+  // delta / lse2 [Hq][ntiles][128], dq_acc [Hq][ntiles][128][D] (padded: ntiles = B L / 128)
+  size_t tiles = (size_t)d->batch * ((d->seq_len + kTile - 1) / kTile);
+  if (d->cu_seqlens) {
+    tiles = 0;
+    for (int b = 0; b < d->batch; ++b) tiles += (size_t)(d->cu_seqlens[b + 1] - d->cu_seqlens[b] + kTile - 1) / kTile;
+  }
+  const size_t rows = tiles * kTile * d->num_q_heads;
   w.delta = 0;
   w.lse2 = align256(rows * 4);
   w.dq_acc = w.lse2 + align256(rows * 4);
@@ -352,22 +393,22 @@ int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (d->dtype == TTT_FP32_CHECK) return cuda_status(launch_fwd_check(p, s));
   FwdMaps maps;
-  if (!encode_bshd(&maps.q, q, p.B, p.L, p.Hq, p.D) || !encode_bshd(&maps.k, k_base, p.B, p.L, p.Hkv, p.D) ||
-      !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D) || !encode_bshd(&maps.out, out, p.B, p.L, p.Hq, p.D) ||
-      (p.out_lo && !encode_bshd(&maps.out_lo, p.out_lo, p.B, p.L, p.Hq, p.D)))
+  if (!encode_bshd(&maps.q, q, map_b(p), map_l(p), p.Hq, p.D) || !encode_bshd(&maps.k, k_base, map_b(p), map_l(p), p.Hkv, p.D) ||
+      !encode_bshd(&maps.v, v_base, map_b(p), map_l(p), p.Hkv, p.D) || !encode_bshd(&maps.out, out, map_b(p), map_l(p), p.Hq, p.D) ||
+      (p.out_lo && !encode_bshd(&maps.out_lo, p.out_lo, map_b(p), map_l(p), p.Hq, p.D)))
     return TTT_ERR_CUDA;
   for (int i = 0; i < p.step; ++i)  // the forward's in-kernel diagonal ring: 16-row boxes of K_i / V_i
-    if (!encode_bshd_rows(&maps.kd[i], p.ks[i], p.B, p.L, p.Hkv, p.D, 16) ||
-        !encode_bshd_rows(&maps.vd[i], p.vs[i], p.B, p.L, p.Hkv, p.D, 16))
+    if (!encode_bshd_rows(&maps.kd[i], p.ks[i], map_b(p), map_l(p), p.Hkv, p.D, 16) ||
+        !encode_bshd_rows(&maps.vd[i], p.vs[i], map_b(p), map_l(p), p.Hkv, p.D, 16))
       return TTT_ERR_CUDA;
   DiagMaps dmaps;
   if (p.step > 0 && fwd_uses_diag_kernel()) {
     const int nr = fwd_diag_rows_per_group(p);
-    const long long rows = (long long)p.B * p.L * p.Hq;
+    const long long rows = (long long)p.nrows * p.Hq;
     if (nr <= 0) return TTT_ERR_UNSUPPORTED;
     if (!encode_rows2d(&dmaps.q, q, rows, p.D, nr * p.G) || !encode_rows2d(&dmaps.out, out, rows, p.D, nr * p.G))
       return TTT_ERR_CUDA;
-    const long long kv_rows = (long long)p.B * p.L * p.Hkv;
+    const long long kv_rows = (long long)p.nrows * p.Hkv;
     for (int i = 0; i < p.step; ++i)
       if (!encode_rows2d(&dmaps.k[i], p.ks[i], kv_rows, p.D, nr) || !encode_rows2d(&dmaps.v[i], p.vs[i], kv_rows, p.D, nr))
         return TTT_ERR_CUDA;
@@ -413,7 +454,7 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
     p.dvs[i] = dv_steps[i];
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const size_t kv_elems = (size_t)p.B * p.L * p.Hkv * p.D;
+  const size_t kv_elems = (size_t)p.nrows * p.Hkv * p.D;
   (void)kv_elems;
   if (d->dtype == TTT_FP32_CHECK) {
     if (!workspace || workspace_bytes < check_bwd_ws_bytes(p)) return TTT_ERR_WORKSPACE;
@@ -429,16 +470,16 @@ int ttt_attn_bwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
   p.lse2 = reinterpret_cast<float*>(ws + w.lse2);
   p.dq_acc = reinterpret_cast<float*>(ws + w.dq_acc);
   BwdMaps maps;
-  if (!encode_bshd(&maps.q, q, p.B, p.L, p.Hq, p.D) || !encode_bshd(&maps.k, k_base, p.B, p.L, p.Hkv, p.D) ||
-      !encode_bshd(&maps.v, v_base, p.B, p.L, p.Hkv, p.D) || !encode_bshd(&maps.dout, dout, p.B, p.L, p.Hq, p.D) ||
-      !encode_bshd(&maps.dout64, dout, p.B, p.L, p.Hq, p.D, 64) ||
-      !encode_dqacc(&maps.dqacc, p.dq_acc, (size_t)p.B * p.L * p.Hq * p.D / 32))
+  if (!encode_bshd(&maps.q, q, map_b(p), map_l(p), p.Hq, p.D) || !encode_bshd(&maps.k, k_base, map_b(p), map_l(p), p.Hkv, p.D) ||
+      !encode_bshd(&maps.v, v_base, map_b(p), map_l(p), p.Hkv, p.D) || !encode_bshd(&maps.dout, dout, map_b(p), map_l(p), p.Hq, p.D) ||
+      !encode_bshd(&maps.dout64, dout, map_b(p), map_l(p), p.Hq, p.D, 64) ||
+      !encode_dqacc(&maps.dqacc, p.dq_acc, (size_t)p.ntiles * kTile * p.Hq * p.D / 32))
     return TTT_ERR_CUDA;
   PreMaps pmaps;
   {
     const int nr = bwd_pre_rows_per_group(p);
     if (nr <= 0) return TTT_ERR_UNSUPPORTED;
-    const long long rows = (long long)p.B * p.L * p.Hq, kv_rows = (long long)p.B * p.L * p.Hkv;
+    const long long rows = (long long)p.nrows * p.Hq, kv_rows = (long long)p.nrows * p.Hkv;
     const int br = nr * p.G;
     if (!encode_rows2d(&pmaps.dout, dout, rows, p.D, br) || !encode_rows2d(&pmaps.o, out, rows, p.D, br) ||
         (p.o_lo && !encode_rows2d(&pmaps.olo, p.o_lo, rows, p.D, br)) ||
@@ -645,11 +686,11 @@ int ttt_attn_bwd_unroll(const ttt_attn_desc* d, int num_steps, const void* const
     up.delta[j] = p.delta;
     up.lse2[j] = p.lse2;
     up.dq_acc[j] = p.dq_acc;
-    if (!encode_bshd(&maps[j].q, q[j], p.B, p.L, p.Hq, p.D) || !encode_bshd(&maps[j].k, k_base, p.B, p.L, p.Hkv, p.D) ||
-        !encode_bshd(&maps[j].v, v_base, p.B, p.L, p.Hkv, p.D) ||
-        !encode_bshd(&maps[j].dout, dout[j], p.B, p.L, p.Hq, p.D) ||
-        !encode_bshd(&maps[j].dout64, dout[j], p.B, p.L, p.Hq, p.D, 64) ||
-        !encode_dqacc(&maps[j].dqacc, p.dq_acc, (size_t)p.B * p.L * p.Hq * p.D / 32))
+    if (!encode_bshd(&maps[j].q, q[j], map_b(p), map_l(p), p.Hq, p.D) || !encode_bshd(&maps[j].k, k_base, map_b(p), map_l(p), p.Hkv, p.D) ||
+        !encode_bshd(&maps[j].v, v_base, map_b(p), map_l(p), p.Hkv, p.D) ||
+        !encode_bshd(&maps[j].dout, dout[j], map_b(p), map_l(p), p.Hq, p.D) ||
+        !encode_bshd(&maps[j].dout64, dout[j], map_b(p), map_l(p), p.Hq, p.D, 64) ||
+        !encode_dqacc(&maps[j].dqacc, p.dq_acc, (size_t)p.ntiles * kTile * p.Hq * p.D / 32))
       return TTT_ERR_CUDA;
   }
   // pre-pass maps: layout of the largest step (S - 1); per-step q / dO / O / O_lo views
@@ -659,7 +700,7 @@ int ttt_attn_bwd_unroll(const ttt_attn_desc* d, int num_steps, const void* const
       if (!out_lo[j]) return TTT_ERR_INVALID_ARG;  // all or none
   const int nr = bwd_pre_rows_per_group(last);
   if (nr <= 0) return TTT_ERR_UNSUPPORTED;
-  const long long rows = (long long)last.B * last.L * last.Hq, kv_rows = (long long)last.B * last.L * last.Hkv;
+  const long long rows = (long long)last.nrows * last.Hq, kv_rows = (long long)last.nrows * last.Hkv;
   const int br = nr * last.G;
   for (int j = 0; j < S; ++j) {
     if (!encode_rows2d(&up.dout[j], dout[j], rows, last.D, br) || !encode_rows2d(&up.o[j], out[j], rows, last.D, br) ||

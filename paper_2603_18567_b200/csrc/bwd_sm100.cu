@@ -81,7 +81,7 @@ __device__ __forceinline__ void load_bf16(const void* base, size_t off, float (&
 //   [B][Hq][L/128][D/32][128 rows][32 cols] fp32
 __device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int r, int d) {
   const int nc = p.D / 32;
-  return ((((size_t)(b * p.Hq + h) * p.nqt + (r >> 7)) * nc + (d >> 5)) * 128 + (r & 127)) * 32 + (d & 31);
+  return ((dq_tile(p, b, h, r >> 7) * nc + (d >> 5)) * 128 + (r & 127)) * 32 + (d & 31);
 }
 
 // ------------------------------------------------------------------ kernel 1
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
   uint8_t* stages = psm + 1024;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = p.G, NR = lay.NR, NS = lay.NS, R = lay.R;
-  const int nrows = p.B * p.L * p.Hkv;  // < 2^31 (host check)
+  const int nrows = p.nrows * p.Hkv;  // kv rows (B L or sum T_b) x Hkv < 2^31 (host check)
   const int ngroups = (nrows + NR - 1) / NR;
   const int ng = (ngroups - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // this CTA's groups
   const int S = U ? up.S : 1;
@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
   auto decode = [&](uint32_t w, int& b_, int& r_, int& g_) {  // w = (b L + r) Hkv + g
     const uint32_t bl = lay.div_hkv.div(w);
     g_ = (int)(w - bl * (uint32_t)p.Hkv);
-    b_ = (int)lay.div_L.div(bl);
-    r_ = (int)(bl - (uint32_t)b_ * (uint32_t)p.L);
+    b_ = p.packed ? seq_of_row(p, (int)bl) : (int)lay.div_L.div(bl);
+    r_ = (int)bl - p.row0[b_];
   };
   uint8_t* scrP = psm + lay.off_scr + cw * 2560;  // [16 rows m][40] bf16 (80-B rows: conflict-free)
   uint8_t* scrS = scrP + 1280;
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
             if (m < mrows0 && k_first * R + wr0 < nv) {
               int b_, r_, g_;
               decode((uint32_t)(w0 + k_first * R + wr0), b_, r_, g_);
-              lse_pf[hf] = lse_in[((size_t)b_ * p.Hq + g_ * G + hh0) * p.L + r_];
+              lse_pf[hf] = lse_in[lse_at(p, b_, g_ * G + hh0, r_)];
             }
           }
         }
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
               decode((uint32_t)(w0 + min(lr0 + wr[hf], nv - 1)), bb[hf], rr[hf], gg[hf]);
               act[hf] = okr[hf] && rr[hf] < p.seq_lens[bb[hf]];
               l2[hf] = okr[hf] ? ((k == k_first && mt == 0) ? lse_pf[hf]
-                                                          : lse_in[((size_t)bb[hf] * p.Hq + gg[hf] * G + hh[hf]) * p.L + rr[hf]]) *
+                                                          : lse_in[lse_at(p, bb[hf], gg[hf] * G + hh[hf], rr[hf])]) *
                                      kLog2e
                                : 0.f;
             }
@@ -415,9 +415,9 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
               const int h = gg[hf] * G + hh[hf];
-              qbase[hf] = ((((size_t)(bb[hf] * p.Hq + h) * p.nqt + (rr[hf] >> 7)) * (D / 32)) * 128 + (rr[hf] & 127)) * 32;
+              qbase[hf] = ((dq_tile(p, bb[hf], h, rr[hf] >> 7) * (D / 32)) * 128 + (rr[hf] & 127)) * 32;
               if (okr[hf] && c4 == 0) {
-                const size_t li = ((size_t)bb[hf] * p.Hq + h) * p.L + rr[hf];
+                const size_t li = ws_at(p, bb[hf], h, rr[hf]);
                 delta_p[li] = -del[hf];  // stored negated: the main kernel's FFMA2 / FADD2 consume -lse2, -Delta
                 lse2_p[li] = -l2[hf];
               }
@@ -627,9 +627,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // kv head run together, so its Q / dO tiles and dq_acc rows stay hot in L2. (A global
   // longest-first order — kv tile slowest — measured slower: 5.3 vs 5.26 ms bwd, 2.73-2.85 vs
   // 2.63-2.66 ms fwd per unroll in an interleaved A/B, bench_tools/ab.sh.)
+  int kt, grp;
+  if (p.packed) {
+    // packed: (tile, kv head, head subset), head subsets fastest; each sequence's kv tiles in
+    // ascending order (the longest CTAs of the sequence first)
+    const int per = p.Hkv * p.head_split;
+    const int tt = (int)blockIdx.x / per;
+    const int bq = seq_of_tile(p, tt);
+    kt = tt - p.tile0[bq];
+    grp = bq * per + (int)blockIdx.x % per;
+  } else {
 #ifdef TTT_ORDER_GROUP
-  const int kt = (int)blockIdx.x % p.nqt;
-  const int grp = (int)blockIdx.x / p.nqt;
+  kt = (int)blockIdx.x % p.nqt;
+  grp = (int)blockIdx.x / p.nqt;
 #else
   // Batched longest-first: kv heads in batches of p.order_batch; inside a batch kv tile slowest (the
   // longest CTAs, kt = 0, first), then the batch's heads. The last batch ends with short CTAs (a
@@ -638,15 +648,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int bsz = p.order_batch * p.nqt;
   const int bat = (int)blockIdx.x / bsz, gbase = bat * p.order_batch;
   const int gb = min(p.order_batch, ngrp - gbase), rr = (int)blockIdx.x - bat * bsz;
-  const int kt = rr / gb;
-  const int grp = gbase + rr % gb;
+  kt = rr / gb;
+  grp = gbase + rr % gb;
 #endif
+  }
   const int hs = grp % hsplit;
   const int g = (grp / hsplit) % p.Hkv;
   const int b = grp / (hsplit * p.Hkv);
   const int T = p.seq_lens[b];
   if (kt * kTile >= T) return;  // every key of the tile is padding: no gradient flows
-  const int nq = p.nqt - kt;
+  const int nqt_b = p.packed ? p.tile0[b + 1] - p.tile0[b] : p.nqt;  // q tiles of this sequence
+  // TMA (row, batch) origin of this sequence: (0, b) padded, (row0[b], 0) packed
+  const int ry = p.packed ? p.row0[b] : 0, by = p.packed ? 0 : b;
+  const int nq = nqt_b - kt;
   const int n_items = nh * nq;  // 128-query tiles
   const int h_first = g * p.G + hs * nh;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1 KB alignment
@@ -694,8 +708,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_expect_tx(&bars.kv_full, 2 * TB);
 #pragma unroll
       for (int bx = 0; bx < NBOX; ++bx) {
-        tma_load_4d(sK + bx * 16384, &maps.k, &bars.kv_full, bx * 64, g, kt * kTile, b);
-        tma_load_4d(sV + bx * 16384, &maps.v, &bars.kv_full, bx * 64, g, kt * kTile, b);
+        tma_load_4d(sK + bx * 16384, &maps.k, &bars.kv_full, bx * 64, g, ry + kt * kTile, by);
+        tma_load_4d(sV + bx * 16384, &maps.v, &bars.kv_full, bx * 64, g, ry + kt * kTile, by);
       }
       for (int t = 0; t < n_items; ++t) {
         const int h = h_first + t / nq, qt = kt + t % nq;
@@ -708,16 +722,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const int hp = h_first + tp / nq, qtp = kt + tp % nq;
 #pragma unroll
           for (int bx = 0; bx < NBOX; ++bx) {
-            tma_prefetch_4d(&maps.q, bx * 64, hp, qtp * kTile, b);
-            tma_prefetch_4d(&maps.dout, bx * 64, hp, qtp * kTile, b);
+            tma_prefetch_4d(&maps.q, bx * 64, hp, ry + qtp * kTile, by);
+            tma_prefetch_4d(&maps.dout, bx * 64, hp, ry + qtp * kTile, by);
           }
         }
         mbar_wait(&bars.q_empty[qs], qph ^ 1);
         mbar_expect_tx(&bars.q_full[qs], TB + 1024);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sQ + qs * TB + bx * 16384, &maps.q, &bars.q_full[qs], bx * 64, h, qt * kTile, b);
-        const size_t li = ((size_t)b * p.Hq + h) * p.L + (size_t)qt * kTile;
+          tma_load_4d(sQ + qs * TB + bx * 16384, &maps.q, &bars.q_full[qs], bx * 64, h, ry + qt * kTile, by);
+        const size_t li = ws_at(p, b, h, qt * kTile);
         bulk_load_1d(sL + qs * 128, p.lse2 + li, 512, &bars.q_full[qs]);
         bulk_load_1d(sDel + qs * 128, p.delta + li, 512, &bars.q_full[qs]);
         TTT_TRACE_EV(2, 11, t);
@@ -729,7 +743,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int bx = 0; bx < NBOX; ++bx)
             tma_load_4d(sDO + slot * HB + bx * (HB / NBOX), &maps.dout64, &bars.do_full[slot], bx * 64, h,
-                        qt * kTile + 64 * x, b);
+                        ry + qt * kTile + 64 * x, by);
           TTT_TRACE_EV(2, 12 + x, t);
         }
       }
@@ -928,8 +942,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t raw[64];
         tmem_ld64w(tS, raw);
         // allowed (k, q): k <= q and k < T; full tiles (qt > kt, whole key tile < T) skip the test
-        const bool full = (qt > kt) && (kt * kTile + kTile <= T);
+        // packed: query rows >= T are the next sequence's (local columns >= cmax are masked too)
+        const bool full = (qt > kt) && (kt * kTile + kTile <= T) && (!p.packed || qt * kTile + kTile <= T);
         const int cmin = (k < T) ? k - qt * kTile - 64 * x : kTile;  // local columns [cmin, 64) allowed
+        const unsigned span = (unsigned)max((p.packed ? T - qt * kTile - 64 * x : kTile) - cmin, 0);  // [cmin, cmin + span)
 #pragma unroll
         for (int c4 = 0; c4 < 16; ++c4) {
           const float4 l4 = Lq[c4];
@@ -951,7 +967,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int c = 4 * c4 + e;
-            pr[c] = (full || c >= cmin) ? ys[e] : 0.f;  // P = exp(S c - lse)
+            pr[c] = (full || (unsigned)(c - cmin) < span) ? ys[e] : 0.f;  // P = exp(S c - lse)
           }
         }
       }
@@ -1051,7 +1067,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const float4 val = *reinterpret_cast<const float4*>(stg + (tsr * NCH + c / 8) * 16384 + lr * 128 +
                                                               (((c & 7) ^ (lr & 7)) << 4));
           if (kk < T)
-            red_add_v4(dst + (((size_t)b * p.L + kk) * p.Hkv + g) * D + x * (D / 2) + c * 4, val.x, val.y, val.z,
+            red_add_v4(dst + (((size_t)p.row0[b] + kk) * p.Hkv + g) * D + x * (D / 2) + c * 4, val.x, val.y, val.z,
                        val.w);
         }
       }
@@ -1078,7 +1094,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars.dq_empty);
       if (threadIdx.x == 0) TTT_TRACE_EV(2, 2, t);
-      const int row_base = (((b * p.Hq + h) * p.nqt + qt) * (D / 32)) * 128 + wq * 32;
+      const int row_base = (int)(dq_tile(p, b, h, qt) * (D / 32)) * 128 + wq * 32;
 #if TTT_BWD_DQ_RED
       {  // dev variant: reduce-add straight from registers (LSU path; the TMA unit then only loads)
         float* dst = p.dq_acc + (size_t)(row_base + lane) * 32;
@@ -1128,13 +1144,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 __global__ void __launch_bounds__(256) ttt_bwd_dq_convert_kernel(const __grid_constant__ Params p) {
   // thread -> (row, 8-column chunk); rows (b L + r) Hq + h in 32-bit (B L Hq < 2^31)
   const uint32_t d8 = (uint32_t)p.D / 8, rows_per_block = blockDim.x / d8;
-  const uint32_t nrows = (uint32_t)p.B * p.L * p.Hq;
+  const uint32_t nrows = (uint32_t)p.nrows * p.Hq;
   const int d = (int)(threadIdx.x % d8) * 8;
   for (uint32_t row = blockIdx.x * rows_per_block + threadIdx.x / d8; row < nrows; row += gridDim.x * rows_per_block) {
     const uint32_t bl = row / (uint32_t)p.Hq;
     const int h = (int)(row - bl * (uint32_t)p.Hq);
-    const int b = (int)(bl / (uint32_t)p.L);
-    const int r = (int)(bl - (uint32_t)b * (uint32_t)p.L);
+    const int b = seq_of_row(p, (int)bl);
+    const int r = (int)bl - p.row0[b];
     const float4* src = reinterpret_cast<const float4*>(p.dq_acc + dqacc_index(p, b, h, r, d));
     const float4 a = src[0], c = src[1];
     uint4 o;
@@ -1147,7 +1163,7 @@ __global__ void __launch_bounds__(256) ttt_bwd_dq_convert_kernel(const __grid_co
 }
 
 int pick_head_split(const Params& p) {
-  const int base = p.nqt * p.B * p.Hkv;
+  const int base = p.ntiles * p.Hkv;
   int hs = 1;
   while (hs < p.G && base * hs < 2 * 148) {
     int nx = hs + 1;
@@ -1186,9 +1202,20 @@ bool pre_layout(const Params& p, int D, PreLayout* lay) {
 
 // dK_0 / dV_0 are accumulated by the main kernel; overwrite mode starts them at zero
 cudaError_t zero_dkv0(const Params& p, int D, cudaStream_t st) {
-  const size_t kvb = (size_t)p.B * p.L * p.Hkv * D * sizeof(float);
+  const size_t kvb = (size_t)p.nrows * p.Hkv * D * sizeof(float);
   cudaError_t e = cudaMemsetAsync(p.dk, 0, kvb, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(p.dv, 0, kvb, st);
+  return e;
+}
+
+// packed layout: the delta / lse2 rows >= T_b of each sequence's last tile are never written by the
+// pre-pass, but the main kernel bulk-loads whole 128-row tiles of them (masked columns: P = 0, and
+// dS = P (dP - Delta) needs a finite Delta) -> zero both workspaces first
+cudaError_t zero_packed_ws(const Params& p, cudaStream_t st) {
+  if (!p.packed) return cudaSuccess;
+  const size_t bytes = (size_t)p.Hq * p.ntiles * kTile * sizeof(float);
+  cudaError_t e = cudaMemsetAsync(p.delta, 0, bytes, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.lse2, 0, bytes, st);
   return e;
 }
 
@@ -1200,7 +1227,7 @@ cudaError_t launch_pre(const Params& p, const PreMaps& pmaps, const UnrollPre& u
   cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)lay.total);
   if (e != cudaSuccess) return e;
-  const int rows = p.B * p.L * p.Hkv;
+  const int rows = p.nrows * p.Hkv;
   const int groups = (rows + lay.NR - 1) / lay.NR;
   UnrollPre u = up;
   if (U) u.M = std::max(lay.NS, 4);  // >= NS: the ring's own wait orders a group's steps
@@ -1215,7 +1242,7 @@ template <int D>
 cudaError_t launch_main_convert(const Params& p_in, const BwdMaps& maps, cudaStream_t st, bool convert = true) {
   Params p = p_in;
   p.head_split = pick_head_split(p);
-  {  // CTA order: CTA kt of a group runs (nqt - kt) items of G / head_split heads; ~4.5k clk per
+  if (!p.packed) {  // CTA order: CTA kt of a group runs (nqt - kt) items of G / head_split heads; ~4.5k clk per
      // item and ~12k of fixed cost (measured traces); a group's Q, dO, dq_acc: 8 B per q element
     std::vector<double> len(p.nqt);
     const int nh = p.G / p.head_split;
@@ -1228,7 +1255,7 @@ cudaError_t launch_main_convert(const Params& p_in, const BwdMaps& maps, cudaStr
     static std::atomic<unsigned long long> attr_done{0};
     cudaError_t ea = set_smem_attr(ttt_bwd_sm100_kernel<D>, smem, attr_done);
     if (ea != cudaSuccess) return ea;
-    const int grid = p.nqt * p.B * p.Hkv * p.head_split;
+    const int grid = p.ntiles * p.Hkv * p.head_split;  // padded: ntiles = B nqt
     prof_mark(kKindBwdMain, true, st);
     ttt_bwd_sm100_kernel<D><<<grid, kBwdThreads, smem, st>>>(p, maps);
     prof_mark(kKindBwdMain, false, st);
@@ -1236,7 +1263,7 @@ cudaError_t launch_main_convert(const Params& p_in, const BwdMaps& maps, cudaStr
     if (e != cudaSuccess) return e;
   }
   if (convert) {
-    const size_t n8 = (size_t)p.B * p.L * p.Hq * D / 8;
+    const size_t n8 = (size_t)p.nrows * p.Hq * D / 8;
     unsigned blocks = (unsigned)((n8 + 255) / 256);
     if (blocks > 148u * 8u) blocks = 148u * 8u;
     prof_mark(kKindBwdConvert, true, st);
@@ -1251,6 +1278,7 @@ template <int D>
 cudaError_t launch_bwd_d(const Params& p, const BwdMaps& maps, const PreMaps& pmaps, cudaStream_t st) {
   cudaError_t e = p.accumulate ? cudaSuccess : zero_dkv0(p, D, st);
   static const UnrollPre kNoUnroll{};
+  if (e == cudaSuccess) e = zero_packed_ws(p, st);
   if (e == cudaSuccess) e = launch_pre<D, false>(p, pmaps, kNoUnroll, st);
   if (e == cudaSuccess) e = launch_main_convert<D>(p, maps, st);
   return e;
@@ -1265,6 +1293,7 @@ cudaError_t launch_bwd_unroll_d(const Params* ps, const BwdMaps* maps, const Pre
   const int S = up.S;
   const Params& last = ps[S - 1];
   cudaError_t e = last.accumulate ? cudaSuccess : zero_dkv0(last, D, st);
+  for (int j = 0; j < S && e == cudaSuccess; ++j) e = zero_packed_ws(ps[j], st);
   if (e == cudaSuccess) e = launch_pre<D, true>(last, pmaps, up, st);
   for (int j = S - 1; j >= 0 && e == cudaSuccess; --j) e = launch_main_convert<D>(ps[j], maps[j], st);
   return e;

@@ -24,14 +24,16 @@ __global__ void __launch_bounds__(256) fwd_check_kernel(const Params p) {
   constexpr int E = D / 32;
   const int lane = threadIdx.x & 31;
   const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const long rows = (long)p.B * p.Hq * p.L;
+  const long rows = (long)p.nrows * p.Hq;
   if (warp >= rows) return;
-  const int r = (int)(warp % p.L);
-  const int h = (int)((warp / p.L) % p.Hq);
-  const int b = (int)(warp / ((long)p.L * p.Hq));
+  // warp -> (head h, row of the [rows][H][D] view) -> (sequence b, position r); padded or packed
+  const int grow = (int)(warp % p.nrows);
+  const int h = (int)(warp / p.nrows);
+  const int b = seq_of_row(p, grow);
+  const int r = grow - p.row0[b];
   const int g = h / p.G;
   const int T = p.seq_lens[b];
-  const float* qrow = (const float*)p.q + (((size_t)b * p.L + r) * p.Hq + h) * D;
+  const float* qrow = (const float*)p.q + ((size_t)grow * p.Hq + h) * D;
   float qv[E], acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -52,21 +54,21 @@ __global__ void __launch_bounds__(256) fwd_check_kernel(const Params p) {
     m = mn;
   };
   const size_t kv_stride = (size_t)p.Hkv * D;
-  const float* K0 = (const float*)p.k + ((size_t)b * p.L * p.Hkv + g) * D;
-  const float* V0 = (const float*)p.v + ((size_t)b * p.L * p.Hkv + g) * D;
+  const float* K0 = (const float*)p.k + ((size_t)p.row0[b] * p.Hkv + g) * D;
+  const float* V0 = (const float*)p.v + ((size_t)p.row0[b] * p.Hkv + g) * D;
   const int nbase = r < T ? r + 1 : T;
   for (int k = 0; k < nbase; ++k) visit(K0 + k * kv_stride, V0 + k * kv_stride);
   if (r < T) {
     for (int i = 0; i < p.step; ++i) {
-      const size_t off = (((size_t)b * p.L + r) * p.Hkv + g) * D;
+      const size_t off = ((size_t)grow * p.Hkv + g) * D;
       visit((const float*)p.ks[i] + off, (const float*)p.vs[i] + off);
     }
   }
-  float* orow = (float*)p.out + (((size_t)b * p.L + r) * p.Hq + h) * D;
+  float* orow = (float*)p.out + ((size_t)grow * p.Hq + h) * D;
   const float inv = 1.f / l;
 #pragma unroll
   for (int e = 0; e < E; ++e) orow[lane + 32 * e] = acc[e] * inv;
-  if (lane == 0) p.lse[((size_t)b * p.Hq + h) * p.L + r] = m + logf(l);
+  if (lane == 0) p.lse[lse_at(p, b, h, r)] = m + logf(l);
 }
 
 template <int D>
@@ -74,14 +76,16 @@ __global__ void __launch_bounds__(256) bwd_check_kernel(const Params p) {
   constexpr int E = D / 32;
   const int lane = threadIdx.x & 31;
   const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const long rows = (long)p.B * p.Hq * p.L;
+  const long rows = (long)p.nrows * p.Hq;
   if (warp >= rows) return;
-  const int r = (int)(warp % p.L);
-  const int h = (int)((warp / p.L) % p.Hq);
-  const int b = (int)(warp / ((long)p.L * p.Hq));
+  // warp -> (head h, row of the [rows][H][D] view) -> (sequence b, position r); padded or packed
+  const int grow = (int)(warp % p.nrows);
+  const int h = (int)(warp / p.nrows);
+  const int b = seq_of_row(p, grow);
+  const int r = grow - p.row0[b];
   const int g = h / p.G;
   const int T = p.seq_lens[b];
-  const size_t qoff = (((size_t)b * p.L + r) * p.Hq + h) * D;
+  const size_t qoff = ((size_t)grow * p.Hq + h) * D;
   const float* qrow = (const float*)p.q + qoff;
   const float* orow = (const float*)p.o + qoff;
   const float* dorow = (const float*)p.dout + qoff;
@@ -95,7 +99,7 @@ __global__ void __launch_bounds__(256) bwd_check_kernel(const Params p) {
     dq[e] = 0.f;
   }
   delta = warp_sum(delta);  // Delta_r = dO_r . O_r
-  const float lse = p.lse_in[((size_t)b * p.Hq + h) * p.L + r];
+  const float lse = p.lse_in[lse_at(p, b, h, r)];
   // dK / dV contributions of every row meet in fp64 accumulators (workspace): an fp32 sum of up to
   // (rows x heads) terms in arbitrary order would drift past 1e-5 where the terms cancel
   auto visit = [&](const float* krow, const float* vrow, double* dkrow, double* dvrow) {
@@ -117,17 +121,17 @@ __global__ void __launch_bounds__(256) bwd_check_kernel(const Params p) {
     }
   };
   const size_t kv_stride = (size_t)p.Hkv * D;
-  const size_t base = ((size_t)b * p.L * p.Hkv + g) * D;
+  const size_t base = ((size_t)p.row0[b] * p.Hkv + g) * D;
   const float* K0 = (const float*)p.k + base;
   const float* V0 = (const float*)p.v + base;
-  const size_t kv_elems = (size_t)p.B * p.L * p.Hkv * D;
+  const size_t kv_elems = (size_t)p.nrows * p.Hkv * D;
   double* dk0 = p.dacc;
   double* dv0 = p.dacc + kv_elems;
   const int nbase = r < T ? r + 1 : T;
   for (int k = 0; k < nbase; ++k)
     visit(K0 + k * kv_stride, V0 + k * kv_stride, dk0 + base + k * kv_stride, dv0 + base + k * kv_stride);
   if (r < T) {
-    const size_t off = (((size_t)b * p.L + r) * p.Hkv + g) * D;
+    const size_t off = ((size_t)grow * p.Hkv + g) * D;
     for (int i = 0; i < p.step; ++i)
       visit((const float*)p.ks[i] + off, (const float*)p.vs[i] + off, p.dacc + (2 + i) * kv_elems + off,
             p.dacc + (2 + p.step + i) * kv_elems + off);
@@ -150,7 +154,7 @@ __global__ void check_dkv_finalize_kernel(const Params p, size_t kv_elems) {
   }
 }
 
-size_t check_bwd_ws_bytes(const Params& p) { return (size_t)(2 + 2 * p.step) * p.B * p.L * p.Hkv * p.D * 8; }
+size_t check_bwd_ws_bytes(const Params& p) { return (size_t)(2 + 2 * p.step) * p.nrows * p.Hkv * p.D * 8; }
 
 __global__ void zero_f32_kernel(float* __restrict__ x, size_t n) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -169,7 +173,7 @@ cudaError_t launch_zero_f32(float* x, size_t n, cudaStream_t st) {
 }
 
 cudaError_t launch_fwd_check(const Params& p, cudaStream_t st) {
-  const long rows = (long)p.B * p.Hq * p.L;
+  const long rows = (long)p.nrows * p.Hq;
   const int blocks = (int)((rows + 7) / 8);
   prof_mark(kKindCheckFwd, true, st);
   if (p.D == 64) fwd_check_kernel<64><<<blocks, 256, 0, st>>>(p);
@@ -243,7 +247,7 @@ cudaError_t launch_tree_check(const Params& p, cudaStream_t st) {
 }
 
 cudaError_t launch_bwd_check(const Params& p, cudaStream_t st) {
-  const long rows = (long)p.B * p.Hq * p.L;
+  const long rows = (long)p.nrows * p.Hq;
   const int blocks = (int)((rows + 7) / 8);
   cudaError_t e = cudaMemsetAsync(p.dacc, 0, check_bwd_ws_bytes(p), st);
   if (e != cudaSuccess) return e;
@@ -253,7 +257,7 @@ cudaError_t launch_bwd_check(const Params& p, cudaStream_t st) {
   prof_mark(kKindCheckBwd, false, st);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t kv_elems = (size_t)p.B * p.L * p.Hkv * p.D;
+  const size_t kv_elems = (size_t)p.nrows * p.Hkv * p.D;
   check_dkv_finalize_kernel<<<148 * 8, 256, 0, st>>>(p, kv_elems);
   return cudaGetLastError();
 }

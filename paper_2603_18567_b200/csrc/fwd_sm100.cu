@@ -120,6 +120,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     qt = 0;
     g = gi % p.Hkv;
     b = gi / p.Hkv;
+  } else if (p.packed) {
+    // packed: (tile, kv head) with the kv head fastest; each sequence's q tiles longest first
+    g = t_ % p.Hkv;
+    const int tt = t_ / p.Hkv;
+    b = seq_of_tile(p, tt);
+    qt = p.tile0[b + 1] - 1 - (tt - p.tile0[b]);
   } else {
 #ifdef TTT_ORDER_GROUP
     qt = p.nqt - 1 - t_ % p.nqt;
@@ -151,6 +157,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     nkv = min(qt + 1, (T + kTile - 1) / kTile);  // BlockMask: skip k0 > q0+127 and k0 >= T
   }
   const int bst = TREE ? split * p.B + b : b;  // batch index of this CTA's out / lse rows
+  // TMA (row, batch) origin of this sequence: (0, b) padded, (row0[b], 0) packed (TREE: never packed)
+  const int ry = p.packed ? p.row0[b] : 0, by = p.packed ? 0 : b;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.q, 1);
@@ -198,8 +206,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_expect_tx(&bars.q, (has1 ? 2 : 1) * TB);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx) {
-          tma_load_4d(sQ + bx * 16384, &maps.q, &bars.q, bx * 64, h0, qt * kTile, b);
-          if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.q, &bars.q, bx * 64, h0 + 1, qt * kTile, b);
+          tma_load_4d(sQ + bx * 16384, &maps.q, &bars.q, bx * 64, h0, ry + qt * kTile, by);
+          if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.q, &bars.q, bx * 64, h0 + 1, ry + qt * kTile, by);
         }
       }
       for (int n = 0; n < nkv; ++n) {
@@ -208,12 +216,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_expect_tx(&bars.k_full[st], TB);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, g, (kvt0 + n) * kTile, b);
+          tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, g, ry + (kvt0 + n) * kTile, by);
         mbar_wait(&bars.v_empty[st], ph ^ 1);
         mbar_expect_tx(&bars.v_full[st], TB);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, (kvt0 + n) * kTile, b);
+          tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, ry + (kvt0 + n) * kTile, by);
       }
       if (!TREE && p.step > 0) {  // diagonal partial of the two heads into the Q tiles once no S MMA
                                   // reads them and the diagonal warps have written it
@@ -222,8 +230,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_expect_tx(&bars.od, (has1 ? 2 : 1) * TB);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx) {
-          tma_load_4d(sQ + bx * 16384, &maps.out, &bars.od, bx * 64, h0, qt * kTile, b);
-          if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.out, &bars.od, bx * 64, h0 + 1, qt * kTile, b);
+          tma_load_4d(sQ + bx * 16384, &maps.out, &bars.od, bx * 64, h0, ry + qt * kTile, by);
+          if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.out, &bars.od, bx * 64, h0 + 1, ry + qt * kTile, by);
         }
       }
     }
@@ -329,8 +337,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               const int r0 = qt * kTile + rb * kDgRows;
 #pragma unroll
               // one box per tensor: 16 rows x D columns, no swizzle (rows of D x 2 bytes)
-              tma_load_4d(base, &maps.kd[i], &bars.dg_full[st], 0, g, r0, b);
-              tma_load_4d(base + NBOX * DGB, &maps.vd[i], &bars.dg_full[st], 0, g, r0, b);
+              tma_load_4d(base, &maps.kd[i], &bars.dg_full[st], 0, g, ry + r0, by);
+              tma_load_4d(base + NBOX * DGB, &maps.vd[i], &bars.dg_full[st], 0, g, ry + r0, by);
               TTT_TRACE_EV(3, 3, n);
             }
         }
@@ -450,7 +458,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               if (hs == 0 || has1) {
                 const float inv = 1.f / l[hs];
                 __nv_bfloat16* orow =
-                    reinterpret_cast<__nv_bfloat16*>(p.out) + (((size_t)b * p.L + r) * p.Hq + h0 + hs) * D;
+                    reinterpret_cast<__nv_bfloat16*>(p.out) + (((size_t)p.row0[b] + r) * p.Hq + h0 + hs) * D;
 #pragma unroll
                 for (int bx = 0; bx < NBOX; ++bx) {
                   uint4 w;
@@ -637,7 +645,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // The j diagonal keys of row r (Alg. 1 "concat s_i") were reduced
       // by the diagonal warps into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum); the
       // merge is the same online-softmax update as one more "tile".
-      const size_t lse_idx = ((size_t)bst * p.Hq + h) * p.L + r;
+      const size_t lse_idx = TREE ? ((size_t)bst * p.Hq + h) * p.L + r : lse_at(p, b, h, r);
       const bool has_diag = !TREE && (r < T) && (p.step > 0);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, 0);
       mbar_wait(&bars.o_full[slot], 0);
@@ -663,6 +671,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // the combine pass)
       const float inv_l = (TREE && l_f == 0.f) ? 0.f : 1.f / l_f;
       const float a_n = alpha * inv_l, b_n = beta * inv_l;
+      // packed layout, the sequence's last (partial) tile: rows >= T belong to the next sequence, so
+      // each thread stores its own row (r < T) straight to global instead of the 128-row TMA boxes
+      const bool direct = !TREE && p.packed && (qt * kTile + kTile > T);
+      __nv_bfloat16* const orow = direct ? reinterpret_cast<__nv_bfloat16*>(p.out) + ((size_t)(ry + r) * p.Hq + h) * D : nullptr;
+      __nv_bfloat16* const lrow = direct && p.out_lo ? reinterpret_cast<__nv_bfloat16*>(p.out_lo) + ((size_t)(ry + r) * p.Hq + h) * D : nullptr;
       // per 64-column box: one 64-column TMEM load (a single wait), the box written to the staging tile,
       // then its TMA store issued right away so it drains under the next box's math (measured: the
       // epilogue, o_full -> CTA end, took ~8k clk with four 32-column load waits and one store at the end)
@@ -691,7 +704,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           w.y = pack_bf16(v[2], v[3]);
           w.z = pack_bf16(v[4], v[5]);
           w.w = pack_bf16(v[6], v[7]);
-          *reinterpret_cast<uint4*>(st_hi + soff) = w;
+          if (direct) {
+            if (r < T) *reinterpret_cast<uint4*>(orow + bx * 64 + q4 * 8) = w;
+          } else {
+            *reinterpret_cast<uint4*>(st_hi + soff) = w;
+          }
           if (p.out_lo) {  // residual O - bf16(O), so the backward's Delta sees ~16-bit O
             const uint32_t hi[4] = {w.x, w.y, w.z, w.w};
             uint32_t lo[4];
@@ -700,9 +717,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hi[e]));
               lo[e] = pack_bf16(v[2 * e] - hf.x, v[2 * e + 1] - hf.y);
             }
-            *reinterpret_cast<uint4*>(st_lo + soff) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            if (direct) {
+              if (r < T) *reinterpret_cast<uint4*>(lrow + bx * 64 + q4 * 8) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            } else {
+              *reinterpret_cast<uint4*>(st_lo + soff) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            }
           }
         }
+        if (direct) continue;
         fence_async_smem();
         named_bar_sync(1 + slot, 128);
         if (row == 0) {
@@ -710,14 +732,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             for (int k = 2 * slot; k < min(2 * slot + 2, nheads); ++k)
               tma_store_4d(&maps.out, st_hi + bx * 16384 + (k & 1) * 8192, bx * 64, h0 + k, 0, bst);
           } else {
-            tma_store_4d(&maps.out, st_hi + bx * 16384, bx * 64, h, qt * kTile, bst);
-            if (p.out_lo) tma_store_4d(&maps.out_lo, st_lo + bx * 16384, bx * 64, h, qt * kTile, b);
+            tma_store_4d(&maps.out, st_hi + bx * 16384, bx * 64, h, ry + qt * kTile, by);
+            if (p.out_lo) tma_store_4d(&maps.out_lo, st_lo + bx * 16384, bx * 64, h, ry + qt * kTile, by);
           }
           bulk_commit();
         }
       }
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 6, 0);
-      if (!TREE || tree_row) p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
+      if ((!TREE || tree_row) && !(p.packed && r >= T)) p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
       if (row == 0) {
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 8, 0);
         bulk_wait_read0();  // smem must stay valid until the bulk engine has read it
@@ -988,7 +1010,7 @@ bool diag_layout(const Params& p, int D, DiagLayout* lay) {
 template <int D>
 cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps& dmaps, cudaStream_t st) {
   Params p = p_in;
-  {  // CTA order: the CTA of q tile qt runs qt + 1 kv tiles (~3.3k clk each) plus ~7k clk of fixed
+  if (!p.packed) {  // CTA order: the CTA of q tile qt runs qt + 1 kv tiles (~3.3k clk each) plus ~7k clk of fixed
      // cost (measured traces); a (b, g) group's K / V: 4 B per kv element
     std::vector<double> len(p.nqt);
     for (int r = 0; r < p.nqt; ++r) len[r] = (double)(p.nqt - r) * 3.3;
@@ -1001,6 +1023,7 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
     if (e != cudaSuccess) return e;
   }
 #if !TTT_FWD_FUSED_DIAG
+  if (p.packed) return cudaErrorNotSupported;  // the dev-only separate pass knows the padded layout only
   if (p.step > 0) {  // dev A/B: the separate diagonal pre-pass of round 1
     DiagLayout lay;
     if (!diag_layout(p, D, &lay)) return cudaErrorInvalidConfiguration;
@@ -1017,7 +1040,7 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
   (void)dmaps;
 #endif
   const int npairs = (p.G + 1) / 2;
-  const int grid = p.nqt * p.B * p.Hkv * npairs;
+  const int grid = p.ntiles * p.Hkv * npairs;  // padded: ntiles = B nqt
   prof_mark(kKindFwdMain, true, st);
   ttt_fwd_sm100_kernel<D, false><<<grid, kFwdThreads, smem, st>>>(p, maps);
   prof_mark(kKindFwdMain, false, st);

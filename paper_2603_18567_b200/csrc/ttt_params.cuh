@@ -48,6 +48,17 @@ struct Params {
   // fp32 check path backward: fp64 accumulators [dK_0 | dV_0 | dK_1..dK_j | dV_1..dV_j] (workspace)
   double* dacc;
   int seq_lens[TTT_MAX_BATCH];
+  // Row layout. Padded: [B][L][H][D], row0[b] = b L, tile0[b] = b nqt. Packed (desc.cu_seqlens):
+  // one [nrows][H][D] view, sequence b = rows [row0[b], row0[b] + T_b) with no padding, its
+  // 128-row tiles numbered from tile0[b]; the tensor maps then have batch extent 1; lse is
+  // [Hq][nrows]. The delta / lse2 workspaces are [Hq][ntiles][128] in both layouts (padded: the
+  // same as [B][Hq][L]), so the main kernel's 128-row bulk loads start 512-B aligned; packed, the
+  // rows >= T_b of a sequence's last tile are zeroed before the pre-pass.
+  int packed;
+  int nrows;   // rows of the [rows][H][D] view (B L or sum T_b)
+  int ntiles;  // 128-row tiles over all sequences (B nqt or sum ceil(T_b / 128))
+  int row0[TTT_MAX_BATCH + 1];
+  int tile0[TTT_MAX_BATCH + 1];
   // tree-attention verification (ttt_tree_attn_fwd): seq_lens = prefix lengths, L = tree size
   int tree_n;                              // n tree tokens (queries), <= 64
   const unsigned long long* tree_mask;     // [B][n] ancestor-or-self bit masks (bit u = tree key u)
@@ -55,6 +66,40 @@ struct Params {
   int tree_kv_len;                         // rows of the K / V cache (check path)
   const int32_t* tree_parents;             // [B][n] parent indices (check path)
 };
+
+#ifdef __CUDACC__
+// ---- row-layout helpers (padded / packed; see Params) ----
+// TMA coordinates of row r of sequence b: (row, batch) = (r, b) padded, (row0[b] + r, 0) packed
+__device__ __forceinline__ int tma_row(const Params& p, int b, int r) { return p.packed ? p.row0[b] + r : r; }
+__device__ __forceinline__ int tma_bat(const Params& p, int b) { return p.packed ? 0 : b; }
+// index of lse[b][h][r] (padded [B][Hq][L], packed [Hq][nrows]) and of the delta / lse2 workspaces
+__device__ __forceinline__ size_t lse_at(const Params& p, int b, int h, int r) {
+  return p.packed ? (size_t)h * p.nrows + p.row0[b] + r : ((size_t)b * p.Hq + h) * p.L + r;
+}
+// 128-row tile (b, h, tile t of the sequence) of the dq accumulator and the delta / lse2 workspaces
+__device__ __forceinline__ size_t dq_tile(const Params& p, int b, int h, int t) {
+  return p.packed ? (size_t)h * p.ntiles + p.tile0[b] + t : ((size_t)b * p.Hq + h) * p.nqt + t;
+}
+__device__ __forceinline__ size_t ws_at(const Params& p, int b, int h, int r) {
+  return dq_tile(p, b, h, r >> 7) * 128 + (r & 127);
+}
+// sequence of a global row / tile: b with row0[b] <= x < row0[b + 1] (binary search when packed)
+__device__ __forceinline__ int seq_search(const int* start, int B, int x) {
+  int lo = 0, hi = B - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ int seq_of_row(const Params& p, int row) {
+  return p.packed ? seq_search(p.row0, p.B, row) : row / p.L;
+}
+__device__ __forceinline__ int seq_of_tile(const Params& p, int t) {
+  return p.packed ? seq_search(p.tile0, p.B, t) : t / p.nqt;
+}
+#endif
 
 // Tensor maps for the tcgen05 paths (4-D: D, H, L, B; box 64 x 1 x 128 x 1, SW128)
 struct FwdMaps {

@@ -107,6 +107,56 @@ def make_case(shape: Shape, dtype: torch.dtype = torch.bfloat16, seed: int = 0,
     return c
 
 
+@dataclass
+class PackedCase:
+    """Host tensors of one unroll over a PACKED batch (sequence b = rows [cu[b], cu[b+1]),
+    include/ttt_attn.h cu_seqlens): q / dout per step [N,Hq,D], k / v lists [N,Hkv,D]."""
+    cu: np.ndarray
+    num_q_heads: int
+    num_kv_heads: int
+    head_dim: int
+    ttt_steps: int
+    dtype: torch.dtype
+    q: list = field(default_factory=list)
+    dout: list = field(default_factory=list)
+    k_base: torch.Tensor = None
+    v_base: torch.Tensor = None
+    k_steps: list = field(default_factory=list)
+    v_steps: list = field(default_factory=list)
+
+    @property
+    def rows(self) -> int:
+        return int(self.cu[-1])
+
+
+def make_packed_case(lens, num_q_heads: int, num_kv_heads: int, head_dim: int, ttt_steps: int,
+                     dtype: torch.dtype = torch.bfloat16, seed: int = 0) -> PackedCase:
+    """Same recipe as make_case (N(0,1) draws rounded to the storage dtype), packed rows."""
+    lens = np.asarray(lens, dtype=np.int64)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    N = int(cu[-1])
+    rng = np.random.default_rng(seed)
+    c = PackedCase(cu, num_q_heads, num_kv_heads, head_dim, ttt_steps, dtype)
+    kv, qs = (N, num_kv_heads, head_dim), (N, num_q_heads, head_dim)
+    c.k_base = to_storage(_normal(rng, kv), dtype)
+    c.v_base = to_storage(_normal(rng, kv), dtype)
+    for _ in range(max(ttt_steps - 1, 0)):
+        c.k_steps.append(to_storage(_normal(rng, kv), dtype))
+        c.v_steps.append(to_storage(_normal(rng, kv), dtype))
+    for _ in range(ttt_steps):
+        c.q.append(to_storage(_normal(rng, qs), dtype))
+    rng_do = np.random.default_rng(seed + 1)
+    for _ in range(ttt_steps):
+        c.dout.append(to_storage(_normal(rng_do, qs), dtype))
+    return c
+
+
+def packed_lens(n: int, max_len: int, seed: int) -> np.ndarray:
+    """Lengths of a packed batch: T_b ~ U[max_len/4, max_len] (the padded recipe's mix, seed + 2)."""
+    rng = np.random.default_rng(seed + 2)
+    return rng.integers(max(1, max_len // 4), max_len + 1, size=n, dtype=np.int64)
+
+
 def sample_rows(shape: Shape, n_per_head: int, seed: int) -> np.ndarray:
     """Boolean row selector [B, Hq, L] with n_per_head random rows per (b, h),
     always including rows 0 and L-1 (the ends of the causal range)."""

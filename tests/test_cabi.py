@@ -81,6 +81,32 @@ def test_alignment_and_null():
     assert ei.value.code == 1
 
 
+@pytest.mark.parametrize("cu,seq_lens,code", [
+    ([0, 3, 3, 9], None, 5),                   # empty sequence
+    ([1, 3, 9], None, 1),                      # cu_seqlens[0] != 0
+    ([0, 5, 9], [5, 4], 1),                    # seq_lens and cu_seqlens both given
+    ([0, 40000000, 80000000], None, 2),        # N x Hq >= 2^31
+])
+def test_packed_validation_codes(cu, seq_lens, code):
+    d = ttt.make_desc(len(cu) - 1, 128, 32, 8, 128, seq_lens=seq_lens, cu_seqlens=cu)
+    with pytest.raises(ttt.TTTError) as ei:
+        _fwd(d, 0)
+    assert ei.value.code == code
+
+
+def test_packed_desc_and_workspace():
+    cu = [0, 5, 133, 300, 301]
+    d = ttt.packed_desc(cu, 4, 2, 64)
+    assert d.packed_rows == 301 and d.batch == 4 and d.seq_len == 167
+    tiles = 1 + 1 + 2 + 1  # T_b = 5, 128, 167, 1
+    assert ttt.ttt_attn_workspace_size(d, 2, True) >= 2 * 4 * tiles * 128 * 4 + 4 * tiles * 128 * 64 * 4
+    assert ttt.ttt_attn_workspace_size(d, 2, False) == 0
+    fp = ttt.packed_desc(cu, 4, 2, 64, dtype=ttt.TTT_FP32_CHECK)
+    assert ttt.ttt_attn_workspace_size(fp, 2, True) == (2 + 2 * 2) * 301 * 2 * 64 * 8
+    with pytest.raises(ttt.TTTError):
+        ttt.make_desc(2, 128, 4, 2, 64, cu_seqlens=[0, 5])  # batch + 1 entries needed
+
+
 def test_workspace_size():
     d = ttt.make_desc(8, 2048, 32, 8, 128)
     ws = ttt.ttt_attn_workspace_size(d, 6, True)
