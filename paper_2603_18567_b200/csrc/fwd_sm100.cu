@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     g = t_ % p.Hkv;
     const int tt = t_ / p.Hkv;
     b = seq_of_tile(p, tt);
-    qt = p.tile0[b + 1] - 1 - (tt - p.tile0[b]);
+    qt = p.tile0[b + 1] - 1 - tt;  // local tile: nqt_b - 1 - (tt - tile0[b])
   } else {
 #ifdef TTT_ORDER_GROUP
     qt = p.nqt - 1 - t_ % p.nqt;
