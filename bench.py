@@ -206,27 +206,42 @@ def workload_config(shape: Shape, world: int, cfg: str = "llama8b"):
 class Unroll:
     """Device buffers of one per-GPU unroll + the C-ABI calls of one step."""
 
-    def __init__(self, shape: Shape, seed: int, dev, bwd_unroll: bool = False):
+    def __init__(self, shape: Shape, seed: int, dev, bwd_unroll: bool = False, seq_lens=None, packed: bool = False):
+        """seq_lens: T_b per sequence (padded layout [B][L] with those lengths, or with packed=True the
+        packed layout: the sequences back to back, [sum T_b][H][D], include/ttt_attn.h cu_seqlens)."""
         import paper_2603_18567_b200 as ttt
         self.ttt = ttt
         self.s = s = shape
         S = s.ttt_steps
+        if packed:
+            cu = [0]
+            for T in seq_lens:
+                cu.append(cu[-1] + int(T))
+            N = cu[-1]
+            q_shape, kv_shape, lse_shape = (N, s.num_q_heads, s.head_dim), (N, s.num_kv_heads, s.head_dim), \
+                (s.num_q_heads, N)
+        else:
+            q_shape, kv_shape, lse_shape = s.q_shape, s.kv_shape, (s.batch, s.num_q_heads, s.seq_len)
         g = torch.Generator(device=dev).manual_seed(seed)
         mk = lambda shp: torch.randn(shp, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
-        self.q = [mk(s.q_shape) for _ in range(S)]
-        self.do = [mk(s.q_shape) for _ in range(S)]
-        self.k, self.v = mk(s.kv_shape), mk(s.kv_shape)
-        self.ks = [mk(s.kv_shape) for _ in range(S - 1)]
-        self.vs = [mk(s.kv_shape) for _ in range(S - 1)]
-        self.out = [torch.empty(s.q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
-        self.out_lo = [torch.empty(s.q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
-        self.lse = [torch.empty(s.batch, s.num_q_heads, s.seq_len, device=dev) for _ in range(S)]
-        self.dq = [torch.empty(s.q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
-        z = lambda: torch.zeros(s.kv_shape, dtype=torch.float32, device=dev)
+        self.q = [mk(q_shape) for _ in range(S)]
+        self.do = [mk(q_shape) for _ in range(S)]
+        self.k, self.v = mk(kv_shape), mk(kv_shape)
+        self.ks = [mk(kv_shape) for _ in range(S - 1)]
+        self.vs = [mk(kv_shape) for _ in range(S - 1)]
+        self.out = [torch.empty(q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
+        self.out_lo = [torch.empty(q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
+        self.lse = [torch.empty(lse_shape, device=dev) for _ in range(S)]
+        self.dq = [torch.empty(q_shape, dtype=torch.bfloat16, device=dev) for _ in range(S)]
+        z = lambda: torch.zeros(kv_shape, dtype=torch.float32, device=dev)
         self.dk, self.dv = z(), z()
         self.dks = [z() for _ in range(S - 1)]
         self.dvs = [z() for _ in range(S - 1)]
-        self.desc = ttt.make_desc(s.batch, s.seq_len, s.num_q_heads, s.num_kv_heads, s.head_dim)
+        if packed:
+            self.desc = ttt.packed_desc(cu, s.num_q_heads, s.num_kv_heads, s.head_dim)
+        else:
+            self.desc = ttt.make_desc(s.batch, s.seq_len, s.num_q_heads, s.num_kv_heads, s.head_dim,
+                                      seq_lens=seq_lens)
         self.ws = torch.empty(ttt.ttt_attn_workspace_size(self.desc, S - 1, True), dtype=torch.uint8, device=dev)
         self.inputs = self.q + self.do + [self.k, self.v] + self.ks + self.vs
         # every result of the unroll (what a caller reads back): out_j, lse_j, dq_j, dK_0, dV_0, dK_i, dV_i
@@ -431,6 +446,7 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         line["next_rows"] = {"loss_inplace": run_loss(args, stream, peaks, world)}
         if world == 1:
             line["next_rows"]["longctx"] = run_longctx(args, stream, peaks)
+            line["next_rows"]["packed"] = run_packed(args, stream, peaks)
             line["next_rows"]["qwen235b"] = run_config(
                 "qwen235b", stream, peaks,
                 "Qwen3-235B-A22B draft shape (BASELINE configs[2]): 1 x L=4096, 64/4 heads, D=128, ttt_steps=7, bf16")
@@ -631,6 +647,42 @@ def run_config(name: str, stream, peaks, workload: str):
     torch.cuda.empty_cache()
     return {"workload": workload, "ms_per_step": ms, "tokens_per_s": shape.batch * shape.seq_len / (ms / 1e3),
             "steps": n, "tflops": tflops, "frac_of_bf16_peak": tflops / peaks["bf16_tflops_sustained"]}
+
+
+def run_packed(args, stream, peaks):
+    """the Llama-3.1-8B draft unroll over a PACKED batch (8 sequences with the
+    paper's padded-conversation length mix T_b ~ U[L/4, L], L = 2048, back to back, cu_seqlens) beside
+    the same sequences in the padded layout (B x L with seq_lens). Throughput counts valid tokens;
+    the FLOP count is the allowed pairs of the valid rows only (a padded row r >= T_b is work the
+    packed layout does not have)."""
+    from paper_2603_18567_b200.inputs import packed_lens
+    shape = CONFIGS["llama8b"]
+    lens = [int(x) for x in packed_lens(shape.batch, shape.seq_len, seed=0)]
+    valid = sum(lens)
+    pairs = sum(shape.num_q_heads * sum(T * (T + 1) // 2 + j * T for T in lens) for j in range(shape.ttt_steps))
+    res = {"workload": (f"Llama-3.1-8B draft heads, {shape.batch} sequences T_b ~ U[{shape.seq_len // 4}, "
+                        f"{shape.seq_len}] ({valid} valid tokens), ttt_steps=7, fwd + bwd unroll"),
+           "seq_lens": lens}
+    for mode in ("packed", "padded"):
+        u = Unroll(shape, seed=98, dev=stream.device, seq_lens=lens, packed=(mode == "packed"))
+        for _ in range(2):
+            u.step(stream)
+        torch.cuda.synchronize()
+        n = 3
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            u.step(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / n
+        tflops = 12 * shape.head_dim * pairs / (ms / 1e3) / 1e12
+        res[mode] = {"ms_per_step": ms, "valid_tokens_per_s": valid / (ms / 1e3), "tflops_valid": tflops,
+                     "frac_of_bf16_peak": tflops / peaks["bf16_tflops_sustained"],
+                     "input_bytes": sum(t.nbytes for t in u.inputs)}
+        del u
+        torch.cuda.empty_cache()
+    return res
 
 
 def run_longctx(args, stream, peaks):

@@ -40,11 +40,18 @@ class _TTTAttention(torch.autograd.Function):
         c = lambda t: t.contiguous()  # the C-ABI takes raw row-major pointers (views are copied here)
         q, k_base, v_base = c(q), c(k_base), c(v_base)
         k_steps, v_steps = [c(t) for t in kv_steps[:j]], [c(t) for t in kv_steps[j:2 * j]]
-        desc = L.desc_for(q, k_base, seq_lens=seq_lens, softmax_scale=scale)
-        B, Lq, Hq, D = q.shape
+        if isinstance(seq_lens, tuple):  # ("packed", cu_seqlens): q [N, Hq, D], K / V [N, Hkv, D]
+            N, Hq, D = q.shape
+            dt = L.TTT_FP32_CHECK if q.dtype == torch.float32 else L.TTT_BF16
+            desc = L.packed_desc(seq_lens[1], Hq, k_base.shape[1], D, dtype=dt, softmax_scale=scale)
+            lse_shape = (Hq, N)
+        else:
+            desc = L.desc_for(q, k_base, seq_lens=seq_lens, softmax_scale=scale)
+            B, Lq, Hq, D = q.shape
+            lse_shape = (B, Hq, Lq)
         out = torch.empty_like(q)
         out_lo = torch.empty_like(q) if q.dtype == torch.bfloat16 else None
-        lse = torch.empty((B, Hq, Lq), dtype=torch.float32, device=q.device)
+        lse = torch.empty(lse_shape, dtype=torch.float32, device=q.device)
         L.ttt_attn_fwd(desc, j, q, k_base, v_base, k_steps, v_steps, out, lse, out_lo=out_lo)
         ctx.j, ctx.desc = j, desc
         ctx.save_for_backward(q, k_base, v_base, out, lse, *([out_lo] if out_lo is not None else []),
@@ -77,14 +84,21 @@ class _TTTAttention(torch.autograd.Function):
 
 def ttt_attention(q: torch.Tensor, k_base: torch.Tensor, v_base: torch.Tensor,
                   k_steps: Sequence[torch.Tensor], v_steps: Sequence[torch.Tensor], step: int,
-                  seq_lens: Optional[Sequence[int]] = None, softmax_scale: float = 0.0) -> torch.Tensor:
+                  seq_lens: Optional[Sequence[int]] = None, softmax_scale: float = 0.0,
+                  cu_seqlens: Optional[Sequence[int]] = None) -> torch.Tensor:
     """Differentiable TTT attention of step ``step`` (uses k_steps[:step], v_steps[:step]).
-    BSHD tensors, contiguous, on the GPU: q [B, L, Hq, D], K/V [B, L, Hkv, D]."""
+    BSHD tensors, contiguous, on the GPU: q [B, L, Hq, D], K/V [B, L, Hkv, D]; or, with
+    ``cu_seqlens`` (B + 1 host offsets), a packed batch: q [N, Hq, D], K/V [N, Hkv, D]."""
     j = int(step)
     ks, vs = list(k_steps[:j]), list(v_steps[:j])
     if len(ks) != j or len(vs) != j:
         raise ValueError(f"step {j} needs {j} step K/V tensors, got {len(ks)} / {len(vs)}")
-    lens = None if seq_lens is None else [int(x) for x in seq_lens]
+    if cu_seqlens is not None:
+        if seq_lens is not None:
+            raise ValueError("pass seq_lens (padded) or cu_seqlens (packed), not both")
+        lens = ("packed", tuple(int(x) for x in cu_seqlens))
+    else:
+        lens = None if seq_lens is None else [int(x) for x in seq_lens]
     return _TTTAttention.apply(j, lens, float(softmax_scale), q, k_base, v_base, *ks, *vs)
 
 

@@ -171,3 +171,27 @@ def test_packed_llama_heads_sampled_rows(cuda_ok):
         assert_close(f"seq {b} out", np32(out[r0:r1]), o_out, **TOL_BF16)
         assert_close(f"seq {b} lse", np32(lse[:, r0:r1]), o_lse, **TOL_BF16)
     assert not torch.isnan(lse).any(), "every lse row of every sequence must be written"
+
+
+def test_packed_autograd(cuda_ok):
+    """autograd.ttt_attention(..., cu_seqlens=...) over a packed batch: loss = sum(out * w) and its
+    gradients w.r.t. q and every K / V against the packed oracle's backward with dO = w."""
+    from paper_2603_18567_b200.autograd import ttt_attention
+    lens = [70, 1, 200]
+    Hq, Hkv, D, j = 4, 2, 64, 2
+    c = make_packed_case(lens, Hq, Hkv, D, j + 1, seed=9)
+    leaf = lambda t: t.cuda().clone().requires_grad_(True)
+    q, k, v = leaf(c.q[j]), leaf(c.k_base), leaf(c.v_base)
+    ks, vs = [leaf(x) for x in c.k_steps], [leaf(x) for x in c.v_steps]
+    w = c.dout[j].cuda()
+    out = ttt_attention(q, k, v, ks, vs, j, cu_seqlens=c.cu)
+    (out.float() * w.float()).sum().backward()
+    og = oracle.bwd_packed(*_oracle_in(c, j), np32(c.dout[j]), c.cu)
+    o_out, _ = oracle.fwd_packed(*_oracle_in(c, j), c.cu)
+    assert_close("autograd packed out", np32(out), o_out, **TOL_BF16)
+    assert_close("autograd packed dq", np32(q.grad), og["dq"], **TOL_BF16)
+    assert_close("autograd packed dk", np32(k.grad), og["dk_base"], **TOL_BF16)
+    assert_close("autograd packed dv", np32(v.grad), og["dv_base"], **TOL_BF16)
+    for i in range(j):
+        assert_close(f"autograd packed dk_{i + 1}", np32(ks[i].grad), og["dk_steps"][i], **TOL_BF16)
+        assert_close(f"autograd packed dv_{i + 1}", np32(vs[i].grad), og["dv_steps"][i], **TOL_BF16)
