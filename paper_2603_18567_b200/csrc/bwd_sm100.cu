@@ -81,7 +81,7 @@ __device__ __forceinline__ void load_bf16(const void* base, size_t off, float (&
 //   [B][Hq][L/128][D/32][128 rows][32 cols] fp32
 __device__ __forceinline__ size_t dqacc_index(const Params& p, int b, int h, int r, int d) {
   const int nc = p.D / 32;
-  return ((dq_tile(p, b, h, r >> 7) * nc + (d >> 5)) * 128 + (r & 127)) * 32 + (d & 31);
+  return ((dq_tile(p, p.packed, b, h, r >> 7) * nc + (d >> 5)) * 128 + (r & 127)) * 32 + (d & 31);
 }
 
 // ------------------------------------------------------------------ kernel 1
@@ -154,7 +154,7 @@ struct PreLayout {
 // reduce-adds: the item -> warp mapping depends on the group only and an element's (lane, register)
 // slot depends on (i, row, column) only, so both come from the same thread in program order
 // (a per-stage __threadfence here measured 20% of the pass's stall samples, r02a ncu).
-template <int D, bool U>
+template <int D, bool U, bool PACKED>
 __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
     ttt_bwd_pre_kernel(const __grid_constant__ Params p, const __grid_constant__ PreMaps maps,
                        const __grid_constant__ UnrollPre up, PreLayout lay) {
@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
   auto decode = [&](uint32_t w, int& b_, int& r_, int& g_) {  // w = (b L + r) Hkv + g
     const uint32_t bl = lay.div_hkv.div(w);
     g_ = (int)(w - bl * (uint32_t)p.Hkv);
-    b_ = p.packed ? seq_of_row(p, (int)bl) : (int)lay.div_L.div(bl);
-    r_ = (int)bl - p.row0[b_];
+    b_ = PACKED ? seq_of_row(p, true, (int)bl) : (int)lay.div_L.div(bl);
+    r_ = (int)bl - (PACKED ? p.row0[b_] : b_ * p.L);
   };
   uint8_t* scrP = psm + lay.off_scr + cw * 2560;  // [16 rows m][40] bf16 (80-B rows: conflict-free)
   uint8_t* scrS = scrP + 1280;
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
             if (m < mrows0 && k_first * R + wr0 < nv) {
               int b_, r_, g_;
               decode((uint32_t)(w0 + k_first * R + wr0), b_, r_, g_);
-              lse_pf[hf] = lse_in[lse_at(p, b_, g_ * G + hh0, r_)];
+              lse_pf[hf] = lse_in[lse_at(p, PACKED, b_, g_ * G + hh0, r_)];
             }
           }
         }
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
               decode((uint32_t)(w0 + min(lr0 + wr[hf], nv - 1)), bb[hf], rr[hf], gg[hf]);
               act[hf] = okr[hf] && rr[hf] < p.seq_lens[bb[hf]];
               l2[hf] = okr[hf] ? ((k == k_first && mt == 0) ? lse_pf[hf]
-                                                          : lse_in[lse_at(p, bb[hf], gg[hf] * G + hh[hf], rr[hf])]) *
+                                                          : lse_in[lse_at(p, PACKED, bb[hf], gg[hf] * G + hh[hf], rr[hf])]) *
                                      kLog2e
                                : 0.f;
             }
@@ -415,9 +415,9 @@ __global__ void __launch_bounds__(32 * (kPreCompute + 1), 1)
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
               const int h = gg[hf] * G + hh[hf];
-              qbase[hf] = ((dq_tile(p, bb[hf], h, rr[hf] >> 7) * (D / 32)) * 128 + (rr[hf] & 127)) * 32;
+              qbase[hf] = ((dq_tile(p, PACKED, bb[hf], h, rr[hf] >> 7) * (D / 32)) * 128 + (rr[hf] & 127)) * 32;
               if (okr[hf] && c4 == 0) {
-                const size_t li = ws_at(p, bb[hf], h, rr[hf]);
+                const size_t li = ws_at(p, PACKED, bb[hf], h, rr[hf]);
                 delta_p[li] = -del[hf];  // stored negated: the main kernel's FFMA2 / FADD2 consume -lse2, -Delta
                 lse2_p[li] = -l2[hf];
               }
@@ -602,7 +602,7 @@ struct BwdBars3 {
   uint32_t tmem_base;
 };
 
-template <int D>
+template <int D, bool PACKED>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     ttt_bwd_sm100_kernel(const __grid_constant__ Params p, const __grid_constant__ BwdMaps maps) {
   using SM = BwdSmem<D>;
@@ -628,12 +628,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // longest-first order — kv tile slowest — measured slower: 5.3 vs 5.26 ms bwd, 2.73-2.85 vs
   // 2.63-2.66 ms fwd per unroll in an interleaved A/B, bench_tools/ab.sh.)
   int kt, grp;
-  if (p.packed) {
+  if (PACKED) {
     // packed: (tile, kv head, head subset), head subsets fastest; each sequence's kv tiles in
     // ascending order (the longest CTAs of the sequence first)
     const int per = p.Hkv * p.head_split;
     const int tt = (int)blockIdx.x / per;
-    const int bq = seq_of_tile(p, tt);
+    const int bq = seq_of_tile(p, true, tt);
     kt = tt - p.tile0[bq];
     grp = bq * per + (int)blockIdx.x % per;
   } else {
@@ -657,9 +657,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int b = grp / (hsplit * p.Hkv);
   const int T = p.seq_lens[b];
   if (kt * kTile >= T) return;  // every key of the tile is padding: no gradient flows
-  const int nqt_b = p.packed ? p.tile0[b + 1] - p.tile0[b] : p.nqt;  // q tiles of this sequence
+  const int nqt_b = PACKED ? p.tile0[b + 1] - p.tile0[b] : p.nqt;  // q tiles of this sequence
   // TMA (row, batch) origin of this sequence: (0, b) padded, (row0[b], 0) packed
-  const int ry = p.packed ? p.row0[b] : 0, by = p.packed ? 0 : b;
+  const int ry = PACKED ? p.row0[b] : 0, by = PACKED ? 0 : b;
   const int nq = nqt_b - kt;
   const int n_items = nh * nq;  // 128-query tiles
   const int h_first = g * p.G + hs * nh;
@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
           tma_load_4d(sQ + qs * TB + bx * 16384, &maps.q, &bars.q_full[qs], bx * 64, h, ry + qt * kTile, by);
-        const size_t li = ws_at(p, b, h, qt * kTile);
+        const size_t li = ws_at(p, PACKED, b, h, qt * kTile);
         bulk_load_1d(sL + qs * 128, p.lse2 + li, 512, &bars.q_full[qs]);
         bulk_load_1d(sDel + qs * 128, p.delta + li, 512, &bars.q_full[qs]);
         TTT_TRACE_EV(2, 11, t);
@@ -943,9 +943,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_ld64w(tS, raw);
         // allowed (k, q): k <= q and k < T; full tiles (qt > kt, whole key tile < T) skip the test
         // packed: query rows >= T are the next sequence's (local columns >= cmax are masked too)
-        const bool full = (qt > kt) && (kt * kTile + kTile <= T) && (!p.packed || qt * kTile + kTile <= T);
+        const bool full = (qt > kt) && (kt * kTile + kTile <= T) && (!PACKED || qt * kTile + kTile <= T);
         const int cmin = (k < T) ? k - qt * kTile - 64 * x : kTile;  // local columns [cmin, 64) allowed
-        const unsigned span = (unsigned)max((p.packed ? T - qt * kTile - 64 * x : kTile) - cmin, 0);  // [cmin, cmin + span)
+        const unsigned span = (unsigned)max((PACKED ? T - qt * kTile - 64 * x : kTile) - cmin, 0);  // [cmin, cmin + span)
 #pragma unroll
         for (int c4 = 0; c4 < 16; ++c4) {
           const float4 l4 = Lq[c4];
@@ -1067,7 +1067,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const float4 val = *reinterpret_cast<const float4*>(stg + (tsr * NCH + c / 8) * 16384 + lr * 128 +
                                                               (((c & 7) ^ (lr & 7)) << 4));
           if (kk < T)
-            red_add_v4(dst + (((size_t)p.row0[b] + kk) * p.Hkv + g) * D + x * (D / 2) + c * 4, val.x, val.y, val.z,
+            red_add_v4(dst + (((size_t)(PACKED ? p.row0[b] : b * p.L) + kk) * p.Hkv + g) * D + x * (D / 2) + c * 4, val.x, val.y, val.z,
                        val.w);
         }
       }
@@ -1094,7 +1094,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars.dq_empty);
       if (threadIdx.x == 0) TTT_TRACE_EV(2, 2, t);
-      const int row_base = (int)(dq_tile(p, b, h, qt) * (D / 32)) * 128 + wq * 32;
+      const int row_base = (int)(dq_tile(p, PACKED, b, h, qt) * (D / 32)) * 128 + wq * 32;
 #if TTT_BWD_DQ_RED
       {  // dev variant: reduce-add straight from registers (LSU path; the TMA unit then only loads)
         float* dst = p.dq_acc + (size_t)(row_base + lane) * 32;
@@ -1149,7 +1149,7 @@ __global__ void __launch_bounds__(256) ttt_bwd_dq_convert_kernel(const __grid_co
   for (uint32_t row = blockIdx.x * rows_per_block + threadIdx.x / d8; row < nrows; row += gridDim.x * rows_per_block) {
     const uint32_t bl = row / (uint32_t)p.Hq;
     const int h = (int)(row - bl * (uint32_t)p.Hq);
-    const int b = seq_of_row(p, (int)bl);
+    const int b = seq_of_row(p, p.packed, (int)bl);
     const int r = (int)bl - p.row0[b];
     const float4* src = reinterpret_cast<const float4*>(p.dq_acc + dqacc_index(p, b, h, r, d));
     const float4 a = src[0], c = src[1];
@@ -1224,15 +1224,15 @@ template <int D, bool U>
 cudaError_t launch_pre(const Params& p, const PreMaps& pmaps, const UnrollPre& up, cudaStream_t st) {
   PreLayout lay;
   if (!pre_layout(p, D, &lay)) return cudaErrorInvalidConfiguration;
-  cudaError_t e = cudaFuncSetAttribute(ttt_bwd_pre_kernel<D, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)lay.total);
+  auto* kern = p.packed ? ttt_bwd_pre_kernel<D, U, true> : ttt_bwd_pre_kernel<D, U, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
   if (e != cudaSuccess) return e;
   const int rows = p.nrows * p.Hkv;
   const int groups = (rows + lay.NR - 1) / lay.NR;
   UnrollPre u = up;
   if (U) u.M = std::max(lay.NS, 4);  // >= NS: the ring's own wait orders a group's steps
   prof_mark(kKindBwdPre, true, st);
-  ttt_bwd_pre_kernel<D, U><<<std::min(groups, 148), 32 * (kPreCompute + 1), lay.total, st>>>(p, pmaps, u, lay);
+  kern<<<std::min(groups, 148), 32 * (kPreCompute + 1), lay.total, st>>>(p, pmaps, u, lay);
   prof_mark(kKindBwdPre, false, st);
   return cudaGetLastError();
 }
@@ -1252,12 +1252,14 @@ cudaError_t launch_main_convert(const Params& p_in, const BwdMaps& maps, cudaStr
   }
   {
     const int smem = BwdSmem<D>::bytes;
-    static std::atomic<unsigned long long> attr_done{0};
-    cudaError_t ea = set_smem_attr(ttt_bwd_sm100_kernel<D>, smem, attr_done);
+    static std::atomic<unsigned long long> attr_done{0}, attr_done_pk{0};
+    cudaError_t ea = p.packed ? set_smem_attr(ttt_bwd_sm100_kernel<D, true>, smem, attr_done_pk)
+                              : set_smem_attr(ttt_bwd_sm100_kernel<D, false>, smem, attr_done);
     if (ea != cudaSuccess) return ea;
     const int grid = p.ntiles * p.Hkv * p.head_split;  // padded: ntiles = B nqt
     prof_mark(kKindBwdMain, true, st);
-    ttt_bwd_sm100_kernel<D><<<grid, kBwdThreads, smem, st>>>(p, maps);
+    if (p.packed) ttt_bwd_sm100_kernel<D, true><<<grid, kBwdThreads, smem, st>>>(p, maps);
+    else ttt_bwd_sm100_kernel<D, false><<<grid, kBwdThreads, smem, st>>>(p, maps);
     prof_mark(kKindBwdMain, false, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) fwd_check_kernel(const Params p) {
   // warp -> (head h, row of the [rows][H][D] view) -> (sequence b, position r); padded or packed
   const int grow = (int)(warp % p.nrows);
   const int h = (int)(warp / p.nrows);
-  const int b = seq_of_row(p, grow);
+  const int b = seq_of_row(p, p.packed, grow);
   const int r = grow - p.row0[b];
   const int g = h / p.G;
   const int T = p.seq_lens[b];
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) fwd_check_kernel(const Params p) {
   const float inv = 1.f / l;
 #pragma unroll
   for (int e = 0; e < E; ++e) orow[lane + 32 * e] = acc[e] * inv;
-  if (lane == 0) p.lse[lse_at(p, b, h, r)] = m + logf(l);
+  if (lane == 0) p.lse[lse_at(p, p.packed, b, h, r)] = m + logf(l);
 }
 
 template <int D>
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) bwd_check_kernel(const Params p) {
   // warp -> (head h, row of the [rows][H][D] view) -> (sequence b, position r); padded or packed
   const int grow = (int)(warp % p.nrows);
   const int h = (int)(warp / p.nrows);
-  const int b = seq_of_row(p, grow);
+  const int b = seq_of_row(p, p.packed, grow);
   const int r = grow - p.row0[b];
   const int g = h / p.G;
   const int T = p.seq_lens[b];
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) bwd_check_kernel(const Params p) {
     dq[e] = 0.f;
   }
   delta = warp_sum(delta);  // Delta_r = dO_r . O_r
-  const float lse = p.lse_in[lse_at(p, b, h, r)];
+  const float lse = p.lse_in[lse_at(p, p.packed, b, h, r)];
   // dK / dV contributions of every row meet in fp64 accumulators (workspace): an fp32 sum of up to
   // (rows x heads) terms in arbitrary order would drift past 1e-5 where the terms cancel
   auto visit = [&](const float* krow, const float* vrow, double* dkrow, double* dvrow) {

@@ -84,7 +84,7 @@ struct FwdBars {
 // same pipeline: one q tile of the n <= 64 tree tokens per (b, head pair); keys = the prefix
 // (all allowed) followed by the tree tokens' own keys, allowed per query row by its
 // ancestor-or-self bit mask; no diagonal step keys.
-template <int D, bool TREE>
+template <int D, bool TREE, bool PACKED>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     ttt_fwd_sm100_kernel(const __grid_constant__ Params p, const __grid_constant__ FwdMaps maps) {
   constexpr int TB = kTile * D * 2;  // bytes of one 128 x D bf16 tile
@@ -120,11 +120,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     qt = 0;
     g = gi % p.Hkv;
     b = gi / p.Hkv;
-  } else if (p.packed) {
+  } else if (PACKED) {
     // packed: (tile, kv head) with the kv head fastest; each sequence's q tiles longest first
     g = t_ % p.Hkv;
     const int tt = t_ / p.Hkv;
-    b = seq_of_tile(p, tt);
+    b = seq_of_tile(p, true, tt);
     qt = p.tile0[b + 1] - 1 - tt;  // local tile: nqt_b - 1 - (tt - tile0[b])
   } else {
 #ifdef TTT_ORDER_GROUP
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
   const int bst = TREE ? split * p.B + b : b;  // batch index of this CTA's out / lse rows
   // TMA (row, batch) origin of this sequence: (0, b) padded, (row0[b], 0) packed (TREE: never packed)
-  const int ry = p.packed ? p.row0[b] : 0, by = p.packed ? 0 : b;
+  const int ry = PACKED ? p.row0[b] : 0, by = PACKED ? 0 : b;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.q, 1);
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               if (hs == 0 || has1) {
                 const float inv = 1.f / l[hs];
                 __nv_bfloat16* orow =
-                    reinterpret_cast<__nv_bfloat16*>(p.out) + (((size_t)p.row0[b] + r) * p.Hq + h0 + hs) * D;
+                    reinterpret_cast<__nv_bfloat16*>(p.out) + (((size_t)(PACKED ? p.row0[b] : b * p.L) + r) * p.Hq + h0 + hs) * D;
 #pragma unroll
                 for (int bx = 0; bx < NBOX; ++bx) {
                   uint4 w;
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // The j diagonal keys of row r (Alg. 1 "concat s_i") were reduced
       // by the diagonal warps into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum); the
       // merge is the same online-softmax update as one more "tile".
-      const size_t lse_idx = TREE ? ((size_t)bst * p.Hq + h) * p.L + r : lse_at(p, b, h, r);
+      const size_t lse_idx = TREE ? ((size_t)bst * p.Hq + h) * p.L + r : lse_at(p, PACKED, b, h, r);
       const bool has_diag = !TREE && (r < T) && (p.step > 0);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, 0);
       mbar_wait(&bars.o_full[slot], 0);
@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const float a_n = alpha * inv_l, b_n = beta * inv_l;
       // packed layout, the sequence's last (partial) tile: rows >= T belong to the next sequence, so
       // each thread stores its own row (r < T) straight to global instead of the 128-row TMA boxes
-      const bool direct = !TREE && p.packed && (qt * kTile + kTile > T);
+      const bool direct = !TREE && PACKED && (qt * kTile + kTile > T);
       __nv_bfloat16* const orow = direct ? reinterpret_cast<__nv_bfloat16*>(p.out) + ((size_t)(ry + r) * p.Hq + h) * D : nullptr;
       __nv_bfloat16* const lrow = direct && p.out_lo ? reinterpret_cast<__nv_bfloat16*>(p.out_lo) + ((size_t)(ry + r) * p.Hq + h) * D : nullptr;
       // per 64-column box: one 64-column TMEM load (a single wait), the box written to the staging tile,
@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 6, 0);
-      if ((!TREE || tree_row) && !(p.packed && r >= T)) p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
+      if ((!TREE || tree_row) && !(PACKED && r >= T)) p.lse[lse_idx] = (m_f + log2f(l_f)) * 0.69314718055994531f;
       if (row == 0) {
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 8, 0);
         bulk_wait_read0();  // smem must stay valid until the bulk engine has read it
@@ -1017,9 +1017,10 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
     p.order_batch = pick_order_batch(p.B * p.Hkv, p.nqt, (p.G + 1) / 2, len.data(), 7.0, (double)p.L * D * 4);
   }
   const int smem = fwd_smem_bytes(D);
-  static std::atomic<unsigned long long> attr_done{0};
+  static std::atomic<unsigned long long> attr_done{0}, attr_done_pk{0};
   {
-    cudaError_t e = set_smem_attr(ttt_fwd_sm100_kernel<D, false>, smem, attr_done);
+    cudaError_t e = set_smem_attr(ttt_fwd_sm100_kernel<D, false, false>, smem, attr_done);
+    if (e == cudaSuccess) e = set_smem_attr(ttt_fwd_sm100_kernel<D, false, true>, smem, attr_done_pk);
     if (e != cudaSuccess) return e;
   }
 #if !TTT_FWD_FUSED_DIAG
@@ -1042,7 +1043,8 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
   const int npairs = (p.G + 1) / 2;
   const int grid = p.ntiles * p.Hkv * npairs;  // padded: ntiles = B nqt
   prof_mark(kKindFwdMain, true, st);
-  ttt_fwd_sm100_kernel<D, false><<<grid, kFwdThreads, smem, st>>>(p, maps);
+  if (p.packed) ttt_fwd_sm100_kernel<D, false, true><<<grid, kFwdThreads, smem, st>>>(p, maps);
+  else ttt_fwd_sm100_kernel<D, false, false><<<grid, kFwdThreads, smem, st>>>(p, maps);
   prof_mark(kKindFwdMain, false, st);
   return cudaGetLastError();
 }
@@ -1108,7 +1110,7 @@ cudaError_t launch_tree_d(const Params& p_in, const FwdMaps& maps, const int32_t
   const int smem = fwd_smem_bytes(D);
   static std::atomic<unsigned long long> attr_done{0};
   {
-    cudaError_t e = set_smem_attr(ttt_fwd_sm100_kernel<D, true>, smem, attr_done);
+    cudaError_t e = set_smem_attr(ttt_fwd_sm100_kernel<D, true, false>, smem, attr_done);
     if (e != cudaSuccess) return e;
   }
   const int nm = p.B * p.tree_n;
@@ -1116,7 +1118,7 @@ cudaError_t launch_tree_d(const Params& p_in, const FwdMaps& maps, const int32_t
                                                         const_cast<unsigned long long*>(p.tree_mask));
   const int grid = p.B * p.Hkv * ((p.G + 3) / 4) * p.tree_splits;
   prof_mark(kKindFwdMain, true, st);
-  ttt_fwd_sm100_kernel<D, true><<<grid, kFwdThreads, smem, st>>>(p, maps);
+  ttt_fwd_sm100_kernel<D, true, false><<<grid, kFwdThreads, smem, st>>>(p, maps);
   prof_mark(kKindFwdMain, false, st);
   return cudaGetLastError();
 }

@@ -68,22 +68,21 @@ struct Params {
 };
 
 #ifdef __CUDACC__
-// ---- row-layout helpers (padded / packed; see Params) ----
-// TMA coordinates of row r of sequence b: (row, batch) = (r, b) padded, (row0[b] + r, 0) packed
-__device__ __forceinline__ int tma_row(const Params& p, int b, int r) { return p.packed ? p.row0[b] + r : r; }
-__device__ __forceinline__ int tma_bat(const Params& p, int b) { return p.packed ? 0 : b; }
-// index of lse[b][h][r] (padded [B][Hq][L], packed [Hq][nrows]) and of the delta / lse2 workspaces
-__device__ __forceinline__ size_t lse_at(const Params& p, int b, int h, int r) {
-  return p.packed ? (size_t)h * p.nrows + p.row0[b] + r : ((size_t)b * p.Hq + h) * p.L + r;
+// ---- row-layout helpers (padded / packed; see Params). `pk` is the layout: the tensor-core kernels
+// pass their PACKED template flag (the padded instantiations compile exactly as before), the
+// CUDA-core check kernels pass p.packed ----
+// index of lse[b][h][r] (padded [B][Hq][L], packed [Hq][nrows])
+__device__ __forceinline__ size_t lse_at(const Params& p, bool pk, int b, int h, int r) {
+  return pk ? (size_t)h * p.nrows + p.row0[b] + r : ((size_t)b * p.Hq + h) * p.L + r;
 }
 // 128-row tile (b, h, tile t of the sequence) of the dq accumulator and the delta / lse2 workspaces
-__device__ __forceinline__ size_t dq_tile(const Params& p, int b, int h, int t) {
-  return p.packed ? (size_t)h * p.ntiles + p.tile0[b] + t : ((size_t)b * p.Hq + h) * p.nqt + t;
+__device__ __forceinline__ size_t dq_tile(const Params& p, bool pk, int b, int h, int t) {
+  return pk ? (size_t)h * p.ntiles + p.tile0[b] + t : ((size_t)b * p.Hq + h) * p.nqt + t;
 }
-__device__ __forceinline__ size_t ws_at(const Params& p, int b, int h, int r) {
-  return dq_tile(p, b, h, r >> 7) * 128 + (r & 127);
+__device__ __forceinline__ size_t ws_at(const Params& p, bool pk, int b, int h, int r) {
+  return dq_tile(p, pk, b, h, r >> 7) * 128 + (r & 127);
 }
-// sequence of a global row / tile: b with row0[b] <= x < row0[b + 1] (binary search when packed)
+// sequence of a global row / tile: b with start[b] <= x < start[b + 1] (binary search when packed)
 __device__ __forceinline__ int seq_search(const int* start, int B, int x) {
   int lo = 0, hi = B - 1;
   while (lo < hi) {
@@ -93,11 +92,11 @@ __device__ __forceinline__ int seq_search(const int* start, int B, int x) {
   }
   return lo;
 }
-__device__ __forceinline__ int seq_of_row(const Params& p, int row) {
-  return p.packed ? seq_search(p.row0, p.B, row) : row / p.L;
+__device__ __forceinline__ int seq_of_row(const Params& p, bool pk, int row) {
+  return pk ? seq_search(p.row0, p.B, row) : row / p.L;
 }
-__device__ __forceinline__ int seq_of_tile(const Params& p, int t) {
-  return p.packed ? seq_search(p.tile0, p.B, t) : t / p.nqt;
+__device__ __forceinline__ int seq_of_tile(const Params& p, bool pk, int t) {
+  return pk ? seq_search(p.tile0, p.B, t) : t / p.nqt;
 }
 #endif
 
