@@ -251,7 +251,9 @@ def _model_worker(rank, world, port, q):
         local = [p.grad.clone() for p in model.parameters()]
         n = sum(p.numel() for p in model.parameters())
         exchange_grads(model, GradBuckets(n, 3, dtype=torch.float64))
-        q.put((rank, local, [p.grad.clone() for p in model.parameters()]))
+        # numpy copies pickle by value (a tensor would travel through a shared-memory file that can
+        # vanish when this process exits before the parent reads the queue)
+        q.put((rank, [t.numpy() for t in local], [p.grad.detach().clone().numpy() for p in model.parameters()]))
     finally:
         dist.destroy_process_group()
 
@@ -268,7 +270,7 @@ def test_exchange_real_model_grads_world2():
     res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
-    mean = [(a + b) / 2 for a, b in zip(res[0][1], res[1][1])]
+    mean = [(torch.from_numpy(a) + torch.from_numpy(b)) / 2 for a, b in zip(res[0][1], res[1][1])]
     for rank, _, got in res:
         for g, m in zip(got, mean):
-            assert torch.allclose(g, m, atol=1e-12), rank
+            assert torch.allclose(torch.from_numpy(g), m, atol=1e-12), rank
