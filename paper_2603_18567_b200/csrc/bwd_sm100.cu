@@ -50,6 +50,13 @@ constexpr float kLog2e = 1.4426950408889634f;
 #ifndef TTT_BWD_ORDER
 #define TTT_BWD_ORDER 0  // dev: MMA issue order of an item's dP / dV halves (see the MMA warp)
 #endif
+#ifndef TTT_BWD_DQ_HALVES
+#define TTT_BWD_DQ_HALVES 1  // 1: the dQ drain frees dP^T[a] after its first 64 columns, so dP(t+1,a) need
+                             // not wait for the whole 128-column read-out
+#endif
+#if TTT_BWD_DQ_HALVES && TTT_BWD_ORDER == 1
+#error "TTT_BWD_ORDER == 1 waits on the whole-tile dq_empty; build it with TTT_BWD_DQ_HALVES=0"
+#endif
 #ifndef TTT_BWD_PREFETCH
 #define TTT_BWD_PREFETCH 0  // dev: items of L2-prefetch lookahead for Q / dO in the main kernel (2 measured
                             // 5.03 vs 4.76 ms per unroll, r02f: off)
@@ -599,6 +606,7 @@ struct BwdBars3 {
   uint64_t do_full[3], do_empty[3];
   uint64_t s_full[2], dp_full[2], p_full[2], ds_full[2];
   uint64_t ds_empty, dq_full, dq_empty, acc_full;
+  uint64_t dq_empty_h[2];  // DQ_HALVES: dQ columns [64x, 64x + 64) (over dP^T[x]) read out
   uint32_t tmem_base;
 };
 
@@ -682,6 +690,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(&bars.ds_empty, 1);
     mbar_init(&bars.dq_full, 1);
     mbar_init(&bars.dq_empty, 128);
+    mbar_init(&bars.dq_empty_h[0], 128);
+    mbar_init(&bars.dq_empty_h[1], 128);
     mbar_init(&bars.acc_full, 1);
     fence_mbar_init();
   }
@@ -813,6 +823,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       auto issue_dP_pair = [&](int t) {
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
+          // DQ_HALVES: dP^T[x] columns held dQ(t-1) columns [64x, 64x+64) (aliased only when 64x < D)
+          if (TTT_BWD_DQ_HALVES && t > 0 && 64 * x < D) mbar_wait(&bars.dq_empty_h[x], (t - 1) & 1);
+          tc_fence_after();
           mbar_wait(&bars.do_full[slot_of(t, x)], use_of(t, x));
           TTT_TRACE_EV(0, 12 + x, t);
           tc_fence_after();
@@ -881,7 +894,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #endif
         TTT_TRACE_EV(0, 9, t);
         if (t + 1 < n_items) {
-          mbar_wait(&bars.dq_empty, t & 1);  // dQ(t) drained: the dP^T buffers are free
+          if (!TTT_BWD_DQ_HALVES) mbar_wait(&bars.dq_empty, t & 1);  // dQ(t) drained: the dP^T buffers are free
           TTT_TRACE_EV(0, 5, t);
           tc_fence_after();
 #if TTT_BWD_ORDER == 1
@@ -1090,9 +1103,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_after();
       uint32_t v[D];
 #pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 64) tmem_ld64w(tQ + c0, *reinterpret_cast<uint32_t(*)[64]>(&v[c0]));
+      for (int c0 = 0; c0 < D; c0 += 64) {
+        tmem_ld64w(tQ + c0, *reinterpret_cast<uint32_t(*)[64]>(&v[c0]));
+        if (TTT_BWD_DQ_HALVES) {
+          tc_fence_before();
+          mbar_arrive(&bars.dq_empty_h[c0 / 64]);
+        }
+      }
       tc_fence_before();
-      mbar_arrive(&bars.dq_empty);
+      if (!TTT_BWD_DQ_HALVES) mbar_arrive(&bars.dq_empty);
       if (threadIdx.x == 0) TTT_TRACE_EV(2, 2, t);
       const int row_base = (int)(dq_tile(p, PACKED, b, h, qt) * (D / 32)) * 128 + wq * 32;
 #if TTT_BWD_DQ_RED

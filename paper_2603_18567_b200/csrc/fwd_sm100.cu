@@ -39,6 +39,11 @@
 #ifndef TTT_FWD_EMU_MASK
 #define TTT_FWD_EMU_MASK 0x88
 #endif
+// 1: the softmax warps read each S row once (128 registers, setmaxnreg-rebalanced roles); 0: round-2
+// form, S read in 64-column halves with keys [0,64) read twice (1.5x the TMEM reads per tile)
+#ifndef TTT_FWD_ONEREAD
+#define TTT_FWD_ONEREAD 1
+#endif
 
 namespace tttk {
 #ifdef TTT_TRACE
@@ -57,6 +62,12 @@ extern "C" int ttt_debug_ftrace_read(void* host, unsigned int cta) {
 namespace {
 
 constexpr int kFwdThreads = 512;
+// ONEREAD register split per SMSP: 2 softmax + 1 diagonal + 1 role warp <= 512 per lane
+#ifndef TTT_FWD_REG_SOFTMAX
+#define TTT_FWD_REG_SOFTMAX 168
+#endif
+constexpr uint32_t kFwdRegSoftmax = TTT_FWD_REG_SOFTMAX, kFwdRegDiag = 128, kFwdRegRole = 48;
+static_assert(2 * kFwdRegSoftmax + kFwdRegDiag + kFwdRegRole <= 512, "register file per SMSP");
 #ifndef TTT_FWD_DIAG_MODE
 #define TTT_FWD_DIAG_MODE 0  // dev timing probes only: 1 = diagonal warps skip the math, 2 = skip the loads
 #endif
@@ -190,8 +201,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   const uint32_t tbase = bars.tmem_base;
 
+  // Per SMSP (warps s, s+4, 8+s, 12+s): two softmax warps, one diagonal warp and one of
+  // {TMA producer, MMA issuer, diagonal producer, idle}. ONEREAD: softmax 168 + 168, diagonal 128
+  // (launch value), the fourth 48 = 512 registers per lane.
   if (warp == 8) {
     // ================= TMA producer =================
+    if (TTT_FWD_ONEREAD) regs_dec<kFwdRegRole>();
     if (lane == 0) {
       tma_prefetch_desc(&maps.q);
       tma_prefetch_desc(&maps.k);
@@ -237,6 +252,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else if (warp == 9) {
     // ================= MMA issuer (whole warp, converged; elect.sync inside each issue) =================
+    if (TTT_FWD_ONEREAD) regs_dec<kFwdRegRole>();
     {
       constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);  // S = Q K^T, both K-major
       constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);     // O += P V, V MN-major
@@ -311,38 +327,38 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
     }
+  } else if (warp >= 14) {
+    // ================= TMA producer of the diagonal ring (warp 14); warp 15 idle =================
+    if (TTT_FWD_ONEREAD) regs_dec<kFwdRegRole>();
+    if (TTT_FWD_FUSED_DIAG && !TREE && p.step > 0 && warp == 14 && lane == 0) {
+      const int j = p.step;
+      const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
+      int n = 0;
+      for (int rb = 0; rb < nrb; ++rb)
+        for (int i = 0; i < j; ++i, ++n) {
+          const int st = n % kDgStages, use = n / kDgStages;
+          mbar_wait(&bars.dg_empty[st], (use & 1) ^ 1);
+          if (TTT_FWD_DIAG_MODE == 2) {  // dev probe: no loads
+            mbar_arrive(&bars.dg_full[st]);
+            continue;
+          }
+          mbar_expect_tx(&bars.dg_full[st], DGS);
+          uint8_t* base = sDg + st * DGS;
+          const int r0 = qt * kTile + rb * kDgRows;
+          // one box per tensor: 16 rows x D columns, no swizzle (rows of D x 2 bytes)
+          tma_load_4d(base, &maps.kd[i], &bars.dg_full[st], 0, g, ry + r0, by);
+          tma_load_4d(base + NBOX * DGB, &maps.vd[i], &bars.dg_full[st], 0, g, ry + r0, by);
+        }
+    }
   } else if (warp >= 10) {
-    // ================= diagonal fold (warps 10-13) + its TMA producer (warp 14) =================
+    // ================= diagonal fold (warps 10-13) =================
+    if (TTT_FWD_ONEREAD) regs_dec<kFwdRegDiag>();
 
     if (TTT_FWD_FUSED_DIAG && !TREE && p.step > 0) {
       const int j = p.step;
       // 16-row blocks of this q tile holding at least one row r < T_b
       const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
-      if (warp == 14) {
-        if (lane == 0) {
-#ifdef TTT_TRACE
-          int trace_n_3 = 32768;
-#endif
-          int n = 0;
-          for (int rb = 0; rb < nrb; ++rb)
-            for (int i = 0; i < j; ++i, ++n) {
-              const int st = n % kDgStages, use = n / kDgStages;
-              mbar_wait(&bars.dg_empty[st], (use & 1) ^ 1);
-              if (TTT_FWD_DIAG_MODE == 2) {  // dev probe: no loads
-                mbar_arrive(&bars.dg_full[st]);
-                continue;
-              }
-              mbar_expect_tx(&bars.dg_full[st], DGS);
-              uint8_t* base = sDg + st * DGS;
-              const int r0 = qt * kTile + rb * kDgRows;
-#pragma unroll
-              // one box per tensor: 16 rows x D columns, no swizzle (rows of D x 2 bytes)
-              tma_load_4d(base, &maps.kd[i], &bars.dg_full[st], 0, g, ry + r0, by);
-              tma_load_4d(base + NBOX * DGB, &maps.vd[i], &bars.dg_full[st], 0, g, ry + r0, by);
-              TTT_TRACE_EV(3, 3, n);
-            }
-        }
-      } else if (warp < 14) {
+      {
         // thread layout: 8 lanes per row (lane k = lane & 7 owns columns 8k..8k+7 of every 64-column
         // box), 4 rows per warp, 16 rows per stage; both head slots per row
         constexpr int E = 8 * NBOX;  // elements per lane
@@ -481,6 +497,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else {
     // ================= softmax + epilogue (warps 0-7) =================
+    if (TTT_FWD_ONEREAD) regs_inc<kFwdRegSoftmax>();
     const int slot = warp >> 2;
     const int wq = warp & 3;
     if (slot == 0 || has1) {
@@ -503,11 +520,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 1, n);
         if (threadIdx.x == 128) TTT_TRACE_EV(2, 1, n);
         tc_fence_after();
-        // S is read in two 64-column halves (64 registers each, so 16 warps fit the register file):
-        // keys [0,64) for their max only, keys [64,128) kept for P; P(keys 64..127) is written over
-        // the already-read S columns [96,128) and published first (p_hi), then keys [0,64) are
-        // re-read and P(keys 0..63) written over columns [0,32) (p_lo).
+        // ONEREAD: the whole S row is read once (raw0 = keys [0,64), raw = keys [64,128)); P(keys
+        // 64..127) is written over the already-read S columns [96,128) and published first (p_hi),
+        // then P(keys 0..63) over columns [0,32) (p_lo). Otherwise S is read in two 64-column halves
+        // (64 registers each): keys [0,64) for their max only, then re-read for P.
         uint32_t raw[64];
+#if TTT_FWD_ONEREAD
+        uint32_t raw0[64];
+#endif
         const int kv0 = (kvt0 + n) * kTile;
         const bool partial = TREE ? (kv0 + kTile > T) : ((n == qt) || (kv0 + kTile > T));
         // TTT: allowed columns c < lim (k <= r and k < T); TREE: per 32-column word bit masks
@@ -532,12 +552,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (!tree_row) w[0] = w[1] = w[2] = w[3] = 0u, w[0] = (kv0 == 0) ? 1u : 0u;
         }
         // masked columns of half hf (columns 64 hf + c) -> -inf
-        auto mask_half = [&](int hf) {
+        auto mask_half = [&](int hf, uint32_t(&rr)[64]) {
 #pragma unroll
           for (int c = 0; c < 64; ++c) {
             const int cc = 64 * hf + c;
             const bool ok = TREE ? (((w[cc >> 5] >> (cc & 31)) & 1u) != 0u) : (cc < lim);
-            raw[c] = ok ? raw[c] : __float_as_uint(-INFINITY);
+            rr[c] = ok ? rr[c] : __float_as_uint(-INFINITY);
           }
         };
         // row max of the raw scores (scale > 0 commutes with max): 8 independent chains of
@@ -545,19 +565,29 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         float mx8[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
-        auto max_half = [&]() {
+        auto max_half = [&](const uint32_t(&rr)[64]) {
 #pragma unroll
           for (int c = 0; c < 64; c += 16)
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-              mx8[u] = fmax3(mx8[u], __uint_as_float(raw[c + u]), __uint_as_float(raw[c + 8 + u]));
+              mx8[u] = fmax3(mx8[u], __uint_as_float(rr[c + u]), __uint_as_float(rr[c + 8 + u]));
         };
+#if TTT_FWD_ONEREAD
+        tmem_ld128w(tS, raw0, raw);
+        if (partial) {
+          mask_half(0, raw0);
+          mask_half(1, raw);
+        }
+        max_half(raw0);
+        max_half(raw);
+#else
         tmem_ld64w(tS, raw);
-        if (partial) mask_half(0);
-        max_half();
+        if (partial) mask_half(0, raw);
+        max_half(raw);
         tmem_ld64w(tS + 64, raw);
-        if (partial) mask_half(1);
-        max_half();
+        if (partial) mask_half(1, raw);
+        max_half(raw);
+#endif
         const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
         const float m_new = fmaxf(m_run, mx);
@@ -595,10 +625,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int hf = 1 - hh;  // keys [64,128) (in registers) first, then [0,64)
+#if TTT_FWD_ONEREAD
+          if (hf == 0) {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) raw[c] = raw0[c];  // register renaming only
+          }
+#else
           if (hf == 0) {
             tmem_ld64w(tS, raw);
-            if (partial) mask_half(0);
+            if (partial) mask_half(0, raw);
           }
+#endif
           uint32_t pk[32];
           if (partial) {  // masked columns are -inf: hardware ex2 gives exact zeros
 #pragma unroll
