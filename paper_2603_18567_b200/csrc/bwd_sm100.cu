@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "ptx_sm100.cuh"
@@ -54,8 +55,34 @@ constexpr float kLog2e = 1.4426950408889634f;
 #define TTT_BWD_DQ_HALVES 1  // 1: the dQ drain frees dP^T[a] after its first 64 columns, so dP(t+1,a) need
                              // not wait for the whole 128-column read-out
 #endif
+#ifndef TTT_BWD_DQT
+#define TTT_BWD_DQT 0  // dev, 1 (D = 128): dQ^T = K^T dS^T per 64-query sub-item (M = D, N = 64) so the two sub-items'
+                       // dP -> dS -> dK -> dQ -> drain chains run independently; 0: one dQ = dS K per tile.
+                       // Measured (r03b / r03e): 5.11 vs 4.66 ms per unroll (5.06 with the reduce-adds probed out):
+                       // the two N = 64 SS MMAs (48 clk per K step) and the serial per-sub-item drain cost more
+                       // than the decoupled chains gain
+#endif
+#if TTT_BWD_DQT && (TTT_BWD_DK_SS || TTT_BWD_DQ_RED || TTT_BWD_ORDER)
+#error "the per-sub-item dQ^T path has no DK_SS / DQ_RED / ORDER variants; build them with TTT_BWD_DQT=0"
+#endif
+#ifndef TTT_BWD_LSU_LOADS
+#define TTT_BWD_LSU_LOADS 0  // dev, 1: Q / lse2 / Delta (warp 14) and dO halves (warp 15) by cp.async on the LSU path, so
+                             // they do not queue in the SM's TMA engine behind the dQ reduce-adds; 0: TMA loads.
+                             // Measured (r03d): 6.64 vs 4.63 ms per unroll (cp.async tiles arrive later than TMA's)
+#endif
 #if TTT_BWD_DQ_HALVES && TTT_BWD_ORDER == 1
 #error "TTT_BWD_ORDER == 1 waits on the whole-tile dq_empty; build it with TTT_BWD_DQ_HALVES=0"
+#endif
+#ifndef TTT_BWD_PSPLIT
+#define TTT_BWD_PSPLIT 1  // P phase: a mask-free copy of the exp loop for full tiles
+#endif
+#ifndef TTT_BWD_EMU_MASK
+#define TTT_BWD_EMU_MASK 0  // quads (c4 mod 8) of the P phase whose 2^x runs as an FMA-pipe polynomial (r03f: none 4.57, 1 in 8 4.58, 1 in 4 4.58, 1 in 2 4.61 ms)
+#endif
+#ifndef TTT_BWD_PROBE
+#define TTT_BWD_PROBE 0  // dev timing probes (wrong results): 1 = no dQ reduce-adds, 2 = Q / dO loaded for the first two
+                         // items only (later items reuse the stale tiles). r03e: 4.63 -> 3.99 (1), 4.31 (2) ms per
+                         // unroll: the dQ egress and the load latency are each only part of the per-item period
 #endif
 #ifndef TTT_BWD_PREFETCH
 #define TTT_BWD_PREFETCH 0  // dev: items of L2-prefetch lookahead for Q / dO in the main kernel (2 measured
@@ -607,6 +634,7 @@ struct BwdBars3 {
   uint64_t s_full[2], dp_full[2], p_full[2], ds_full[2];
   uint64_t ds_empty, dq_full, dq_empty, acc_full;
   uint64_t dq_empty_h[2];  // DQ_HALVES: dQ columns [64x, 64x + 64) (over dP^T[x]) read out
+  uint64_t dq_full_x[2], ds_empty_x[2];  // DQT: dQ^T(t, x) in TMEM; dS(t, x) smem box read by dQ^T(t, x)
   uint32_t tmem_base;
 };
 
@@ -615,6 +643,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     ttt_bwd_sm100_kernel(const __grid_constant__ Params p, const __grid_constant__ BwdMaps maps) {
   using SM = BwdSmem<D>;
   constexpr int TB = SM::TB, HB = SM::HB;
+  constexpr bool DQT = TTT_BWD_DQT && D == 128;  // D = 64 keeps the per-tile dQ = dS K (M = 64 would run at half rate)
   constexpr int NBOX = D / 64;
   // dynamic smem only (no static __shared__): the window base is 1024-B aligned, checked below
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -676,7 +705,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(&bars.kv_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars.q_full[i], 1);
+      mbar_init(&bars.q_full[i], TTT_BWD_LSU_LOADS ? 32 : 1);  // LSU: one noinc arrive per loader lane
       mbar_init(&bars.q_empty[i], 1);
       mbar_init(&bars.s_full[i], 1);
       mbar_init(&bars.dp_full[i], 1);
@@ -684,7 +713,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&bars.ds_full[i], 128);
     }
     for (int i = 0; i < 3; ++i) {
-      mbar_init(&bars.do_full[i], 1);
+      mbar_init(&bars.do_full[i], TTT_BWD_LSU_LOADS ? 32 : 1);
       mbar_init(&bars.do_empty[i], 1);
     }
     mbar_init(&bars.ds_empty, 1);
@@ -692,6 +721,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(&bars.dq_empty, 128);
     mbar_init(&bars.dq_empty_h[0], 128);
     mbar_init(&bars.dq_empty_h[1], 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars.dq_full_x[i], 1);
+      mbar_init(&bars.ds_empty_x[i], 1);
+    }
     mbar_init(&bars.acc_full, 1);
     fence_mbar_init();
   }
@@ -721,7 +754,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_load_4d(sK + bx * 16384, &maps.k, &bars.kv_full, bx * 64, g, ry + kt * kTile, by);
         tma_load_4d(sV + bx * 16384, &maps.v, &bars.kv_full, bx * 64, g, ry + kt * kTile, by);
       }
-      for (int t = 0; t < n_items; ++t) {
+      for (int t = 0; t < (TTT_BWD_LSU_LOADS ? 0 : n_items); ++t) {
         const int h = h_first + t / nq, qt = kt + t % nq;
         const int qs = t & 1, qph = (t >> 1) & 1;
         if (TTT_BWD_PREFETCH && t + TTT_BWD_PREFETCH < n_items) {
@@ -737,6 +770,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         }
         mbar_wait(&bars.q_empty[qs], qph ^ 1);
+        if (TTT_BWD_PROBE == 2 && t >= 2) {  // dev probe: no loads after the first two items
+          mbar_arrive(&bars.q_full[qs]);
+          for (int x = 0; x < 2; ++x) {
+            const int u = 2 * t + x, slot = u % 3, use = u / 3;
+            mbar_wait(&bars.do_empty[slot], (use & 1) ^ 1);
+            mbar_arrive(&bars.do_full[slot]);
+          }
+          continue;
+        }
         mbar_expect_tx(&bars.q_full[qs], TB + 1024);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
@@ -824,7 +866,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
           // DQ_HALVES: dP^T[x] columns held dQ(t-1) columns [64x, 64x+64) (aliased only when 64x < D)
-          if (TTT_BWD_DQ_HALVES && t > 0 && 64 * x < D) mbar_wait(&bars.dq_empty_h[x], (t - 1) & 1);
+          // DQT: dP^T[x] held dQ^T(t-1, x)
+          if ((DQT || TTT_BWD_DQ_HALVES) && t > 0 && (DQT || 64 * x < D)) mbar_wait(&bars.dq_empty_h[x], (t - 1) & 1);
           tc_fence_after();
           mbar_wait(&bars.do_full[slot_of(t, x)], use_of(t, x));
           TTT_TRACE_EV(0, 12 + x, t);
@@ -854,6 +897,46 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_after();
         issue_S(1);
       }
+      if constexpr (DQT) {
+        // Per sub-item x: dK(t,x) (TS, A = dS^T[x] in TMEM) then dQ^T(t,x) = K^T dS^T[x] (SS: A = K^T, the K
+        // tile as an MN-major operand; B = the smem dS box x, MN-major) into the dP^T[x] columns, which
+        // dK(t,x) has just read (in-order pipe). Order per tile t:
+        //   dK(t,a) dQ^T(t,a) | dK(t,b) dQ^T(t,b) | [drain a] dP(t+1,a) [drain b] dP(t+1,b) | dV(t+1,a)
+        //   dV(t+1,b) | S(t+2)
+        // The drain of dQ^T(t,a) runs under dK / dQ^T(t,b); sub-item a's dS(t+1) compute runs under
+        // dP(t+1,b) / dV(t+1) / S(t+2): no whole-tile dQ drain on the critical path.
+        constexpr uint32_t idDQT = idesc_bf16_f32(128, 64, true, true);
+        for (int t = 0; t < n_items; ++t) {
+          const int qs = t & 1;
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            mbar_wait(&bars.ds_full[x], t & 1);
+            TTT_TRACE_EV(0, 3 + x, t);
+            tc_fence_after();
+            issue_dK(qs, x, t == 0 && x == 0);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              umma_ss_e(tbase + 128 + 64 * x, sdesc_add(dK_mn, ks * 2048), sdesc_add(dDS_mn, x * 16384 + ks * 2048),
+                        idDQT, ks > 0);
+            umma_commit_e(&bars.dq_full_x[x]);
+            umma_commit_e(&bars.ds_empty_x[x]);
+            TTT_TRACE_EV(0, 7 + x, t);
+          }
+          umma_commit_e(&bars.q_empty[qs]);
+          if (t + 1 < n_items) {
+            issue_dP_pair(t + 1);  // waits dq_empty_h[x] (dQ^T(t,x) drained) before dP(t+1,x)
+            TTT_TRACE_EV(0, 6, t);
+            issue_dV_pair(t + 1);
+            if (t + 2 < n_items) {
+              mbar_wait(&bars.q_full[(t + 2) & 1], ((t + 2) >> 1) & 1);
+              TTT_TRACE_EV(0, 11, t + 2);
+              tc_fence_after();
+              issue_S((t + 2) & 1);
+              TTT_TRACE_EV(0, 10, t);
+            }
+          }
+        }
+      } else
       for (int t = 0; t < n_items; ++t) {
         const int qs = t & 1;
 #if TTT_BWD_DK_SS
@@ -959,30 +1042,36 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const bool full = (qt > kt) && (kt * kTile + kTile <= T) && (!PACKED || qt * kTile + kTile <= T);
         const int cmin = (k < T) ? k - qt * kTile - 64 * x : kTile;  // local columns [cmin, 64) allowed
         const unsigned span = (unsigned)max((PACKED ? T - qt * kTile - 64 * x : kTile) - cmin, 0);  // [cmin, cmin + span)
+        // P = exp(S c - lse); full tiles take a mask-free copy of the loop (TTT_BWD_PSPLIT)
+        auto p_phase = [&](auto masked_t) {
+          constexpr bool masked = decltype(masked_t)::value;
 #pragma unroll
-        for (int c4 = 0; c4 < 16; ++c4) {
-          const float4 l4 = Lq[c4];
-          float x0, x1, x2, x3;
-          f2unpack(ffma2(f2pack(__uint_as_float(raw[4 * c4]), __uint_as_float(raw[4 * c4 + 1])), sl2x2,
-                         f2pack(l4.x, l4.y)), x0, x1);
-          f2unpack(ffma2(f2pack(__uint_as_float(raw[4 * c4 + 2]), __uint_as_float(raw[4 * c4 + 3])), sl2x2,
-                         f2pack(l4.z, l4.w)), x2, x3);
-          float ys[4];
-          if ((c4 & 3) == 3) {  // 1 in 4: 2^x on the FMA pipe (MUFU is the P phase's bottleneck)
-            ex2_emu2(x0, x1, ys[0], ys[1]);
-            ex2_emu2(x2, x3, ys[2], ys[3]);
-          } else {
-            ys[0] = ex2(x0);
-            ys[1] = ex2(x1);
-            ys[2] = ex2(x2);
-            ys[3] = ex2(x3);
-          }
+          for (int c4 = 0; c4 < 16; ++c4) {
+            const float4 l4 = Lq[c4];
+            float x0, x1, x2, x3;
+            f2unpack(ffma2(f2pack(__uint_as_float(raw[4 * c4]), __uint_as_float(raw[4 * c4 + 1])), sl2x2,
+                           f2pack(l4.x, l4.y)), x0, x1);
+            f2unpack(ffma2(f2pack(__uint_as_float(raw[4 * c4 + 2]), __uint_as_float(raw[4 * c4 + 3])), sl2x2,
+                           f2pack(l4.z, l4.w)), x2, x3);
+            float ys[4];
+            if ((TTT_BWD_EMU_MASK >> (c4 & 7)) & 1) {  // 2^x on the FMA pipe for the selected quads
+              ex2_emu2(x0, x1, ys[0], ys[1]);
+              ex2_emu2(x2, x3, ys[2], ys[3]);
+            } else {
+              ys[0] = ex2(x0);
+              ys[1] = ex2(x1);
+              ys[2] = ex2(x2);
+              ys[3] = ex2(x3);
+            }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = 4 * c4 + e;
-            pr[c] = (full || (unsigned)(c - cmin) < span) ? ys[e] : 0.f;  // P = exp(S c - lse)
+            for (int e = 0; e < 4; ++e) {
+              const int c = 4 * c4 + e;
+              pr[c] = (!masked || full || (unsigned)(c - cmin) < span) ? ys[e] : 0.f;
+            }
           }
-        }
+        };
+        if (TTT_BWD_PSPLIT && full) p_phase(std::false_type{});
+        else p_phase(std::true_type{});
       }
       {
         uint32_t pk[32];
@@ -999,7 +1088,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         g_ttt_trace[3][t * 16 + warp] = (clock64() << 20) | ((unsigned long long)warp << 12) | (unsigned long long)(t & 0xFFF);
 #endif
       mbar_wait(&bars.dp_full[x], t & 1);
-      mbar_wait(&bars.ds_empty, (t & 1) ^ 1);  // dQ of the previous tile has read the dS buffer
+      if constexpr (DQT) mbar_wait(&bars.ds_empty_x[x], (t & 1) ^ 1);  // dQ^T(t-1, x) has read dS box x
+      else mbar_wait(&bars.ds_empty, (t & 1) ^ 1);  // dQ of the previous tile has read the dS buffer
       if (threadIdx.x == 128) TTT_TRACE_EV(1, 3, t);
       tc_fence_after();
 #pragma unroll
@@ -1096,6 +1186,47 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint8_t* stage = sDQ + wq * 4096;
     if (lane == 0) tma_prefetch_desc(&maps.dqacc);
     TTT_TRACE_DECL(2);
+    if constexpr (DQT) {
+      // dQ^T(t, x): TMEM lane = d (this warp: d in [32 wq, 32 wq + 32), i.e. column chunk wq of the dq_acc
+      // tile), column = query 64 x + c. Each 32-query half is staged as a 32 x 32 box (row = query,
+      // SW128 16-B chunks XOR (row & 7); a lane writes column d % 32 of every row: conflict-free) and
+      // TMA reduce-added into rows 64 x + 32 hh of chunk wq.
+      const uint32_t tQT = tbase + ((uint32_t)(wq * 32) << 16) + 128;
+      const float c = p.scale;
+      const uint32_t sbase = smem_u32(stage);
+      for (int t = 0; t < n_items; ++t) {
+        const int h = h_first + t / nq, qt = kt + t % nq;
+        const int row_base = (int)(dq_tile(p, PACKED, b, h, qt) * (D / 32)) * 128 + wq * 128;
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          mbar_wait(&bars.dq_full_x[x], t & 1);
+          if (threadIdx.x == 0) TTT_TRACE_EV(2, 1, t);
+          tc_fence_after();
+          uint32_t v[64];
+          tmem_ld64w(tQT + 64 * x, v);
+          tc_fence_before();
+          mbar_arrive(&bars.dq_empty_h[x]);
+          if (threadIdx.x == 0) TTT_TRACE_EV(2, 2, t);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            if (lane == 0) bulk_wait_read0();  // the previous reduce has read the staging buffer
+            __syncwarp();
+#pragma unroll
+            for (int qi = 0; qi < 32; ++qi)
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(sbase + qi * 128 + ((((uint32_t)(lane >> 2)) ^ (qi & 7)) << 4) +
+                                                           (lane & 3) * 4),
+                           "f"(c * __uint_as_float(v[32 * hh + qi]))
+                           : "memory");
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_reduce_add_2d(&maps.dqacc, stage, 0, row_base + 64 * x + 32 * hh);
+              bulk_commit();
+            }
+          }
+        }
+      }
+    } else
     for (int t = 0; t < n_items; ++t) {
       const int h = h_first + t / nq, qt = kt + t % nq;
       mbar_wait(&bars.dq_full, t & 1);
@@ -1142,13 +1273,65 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         fence_async_smem();
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0 && TTT_BWD_PROBE != 1) {
           tma_reduce_add_2d(&maps.dqacc, stage, 0, row_base + cc * 128);
           bulk_commit();
         }
       }
     }
     if (lane == 0) bulk_wait_read0();
+  } else if (TTT_BWD_LSU_LOADS) {
+    // ================= LSU loaders: warp 14 Q tiles + lse2 / Delta, warp 15 dO halves =================
+    // 16-byte cp.async per lane into the SW128 layout the TMA would produce (box bx = 64 columns, row r,
+    // chunk c at bx 16 KB (or bx 8 KB for a 64-row half) + r 128 + ((c ^ (r & 7)) << 4)); rows past the
+    // sequence view zero-fill. Completion: one cp.async.mbarrier.arrive.noinc per lane (count 32); the
+    // MMA warp fences the async proxy after its wait.
+    reg_dealloc<88>();
+    const bool isq = warp == 14;
+    const size_t rstride = (size_t)p.Hq * D;  // elements between consecutive rows of one head
+    const int lim = PACKED ? p.nrows : p.L;   // bound on (PACKED ? global : local) rows
+    const int c = lane & 7, r4 = lane >> 3;   // chunk c of rows r4, r4 + 4, ...
+    for (int t = 0; t < n_items; ++t) {
+      const int h = h_first + t / nq, qt = kt + t % nq;
+      const int loc0 = qt * kTile;  // first local row of the tile
+      if (isq) {
+        const int qs = t & 1, qph = (t >> 1) & 1;
+        mbar_wait(&bars.q_empty[qs], qph ^ 1);
+        const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((size_t)p.row0[b] + loc0) * rstride + (size_t)h * D;
+        const uint32_t dst = smem_u32(sQ + qs * TB);
+#pragma unroll 4
+        for (int i = 0; i < kTile * NBOX / 4; ++i) {  // (row, box) pairs: 4 rows per instruction
+          const int r = (i % (kTile / 4)) * 4 + r4, bx = i / (kTile / 4);
+          const int lr = loc0 + r;
+          const bool ok = (PACKED ? p.row0[b] + lr : lr) < lim;
+          cp_async16(dst + bx * 16384 + r * 128 + ((c ^ (r & 7)) << 4), src + (ok ? (size_t)r * rstride + bx * 64 + c * 8 : 0),
+                     ok ? 16u : 0u);
+        }
+        const size_t li = ws_at(p, PACKED, b, h, loc0);
+        cp_async16(smem_u32(sL + qs * 128) + lane * 16, p.lse2 + li + lane * 4, 16u);
+        cp_async16(smem_u32(sDel + qs * 128) + lane * 16, p.delta + li + lane * 4, 16u);
+        cp_async_arrive_noinc(&bars.q_full[qs]);
+      } else {
+#pragma unroll 1
+        for (int x = 0; x < 2; ++x) {
+          const int u = 2 * t + x, slot = u % 3, use = u / 3;
+          mbar_wait(&bars.do_empty[slot], (use & 1) ^ 1);
+          const int lb = loc0 + 64 * x;
+          const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.dout) + ((size_t)p.row0[b] + lb) * rstride + (size_t)h * D;
+          const uint32_t dst = smem_u32(sDO + slot * HB);
+#pragma unroll 4
+          for (int i = 0; i < 64 * NBOX / 4; ++i) {
+            const int r = (i % 16) * 4 + r4, bx = i / 16;
+            const int lr = lb + r;
+            const bool ok = (PACKED ? p.row0[b] + lr : lr) < lim;
+            cp_async16(dst + bx * (HB / NBOX) + r * 128 + ((c ^ (r & 7)) << 4),
+                       src + (ok ? (size_t)r * rstride + bx * 64 + c * 8 : 0), ok ? 16u : 0u);
+          }
+          cp_async_arrive_noinc(&bars.do_full[slot]);
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else {
     reg_dealloc<24>();  // warps 14-15: idle (a dq conversion of the previous unroll step here measured
                         // 5.78 vs 4.47 ms of main passes per unroll, r02c: reverted)
