@@ -64,9 +64,13 @@ namespace {
 constexpr int kFwdThreads = 512;
 // ONEREAD register split per SMSP: 2 softmax + 1 diagonal + 1 role warp <= 512 per lane
 #ifndef TTT_FWD_REG_SOFTMAX
-#define TTT_FWD_REG_SOFTMAX 168
+#define TTT_FWD_REG_SOFTMAX 176
 #endif
-constexpr uint32_t kFwdRegSoftmax = TTT_FWD_REG_SOFTMAX, kFwdRegDiag = 128, kFwdRegRole = 48;
+#ifndef TTT_FWD_REG_DIAG
+#define TTT_FWD_REG_DIAG 128
+#endif
+constexpr uint32_t kFwdRegSoftmax = TTT_FWD_REG_SOFTMAX, kFwdRegDiag = TTT_FWD_REG_DIAG,
+                   kFwdRegRole = 512 - 2 * TTT_FWD_REG_SOFTMAX - TTT_FWD_REG_DIAG;
 static_assert(2 * kFwdRegSoftmax + kFwdRegDiag + kFwdRegRole <= 512, "register file per SMSP");
 #ifndef TTT_FWD_DIAG_MODE
 #define TTT_FWD_DIAG_MODE 0  // dev timing probes only: 1 = diagonal warps skip the math, 2 = skip the loads
