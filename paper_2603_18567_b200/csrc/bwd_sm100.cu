@@ -617,6 +617,15 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
 // Shared memory (D = 128): K, V 64 KB | Q 2 x 32 KB | dO 3 x 16 KB ring of 64-row halves |
 // dS 32 KB ([kv][q], two 64-query SW128 boxes) | lse2, Delta 2 KB | dQ staging 4 x 4 KB.
 constexpr int kBwdThreads = 512;
+// setmaxnreg split per SMSP (warps s, 4+s, 8+s, 12+s): dQ drain + 2 compute + role (MMA / TMA / idle) <= 512
+#ifndef TTT_BWD_REG_CMP
+#define TTT_BWD_REG_CMP 136
+#endif
+#ifndef TTT_BWD_REG_DRAIN
+#define TTT_BWD_REG_DRAIN 152
+#endif
+constexpr uint32_t kBwdRegDrain = TTT_BWD_REG_DRAIN, kBwdRegCmp = TTT_BWD_REG_CMP, kBwdRegRole = 512 - kBwdRegDrain - 2 * kBwdRegCmp;
+static_assert(kBwdRegRole >= 24, "register file per SMSP");
 
 template <int D>
 struct BwdSmem {
@@ -739,7 +748,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 13) {
     // ================= TMA producer =================
-    reg_dealloc<88>();
+    reg_dealloc<kBwdRegRole>();
     if (lane == 0) {
       tma_prefetch_desc(&maps.q);
       tma_prefetch_desc(&maps.k);
@@ -802,7 +811,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp == 12) {
     // ================= MMA issuer (whole warp, converged; elect.sync inside each issue) =================
-    reg_dealloc<88>();
+    reg_dealloc<kBwdRegRole>();
     {
       TTT_TRACE_DECL(0);
       constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);  // S^T = K Q^T
@@ -1015,7 +1024,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp >= 4 && warp < 12) {
     // ================= compute: P^T, dS^T of sub-item x (thread = key row, 64 query columns) ====
-    reg_alloc<136>();
+    reg_alloc<kBwdRegCmp>();
     const int quad = warp & 3, x = (warp - 4) >> 2;
     const int row = quad * 32 + lane;
     const int k = kt * kTile + row;
@@ -1180,7 +1189,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ================= dQ drain (warps 0-3, thread = query row) =================
     // TMEM -> registers (scaled by c) -> warp-private SW128 staging -> TMA reduce-add into
     // the tile-contiguous fp32 dq_acc (one 32 x 32 box per 32-column chunk).
-    reg_alloc<152>();
+    reg_alloc<kBwdRegDrain>();
     const int wq = warp;
     const uint32_t tQ = tbase + ((uint32_t)(wq * 32) << 16) + 128;
     uint8_t* stage = sDQ + wq * 4096;
