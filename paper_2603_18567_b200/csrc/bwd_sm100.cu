@@ -711,7 +711,58 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int h_first = g * p.G + hs * nh;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1 KB alignment
 
-  if (threadIdx.x == 0) {
+  // producer: the loads of item t (Q tile + lse2 / Delta, then the two dO halves), each after its slot is free
+  auto issue_item = [&](int t) {
+#ifdef TTT_TRACE
+    int trace_n_2 = 32768 + 4 * t;
+#endif
+    const int h = h_first + t / nq, qt = kt + t % nq;
+    const int qs = t & 1, qph = (t >> 1) & 1;
+    if (TTT_BWD_PREFETCH && t + TTT_BWD_PREFETCH < n_items) {
+      // L2 prefetch of a later item's Q and dO tiles: the 2-slot Q / 3-half dO rings give ~1 item
+      // of lookahead, less than a TMA load's latency when the tile is not in L2 (r02e trace: the
+      // MMA pipe idled ~0.8k clk per item waiting for dO halves)
+      const int tp = t + TTT_BWD_PREFETCH;
+      const int hp = h_first + tp / nq, qtp = kt + tp % nq;
+#pragma unroll
+      for (int bx = 0; bx < NBOX; ++bx) {
+        tma_prefetch_4d(&maps.q, bx * 64, hp, ry + qtp * kTile, by);
+        tma_prefetch_4d(&maps.dout, bx * 64, hp, ry + qtp * kTile, by);
+      }
+    }
+    mbar_wait(&bars.q_empty[qs], qph ^ 1);
+    if (TTT_BWD_PROBE == 2 && t >= 2) {  // dev probe: no loads after the first two items
+      mbar_arrive(&bars.q_full[qs]);
+      for (int x = 0; x < 2; ++x) {
+        const int u = 2 * t + x, slot = u % 3, use = u / 3;
+        mbar_wait(&bars.do_empty[slot], (use & 1) ^ 1);
+        mbar_arrive(&bars.do_full[slot]);
+      }
+      return;
+    }
+    mbar_expect_tx(&bars.q_full[qs], TB + 1024);
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx)
+      tma_load_4d(sQ + qs * TB + bx * 16384, &maps.q, &bars.q_full[qs], bx * 64, h, ry + qt * kTile, by);
+    const size_t li = ws_at(p, PACKED, b, h, qt * kTile);
+    bulk_load_1d(sL + qs * 128, p.lse2 + li, 512, &bars.q_full[qs]);
+    bulk_load_1d(sDel + qs * 128, p.delta + li, 512, &bars.q_full[qs]);
+    TTT_TRACE_EV(2, 11, t);
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const int u = 2 * t + x, slot = u % 3, use = u / 3;
+      mbar_wait(&bars.do_empty[slot], (use & 1) ^ 1);
+      mbar_expect_tx(&bars.do_full[slot], HB);
+#pragma unroll
+      for (int bx = 0; bx < NBOX; ++bx)
+        tma_load_4d(sDO + slot * HB + bx * (HB / NBOX), &maps.dout64, &bars.do_full[slot], bx * 64, h,
+                    ry + qt * kTile + 64 * x, by);
+      TTT_TRACE_EV(2, 12 + x, t);
+    }
+  };
+  // The TMA producer thread (warp 13, lane 0) initialises the barriers and issues K / V and item 0's loads
+  // before the CTA-wide barrier, so their latency overlaps the TMEM allocation and the sync.
+  if (threadIdx.x == 416) {
     mbar_init(&bars.kv_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars.q_full[i], TTT_BWD_LSU_LOADS ? 32 : 1);  // LSU: one noinc arrive per loader lane
@@ -736,6 +787,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_init(&bars.acc_full, 1);
     fence_mbar_init();
+    tma_prefetch_desc(&maps.q);
+    tma_prefetch_desc(&maps.k);
+    tma_prefetch_desc(&maps.v);
+    tma_prefetch_desc(&maps.dout);
+    mbar_expect_tx(&bars.kv_full, 2 * TB);
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx) {
+      tma_load_4d(sK + bx * 16384, &maps.k, &bars.kv_full, bx * 64, g, ry + kt * kTile, by);
+      tma_load_4d(sV + bx * 16384, &maps.v, &bars.kv_full, bx * 64, g, ry + kt * kTile, by);
+    }
+    if (!TTT_BWD_LSU_LOADS) issue_item(0);  // n_items >= 1
   }
   if (warp == 12) {
     tmem_alloc(&bars.tmem_base, 512);
@@ -749,66 +811,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 13) {
     // ================= TMA producer =================
     reg_dealloc<kBwdRegRole>();
-    if (lane == 0) {
-      tma_prefetch_desc(&maps.q);
-      tma_prefetch_desc(&maps.k);
-      tma_prefetch_desc(&maps.v);
-      tma_prefetch_desc(&maps.dout);
-#ifdef TTT_TRACE
-      int trace_n_2 = 32768;  // the producer's events after the dQ drain warp's (role 2, index 0..)
-#endif
-      mbar_expect_tx(&bars.kv_full, 2 * TB);
-#pragma unroll
-      for (int bx = 0; bx < NBOX; ++bx) {
-        tma_load_4d(sK + bx * 16384, &maps.k, &bars.kv_full, bx * 64, g, ry + kt * kTile, by);
-        tma_load_4d(sV + bx * 16384, &maps.v, &bars.kv_full, bx * 64, g, ry + kt * kTile, by);
-      }
-      for (int t = 0; t < (TTT_BWD_LSU_LOADS ? 0 : n_items); ++t) {
-        const int h = h_first + t / nq, qt = kt + t % nq;
-        const int qs = t & 1, qph = (t >> 1) & 1;
-        if (TTT_BWD_PREFETCH && t + TTT_BWD_PREFETCH < n_items) {
-          // L2 prefetch of a later item's Q and dO tiles: the 2-slot Q / 3-half dO rings give ~1 item
-          // of lookahead, less than a TMA load's latency when the tile is not in L2 (r02e trace: the
-          // MMA pipe idled ~0.8k clk per item waiting for dO halves)
-          const int tp = t + TTT_BWD_PREFETCH;
-          const int hp = h_first + tp / nq, qtp = kt + tp % nq;
-#pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx) {
-            tma_prefetch_4d(&maps.q, bx * 64, hp, ry + qtp * kTile, by);
-            tma_prefetch_4d(&maps.dout, bx * 64, hp, ry + qtp * kTile, by);
-          }
-        }
-        mbar_wait(&bars.q_empty[qs], qph ^ 1);
-        if (TTT_BWD_PROBE == 2 && t >= 2) {  // dev probe: no loads after the first two items
-          mbar_arrive(&bars.q_full[qs]);
-          for (int x = 0; x < 2; ++x) {
-            const int u = 2 * t + x, slot = u % 3, use = u / 3;
-            mbar_wait(&bars.do_empty[slot], (use & 1) ^ 1);
-            mbar_arrive(&bars.do_full[slot]);
-          }
-          continue;
-        }
-        mbar_expect_tx(&bars.q_full[qs], TB + 1024);
-#pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sQ + qs * TB + bx * 16384, &maps.q, &bars.q_full[qs], bx * 64, h, ry + qt * kTile, by);
-        const size_t li = ws_at(p, PACKED, b, h, qt * kTile);
-        bulk_load_1d(sL + qs * 128, p.lse2 + li, 512, &bars.q_full[qs]);
-        bulk_load_1d(sDel + qs * 128, p.delta + li, 512, &bars.q_full[qs]);
-        TTT_TRACE_EV(2, 11, t);
-#pragma unroll
-        for (int x = 0; x < 2; ++x) {
-          const int u = 2 * t + x, slot = u % 3, use = u / 3;
-          mbar_wait(&bars.do_empty[slot], (use & 1) ^ 1);
-          mbar_expect_tx(&bars.do_full[slot], HB);
-#pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx)
-            tma_load_4d(sDO + slot * HB + bx * (HB / NBOX), &maps.dout64, &bars.do_full[slot], bx * 64, h,
-                        ry + qt * kTile + 64 * x, by);
-          TTT_TRACE_EV(2, 12 + x, t);
-        }
-      }
-    }
+    if (lane == 0)
+      for (int t = 1; t < (TTT_BWD_LSU_LOADS ? 0 : n_items); ++t) issue_item(t);
   } else if (warp == 12) {
     // ================= MMA issuer (whole warp, converged; elect.sync inside each issue) =================
     reg_dealloc<kBwdRegRole>();

@@ -175,7 +175,41 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   // TMA (row, batch) origin of this sequence: (0, b) padded, (row0[b], 0) packed (TREE: never packed)
   const int ry = PACKED ? p.row0[b] : 0, by = PACKED ? 0 : b;
 
-  if (threadIdx.x == 0) {
+  // The TMA producer thread (warp 8, lane 0) initialises the barriers and issues the Q and first K / V
+  // loads before the CTA-wide barrier, so their latency overlaps the TMEM allocation and the sync.
+  auto load_q = [&]() {
+    tma_prefetch_desc(&maps.q);
+    tma_prefetch_desc(&maps.k);
+    tma_prefetch_desc(&maps.v);
+    if constexpr (TREE) {  // 64-row boxes: head h0 + k -> slot k / 2, rows 64 (k % 2) ..
+      mbar_expect_tx(&bars.q, nheads * (TB / 2));
+#pragma unroll
+      for (int bx = 0; bx < NBOX; ++bx)
+        for (int k = 0; k < nheads; ++k)
+          tma_load_4d(sQ + (k >> 1) * TB + bx * 16384 + (k & 1) * 8192, &maps.q, &bars.q, bx * 64, h0 + k, 0, b);
+    } else {
+      mbar_expect_tx(&bars.q, (has1 ? 2 : 1) * TB);
+#pragma unroll
+      for (int bx = 0; bx < NBOX; ++bx) {
+        tma_load_4d(sQ + bx * 16384, &maps.q, &bars.q, bx * 64, h0, ry + qt * kTile, by);
+        if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.q, &bars.q, bx * 64, h0 + 1, ry + qt * kTile, by);
+      }
+    }
+  };
+  auto load_kv = [&](int n) {
+    const int st = n & 1, ph = (n >> 1) & 1;
+    mbar_wait(&bars.k_empty[st], ph ^ 1);
+    mbar_expect_tx(&bars.k_full[st], TB);
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx)
+      tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, g, ry + (kvt0 + n) * kTile, by);
+    mbar_wait(&bars.v_empty[st], ph ^ 1);
+    mbar_expect_tx(&bars.v_full[st], TB);
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx)
+      tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, ry + (kvt0 + n) * kTile, by);
+  };
+  if (threadIdx.x == 256) {
     mbar_init(&bars.q, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars.k_full[i], 1);
@@ -195,6 +229,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     mbar_init(&bars.diag_done, 128);  // every thread of the diagonal warps arrives after its own reads / writes
     fence_mbar_init();
+    load_q();
+    load_kv(0);  // nkv >= 1 (T_b >= 1; tree splits are never empty)
   }
   if (warp == 9) {
     tmem_alloc(&bars.tmem_base, 512);
@@ -212,36 +248,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // ================= TMA producer =================
     if (TTT_FWD_ONEREAD) regs_dec<kFwdRegRole>();
     if (lane == 0) {
-      tma_prefetch_desc(&maps.q);
-      tma_prefetch_desc(&maps.k);
-      tma_prefetch_desc(&maps.v);
-      if constexpr (TREE) {  // 64-row boxes: head h0 + k -> slot k / 2, rows 64 (k % 2) ..
-        mbar_expect_tx(&bars.q, nheads * (TB / 2));
-#pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx)
-          for (int k = 0; k < nheads; ++k)
-            tma_load_4d(sQ + (k >> 1) * TB + bx * 16384 + (k & 1) * 8192, &maps.q, &bars.q, bx * 64, h0 + k, 0, b);
-      } else {
-        mbar_expect_tx(&bars.q, (has1 ? 2 : 1) * TB);
-#pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx) {
-          tma_load_4d(sQ + bx * 16384, &maps.q, &bars.q, bx * 64, h0, ry + qt * kTile, by);
-          if (has1) tma_load_4d(sQ + TB + bx * 16384, &maps.q, &bars.q, bx * 64, h0 + 1, ry + qt * kTile, by);
-        }
-      }
-      for (int n = 0; n < nkv; ++n) {
-        const int st = n & 1, ph = (n >> 1) & 1;
-        mbar_wait(&bars.k_empty[st], ph ^ 1);
-        mbar_expect_tx(&bars.k_full[st], TB);
-#pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, g, ry + (kvt0 + n) * kTile, by);
-        mbar_wait(&bars.v_empty[st], ph ^ 1);
-        mbar_expect_tx(&bars.v_full[st], TB);
-#pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, ry + (kvt0 + n) * kTile, by);
-      }
+      for (int n = 1; n < nkv; ++n) load_kv(n);  // Q and tile 0 were issued with the barrier setup
       if (!TREE && p.step > 0) {  // diagonal partial of the two heads into the Q tiles once no S MMA
                                   // reads them and the diagonal warps have written it
         mbar_wait(&bars.s_done, 0);
