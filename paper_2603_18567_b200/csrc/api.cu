@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <cstdlib>
 #include <mutex>
 #include <queue>
 #include <vector>
@@ -182,6 +183,11 @@ int map_l(const Params& p) { return p.packed ? p.nrows : p.L; }
 }  // namespace
 
 namespace tttk {
+int dev_env_int(const char* name, int def) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : def;
+}
+
 int pick_order_batch(int ngroups, int nranks, int copies, const double* len_of_rank, double overhead,
                      double bytes_per_group) {
   struct Key {

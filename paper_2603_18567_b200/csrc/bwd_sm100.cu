@@ -1456,7 +1456,8 @@ cudaError_t launch_pre(const Params& p, const PreMaps& pmaps, const UnrollPre& u
 template <int D>
 cudaError_t launch_main_convert(const Params& p_in, const BwdMaps& maps, cudaStream_t st, bool convert = true) {
   Params p = p_in;
-  p.head_split = pick_head_split(p);
+  static const int env_hs = dev_env_int("TTT_DEV_BWD_HSPLIT", 0), env_ob = dev_env_int("TTT_DEV_BWD_ORDER_BATCH", 0);
+  p.head_split = env_hs > 0 && p.G % env_hs == 0 ? env_hs : pick_head_split(p);
   if (!p.packed) {  // CTA order: CTA kt of a group runs (nqt - kt) items of G / head_split heads; ~4.5k clk per
      // item and ~12k of fixed cost (measured traces); a group's Q, dO, dq_acc: 8 B per q element
     std::vector<double> len(p.nqt);
@@ -1464,6 +1465,7 @@ cudaError_t launch_main_convert(const Params& p_in, const BwdMaps& maps, cudaStr
     for (int r = 0; r < p.nqt; ++r) len[r] = (double)nh * (p.nqt - r) * 4.5;
     p.order_batch = pick_order_batch(p.B * p.Hkv * p.head_split, p.nqt, 1, len.data(), 12.0,
                                      (double)nh * p.L * D * 8);
+    if (env_ob > 0) p.order_batch = env_ob;
   }
   {
     const int smem = BwdSmem<D>::bytes;

@@ -164,5 +164,7 @@ inline cudaError_t set_smem_attr(F* fn, int bytes, std::atomic<unsigned long lon
 
 int pick_order_batch(int ngroups, int nranks, int copies, const double* len_of_rank, double overhead,
                      double bytes_per_group);
+// dev-only schedule overrides (A/B experiments): integer environment variable, read once; `def` when unset
+int dev_env_int(const char* name, int def);
 
 }  // namespace tttk
