@@ -93,3 +93,18 @@ def test_ttt_length_17_llama_full_size_row_subset(cuda_ok):
         assert_close(f"S17 llama dk_{i + 1}", np32(g["dk_steps"][i]), og["dk_steps"][i], **TOL_BF16)
         assert_close(f"S17 llama dv_{i + 1}", np32(g["dv_steps"][i]), og["dv_steps"][i], **TOL_BF16)
     assert np.abs(np32(dq)[~selq]).max() == 0.0
+
+
+@pytest.mark.parametrize("dtype,shape,tol", [
+    (torch.bfloat16, Shape(1, 256, 8, 2, 128, 32), TOL_BF16),
+    (torch.bfloat16, Shape(1, 256, 4, 4, 64, 32), TOL_BF16),
+    (torch.float32, Shape(1, 128, 4, 2, 64, 32), TOL_FP32),
+], ids=["bf16_g4_d128", "bf16_mha_d64", "fp32_check"])
+def test_max_step_31(cuda_ok, dtype, shape, tol):
+    """The ABI's largest step, j = TTT_MAX_STEPS - 1 = 31 (31 diagonal keys per row, every step-list
+    slot of the parameter block and of the diagonal rings in use; an odd count, so the forward's
+    diagonal warps end on a single-stage pass), plus j = 30, against the oracle with ragged lengths."""
+    case = make_case(shape, dtype=dtype, seed=31, lens="ragged")
+    dc = DeviceCase(case)
+    for j in (31, 30):
+        _check_step(f"S32 {dtype}", dc, case, j, tol)
