@@ -427,6 +427,8 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
         "frac_of_bf16_burst_peak": tflops / peaks["bf16_tflops"],
         "frac_of_bf16_sustained_peak": tflops / peaks["bf16_tflops_sustained"],
         "flops_convention": "algorithmic 12*D per allowed (q,k) pair (fwd 4D + bwd 8D; recompute excluded)",
+        # the FlashAttention literature's convention, bwd = 2.5 x fwd (14 D per pair), for comparison
+        "tflops_per_gpu_fa_convention": tflops * 14.0 / 12.0,
         "bwd_api": "ttt_attn_bwd_unroll (one call per unroll)" if u.bwd_unroll else "ttt_attn_bwd x S",
         "roofline": roof,
         "kernels_ms_per_step": {k: v[0] / prof_steps for k, v in kern.items()},
