@@ -1063,6 +1063,9 @@ cudaError_t launch_fwd_d(const Params& p_in, const FwdMaps& maps, const DiagMaps
     std::vector<double> len(p.nqt);
     for (int r = 0; r < p.nqt; ++r) len[r] = (double)(p.nqt - r) * 3.3;
     p.order_batch = pick_order_batch(p.B * p.Hkv, p.nqt, (p.G + 1) / 2, len.data(), 7.0, (double)p.L * D * 4);
+    // at most 4 (b, g) groups per batch: the model (tail balance only) picks 32 at the Llama shape, but fewer
+    // groups in flight measured faster (r03s / r03y: 4 groups -1.2% at Llama, -2% at L = 16K; 1-2 slower)
+    p.order_batch = std::min(p.order_batch, 4);
     static const int env_ob = dev_env_int("TTT_DEV_FWD_ORDER_BATCH", 0);
     if (env_ob > 0) p.order_batch = env_ob;
   }
