@@ -80,6 +80,12 @@ static_assert(2 * kFwdRegSoftmax + kFwdRegDiag + kFwdRegRole <= 512, "register f
 #endif
 constexpr int kDgRows = 16;    // rows per diagonal-ring stage (one TMA box per 64 columns per tensor)
 constexpr int kDgStages = 4;   // diagonal-ring depth
+// Short CTAs (nkv <= TTT_FWD_SHD_NKV kv tiles) finish their main loop long before the diagonal (r03g: a
+// 1-tile CTA at j = 6 ran 53k clk vs 16k at j = 0): there the softmax warps take the last 2/3 of the
+// diagonal's 16-row blocks after their main loop, loading K_i / V_i rows straight from global memory.
+#ifndef TTT_FWD_SHD_NKV
+#define TTT_FWD_SHD_NKV 4
+#endif
 // Q (2 tiles) | K (2 stages) | V (2 stages) | diagonal ring | 1 KB alignment slack
 constexpr int fwd_smem_bytes(int D) { return 6 * kTile * D * 2 + kDgStages * 2 * (D / 64) * kDgRows * 128 + 1024; }
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only when the max grows by > 2^8
@@ -172,6 +178,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     nkv = min(qt + 1, (T + kTile - 1) / kTile);  // BlockMask: skip k0 > q0+127 and k0 >= T
   }
   const int bst = TREE ? split * p.B + b : b;  // batch index of this CTA's out / lse rows
+  // diagonal row blocks: nrb of this q tile hold rows r < T_b; the diagonal warps take [0, nrb_d), the
+  // softmax warps (SHD, short CTAs) the rest
+  const int nrb = (!TREE && T > qt * kTile) ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
+  const bool shd = !TREE && TTT_FWD_FUSED_DIAG && p.step > 0 && nkv <= TTT_FWD_SHD_NKV;
+  const int nrb_d = shd ? (nrb + 2) / 3 : nrb;
   // TMA (row, batch) origin of this sequence: (0, b) padded, (row0[b], 0) packed (TREE: never packed)
   const int ry = PACKED ? p.row0[b] : 0, by = PACKED ? 0 : b;
 
@@ -227,7 +238,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bars.dg_full[i], 1);
       mbar_init(&bars.dg_empty[i], 4);  // the four diagonal compute warps
     }
-    mbar_init(&bars.diag_done, 128);  // every thread of the diagonal warps arrives after its own reads / writes
+    // every thread of the diagonal warps (and, SHD, of the active softmax warps) arrives after its own reads / writes
+    mbar_init(&bars.diag_done, 128 + (shd ? (has1 ? 256 : 128) : 0));
     fence_mbar_init();
     load_q();
     load_kv(0);  // nkv >= 1 (T_b >= 1; tree splits are never empty)
@@ -343,9 +355,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (TTT_FWD_ONEREAD) regs_dec<kFwdRegRole>();
     if (TTT_FWD_FUSED_DIAG && !TREE && p.step > 0 && warp == 14 && lane == 0) {
       const int j = p.step;
-      const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
       int n = 0;
-      for (int rb = 0; rb < nrb; ++rb)
+      for (int rb = 0; rb < nrb_d; ++rb)
         for (int i = 0; i < j; ++i, ++n) {
           const int st = n % kDgStages, use = n / kDgStages;
           mbar_wait(&bars.dg_empty[st], (use & 1) ^ 1);
@@ -367,8 +378,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
     if (TTT_FWD_FUSED_DIAG && !TREE && p.step > 0) {
       const int j = p.step;
-      // 16-row blocks of this q tile holding at least one row r < T_b
-      const int nrb = T > qt * kTile ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
       {
         // thread layout: 8 lanes per row (lane k = lane & 7 owns columns 8k..8k+7 of every 64-column
         // box), 4 rows per warp, 16 rows per stage; both head slots per row
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         TTT_TRACE_DECL(3);
         if (threadIdx.x == 320) TTT_TRACE_EV(3, 4, 0);
         int n = 0;
-        for (int rb = 0; rb < nrb; ++rb) {
+        for (int rb = 0; rb < nrb_d; ++rb) {
           const int row = rb * kDgRows + srow;
           const int r = qt * kTile + row;
           float qf[2][E], acc[2][E], m[2], l[2];
@@ -688,6 +697,139 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 2, n);
         if (threadIdx.x == 128) TTT_TRACE_EV(2, 2, n);
+      }
+      if (shd) {
+        // ---- SHD: diagonal rows [nrb_d 16, nrb 16) on the softmax warps (same math as warps 10-13) ----
+        // 8 lanes per row (lane k owns columns 8k..8k+7 of every 64-column box), 4 rows per warp, both head
+        // slots per row; K_i / V_i rows from global memory, the next stage pair's loads issued before the
+        // current pair's math.
+        constexpr int E = 8 * NBOX;
+        const int hw = warp, k8 = lane & 7;            // helper warp 0..7 (0..3 without slot 1)
+        const int hrows = (has1 ? 8 : 4) * 4;           // rows per pass
+        const int j = p.step;
+        const float hsl2 = p.scale_log2;
+        const size_t kvrow0 = (size_t)(PACKED ? p.row0[b] : b * p.L);
+        for (int hrow = nrb_d * kDgRows + hw * 4 + (lane >> 3); hrow < nrb * kDgRows; hrow += hrows) {
+          const int hr = qt * kTile + hrow;
+          const bool valid = hr < T;
+          float qf[2][E], acc[2][E], m[2], l[2];
+#pragma unroll
+          for (int hs = 0; hs < 2; ++hs) {
+            m[hs] = -INFINITY;
+            l[hs] = 0.f;
+#pragma unroll
+            for (int bx = 0; bx < NBOX; ++bx) {
+              const uint4 u = lds128(smem_u32(sQ + hs * TB + bx * 16384) + sw128_off(hrow, k8));
+              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+                qf[hs][bx * 8 + 2 * e] = f.x * hsl2;
+                qf[hs][bx * 8 + 2 * e + 1] = f.y * hsl2;
+                acc[hs][bx * 8 + 2 * e] = 0.f;
+                acc[hs][bx * 8 + 2 * e + 1] = 0.f;
+              }
+            }
+          }
+          const size_t eoff = ((kvrow0 + hr) * p.Hkv + g) * D + k8 * 8;  // this lane's first element
+          auto load_step = [&](int i, uint32_t (&kw)[E / 2], uint32_t (&vw)[E / 2]) {
+            if (valid && i < j) {
+              const __nv_bfloat16* kp = reinterpret_cast<const __nv_bfloat16*>(p.ks[i]) + eoff;
+              const __nv_bfloat16* vp = reinterpret_cast<const __nv_bfloat16*>(p.vs[i]) + eoff;
+#pragma unroll
+              for (int bx = 0; bx < NBOX; ++bx) {
+                const uint4 uk = __ldg(reinterpret_cast<const uint4*>(kp + bx * 64));
+                const uint4 uv = __ldg(reinterpret_cast<const uint4*>(vp + bx * 64));
+                kw[bx * 4 + 0] = uk.x; kw[bx * 4 + 1] = uk.y; kw[bx * 4 + 2] = uk.z; kw[bx * 4 + 3] = uk.w;
+                vw[bx * 4 + 0] = uv.x; vw[bx * 4 + 1] = uv.y; vw[bx * 4 + 2] = uv.z; vw[bx * 4 + 3] = uv.w;
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < E / 2; ++e) kw[e] = vw[e] = 0u;
+            }
+          };
+          uint32_t kc[2][E / 2], vc[2][E / 2];  // current pair
+          load_step(0, kc[0], vc[0]);
+          load_step(1, kc[1], vc[1]);
+          for (int i = 0; i < j; i += 2) {
+            const int ns = min(2, j - i);
+            uint32_t kn[2][E / 2], vn[2][E / 2];  // next pair, in flight during this pair's math
+            load_step(i + 2, kn[0], vn[0]);
+            load_step(i + 3, kn[1], vn[1]);
+            float t[2][2];
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                uint64_t d0 = 0, d1 = 0;
+#pragma unroll
+                for (int e = 0; e < E / 2; e += 2) {
+                  d0 = ffma2(f2pack(qf[hs][2 * e], qf[hs][2 * e + 1]), bf2_to_f2(kc[u][e]), d0);
+                  d1 = ffma2(f2pack(qf[hs][2 * e + 2], qf[hs][2 * e + 3]), bf2_to_f2(kc[u][e + 1]), d1);
+                }
+                float a0, a1, b0, b1;
+                f2unpack(d0, a0, a1);
+                f2unpack(d1, b0, b1);
+                t[hs][u] = (a0 + a1) + (b0 + b1);
+              }
+#pragma unroll
+            for (int sh = 1; sh < 8; sh <<= 1)
+#pragma unroll
+              for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) t[hs][u] += __shfl_xor_sync(0xffffffffu, t[hs][u], sh);
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs) {
+              const float tmax = ns > 1 ? fmaxf(t[hs][0], t[hs][1]) : t[hs][0];
+              if (__any_sync(0xffffffffu, tmax > m[hs] + 8.f)) {  // rare: the max moved (always at i = 0)
+                const float m_new = fmaxf(m[hs], tmax);
+                const float alpha = ex2(m[hs] - m_new);
+                l[hs] *= alpha;
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc[hs][e] *= alpha;
+                m[hs] = m_new;
+              }
+              const float p0 = ex2(t[hs][0] - m[hs]), p1 = ns > 1 ? ex2(t[hs][1] - m[hs]) : 0.f;
+              l[hs] += p0 + p1;
+              const uint64_t p02 = f2pack(p0, p0), p12 = f2pack(p1, p1);
+#pragma unroll
+              for (int e = 0; e < E / 2; ++e) {
+                uint64_t o = ffma2(bf2_to_f2(vc[0][e]), p02, f2pack(acc[hs][2 * e], acc[hs][2 * e + 1]));
+                o = ffma2(bf2_to_f2(vc[1][e]), p12, o);
+                f2unpack(o, acc[hs][2 * e], acc[hs][2 * e + 1]);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+              for (int e = 0; e < E / 2; ++e) {
+                kc[u][e] = kn[u][e];
+                vc[u][e] = vn[u][e];
+              }
+          }
+          if (valid) {
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs) {
+              if (hs == 0 || has1) {
+                const float inv = 1.f / l[hs];
+                __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + ((kvrow0 + hr) * p.Hq + h0 + hs) * D;
+#pragma unroll
+                for (int bx = 0; bx < NBOX; ++bx) {
+                  uint4 w;
+                  w.x = pack_bf16(acc[hs][bx * 8 + 0] * inv, acc[hs][bx * 8 + 1] * inv);
+                  w.y = pack_bf16(acc[hs][bx * 8 + 2] * inv, acc[hs][bx * 8 + 3] * inv);
+                  w.z = pack_bf16(acc[hs][bx * 8 + 4] * inv, acc[hs][bx * 8 + 5] * inv);
+                  w.w = pack_bf16(acc[hs][bx * 8 + 6] * inv, acc[hs][bx * 8 + 7] * inv);
+                  *reinterpret_cast<uint4*>(orow + bx * 64 + k8 * 8) = w;
+                }
+                if (k8 == 0) bars.a_d[hs][hrow] = m[hs] + log2f(l[hs]);
+              }
+            }
+          }
+        }
+        fence_async_global();  // the out rows are read back by the producer's TMA (async proxy)
+        __threadfence_block();
+        mbar_arrive(&bars.diag_done);
       }
       // ---- epilogue: merge the diagonal partial, normalise, store ----
       // The j diagonal keys of row r (Alg. 1 "concat s_i") were reduced
