@@ -618,8 +618,11 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
 // dS 32 KB ([kv][q], two 64-query SW128 boxes) | lse2, Delta 2 KB | dQ staging 4 x 4 KB.
 constexpr int kBwdThreads = 512;
 // setmaxnreg split per SMSP (warps s, 4+s, 8+s, 12+s): dQ drain + 2 compute + role (MMA / TMA / idle) <= 512
+#ifndef TTT_BWD_DS_ONEWAIT
+#define TTT_BWD_DS_ONEWAIT 0  // dev, 1: dS phase loads dP^T with one 64-column TMEM load (152-register split); r04b: equal (4.55-4.56 ms)
+#endif
 #ifndef TTT_BWD_REG_CMP
-#define TTT_BWD_REG_CMP 136
+#define TTT_BWD_REG_CMP (TTT_BWD_DS_ONEWAIT ? 152 : 136)
 #endif
 #ifndef TTT_BWD_REG_DRAIN
 #define TTT_BWD_REG_DRAIN 152
@@ -1106,9 +1109,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (threadIdx.x == 128) TTT_TRACE_EV(1, 3, t);
       tc_fence_after();
 #pragma unroll
+#if TTT_BWD_DS_ONEWAIT
+      uint32_t rawdp[64];
+      tmem_ld64w(tdP, rawdp);  // both 32-column halves of dP^T with one wait (needs the 152-register split)
+#endif
       for (int cc = 0; cc < 2; ++cc) {
+#if TTT_BWD_DS_ONEWAIT
+        const uint32_t* raw = rawdp + cc * 32;
+#else
         uint32_t raw[32];
         tmem_ld32(tdP + cc * 32, raw);
+#endif
         uint32_t pk[16];
 #pragma unroll
         for (int e4 = 0; e4 < 8; ++e4) {
