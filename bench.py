@@ -456,6 +456,9 @@ def run_ours(args, shape: Shape, rank: int, world: int, local_rank: int):
                 del sets, u, opt
                 torch.cuda.empty_cache()
                 line["next_rows"]["dp_sweep_n1"] = run_dp_n1(args, stream, peaks)
+        if world == 1:
+            line["next_rows"]["draft_layer_step"] = run_draft(args, stream, peaks,
+                                                              warm_unroll_ms if cfg == "llama8b" else None)
         line["next_rows"]["tree_verify"] = run_tree(args, stream, peaks)
         line["next_rows"]["qkv_rope"] = run_rope(args, stream, peaks)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -553,6 +556,54 @@ def run_loss(args, stream, peaks, world: int):
                      "avg_launch_ms": avg, "algorithmic_bytes_per_launch": alg_bytes,
                      "traffic": ncu_traffic("ttt_loss_ring_kernel") or ncu_traffic("ttt_loss_kernel")},
     }
+
+
+def run_draft(args, stream, peaks, attn_unroll_ms=None):
+    """SURVEY.md §8(f) NEXT #2, beside the headline: one training step (forward + backward, no optimizer
+    update) of the EAGLE-3 draft layer unrolled over 7 TTT steps (draft.DraftTTT: fc 3d -> d, RMSNorms,
+    the q/k/v projection with our RoPE / step-slot kernel, our TTT attention, o_proj, SwiGLU MLP 14336,
+    LM head 32000 and our soft-label loss with the Alg. 3 in-place backward; projections on cuBLAS) at the
+    Llama-3.1-8B draft shape B = 8, L = 2048 — how much of a draft-training step the attention is."""
+    from paper_2603_18567_b200.draft import DraftTTT
+    B, L, d, Hq, Hkv, D, V, I, S = 8, 2048, 4096, 32, 8, 128, 32000, 14336, 7
+    dev = stream.device
+    try:
+        model = DraftTTT(d, Hq, Hkv, D, V, intermediate=I, device=dev, seed=3)
+        g = torch.Generator(device=dev).manual_seed(21)
+        lmh = (torch.randn(B, L, 3 * d, device=dev, generator=g) * 0.5).to(torch.bfloat16)
+        targets = [torch.softmax(torch.randn(B * L, V, device=dev, generator=g), -1).to(torch.bfloat16)
+                   for _ in range(S)]
+
+        def one():
+            for prm in model.parameters():
+                prm.grad = None
+            model(lmh, targets).backward()
+
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                one()
+            torch.cuda.synchronize()
+            iters = 3
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(iters):
+                one()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / iters
+        res = {"workload": f"EAGLE-3 draft layer (d={d}, {Hq}/{Hkv} heads x {D}, MLP {I}, vocab {V}), {S} TTT steps, "
+                           f"B={B} x L={L}, forward + backward (no optimizer update)",
+               "ms_per_step": ms, "tokens_per_s": B * L / (ms / 1e3)}
+        if attn_unroll_ms:
+            res["attention_unroll_ms"] = attn_unroll_ms
+            res["attention_share"] = attn_unroll_ms / ms
+            res["note"] = ("attention = the headline's 7-step unroll of the same shape (same calls); the rest is cuBLAS "
+                           "projections / MLP / LM head, torch RMSNorms and our RoPE and loss kernels")
+        del model, lmh, targets
+        torch.cuda.empty_cache()
+        return res
+    except Exception as e:  # noqa: BLE001 - a side row; the headline stands without it
+        return {"error": f"{type(e).__name__}: {str(e)[:300]}"}
 
 
 def run_rope(args, stream, peaks):
