@@ -101,6 +101,106 @@ struct FwdBars {
   float a_d[2][kTile];  // A_d = log2 sum_i 2^t_i per (head slot, row), from the diagonal warps
 };
 
+// ---- the diagonal fold's per-row math, shared by the diagonal warps and, in
+// short CTAs, the softmax warps. Thread layout: 8 lanes per row (lane k8 owns columns 8 k8 .. 8 k8 + 7 of
+// every 64-column box, E = 8 NBOX elements), both head slots of the CTA per row.
+// q row (bf16 in the SW128 Q tiles) -> fp32 scaled by c log2 e; acc, l = 0; m = -inf
+template <int NBOX>
+__device__ __forceinline__ void diag_row_init(const uint8_t* sQ, int TB, int row, int k8, float sl2, float (&qf)[2][8 * NBOX],
+                                              float (&acc)[2][8 * NBOX], float (&m)[2], float (&l)[2]) {
+#pragma unroll
+  for (int hs = 0; hs < 2; ++hs) {
+    m[hs] = -INFINITY;
+    l[hs] = 0.f;
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx) {
+      const uint4 u = lds128(smem_u32(sQ + hs * TB + bx * 16384) + sw128_off(row, k8));
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+        qf[hs][bx * 8 + 2 * e] = f.x * sl2;
+        qf[hs][bx * 8 + 2 * e + 1] = f.y * sl2;
+        acc[hs][bx * 8 + 2 * e] = 0.f;
+        acc[hs][bx * 8 + 2 * e + 1] = 0.f;
+      }
+    }
+  }
+}
+// One pass over ns (1 or 2) stages (i, i + 1) of this lane's K_i / V_i words (bf16 pairs): the two
+// stages' dot products, shuffles and exps are independent, and the running max only moves (a
+// warp-uniform rescale) when a score exceeds it by 2^8 — the j-long chain of an exact online softmax
+// was the fused pass's critical path. t = c log2e q . K_i[r]; p = 2^(t - m); acc += p V_i[r].
+template <int E>
+__device__ __forceinline__ void diag_pair_update(const float (&qf)[2][E], float (&acc)[2][E], float (&m)[2], float (&l)[2],
+                                                 const uint32_t (&kw)[2][E / 2], const uint32_t (&vw)[2][E / 2], int ns) {
+  float t[2][2];  // 8-lane partial dots (two FFMA2 chains each)
+#pragma unroll
+  for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      uint64_t d0 = 0, d1 = 0;
+#pragma unroll
+      for (int e = 0; e < E / 2; e += 2) {
+        d0 = ffma2(f2pack(qf[hs][2 * e], qf[hs][2 * e + 1]), bf2_to_f2(kw[u][e]), d0);
+        d1 = ffma2(f2pack(qf[hs][2 * e + 2], qf[hs][2 * e + 3]), bf2_to_f2(kw[u][e + 1]), d1);
+      }
+      float a0, a1, b0, b1;
+      f2unpack(d0, a0, a1);
+      f2unpack(d1, b0, b1);
+      t[hs][u] = (a0 + a1) + (b0 + b1);
+    }
+#pragma unroll
+  for (int sh = 1; sh < 8; sh <<= 1)
+#pragma unroll
+    for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) t[hs][u] += __shfl_xor_sync(0xffffffffu, t[hs][u], sh);
+#pragma unroll
+  for (int hs = 0; hs < 2; ++hs) {
+    const float tmax = ns > 1 ? fmaxf(t[hs][0], t[hs][1]) : t[hs][0];
+    if (__any_sync(0xffffffffu, tmax > m[hs] + 8.f)) {  // rare: the max moved (always at i = 0)
+      const float m_new = fmaxf(m[hs], tmax);
+      const float alpha = ex2(m[hs] - m_new);  // 0 when m was -inf
+      l[hs] *= alpha;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[hs][e] *= alpha;
+      m[hs] = m_new;
+    }
+    const float p0 = ex2(t[hs][0] - m[hs]), p1 = ns > 1 ? ex2(t[hs][1] - m[hs]) : 0.f;
+    l[hs] += p0 + p1;
+    const uint64_t p02 = f2pack(p0, p0), p12 = f2pack(p1, p1);
+#pragma unroll
+    for (int e = 0; e < E / 2; ++e) {
+      uint64_t o = ffma2(bf2_to_f2(vw[0][e]), p02, f2pack(acc[hs][2 * e], acc[hs][2 * e + 1]));
+      o = ffma2(bf2_to_f2(vw[1][e]), p12, o);
+      f2unpack(o, acc[hs][2 * e], acc[hs][2 * e + 1]);
+    }
+  }
+}
+// O_d (normalised, bf16) -> the out rows (staging; read back by TMA), A_d = m + log2 l -> shared memory
+template <int NBOX>
+__device__ __forceinline__ void diag_row_store(__nv_bfloat16* orow0, int Dh, int k8, bool has1, const float (&acc)[2][8 * NBOX],
+                                               const float (&m)[2], const float (&l)[2], float* a_d0, float* a_d1) {
+#pragma unroll
+  for (int hs = 0; hs < 2; ++hs) {
+    if (hs == 0 || has1) {
+      const float inv = 1.f / l[hs];
+      __nv_bfloat16* orow = orow0 + hs * Dh;
+#pragma unroll
+      for (int bx = 0; bx < NBOX; ++bx) {
+        uint4 w;
+        w.x = pack_bf16(acc[hs][bx * 8 + 0] * inv, acc[hs][bx * 8 + 1] * inv);
+        w.y = pack_bf16(acc[hs][bx * 8 + 2] * inv, acc[hs][bx * 8 + 3] * inv);
+        w.z = pack_bf16(acc[hs][bx * 8 + 4] * inv, acc[hs][bx * 8 + 5] * inv);
+        w.w = pack_bf16(acc[hs][bx * 8 + 6] * inv, acc[hs][bx * 8 + 7] * inv);
+        *reinterpret_cast<uint4*>(orow + bx * 64 + k8 * 8) = w;
+      }
+      if (k8 == 0) *(hs == 0 ? a_d0 : a_d1) = m[hs] + log2f(l[hs]);
+    }
+  }
+}
+
 // TREE = true: tree-attention verification (ttt_tree_attn_fwd) on the
 // same pipeline: one q tile of the n <= 64 tree tokens per (b, head pair); keys = the prefix
 // (all allowed) followed by the tree tokens' own keys, allowed per query row by its
@@ -393,27 +493,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int row = rb * kDgRows + srow;
           const int r = qt * kTile + row;
           float qf[2][E], acc[2][E], m[2], l[2];
-#pragma unroll
-          for (int hs = 0; hs < 2; ++hs) {
-            m[hs] = -INFINITY;
-            l[hs] = 0.f;
-#pragma unroll
-            for (int bx = 0; bx < NBOX; ++bx) {
-              const uint4 u = lds128(smem_u32(sQ + hs * TB + bx * 16384) + sw128_off(row, k8));
-              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
-                qf[hs][bx * 8 + 2 * e] = f.x * sl2;
-                qf[hs][bx * 8 + 2 * e + 1] = f.y * sl2;
-                acc[hs][bx * 8 + 2 * e] = 0.f;
-                acc[hs][bx * 8 + 2 * e + 1] = 0.f;
-              }
-            }
-          }
-          // Stages two at a time (i, i + 1): their dot products, shuffles and exps are independent,
-          // and the running max only moves (a warp-uniform rescale) when a score exceeds it by
-          // 2^8 — the j-long chain of an exact online softmax was the fused pass's critical path.
+          diag_row_init<NBOX>(sQ, TB, row, k8, sl2, qf, acc, m, l);
           for (int i = 0; i < j; i += 2) {
             const int ns = min(2, j - i);
             uint32_t kw[2][E / 2], vw[2][E / 2];  // packed bf16 pairs of K_i, V_i (this lane's columns)
@@ -442,72 +522,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               for (int u = 0; u < ns; ++u) mbar_arrive(&bars.dg_empty[(n + u) % kDgStages]);  // values in registers
             n += ns;
             if (TTT_FWD_DIAG_MODE == 1) continue;  // dev probe: no math
-            // t = c log2e q . K_i[r] for (head, stage): 8-lane partial dots (two FFMA2 chains each)
-            float t[2][2];
-#pragma unroll
-            for (int hs = 0; hs < 2; ++hs)
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                uint64_t d0 = 0, d1 = 0;
-#pragma unroll
-                for (int e = 0; e < E / 2; e += 2) {
-                  d0 = ffma2(f2pack(qf[hs][2 * e], qf[hs][2 * e + 1]), bf2_to_f2(kw[u][e]), d0);
-                  d1 = ffma2(f2pack(qf[hs][2 * e + 2], qf[hs][2 * e + 3]), bf2_to_f2(kw[u][e + 1]), d1);
-                }
-                float a0, a1, b0, b1;
-                f2unpack(d0, a0, a1);
-                f2unpack(d1, b0, b1);
-                t[hs][u] = (a0 + a1) + (b0 + b1);
-              }
-#pragma unroll
-            for (int sh = 1; sh < 8; sh <<= 1)
-#pragma unroll
-              for (int hs = 0; hs < 2; ++hs)
-#pragma unroll
-                for (int u = 0; u < 2; ++u) t[hs][u] += __shfl_xor_sync(0xffffffffu, t[hs][u], sh);
-#pragma unroll
-            for (int hs = 0; hs < 2; ++hs) {
-              const float tmax = ns > 1 ? fmaxf(t[hs][0], t[hs][1]) : t[hs][0];
-              if (__any_sync(0xffffffffu, tmax > m[hs] + 8.f)) {  // rare: the max moved (always at i = 0)
-                const float m_new = fmaxf(m[hs], tmax);
-                const float alpha = ex2(m[hs] - m_new);  // 0 when m was -inf
-                l[hs] *= alpha;
-#pragma unroll
-                for (int e = 0; e < E; ++e) acc[hs][e] *= alpha;
-                m[hs] = m_new;
-              }
-              const float p0 = ex2(t[hs][0] - m[hs]), p1 = ns > 1 ? ex2(t[hs][1] - m[hs]) : 0.f;
-              l[hs] += p0 + p1;
-              const uint64_t p02 = f2pack(p0, p0), p12 = f2pack(p1, p1);
-#pragma unroll
-              for (int e = 0; e < E / 2; ++e) {
-                uint64_t o = ffma2(bf2_to_f2(vw[0][e]), p02, f2pack(acc[hs][2 * e], acc[hs][2 * e + 1]));
-                o = ffma2(bf2_to_f2(vw[1][e]), p12, o);
-                f2unpack(o, acc[hs][2 * e], acc[hs][2 * e + 1]);
-              }
-            }
+            diag_pair_update<E>(qf, acc, m, l, kw, vw, ns);
           }
-          // O_d (normalised, bf16) -> the out rows (staging; read back by TMA), A_d -> shared memory
-          if (r < T) {
-#pragma unroll
-            for (int hs = 0; hs < 2; ++hs) {
-              if (hs == 0 || has1) {
-                const float inv = 1.f / l[hs];
-                __nv_bfloat16* orow =
-                    reinterpret_cast<__nv_bfloat16*>(p.out) + (((size_t)(PACKED ? p.row0[b] : b * p.L) + r) * p.Hq + h0 + hs) * D;
-#pragma unroll
-                for (int bx = 0; bx < NBOX; ++bx) {
-                  uint4 w;
-                  w.x = pack_bf16(acc[hs][bx * 8 + 0] * inv, acc[hs][bx * 8 + 1] * inv);
-                  w.y = pack_bf16(acc[hs][bx * 8 + 2] * inv, acc[hs][bx * 8 + 3] * inv);
-                  w.z = pack_bf16(acc[hs][bx * 8 + 4] * inv, acc[hs][bx * 8 + 5] * inv);
-                  w.w = pack_bf16(acc[hs][bx * 8 + 6] * inv, acc[hs][bx * 8 + 7] * inv);
-                  *reinterpret_cast<uint4*>(orow + bx * 64 + k8 * 8) = w;
-                }
-                if (k8 == 0) bars.a_d[hs][row] = m[hs] + log2f(l[hs]);
-              }
-            }
-          }
+          if (r < T)
+            diag_row_store<NBOX>(reinterpret_cast<__nv_bfloat16*>(p.out) + (((size_t)(PACKED ? p.row0[b] : b * p.L) + r) * p.Hq + h0) * D,
+                                 D, k8, has1, acc, m, l, &bars.a_d[0][row], &bars.a_d[1][row]);
         }
         if (threadIdx.x == 320) TTT_TRACE_EV(3, 2, n);
         fence_async_global();  // the out rows are read back by the producer's TMA (async proxy)
@@ -713,24 +732,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int hr = qt * kTile + hrow;
           const bool valid = hr < T;
           float qf[2][E], acc[2][E], m[2], l[2];
-#pragma unroll
-          for (int hs = 0; hs < 2; ++hs) {
-            m[hs] = -INFINITY;
-            l[hs] = 0.f;
-#pragma unroll
-            for (int bx = 0; bx < NBOX; ++bx) {
-              const uint4 u = lds128(smem_u32(sQ + hs * TB + bx * 16384) + sw128_off(hrow, k8));
-              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
-                qf[hs][bx * 8 + 2 * e] = f.x * hsl2;
-                qf[hs][bx * 8 + 2 * e + 1] = f.y * hsl2;
-                acc[hs][bx * 8 + 2 * e] = 0.f;
-                acc[hs][bx * 8 + 2 * e + 1] = 0.f;
-              }
-            }
-          }
+          diag_row_init<NBOX>(sQ, TB, hrow, k8, hsl2, qf, acc, m, l);
           const size_t eoff = ((kvrow0 + hr) * p.Hkv + g) * D + k8 * 8;  // this lane's first element
           auto load_step = [&](int i, uint32_t (&kw)[E / 2], uint32_t (&vw)[E / 2]) {
             if (valid && i < j) {
@@ -756,49 +758,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             uint32_t kn[2][E / 2], vn[2][E / 2];  // next pair, in flight during this pair's math
             load_step(i + 2, kn[0], vn[0]);
             load_step(i + 3, kn[1], vn[1]);
-            float t[2][2];
-#pragma unroll
-            for (int hs = 0; hs < 2; ++hs)
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                uint64_t d0 = 0, d1 = 0;
-#pragma unroll
-                for (int e = 0; e < E / 2; e += 2) {
-                  d0 = ffma2(f2pack(qf[hs][2 * e], qf[hs][2 * e + 1]), bf2_to_f2(kc[u][e]), d0);
-                  d1 = ffma2(f2pack(qf[hs][2 * e + 2], qf[hs][2 * e + 3]), bf2_to_f2(kc[u][e + 1]), d1);
-                }
-                float a0, a1, b0, b1;
-                f2unpack(d0, a0, a1);
-                f2unpack(d1, b0, b1);
-                t[hs][u] = (a0 + a1) + (b0 + b1);
-              }
-#pragma unroll
-            for (int sh = 1; sh < 8; sh <<= 1)
-#pragma unroll
-              for (int hs = 0; hs < 2; ++hs)
-#pragma unroll
-                for (int u = 0; u < 2; ++u) t[hs][u] += __shfl_xor_sync(0xffffffffu, t[hs][u], sh);
-#pragma unroll
-            for (int hs = 0; hs < 2; ++hs) {
-              const float tmax = ns > 1 ? fmaxf(t[hs][0], t[hs][1]) : t[hs][0];
-              if (__any_sync(0xffffffffu, tmax > m[hs] + 8.f)) {  // rare: the max moved (always at i = 0)
-                const float m_new = fmaxf(m[hs], tmax);
-                const float alpha = ex2(m[hs] - m_new);
-                l[hs] *= alpha;
-#pragma unroll
-                for (int e = 0; e < E; ++e) acc[hs][e] *= alpha;
-                m[hs] = m_new;
-              }
-              const float p0 = ex2(t[hs][0] - m[hs]), p1 = ns > 1 ? ex2(t[hs][1] - m[hs]) : 0.f;
-              l[hs] += p0 + p1;
-              const uint64_t p02 = f2pack(p0, p0), p12 = f2pack(p1, p1);
-#pragma unroll
-              for (int e = 0; e < E / 2; ++e) {
-                uint64_t o = ffma2(bf2_to_f2(vc[0][e]), p02, f2pack(acc[hs][2 * e], acc[hs][2 * e + 1]));
-                o = ffma2(bf2_to_f2(vc[1][e]), p12, o);
-                f2unpack(o, acc[hs][2 * e], acc[hs][2 * e + 1]);
-              }
-            }
+            diag_pair_update<E>(qf, acc, m, l, kc, vc, ns);
 #pragma unroll
             for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -807,25 +767,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 vc[u][e] = vn[u][e];
               }
           }
-          if (valid) {
-#pragma unroll
-            for (int hs = 0; hs < 2; ++hs) {
-              if (hs == 0 || has1) {
-                const float inv = 1.f / l[hs];
-                __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.out) + ((kvrow0 + hr) * p.Hq + h0 + hs) * D;
-#pragma unroll
-                for (int bx = 0; bx < NBOX; ++bx) {
-                  uint4 w;
-                  w.x = pack_bf16(acc[hs][bx * 8 + 0] * inv, acc[hs][bx * 8 + 1] * inv);
-                  w.y = pack_bf16(acc[hs][bx * 8 + 2] * inv, acc[hs][bx * 8 + 3] * inv);
-                  w.z = pack_bf16(acc[hs][bx * 8 + 4] * inv, acc[hs][bx * 8 + 5] * inv);
-                  w.w = pack_bf16(acc[hs][bx * 8 + 6] * inv, acc[hs][bx * 8 + 7] * inv);
-                  *reinterpret_cast<uint4*>(orow + bx * 64 + k8 * 8) = w;
-                }
-                if (k8 == 0) bars.a_d[hs][hrow] = m[hs] + log2f(l[hs]);
-              }
-            }
-          }
+          if (valid)
+            diag_row_store<NBOX>(reinterpret_cast<__nv_bfloat16*>(p.out) + ((kvrow0 + hr) * p.Hq + h0) * D, D, k8, has1, acc,
+                                 m, l, &bars.a_d[0][hrow], &bars.a_d[1][hrow]);
         }
         fence_async_global();  // the out rows are read back by the producer's TMA (async proxy)
         __threadfence_block();
