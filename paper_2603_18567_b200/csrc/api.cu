@@ -404,8 +404,10 @@ int ttt_attn_fwd(const ttt_attn_desc* d, int step, const void* q, const void* k_
       (p.out_lo && !encode_bshd(&maps.out_lo, p.out_lo, map_b(p), map_l(p), p.Hq, p.D)))
     return TTT_ERR_CUDA;
   for (int i = 0; i < p.step; ++i)  // the forward's in-kernel diagonal ring: 16-row boxes of K_i / V_i
-    if (!encode_bshd_rows(&maps.kd[i], p.ks[i], map_b(p), map_l(p), p.Hkv, p.D, 16) ||
-        !encode_bshd_rows(&maps.vd[i], p.vs[i], map_b(p), map_l(p), p.Hkv, p.D, 16))
+    if (TTT_FWD_TC_DIAG ? (!encode_bshd(&maps.kd[i], p.ks[i], map_b(p), map_l(p), p.Hkv, p.D) ||  // 128-row tiles
+                           !encode_bshd(&maps.vd[i], p.vs[i], map_b(p), map_l(p), p.Hkv, p.D))
+                        : (!encode_bshd_rows(&maps.kd[i], p.ks[i], map_b(p), map_l(p), p.Hkv, p.D, 16) ||
+                           !encode_bshd_rows(&maps.vd[i], p.vs[i], map_b(p), map_l(p), p.Hkv, p.D, 16)))
       return TTT_ERR_CUDA;
   DiagMaps dmaps;
   if (p.step > 0 && fwd_uses_diag_kernel()) {

@@ -67,11 +67,17 @@ constexpr int kFwdThreads = 512;
 #define TTT_FWD_REG_SOFTMAX 176
 #endif
 #ifndef TTT_FWD_REG_DIAG
-#define TTT_FWD_REG_DIAG 128
+#define TTT_FWD_REG_DIAG (TTT_FWD_TC_DIAG ? 24 : 128)  // TC_DIAG: the diagonal warps idle, the role warps get the rest
 #endif
 constexpr uint32_t kFwdRegSoftmax = TTT_FWD_REG_SOFTMAX, kFwdRegDiag = TTT_FWD_REG_DIAG,
                    kFwdRegRole = 512 - 2 * TTT_FWD_REG_SOFTMAX - TTT_FWD_REG_DIAG;
 static_assert(2 * kFwdRegSoftmax + kFwdRegDiag + kFwdRegRole <= 512, "register file per SMSP");
+// setmaxnreg from the launch allocation (128 per thread at 512 threads) to N: inc or dec by direction
+template <uint32_t N>
+__device__ __forceinline__ void regs_to() {
+  if constexpr (N > 128) regs_inc<N>();
+  else if constexpr (N < 128) regs_dec<N>();
+}
 #ifndef TTT_FWD_DIAG_MODE
 #define TTT_FWD_DIAG_MODE 0  // dev timing probes only: 1 = diagonal warps skip the math, 2 = skip the loads
 #endif
@@ -281,7 +287,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   // diagonal row blocks: nrb of this q tile hold rows r < T_b; the diagonal warps take [0, nrb_d), the
   // softmax warps (SHD, short CTAs) the rest
   const int nrb = (!TREE && T > qt * kTile) ? min(kTile / kDgRows, (T - qt * kTile + kDgRows - 1) / kDgRows) : 0;
-  const bool shd = !TREE && TTT_FWD_FUSED_DIAG && p.step > 0 && nkv <= TTT_FWD_SHD_NKV;
+  const bool shd = !TREE && !TTT_FWD_TC_DIAG && TTT_FWD_FUSED_DIAG && p.step > 0 && nkv <= TTT_FWD_SHD_NKV;
+  // TC_DIAG: the j diagonal steps run as kv tiles nkv .. ntot-1 (none when the whole q tile is padding)
+  const int ntot = nkv + ((TTT_FWD_TC_DIAG && !TREE && T > qt * kTile) ? p.step : 0);
   const int nrb_d = shd ? (nrb + 2) / 3 : nrb;
   // TMA (row, batch) origin of this sequence: (0, b) padded, (row0[b], 0) packed (TREE: never packed)
   const int ry = PACKED ? p.row0[b] : 0, by = PACKED ? 0 : b;
@@ -309,16 +317,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   };
   auto load_kv = [&](int n) {
     const int st = n & 1, ph = (n >> 1) & 1;
+    // TC_DIAG: tiles n >= nkv are step i = n - nkv's K_i / V_i rows of this q tile
+    const bool dg = TTT_FWD_TC_DIAG && n >= nkv;
+    const CUtensorMap* mk = dg ? &maps.kd[n - nkv] : &maps.k;
+    const CUtensorMap* mv = dg ? &maps.vd[n - nkv] : &maps.v;
+    const int row = ry + (dg ? qt : kvt0 + n) * kTile;
     mbar_wait(&bars.k_empty[st], ph ^ 1);
     mbar_expect_tx(&bars.k_full[st], TB);
 #pragma unroll
     for (int bx = 0; bx < NBOX; ++bx)
-      tma_load_4d(sK + st * TB + bx * 16384, &maps.k, &bars.k_full[st], bx * 64, g, ry + (kvt0 + n) * kTile, by);
+      tma_load_4d(sK + st * TB + bx * 16384, mk, &bars.k_full[st], bx * 64, g, row, by);
     mbar_wait(&bars.v_empty[st], ph ^ 1);
     mbar_expect_tx(&bars.v_full[st], TB);
 #pragma unroll
     for (int bx = 0; bx < NBOX; ++bx)
-      tma_load_4d(sV + st * TB + bx * 16384, &maps.v, &bars.v_full[st], bx * 64, g, ry + (kvt0 + n) * kTile, by);
+      tma_load_4d(sV + st * TB + bx * 16384, mv, &bars.v_full[st], bx * 64, g, row, by);
   };
   if (threadIdx.x == 256) {
     mbar_init(&bars.q, 1);
@@ -358,10 +371,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   // (launch value), the fourth 48 = 512 registers per lane.
   if (warp == 8) {
     // ================= TMA producer =================
-    if (TTT_FWD_ONEREAD) regs_dec<kFwdRegRole>();
+    if (TTT_FWD_ONEREAD) regs_to<kFwdRegRole>();
     if (lane == 0) {
-      for (int n = 1; n < nkv; ++n) load_kv(n);  // Q and tile 0 were issued with the barrier setup
-      if (!TREE && p.step > 0) {  // diagonal partial of the two heads into the Q tiles once no S MMA
+      for (int n = 1; n < ntot; ++n) load_kv(n);  // Q and tile 0 were issued with the barrier setup
+      if (!TREE && !TTT_FWD_TC_DIAG && p.step > 0) {  // diagonal partial of the two heads into the Q tiles once no S MMA
                                   // reads them and the diagonal warps have written it
         mbar_wait(&bars.s_done, 0);
         if (TTT_FWD_FUSED_DIAG) mbar_wait(&bars.diag_done, 0);
@@ -375,7 +388,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else if (warp == 9) {
     // ================= MMA issuer (whole warp, converged; elect.sync inside each issue) =================
-    if (TTT_FWD_ONEREAD) regs_dec<kFwdRegRole>();
+    if (TTT_FWD_ONEREAD) regs_to<kFwdRegRole>();
     {
       constexpr uint32_t idS = idesc_bf16_f32(128, 128, false, false);  // S = Q K^T, both K-major
       constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);     // O += P V, V MN-major
@@ -404,6 +417,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
           umma_ts_e(tbase + 256 + slot * 128, tbase + slot * 128 + ks * 8, sdesc_add(dV0, vst * TB + ks * 2048), idO, 1u);
+        if (TTT_FWD_TC_DIAG && n >= nkv) {
+          // diagonal tile: P = P_hi + P_lo (the bf16 residual at columns [64, 96) for keys 64..127 and
+          // [32, 64) for keys 0..63), so the diagonal weight enters O with ~16-bit precision as the
+          // CUDA-core diagonal did
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            umma_ts_e(tbase + 256 + slot * 128, tbase + slot * 128 + (ks < 4 ? 32 + ks * 8 : 64 + (ks - 4) * 8),
+                      sdesc_add(dV0, vst * TB + ks * 2048), idO, 1u);
+        }
       };
       mbar_wait(&bars.q, 0);
       mbar_wait(&bars.k_full[0], 0);
@@ -416,9 +438,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         umma_commit_e(&bars.s_full[1]);
       }
       umma_commit_e(&bars.k_empty[0]);
-      for (int n = 0; n < nkv; ++n) {
+      for (int n = 0; n < ntot; ++n) {
         const int vst = n & 1, vph = (n >> 1) & 1;
-        const bool more = n + 1 < nkv;
+        const bool more = n + 1 < ntot;
         const int kst = (n + 1) & 1, kph = ((n + 1) >> 1) & 1;
         if (!more) umma_commit_e(&bars.s_done);
         mbar_wait(&bars.v_full[vst], vph);
@@ -452,8 +474,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else if (warp >= 14) {
     // ================= TMA producer of the diagonal ring (warp 14); warp 15 idle =================
-    if (TTT_FWD_ONEREAD) regs_dec<kFwdRegRole>();
-    if (TTT_FWD_FUSED_DIAG && !TREE && p.step > 0 && warp == 14 && lane == 0) {
+    if (TTT_FWD_ONEREAD) regs_to<kFwdRegRole>();
+    if (TTT_FWD_FUSED_DIAG && !TTT_FWD_TC_DIAG && !TREE && p.step > 0 && warp == 14 && lane == 0) {
       const int j = p.step;
       int n = 0;
       for (int rb = 0; rb < nrb_d; ++rb)
@@ -474,9 +496,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else if (warp >= 10) {
     // ================= diagonal fold (warps 10-13) =================
-    if (TTT_FWD_ONEREAD) regs_dec<kFwdRegDiag>();
+    if (TTT_FWD_ONEREAD) regs_to<kFwdRegDiag>();
 
-    if (TTT_FWD_FUSED_DIAG && !TREE && p.step > 0) {
+    if (TTT_FWD_FUSED_DIAG && !TTT_FWD_TC_DIAG && !TREE && p.step > 0) {
       const int j = p.step;
       {
         // thread layout: 8 lanes per row (lane k = lane & 7 owns columns 8k..8k+7 of every 64-column
@@ -536,7 +558,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else {
     // ================= softmax + epilogue (warps 0-7) =================
-    if (TTT_FWD_ONEREAD) regs_inc<kFwdRegSoftmax>();
+    if (TTT_FWD_ONEREAD) regs_to<kFwdRegSoftmax>();
     const int slot = warp >> 2;
     const int wq = warp & 3;
     if (slot == 0 || has1) {
@@ -554,11 +576,65 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const unsigned long long tree_am = tree_row ? p.tree_mask[(size_t)b * p.tree_n + r] : 0ull;
       TTT_TRACE_DECL(1);
       TTT_TRACE_DECL(2);
-      for (int n = 0; n < nkv; ++n) {
+      for (int n = 0; n < ntot; ++n) {
         mbar_wait(&bars.s_full[slot], n & 1);
         if (threadIdx.x == 0) TTT_TRACE_EV(1, 1, n);
         if (threadIdx.x == 128) TTT_TRACE_EV(2, 1, n);
         tc_fence_after();
+        if (TTT_FWD_TC_DIAG && n >= nkv) {
+          // ---- diagonal tile (step i = n - nkv + 1): only column c = row is allowed (Alg. 2 M_suffix,
+          // PAPER.md:305-309), and only for rows r < T. The warp's rows are TMEM lanes 32 wq + lane, so
+          // their diagonal entries are columns 32 wq .. 32 wq + 31: one 32-column load, lane picks its own.
+          uint32_t d32[32];
+          tmem_ld32(tS + wq * 32, d32);
+          float sd = __uint_as_float(d32[0]);
+#pragma unroll
+          for (int c = 1; c < 32; ++c) sd = (lane == c) ? __uint_as_float(d32[c]) : sd;
+          const float xd = (r < T) ? sd * sl2 : -INFINITY;
+          const float m_new = fmaxf(m_run, xd);
+          if (__any_sync(0xffffffffu, m_new > m_run + kRescaleThreshold)) {  // rare: rescale O (PV_{n-1} done)
+            const float alpha = ex2(m_run - m_new);
+            const uint64_t a2 = f2pack(alpha, alpha);
+#pragma unroll 1
+            for (int c0 = 0; c0 < D; c0 += 32) {
+              uint32_t o[32];
+              tmem_ld32(tO + c0, o);
+#pragma unroll
+              for (int i2 = 0; i2 < 32; i2 += 2) {
+                float lo, hi;
+                f2unpack(fmul2(f2pack(__uint_as_float(o[i2]), __uint_as_float(o[i2 + 1])), a2), lo, hi);
+                o[i2] = __float_as_uint(lo);
+                o[i2 + 1] = __float_as_uint(hi);
+              }
+              tmem_st32(tO + c0, o);
+            }
+            l_run *= alpha;
+            m_run = m_new;
+          }
+          const float pd = ex2(xd - m_run);  // 0 for masked rows
+          l_run += pd;
+          // P row: zero except key `row` (bf16 pairs, 2 keys per 32-bit column): keys 64..127 -> columns
+          // [96, 128) (p_hi, published first), keys 0..63 -> columns [0, 32) (p_lo)
+          const float pd_hi = __bfloat162float(__float2bfloat16_rn(pd)), pd_lo = pd - pd_hi;
+          const uint32_t pw = (row & 1) ? pack_bf16(0.f, pd_hi) : pack_bf16(pd_hi, 0.f);
+          const uint32_t pwl = (row & 1) ? pack_bf16(0.f, pd_lo) : pack_bf16(pd_lo, 0.f);
+          const int wsel = (row & 63) >> 1;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int hf = 1 - hh;
+            uint32_t pk[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) pk[c] = ((row >> 6) == hf && c == wsel) ? pw : 0u;
+            tmem_st32(tS + (hf ? 96 : 0), pk);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) pk[c] = ((row >> 6) == hf && c == wsel) ? pwl : 0u;
+            tmem_st32(tS + (hf ? 64 : 32), pk);  // P_lo (second PV pass of the diagonal tile)
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(hf == 0 ? &bars.p_lo[slot] : &bars.p_hi[slot]);
+          }
+          continue;
+        }
         // ONEREAD: the whole S row is read once (raw0 = keys [0,64), raw = keys [64,128)); P(keys
         // 64..127) is written over the already-read S columns [96,128) and published first (p_hi),
         // then P(keys 0..63) over columns [0,32) (p_lo). Otherwise S is read in two 64-column halves
@@ -780,12 +856,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // by the diagonal warps into (A_d = log2 sum_i 2^{t_i}, O_d = normalised sum); the
       // merge is the same online-softmax update as one more "tile".
       const size_t lse_idx = TREE ? ((size_t)bst * p.Hq + h) * p.L + r : lse_at(p, PACKED, b, h, r);
-      const bool has_diag = !TREE && (r < T) && (p.step > 0);
+      const bool has_diag = !TREE && !TTT_FWD_TC_DIAG && (r < T) && (p.step > 0);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 3, 0);
       mbar_wait(&bars.o_full[slot], 0);
       if (threadIdx.x == 0) TTT_TRACE_EV(1, 4, 0);
       tc_fence_after();
-      if (!TREE && p.step > 0) {
+      if (!TREE && !TTT_FWD_TC_DIAG && p.step > 0) {
         if (TTT_FWD_FUSED_DIAG) mbar_wait(&bars.diag_done, 0);  // A_d in shared memory
         mbar_wait(&bars.od, 0);                                 // O_d tile in the Q buffer
       }

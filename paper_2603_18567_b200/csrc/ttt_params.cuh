@@ -101,6 +101,16 @@ __device__ __forceinline__ int seq_of_tile(const Params& p, bool pk, int t) {
 #endif
 
 // Tensor maps for the tcgen05 paths (4-D: D, H, L, B; box 64 x 1 x 128 x 1, SW128)
+// TTT_FWD_TC_DIAG = 1 (dev, off): the forward treats step j's diagonal keys as j extra kv tiles (K_i / V_i
+// rows of the q tile, 128-row SW128 boxes in FwdMaps::kd / vd) on the tensor cores with a diagonal-only
+// mask and a second P_lo pass, instead of the CUDA-core diagonal warps (0). Measured (r04g-r04j): without
+// the P_lo pass the forward was 7% faster but the bf16-rounded diagonal weights broke the plain bound on
+// accumulated dK_i at the Llama shape (6 of 16.7M elements, 4.9e-2); with it every test passes but the
+// forward is 1.6-3% slower (three 1024-clk MMAs per diagonal step for the two heads). Shared by api.cu (map
+// boxes) and fwd_sm100.cu.
+#ifndef TTT_FWD_TC_DIAG
+#define TTT_FWD_TC_DIAG 0
+#endif
 struct FwdMaps {
   CUtensorMap q, k, v, out, out_lo;
   // step lists K_i / V_i (i < step) as 4-D BSHD maps with 16-row boxes: the forward's diagonal ring
